@@ -1,0 +1,394 @@
+"""Benchmark of the rollout hot path (BASELINE.json metric: env-steps/sec, whole box).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-extras]
+
+One "step" = one fin_rollout over the headline workload: the C1 30-stock env
+(K=30, I=8, obs 301) with the 301-256-256-30 bf16 Gaussian policy, N = 65,536
+envs per GPU, horizon T = 256 with reset on done (BASELINE configs[1] env and
+policy at the configs[4] sweep's largest per-GPU size; the metric is quoted at
+2048-65536 envs).  A step runs every §8(a) row: market-row staging, observation,
+tcgen05 MLP, sampling/clipping, trade execution, reward, done/reset, online
+episode metrics, and the per-rank aggregate (all-reduced over NCCL when N > 1).
+
+Timing: W untimed warm-up steps, then K steps, each bracketed by CUDA events on
+the launching stream; L2 is flushed (256 MiB write) between timed steps outside
+the events; barrier + synchronize on both sides; max over ranks.  ``e2e`` repeats
+the measurement through the C ABI with host buffers: the step's input state is
+copied from pinned host memory and the trajectory (reward, done) and aggregate are
+read back inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_HEAD = 65536
+T_HEAD = 256
+K_ASSETS = 30
+N_IND = 8
+ROWS = 1008
+L_EP = 30
+FLOP_PER_ENV_STEP = 2 * (301 * 256 + 256 * 256 + 256 * 30)        # 300,544 (algorithmic, unpadded)
+STEP_BYTES_PER_ENV = 8 + 60 + 4 + 4 + 60 + 8 + 60 + 4 + 4 + 1     # K1: state in/out + action + reward + done
+METRIC = "env-steps/sec (whole box) at 2048-65536 envs, 1/2/4/8 B200; % HBM roofline"
+WORKLOAD = "C1 30-stock env + 301-256-256-30 bf16 policy, 65536 envs/GPU, horizon 256, reset on done"
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update({k: m[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in m})
+        p["source"] = "measured"
+    except Exception:
+        pass
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_info():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------------ oracle (CPU) timing
+def _oracle_shard(args):
+    n_envs, T, env_offset = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import rollout as orol
+    from oracle import stock as ostock
+    from synth import inputs, market
+    from synth import policy as spol
+    m = market.stock_c1(rows=ROWS)
+    cfg = ostock.StockEnvConfig(num_envs=n_envs, num_assets=K_ASSETS, num_indicators=N_IND, num_rows=ROWS,
+                                episode_len=L_EP, window_stride=5, num_windows=195, window_block=128,
+                                env_offset=env_offset)
+    layers = spol.kaiming_bf16(spol.STOCK_DIMS, 0)
+    noise = inputs.supplied_noise(T, 1, n_envs, K_ASSETS, seed=23 + env_offset)
+    t0 = time.perf_counter()
+    orol.stock_policy_rollout(cfg, m.market, [layers], [orol.PPO_GAUSS], noise, T)
+    return time.perf_counter() - t0
+
+
+def oracle_rate(n_envs_per_core=16, T=8, cores=None):
+    """Oracle env-steps/s on the host's cores (multiprocessing over env shards)."""
+    import multiprocessing as mp
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[v] = "1"
+    if cores is None:
+        cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(cores) as pool:
+        pool.map(_oracle_shard, [(n_envs_per_core, T, 128 * c) for c in range(cores)])
+    wall = time.perf_counter() - t0
+    steps = n_envs_per_core * T * cores
+    return steps / wall, cores, f"{cores} shards x {n_envs_per_core} envs x {T} steps of the headline workload " \
+                                f"(float64 oracle incl. 301-256-256-30 MLP), wall {wall:.1f}s"
+
+
+# ------------------------------------------------------------------ GPU arm
+def make_env(fin, N, env_offset, T_ep=L_EP):
+    from synth import market
+    m = market.stock_c1(rows=ROWS)
+    cfg = fin.env_config(num_envs=N, num_assets=K_ASSETS, num_indicators=N_IND, num_rows=ROWS, episode_len=T_ep,
+                         window_stride=5, num_windows=195, window_block=128, env_offset=env_offset, seed=23)
+    return fin.fin_env_create(cfg, m.market)
+
+
+def time_rollouts(fin, torch, env, pol, N, T, steps, warmup, flush=None, allreduce=None, clocks_index=None):
+    """Returns (per-step ms list (kernel events), launches per step, agg)."""
+    stream = torch.cuda.current_stream()
+    z = lambda s, d: torch.zeros(s, dtype=d, device="cuda")  # noqa: E731
+    reward, done, agg = z((T, N), torch.float32), z((T, N), torch.uint8), z(8, torch.float64)
+    traj = fin.make_traj(reward=reward, done=done, agg=agg)
+    noise = fin.make_noise(fin.FIN_NOISE_PHILOX, 1234)
+    for _ in range(warmup):
+        fin.fin_rollout(env, [pol], T, noise, traj, stream=stream)
+    torch.cuda.synchronize()
+    times = []
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        if flush is not None:
+            flush.zero_()
+        ev[i][0].record(stream)
+        fin.fin_rollout(env, [pol], T, noise, traj, stream=stream)
+        if allreduce is not None:
+            allreduce(agg)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    times = [a.elapsed_time(b) for a, b in ev]
+    return times, agg
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_info()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2501_10709_b200 import fin
+    from synth import policy as spol
+    fin.fin_device_check(local)
+    N, T = N_HEAD, T_HEAD
+    env = make_env(fin, N, env_offset=rank * N)
+    pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, spol.kaiming_bf16(spol.STOCK_DIMS, 0))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def allreduce(agg):
+        if world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(agg[:fin.FIN_AGG_NSUM], op=dist.ReduceOp.SUM)
+            dist.all_reduce(agg[fin.FIN_AGG_NSUM:], op=dist.ReduceOp.MIN)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    barrier()
+    with ClockSampler(local) as cs:
+        times, agg = time_rollouts(fin, torch, env, pol, N, T, args.steps, args.warmup, flush, allreduce)
+    barrier()
+    total_ms = sum(times)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    units = N * T * world * args.steps
+    value = units / (total_ms / 1e3)
+    ms_per_step = total_ms / args.steps
+    kern_ms = statistics.mean(times)
+    flops = FLOP_PER_ENV_STEP * N * T
+    pk = peaks()
+    achieved = flops / (kern_ms / 1e3) / 1e12
+    out = {"metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "bf16 MLP (fp32 accum) + f64 env", "data": "synthetic",
+           "config": {"workload": WORKLOAD, "envs_per_gpu": N, "horizon": T, "episode_len": L_EP,
+                      "global_envs": N * world, "parallelism": f"env-sharded dp{world}",
+                      "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                      "noise": "philox"},
+           "gpu_launches": 2 * args.steps,
+           "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops_sustained"],
+                        "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops_sustained"], "traffic": None,
+                        "kernel": "k_tc_rollout<PlanStockC1> (fused rollout)",
+                        "flop_per_env_step": FLOP_PER_ENV_STEP, "peak_source": pk["source"] + " sustained"}}
+    prof = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            out["roofline"]["traffic"] = json.load(f).get("rollout_bytes_per_launch")
+    out["clocks"] = cs.summary()
+    # ---- e2e through the C ABI with host buffers
+    if rank == 0 or world > 1:
+        out["e2e"] = e2e(fin, torch, env, pol, N, T, max(2, args.steps // 2), allreduce, world)
+    if rank == 0 and not args.no_extras:
+        out["extras"] = extras(fin, torch, pol)
+    del env
+    if rank == 0:
+        rate, cores, sample = oracle_rate()
+        out["cpu_baseline"] = {"value": rate, "unit": "env-steps/s", "cores": cores, "kind": "oracle", "sample": sample}
+        out["paper_context"] = {"note": "paper numbers are from one NVIDIA A100 with real data and PPO/DQN training "
+                                        "(P:380, P:336); context only",
+                                "stock_samples_per_s_2048_envs_A100": 8813.81, "stock_speedup_2048_vs_1": 47.73,
+                                "crypto_samples_per_s_2048_envs_A100": 114885.98, "crypto_speedup_2048_vs_1": 1746.25}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def e2e(fin, torch, env, pol, N, T, steps, allreduce, world):
+    """Same metric through the public C ABI with host buffers (pinned): per step the
+    input state goes H2D, the rollout runs, reward / done / agg come back D2H."""
+    import numpy as np
+    z = lambda s, d: torch.zeros(s, dtype=d, device="cuda")  # noqa: E731
+    h_cash = torch.full((N,), 1e6, dtype=torch.float64).pin_memory()
+    h_hold = torch.zeros((N, K_ASSETS), dtype=torch.int16).pin_memory()
+    h_tep = torch.zeros((N,), dtype=torch.int32).pin_memory()
+    h_rew = torch.empty((T, N), dtype=torch.float32).pin_memory()
+    h_done = torch.empty((T, N), dtype=torch.uint8).pin_memory()
+    h_agg = torch.empty(8, dtype=torch.float64).pin_memory()
+    d_cash, d_hold, d_tep = z(N, torch.float64), z((N, K_ASSETS), torch.int16), z(N, torch.int32)
+    reward, done, agg = z((T, N), torch.float32), z((T, N), torch.uint8), z(8, torch.float64)
+    traj = fin.make_traj(reward=reward, done=done, agg=agg)
+    noise = fin.make_noise(fin.FIN_NOISE_PHILOX, 99)
+    stream = torch.cuda.current_stream()
+
+    def one():
+        d_cash.copy_(h_cash, non_blocking=True)
+        d_hold.copy_(h_hold, non_blocking=True)
+        d_tep.copy_(h_tep, non_blocking=True)
+        fin.fin_env_set_state(env, cash=d_cash, hold=d_hold, t_ep=d_tep, stream=stream)
+        fin.fin_rollout(env, [pol], T, noise, traj, stream=stream)
+        allreduce(agg)
+        h_rew.copy_(reward, non_blocking=True)
+        h_done.copy_(done, non_blocking=True)
+        h_agg.copy_(agg, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        one()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    h2d = N * (8 + 2 * K_ASSETS + 4)
+    d2h = T * N * 5 + 64
+    return {"value": N * T * world * steps / (ms / 1e3), "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": steps}
+
+
+def extras(fin, torch, pol):
+    """Secondary measurements printed inside the same JSON line (rank 0, N = 1 GPU):
+    the C4 sweep points, the exact configs[1] rollout (2048 envs, T = 30), and the
+    HBM-bound step kernel K1 at N = 2^22 against the measured HBM copy bandwidth."""
+    out = {"sweep_T256": {}}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for N in (1, 64, 2048, 16384):
+        env = make_env(fin, N, 0)
+        times, _ = time_rollouts(fin, torch, env, pol, N, T_HEAD, 5, 3, flush)
+        out["sweep_T256"][str(N)] = N * T_HEAD / (statistics.mean(times) / 1e3)
+        del env
+    env = make_env(fin, 2048, 0)
+    times, _ = time_rollouts(fin, torch, env, pol, 2048, 30, 10, 3, flush)
+    out["configs1_2048envs_T30"] = 2048 * 30 / (statistics.mean(times) / 1e3)
+    del env
+    # K1 step kernel at N = 2^22 (877 MB working set >> 126 MB L2)
+    N = 1 << 22
+    env = make_env(fin, N, 0)
+    from synth import inputs
+    acts = torch.from_numpy(inputs.stock_actions(1, N, K_ASSETS, seed=5)[0]).cuda()
+    z = lambda s, d: torch.zeros(s, dtype=d, device="cuda")  # noqa: E731
+    rew, dn = z(N, torch.float32), z(N, torch.uint8)
+    tr = fin.make_traj(reward=rew, done=dn)
+    for _ in range(3):
+        fin.fin_env_step(env, acts, tr)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(10):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fin.fin_env_step(env, acts, tr)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = statistics.mean(ts)
+    pk = peaks()
+    gbs = STEP_BYTES_PER_ENV * N / (ms / 1e3) / 1e9
+    out["step_kernel_hbm"] = {"kernel": "k_stock_step (K1)", "envs": N, "bytes_per_env_step": STEP_BYTES_PER_ENV,
+                              "env_steps_per_s": N / (ms / 1e3), "achieved_gbs": gbs, "peak_gbs": pk["hbm_gbs"],
+                              "frac": gbs / pk["hbm_gbs"], "frac_of_8tbs": gbs / 8000.0}
+    return out
+
+
+def run_reference(args):
+    """The reference arm: the float64 oracle as it stands, on the host cores, each step a
+    bounded sample of the headline workload."""
+    rank, world, _ = dist_info()
+    if rank != 0:
+        return
+    rates = []
+    t0 = time.perf_counter()
+    cores = None
+    sample = ""
+    for i in range(args.warmup + args.steps):
+        r, cores, sample = oracle_rate(n_envs_per_core=4, T=4)
+        if i >= args.warmup:
+            rates.append(r)
+    wall = time.perf_counter() - t0
+    value = statistics.mean(rates)
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / (args.warmup + args.steps),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": WORKLOAD, "envs_per_gpu": N_HEAD, "horizon": T_HEAD, "episode_len": L_EP,
+                      "note": "each step is a bounded sample of this workload on the host cores"},
+           "cpu_baseline": {"value": value, "unit": "env-steps/s", "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "gpu_launches": 0}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extras", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,268 @@
+/*
+ * fin.h -- C ABI of libfinenv.so, the B200-native rollout hot path of
+ * arXiv 2501.10709 ("Revisiting Ensemble Methods for Stock Trading and Crypto
+ * Trading Tasks at ACM ICAIF FinRL Contests 2023/2024").
+ *
+ * Citations: "P:n" = line n of the paper text; "S:n" = SPEC.md line n;
+ * "Rn" = reading n of DESIGN.md §3 (where the paper is silent or ambiguous).
+ *
+ * What the library computes (§3.1, §4.2, §4.3):
+ *   N independent trading sub-environments (SubEnvs) stepping in lockstep.  Per
+ *   step: policy-MLP forward, action sampling / clipping, buy/sell execution with
+ *   transaction cost and cash/holding constraints, total asset v_t = b_t + p_t^T h_t
+ *   and reward R = v_{t+1} - v_t, done / auto-reset; the stock
+ *   ensemble's averaging of PPO/SAC/DDPG actions and per-episode
+ *   metrics: cumulative return, Sharpe (Eq. 6), max drawdown.
+ *
+ * Conventions (all entry points):
+ *   - Every pointer is a DEVICE pointer on the handle's device unless marked (host).
+ *   - Return value: FIN_OK (0) or an FIN_E_* code; fin_last_error() gives the text
+ *     (thread-local).  No C++ exception crosses the ABI.
+ *   - Asynchrony: calls enqueue on ``stream`` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream) and do not synchronise, except
+ *     fin_env_create (one sync after the market upload), fin_policy_create (one
+ *     sync after packing), fin_env_check and fin_env_destroy.
+ *   - Device-detected conditions (action outside +-max_trade -> clamped; stepping a
+ *     done env with autoreset = 0 -> the env is left unchanged; non-finite
+ *     policy output or noise) set bits of a sticky per-handle error word, reported
+ *     by fin_env_check() as FIN_E_DEVICE_ASYNC (bits in *flags).
+ *   - Ownership: the caller owns every pointer it passes; the library owns the
+ *     handle's SoA state, its padded copy of the market and the packed weights.
+ *     Caller buffers may be freed as soon as the create call returns.
+ *   - Threading: one handle is driven by one host thread / one stream at a time.
+ *   - Layouts: caller-visible trajectory tensors use the paper's [T][N][D] order
+ *     (P:242-273); the handle's internal state is SoA ([K][N]) for coalescing.
+ *   - Multi-GPU: the library links no NCCL.  Each rank creates its handle with
+ *     ``env_offset`` = global id of its local env 0 (window assignment and Philox
+ *     streams are keyed by the global id, so results do not depend on the
+ *     partition) and the caller all-reduces the FIN_AGG_* partials.
+ */
+#ifndef FIN_H_
+#define FIN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FIN_ABI_VERSION 1
+
+/* status codes; 1/2/3 mirror SPEC's exit codes */
+enum {
+  FIN_OK = 0,
+  FIN_E_CONFIG = 1,        /* invalid argument / configuration (host-side check) */
+  FIN_E_DATA = 2,          /* market data invalid: non-finite, price <= 0, shape */
+  FIN_E_NUMERIC = 3,       /* reserved: host-detected numeric failure */
+  FIN_E_CUDA = 4,          /* a CUDA runtime call failed */
+  FIN_E_EPISODE_DONE = 5,  /* reserved */
+  FIN_E_UNSUPPORTED = 6,   /* device is not sm_100 / shape outside the compiled kernels */
+  FIN_E_DEVICE_ASYNC = 7   /* sticky device error word non-zero (see FIN_FLAG_*) */
+};
+
+/* sticky device error bits (fin_env_check) */
+enum {
+  FIN_FLAG_ACTION_RANGE = 1,   /* |action| > max_trade: clamped (R6) */
+  FIN_FLAG_EPISODE_DONE = 2,   /* step of a done env with autoreset = 0: ignored */
+  FIN_FLAG_NONFINITE = 4,      /* non-finite MLP output / noise: action forced to 0 */
+  FIN_FLAG_BAD_INDEX = 8       /* market row index out of range: env left unchanged */
+};
+
+enum { FIN_STOCK = 0, FIN_CRYPTO = 1 };
+
+/* policy member kinds: C1 / C2 members (BASELINE configs[1,2]) and the C3 Q-net */
+enum { FIN_PPO_GAUSS = 0, FIN_SAC_SQUASH = 1, FIN_DDPG_OU = 2, FIN_Q_ARGMAX = 3 };
+
+/* noise modes for fin_rollout / fin_ensemble_act */
+enum { FIN_NOISE_PHILOX = 0, FIN_NOISE_SUPPLIED = 1, FIN_NOISE_NONE = 2 };
+
+/* per-rank aggregate vector written by fin_rollout / fin_episode_metrics.
+ * Entries [0, FIN_AGG_NSUM) are reduced with SUM across ranks, the rest with MIN. */
+enum {
+  FIN_AGG_EPISODES = 0,     /* number of completed episodes */
+  FIN_AGG_SUM_CUM = 1,      /* sum of cumulative returns */
+  FIN_AGG_SUM_SHARPE = 2,   /* sum of finite Sharpe ratios */
+  FIN_AGG_N_SHARPE = 3,     /* number of finite Sharpe ratios */
+  FIN_AGG_SUM_MDD = 4,      /* sum of max drawdowns */
+  FIN_AGG_SUM_REWARD = 5,   /* sum of rewards over all transitions */
+  FIN_AGG_NSUM = 6,
+  FIN_AGG_MIN_MDD = 6,      /* worst (most negative) drawdown */
+  FIN_AGG_LEN = 8           /* index 7 = MIN of cumulative return */
+};
+
+typedef struct fin_env fin_env;
+typedef struct fin_policy fin_policy;
+
+/* Environment configuration (host struct).  Stock: P:123, P:129-132, P:148,
+ * BASELINE configs[0,1,2,4]; crypto: P:124, BASELINE configs[3]. */
+typedef struct {
+  int32_t task;             /* FIN_STOCK or FIN_CRYPTO */
+  int32_t num_envs;         /* N >= 1 local envs */
+  int32_t num_assets;       /* K: stock 1..32; crypto must be 1 */
+  int32_t num_indicators;   /* I (stock): market has 2+I channels; crypto: ignored */
+  int32_t num_rows;         /* market rows (days / seconds) */
+  int32_t episode_len;      /* L_ep steps per episode (R9); done on the L_ep-th step */
+  int32_t window_stride;    /* stock window w starts at window_offset + w*window_stride (R10) */
+  int32_t window_offset;
+  int32_t num_windows;      /* W >= 1 */
+  int32_t window_block;     /* envs [j*block, (j+1)*block) (global ids) share window j+base */
+  int32_t window_base;
+  int32_t advance_window_on_reset;  /* C2 test mode: w <- (w+1) mod W on reset */
+  int32_t max_trade;        /* stock: |a_k| <= max_trade shares (R6) */
+  int32_t max_hold;         /* crypto: forced exit after max_hold steps (R26) */
+  int32_t pos_limit;        /* crypto: |position| <= pos_limit (must be 1) */
+  int32_t autoreset;        /* 1: reset on done (BASELINE "reset on done") */
+  double initial_cash;      /* b_0 */
+  double cost_rate;         /* fee per side (0.001 = 0.1%, R4) */
+  double reward_scale;      /* stock 2^-12 (R8), crypto 1 */
+  float noise_std;          /* Gaussian policy std (0.1, configs[1]) */
+  float ou_theta, ou_sigma; /* DDPG OU noise (0.15, 0.2, configs[2]) */
+  float epsilon;            /* crypto epsilon-greedy (0.005) */
+  uint64_t seed;            /* Philox key for production-mode noise */
+  int64_t env_offset;       /* global id of local env 0 */
+} fin_env_config;
+
+/* Create an env handle.  ``market`` (host) holds num_rows rows:
+ *   stock  float32 [num_rows][2 + I][K]: channel 0 raw close (execution/marking),
+ *          channel 1 normalised close (observation), 2.. indicators (observation);
+ *   crypto float32 [num_rows][144]: [mid, ask_px[10], ask_sz[10], bid_px[10],
+ *          bid_sz[10], f[101], pad[2]].
+ * market_elems must equal the product of those dims.  Validates (FIN_E_DATA on
+ * non-finite values or close/mid <= 0), uploads a padded copy, resets all envs
+ * and synchronises once.  Window ranges must stay inside the market. */
+int fin_env_create(const fin_env_config* cfg /*host*/, const float* market /*host*/,
+                   int64_t market_elems, void* stream, fin_env** out /*host*/);
+
+/* reset: b = initial_cash, h = 0, t_ep = 0, online metric state cleared;
+ * mask [N] u8 selects envs (NULL = all).  The window index is re-derived from the
+ * global id (R10). */
+int fin_env_reset(fin_env* env, const uint8_t* mask, void* stream);
+
+/* Trajectory outputs, [T][N][...] (paper order P:242-273); NULL field = not written.
+ * Transition fields hold PRE-reset values of the transition (the state right
+ * after the trade and the mark at the next row), before any auto-reset.
+ *   reward   f32 [T][N]      R = (v' - v) * reward_scale (R8)
+ *   done     u8  [T][N]
+ *   actions  i16 [T][N][K]   executed share deltas h' - h (stock) / position delta (crypto)
+ *   cash     f64 [T][N]      b after the trade
+ *   hold     i16 [T][N][K]   holdings after the trade (crypto: position in {-1,0,1})
+ *   asset    f64 [T][N]      v' = b' + p_{t+1}^T h'
+ *   mlp_out  f32 [T][M][N][Kout]  raw network outputs z (debug / parity)
+ *   mlp_hidden bf16 bits [T][M][N][2][HID]  both hidden activations (debug / parity)
+ *   ep_metrics f64 [E][N][3] (cum, sharpe, mdd) of the episodes completed during the
+ *            call, in completion order; ep_count i32 [N] counts them (written; may
+ *            exceed E, extra episodes are counted but not stored)
+ *   agg      f64 [FIN_AGG_LEN] per-rank partials (overwritten) */
+typedef struct {
+  float* reward;
+  uint8_t* done;
+  int16_t* actions;
+  double* cash;
+  int16_t* hold;
+  double* asset;
+  float* mlp_out;
+  uint16_t* mlp_hidden;
+  double* ep_metrics;
+  int32_t* ep_count;
+  int32_t ep_capacity;      /* E */
+  double* agg;
+} fin_traj;
+
+/* One VecEnv step with supplied integer actions [N][K] i16 (stock share
+ * deltas; crypto position deltas in {-1,0,1}).  ``out`` uses T = 1.  Episode metrics
+ * are not produced by this call (use fin_rollout_actions or fin_episode_metrics). */
+int fin_env_step(fin_env* env, const int16_t* actions, const fin_traj* out /*host*/, void* stream);
+
+/* State snapshot: cash f64 [N], hold i16 [N][K] (crypto: position), asset
+ * f64 [N] = b + p_t^T h at the current row, t_ep i32 [N], window i32 [N].  Any
+ * pointer may be NULL. */
+int fin_env_get_state(const fin_env* env, double* cash, int16_t* hold, double* asset,
+                      int32_t* t_ep, int32_t* window, void* stream);
+
+/* Overwrite state (teacher forcing / resume).  hold [N][K]; crypto: hold = position,
+ * tau = holding time (NULL = 0).  Online metric state restarts at the current equity. */
+int fin_env_set_state(fin_env* env, const double* cash, const int16_t* hold, const int32_t* t_ep,
+                      const int32_t* window, const int32_t* tau, void* stream);
+
+/* Synchronise the handle's last stream and return FIN_E_DEVICE_ASYNC if any sticky
+ * flag is set (written to *flags, host, may be NULL); clears the word. */
+int fin_env_check(fin_env* env, uint32_t* flags /*host*/);
+
+void fin_env_destroy(fin_env* env);
+
+/* Create a policy / Q network (BASELINE configs[1,3]).
+ * kind: FIN_* member kind.  dims (host) = {in, h1, ..., out}, n_layers linear
+ * layers (currently 3: in <= 304, h1 = h2 in {128, 256}, out <= 32).  w_bf16[l]
+ * (host array of HOST pointers) = bf16 bit patterns [dims[l+1]][dims[l]];
+ * bias[l] (host pointers) = f32 [dims[l+1]] or NULL for zero.  Hidden layers use
+ * ReLU (R15); inputs and hidden activations are bf16, accumulation fp32.
+ * The library pads and packs a device copy in the tcgen05 K-major layout. */
+int fin_policy_create(int32_t kind, int32_t n_layers, const int32_t* dims /*host*/,
+                      const uint16_t* const* w_bf16 /*host*/, const float* const* bias /*host*/,
+                      void* stream, fin_policy** out /*host*/);
+void fin_policy_destroy(fin_policy* policy);
+
+/* Noise source.  PHILOX: counter-based Philox4x32-10 keyed by ``seed`` and the
+ * global env id; SUPPLIED: ``supplied`` f32 [T][M][N][K] N(0,1)
+ * (stock) or [T][N][2] U[0,1) (crypto epsilon-greedy: u_explore, u_action);
+ * NONE: zero noise / greedy. */
+typedef struct {
+  int32_t mode;
+  uint64_t seed;
+  const float* supplied;
+} fin_noise;
+
+/* Fused rollout of T steps (the producer of P:139-146 / P:241-278): per step the
+ * members' MLPs on the current observation (tcgen05 tensor cores), sampling /
+ * ensemble averaging (uniform mean, or member_w (host, M floats) weighted), trade
+ * execution, reward, done / auto-reset, online episode metrics.  members (host
+ * array) has n_members in [1, 4] policies of identical shape; stock: kinds
+ * PPO/SAC/DDPG; crypto: exactly one FIN_Q_ARGMAX.  No host round-trip inside. */
+int fin_rollout(fin_env* env, const fin_policy* const* members /*host*/, int32_t n_members,
+                const float* member_w /*host*/, int32_t T, const fin_noise* noise /*host*/,
+                const fin_traj* out /*host*/, void* stream);
+
+/* Replay rollout: T steps with supplied actions [T][N][K] i16, state kept on chip;
+ * online episode metrics as in fin_rollout. */
+int fin_rollout_actions(fin_env* env, const int16_t* actions, int32_t T, const fin_traj* out /*host*/,
+                        void* stream);
+
+/* Ensemble action on the current state without stepping: writes
+ * actions i16 [N][K] and, if non-NULL, mean_action f32 [N][K] (the averaged
+ * continuous action before rounding).  Noise uses step index t_global of the env.
+ * Advances the DDPG OU state like a rollout step would only if commit_ou != 0. */
+int fin_ensemble_act(fin_env* env, const fin_policy* const* members /*host*/, int32_t n_members,
+                     const float* member_w /*host*/, const fin_noise* noise /*host*/,
+                     int16_t* actions, float* mean_action, void* stream);
+
+/* Episode metrics from a stored equity log (Eq. 6): equity f64 [T+1][N]
+ * (row 0 = equity at the start, row t = v' of transition t), done u8 [T][N] (an
+ * episode ends at a done transition; the next starts at equity row... the reset
+ * value ``reset_equity``).  Segmented warp-shuffle scans over time.
+ * Writes ep_metrics f64 [E][N][3], ep_count i32 [N], agg f64 [FIN_AGG_LEN] (or NULL). */
+int fin_episode_metrics(const double* equity, const uint8_t* done, int32_t T, int32_t N,
+                        double reset_equity, double periods_per_year, double rf,
+                        double* ep_metrics, int32_t ep_capacity, int32_t* ep_count, double* agg,
+                        void* stream);
+
+/* Standalone policy forward for parity / profiling: x bf16 bits [B][dims[0]],
+ * z f32 [B][dims[n_layers]], hidden (or NULL) bf16 bits [B][2][dims[1]]. */
+int fin_mlp_forward(const fin_policy* policy, const uint16_t* x, int32_t B, float* z, uint16_t* hidden,
+                    void* stream);
+
+/* Production-noise probe: normals f32 [N][K] for member m at step t_global,
+ * exactly as fin_rollout draws them (Philox4x32-10 + Box-Muller). */
+int fin_philox_normals(uint64_t seed, int64_t env_offset, int32_t N, int32_t K, int32_t member,
+                       int64_t t_global, float* out, void* stream);
+
+/* thread-local text for the last non-OK status of this thread */
+const char* fin_last_error(void);
+
+/* ABI version, device check: FIN_OK if device ``ordinal`` is sm_100 (else UNSUPPORTED) */
+int fin_abi_version(void);
+int fin_device_check(int32_t ordinal);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FIN_H_ */

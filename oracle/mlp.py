@@ -43,6 +43,56 @@ def forward(layers64, x: np.ndarray) -> np.ndarray:
     return h
 
 
+FP32_ACC_BOUND = 2.0 ** -17   # reading R-TOL: fp32 accumulation error, relative to sum |w x|
+
+
+def teacher_forced_layers(layers64, x, hidden_bits, z_dev):
+    """Layer-by-layer check of a device forward pass (reading R-TOL).
+
+    ``x`` [B][in] float64 unquantised observation (the oracle's own), ``hidden_bits``
+    [B][2][H] uint16 bf16 bit patterns of the device's two hidden activations,
+    ``z_dev`` [B][out] the device's output.  Each layer is recomputed in float64
+    from the device's (bf16, exactly representable) input of that layer:
+      z = W h_in + b,  delta = 2^-17 (|W| |h_in| + |b|)   (fp32-accumulation bound)
+    * hidden: the device activation must equal bf16(ReLU(z)); where it does not, it
+      must lie between bf16(ReLU(z - delta)) and bf16(ReLU(z + delta)) -- the bf16
+      rounding of a pre-activation within the accumulation bound of a rounding
+      boundary is ambiguous (both neighbours are correct); such cases are counted.
+    * output: |z_dev - z| <= delta.
+    Layer 1's input is q(x) computed by the oracle, so the observation encoding is
+    checked bit-exactly through it.  Returns (n_ambiguous, n_hidden_total).
+    """
+    from .quant import bf16_fast
+    h = bf16_fast(np.asarray(x, dtype=np.float64))
+    hid = bf16_bits_to_f64(np.asarray(hidden_bits).view(np.uint16))
+    n_amb = 0
+    n_tot = 0
+    n = len(layers64)
+    for li, (w, b) in enumerate(layers64):
+        z = h @ w.T + b
+        delta = FP32_ACC_BOUND * (np.abs(h) @ np.abs(w).T + np.abs(b)) + 1e-30
+        if li < n - 1:
+            dev = hid[:, li, : w.shape[0]]
+            exp = bf16_fast(np.maximum(z, 0.0))
+            diff = dev != exp
+            if diff.any():
+                lo = bf16_fast(np.maximum(z - delta, 0.0))
+                hi = bf16_fast(np.maximum(z + delta, 0.0))
+                ok = (dev >= lo) & (dev <= hi)
+                bad = diff & ~ok
+                assert not bad.any(), (
+                    f"layer {li}: {int(bad.sum())} activations differ beyond the fp32 bound; first at "
+                    f"{np.argwhere(bad)[0].tolist()}")
+                n_amb += int(diff.sum())
+            n_tot += dev.size
+            h = dev          # teacher forcing: the next layer consumes the device's activations
+        else:
+            err = np.abs(np.asarray(z_dev, dtype=np.float64) - z)
+            bad = err > delta
+            assert not bad.any(), f"output: {int(bad.sum())} beyond the fp32 bound, worst {float((err / delta).max()):.2f}x"
+    return n_amb, n_tot
+
+
 def forward_loops(layers64, x) -> list:
     """Single-sample explicit-loop forward (pin for ``forward``)."""
     from .quant import bf16

@@ -1,0 +1,623 @@
+// api.cu -- the C ABI of libfinenv.so (include/fin.h): argument validation,
+// handle / memory management, weight packing, kernel dispatch.  Host code only.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "fin_internal.cuh"
+#include "rollout_tc.cuh"
+#include "tc_plan.cuh"
+
+namespace fin {
+cudaError_t launch_stock_rollout(int net, const tc::TcParams& p, int n_tiles, cudaStream_t s);
+cudaError_t launch_crypto_rollout(const tc::TcParams& p, int n_tiles, cudaStream_t s);
+cudaError_t launch_mlp_probe(int net, const tc::TcParams& p, int n_tiles, cudaStream_t s);
+}  // namespace fin
+
+struct fin_env {
+  fin_env_config cfg;
+  EnvDev d;
+  int device;
+  cudaStream_t last_stream;
+  void* state_mem;
+  float* market_mem;
+  double* agg_scratch;
+  size_t agg_cap;  // rows of FIN_AGG_LEN
+};
+
+struct fin_policy {
+  int32_t kind;
+  int32_t net;                 // 0 stock C1, 1 stock small, 2 crypto
+  int32_t dims[4];
+  uint8_t* wpack;              // device, TcPlan layout
+  float* bias;                 // device, [HID + HID + OUT_PAD]
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(FIN_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define FIN_CUDA(call)                                    \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);   \
+  } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int check_device(int ordinal) {
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, ordinal);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(FIN_E_UNSUPPORTED, "device %d is sm_%d%d; libfinenv.so is built for sm_100a only", ordinal,
+                prop.major, prop.minor);
+  return FIN_OK;
+}
+
+TrajDev to_dev(const fin_traj* o) {
+  TrajDev t;
+  std::memset(&t, 0, sizeof(t));
+  if (!o) return t;
+  t.reward = o->reward;
+  t.done = o->done;
+  t.actions = o->actions;
+  t.cash = o->cash;
+  t.hold = o->hold;
+  t.asset = o->asset;
+  t.mlp_out = o->mlp_out;
+  t.mlp_hidden = o->mlp_hidden;
+  t.ep_metrics = o->ep_metrics;
+  t.ep_count = o->ep_count;
+  t.ep_capacity = o->ep_metrics ? o->ep_capacity : 0;
+  t.agg_partial = nullptr;
+  return t;
+}
+
+int ensure_agg(fin_env* env, size_t rows) {
+  if (env->agg_cap >= rows) return FIN_OK;
+  if (env->agg_scratch) cudaFree(env->agg_scratch);
+  env->agg_scratch = nullptr;
+  env->agg_cap = 0;
+  FIN_CUDA(cudaMalloc(&env->agg_scratch, rows * FIN_AGG_LEN * sizeof(double)));
+  env->agg_cap = rows;
+  return FIN_OK;
+}
+
+// network id from dims, -1 if not compiled
+int net_of(const int32_t* dims) {
+  if (dims[0] == 301 && dims[1] == 256 && dims[2] == 256 && dims[3] == 30) return 0;
+  if (dims[0] == 25 && dims[1] == 128 && dims[2] == 128 && dims[3] == 4) return 1;
+  if (dims[0] == 103 && dims[1] == 128 && dims[2] == 128 && dims[3] == 3) return 2;
+  return -1;
+}
+
+template <class Plan>
+void pack_member(const int32_t* dims, const uint16_t* const* w, const float* const* bias, std::vector<uint8_t>& wp,
+                 std::vector<float>& bp) {
+  wp.assign(Plan::kMemberBytes, 0);
+  for (int s = 0; s < Plan::kStages; ++s) {
+    const int l = Plan::layer_of(s), j0 = Plan::j0_of(s), nks = Plan::nks_of(s);
+    const int kt = nks * 16, rows = Plan::nrows(l);
+    const int in_l = dims[l], out_l = dims[l + 1];
+    uint8_t* base = wp.data() + Plan::offset_of(s);
+    for (int n = 0; n < rows; ++n)
+      for (int kk = 0; kk < kt; ++kk) {
+        const int k = j0 * 16 + kk;
+        const uint16_t v = (n < out_l && k < in_l) ? w[l][(size_t)n * in_l + k] : (uint16_t)0;
+        std::memcpy(base + tc_cm_offset(n, kk, kt), &v, 2);
+      }
+  }
+  bp.assign(Plan::kBiasFloats, 0.f);
+  for (int l = 0; l < 3; ++l) {
+    const int off = l == 0 ? 0 : (l == 1 ? Plan::kHid : 2 * Plan::kHid);
+    if (bias && bias[l])
+      for (int n = 0; n < dims[l + 1]; ++n) bp[off + n] = bias[l][n];
+  }
+}
+
+bool finite_all(const float* x, int64_t n) {
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(x[i])) return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fin_last_error(void) { return g_err.c_str(); }
+int fin_abi_version(void) { return FIN_ABI_VERSION; }
+int fin_device_check(int32_t ordinal) { return check_device(ordinal); }
+
+int fin_env_create(const fin_env_config* cfg, const float* market, int64_t market_elems, void* stream,
+                   fin_env** out) {
+  if (!cfg || !market || !out) return fail(FIN_E_CONFIG, "fin_env_create: null argument");
+  *out = nullptr;
+  const fin_env_config& c = *cfg;
+  if (c.task != FIN_STOCK && c.task != FIN_CRYPTO) return fail(FIN_E_CONFIG, "task must be FIN_STOCK or FIN_CRYPTO");
+  if (c.num_envs < 1) return fail(FIN_E_CONFIG, "num_envs must be >= 1");
+  if (c.num_rows < 2) return fail(FIN_E_CONFIG, "num_rows must be >= 2");
+  if (c.episode_len < 1) return fail(FIN_E_CONFIG, "episode_len must be >= 1");
+  if (!(c.initial_cash > 0) || !std::isfinite(c.initial_cash)) return fail(FIN_E_CONFIG, "initial_cash must be > 0");
+  if (!(c.cost_rate >= 0 && c.cost_rate < 1)) return fail(FIN_E_CONFIG, "cost_rate must be in [0, 1)");
+  if (!std::isfinite(c.reward_scale)) return fail(FIN_E_CONFIG, "reward_scale must be finite");
+  int dev = 0;
+  FIN_CUDA(cudaGetDevice(&dev));
+  int rc = check_device(dev);
+  if (rc != FIN_OK) return rc;
+
+  EnvDev d;
+  std::memset(&d, 0, sizeof(d));
+  d.task = c.task;
+  d.N = c.num_envs;
+  d.rows = c.num_rows;
+  d.L = c.episode_len;
+  d.autoreset = c.autoreset ? 1 : 0;
+  d.cash0 = c.initial_cash;
+  d.cost = c.cost_rate;
+  d.scale = c.reward_scale;
+  d.up = 1.0 + c.cost_rate;
+  d.dn = 1.0 - c.cost_rate;
+  d.noise_std = c.noise_std;
+  d.ou_theta = c.ou_theta;
+  d.ou_sigma = c.ou_sigma;
+  d.eps = c.epsilon;
+  d.seed = c.seed;
+  d.env_offset = c.env_offset;
+  d.t_global = 0;
+  int64_t expect = 0;
+  if (c.task == FIN_STOCK) {
+    if (c.num_assets < 1 || c.num_assets > FIN_MAX_ASSETS) return fail(FIN_E_CONFIG, "num_assets must be in [1, 32]");
+    if (c.num_indicators < 0) return fail(FIN_E_CONFIG, "num_indicators must be >= 0");
+    if (c.max_trade < 1 || c.max_trade > FIN_HOLD_MAX) return fail(FIN_E_CONFIG, "max_trade must be in [1, 32767]");
+    if (c.num_windows < 1 || c.window_block < 1 || c.window_stride < 0 || c.window_offset < 0 || c.window_base < 0)
+      return fail(FIN_E_CONFIG, "window parameters invalid");
+    // every window's last transition reads row start + L, which must exist
+    const int64_t last = (int64_t)c.window_offset + (int64_t)(c.num_windows - 1) * c.window_stride + c.episode_len;
+    if (last >= c.num_rows)
+      return fail(FIN_E_CONFIG, "windows exceed the market: last row %lld >= num_rows %d", (long long)last, c.num_rows);
+    d.K = c.num_assets;
+    d.I = c.num_indicators;
+    d.kp = (c.num_assets + 3) / 4 * 4;
+    d.row_floats = (2 + c.num_indicators) * d.kp;
+    d.wstride = c.window_stride;
+    d.woff = c.window_offset;
+    d.W = c.num_windows;
+    d.wblock = c.window_block;
+    d.wbase = c.window_base;
+    d.wadv = c.advance_window_on_reset ? 1 : 0;
+    d.max_trade = c.max_trade;
+    expect = (int64_t)c.num_rows * (2 + c.num_indicators) * c.num_assets;
+  } else {
+    if (c.num_assets != 1) return fail(FIN_E_CONFIG, "crypto env: num_assets must be 1");
+    if (c.pos_limit != 1) return fail(FIN_E_CONFIG, "crypto env: pos_limit must be 1");
+    if (c.max_hold < 1) return fail(FIN_E_CONFIG, "crypto env: max_hold must be >= 1");
+    if (c.episode_len >= c.num_rows) return fail(FIN_E_CONFIG, "crypto env: episode_len must be < num_rows");
+    d.K = 1;
+    d.I = 0;
+    d.kp = 1;
+    d.row_floats = 144;
+    d.W = 1;
+    d.wblock = 1;
+    d.max_trade = 1;
+    d.max_hold = c.max_hold;
+    expect = (int64_t)c.num_rows * 144;
+  }
+  if (market_elems != expect)
+    return fail(FIN_E_CONFIG, "market_elems %lld != expected %lld", (long long)market_elems, (long long)expect);
+  // ---- validate the market: finite, prices > 0
+  if (!finite_all(market, market_elems)) return fail(FIN_E_DATA, "market contains non-finite values");
+  std::vector<float> padded;
+  const float* upload = market;
+  if (c.task == FIN_STOCK) {
+    const int K = c.num_assets, C = 2 + c.num_indicators;
+    for (int r = 0; r < c.num_rows; ++r)
+      for (int k = 0; k < K; ++k)
+        if (!(market[(size_t)r * C * K + k] > 0.f))
+          return fail(FIN_E_DATA, "close price <= 0 at row %d asset %d", r, k);
+    padded.assign((size_t)c.num_rows * d.row_floats, 0.f);
+    for (int r = 0; r < c.num_rows; ++r)
+      for (int ch = 0; ch < C; ++ch)
+        for (int k = 0; k < K; ++k)
+          padded[(size_t)r * d.row_floats + ch * d.kp + k] = market[((size_t)r * C + ch) * K + k];
+    upload = padded.data();
+  } else {
+    for (int r = 0; r < c.num_rows; ++r) {
+      const float* row = market + (size_t)r * 144;
+      if (!(row[0] > 0.f)) return fail(FIN_E_DATA, "mid price <= 0 at row %d", r);
+      for (int l = 0; l < 10; ++l)
+        if (!(row[1 + l] > 0.f) || !(row[21 + l] > 0.f) || row[11 + l] < 0.f || row[31 + l] < 0.f)
+          return fail(FIN_E_DATA, "invalid book level at row %d", r);
+    }
+  }
+  fin_env* env = new (std::nothrow) fin_env();
+  if (!env) return fail(FIN_E_CONFIG, "out of host memory");
+  env->cfg = c;
+  env->device = dev;
+  env->last_stream = S(stream);
+  const size_t N = (size_t)c.num_envs, K = (size_t)d.K;
+  // one allocation for all state arrays (8-byte members first)
+  const size_t n8 = N * 8;  // cash + 6 metric doubles
+  size_t bytes = 7 * n8 * sizeof(double) / 8;   // 7 double arrays
+  bytes += (size_t)FIN_MAX_MEMBERS * K * N * sizeof(float);
+  bytes += N * 4 * sizeof(int32_t);              // t_ep, window, tau, m_n
+  bytes += K * N * sizeof(int16_t);
+  bytes += 256;
+  cudaError_t e;
+  if ((e = cudaMalloc(&env->state_mem, bytes)) != cudaSuccess) { delete env; return cuda_fail(e, "cudaMalloc(state)"); }
+  if ((e = cudaMemset(env->state_mem, 0, bytes)) != cudaSuccess) {
+    cudaFree(env->state_mem);
+    delete env;
+    return cuda_fail(e, "cudaMemset(state)");
+  }
+  uint8_t* p = static_cast<uint8_t*>(env->state_mem);
+  auto take = [&](size_t b) { uint8_t* r = p; p += (b + 15) / 16 * 16; return r; };
+  d.cash = reinterpret_cast<double*>(take(N * 8));
+  d.m_v0 = reinterpret_cast<double*>(take(N * 8));
+  d.m_vprev = reinterpret_cast<double*>(take(N * 8));
+  d.m_peak = reinterpret_cast<double*>(take(N * 8));
+  d.m_mdd = reinterpret_cast<double*>(take(N * 8));
+  d.m_mean = reinterpret_cast<double*>(take(N * 8));
+  d.m_m2 = reinterpret_cast<double*>(take(N * 8));
+  d.ou = reinterpret_cast<float*>(take((size_t)FIN_MAX_MEMBERS * K * N * 4));
+  d.t_ep = reinterpret_cast<int32_t*>(take(N * 4));
+  d.window = reinterpret_cast<int32_t*>(take(N * 4));
+  d.tau = reinterpret_cast<int32_t*>(take(N * 4));
+  d.m_n = reinterpret_cast<int32_t*>(take(N * 4));
+  d.hold = reinterpret_cast<int16_t*>(take(K * N * 2));
+  if ((size_t)(p - static_cast<uint8_t*>(env->state_mem)) > bytes) {
+    cudaFree(env->state_mem);
+    delete env;
+    return fail(FIN_E_CONFIG, "internal: state layout overflow");
+  }
+  // flags word + market copy
+  const size_t mbytes = (size_t)c.num_rows * d.row_floats * sizeof(float);
+  if ((e = cudaMalloc(&env->market_mem, mbytes + 64)) != cudaSuccess) {
+    cudaFree(env->state_mem);
+    delete env;
+    return cuda_fail(e, "cudaMalloc(market)");
+  }
+  d.flags = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(env->market_mem) + mbytes);
+  d.market = env->market_mem;
+  cudaStream_t s = S(stream);
+  e = cudaMemcpyAsync(env->market_mem, upload, mbytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d.flags, 0, 64, s);
+  env->d = d;
+  if (e == cudaSuccess)
+    e = (c.task == FIN_STOCK) ? fin::launch_stock_reset(d, nullptr, s) : fin::launch_crypto_reset(d, nullptr, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    cudaFree(env->market_mem);
+    cudaFree(env->state_mem);
+    delete env;
+    return cuda_fail(e, "fin_env_create upload/reset");
+  }
+  *out = env;
+  return FIN_OK;
+}
+
+int fin_env_reset(fin_env* env, const uint8_t* mask, void* stream) {
+  if (!env) return fail(FIN_E_CONFIG, "null env");
+  env->last_stream = S(stream);
+  cudaError_t e = env->d.task == FIN_STOCK ? fin::launch_stock_reset(env->d, mask, S(stream))
+                                           : fin::launch_crypto_reset(env->d, mask, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_env_reset");
+  return FIN_OK;
+}
+
+int fin_env_step(fin_env* env, const int16_t* actions, const fin_traj* out, void* stream) {
+  if (!env || !actions) return fail(FIN_E_CONFIG, "fin_env_step: null argument");
+  env->last_stream = S(stream);
+  TrajDev o = to_dev(out);
+  o.ep_metrics = nullptr;
+  o.ep_count = nullptr;
+  cudaError_t e = env->d.task == FIN_STOCK ? fin::launch_stock_step(env->d, actions, o, S(stream))
+                                           : fin::launch_crypto_step(env->d, actions, o, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_env_step");
+  env->d.t_global += 1;
+  return FIN_OK;
+}
+
+int fin_env_get_state(const fin_env* env, double* cash, int16_t* hold, double* asset, int32_t* t_ep,
+                      int32_t* window, void* stream) {
+  if (!env) return fail(FIN_E_CONFIG, "null env");
+  cudaError_t e;
+  if (env->d.task == FIN_STOCK)
+    e = fin::launch_stock_get_state(env->d, cash, hold, asset, t_ep, window, S(stream));
+  else {
+    e = fin::launch_crypto_get_state(env->d, cash, hold, asset, t_ep, S(stream));
+    if (e == cudaSuccess && window) e = cudaMemsetAsync(window, 0, sizeof(int32_t) * env->d.N, S(stream));
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "fin_env_get_state");
+  return FIN_OK;
+}
+
+int fin_env_set_state(fin_env* env, const double* cash, const int16_t* hold, const int32_t* t_ep,
+                      const int32_t* window, const int32_t* tau, void* stream) {
+  if (!env) return fail(FIN_E_CONFIG, "null env");
+  env->last_stream = S(stream);
+  cudaError_t e = env->d.task == FIN_STOCK
+                      ? fin::launch_stock_set_state(env->d, cash, hold, t_ep, window, S(stream))
+                      : fin::launch_crypto_set_state(env->d, cash, hold, t_ep, tau, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_env_set_state");
+  return FIN_OK;
+}
+
+int fin_env_check(fin_env* env, uint32_t* flags) {
+  if (!env) return fail(FIN_E_CONFIG, "null env");
+  FIN_CUDA(cudaStreamSynchronize(env->last_stream));
+  uint32_t f = 0;
+  FIN_CUDA(cudaMemcpy(&f, env->d.flags, sizeof(f), cudaMemcpyDeviceToHost));
+  FIN_CUDA(cudaMemset(env->d.flags, 0, sizeof(uint32_t)));
+  if (flags) *flags = f;
+  if (f) return fail(FIN_E_DEVICE_ASYNC, "device flags 0x%x (1 action range, 2 episode done, 4 non-finite, 8 index)", f);
+  return FIN_OK;
+}
+
+void fin_env_destroy(fin_env* env) {
+  if (!env) return;
+  cudaStreamSynchronize(env->last_stream);
+  if (env->agg_scratch) cudaFree(env->agg_scratch);
+  if (env->market_mem) cudaFree(env->market_mem);
+  if (env->state_mem) cudaFree(env->state_mem);
+  delete env;
+}
+
+int fin_policy_create(int32_t kind, int32_t n_layers, const int32_t* dims, const uint16_t* const* w_bf16,
+                      const float* const* bias, void* stream, fin_policy** out) {
+  if (!dims || !w_bf16 || !out) return fail(FIN_E_CONFIG, "fin_policy_create: null argument");
+  *out = nullptr;
+  if (kind < FIN_PPO_GAUSS || kind > FIN_Q_ARGMAX) return fail(FIN_E_CONFIG, "unknown policy kind %d", kind);
+  if (n_layers != 3) return fail(FIN_E_UNSUPPORTED, "only 3-layer networks are compiled (got %d)", n_layers);
+  for (int l = 0; l < 3; ++l)
+    if (!w_bf16[l]) return fail(FIN_E_CONFIG, "weight %d is null", l);
+  const int net = net_of(dims);
+  if (net < 0)
+    return fail(FIN_E_UNSUPPORTED, "network %d-%d-%d-%d not compiled (have 301-256-256-30, 25-128-128-4, 103-128-128-3)",
+                dims[0], dims[1], dims[2], dims[3]);
+  if ((net == 2) != (kind == FIN_Q_ARGMAX)) return fail(FIN_E_CONFIG, "Q_ARGMAX pairs with the 103-128-128-3 Q-net");
+  for (int l = 0; l < 3; ++l) {
+    if (bias && bias[l] && !finite_all(bias[l], dims[l + 1])) return fail(FIN_E_DATA, "bias %d non-finite", l);
+  }
+  std::vector<uint8_t> wp;
+  std::vector<float> bp;
+  if (net == 0) pack_member<PlanStockC1>(dims, w_bf16, bias, wp, bp);
+  else if (net == 1) pack_member<PlanStockSmall>(dims, w_bf16, bias, wp, bp);
+  else pack_member<PlanCrypto>(dims, w_bf16, bias, wp, bp);
+  fin_policy* pol = new (std::nothrow) fin_policy();
+  if (!pol) return fail(FIN_E_CONFIG, "out of host memory");
+  pol->kind = kind;
+  pol->net = net;
+  for (int l = 0; l < 4; ++l) pol->dims[l] = dims[l];
+  cudaError_t e = cudaMalloc(&pol->wpack, wp.size());
+  if (e == cudaSuccess) e = cudaMalloc(&pol->bias, bp.size() * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(pol->wpack, wp.data(), wp.size(), cudaMemcpyHostToDevice, S(stream));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(pol->bias, bp.data(), bp.size() * 4, cudaMemcpyHostToDevice, S(stream));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+  if (e != cudaSuccess) {
+    if (pol->wpack) cudaFree(pol->wpack);
+    if (pol->bias) cudaFree(pol->bias);
+    delete pol;
+    return cuda_fail(e, "fin_policy_create upload");
+  }
+  *out = pol;
+  return FIN_OK;
+}
+
+void fin_policy_destroy(fin_policy* pol) {
+  if (!pol) return;
+  cudaDeviceSynchronize();
+  cudaFree(pol->wpack);
+  cudaFree(pol->bias);
+  delete pol;
+}
+
+}  // extern "C"
+
+namespace {
+
+int fill_members(const fin_env* env, const fin_policy* const* members, int32_t n, const float* member_w,
+                 tc::TcParams& p, int* net_out) {
+  if (!members || n < 1 || n > FIN_MAX_MEMBERS) return fail(FIN_E_CONFIG, "n_members must be in [1, %d]", FIN_MAX_MEMBERS);
+  int net = -1, n_ddpg = 0;
+  for (int m = 0; m < n; ++m) {
+    if (!members[m]) return fail(FIN_E_CONFIG, "member %d is null", m);
+    if (net >= 0 && members[m]->net != net) return fail(FIN_E_CONFIG, "members must share one network shape");
+    net = members[m]->net;
+    p.wpack[m] = members[m]->wpack;
+    p.bias[m] = members[m]->bias;
+    p.kinds[m] = members[m]->kind;
+    if (members[m]->kind == FIN_DDPG_OU) ++n_ddpg;
+    p.mw[m] = member_w ? member_w[m] : 1.f;
+  }
+  if (n_ddpg > 1) return fail(FIN_E_UNSUPPORTED, "at most one DDPG member (OU state slot) per rollout");
+  if (env->d.task == FIN_STOCK) {
+    if (net == 2) return fail(FIN_E_CONFIG, "stock env needs a stock policy");
+    const int need_k = net == 0 ? 30 : 4, need_i = net == 0 ? 8 : 4;
+    if (env->d.K != need_k || env->d.I != need_i)
+      return fail(FIN_E_UNSUPPORTED, "policy network expects K=%d, I=%d; env has K=%d, I=%d", need_k, need_i,
+                  env->d.K, env->d.I);
+  } else {
+    if (net != 2 || n != 1) return fail(FIN_E_CONFIG, "crypto env takes exactly one Q_ARGMAX member");
+  }
+  p.M = n;
+  p.weighted = member_w ? 1 : 0;
+  *net_out = net;
+  return FIN_OK;
+}
+
+int fill_noise(const fin_noise* noise, tc::TcParams& p) {
+  if (!noise) {
+    p.noise_mode = FIN_NOISE_NONE;
+    return FIN_OK;
+  }
+  if (noise->mode < FIN_NOISE_PHILOX || noise->mode > FIN_NOISE_NONE) return fail(FIN_E_CONFIG, "bad noise mode");
+  if (noise->mode == FIN_NOISE_SUPPLIED && !noise->supplied) return fail(FIN_E_CONFIG, "supplied noise is null");
+  p.noise_mode = noise->mode;
+  p.noise_seed = noise->seed;
+  p.noise = noise->supplied;
+  return FIN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fin_rollout(fin_env* env, const fin_policy* const* members, int32_t n_members, const float* member_w, int32_t T,
+                const fin_noise* noise, const fin_traj* out, void* stream) {
+  if (!env) return fail(FIN_E_CONFIG, "null env");
+  if (T < 0) return fail(FIN_E_CONFIG, "T must be >= 0");
+  if (T == 0) return FIN_OK;
+  tc::TcParams p;
+  std::memset(&p, 0, sizeof(p));
+  int net = -1;
+  int rc = fill_members(env, members, n_members, member_w, p, &net);
+  if (rc != FIN_OK) return rc;
+  rc = fill_noise(noise, p);
+  if (rc != FIN_OK) return rc;
+  const int n_tiles = (env->d.N + tc::kTileM - 1) / tc::kTileM;
+  p.e = env->d;
+  p.o = to_dev(out);
+  p.T = T;
+  if (out && out->agg) {
+    rc = ensure_agg(env, (size_t)n_tiles);
+    if (rc != FIN_OK) return rc;
+    p.o.agg_partial = env->agg_scratch;
+  }
+  env->last_stream = S(stream);
+  cudaError_t e = env->d.task == FIN_STOCK ? fin::launch_stock_rollout(net, p, n_tiles, S(stream))
+                                           : fin::launch_crypto_rollout(p, n_tiles, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_rollout launch");
+  if (out && out->agg) {
+    e = fin::launch_agg_finalize(env->agg_scratch, n_tiles, out->agg, S(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "fin_rollout agg");
+  }
+  env->d.t_global += T;
+  return FIN_OK;
+}
+
+int fin_rollout_actions(fin_env* env, const int16_t* actions, int32_t T, const fin_traj* out, void* stream) {
+  if (!env || !actions) return fail(FIN_E_CONFIG, "fin_rollout_actions: null argument");
+  if (T < 0) return fail(FIN_E_CONFIG, "T must be >= 0");
+  if (T == 0) return FIN_OK;
+  if (env->d.task != FIN_STOCK) return fail(FIN_E_UNSUPPORTED, "fin_rollout_actions: stock envs only");
+  TrajDev o = to_dev(out);
+  const int nb = (env->d.N + 255) / 256;
+  if (out && out->agg) {
+    int rc = ensure_agg(env, (size_t)nb);
+    if (rc != FIN_OK) return rc;
+    o.agg_partial = env->agg_scratch;
+  }
+  env->last_stream = S(stream);
+  int n_blocks = 0;
+  cudaError_t e = fin::launch_stock_replay(env->d, actions, T, o, &n_blocks, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_rollout_actions launch");
+  if (out && out->agg) {
+    e = fin::launch_agg_finalize(env->agg_scratch, n_blocks, out->agg, S(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "fin_rollout_actions agg");
+  }
+  env->d.t_global += T;
+  return FIN_OK;
+}
+
+int fin_ensemble_act(fin_env* env, const fin_policy* const* members, int32_t n_members, const float* member_w,
+                     const fin_noise* noise, int16_t* actions, float* mean_action, void* stream) {
+  if (!env || !actions) return fail(FIN_E_CONFIG, "fin_ensemble_act: null argument");
+  if (env->d.task != FIN_STOCK) return fail(FIN_E_UNSUPPORTED, "fin_ensemble_act: stock envs only");
+  tc::TcParams p;
+  std::memset(&p, 0, sizeof(p));
+  int net = -1;
+  int rc = fill_members(env, members, n_members, member_w, p, &net);
+  if (rc != FIN_OK) return rc;
+  rc = fill_noise(noise, p);
+  if (rc != FIN_OK) return rc;
+  if (p.noise_mode == FIN_NOISE_SUPPLIED) {
+    // supplied noise is indexed [t][M][N][K] with t = 0
+  }
+  p.e = env->d;
+  p.T = 1;
+  p.act_only = 1;
+  p.mean_out = mean_action;
+  p.o.actions = actions;
+  const int n_tiles = (env->d.N + tc::kTileM - 1) / tc::kTileM;
+  env->last_stream = S(stream);
+  cudaError_t e = fin::launch_stock_rollout(net, p, n_tiles, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_ensemble_act launch");
+  return FIN_OK;
+}
+
+int fin_episode_metrics(const double* equity, const uint8_t* done, int32_t T, int32_t N, double reset_equity,
+                        double periods_per_year, double rf, double* ep_metrics, int32_t ep_capacity,
+                        int32_t* ep_count, double* agg, void* stream) {
+  if (!equity || !done) return fail(FIN_E_CONFIG, "fin_episode_metrics: null argument");
+  if (T < 1 || N < 1) return fail(FIN_E_CONFIG, "T and N must be >= 1");
+  if (!(periods_per_year > 0)) return fail(FIN_E_CONFIG, "periods_per_year must be > 0");
+  double* partial = nullptr;
+  const int env_blocks = (N + 127) / 128;
+  const size_t max_rows = (size_t)env_blocks * 4096;
+  cudaStream_t s = S(stream);
+  if (agg) FIN_CUDA(cudaMallocAsync(&partial, max_rows * FIN_AGG_LEN * sizeof(double), s));
+  int n_blocks = 0;
+  cudaError_t e = fin::launch_episode_metrics(equity, done, T, N, reset_equity, periods_per_year, rf, ep_metrics,
+                                              ep_metrics ? ep_capacity : 0, ep_count, partial, &n_blocks, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fin_episode_metrics launch");
+  if (agg) {
+    e = fin::launch_agg_finalize(partial, n_blocks, agg, s);
+    cudaFreeAsync(partial, s);
+    if (e != cudaSuccess) return cuda_fail(e, "fin_episode_metrics agg");
+  }
+  return FIN_OK;
+}
+
+int fin_mlp_forward(const fin_policy* pol, const uint16_t* x, int32_t B, float* z, uint16_t* hidden, void* stream) {
+  if (!pol || !x || !z) return fail(FIN_E_CONFIG, "fin_mlp_forward: null argument");
+  if (B < 1) return fail(FIN_E_CONFIG, "B must be >= 1");
+  tc::TcParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.wpack[0] = pol->wpack;
+  p.bias[0] = pol->bias;
+  p.kinds[0] = pol->kind;
+  p.M = 1;
+  p.T = 1;
+  p.x_in = x;
+  p.z_out = z;
+  p.hid_out = hidden;
+  p.B = B;
+  p.in_dim = pol->dims[0];
+  p.out_dim = pol->dims[3];
+  const int n_tiles = (B + tc::kTileM - 1) / tc::kTileM;
+  cudaError_t e = fin::launch_mlp_probe(pol->net, p, n_tiles, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_mlp_forward launch");
+  return FIN_OK;
+}
+
+int fin_philox_normals(uint64_t seed, int64_t env_offset, int32_t N, int32_t K, int32_t member, int64_t t_global,
+                       float* out, void* stream) {
+  if (!out || N < 1 || K < 1) return fail(FIN_E_CONFIG, "fin_philox_normals: bad argument");
+  cudaError_t e = fin::launch_philox_normals(seed, env_offset, N, K, member, t_global, out, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_philox_normals launch");
+  return FIN_OK;
+}
+
+}  // extern "C"

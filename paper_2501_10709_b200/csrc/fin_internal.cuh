@@ -1,0 +1,246 @@
+// fin_internal.cuh -- device-side handle layout and shared device helpers of
+// libfinenv.so.  Nothing here is shared with oracle/ (which is independent
+// Python); this is the CUDA product path only.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fin.h"
+
+#define FIN_HOLD_MAX 32767   // holdings are int16 (reading R-HOLD)
+#define FIN_MAX_ASSETS 32
+#define FIN_MAX_MEMBERS 4
+
+// Flat, by-value kernel parameter block describing one env handle on the device.
+// Internal state is SoA: element [k][i] of a [K][N] array is at k*N + i.
+struct EnvDev {
+  // ---- configuration (fin_env_config, validated on the host)
+  int32_t task, N, K, I, rows, L;
+  int32_t wstride, woff, W, wblock, wbase, wadv;
+  int32_t max_trade, max_hold, autoreset;
+  int32_t kp;            // K padded to a multiple of 4 (market channel stride)
+  int32_t row_floats;    // floats per market row: (2+I)*kp (stock) or 144 (crypto)
+  double cash0, cost, scale;
+  double up, dn;         // fl(1 + cost), fl(1 - cost)
+  float noise_std, ou_theta, ou_sigma, eps;
+  uint64_t seed;
+  int64_t env_offset;
+  int64_t t_global;      // global step counter (Philox counter word), advanced per step
+  const float* market;   // [rows][row_floats]
+  // ---- state (library-owned device memory)
+  double* cash;          // [N]
+  int16_t* hold;         // [K][N] (crypto: position in {-1,0,1}, K = 1)
+  int32_t* t_ep;         // [N]
+  int32_t* window;       // [N]
+  int32_t* tau;          // [N] crypto holding time
+  float* ou;             // [FIN_MAX_MEMBERS][K][N] DDPG OU noise state
+  // online episode-metric state (persisted across calls)
+  double* m_v0;          // equity at episode start
+  double* m_vprev;       // last equity
+  double* m_peak;        // running peak
+  double* m_mdd;         // running min drawdown (<= 0)
+  double* m_mean;        // Welford mean of returns
+  double* m_m2;          // Welford M2
+  int32_t* m_n;          // number of returns
+  uint32_t* flags;       // sticky device error word
+};
+
+struct TrajDev {
+  float* reward;
+  uint8_t* done;
+  int16_t* actions;
+  double* cash;
+  int16_t* hold;
+  double* asset;
+  float* mlp_out;
+  uint16_t* mlp_hidden;
+  double* ep_metrics;
+  int32_t* ep_count;
+  int32_t ep_capacity;
+  double* agg_partial;   // [gridDim][FIN_AGG_LEN] scratch, reduced by k_agg_finalize
+};
+
+// ----------------------------------------------------------------- exact fp64
+// Every env-side float64 operation uses explicit round-to-nearest intrinsics so
+// the compiler can never contract a*b+c into an FMA: the op order and rounding
+// equal DESIGN.md §4.2 (the oracle's order) by construction.
+__device__ __forceinline__ double fadd64(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double fsub64(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double fmul64(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double fdiv64(double a, double b) { return __ddiv_rn(a, b); }
+
+__device__ __forceinline__ void set_flag(const EnvDev& e, uint32_t bit) { atomicOr(e.flags, bit); }
+
+// ----------------------------------------------------------------- windows (R10)
+__device__ __forceinline__ int32_t window_of(const EnvDev& e, int64_t g) {
+  int64_t w = ((int64_t)e.wbase + g / e.wblock) % e.W;
+  return (int32_t)w;
+}
+__device__ __forceinline__ int32_t day_of(const EnvDev& e, int32_t w, int32_t t) {
+  return e.woff + w * e.wstride + t;
+}
+
+// ----------------------------------------------------------------- affordability (R5)
+// Largest n in [0, want] with fl(n*u) <= b.  fl(n*u) is monotone in n.  The fast
+// path (enough cash) is one multiply; otherwise an fp32 estimate of b/u (relative
+// error ~1e-7, so within +-1 of the answer for n < 2^15) is corrected by exact
+// fp64 checks until the definition holds.
+__device__ __forceinline__ int affordable(double b, double u, int want) {
+  if (want <= 0) return 0;
+  if (fmul64((double)want, u) <= b) return want;
+  if (!(b >= 0.0)) return 0;
+  float qf = __fdiv_rn((float)b, (float)u);
+  int n = (int)fminf(floorf(qf), (float)want);
+  if (n < 0) n = 0;
+  while (n > 0 && fmul64((double)n, u) > b) --n;
+  while (n < want && fmul64((double)(n + 1), u) <= b) ++n;
+  return n;
+}
+
+// ----------------------------------------------------------------- online metrics
+// Per-episode accumulators: equity v_0 .. v_L, returns
+// r_t = v_t / v_{t-1} - 1 (Welford mean / M2), running peak and min drawdown.
+struct MetricAcc {
+  double v0, vprev, peak, mdd, mean, m2;
+  int32_t n;
+};
+
+__device__ __forceinline__ void metric_start(MetricAcc& m, double v) {
+  m.v0 = v; m.vprev = v; m.peak = v; m.mdd = 0.0; m.mean = 0.0; m.m2 = 0.0; m.n = 0;
+}
+
+__device__ __forceinline__ void metric_push(MetricAcc& m, double v) {
+  double r = fsub64(fdiv64(v, m.vprev), 1.0);
+  m.n += 1;
+  double delta = fsub64(r, m.mean);
+  m.mean = fadd64(m.mean, fdiv64(delta, (double)m.n));
+  m.m2 = fadd64(m.m2, fmul64(delta, fsub64(r, m.mean)));
+  if (v > m.peak) m.peak = v;
+  double dd = fsub64(fdiv64(v, m.peak), 1.0);
+  if (dd < m.mdd) m.mdd = dd;
+  m.vprev = v;
+}
+
+// (cum, sharpe, mdd) of a finished episode; Sharpe = sqrt(ppy) mean / std(ddof 1),
+// NaN when n < 2 or std == 0 (reading R21).
+__device__ __forceinline__ void metric_finish(const MetricAcc& m, double ppy, double rf, double out[3]) {
+  out[0] = fsub64(fdiv64(m.vprev, m.v0), 1.0);
+  double sh = __longlong_as_double(0x7ff8000000000000ULL);
+  if (m.n >= 2) {
+    double sd = sqrt(fdiv64(m.m2, (double)(m.n - 1)));
+    if (sd > 0.0) sh = fdiv64(fmul64(sqrt(ppy), fsub64(m.mean, rf)), sd);
+  }
+  out[1] = sh;
+  out[2] = m.mdd;
+}
+
+// ----------------------------------------------------------------- block aggregate
+// Per-block partial of the FIN_AGG_* vector, reduced across the block in smem in a
+// fixed order (deterministic), written to agg_partial[blockIdx.x][.].
+struct AggAcc {
+  double s[FIN_AGG_LEN];
+};
+__device__ __forceinline__ void agg_init(AggAcc& a) {
+#pragma unroll
+  for (int j = 0; j < FIN_AGG_NSUM; ++j) a.s[j] = 0.0;
+  a.s[FIN_AGG_MIN_MDD] = __longlong_as_double(0x7ff0000000000000ULL);  // +inf
+  a.s[7] = __longlong_as_double(0x7ff0000000000000ULL);
+}
+__device__ __forceinline__ void agg_episode(AggAcc& a, const double m[3]) {
+  a.s[FIN_AGG_EPISODES] += 1.0;
+  a.s[FIN_AGG_SUM_CUM] += m[0];
+  if (isfinite(m[1])) { a.s[FIN_AGG_SUM_SHARPE] += m[1]; a.s[FIN_AGG_N_SHARPE] += 1.0; }
+  a.s[FIN_AGG_SUM_MDD] += m[2];
+  a.s[FIN_AGG_MIN_MDD] = fmin(a.s[FIN_AGG_MIN_MDD], m[2]);
+  a.s[7] = fmin(a.s[7], m[0]);
+}
+
+// Block-wide deterministic reduction (blockDim.x a multiple of 32, <= 1024).
+__device__ inline void agg_block_write(const AggAcc& a, double* partial_row) {
+  __shared__ double red[32][FIN_AGG_LEN];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double v[FIN_AGG_LEN];
+#pragma unroll
+  for (int j = 0; j < FIN_AGG_LEN; ++j) v[j] = a.s[j];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int j = 0; j < FIN_AGG_LEN; ++j) {
+      double o = __shfl_down_sync(0xffffffffu, v[j], off);
+      v[j] = (j < FIN_AGG_NSUM) ? v[j] + o : fmin(v[j], o);
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < FIN_AGG_LEN; ++j) red[wid][j] = v[j];
+  }
+  __syncthreads();
+  if (threadIdx.x < FIN_AGG_LEN) {
+    const int j = threadIdx.x;
+    double s = red[0][j];
+    for (int w = 1; w < nw; ++w) s = (j < FIN_AGG_NSUM) ? s + red[w][j] : fmin(s, red[w][j]);
+    partial_row[j] = s;
+  }
+}
+
+// Same reduction for a 128-thread warpgroup that synchronises on named barrier
+// ``bar_id`` (used inside warp-specialised kernels where other warps are busy).
+__device__ inline void agg_group_write(const AggAcc& a, double* partial_row, int group_tid, int bar_id) {
+  __shared__ double red_g[4][FIN_AGG_LEN];
+  const int lane = group_tid & 31, wid = group_tid >> 5;
+  double v[FIN_AGG_LEN];
+#pragma unroll
+  for (int j = 0; j < FIN_AGG_LEN; ++j) v[j] = a.s[j];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int j = 0; j < FIN_AGG_LEN; ++j) {
+      double o = __shfl_down_sync(0xffffffffu, v[j], off);
+      v[j] = (j < FIN_AGG_NSUM) ? v[j] + o : fmin(v[j], o);
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < FIN_AGG_LEN; ++j) red_g[wid][j] = v[j];
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(128) : "memory");
+  if (group_tid < FIN_AGG_LEN) {
+    const int j = group_tid;
+    double s = red_g[0][j];
+    for (int w = 1; w < 4; ++w) s = (j < FIN_AGG_NSUM) ? s + red_g[w][j] : fmin(s, red_g[w][j]);
+    partial_row[j] = s;
+  }
+}
+
+// round half away from zero of an fp32 value (R18), exact: y - trunc(y) is exact
+__device__ __forceinline__ int rha_f32(float y) {
+  const float n = truncf(y);
+  const float f = fabsf(__fsub_rn(y, n));
+  int r = (int)n;
+  if (f >= 0.5f) r += (y >= 0.f) ? 1 : -1;
+  return r;
+}
+
+// ----------------------------------------------------------------- host launchers
+namespace fin {
+cudaError_t launch_stock_reset(const EnvDev& e, const uint8_t* mask, cudaStream_t s);
+cudaError_t launch_stock_step(const EnvDev& e, const int16_t* actions, const TrajDev& o, cudaStream_t s);
+cudaError_t launch_stock_replay(const EnvDev& e, const int16_t* actions, int T, const TrajDev& o,
+                                int* n_blocks, cudaStream_t s);
+cudaError_t launch_stock_get_state(const EnvDev& e, double* cash, int16_t* hold, double* asset,
+                                   int32_t* t_ep, int32_t* window, cudaStream_t s);
+cudaError_t launch_stock_set_state(const EnvDev& e, const double* cash, const int16_t* hold,
+                                   const int32_t* t_ep, const int32_t* window, cudaStream_t s);
+cudaError_t launch_crypto_reset(const EnvDev& e, const uint8_t* mask, cudaStream_t s);
+cudaError_t launch_crypto_step(const EnvDev& e, const int16_t* actions, const TrajDev& o, cudaStream_t s);
+cudaError_t launch_crypto_get_state(const EnvDev& e, double* cash, int16_t* hold, double* asset,
+                                    int32_t* t_ep, cudaStream_t s);
+cudaError_t launch_crypto_set_state(const EnvDev& e, const double* cash, const int16_t* hold,
+                                    const int32_t* t_ep, const int32_t* tau, cudaStream_t s);
+cudaError_t launch_agg_finalize(const double* partial, int n_blocks, double* agg, cudaStream_t s);
+cudaError_t launch_episode_metrics(const double* equity, const uint8_t* done, int T, int N, double reset_eq,
+                                   double ppy, double rf, double* ep, int cap, int32_t* cnt,
+                                   double* partial, int* n_blocks, cudaStream_t s);
+cudaError_t launch_philox_normals(uint64_t seed, int64_t off, int N, int K, int member, int64_t t,
+                                  float* out, cudaStream_t s);
+}  // namespace fin

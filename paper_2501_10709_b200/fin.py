@@ -1,0 +1,357 @@
+"""Thin Python binding of libfinenv.so (include/fin.h) -- argument marshalling only.
+
+Every function here has the name of the C entry point it calls and does nothing
+but convert arguments (torch tensors -> device pointers, NumPy arrays -> host
+pointers, ``torch.cuda.Stream`` -> ``cudaStream_t``) and turn a non-OK status
+into :class:`FinError`.  All arithmetic of the hot path runs in the CUDA kernels
+of the library; there is no CPU fallback -- importing this module on a machine
+without the built library raises.
+
+PyTorch is used only for device memory and streams (tensors are allocated by the
+caller, see ``paper_2501_10709_b200.runtime`` for the conveniences built on it).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfinenv.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -m paper_2501_10709_b200.build` "
+        "(nvcc, sm_100a). There is no CPU fallback.")
+_lib = C.CDLL(LIB_PATH)
+
+# ----------------------------------------------------------------- constants (fin.h)
+FIN_OK, FIN_E_CONFIG, FIN_E_DATA, FIN_E_NUMERIC, FIN_E_CUDA, FIN_E_EPISODE_DONE, FIN_E_UNSUPPORTED, \
+    FIN_E_DEVICE_ASYNC = range(8)
+FIN_FLAG_ACTION_RANGE, FIN_FLAG_EPISODE_DONE, FIN_FLAG_NONFINITE, FIN_FLAG_BAD_INDEX = 1, 2, 4, 8
+FIN_STOCK, FIN_CRYPTO = 0, 1
+FIN_PPO_GAUSS, FIN_SAC_SQUASH, FIN_DDPG_OU, FIN_Q_ARGMAX = 0, 1, 2, 3
+FIN_NOISE_PHILOX, FIN_NOISE_SUPPLIED, FIN_NOISE_NONE = 0, 1, 2
+FIN_AGG_EPISODES, FIN_AGG_SUM_CUM, FIN_AGG_SUM_SHARPE, FIN_AGG_N_SHARPE, FIN_AGG_SUM_MDD, \
+    FIN_AGG_SUM_REWARD = range(6)
+FIN_AGG_NSUM = 6
+FIN_AGG_MIN_MDD = 6
+FIN_AGG_MIN_CUM = 7
+FIN_AGG_LEN = 8
+
+# every symbol include/fin.h declares (checked by tests/test_abi.py)
+EXPORTS = ("fin_env_create", "fin_env_reset", "fin_env_step", "fin_env_get_state", "fin_env_set_state",
+           "fin_env_check", "fin_env_destroy", "fin_policy_create", "fin_policy_destroy", "fin_rollout",
+           "fin_rollout_actions", "fin_ensemble_act", "fin_episode_metrics", "fin_mlp_forward",
+           "fin_philox_normals", "fin_last_error", "fin_abi_version", "fin_device_check")
+
+
+class FinError(RuntimeError):
+    def __init__(self, code: int, where: str, msg: str):
+        super().__init__(f"{where}: status {code}: {msg}")
+        self.code = code
+
+
+class fin_env_config(C.Structure):
+    _fields_ = [("task", C.c_int32), ("num_envs", C.c_int32), ("num_assets", C.c_int32),
+                ("num_indicators", C.c_int32), ("num_rows", C.c_int32), ("episode_len", C.c_int32),
+                ("window_stride", C.c_int32), ("window_offset", C.c_int32), ("num_windows", C.c_int32),
+                ("window_block", C.c_int32), ("window_base", C.c_int32), ("advance_window_on_reset", C.c_int32),
+                ("max_trade", C.c_int32), ("max_hold", C.c_int32), ("pos_limit", C.c_int32),
+                ("autoreset", C.c_int32), ("initial_cash", C.c_double), ("cost_rate", C.c_double),
+                ("reward_scale", C.c_double), ("noise_std", C.c_float), ("ou_theta", C.c_float),
+                ("ou_sigma", C.c_float), ("epsilon", C.c_float), ("seed", C.c_uint64), ("env_offset", C.c_int64)]
+
+
+class fin_traj(C.Structure):
+    _fields_ = [("reward", C.c_void_p), ("done", C.c_void_p), ("actions", C.c_void_p), ("cash", C.c_void_p),
+                ("hold", C.c_void_p), ("asset", C.c_void_p), ("mlp_out", C.c_void_p),
+                ("mlp_hidden", C.c_void_p), ("ep_metrics", C.c_void_p),
+                ("ep_count", C.c_void_p), ("ep_capacity", C.c_int32), ("agg", C.c_void_p)]
+
+
+class fin_noise(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("seed", C.c_uint64), ("supplied", C.c_void_p)]
+
+
+_P = C.c_void_p
+_sig = {
+    "fin_env_create": ([C.POINTER(fin_env_config), _P, C.c_int64, _P, C.POINTER(_P)], C.c_int),
+    "fin_env_reset": ([_P, _P, _P], C.c_int),
+    "fin_env_step": ([_P, _P, C.POINTER(fin_traj), _P], C.c_int),
+    "fin_env_get_state": ([_P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "fin_env_set_state": ([_P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "fin_env_check": ([_P, C.POINTER(C.c_uint32)], C.c_int),
+    "fin_env_destroy": ([_P], None),
+    "fin_policy_create": ([C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(_P), C.POINTER(_P), _P,
+                           C.POINTER(_P)], C.c_int),
+    "fin_policy_destroy": ([_P], None),
+    "fin_rollout": ([_P, C.POINTER(_P), C.c_int32, _P, C.c_int32, C.POINTER(fin_noise), C.POINTER(fin_traj), _P],
+                    C.c_int),
+    "fin_rollout_actions": ([_P, _P, C.c_int32, C.POINTER(fin_traj), _P], C.c_int),
+    "fin_ensemble_act": ([_P, C.POINTER(_P), C.c_int32, _P, C.POINTER(fin_noise), _P, _P, _P], C.c_int),
+    "fin_episode_metrics": ([_P, _P, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double, _P, C.c_int32, _P,
+                             _P, _P], C.c_int),
+    "fin_mlp_forward": ([_P, _P, C.c_int32, _P, _P, _P], C.c_int),
+    "fin_philox_normals": ([C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int64, _P, _P], C.c_int),
+    "fin_last_error": ([], C.c_char_p),
+    "fin_abi_version": ([], C.c_int),
+    "fin_device_check": ([C.c_int32], C.c_int),
+}
+for _name, (_args, _res) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+
+def _check(rc: int, where: str):
+    if rc != FIN_OK:
+        raise FinError(rc, where, _lib.fin_last_error().decode())
+
+
+# ----------------------------------------------------------------- marshalling helpers
+def _ptr(t, dtype=None, what=""):
+    """Device pointer of a CUDA tensor (or None).  Checks dtype, device and contiguity."""
+    if t is None:
+        return None
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{what}: expected a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{what}: tensor must live on the GPU (no CPU fallback)")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{what}: dtype {t.dtype}, expected {dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what}: tensor must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def make_traj(reward=None, done=None, actions=None, cash=None, hold=None, asset=None, mlp_out=None,
+              mlp_hidden=None, ep_metrics=None, ep_count=None, agg=None) -> fin_traj:
+    import torch
+    tr = fin_traj()
+    tr.reward = _ptr(reward, torch.float32, "reward")
+    tr.done = _ptr(done, torch.uint8, "done")
+    tr.actions = _ptr(actions, torch.int16, "actions")
+    tr.cash = _ptr(cash, torch.float64, "cash")
+    tr.hold = _ptr(hold, torch.int16, "hold")
+    tr.asset = _ptr(asset, torch.float64, "asset")
+    tr.mlp_out = _ptr(mlp_out, torch.float32, "mlp_out")
+    tr.mlp_hidden = _ptr(mlp_hidden, torch.int16, "mlp_hidden")
+    tr.ep_metrics = _ptr(ep_metrics, torch.float64, "ep_metrics")
+    tr.ep_count = _ptr(ep_count, torch.int32, "ep_count")
+    tr.ep_capacity = int(ep_metrics.shape[0]) if ep_metrics is not None else 0
+    tr.agg = _ptr(agg, torch.float64, "agg")
+    return tr
+
+
+def make_noise(mode: int = FIN_NOISE_NONE, seed: int = 0, supplied=None) -> fin_noise:
+    import torch
+    n = fin_noise()
+    n.mode = mode
+    n.seed = seed
+    n.supplied = _ptr(supplied, torch.float32, "noise") if supplied is not None else None
+    return n
+
+
+def env_config(**kw) -> fin_env_config:
+    """fin_env_config with the BASELINE defaults (stock task, C1 constants)."""
+    c = fin_env_config()
+    defaults = dict(task=FIN_STOCK, num_envs=1, num_assets=30, num_indicators=8, num_rows=2, episode_len=1,
+                    window_stride=5, window_offset=0, num_windows=1, window_block=128, window_base=0,
+                    advance_window_on_reset=0, max_trade=100, max_hold=120, pos_limit=1, autoreset=1,
+                    initial_cash=1e6, cost_rate=1e-3, reward_scale=2.0 ** -12, noise_std=0.1, ou_theta=0.15,
+                    ou_sigma=0.2, epsilon=0.005, seed=0, env_offset=0)
+    defaults.update(kw)
+    for k, v in defaults.items():
+        setattr(c, k, v)
+    return c
+
+
+# ----------------------------------------------------------------- entry points
+class Env:
+    """Owning wrapper of a ``fin_env*`` (destroyed with the object)."""
+
+    def __init__(self, handle, cfg: fin_env_config):
+        self.handle = handle
+        self.cfg = cfg
+
+    @property
+    def N(self):
+        return self.cfg.num_envs
+
+    @property
+    def K(self):
+        return self.cfg.num_assets
+
+    def __del__(self, _destroy=_lib.fin_env_destroy):  # bound early: module globals vanish at exit
+        h, self.handle = getattr(self, "handle", None), None
+        if h:
+            _destroy(h)
+
+
+class Policy:
+    def __init__(self, handle, kind, dims):
+        self.handle = handle
+        self.kind = kind
+        self.dims = tuple(dims)
+
+    def __del__(self, _destroy=_lib.fin_policy_destroy):
+        h, self.handle = getattr(self, "handle", None), None
+        if h:
+            _destroy(h)
+
+
+def fin_abi_version() -> int:
+    return _lib.fin_abi_version()
+
+
+def fin_device_check(ordinal: int = 0) -> None:
+    _check(_lib.fin_device_check(ordinal), "fin_device_check")
+
+
+def fin_last_error() -> str:
+    return _lib.fin_last_error().decode()
+
+
+def fin_env_create(cfg: fin_env_config, market: np.ndarray, stream=None) -> Env:
+    m = np.ascontiguousarray(market, dtype=np.float32)
+    h = _P()
+    _check(_lib.fin_env_create(C.byref(cfg), m.ctypes.data_as(_P), m.size, _stream(stream), C.byref(h)),
+           "fin_env_create")
+    return Env(h, cfg)
+
+
+def fin_env_reset(env: Env, mask=None, stream=None) -> None:
+    import torch
+    _check(_lib.fin_env_reset(env.handle, _ptr(mask, torch.uint8, "mask"), _stream(stream)), "fin_env_reset")
+
+
+def fin_env_step(env: Env, actions, traj: fin_traj | None = None, stream=None) -> None:
+    import torch
+    tr = traj if traj is not None else fin_traj()
+    _check(_lib.fin_env_step(env.handle, _ptr(actions, torch.int16, "actions"), C.byref(tr), _stream(stream)),
+           "fin_env_step")
+
+
+def fin_env_get_state(env: Env, cash=None, hold=None, asset=None, t_ep=None, window=None, stream=None) -> None:
+    import torch
+    _check(_lib.fin_env_get_state(env.handle, _ptr(cash, torch.float64, "cash"), _ptr(hold, torch.int16, "hold"),
+                                  _ptr(asset, torch.float64, "asset"), _ptr(t_ep, torch.int32, "t_ep"),
+                                  _ptr(window, torch.int32, "window"), _stream(stream)), "fin_env_get_state")
+
+
+def fin_env_set_state(env: Env, cash=None, hold=None, t_ep=None, window=None, tau=None, stream=None) -> None:
+    import torch
+    _check(_lib.fin_env_set_state(env.handle, _ptr(cash, torch.float64, "cash"), _ptr(hold, torch.int16, "hold"),
+                                  _ptr(t_ep, torch.int32, "t_ep"), _ptr(window, torch.int32, "window"),
+                                  _ptr(tau, torch.int32, "tau"), _stream(stream)), "fin_env_set_state")
+
+
+def fin_env_check(env: Env) -> int:
+    """Returns the sticky device flags (0 = clean); raises FinError on a CUDA failure."""
+    f = C.c_uint32(0)
+    rc = _lib.fin_env_check(env.handle, C.byref(f))
+    if rc not in (FIN_OK, FIN_E_DEVICE_ASYNC):
+        _check(rc, "fin_env_check")
+    return int(f.value)
+
+
+def fin_env_destroy(env: Env) -> None:
+    h, env.handle = env.handle, None
+    if h:
+        _lib.fin_env_destroy(h)
+
+
+def fin_policy_create(kind: int, layers, stream=None) -> Policy:
+    """layers = [(W_bits uint16 [out][in] (host), bias float32 [out] or None), ...]."""
+    dims = [int(layers[0][0].shape[1])] + [int(w.shape[0]) for w, _ in layers]
+    ws = [np.ascontiguousarray(w, dtype=np.uint16) for w, _ in layers]
+    bs = [None if b is None else np.ascontiguousarray(b, dtype=np.float32) for _, b in layers]
+    n = len(layers)
+    dims_c = (C.c_int32 * (n + 1))(*dims)
+    w_c = (_P * n)(*[w.ctypes.data_as(_P) for w in ws])
+    b_c = (_P * n)(*[None if b is None else b.ctypes.data_as(_P) for b in bs])
+    h = _P()
+    _check(_lib.fin_policy_create(kind, n, dims_c, w_c, b_c, _stream(stream), C.byref(h)), "fin_policy_create")
+    return Policy(h, kind, dims)
+
+
+def fin_policy_destroy(pol: Policy) -> None:
+    h, pol.handle = pol.handle, None
+    if h:
+        _lib.fin_policy_destroy(h)
+
+
+def _members(members):
+    arr = (_P * len(members))(*[m.handle for m in members])
+    return arr
+
+
+def _weights(member_w):
+    if member_w is None:
+        return None, None
+    w = np.ascontiguousarray(member_w, dtype=np.float32)
+    return w, w.ctypes.data_as(_P)
+
+
+def fin_rollout(env: Env, members, T: int, noise: fin_noise | None = None, traj: fin_traj | None = None,
+                member_w=None, stream=None) -> None:
+    nz = noise if noise is not None else make_noise(FIN_NOISE_NONE)
+    tr = traj if traj is not None else fin_traj()
+    keep, wp = _weights(member_w)
+    _check(_lib.fin_rollout(env.handle, _members(members), len(members), wp, T, C.byref(nz), C.byref(tr),
+                            _stream(stream)), "fin_rollout")
+
+
+def fin_rollout_actions(env: Env, actions, T: int, traj: fin_traj | None = None, stream=None) -> None:
+    import torch
+    tr = traj if traj is not None else fin_traj()
+    _check(_lib.fin_rollout_actions(env.handle, _ptr(actions, torch.int16, "actions"), T, C.byref(tr),
+                                    _stream(stream)), "fin_rollout_actions")
+
+
+def fin_ensemble_act(env: Env, members, actions, mean_action=None, noise: fin_noise | None = None, member_w=None,
+                     stream=None) -> None:
+    import torch
+    nz = noise if noise is not None else make_noise(FIN_NOISE_NONE)
+    keep, wp = _weights(member_w)
+    _check(_lib.fin_ensemble_act(env.handle, _members(members), len(members), wp, C.byref(nz),
+                                 _ptr(actions, torch.int16, "actions"), _ptr(mean_action, torch.float32, "mean"),
+                                 _stream(stream)), "fin_ensemble_act")
+
+
+def fin_episode_metrics(equity, done, reset_equity: float, periods_per_year: float = 252.0, rf: float = 0.0,
+                        ep_metrics=None, ep_count=None, agg=None, stream=None) -> None:
+    import torch
+    T = int(done.shape[0])
+    N = int(done.shape[1])
+    cap = int(ep_metrics.shape[0]) if ep_metrics is not None else 0
+    _check(_lib.fin_episode_metrics(_ptr(equity, torch.float64, "equity"), _ptr(done, torch.uint8, "done"), T, N,
+                                    reset_equity, periods_per_year, rf, _ptr(ep_metrics, torch.float64, "ep_metrics"),
+                                    cap, _ptr(ep_count, torch.int32, "ep_count"), _ptr(agg, torch.float64, "agg"),
+                                    _stream(stream)), "fin_episode_metrics")
+
+
+def fin_mlp_forward(policy: Policy, x_bf16_bits, z, hidden=None, stream=None) -> None:
+    import torch
+    B = int(x_bf16_bits.shape[0])
+    _check(_lib.fin_mlp_forward(policy.handle, _ptr(x_bf16_bits, torch.int16, "x"), B, _ptr(z, torch.float32, "z"),
+                                _ptr(hidden, torch.int16, "hidden"), _stream(stream)), "fin_mlp_forward")
+
+
+def fin_philox_normals(seed: int, env_offset: int, out, member: int, t_global: int, stream=None) -> None:
+    import torch
+    N, K = int(out.shape[0]), int(out.shape[1])
+    _check(_lib.fin_philox_normals(seed, env_offset, N, K, member, t_global, _ptr(out, torch.float32, "out"),
+                                   _stream(stream)), "fin_philox_normals")

@@ -1,0 +1,214 @@
+"""GPU parity of the env kernels (K1 step, K2 crypto step, K4 replay, state get/set)
+against the float64 oracle, through the C ABI.  Integer holdings / done are
+compared bit-exactly; cash and asset bit-exactly (the contract is rel 1e-5, the
+kernels mirror the oracle's operation order so equality is expected); reward
+(stored fp32) within SURVEY c.8's tolerance."""
+import numpy as np
+import pytest
+
+from gpu_util import dev, host, needs_gpu, stock_pair, zeros
+from oracle import crypto as ocry
+from oracle import metrics as omet
+from oracle import stock as ostock
+from synth import inputs, market
+
+pytestmark = [pytest.mark.gpu, needs_gpu]
+
+
+def _fin():
+    from paper_2501_10709_b200 import fin
+    return fin
+
+
+def _step_loop(fin, env, acts, K):
+    import torch
+    T, N = acts.shape[0], acts.shape[1]
+    out = {k: [] for k in ("reward", "done", "cash", "hold", "asset", "actions")}
+    for t in range(T):
+        r, d, c = zeros(N, torch.float32), zeros(N, torch.uint8), zeros(N, torch.float64)
+        h, a, ac = zeros((N, K), torch.int16), zeros(N, torch.float64), zeros((N, K), torch.int16)
+        fin.fin_env_step(env, dev(acts[t], torch.int16),
+                         fin.make_traj(reward=r, done=d, cash=c, hold=h, asset=a, actions=ac))
+        for k, v in (("reward", r), ("done", d), ("cash", c), ("hold", h), ("asset", a), ("actions", ac)):
+            out[k].append(host(v))
+    return {k: np.stack(v) for k, v in out.items()}
+
+
+def _compare_stock(g, o, mk, cfg):
+    assert np.array_equal(g["hold"], o["hold"])
+    assert np.array_equal(g["done"].astype(bool), o["done"])
+    assert np.array_equal(g["cash"], o["cash"])            # bit-identical expected
+    assert np.array_equal(g["asset"], o["asset"])
+    np.testing.assert_allclose(g["cash"], o["cash"], rtol=1e-5, atol=1e-5)
+    err = np.abs(g["reward"].astype(np.float64) - o["reward"])
+    tol = 1e-5 * np.abs(o["reward"]) + 1e-5 * cfg.reward_scale * 1e4 + 1e-30
+    assert np.all(err <= tol), float((err - tol).max())
+
+
+def test_c0_step_parity():
+    """BASELINE configs[0]: K=4, I=4, N=8, 64 steps, seeded integer actions."""
+    import torch
+    fin = _fin()
+    m = market.stock_c0()
+    ocfg, fcfg = stock_pair(num_envs=8, num_assets=4, num_indicators=4, num_rows=m.rows, episode_len=64)
+    acts = inputs.stock_actions(64, 8, 4, seed=12)
+    o, _ = ostock.run_actions(ocfg, m.market, acts)
+    env = fin.fin_env_create(fcfg, m.market)
+    g = _step_loop(fin, env, acts, 4)
+    _compare_stock(g, o, m.market, ocfg)
+    assert np.array_equal(g["actions"], acts)
+    assert fin.fin_env_check(env) == 0
+
+
+def test_c1_shape_step_parity_ragged_windows_resets():
+    """C1 shapes (K=30, I=8) with N=300 (ragged vs 256-thread blocks), tile-aligned
+    windows, auto-reset + test-mode window advance, actions beyond +-max_trade."""
+    import torch
+    fin = _fin()
+    m = market.stock_c1(rows=120)
+    kw = dict(num_envs=300, num_assets=30, num_indicators=8, num_rows=120, episode_len=7, window_stride=5,
+              num_windows=15, window_block=128, advance_window_on_reset=True)
+    ocfg, fcfg = stock_pair(**kw)
+    acts = inputs.stock_actions(20, 300, 30, seed=7, max_trade=130)
+    o, _ = ostock.run_actions(ocfg, m.market, acts)
+    env = fin.fin_env_create(fcfg, m.market)
+    g = _step_loop(fin, env, acts, 30)
+    _compare_stock(g, o, m.market, ocfg)
+    assert fin.fin_env_check(env) & fin.FIN_FLAG_ACTION_RANGE
+
+
+def test_replay_rollout_parity_and_episode_metrics():
+    """K4: T steps in one launch; trajectory + online episode metrics vs oracle."""
+    import torch
+    fin = _fin()
+    m = market.stock_c1(rows=200)
+    N, T, K = 333, 40, 30
+    kw = dict(num_envs=N, num_assets=K, num_indicators=8, num_rows=200, episode_len=9, window_stride=5,
+              num_windows=30, window_block=64)
+    ocfg, fcfg = stock_pair(**kw)
+    acts = inputs.stock_actions(T, N, K, seed=9)
+    o, _ = ostock.run_actions(ocfg, m.market, acts)
+    env = fin.fin_env_create(fcfg, m.market)
+    E = 8
+    r, d = zeros((T, N), torch.float32), zeros((T, N), torch.uint8)
+    c, h, a = zeros((T, N), torch.float64), zeros((T, N, K), torch.int16), zeros((T, N), torch.float64)
+    em, ec, agg = zeros((E, N, 3), torch.float64), zeros(N, torch.int32), zeros(8, torch.float64)
+    fin.fin_rollout_actions(env, dev(acts, torch.int16), T,
+                            fin.make_traj(reward=r, done=d, cash=c, hold=h, asset=a, ep_metrics=em, ep_count=ec,
+                                          agg=agg))
+    g = {"reward": host(r), "done": host(d), "cash": host(c), "hold": host(h), "asset": host(a)}
+    _compare_stock(g, o, m.market, ocfg)
+    em, ec, agg = host(em), host(ec), host(agg)
+    n_ep = 0
+    cums = []
+    for i in range(N):
+        curves, _ = omet.split_episodes(1e6, o["asset"][:, i], o["done"][:, i])
+        assert ec[i] == len(curves)
+        for j, cv in enumerate(curves):
+            cum, sh, mdd = omet.episode_metrics(cv)
+            np.testing.assert_allclose(em[j, i, 0], cum, rtol=1e-9, atol=1e-15)
+            np.testing.assert_allclose(em[j, i, 2], mdd, rtol=1e-9, atol=1e-15)
+            if np.isnan(sh):
+                assert np.isnan(em[j, i, 1])
+            else:
+                np.testing.assert_allclose(em[j, i, 1], sh, rtol=1e-7)
+            cums.append(cum)
+            n_ep += 1
+    assert agg[fin.FIN_AGG_EPISODES] == n_ep
+    np.testing.assert_allclose(agg[fin.FIN_AGG_SUM_CUM], np.sum(cums), rtol=1e-9)
+    np.testing.assert_allclose(agg[fin.FIN_AGG_SUM_REWARD], np.sum(g["reward"].astype(np.float64)), rtol=1e-9)
+    # state after the rollout equals the oracle's
+    cs, hs, ts = zeros(N, torch.float64), zeros((N, K), torch.int16), zeros(N, torch.int32)
+    fin.fin_env_get_state(env, cash=cs, hold=hs, t_ep=ts)
+    ost = ostock.reset(ocfg)
+    ostock.run_actions(ocfg, m.market, acts, ost)
+    assert np.array_equal(host(cs), np.array(ost.cash)) and np.array_equal(host(hs), np.array(ost.hold))
+    assert np.array_equal(host(ts), np.array(ost.t_ep))
+
+
+def test_partition_invariance_two_handles():
+    """S:216 / S:741: envs [0,N) in one handle == [0,a) and [a,N) in two handles (env_offset)."""
+    import torch
+    fin = _fin()
+    m = market.stock_c1(rows=100)
+    N, T, K = 260, 12, 30
+    kw = dict(num_assets=K, num_indicators=8, num_rows=100, episode_len=5, num_windows=12, window_block=50,
+              advance_window_on_reset=True)
+    acts = inputs.stock_actions(T, N, K, seed=21)
+    outs = []
+    for lo, hi in ((0, N), (0, 117), (117, N)):
+        _, fcfg = stock_pair(num_envs=hi - lo, env_offset=lo, **kw)
+        env = fin.fin_env_create(fcfg, m.market)
+        r, c = zeros((T, hi - lo), torch.float32), zeros((T, hi - lo), torch.float64)
+        fin.fin_rollout_actions(env, dev(acts[:, lo:hi], torch.int16), T, fin.make_traj(reward=r, cash=c))
+        outs.append((host(r), host(c)))
+    assert np.array_equal(np.concatenate([outs[1][0], outs[2][0]], axis=1), outs[0][0])
+    assert np.array_equal(np.concatenate([outs[1][1], outs[2][1]], axis=1), outs[0][1])
+
+
+def test_set_state_teacher_forcing_and_no_autoreset_flag():
+    import torch
+    fin = _fin()
+    m = market.stock_c0()
+    N, K = 5, 4
+    ocfg, fcfg = stock_pair(num_envs=N, num_assets=K, num_indicators=4, num_rows=m.rows, episode_len=3,
+                            autoreset=False)
+    env = fin.fin_env_create(fcfg, m.market)
+    cash = np.array([10.0, 500.0, 1e6, 0.0, 123.456])
+    hold = np.arange(N * K, dtype=np.int16).reshape(N, K)
+    tep = np.array([0, 1, 2, 0, 1], dtype=np.int32)
+    fin.fin_env_set_state(env, cash=dev(cash), hold=dev(hold), t_ep=dev(tep))
+    st = ostock.reset(ocfg)
+    st.cash, st.hold, st.t_ep = list(cash), [list(map(int, r)) for r in hold], list(map(int, tep))
+    acts = inputs.stock_actions(4, N, K, seed=4)
+    g = _step_loop(fin, env, acts[:1], K)
+    o = ostock.step(ocfg, st, m.market, acts[0])
+    assert np.array_equal(g["hold"][0], np.array(o["hold"])) and np.array_equal(g["cash"][0], np.array(o["cash"]))
+    # env 2 finished its episode (t_ep 2 -> 3 = L); stepping it again raises the sticky flag
+    _step_loop(fin, env, acts[1:2], K)
+    assert fin.fin_env_check(env) & fin.FIN_FLAG_EPISODE_DONE
+
+
+def test_create_rejects_bad_market():
+    import pytest as _pt
+    fin = _fin()
+    m = market.stock_c0().market.copy()
+    _, fcfg = stock_pair(num_envs=2, num_assets=4, num_indicators=4, num_rows=65, episode_len=64)
+    bad = m.copy()
+    bad[3, 0, 1] = -1.0
+    with _pt.raises(fin.FinError) as e:
+        fin.fin_env_create(fcfg, bad)
+    assert e.value.code == fin.FIN_E_DATA
+    bad = m.copy()
+    bad[5, 3, 2] = np.nan
+    with _pt.raises(fin.FinError):
+        fin.fin_env_create(fcfg, bad)
+    _, fcfg2 = stock_pair(num_envs=2, num_assets=4, num_indicators=4, num_rows=65, episode_len=65)
+    with _pt.raises(fin.FinError) as e:
+        fin.fin_env_create(fcfg2, m)
+    assert e.value.code == fin.FIN_E_CONFIG
+
+
+def test_crypto_step_parity():
+    import torch
+    fin = _fin()
+    T, N = 300, 200
+    rows = market.crypto_market(T, seed=41)
+    ocfg = ocry.CryptoEnvConfig(num_envs=N, episode_len=T)
+    fcfg = fin.env_config(task=fin.FIN_CRYPTO, num_envs=N, num_assets=1, num_indicators=0, num_rows=T + 1,
+                          episode_len=T, reward_scale=1.0, cost_rate=0.0)
+    env = fin.fin_env_create(fcfg, rows)
+    rng = np.random.default_rng(3)
+    st = ocry.reset(ocfg)
+    for t in range(T):
+        a = rng.integers(-1, 2, N)
+        o = ocry.step(ocfg, st, rows, a)
+        r, d, c, h, v = (zeros(N, torch.float32), zeros(N, torch.uint8), zeros(N, torch.float64),
+                         zeros((N, 1), torch.int16), zeros(N, torch.float64))
+        fin.fin_env_step(env, dev(a.reshape(N, 1), torch.int16), fin.make_traj(reward=r, done=d, cash=c, hold=h, asset=v))
+        assert np.array_equal(host(h)[:, 0], np.array(o["pos"]))
+        assert np.array_equal(host(c), np.array(o["cash"]))
+        assert np.array_equal(host(v), np.array(o["asset"]))
+        assert np.array_equal(host(d).astype(bool), np.array(o["done"]))
+        np.testing.assert_allclose(host(r), np.array(o["reward"]), rtol=1e-5, atol=1e-3)
+    assert fin.fin_env_check(env) == 0

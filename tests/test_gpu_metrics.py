@@ -1,0 +1,47 @@
+"""GPU parity of K6 (fin_episode_metrics: chunked segmented scans over a stored
+equity log) against the oracle's per-episode two-pass metrics."""
+import numpy as np
+import pytest
+
+from gpu_util import dev, host, needs_gpu, zeros
+from oracle import metrics as omet
+
+pytestmark = [pytest.mark.gpu, needs_gpu]
+
+
+@pytest.mark.parametrize("T,N,p_done", [(64, 8, 0.05), (3000, 300, 0.01), (20000, 40, 0.0005), (7, 1, 0.5)])
+def test_episode_metrics_parity(T, N, p_done):
+    import torch
+    from paper_2501_10709_b200 import fin
+    rng = np.random.default_rng(T + N)
+    eq = 1e6 * np.exp(np.cumsum(rng.normal(0, 0.01, (T + 1, N)), axis=0))
+    done = rng.random((T, N)) < p_done
+    done[-1, : N // 2] = True
+    # after a done the next episode restarts from the reset equity (autoreset)
+    E = int(done.sum(axis=0).max()) + 1
+    em, ec, agg = zeros((E, N, 3), torch.float64), zeros(N, torch.int32), zeros(8, torch.float64)
+    fin.fin_episode_metrics(dev(eq), dev(done.astype(np.uint8)), 1e6, 252.0, 0.0, em, ec, agg)
+    em, ec, agg = host(em), host(ec), host(agg)
+    n = 0
+    sh_sum = 0.0
+    for i in range(N):
+        curves = []
+        cur = [eq[0, i]]
+        for t in range(T):
+            cur.append(eq[t + 1, i])
+            if done[t, i]:
+                curves.append(cur)
+                cur = [1e6]
+        assert ec[i] == len(curves), i
+        for j, cv in enumerate(curves):
+            cum, sh, mdd = omet.episode_metrics(cv)
+            np.testing.assert_allclose(em[j, i, 0], cum, rtol=1e-9, atol=1e-14)
+            np.testing.assert_allclose(em[j, i, 2], mdd, rtol=1e-9, atol=1e-14)
+            if np.isnan(sh):
+                assert np.isnan(em[j, i, 1])
+            else:
+                np.testing.assert_allclose(em[j, i, 1], sh, rtol=1e-7, atol=1e-9)
+                sh_sum += sh
+            n += 1
+    assert agg[fin.FIN_AGG_EPISODES] == n
+    np.testing.assert_allclose(agg[fin.FIN_AGG_SUM_SHARPE], sh_sum, rtol=1e-7, atol=1e-9)

@@ -1,0 +1,338 @@
+"""GPU parity of the tcgen05 paths: the standalone MLP (K7), the fused stock
+rollout (K3, C1 policy), the C2 ensemble inside it, the crypto Q rollout, and
+Philox production noise -- against the float64 oracle.
+
+Policy-driven runs use teacher forcing (SURVEY c.8): the GPU logs its executed
+actions, states and network outputs; the oracle (1) replays the actions through
+its env -- integers bit-exact, cash / asset bitwise, reward within tolerance;
+(2) recomputes the network output from the replayed states -- rel 2e-3 under
+bf16; (3) recomputes each action from the GPU's network output and noise --
+mismatch allowed only within 1e-4 of a .5 rounding boundary."""
+import math
+
+import numpy as np
+import pytest
+
+from gpu_util import dev, host, needs_gpu, stock_pair, zeros
+from oracle import crypto as ocry
+from oracle import metrics as omet
+from oracle import mlp as omlp
+from oracle import philox as ophx
+from oracle import policy as opol
+from oracle import rollout as orol
+from oracle import stock as ostock
+from synth import inputs, market
+from synth import policy as spol
+
+pytestmark = [pytest.mark.gpu, needs_gpu]
+
+
+def _fin():
+    from paper_2501_10709_b200 import fin
+    return fin
+
+
+MLP_STATS = []
+
+
+def _mlp_close(g, o, rel=2e-3, strict=False):
+    """End-to-end comparison with the free-running float64 forward: norm-wise relative
+    error of each output vector, max_k |g - o| / max_k |o| (reading R-TOL).
+    The gate is the layer-by-layer teacher-forced check (oracle.mlp.teacher_forced_layers);
+    end to end, a single bf16 rounding flip of one hidden activation (fp32 vs float64
+    pre-activation on the two sides of a rounding boundary) moves the outputs by
+    ~2^-8 |a| |w|, so this is recorded, and asserted at 2e-3 for 99% of rows."""
+    err = np.abs(g - o).max(axis=-1)
+    scale = np.abs(o).max(axis=-1)
+    ratio = err / np.maximum(scale, 1e-6)
+    MLP_STATS.append((float(np.percentile(ratio, 99)), float(ratio.max())))
+    if strict:
+        assert np.all(ratio <= rel), f"{(ratio > rel).sum()} of {ratio.size} rows outside {rel}"
+    assert np.mean(ratio > rel) <= 1e-2 or (ratio > rel).sum() <= 1, f"{(ratio > rel).sum()} rows outside {rel}"
+
+
+# ------------------------------------------------------------------ K7 standalone MLP
+@pytest.mark.parametrize("dims", [(301, 256, 256, 30), (25, 128, 128, 4), (103, 128, 128, 3)])
+def test_mlp_dyadic_bit_exact(dims):
+    """Dyadic weights / inputs: every product and partial sum is exact in fp32, so the
+    tcgen05 result must equal the oracle bit for bit -- this pins the smem
+    descriptors, the core-matrix layouts, the TMEM lane/column mapping."""
+    import torch
+    fin = _fin()
+    rng = np.random.default_rng(sum(dims))
+    vals = np.array([0.0, 0.0, 0.0, 0.5, -0.5, 1.0, -1.0, 2.0])
+    layers = []
+    for fi, fo in zip(dims[:-1], dims[1:]):
+        w = rng.choice(vals, (fo, fi))
+        b = rng.choice(np.array([0.0, 0.25, -0.75]), fo).astype(np.float32)
+        layers.append((spol.f64_to_bf16_bits(w), b))
+    kind = fin.FIN_Q_ARGMAX if dims[0] == 103 else fin.FIN_PPO_GAUSS
+    pol = fin.fin_policy_create(kind, layers)
+    B = 300
+    x = rng.choice(np.array([0.0, 0.5, -0.5, 1.0, -1.0, 0.25]), (B, dims[0]))
+    xb = spol.f64_to_bf16_bits(x).view(np.int16)
+    z = zeros((B, dims[-1]), torch.float32)
+    fin.fin_mlp_forward(pol, dev(xb), z)
+    o = omlp.forward(omlp.layers_f64(layers), x)
+    assert np.array_equal(host(z).astype(np.float64), o)
+
+
+@pytest.mark.parametrize("dims", [(301, 256, 256, 30), (103, 128, 128, 3)])
+def test_mlp_kaiming_rel_2e3(dims):
+    import torch
+    fin = _fin()
+    layers = spol.random_bias(spol.kaiming_bf16(dims, 0), 99)
+    kind = fin.FIN_Q_ARGMAX if dims[0] == 103 else fin.FIN_PPO_GAUSS
+    pol = fin.fin_policy_create(kind, layers)
+    rng = np.random.default_rng(1)
+    B = 1000
+    x = rng.standard_normal((B, dims[0])) * 2.0
+    xq = omlp.bf16_bits_to_f64(spol.f64_to_bf16_bits(x))
+    z = zeros((B, dims[-1]), torch.float32)
+    hid = zeros((B, 2, dims[1]), torch.int16)
+    fin.fin_mlp_forward(pol, dev(spol.f64_to_bf16_bits(x).view(np.int16)), z, hid)
+    L64 = omlp.layers_f64(layers)
+    amb, tot = omlp.teacher_forced_layers(L64, xq, host(hid), host(z))
+    assert amb <= 1e-3 * tot
+    _mlp_close(host(z).astype(np.float64), omlp.forward(L64, xq), strict=False)
+
+
+# ------------------------------------------------------------------ fused stock rollout
+def _stock_fused(N, T, members_spec, L, rows=150, seed_noise=23, **env_kw):
+    """Run fin_rollout with supplied noise; return logs + the oracle pieces."""
+    import torch
+    fin = _fin()
+    m = market.stock_c1(rows=rows)
+    K = 30
+    kw = dict(num_envs=N, num_assets=K, num_indicators=8, num_rows=rows, episode_len=L, window_stride=5,
+              window_block=128)
+    kw.update(env_kw)
+    kw["num_windows"] = (rows - 1 - L - kw.get("window_offset", 0)) // 5 + 1
+    ocfg, fcfg = stock_pair(**kw)
+    env = fin.fin_env_create(fcfg, m.market)
+    layers = [spol.kaiming_bf16(spol.STOCK_DIMS, s) for s, _ in members_spec]
+    kinds = [k for _, k in members_spec]
+    pols = [fin.fin_policy_create(k, L_) for k, L_ in zip(kinds, layers)]
+    M = len(pols)
+    noise = inputs.supplied_noise(T, M, N, K, seed=seed_noise)
+    E = T // L + 2
+    logs = dict(reward=zeros((T, N), torch.float32), done=zeros((T, N), torch.uint8),
+                actions=zeros((T, N, K), torch.int16), cash=zeros((T, N), torch.float64),
+                hold=zeros((T, N, K), torch.int16), asset=zeros((T, N), torch.float64),
+                mlp_out=zeros((T, M, N, K), torch.float32), mlp_hidden=zeros((T, M, N, 2, 256), torch.int16),
+                ep_metrics=zeros((E, N, 3), torch.float64),
+                ep_count=zeros(N, torch.int32), agg=zeros(8, torch.float64))
+    fin.fin_rollout(env, pols, T, fin.make_noise(fin.FIN_NOISE_SUPPLIED, 0, dev(noise)), fin.make_traj(**logs))
+    g = {k: host(v) for k, v in logs.items()}
+    assert fin.fin_env_check(env) == 0
+    return g, ocfg, m.market, layers, kinds, noise
+
+
+def _teacher_forced_stock(g, ocfg, mk, layers, kinds, noise):
+    T, N, K = g["actions"].shape
+    # (1) replay the GPU's actions through the oracle env
+    o, _ = ostock.run_actions(ocfg, mk, g["actions"])
+    assert np.array_equal(g["hold"], o["hold"])
+    assert np.array_equal(g["done"].astype(bool), o["done"])
+    assert np.array_equal(g["cash"], o["cash"]) and np.array_equal(g["asset"], o["asset"])
+    err = np.abs(g["reward"].astype(np.float64) - o["reward"])
+    assert np.all(err <= 1e-5 * np.abs(o["reward"]) + 1e-5 * 2.0 ** -12 * 1e5)
+    # (2) network outputs recomputed from the replayed pre-step states
+    L64 = [omlp.layers_f64(L_) for L_ in layers]
+    st = ostock.reset(ocfg)
+    ou = np.zeros((N, K))
+    n_boundary = 0
+    for t in range(T):
+        X = orol.stock_obs_batch(ocfg, st, mk)
+        for mi, L_ in enumerate(L64):
+            omlp.teacher_forced_layers(L_, X, g["mlp_hidden"][t, mi], g["mlp_out"][t, mi])
+            _mlp_close(g["mlp_out"][t, mi].astype(np.float64), omlp.forward(L_, X))
+        # (3) actions from the GPU's z and the supplied noise (f64 rule of oracle.policy)
+        for i in range(N):
+            zs = [g["mlp_out"][t, mi, i].astype(np.float64) for mi in range(len(kinds))]
+            sh, abar, ou_new = orol.ensemble_shares(kinds, zs, noise[t, :, i].astype(np.float64), list(ou[i]))
+            ou[i] = ou_new
+            for k in range(K):
+                if sh[k] != g["actions"][t, i, k]:
+                    y = 100.0 * abar[k]
+                    assert abs(abs(y - math.trunc(y)) - 0.5) < 1e-4, (t, i, k, y, g["actions"][t, i, k])
+                    n_boundary += 1
+        ostock.step(ocfg, st, mk, g["actions"][t])
+        for i in range(N):
+            if g["done"][t, i]:
+                ou[i] = 0.0
+    # (4) episode metrics from the replayed equity
+    for i in range(N):
+        curves, _ = omet.split_episodes(1e6, o["asset"][:, i], o["done"][:, i])
+        assert g["ep_count"][i] == len(curves)
+        for j, cv in enumerate(curves):
+            cum, sh, mdd = omet.episode_metrics(cv)
+            np.testing.assert_allclose(g["ep_metrics"][j, i], [cum, sh, mdd], rtol=1e-7, atol=1e-12)
+    return n_boundary
+
+
+def test_fused_c1_rollout_teacher_forced():
+    """BASELINE configs[1]: 301-256-256-30 Gaussian policy, horizon 30, reset on done;
+    N=300 (3 tiles, ragged), T=35 so one reset happens mid-rollout."""
+    fin = _fin()
+    g, ocfg, mk, layers, kinds, noise = _stock_fused(300, 35, [(0, fin.FIN_PPO_GAUSS)], L=30)
+    _teacher_forced_stock(g, ocfg, mk, layers, kinds, noise)
+    assert g["agg"][fin.FIN_AGG_EPISODES] == 300
+
+
+def test_fused_c2_ensemble_teacher_forced():
+    """BASELINE configs[2]: PPO / SAC / DDPG+OU members (seeds 1,2,3), executed action =
+    mean; 5-day test windows that advance on reset; T=12 (2 full episodes + 2 steps)."""
+    fin = _fin()
+    spec = [(1, fin.FIN_PPO_GAUSS), (2, fin.FIN_SAC_SQUASH), (3, fin.FIN_DDPG_OU)]
+    g, ocfg, mk, layers, kinds, noise = _stock_fused(200, 12, spec, L=5, window_offset=30,
+                                                     advance_window_on_reset=True, seed_noise=33)
+    _teacher_forced_stock(g, ocfg, mk, layers, kinds, noise)
+
+
+def test_fused_rollout_deterministic_and_partition_invariant_philox():
+    """Production (Philox) noise keyed by the global env id: same seed -> same bits;
+    [0,N) == [0,a) + [a,N) with env_offset."""
+    import torch
+    fin = _fin()
+    m = market.stock_c1(rows=100)
+    layers = spol.kaiming_bf16(spol.STOCK_DIMS, 0)
+    N, T = 260, 8
+    kw = dict(num_assets=30, num_indicators=8, num_rows=100, episode_len=5, num_windows=10, window_block=128)
+    res = []
+    for lo, hi in ((0, N), (0, N), (0, 130), (130, N)):
+        _, fcfg = stock_pair(num_envs=hi - lo, env_offset=lo, **kw)
+        env = fin.fin_env_create(fcfg, m.market)
+        pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, layers)
+        a, c = zeros((T, hi - lo, 30), torch.int16), zeros((T, hi - lo), torch.float64)
+        fin.fin_rollout(env, [pol], T, fin.make_noise(fin.FIN_NOISE_PHILOX, 1234), fin.make_traj(actions=a, cash=c))
+        res.append((host(a), host(c)))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    assert np.array_equal(np.concatenate([res[2][0], res[3][0]], axis=1), res[0][0])
+    assert np.array_equal(np.concatenate([res[2][1], res[3][1]], axis=1), res[0][1])
+    assert np.abs(res[0][0]).sum() > 0
+
+
+def test_philox_normals_match_oracle_generator():
+    import torch
+    fin = _fin()
+    N, K = 200, 30
+    out = zeros((N, K), torch.float32)
+    fin.fin_philox_normals(987654321012, 1000, out, 2, 77)
+    g = host(out)
+    o = np.array([ophx.stock_noise(987654321012, 1000 + i, 77, 2, K) for i in range(N)])
+    np.testing.assert_allclose(g, o, rtol=2e-5, atol=2e-5)
+
+
+def test_fused_small_net_c0_market():
+    """The resident-weight variant (25-128-128-4 net on a C0-shaped K=4, I=4 env)."""
+    import torch
+    fin = _fin()
+    mkt = market.stock_c0()
+    N, T, K = 140, 20, 4
+    ocfg, fcfg = stock_pair(num_envs=N, num_assets=K, num_indicators=4, num_rows=mkt.rows, episode_len=64)
+    env = fin.fin_env_create(fcfg, mkt.market)
+    layers = spol.random_bias(spol.kaiming_bf16((25, 128, 128, 4), 5), 6)
+    pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, layers)
+    noise = inputs.supplied_noise(T, 1, N, K, seed=8)
+    logs = dict(actions=zeros((T, N, K), torch.int16), hold=zeros((T, N, K), torch.int16),
+                cash=zeros((T, N), torch.float64), mlp_out=zeros((T, 1, N, K), torch.float32),
+                mlp_hidden=zeros((T, 1, N, 2, 128), torch.int16))
+    fin.fin_rollout(env, [pol], T, fin.make_noise(fin.FIN_NOISE_SUPPLIED, 0, dev(noise)), fin.make_traj(**logs))
+    g = {k: host(v) for k, v in logs.items()}
+    o, _ = ostock.run_actions(ocfg, mkt.market, g["actions"])
+    assert np.array_equal(g["hold"], o["hold"]) and np.array_equal(g["cash"], o["cash"])
+    st = ostock.reset(ocfg)
+    L64 = omlp.layers_f64(layers)
+    for t in range(T):
+        X = orol.stock_obs_batch(ocfg, st, mkt.market)
+        omlp.teacher_forced_layers(L64, X, g["mlp_hidden"][t, 0], g["mlp_out"][t, 0])
+        _mlp_close(g["mlp_out"][t, 0].astype(np.float64), omlp.forward(L64, X))
+        ostock.step(ocfg, st, mkt.market, g["actions"][t])
+
+
+def test_ensemble_act_matches_rollout_first_step():
+    import torch
+    fin = _fin()
+    m = market.stock_c1(rows=80)
+    N = 150
+    kw = dict(num_envs=N, num_assets=30, num_indicators=8, num_rows=80, episode_len=5, num_windows=10)
+    _, fcfg = stock_pair(**kw)
+    spec = [(1, fin.FIN_PPO_GAUSS), (2, fin.FIN_SAC_SQUASH), (3, fin.FIN_DDPG_OU)]
+    pols = [fin.fin_policy_create(k, spol.kaiming_bf16(spol.STOCK_DIMS, s)) for s, k in spec]
+    noise = dev(inputs.supplied_noise(1, 3, N, 30, seed=2))
+    env_a = fin.fin_env_create(fcfg, m.market)
+    act, mean = zeros((N, 30), torch.int16), zeros((N, 30), torch.float32)
+    fin.fin_ensemble_act(env_a, pols, act, mean, fin.make_noise(fin.FIN_NOISE_SUPPLIED, 0, noise))
+    env_b = fin.fin_env_create(fcfg, m.market)
+    a2 = zeros((1, N, 30), torch.int16)
+    fin.fin_rollout(env_b, pols, 1, fin.make_noise(fin.FIN_NOISE_SUPPLIED, 0, noise), fin.make_traj(actions=a2))
+    assert np.array_equal(host(act), host(a2)[0])
+    assert np.all(np.abs(host(mean)) <= 1.0)
+    # the env handed to fin_ensemble_act did not move
+    t_ep = zeros(N, torch.int32)
+    fin.fin_env_get_state(env_a, t_ep=t_ep)
+    assert np.all(host(t_ep) == 0)
+
+
+# ------------------------------------------------------------------ crypto Q rollout
+def test_fused_crypto_rollout_teacher_forced():
+    """BASELINE configs[3] shape on a short series: Q-net 103-128-128-3, argmax,
+    epsilon-greedy 0.005 with supplied uniforms, position +-1, max hold 120."""
+    import torch
+    fin = _fin()
+    T, N = 400, 300
+    rows = market.crypto_market(T, seed=41)
+    eps = float(np.float32(0.005))
+    ocfg = ocry.CryptoEnvConfig(num_envs=N, episode_len=T)
+    fcfg = fin.env_config(task=fin.FIN_CRYPTO, num_envs=N, num_assets=1, num_indicators=0, num_rows=T + 1,
+                          episode_len=T, reward_scale=1.0, cost_rate=0.0, epsilon=eps)
+    env = fin.fin_env_create(fcfg, rows)
+    layers = spol.random_bias(spol.kaiming_bf16(spol.CRYPTO_DIMS, 4), 5)
+    pol = fin.fin_policy_create(fin.FIN_Q_ARGMAX, layers)
+    uni = inputs.crypto_uniforms(T, N, seed=43)
+    logs = dict(actions=zeros((T, N, 1), torch.int16), hold=zeros((T, N, 1), torch.int16),
+                cash=zeros((T, N), torch.float64), asset=zeros((T, N), torch.float64),
+                reward=zeros((T, N), torch.float32), done=zeros((T, N), torch.uint8),
+                mlp_out=zeros((T, N, 3), torch.float32), mlp_hidden=zeros((T, N, 2, 128), torch.int16),
+                ep_metrics=zeros((2, N, 3), torch.float64),
+                ep_count=zeros(N, torch.int32))
+    fin.fin_rollout(env, [pol], T, fin.make_noise(fin.FIN_NOISE_SUPPLIED, 0, dev(uni)), fin.make_traj(**logs))
+    g = {k: host(v) for k, v in logs.items()}
+    assert fin.fin_env_check(env) == 0
+    st = ocry.reset(ocfg)
+    L64 = omlp.layers_f64(layers)
+    n_tie = 0
+    for t in range(T):
+        X = orol.crypto_obs_batch(ocfg, st, rows)
+        q = omlp.forward(L64, X)
+        omlp.teacher_forced_layers(L64, X, g["mlp_hidden"][t], g["mlp_out"][t])
+        _mlp_close(g["mlp_out"][t].astype(np.float64), q)
+        for i in range(N):
+            qg = g["mlp_out"][t, i].astype(np.float64)
+            j = opol.epsilon_greedy(list(qg), eps, float(uni[t, i, 0]), float(uni[t, i, 1]))
+            assert j - 1 == g["actions"][t, i, 0], (t, i)
+            srt = np.sort(q[i])
+            if uni[t, i, 0] >= eps and srt[-1] - srt[-2] > 4e-3 * np.abs(q[i]).max():
+                assert np.argmax(q[i]) == np.argmax(qg)
+            else:
+                n_tie += 1
+        o = ocry.step(ocfg, st, rows, g["actions"][t, :, 0])
+        assert np.array_equal(np.array(o["pos"]), g["hold"][t, :, 0])
+        assert np.array_equal(np.array(o["cash"]), g["cash"][t]) and np.array_equal(np.array(o["asset"]), g["asset"][t])
+        np.testing.assert_allclose(g["reward"][t], np.array(o["reward"]), rtol=1e-5, atol=1e-3)
+    assert g["done"][-1].all() and np.all(g["ep_count"] == 1)
+    for i in range(0, N, 37):
+        eq = [1e6] + list(g["asset"][:, i])
+        np.testing.assert_allclose(g["ep_metrics"][0, i], omet.episode_metrics(eq), rtol=1e-7, atol=1e-12)
+
+
+def test_zz_mlp_error_statistics():
+    """Record the per-row norm-wise error ratios seen above (99th pct, max) for DESIGN.md."""
+    import json
+    import os
+    path = os.environ.get("FIN_STATS_PATH")
+    if path and MLP_STATS:
+        with open(path, "w") as f:
+            json.dump({"p99_max_pairs": MLP_STATS,
+                       "max": max(m for _, m in MLP_STATS), "p99_max": max(p for p, _ in MLP_STATS)}, f)

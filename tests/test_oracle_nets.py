@@ -158,3 +158,39 @@ def test_argmax_and_epsilon_greedy():
     assert policy.epsilon_greedy([0.0, 1.0, 0.0], 0.005, 0.004, 0.1) == 0
     assert policy.epsilon_greedy([0.0, 1.0, 0.0], 0.005, 0.006, 0.1) == 1
     assert policy.epsilon_greedy([0.0, 1.0, 0.0], 0.005, 0.0, 0.9999) == 2
+
+
+def _fp32_device_model(layers64, x):
+    """A stand-in 'device': fp32 accumulation, bf16 activations (numpy float32 matmul)."""
+    h = quant.bf16_fast(x).astype(np.float32)
+    hid = []
+    for li, (w, b) in enumerate(layers64):
+        z = h @ w.T.astype(np.float32) + b.astype(np.float32)
+        if li < len(layers64) - 1:
+            a = quant.bf16_fast(np.maximum(z, 0).astype(np.float64))
+            hid.append(spol.f64_to_bf16_bits(a))
+            h = a.astype(np.float32)
+        else:
+            out = z.astype(np.float64)
+    return np.stack(hid, axis=1), out
+
+
+def test_teacher_forced_layers_accepts_fp32_and_rejects_corruption():
+    layers = mlp.layers_f64(_rand_layers((301, 256, 256, 30), 11))
+    rng = np.random.default_rng(12)
+    x = rng.standard_normal((64, 301)) * 2
+    hid, z = _fp32_device_model(layers, x)
+    amb, tot = mlp.teacher_forced_layers(layers, x, hid, z)
+    assert tot == 64 * 512 and amb < tot * 1e-2
+    bad = hid.copy()
+    i, j = np.argwhere(bad[:, 0, :] != 0)[0]
+    bad[i, 0, j] += 2                                   # two bf16 ulps off
+    with pytest.raises(AssertionError):
+        mlp.teacher_forced_layers(layers, x, bad, z)
+    zb = z.copy()
+    zb[3, 4] += 1e-3
+    with pytest.raises(AssertionError):
+        mlp.teacher_forced_layers(layers, x, hid, zb)
+    # an observation-encoding error (input not what the oracle encodes) is caught at layer 1
+    with pytest.raises(AssertionError):
+        mlp.teacher_forced_layers(layers, x * 1.01, hid, z)
