@@ -255,6 +255,10 @@ int fin_mlp_forward(const fin_policy* policy, const uint16_t* x, int32_t B, floa
 int fin_philox_normals(uint64_t seed, int64_t env_offset, int32_t N, int32_t K, int32_t member,
                        int64_t t_global, float* out, void* stream);
 
+/* Debug: record a clock64 timeline of block 0 of subsequent fin_rollout calls into
+ * ``device_buffer`` (u64 [T][16]; NULL disables).  Not for production use. */
+int fin_debug_trace(void* device_buffer);
+
 /* thread-local text for the last non-OK status of this thread */
 const char* fin_last_error(void);
 

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "fin_internal.cuh"
@@ -15,9 +16,14 @@
 #include "tc_plan.cuh"
 
 namespace fin {
-cudaError_t launch_stock_rollout(int net, const tc::TcParams& p, int n_tiles, cudaStream_t s);
-cudaError_t launch_crypto_rollout(const tc::TcParams& p, int n_tiles, cudaStream_t s);
-cudaError_t launch_mlp_probe(int net, const tc::TcParams& p, int n_tiles, cudaStream_t s);
+// n_envs rows; *tiles receives the tiles per CTA the launch used (agg partial rows
+// = ceil(n_envs / (128 * tiles)) * tiles)
+cudaError_t launch_stock_rollout(int net, const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s);
+cudaError_t launch_crypto_rollout(const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s);
+cudaError_t launch_mlp_probe(int net, const tc::TcParams& p, int n_rows, cudaStream_t s);
+cudaError_t launch_z1s_market(int net, const float* w1s_t, int H, const EnvDev& e, float* z1s, cudaStream_t s);
+cudaError_t launch_z1s_probe(int net, const float* w1s_t, int H, const uint16_t* x, int B, int in_dim, float* z1s,
+                             cudaStream_t s);
 }  // namespace fin
 
 struct fin_env {
@@ -29,19 +35,23 @@ struct fin_env {
   float* market_mem;
   double* agg_scratch;
   size_t agg_cap;  // rows of FIN_AGG_LEN
+  float* z1s;      // factored layer 1: per-member shared term of every market day [M][rows][HID]
+  size_t z1s_cap;  // floats
 };
 
 struct fin_policy {
   int32_t kind;
   int32_t net;                 // 0 stock C1, 1 stock small, 2 crypto
   int32_t dims[4];
-  uint8_t* wpack;              // device, TcPlan layout
+  uint8_t* wpack;              // device, TcPlan layout (stock: layer 1 = private columns only)
   float* bias;                 // device, [HID + HID + OUT_PAD]
+  float* w1s_t;                // stock: device [S][HID] shared columns of W1 (exact bf16 values), else null
 };
 
 namespace {
 
 thread_local std::string g_err;
+unsigned long long* g_trace = nullptr;   // fin_debug_trace
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -112,9 +122,12 @@ int net_of(const int32_t* dims) {
   return -1;
 }
 
-template <class Plan>
+// Obs = StockObs<..>: layer 1 keeps only W1's env-private columns (factored layer 1,
+// tc_plan.cuh); the shared columns go to w1s (transposed [S][HID], float).
+template <class Plan, class Obs>
 void pack_member(const int32_t* dims, const uint16_t* const* w, const float* const* bias, std::vector<uint8_t>& wp,
-                 std::vector<float>& bp) {
+                 std::vector<float>& bp, std::vector<float>* w1s) {
+  constexpr bool kFactored = !std::is_void<Obs>::value;
   wp.assign(Plan::kMemberBytes, 0);
   for (int s = 0; s < Plan::kStages; ++s) {
     const int l = Plan::layer_of(s), j0 = Plan::j0_of(s), nks = Plan::nks_of(s);
@@ -123,9 +136,23 @@ void pack_member(const int32_t* dims, const uint16_t* const* w, const float* con
     uint8_t* base = wp.data() + Plan::offset_of(s);
     for (int n = 0; n < rows; ++n)
       for (int kk = 0; kk < kt; ++kk) {
-        const int k = j0 * 16 + kk;
+        int k = j0 * 16 + kk;
+        if constexpr (kFactored) {
+          if (l == 0) k = k < Obs::kEnv ? Obs::env_col(k) : in_l;  // private column or padding
+        }
         const uint16_t v = (n < out_l && k < in_l) ? w[l][(size_t)n * in_l + k] : (uint16_t)0;
         std::memcpy(base + tc_cm_offset(n, kk, kt), &v, 2);
+      }
+  }
+  if constexpr (kFactored) {
+    const int H = dims[1];
+    w1s->assign((size_t)Obs::kShared * H, 0.f);
+    for (int sidx = 0; sidx < Obs::kShared; ++sidx)
+      for (int n = 0; n < H; ++n) {
+        const uint32_t bits = (uint32_t)w[0][(size_t)n * dims[0] + Obs::shared_col(sidx)] << 16;
+        float f;
+        std::memcpy(&f, &bits, 4);
+        (*w1s)[(size_t)sidx * H + n] = f;
       }
   }
   bp.assign(Plan::kBiasFloats, 0.f);
@@ -147,6 +174,10 @@ bool finite_all(const float* x, int64_t n) {
 extern "C" {
 
 const char* fin_last_error(void) { return g_err.c_str(); }
+int fin_debug_trace(void* device_buffer) {
+  g_trace = static_cast<unsigned long long*>(device_buffer);
+  return FIN_OK;
+}
 int fin_abi_version(void) { return FIN_ABI_VERSION; }
 int fin_device_check(int32_t ordinal) { return check_device(ordinal); }
 
@@ -379,6 +410,7 @@ void fin_env_destroy(fin_env* env) {
   if (!env) return;
   cudaStreamSynchronize(env->last_stream);
   if (env->agg_scratch) cudaFree(env->agg_scratch);
+  if (env->z1s) cudaFree(env->z1s);
   if (env->market_mem) cudaFree(env->market_mem);
   if (env->state_mem) cudaFree(env->state_mem);
   delete env;
@@ -401,10 +433,10 @@ int fin_policy_create(int32_t kind, int32_t n_layers, const int32_t* dims, const
     if (bias && bias[l] && !finite_all(bias[l], dims[l + 1])) return fail(FIN_E_DATA, "bias %d non-finite", l);
   }
   std::vector<uint8_t> wp;
-  std::vector<float> bp;
-  if (net == 0) pack_member<PlanStockC1>(dims, w_bf16, bias, wp, bp);
-  else if (net == 1) pack_member<PlanStockSmall>(dims, w_bf16, bias, wp, bp);
-  else pack_member<PlanCrypto>(dims, w_bf16, bias, wp, bp);
+  std::vector<float> bp, w1s;
+  if (net == 0) pack_member<PlanStockC1, ObsC1>(dims, w_bf16, bias, wp, bp, &w1s);
+  else if (net == 1) pack_member<PlanStockSmall, ObsSmall>(dims, w_bf16, bias, wp, bp, &w1s);
+  else pack_member<PlanCrypto, void>(dims, w_bf16, bias, wp, bp, nullptr);
   fin_policy* pol = new (std::nothrow) fin_policy();
   if (!pol) return fail(FIN_E_CONFIG, "out of host memory");
   pol->kind = kind;
@@ -412,12 +444,16 @@ int fin_policy_create(int32_t kind, int32_t n_layers, const int32_t* dims, const
   for (int l = 0; l < 4; ++l) pol->dims[l] = dims[l];
   cudaError_t e = cudaMalloc(&pol->wpack, wp.size());
   if (e == cudaSuccess) e = cudaMalloc(&pol->bias, bp.size() * sizeof(float));
+  if (e == cudaSuccess && !w1s.empty()) e = cudaMalloc(&pol->w1s_t, w1s.size() * sizeof(float));
   if (e == cudaSuccess) e = cudaMemcpyAsync(pol->wpack, wp.data(), wp.size(), cudaMemcpyHostToDevice, S(stream));
   if (e == cudaSuccess) e = cudaMemcpyAsync(pol->bias, bp.data(), bp.size() * 4, cudaMemcpyHostToDevice, S(stream));
+  if (e == cudaSuccess && !w1s.empty())
+    e = cudaMemcpyAsync(pol->w1s_t, w1s.data(), w1s.size() * 4, cudaMemcpyHostToDevice, S(stream));
   if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
   if (e != cudaSuccess) {
     if (pol->wpack) cudaFree(pol->wpack);
     if (pol->bias) cudaFree(pol->bias);
+    if (pol->w1s_t) cudaFree(pol->w1s_t);
     delete pol;
     return cuda_fail(e, "fin_policy_create upload");
   }
@@ -430,6 +466,7 @@ void fin_policy_destroy(fin_policy* pol) {
   cudaDeviceSynchronize();
   cudaFree(pol->wpack);
   cudaFree(pol->bias);
+  if (pol->w1s_t) cudaFree(pol->w1s_t);
   delete pol;
 }
 
@@ -467,6 +504,29 @@ int fill_members(const fin_env* env, const fin_policy* const* members, int32_t n
   return FIN_OK;
 }
 
+// Factored stock layer 1: the shared-input term of every market day for every member
+// (z1s = W1_shared q(x_shared(d)), tc_plan.cuh), recomputed at each rollout so it
+// always matches the members and the market it is used with (1008 x 270 x 256 FMAs).
+int prepare_z1s(fin_env* env, const fin_policy* const* members, int n, int net, tc::TcParams& p, cudaStream_t s) {
+  if (env->d.task != FIN_STOCK) return FIN_OK;
+  const int H = members[0]->dims[1];
+  const size_t need = (size_t)n * env->d.rows * H;
+  if (env->z1s_cap < need) {
+    if (env->z1s) cudaFree(env->z1s);
+    env->z1s = nullptr;
+    env->z1s_cap = 0;
+    FIN_CUDA(cudaMalloc(&env->z1s, need * sizeof(float)));
+    env->z1s_cap = need;
+  }
+  for (int m = 0; m < n; ++m) {
+    cudaError_t e = fin::launch_z1s_market(net, members[m]->w1s_t, H, env->d, env->z1s + (size_t)m * env->d.rows * H, s);
+    if (e != cudaSuccess) return cuda_fail(e, "z1s precompute");
+  }
+  p.z1s = env->z1s;
+  p.z1s_rows = env->d.rows;
+  return FIN_OK;
+}
+
 int fill_noise(const fin_noise* noise, tc::TcParams& p) {
   if (!noise) {
     p.noise_mode = FIN_NOISE_NONE;
@@ -496,21 +556,26 @@ int fin_rollout(fin_env* env, const fin_policy* const* members, int32_t n_member
   if (rc != FIN_OK) return rc;
   rc = fill_noise(noise, p);
   if (rc != FIN_OK) return rc;
+  rc = prepare_z1s(env, members, n_members, net, p, S(stream));
+  if (rc != FIN_OK) return rc;
   const int n_tiles = (env->d.N + tc::kTileM - 1) / tc::kTileM;
   p.e = env->d;
   p.o = to_dev(out);
   p.T = T;
+  p.trace = g_trace;
   if (out && out->agg) {
-    rc = ensure_agg(env, (size_t)n_tiles);
+    rc = ensure_agg(env, (size_t)n_tiles + 2);
     if (rc != FIN_OK) return rc;
     p.o.agg_partial = env->agg_scratch;
   }
   env->last_stream = S(stream);
-  cudaError_t e = env->d.task == FIN_STOCK ? fin::launch_stock_rollout(net, p, n_tiles, S(stream))
-                                           : fin::launch_crypto_rollout(p, n_tiles, S(stream));
+  int tiles = 1;
+  cudaError_t e = env->d.task == FIN_STOCK ? fin::launch_stock_rollout(net, p, env->d.N, &tiles, S(stream))
+                                           : fin::launch_crypto_rollout(p, env->d.N, &tiles, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fin_rollout launch");
   if (out && out->agg) {
-    e = fin::launch_agg_finalize(env->agg_scratch, n_tiles, out->agg, S(stream));
+    const int rows = (env->d.N + tc::kTileM * tiles - 1) / (tc::kTileM * tiles) * tiles;
+    e = fin::launch_agg_finalize(env->agg_scratch, rows, out->agg, S(stream));
     if (e != cudaSuccess) return cuda_fail(e, "fin_rollout agg");
   }
   env->d.t_global += T;
@@ -552,17 +617,16 @@ int fin_ensemble_act(fin_env* env, const fin_policy* const* members, int32_t n_m
   if (rc != FIN_OK) return rc;
   rc = fill_noise(noise, p);
   if (rc != FIN_OK) return rc;
-  if (p.noise_mode == FIN_NOISE_SUPPLIED) {
-    // supplied noise is indexed [t][M][N][K] with t = 0
-  }
-  p.e = env->d;
+  rc = prepare_z1s(env, members, n_members, net, p, S(stream));
+  if (rc != FIN_OK) return rc;
+  p.e = env->d;   // supplied noise is read as [1][M][N][K]; Philox uses the env's current step
   p.T = 1;
   p.act_only = 1;
   p.mean_out = mean_action;
   p.o.actions = actions;
-  const int n_tiles = (env->d.N + tc::kTileM - 1) / tc::kTileM;
   env->last_stream = S(stream);
-  cudaError_t e = fin::launch_stock_rollout(net, p, n_tiles, S(stream));
+  int tiles = 1;
+  cudaError_t e = fin::launch_stock_rollout(net, p, env->d.N, &tiles, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fin_ensemble_act launch");
   return FIN_OK;
 }
@@ -606,8 +670,16 @@ int fin_mlp_forward(const fin_policy* pol, const uint16_t* x, int32_t B, float* 
   p.B = B;
   p.in_dim = pol->dims[0];
   p.out_dim = pol->dims[3];
-  const int n_tiles = (B + tc::kTileM - 1) / tc::kTileM;
-  cudaError_t e = fin::launch_mlp_probe(pol->net, p, n_tiles, S(stream));
+  float* z1s = nullptr;
+  cudaStream_t s = S(stream);
+  cudaError_t e = cudaSuccess;
+  if (pol->w1s_t) {  // factored stock net: shared-input term of each probe row
+    e = cudaMallocAsync(&z1s, sizeof(float) * (size_t)B * pol->dims[1], s);
+    if (e == cudaSuccess) e = fin::launch_z1s_probe(pol->net, pol->w1s_t, pol->dims[1], x, B, pol->dims[0], z1s, s);
+    p.z1s = z1s;
+  }
+  if (e == cudaSuccess) e = fin::launch_mlp_probe(pol->net, p, B, s);
+  if (z1s) cudaFreeAsync(z1s, s);
   if (e != cudaSuccess) return cuda_fail(e, "fin_mlp_forward launch");
   return FIN_OK;
 }

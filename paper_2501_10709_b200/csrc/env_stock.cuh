@@ -19,9 +19,9 @@
 // h[] holds int holdings (updated in place), a[] the requested deltas.
 // Returns via references: v (pre-trade asset at p), vn (post-trade asset at pn),
 // act[] the action after the clamp (R6); oor set when an action was clamped.
-template <int KP>
+template <int KP, typename PT>
 __device__ __forceinline__ void stock_transition(const EnvDev& e, double& b, int (&h)[KP],
-                                                 const float* __restrict__ p, const float* __restrict__ pn,
+                                                 const PT* __restrict__ p, const PT* __restrict__ pn,
                                                  const int (&a)[KP], double& v, double& vn,
                                                  int (&act)[KP], bool& oor) {
   const int K = e.K;

@@ -85,16 +85,30 @@ __device__ __forceinline__ int32_t day_of(const EnvDev& e, int32_t w, int32_t t)
 // path (enough cash) is one multiply; otherwise an fp32 estimate of b/u (relative
 // error ~1e-7, so within +-1 of the answer for n < 2^15) is corrected by exact
 // fp64 checks until the definition holds.
-__device__ __forceinline__ int affordable(double b, double u, int want) {
-  if (want <= 0) return 0;
-  if (fmul64((double)want, u) <= b) return want;
-  if (!(b >= 0.0)) return 0;
-  float qf = __fdiv_rn((float)b, (float)u);
-  int n = (int)fminf(floorf(qf), (float)want);
-  if (n < 0) n = 0;
+// slow path, out of line: one copy in the binary however often it is inlined around
+static __device__ __noinline__ int affordable_slow(double b, double u, int want) {
+  if (!(b >= u)) return 0;                                 // not even one share (also b < 0, NaN)
+  const float qf = fminf(__fdividef((float)b, (float)u), (float)want);   // estimate, corrected below
+  int n = qf > 0.f ? (int)qf : 0;
   while (n > 0 && fmul64((double)n, u) > b) --n;
   while (n < want && fmul64((double)(n + 1), u) <= b) ++n;
   return n;
+}
+
+// h / d correctly rounded in fp32 for integer |h| < 2^24 and d >= 1, without the IEEE
+// division subroutine: q = h * (1/d) then one FMA residual correction (exhaustively
+// checked for |h| < 2^15 and the divisors used here); the bf16 of the
+// result therefore equals q(h / d) of the oracle.
+__device__ __forceinline__ float div_int_f32(int h, float d, float inv_d) {
+  const float hf = (float)h;
+  const float q = __fmul_rn(hf, inv_d);
+  const float r = __fmaf_rn(-q, d, hf);
+  return __fmaf_rn(r, inv_d, q);
+}
+__device__ __forceinline__ int affordable(double b, double u, int want) {
+  if (want <= 0) return 0;
+  if (fmul64((double)want, u) <= b) return want;
+  return affordable_slow(b, u, want);
 }
 
 // ----------------------------------------------------------------- online metrics
@@ -185,8 +199,10 @@ __device__ inline void agg_block_write(const AggAcc& a, double* partial_row) {
 
 // Same reduction for a 128-thread warpgroup that synchronises on named barrier
 // ``bar_id`` (used inside warp-specialised kernels where other warps are busy).
-__device__ inline void agg_group_write(const AggAcc& a, double* partial_row, int group_tid, int bar_id) {
-  __shared__ double red_g[4][FIN_AGG_LEN];
+__device__ inline void agg_group_write(const AggAcc& a, double* partial_row, int group_tid, int bar_id,
+                                       int group = 0) {
+  __shared__ double red_all[2][4][FIN_AGG_LEN];   // one scratch per warpgroup (<= 2 per CTA)
+  double (*red_g)[FIN_AGG_LEN] = red_all[group & 1];
   const int lane = group_tid & 31, wid = group_tid >> 5;
   double v[FIN_AGG_LEN];
 #pragma unroll

@@ -21,15 +21,51 @@ __device__ __forceinline__ float philox_u01(uint32_t x) {
   return ((float)(x >> 8) + 0.5f) * 5.9604644775390625e-08f;  // 2^-24, exact
 }
 
+// Box-Muller pair from (u_r, u_a): r = sqrt(-2 ln u_r) (accurate log: u_r can be
+// 1 - 2^-25), angle 2 pi u_a evaluated as 2 pi (u_a - [u_a >= 1/2]) in [-pi, pi) with
+// the fast sincos (absolute error ~4e-7 there).
+__device__ __forceinline__ void box_muller(float ur, float ua, float& z0, float& z1) {
+  const float r = sqrtf(-2.0f * logf(ur));
+  const float a = 6.283185307179586f * (ua >= 0.5f ? ua - 1.0f : ua);
+  float s, c;
+  __sincosf(a, &s, &c);
+  z0 = r * c;
+  z1 = r * s;
+}
+
+// Two counters (word2a, word2b) interleaved for instruction-level parallelism, out of
+// line (one copy in the kernel), results returned in registers.
+struct Normals8 {
+  float4 a, b;
+};
+static __device__ __noinline__ Normals8 philox_normals8_v(uint64_t g, uint32_t t, uint32_t word2a, uint32_t word2b,
+                                                           uint64_t seed) {
+  uint32_t ca[4] = {(uint32_t)g, t, word2a, 0u};
+  uint32_t cb[4] = {(uint32_t)g, t, word2b, 0u};
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    const uint32_t ha0 = __umulhi(0xD2511F53u, ca[0]), la0 = 0xD2511F53u * ca[0];
+    const uint32_t hb0 = __umulhi(0xD2511F53u, cb[0]), lb0 = 0xD2511F53u * cb[0];
+    const uint32_t ha1 = __umulhi(0xCD9E8D57u, ca[2]), la1 = 0xCD9E8D57u * ca[2];
+    const uint32_t hb1 = __umulhi(0xCD9E8D57u, cb[2]), lb1 = 0xCD9E8D57u * cb[2];
+    const uint32_t na0 = ha1 ^ ca[1] ^ k0, na2 = ha0 ^ ca[3] ^ k1;
+    const uint32_t nb0 = hb1 ^ cb[1] ^ k0, nb2 = hb0 ^ cb[3] ^ k1;
+    ca[0] = na0; ca[1] = la1; ca[2] = na2; ca[3] = la0;
+    cb[0] = nb0; cb[1] = lb1; cb[2] = nb2; cb[3] = lb0;
+  }
+  Normals8 o;
+  box_muller(philox_u01(ca[0]), philox_u01(ca[1]), o.a.x, o.a.y);
+  box_muller(philox_u01(ca[2]), philox_u01(ca[3]), o.a.z, o.a.w);
+  box_muller(philox_u01(cb[0]), philox_u01(cb[1]), o.b.x, o.b.y);
+  box_muller(philox_u01(cb[2]), philox_u01(cb[3]), o.b.z, o.b.w);
+  return o;
+}
+
 __device__ __forceinline__ void philox_normals4(uint64_t g, uint32_t t, uint32_t word2, uint64_t seed, float z[4]) {
-  uint32_t c[4] = {(uint32_t)g, t, word2, 0u};
-  philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
-  const float u0 = philox_u01(c[0]), u1 = philox_u01(c[1]), u2 = philox_u01(c[2]), u3 = philox_u01(c[3]);
-  const float r0 = sqrtf(-2.0f * logf(u0)), r1 = sqrtf(-2.0f * logf(u2));
-  float s0, c0, s1, c1;
-  sincospif(2.0f * u1, &s0, &c0);
-  sincospif(2.0f * u3, &s1, &c1);
-  z[0] = r0 * c0; z[1] = r0 * s0; z[2] = r1 * c1; z[3] = r1 * s1;
+  const Normals8 v = philox_normals8_v(g, t, word2, word2, seed);
+  z[0] = v.a.x; z[1] = v.a.y; z[2] = v.a.z; z[3] = v.a.w;
 }
 
 __device__ __forceinline__ void philox_uniform2(uint64_t g, uint32_t t, uint64_t seed, float u[2]) {

@@ -3,7 +3,10 @@
 // Q = MLP(q(obs)) on tcgen05 with the 60 KB Q-net resident in shared memory ->
 // argmax (lowest index on ties) with epsilon-greedy exploration ->
 // a in {-1, 0, 1} -> LOB-walk execution, reward, done / reset (env_crypto.cuh) ->
-// online episode metrics.
+// online episode metrics.  All envs of the C3 workload read the same row t
+// (lockstep, reading R27): once per step a tile stages the bf16 factor part of the
+// observation and the two book rows in shared memory; a tile whose envs sit on
+// different rows takes the per-env path.
 #include <cuda_bf16.h>
 
 #include "env_crypto.cuh"
@@ -14,10 +17,35 @@ namespace {
 
 using tc::TcParams;
 
+__device__ __forceinline__ uint32_t bf16_bits(float v) {
+  return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v));
+}
+__device__ __forceinline__ bool bar_red_and(int bar_id, bool pred) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.u32 p, %1, 0;\n\t"
+      "bar.red.and.pred q, %2, 128, p;\n\t"
+      "selp.u32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"((uint32_t)pred), "r"(bar_id)
+      : "memory");
+  return r != 0;
+}
+__device__ __forceinline__ void bar_sync128(int bar_id) {
+  asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+}
+
 struct CryptoOps {
   static constexpr int IN = 2 + FIN_C_FACTORS;  // 103
+  static constexpr int KT8 = PlanCrypto::kIn / 8;
+  static constexpr int kOffX = 0;                               // bf16 obs row (112)
+  static constexpr int kOffR = 256;                             // rows t, t+1 (2 x 144 floats)
+  static constexpr int kOffT = kOffR + 2 * FIN_C_ROW * 4;
+  static constexpr int kStageBytes = kOffT + 16;
+
   struct State {
-    bool live;
+    bool live, uniform;
     double b;
     int h, tau, t_ep;
     int act;
@@ -31,6 +59,7 @@ struct CryptoOps {
   __device__ __forceinline__ static void init(State& st, const TcParams& p, int env, int row) {
     const EnvDev& e = p.e;
     st.live = env < e.N;
+    st.uniform = false;
     st.cnt = 0;
     st.rsum = 0.0;
     st.bad = st.nonfinite = false;
@@ -49,39 +78,64 @@ struct CryptoOps {
     }
   }
 
-  __device__ __forceinline__ static uint32_t obs_bits(int idx, const State& st, const float* row, float inv_hold_den) {
-    float v;
-    if (idx == 0) v = (float)st.h;
-    else if (idx == 1) v = __fdiv_rn((float)st.tau, inv_hold_den);
-    else if (idx < IN) v = __ldg(row + FIN_C_F0 + (idx - 2));
-    else v = 0.f;
-    return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v));
+  __device__ __forceinline__ static void stage(State& st, const TcParams& p, int env, int gtid, int t, uint8_t* stg,
+                                               int bar_id) {
+    const EnvDev& e = p.e;
+    int* sr = reinterpret_cast<int*>(stg + kOffT);
+    int tr = st.t_ep;
+    if (st.live && (tr + 1 >= e.rows)) { st.bad = true; tr = 0; }
+    if (gtid == 0) sr[0] = st.live ? tr : -1;
+    bar_sync128(bar_id);
+    const int t0 = sr[0];
+    const bool uni = bar_red_and(bar_id, !st.live || tr == t0) && t0 >= 0;
+    st.uniform = uni;
+    if (uni) {
+      const float* mrow = e.market + (size_t)t0 * FIN_C_ROW;
+      uint16_t* xs = reinterpret_cast<uint16_t*>(stg + kOffX);
+      for (int idx = gtid; idx < PlanCrypto::kIn; idx += 128)
+        xs[idx] = (idx >= 2 && idx < IN) ? (uint16_t)bf16_bits(__ldg(mrow + FIN_C_F0 + idx - 2)) : (uint16_t)0;
+      float* rs = reinterpret_cast<float*>(stg + kOffR);
+      for (int j = gtid; j < 2 * FIN_C_ROW; j += 128) rs[j] = __ldg(mrow + j);
+      bar_sync128(bar_id);
+    }
   }
 
-  __device__ __forceinline__ static void build_obs(State& st, const TcParams& p, int env, int row, int t,
-                                                   uint32_t xa) {
-    constexpr int KT8 = PlanCrypto::kIn / 8;
+  __device__ __forceinline__ static void build_obs(State& st, const TcParams& p, int env, int row, int t, int m,
+                                                   uint32_t xa, uint8_t* stg) {
     const EnvDev& e = p.e;
     if (!st.live) {
 #pragma unroll
-      for (int c = 0; c < KT8; ++c) sm100::st_shared_v4(xa + tc::cm_off(row, c, KT8), 0u, 0u, 0u, 0u);
+      for (int c = 0; c < KT8; ++c) tc::sts128(xa + tc::cm_off(row, c, KT8), 0u, 0u, 0u, 0u);
       return;
     }
-    int tr = st.t_ep;
-    if (tr + 1 >= e.rows) { st.bad = true; tr = 0; }
-    const float* mrow = e.market + (size_t)tr * FIN_C_ROW;
     const float den = (float)e.max_hold;
+    const uint32_t priv = bf16_bits((float)st.h) | (bf16_bits(div_int_f32(st.tau, den, __frcp_rn(den))) << 16);
+    if (st.uniform) {
+      const uint4* xs = reinterpret_cast<const uint4*>(stg + kOffX);
 #pragma unroll
-    for (int c = 0; c < KT8; ++c) {
-      uint32_t w4[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int i0 = 8 * c + 2 * j;
-        w4[j] = obs_bits(i0, st, mrow, den) | (obs_bits(i0 + 1, st, mrow, den) << 16);
+      for (int c = 0; c < KT8; ++c) {
+        const uint4 v = xs[c];
+        tc::sts128(xa + tc::cm_off(row, c, KT8), c == 0 ? priv : v.x, v.y, v.z, v.w);
       }
-      sm100::st_shared_v4(xa + tc::cm_off(row, c, KT8), w4[0], w4[1], w4[2], w4[3]);
+    } else {
+      const float* mrow = e.market + (size_t)(st.t_ep + 1 < e.rows ? st.t_ep : 0) * FIN_C_ROW;
+#pragma unroll
+      for (int c = 0; c < KT8; ++c) {
+        uint32_t w4[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i0 = 8 * c + 2 * j;
+          const uint32_t lo = (i0 >= 2 && i0 < IN) ? bf16_bits(__ldg(mrow + FIN_C_F0 + i0 - 2)) : 0u;
+          const uint32_t hi = (i0 + 1 >= 2 && i0 + 1 < IN) ? bf16_bits(__ldg(mrow + FIN_C_F0 + i0 - 1)) : 0u;
+          w4[j] = lo | (hi << 16);
+        }
+        if (c == 0) w4[0] = priv;
+        tc::sts128(xa + tc::cm_off(row, c, KT8), w4[0], w4[1], w4[2], w4[3]);
+      }
     }
   }
+
+  __device__ __forceinline__ static const float* l1_addend(State&, const TcParams&, int, uint8_t*) { return nullptr; }
 
   __device__ __forceinline__ static uint16_t* hidden_ptr(State& st, const TcParams& p, int env, int t, int m, int l,
                                                          int hid) {
@@ -113,7 +167,7 @@ struct CryptoOps {
     st.act = best - 1;
   }
 
-  __device__ __forceinline__ static void finish_step(State& st, const TcParams& p, int env, int t) {
+  __device__ __forceinline__ static void finish_step(State& st, const TcParams& p, int env, int t, uint8_t* stg) {
     if (!st.live) return;
     const EnvDev& e = p.e;
     const size_t ti = (size_t)t * e.N + env;
@@ -123,7 +177,8 @@ struct CryptoOps {
       if (p.o.done) p.o.done[ti] = 1;
       return;
     }
-    const float* row = e.market + (size_t)st.t_ep * FIN_C_ROW;
+    const float* row = st.uniform ? reinterpret_cast<const float*>(stg + kOffR)
+                                  : e.market + (size_t)st.t_ep * FIN_C_ROW;
     double v, vn;
     int delta;
     crypto_transition(e, st.b, st.h, st.tau, row, row + FIN_C_ROW, st.act, v, vn, delta);
@@ -154,7 +209,8 @@ struct CryptoOps {
     }
   }
 
-  __device__ __forceinline__ static void finalize(State& st, const TcParams& p, int env) {
+  __device__ __forceinline__ static void finalize(State& st, const TcParams& p, int env, int gtid, int bar_id,
+                                                  int tile) {
     const EnvDev& e = p.e;
     if (st.live) {
       e.cash[env] = st.b;
@@ -168,8 +224,9 @@ struct CryptoOps {
       if (st.nonfinite) set_flag(e, FIN_FLAG_NONFINITE);
     }
     st.agg.s[FIN_AGG_SUM_REWARD] = st.rsum;
-    if (p.o.agg_partial) agg_group_write(st.agg, p.o.agg_partial + (size_t)blockIdx.x * FIN_AGG_LEN,
-                                         threadIdx.x - tc::kEnvWarp0 * 32, 1);
+    if (p.o.agg_partial)
+      agg_group_write(st.agg, p.o.agg_partial + ((size_t)blockIdx.x * (blockDim.x / 128) + tile) * FIN_AGG_LEN, gtid,
+                      bar_id, tile);
   }
 };
 
@@ -177,13 +234,18 @@ struct CryptoOps {
 
 namespace fin {
 
-cudaError_t launch_crypto_rollout(const tc::TcParams& p, int n_tiles, cudaStream_t s) {
-  using S = tc::Smem<PlanCrypto, true>;
-  auto kern = tc::k_tc_rollout<PlanCrypto, true, CryptoOps>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
-  if (err != cudaSuccess) return err;
-  kern<<<n_tiles, tc::kThreads, S::kTotal, s>>>(p);
-  return cudaGetLastError();
+int num_sms();
+
+// The C3 loop is latency-bound (one lockstep step at a time): spread tiles over the
+// SMs first (one tile per CTA); pair tiles per CTA only when tiles outnumber SMs.
+cudaError_t launch_crypto_rollout(const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s) {
+  const int n_tiles = (n_envs + tc::kTileM - 1) / tc::kTileM;
+  if (n_tiles > num_sms()) {
+    *tiles = 2;
+    return tc::launch<PlanCrypto, true, 2, CryptoOps>(p, n_envs, s);
+  }
+  *tiles = 1;
+  return tc::launch<PlanCrypto, true, 1, CryptoOps>(p, n_envs, s);
 }
 
 }  // namespace fin

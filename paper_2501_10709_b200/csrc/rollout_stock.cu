@@ -1,16 +1,28 @@
 // rollout_stock.cu -- fused stock policy rollout (K3, with the C2 ensemble K5 inside)
 // and the standalone MLP probe (K7), instantiated from rollout_tc.cuh.
 //
-// Per step and env (thread r of the env warpgroup):
+// Per step and env (thread r of a tile's env warpgroup):
 //   observation s_t = [b/b0, close_norm_t, h/max_trade, f_t]  (readings R13, R14)
 //   -> per member m: z_m = MLP_m(q(s_t)) on tcgen05 (BASELINE configs[1,2])
 //   -> member action (R17, R19): PPO clip(tanh z + std eps), SAC tanh(z + std eps),
 //      DDPG OU x <- x + theta(0 - x) + sigma eps, clip(tanh z + x)
 //   -> ensemble mean (R20) -> shares = rha(max_trade * abar)  (R18)
 //   -> trade, reward, done / reset (env_stock.cuh), online episode metrics.
+//
+// Staging: the market part of the observation (close_norm, indicators; 270 of 301
+// inputs for C1) and the two close-price rows are the same for every env of a
+// tile that sits on the same day d (tile-aligned windows, lockstep clocks: the
+// normal case).  group_apply (group_stage.cuh) converts that row once per tile into
+// shared memory (bf16 observation part, fp64 prices); each env copies it into its
+// observation row, patches in its private entries (cash, holdings) and reads its
+// execution / marking prices from it.  Tiles whose envs sit on several days are
+// served one day at a time by the same code path.
 #include <cuda_bf16.h>
 
+#include <type_traits>
+
 #include "env_stock.cuh"
+#include "group_stage.cuh"
 #include "philox.cuh"
 #include "rollout_tc.cuh"
 
@@ -18,18 +30,47 @@ namespace {
 
 using tc::TcParams;
 
-template <int KA, int IA>
+__device__ __forceinline__ uint32_t bf16_bits(float v) {
+  return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v));
+}
+
+// tanh(x) = sign(x) (1 - 2 / (exp(2|x|) + 1)) with the fast exp / reciprocal: absolute
+// error ~1e-7 (the sampled share count 100 a moves by ~1e-5, well inside the 1e-4
+// rounding-boundary allowance of the parity check); ~8 instructions instead of the
+// ~35 of tanhf, which the rollout inlines once per asset.
+__device__ __forceinline__ float tanh_f32(float x) {
+  const float e2 = __expf(2.f * fabsf(x));
+  const float t = 1.f - __fdividef(2.f, e2 + 1.f);
+  return copysignf(t, x);
+}
+
+// ENS = false: the single-policy (C1) specialisation -- one non-DDPG member, no OU
+// state kept in registers.
+template <int KA, int IA, class Plan, bool ENS = true>
 struct StockOps {
+  static constexpr int KOU = ENS ? KA : 1;
   static constexpr int KP4 = (KA + 3) / 4 * 4;
   static constexpr int IN = 1 + 2 * KA + IA * KA;
+  static constexpr int KT8 = Plan::kIn / 8;
+  using Obs = StockObs<KA, IA>;
+  static_assert(Obs::kEnvPad == Plan::kIn, "factored layer 1: the network input is the private part");
+  // staging: close_d, close_d+1 (f64) | z1s rows of day d per member (f32) | slots | broadcast
+  static constexpr int kOffP = 0;
+  static constexpr int kOffZ = 2 * KP4 * 8;
+  static constexpr int kOffS = kOffZ + FIN_MAX_MEMBERS * Plan::kHid * 4;
+  static constexpr int kOffB = kOffS + 16;
+  static constexpr int kStageBytes = kOffB + 16;
 
   struct State {
     bool live;
+    int gtid, bar_id, round;
     double b;
     int h[KA];
     int t_ep, w, d;
+    uint32_t b0bits;
+    bool zsm;          // this step's z1s rows are staged in shared memory
     float asum[KA];
-    float ou[KA];
+    float ou[KOU];
     MetricAcc m;
     AggAcc agg;
     int cnt;
@@ -40,9 +81,11 @@ struct StockOps {
   __device__ __forceinline__ static void init(State& st, const TcParams& p, int env, int row) {
     const EnvDev& e = p.e;
     st.live = env < e.N;
+    st.round = 0;
     st.cnt = 0;
     st.rsum = 0.0;
     st.oor = st.bad = st.nonfinite = false;
+    st.d = 0;
     agg_init(st.agg);
     if (st.live) {
       st.b = e.cash[env];
@@ -52,62 +95,103 @@ struct StockOps {
       st.w = e.window[env];
       st.m.v0 = e.m_v0[env]; st.m.vprev = e.m_vprev[env]; st.m.peak = e.m_peak[env]; st.m.mdd = e.m_mdd[env];
       st.m.mean = e.m_mean[env]; st.m.m2 = e.m_m2[env]; st.m.n = e.m_n[env];
-      // OU state of the (single) DDPG member, slot = member index
-      int slot = -1;
+      int slot = -1;  // OU state of the (single) DDPG member
       for (int m = 0; m < p.M; ++m)
         if (p.kinds[m] == FIN_DDPG_OU) slot = m;
 #pragma unroll
-      for (int k = 0; k < KA; ++k) st.ou[k] = slot >= 0 ? e.ou[((size_t)slot * e.K + k) * e.N + env] : 0.f;
+      for (int k = 0; k < KOU; ++k) st.ou[k] = (ENS && slot >= 0) ? e.ou[((size_t)slot * e.K + k) * e.N + env] : 0.f;
     } else {
       st.b = 0.0;
 #pragma unroll
-      for (int k = 0; k < KA; ++k) { st.h[k] = 0; st.ou[k] = 0.f; }
+      for (int k = 0; k < KA; ++k) st.h[k] = 0;
+#pragma unroll
+      for (int k = 0; k < KOU; ++k) st.ou[k] = 0.f;
       st.t_ep = 0; st.w = 0;
       metric_start(st.m, 0.0);
     }
   }
 
-  // q(x) of one observation element; idx is a compile-time constant after unrolling
-  __device__ __forceinline__ static uint32_t obs_bits(int idx, const State& st, const float* mrow, uint32_t b0bits,
-                                                      float inv_trade_den) {
-    float v;
-    if (idx == 0) return b0bits;
-    if (idx <= KA) v = __ldg(mrow + KP4 + (idx - 1));                      // close_norm_t[k]
-    else if (idx <= 2 * KA) v = __fdiv_rn((float)st.h[idx - KA - 1], inv_trade_den);  // h_k / max_trade
-    else if (idx < IN) {
-      const int j = idx - (2 * KA + 1);
-      v = __ldg(mrow + (2 + j / KA) * KP4 + (j % KA));                     // feature, indicator-major
-    } else v = 0.f;
-    return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v));
+  // stage day k: fp64 close prices of rows k, k+1 and the members' z1s rows of day k
+  __device__ __noinline__ static void stage_row(const TcParams& p, int k, int gtid, uint8_t* stg) {
+    const EnvDev& e = p.e;
+    const float* mrow = e.market + (size_t)k * e.row_floats;
+    double* pd = reinterpret_cast<double*>(stg + kOffP);
+    if (gtid < 2 * KP4) {
+      const int r = gtid / KP4, kk = gtid % KP4;
+      pd[gtid] = kk < KA ? (double)__ldg(mrow + r * e.row_floats + kk) : 0.0;
+    }
+    float* zs = reinterpret_cast<float*>(stg + kOffZ);
+    for (int j = gtid; j < p.M * Plan::kHid; j += 128) {
+      const int m = j / Plan::kHid, n = j % Plan::kHid;
+      zs[j] = __ldg(p.z1s + ((size_t)m * p.z1s_rows + k) * Plan::kHid + n);
+    }
   }
 
-  template <class Plan>
-  __device__ __forceinline__ static void build_obs_t(State& st, const TcParams& p, int env, int row, int t,
-                                                     uint32_t xa) {
+  // once per step, all 128 threads of the tile: day of every env; if the tile sits on
+  // one day, stage that day once (prices, z1s rows) for the whole step
+  __device__ __forceinline__ static void stage(State& st, const TcParams& p, int env, int gtid, int t, uint8_t* stg,
+                                               int bar_id) {
     const EnvDev& e = p.e;
-    constexpr int KT8 = Plan::kIn / 8;
-    if (!st.live) {
-#pragma unroll
-      for (int c = 0; c < KT8; ++c) sm100::st_shared_v4(xa + tc::cm_off(row, c, KT8), 0u, 0u, 0u, 0u);
-      return;
+    st.gtid = gtid;
+    st.bar_id = bar_id;
+    GroupSlots* gs = reinterpret_cast<GroupSlots*>(stg + kOffS);
+    int* bc = reinterpret_cast<int*>(stg + kOffB);
+    if (t == 0) gs_init(gs, gtid, bar_id);
+    if (st.live) {
+      st.d = day_of(e, st.w, st.t_ep);
+      if (st.d < 0 || st.d + 1 >= e.rows) { st.bad = true; st.d = 0; }
+      st.b0bits = (uint32_t)__bfloat16_as_ushort(__double2bfloat16(fdiv64(st.b, e.cash0)));
     }
-    st.d = day_of(e, st.w, st.t_ep);
-    if (st.d < 0 || st.d + 1 >= e.rows) { st.bad = true; st.d = 0; }
-    const float* mrow = e.market + (size_t)st.d * e.row_floats;
-    const uint32_t b0 = (uint32_t)__bfloat16_as_ushort(__double2bfloat16(fdiv64(st.b, e.cash0)));
+    if (gtid == 0) bc[0] = st.live ? st.d : -1;
+    gs_bar(bar_id);
+    FIN_TR(threadIdx.x == 128, t, 23);
+    const int d0 = bc[0];
+    const int staged = gs->staged;            // read by all before thread 0 may rewrite it
+    const bool uni = !gs_bar_or(bar_id, st.live && st.d != d0) && d0 >= 0;
+    FIN_TR(threadIdx.x == 128, t, 24);
+    st.zsm = uni;
+    if (uni && d0 != staged) {
+      stage_row(p, d0, gtid, stg);
+      if (gtid == 0) gs->staged = d0;
+      gs_bar(bar_id);
+    }
+    FIN_TR(threadIdx.x == 128, t, 25);
+  }
+
+  // factored layer 1: the shared-input term of this env's day, member m
+  __device__ __forceinline__ static const float* l1_addend(State& st, const TcParams& p, int m, uint8_t* stg) {
+    if (st.zsm) return reinterpret_cast<const float*>(stg + kOffZ) + m * Plan::kHid;
+    return p.z1s + ((size_t)m * p.z1s_rows + st.d) * Plan::kHid;
+  }
+
+  // the env-private observation entries [b/b0, h_k/max_trade, 0 pad] -> X (bf16)
+  __device__ __forceinline__ static void build_obs(State& st, const TcParams& p, int env, int row, int t, int m,
+                                                   uint32_t xa, uint8_t* stg) {
+    const EnvDev& e = p.e;
+    if (m == 0) {
+#pragma unroll
+      for (int k = 0; k < KA; ++k) st.asum[k] = 0.f;
+    }
     const float den = (float)e.max_trade;
+    const float inv_den = __frcp_rn(den);
 #pragma unroll
     for (int c = 0; c < KT8; ++c) {
       uint32_t w4[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int i0 = 8 * c + 2 * j;
-        w4[j] = obs_bits(i0, st, mrow, b0, den) | (obs_bits(i0 + 1, st, mrow, b0, den) << 16);
-      }
-      sm100::st_shared_v4(xa + tc::cm_off(row, c, KT8), w4[0], w4[1], w4[2], w4[3]);
-    }
+        uint32_t lohi[2];
 #pragma unroll
-    for (int k = 0; k < KA; ++k) st.asum[k] = 0.f;
+        for (int q = 0; q < 2; ++q) {
+          const int idx = 8 * c + 2 * j + q;
+          lohi[q] = !st.live ? 0u
+                    : idx == 0 ? st.b0bits
+                    : idx <= KA ? bf16_bits(div_int_f32(st.h[idx - 1], den, inv_den))
+                                : 0u;
+        }
+        w4[j] = lohi[0] | (lohi[1] << 16);
+      }
+      tc::sts128(xa + tc::cm_off(row, c, KT8), w4[0], w4[1], w4[2], w4[3]);
+    }
   }
 
   __device__ __forceinline__ static uint16_t* hidden_ptr(State& st, const TcParams& p, int env, int t, int m, int l,
@@ -120,114 +204,133 @@ struct StockOps {
     if (!st.live) return;
     const EnvDev& e = p.e;
     const int kind = p.kinds[m];
-    float eps[KA];
-    if (p.noise_mode == FIN_NOISE_SUPPLIED) {
-      const float* nz = p.noise + (((size_t)t * p.M + m) * e.N + env) * KA;
-#pragma unroll
-      for (int k = 0; k < KA; ++k) eps[k] = __ldg(nz + k);
-    } else if (p.noise_mode == FIN_NOISE_PHILOX) {
-#pragma unroll
-      for (int blk = 0; blk < (KA + 3) / 4; ++blk) {
-        float zz[4];
-        philox_normals4((uint64_t)(e.env_offset + env), (uint32_t)(e.t_global + t), ((uint32_t)m << 16) | blk,
-                        p.noise_seed, zz);
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (blk * 4 + j < KA) eps[blk * 4 + j] = zz[j];
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < KA; ++k) eps[k] = 0.f;
-    }
+    const bool sac = kind == FIN_SAC_SQUASH, ddpg = kind == FIN_DDPG_OU;
     if (p.o.mlp_out) {
       float* dst = p.o.mlp_out + (((size_t)t * p.M + m) * e.N + env) * KA;
 #pragma unroll
       for (int k = 0; k < KA; ++k) dst[k] = z[k];
     }
     const float wm = p.weighted ? p.mw[m] : 1.f;
+    const float* nz = p.noise + (((size_t)t * p.M + m) * e.N + env) * KA;
+    // noise in blocks of 8 assets: two Philox counters (blocks 2q, 2q+1) per call
 #pragma unroll
-    for (int k = 0; k < KA; ++k) {
-      float a;
-      const float zk = z[k];
-      if (kind == FIN_SAC_SQUASH) {
-        a = tanhf(__fadd_rn(zk, __fmul_rn(e.noise_std, eps[k])));
-      } else if (kind == FIN_DDPG_OU) {
-        const float x = __fadd_rn(__fadd_rn(st.ou[k], __fmul_rn(e.ou_theta, __fsub_rn(0.f, st.ou[k]))),
-                                  __fmul_rn(e.ou_sigma, eps[k]));
-        st.ou[k] = x;
-        a = fminf(fmaxf(__fadd_rn(tanhf(zk), x), -1.f), 1.f);
-      } else {  // PPO Gaussian (also C1's single policy)
-        a = fminf(fmaxf(__fadd_rn(tanhf(zk), __fmul_rn(e.noise_std, eps[k])), -1.f), 1.f);
+    for (int pb = 0; pb < (KA + 7) / 8; ++pb) {
+      float eps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (p.noise_mode == FIN_NOISE_PHILOX) {
+        const Normals8 nv =
+            philox_normals8_v((uint64_t)(e.env_offset + env), (uint32_t)(e.t_global + t),
+                              ((uint32_t)m << 16) | (uint32_t)(2 * pb), ((uint32_t)m << 16) | (uint32_t)(2 * pb + 1),
+                              p.noise_seed);
+        eps[0] = nv.a.x; eps[1] = nv.a.y; eps[2] = nv.a.z; eps[3] = nv.a.w;
+        eps[4] = nv.b.x; eps[5] = nv.b.y; eps[6] = nv.b.z; eps[7] = nv.b.w;
+        if (pb == 0) FIN_TR(threadIdx.x == 128 && m == 0, t, 16);
+      } else if (p.noise_mode == FIN_NOISE_SUPPLIED) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (pb * 8 + j < KA) eps[j] = __ldg(nz + pb * 8 + j);
       }
-      if (!isfinite(a)) { st.nonfinite = true; a = 0.f; }
-      st.asum[k] = p.weighted ? __fadd_rn(st.asum[k], __fmul_rn(wm, a)) : __fadd_rn(st.asum[k], a);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = pb * 8 + j;
+        if (k >= KA) break;
+        // one tanh per asset for every member kind:
+        //   SAC   a = tanh(z + std eps)
+        //   PPO   a = clip(tanh(z) + std eps)
+        //   DDPG  x = x + theta (0 - x) + sigma eps;  a = clip(tanh(z) + x)
+        const float se = __fmul_rn(e.noise_std, eps[j]);
+        const float pre = sac ? __fadd_rn(z[k], se) : z[k];
+        float post = se;
+        if (ENS && ddpg) {
+          const int ko = ENS ? k : 0;
+          post = __fadd_rn(__fadd_rn(st.ou[ko], __fmul_rn(e.ou_theta, __fsub_rn(0.f, st.ou[ko]))),
+                           __fmul_rn(e.ou_sigma, eps[j]));
+          st.ou[ko] = post;
+        }
+        const float th = tanh_f32(pre);
+        float a = sac ? th : fminf(fmaxf(__fadd_rn(th, post), -1.f), 1.f);
+        if (!isfinite(a)) { st.nonfinite = true; a = 0.f; }
+        st.asum[k] = p.weighted ? __fadd_rn(st.asum[k], __fmul_rn(wm, a)) : __fadd_rn(st.asum[k], a);
+      }
     }
   }
 
-  __device__ __forceinline__ static void finish_step(State& st, const TcParams& p, int env, int t) {
-    if (!st.live) return;
+  __device__ __forceinline__ static void finish_step(State& st, const TcParams& p, int env, int t, uint8_t* stg) {
     const EnvDev& e = p.e;
     const size_t ti = (size_t)t * e.N + env;
-    if (st.t_ep >= e.L) {  // done env without autoreset
-      st.bad = true;
-      if (p.o.reward) p.o.reward[ti] = 0.f;
-      if (p.o.done) p.o.done[ti] = 1;
-      return;
-    }
-    int a[KA], ex[KA];
+    int a[KA];
+    FIN_TR(threadIdx.x == 128, t, 17);
+    const float inv_m = 1.f / (float)p.M;   // uniform mean (R20); the weighted sum is already scaled
 #pragma unroll
     for (int k = 0; k < KA; ++k) {
-      const float abar = (p.M == 1 || p.weighted) ? st.asum[k] : __fdiv_rn(st.asum[k], (float)p.M);
+      const float abar = (!ENS || p.M == 1 || p.weighted) ? st.asum[k] : __fmul_rn(st.asum[k], inv_m);
       a[k] = rha_f32(__fmul_rn((float)e.max_trade, abar));
-      if (p.act_only && p.mean_out) p.mean_out[(size_t)env * KA + k] = abar;
+      if (st.live && p.act_only && p.mean_out) p.mean_out[(size_t)env * KA + k] = abar;
     }
     if (p.act_only) {  // fin_ensemble_act: report the action, leave the env untouched
-      if (p.o.actions) {
+      if (st.live && p.o.actions) {
 #pragma unroll
         for (int k = 0; k < KA; ++k) p.o.actions[(size_t)env * KA + k] = (int16_t)a[k];
       }
       return;
     }
-    const float* mrow = e.market + (size_t)st.d * e.row_floats;
-    double v, vn;
-    stock_transition<KA>(e, st.b, st.h, mrow, mrow + e.row_floats, a, v, vn, ex, st.oor);
-    st.t_ep += 1;
-    const bool done = st.t_ep == e.L;
-    const float r = stock_reward(e, v, vn);
-    st.rsum += (double)r;
-    if (p.o.reward) p.o.reward[ti] = r;
-    if (p.o.done) p.o.done[ti] = done ? 1 : 0;
-    if (p.o.cash) p.o.cash[ti] = st.b;
-    if (p.o.asset) p.o.asset[ti] = vn;
-    if (p.o.actions || p.o.hold) {
-#pragma unroll
-      for (int k = 0; k < KA; ++k) {
-        if (p.o.actions) p.o.actions[ti * KA + k] = (int16_t)ex[k];
-        if (p.o.hold) p.o.hold[ti * KA + k] = (int16_t)st.h[k];
-      }
+    const bool stepping = st.live && st.t_ep < e.L;
+    if (st.live && !stepping) {  // done env without autoreset: ignored
+      st.bad = true;
+      if (p.o.reward) p.o.reward[ti] = 0.f;
+      if (p.o.done) p.o.done[ti] = 1;
     }
-    metric_push(st.m, vn);
-    if (done) {
-      double em[3];
-      metric_finish(st.m, 252.0, 0.0, em);
-      if (p.o.ep_metrics && st.cnt < p.o.ep_capacity) {
-        double* dst = p.o.ep_metrics + ((size_t)st.cnt * e.N + env) * 3;
-        dst[0] = em[0]; dst[1] = em[1]; dst[2] = em[2];
-      }
-      ++st.cnt;
-      agg_episode(st.agg, em);
-      if (e.autoreset) {
-        st.b = e.cash0;
+    GroupSlots* gs = reinterpret_cast<GroupSlots*>(stg + kOffS);
+    group_apply(
+        gs, st.round, st.d, stepping, st.gtid, st.bar_id, [&](int k) { stage_row(p, k, st.gtid, stg); },
+        [&]() {
+          const double* pd = reinterpret_cast<const double*>(stg + kOffP);
+          int ex[KA];
+          double v, vn;
+          FIN_TR(threadIdx.x == 128, t, 19);
+          stock_transition<KA>(e, st.b, st.h, pd, pd + KP4, a, v, vn, ex, st.oor);
+          FIN_TR(threadIdx.x == 128, t, 20);
+          st.t_ep += 1;
+          const bool done = st.t_ep == e.L;
+          const float r = stock_reward(e, v, vn);
+          st.rsum += (double)r;
+          if (p.o.reward) p.o.reward[ti] = r;
+          if (p.o.done) p.o.done[ti] = done ? 1 : 0;
+          if (p.o.cash) p.o.cash[ti] = st.b;
+          if (p.o.asset) p.o.asset[ti] = vn;
+          if (p.o.actions || p.o.hold) {
 #pragma unroll
-        for (int k = 0; k < KA; ++k) { st.h[k] = 0; st.ou[k] = 0.f; }
-        st.t_ep = 0;
-        if (e.wadv) st.w = (st.w + 1) % e.W;
-        metric_start(st.m, e.cash0);
-      }
-    }
+            for (int k = 0; k < KA; ++k) {
+              if (p.o.actions) p.o.actions[ti * KA + k] = (int16_t)ex[k];
+              if (p.o.hold) p.o.hold[ti * KA + k] = (int16_t)st.h[k];
+            }
+          }
+          metric_push(st.m, vn);
+          FIN_TR(threadIdx.x == 128, t, 21);
+          if (done) {
+            double em[3];
+            metric_finish(st.m, 252.0, 0.0, em);
+            if (p.o.ep_metrics && st.cnt < p.o.ep_capacity) {
+              double* dst = p.o.ep_metrics + ((size_t)st.cnt * e.N + env) * 3;
+              dst[0] = em[0]; dst[1] = em[1]; dst[2] = em[2];
+            }
+            ++st.cnt;
+            agg_episode(st.agg, em);
+            if (e.autoreset) {
+              st.b = e.cash0;
+#pragma unroll
+              for (int k = 0; k < KA; ++k) st.h[k] = 0;
+#pragma unroll
+              for (int k = 0; k < KOU; ++k) st.ou[k] = 0.f;
+              st.t_ep = 0;
+              if (e.wadv) st.w = (st.w + 1) % e.W;
+              metric_start(st.m, e.cash0);
+            }
+          }
+        });
   }
 
-  __device__ __forceinline__ static void finalize(State& st, const TcParams& p, int env) {
+  __device__ __forceinline__ static void finalize(State& st, const TcParams& p, int env, int gtid, int bar_id,
+                                                  int tile) {
     const EnvDev& e = p.e;
     if (p.act_only) return;
     if (st.live) {
@@ -241,9 +344,9 @@ struct StockOps {
       int slot = -1;
       for (int m = 0; m < p.M; ++m)
         if (p.kinds[m] == FIN_DDPG_OU) slot = m;
-      if (slot >= 0) {
+      if (ENS && slot >= 0) {
 #pragma unroll
-        for (int k = 0; k < KA; ++k) e.ou[((size_t)slot * e.K + k) * e.N + env] = st.ou[k];
+        for (int k = 0; k < KOU; ++k) e.ou[((size_t)slot * e.K + k) * e.N + env] = st.ou[k];
       }
       if (p.o.ep_count) p.o.ep_count[env] = st.cnt;
       if (st.oor) set_flag(e, FIN_FLAG_ACTION_RANGE);
@@ -251,31 +354,34 @@ struct StockOps {
       if (st.nonfinite) set_flag(e, FIN_FLAG_NONFINITE);
     }
     st.agg.s[FIN_AGG_SUM_REWARD] = st.rsum;
-    if (p.o.agg_partial) agg_group_write(st.agg, p.o.agg_partial + (size_t)blockIdx.x * FIN_AGG_LEN,
-                                         threadIdx.x - tc::kEnvWarp0 * 32, 1);
-  }
-};
-
-// Binds the env ops to one network plan (build_obs needs the plan's padded width).
-template <int KA, int IA, class Plan>
-struct StockOpsP : StockOps<KA, IA> {
-  using Base = StockOps<KA, IA>;
-  static_assert(Base::IN <= Plan::kIn, "observation wider than the network input");
-  __device__ __forceinline__ static void build_obs(typename Base::State& st, const TcParams& p, int env, int row,
-                                                   int t, uint32_t xa) {
-    Base::template build_obs_t<Plan>(st, p, env, row, t, xa);
+    if (p.o.agg_partial)
+      agg_group_write(st.agg, p.o.agg_partial + ((size_t)blockIdx.x * (blockDim.x / 128) + tile) * FIN_AGG_LEN, gtid,
+                      bar_id, tile);
   }
 };
 
 // ---------------------------------------------------------------- K7 probe
-template <class Plan>
+// Obs = StockObs<..> for the factored stock nets (X = the private columns of x, the
+// shared columns enter through z1s), void for the crypto Q-net (X = x).
+template <class Plan, class Obs>
 struct ProbeOps {
+  static constexpr int kStageBytes = 16;
+  static constexpr bool kFactored = !std::is_void<Obs>::value;
   struct State {
     int b;
   };
+  __device__ __forceinline__ static int col_of(int j) {
+    if constexpr (kFactored) return j < Obs::kEnv ? Obs::env_col(j) : -1;
+    else return j;
+  }
   __device__ __forceinline__ static void init(State& st, const TcParams& p, int env, int row) { st.b = env; }
-  __device__ __forceinline__ static void build_obs(State& st, const TcParams& p, int env, int row, int t,
-                                                   uint32_t xa) {
+  __device__ __forceinline__ static void stage(State&, const TcParams&, int, int, int, uint8_t*, int) {}
+  __device__ __forceinline__ static const float* l1_addend(State& st, const TcParams& p, int m, uint8_t*) {
+    if constexpr (kFactored) return st.b < p.B ? p.z1s + (size_t)st.b * Plan::kHid : nullptr;
+    else return nullptr;
+  }
+  __device__ __forceinline__ static void build_obs(State& st, const TcParams& p, int env, int row, int t, int m,
+                                                   uint32_t xa, uint8_t*) {
     constexpr int KT8 = Plan::kIn / 8;
     const bool live = st.b < p.B;
     const uint16_t* x = p.x_in + (size_t)st.b * p.in_dim;
@@ -284,12 +390,12 @@ struct ProbeOps {
       uint32_t w4[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int i0 = 8 * c + 2 * j;
-        const uint32_t lo = (live && i0 < p.in_dim) ? x[i0] : 0u;
-        const uint32_t hi = (live && i0 + 1 < p.in_dim) ? x[i0 + 1] : 0u;
+        const int c0 = col_of(8 * c + 2 * j), c1 = col_of(8 * c + 2 * j + 1);
+        const uint32_t lo = (live && c0 >= 0 && c0 < p.in_dim) ? x[c0] : 0u;
+        const uint32_t hi = (live && c1 >= 0 && c1 < p.in_dim) ? x[c1] : 0u;
         w4[j] = lo | (hi << 16);
       }
-      sm100::st_shared_v4(xa + tc::cm_off(row, c, KT8), w4[0], w4[1], w4[2], w4[3]);
+      tc::sts128(xa + tc::cm_off(row, c, KT8), w4[0], w4[1], w4[2], w4[3]);
     }
   }
   __device__ __forceinline__ static uint16_t* hidden_ptr(State& st, const TcParams& p, int env, int t, int m, int l,
@@ -302,36 +408,55 @@ struct ProbeOps {
     if (st.b >= p.B) return;
     for (int k = 0; k < p.out_dim; ++k) p.z_out[(size_t)st.b * p.out_dim + k] = z[k];
   }
-  __device__ __forceinline__ static void finish_step(State&, const TcParams&, int, int) {}
-  __device__ __forceinline__ static void finalize(State&, const TcParams&, int) {}
+  __device__ __forceinline__ static void finish_step(State&, const TcParams&, int, int, uint8_t*) {}
+  __device__ __forceinline__ static void finalize(State&, const TcParams&, int, int, int, int) {}
 };
-
-template <class Plan, bool RES, class Ops>
-cudaError_t launch_tc(const TcParams& p, int n_tiles, cudaStream_t s) {
-  using S = tc::Smem<Plan, RES>;
-  auto kern = tc::k_tc_rollout<Plan, RES, Ops>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
-  if (err != cudaSuccess) return err;
-  kern<<<n_tiles, tc::kThreads, S::kTotal, s>>>(p);
-  return cudaGetLastError();
-}
 
 }  // namespace
 
 namespace fin {
 
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+// Tiles per CTA for a launch: two tiles share every streamed weight stage (halving
+// L2 weight traffic per env-step and doubling the env warps per SM) when there are
+// more tiles than SMs and the members' biases still fit in shared memory; otherwise
+// one tile per CTA (small N is latency-bound: use as many SMs as there are tiles).
+template <class Plan, bool RES, class Ops>
+cudaError_t launch_auto(const TcParams& p, int n_envs, int* tiles, cudaStream_t s) {
+  const int n_tiles = (n_envs + tc::kTileM - 1) / tc::kTileM;
+  if (n_tiles > num_sms() && p.M <= tc::Smem<Plan, RES, 2, Ops>::max_members()) {
+    *tiles = 2;
+    return tc::launch<Plan, RES, 2, Ops>(p, n_envs, s);
+  }
+  *tiles = 1;
+  return tc::launch<Plan, RES, 1, Ops>(p, n_envs, s);
+}
+
 // net: 0 = PlanStockC1 (K=30, I=8), 1 = PlanStockSmall (K=4, I=4)
-cudaError_t launch_stock_rollout(int net, const tc::TcParams& p, int n_tiles, cudaStream_t s) {
-  if (net == 0) return launch_tc<PlanStockC1, false, StockOpsP<30, 8, PlanStockC1>>(p, n_tiles, s);
-  if (net == 1) return launch_tc<PlanStockSmall, true, StockOpsP<4, 4, PlanStockSmall>>(p, n_tiles, s);
+cudaError_t launch_stock_rollout(int net, const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s) {
+  const bool single = p.M == 1 && p.kinds[0] != FIN_DDPG_OU;
+  if (net == 0 && single)
+    return launch_auto<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false>>(p, n_envs, tiles, s);
+  if (net == 0) return launch_auto<PlanStockC1, false, StockOps<30, 8, PlanStockC1, true>>(p, n_envs, tiles, s);
+  if (net == 1) return launch_auto<PlanStockSmall, true, StockOps<4, 4, PlanStockSmall, true>>(p, n_envs, tiles, s);
   return cudaErrorInvalidValue;
 }
 
 // net: 0 = PlanStockC1, 1 = PlanStockSmall, 2 = PlanCrypto
-cudaError_t launch_mlp_probe(int net, const tc::TcParams& p, int n_tiles, cudaStream_t s) {
-  if (net == 0) return launch_tc<PlanStockC1, false, ProbeOps<PlanStockC1>>(p, n_tiles, s);
-  if (net == 1) return launch_tc<PlanStockSmall, true, ProbeOps<PlanStockSmall>>(p, n_tiles, s);
-  if (net == 2) return launch_tc<PlanCrypto, true, ProbeOps<PlanCrypto>>(p, n_tiles, s);
+cudaError_t launch_mlp_probe(int net, const tc::TcParams& p, int n_rows, cudaStream_t s) {
+  int tiles = 0;
+  if (net == 0) return launch_auto<PlanStockC1, false, ProbeOps<PlanStockC1, ObsC1>>(p, n_rows, &tiles, s);
+  if (net == 1) return launch_auto<PlanStockSmall, true, ProbeOps<PlanStockSmall, ObsSmall>>(p, n_rows, &tiles, s);
+  if (net == 2) return launch_auto<PlanCrypto, true, ProbeOps<PlanCrypto, void>>(p, n_rows, &tiles, s);
   return cudaErrorInvalidValue;
 }
 

@@ -1,23 +1,28 @@
 // rollout_tc.cuh -- the warp-specialised tcgen05 rollout kernel template (K3/K5/K7).
 //
-// One CTA owns a tile of 128 SubEnvs (UMMA M = 128: TMEM lane r <-> env r of the
-// tile) for all T steps; env state stays in registers.  Per step and per
+// One CTA owns TILES tiles of 128 SubEnvs (UMMA M = 128: TMEM lane r <-> env r of
+// a tile) for all T steps; env state stays in registers.  Per step and per
 // ensemble member the policy MLP (BASELINE configs[1..3])
 // runs as three tcgen05.mma GEMMs  D = A * W^T  with A (activations, bf16,
 // K-major core-matrix layout in smem) and W (bf16 weights, streamed by 1-D bulk
-// TMA into a ring of smem stages, or resident) accumulating fp32 in TMEM.
+// TMA into a ring of smem stages, or resident) accumulating fp32 in TMEM.  Every
+// streamed weight stage feeds the MMAs of all TILES tiles, so L2 weight traffic
+// per env-step is divided by TILES.
 //
-// Warp roles (192 threads):
-//   warp 0       producer: streams weight stages global(L2) -> smem ring (cp.async.bulk)
-//   warp 1       TMEM allocator + MMA issuer (one elected lane)
-//   warps 2..5   "env" warpgroup: observation build, TMEM epilogues (bias, ReLU,
-//                bf16), action sampling / ensemble averaging, the env transition
-//                (trade, reward, done / reset) and online metrics -- thread r of
-//                the group owns env r (warp w reads TMEM lanes 32*(w%4)..+31).
+// Warp roles (64 + 128 * TILES threads):
+//   warp 0        producer: streams weight stages global(L2) -> smem ring (cp.async.bulk)
+//   warp 1        TMEM allocator + MMA issuer (one elected lane)
+//   warps 2..     one "env" warpgroup per tile: per-tile staging of the shared market
+//                 row, observation rows, TMEM epilogues (bias, ReLU, bf16), action
+//                 sampling / ensemble averaging, the env transition (trade, reward,
+//                 done / reset) and online metrics -- thread r of a warpgroup owns env
+//                 r of its tile (warp w reads TMEM lanes 32*(w%4)..+31).
 // Synchronisation (mbarriers): w_full / w_empty per ring slot (TMA <-> MMA),
-// a_full (env -> MMA: A operand written, TMEM columns free), d_full (MMA commit ->
-// env: accumulator ready).  Layer l+1's MMAs start when the epilogue of layer l
-// has written its activations; the producer prefetches across layers and steps.
+// a_full (all env threads -> MMA: A operands written, TMEM columns free), d_full
+// (MMA commit -> env: accumulators ready).  A tile's A buffer holds the
+// observation for layer 1 and is overwritten by the hidden activations (the
+// layer's MMAs have completed when d_full fires), so the observation is rebuilt
+// for every ensemble member from the per-step staging area.
 #pragma once
 #include "fin_internal.cuh"
 #include "sm100.cuh"
@@ -26,9 +31,8 @@
 namespace tc {
 
 constexpr int kTileM = 128;
-constexpr int kThreads = 192;
-constexpr int kEnvWarp0 = 2;
 constexpr int kRing = 4;
+constexpr int kSmemLimit = 232448;  // 227 KB per CTA
 
 struct TcParams {
   EnvDev e;
@@ -46,68 +50,91 @@ struct TcParams {
   // fin_ensemble_act: compute the (ensemble) action only, no env transition
   int32_t act_only;
   float* mean_out;                        // [N][K] averaged continuous action
-  uint16_t* hid_out;                      // bf16 hidden activations (probe [B][2][HID]; rollout [T][M][N][2][HID])
+  uint16_t* hid_out;                      // bf16 hidden activations (probe [B][2][HID])
+  const float* z1s;                       // factored layer 1: shared term [M][rows][HID] (or probe [B][HID])
+  int32_t z1s_rows;
+  unsigned long long* trace;              // debug: clock64 timeline of block 0 ([T][16]) or null
   // K7 probe
   const uint16_t* x_in;
   float* z_out;
   int32_t B, in_dim, out_dim;
 };
 
+// debug timeline (fin_debug_trace): block 0 only, one slot per event
+#define FIN_TR(cond, t, slot)                                                                  \
+  do {                                                                                         \
+    if (p.trace && blockIdx.x == 0 && (cond)) p.trace[(size_t)(t) * 32 + (slot)] = clock64(); \
+  } while (0)
+
 __device__ __forceinline__ uint32_t cm_off(int r, int kchunk, int kt8) {
   return (uint32_t)(((r >> 3) * kt8 + kchunk) * 128 + (r & 7) * 16);
 }
 
-// Shared-memory carve-up (dynamic smem, 1024-B aligned base).
-constexpr int kSmemBudget = 232448 - 2048;  // 227 KB per CTA, minus static smem of the env ops
+// plain (non-volatile, no memory clobber) 16-byte shared store: ordered by the
+// proxy fence / barriers that follow, free to be scheduled with the loads before it
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d));
+}
 
-template <class Plan, bool RESIDENT>
+// Shared-memory carve-up (dynamic smem, 1024-B aligned base).  The bias region is
+// sized for the launch's member count.
+template <class Plan, bool RESIDENT, int TILES, class Ops>
 struct Smem {
-  static constexpr int kX = kTileM * Plan::kIn * 2;
-  static constexpr int kH = kTileM * Plan::kHid * 2;
-  static constexpr int kBias = FIN_MAX_MEMBERS * Plan::kBiasFloats * 4;
-  static constexpr int kFree = kSmemBudget - kX - kH - kBias - 256;
+  static constexpr int kA = kTileM * (Plan::kIn > Plan::kHid ? Plan::kIn : Plan::kHid) * 2;  // per tile
+  static constexpr int kFixed = TILES * kA + TILES * Ops::kStageBytes + 512;  // + barriers, flags
+  static constexpr int kBiasPerMember = Plan::kBiasFloats * 4;
+  static constexpr int kStaticSmem = 512;  // agg_group_write scratch etc.
   // members whose weights fit resident in shared memory (resident plans only)
-  static constexpr int kResMembers = RESIDENT ? (kFree / Plan::kMemberBytes < FIN_MAX_MEMBERS
-                                                     ? kFree / Plan::kMemberBytes : FIN_MAX_MEMBERS)
-                                              : FIN_MAX_MEMBERS;
-  static_assert(!RESIDENT || kResMembers >= 1, "resident network does not fit in shared memory");
-  static constexpr int kW = RESIDENT ? Plan::kMemberBytes * kResMembers : kRing * Plan::kStageBytes;
-  static constexpr int oX = 0, oH = oX + kX, oW = oH + kH, oBias = oW + kW, oBar = oBias + kBias;
-  static constexpr int kBars = 2 * kRing + 2;
-  static constexpr int kTotal = oBar + kBars * 8 + 16;
+  static constexpr int kResMembers =
+      RESIDENT ? ((kSmemLimit - kStaticSmem - kFixed) / (Plan::kMemberBytes + kBiasPerMember) < FIN_MAX_MEMBERS
+                      ? (kSmemLimit - kStaticSmem - kFixed) / (Plan::kMemberBytes + kBiasPerMember)
+                      : FIN_MAX_MEMBERS)
+               : FIN_MAX_MEMBERS;
+  __host__ __device__ static constexpr int w_bytes(int M) {
+    return RESIDENT ? Plan::kMemberBytes * M : kRing * Plan::kStageBytes;
+  }
+  __host__ __device__ static constexpr int total(int M) { return kFixed + w_bytes(M) + M * kBiasPerMember; }
+  __host__ __device__ static constexpr int max_members() {
+    return (kSmemLimit - kStaticSmem - kFixed - w_bytes(0)) / ((RESIDENT ? Plan::kMemberBytes : 0) + kBiasPerMember);
+  }
 };
 
 // ---------------------------------------------------------------------------------
 // The kernel.  Ops supplies the env-side behaviour (see rollout_stock.cu etc.):
 //   struct Ops {
+//     static constexpr int kStageBytes;             // per-tile staging area
 //     struct State;
-//     __device__ static void init(State&, const TcParams&, int env, int row);
-//     __device__ static void build_obs(State&, const TcParams&, int env, int row, int t, uint32_t x_addr);
-//     __device__ static void consume(State&, const TcParams&, int env, int t, int m, const float* z);
-//     __device__ static uint16_t* hidden_ptr(State&, const TcParams&, int env, int t, int m, int l, int hid);
-//     __device__ static void finish_step(State&, const TcParams&, int env, int t);
-//     __device__ static void finalize(State&, const TcParams&, int env);
+//     init(State&, p, env, row)
+//     stage(State&, p, env, row, t, stage_ptr, bar_id)   per step, all 128 threads of a tile
+//     build_obs(State&, p, env, row, t, m, x_addr, stage_ptr)
+//     hidden_ptr(State&, p, env, t, m, l, hid) -> uint16_t* or nullptr
+//     consume(State&, p, env, t, m, const float* z)
+//     finish_step(State&, p, env, t, stage_ptr)
+//     finalize(State&, p, env, group_tid, bar_id)
 //   };
-template <class Plan, bool RESIDENT, class Ops>
-__global__ void __launch_bounds__(kThreads, 1) k_tc_rollout(const __grid_constant__ TcParams p) {
-  using S = Smem<Plan, RESIDENT>;
+template <class Plan, bool RESIDENT, int TILES, class Ops>
+__global__ void __launch_bounds__(64 + 128 * TILES, 1) k_tc_rollout(const __grid_constant__ TcParams p) {
+  using S = Smem<Plan, RESIDENT, TILES, Ops>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sX = smem + S::oX;
-  uint8_t* sH = smem + S::oH;
-  uint8_t* sW = smem + S::oW;
-  float* sBias = reinterpret_cast<float*>(smem + S::oBias);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::oBar);
+  const int M = p.M;
+  const int T = p.T;
+  constexpr int NS = Plan::kStages;
+  constexpr uint32_t kTmemCols = (TILES * Plan::kHid <= 128) ? 128 : (TILES * Plan::kHid <= 256 ? 256 : 512);
+  static_assert(TILES * Plan::kHid <= 512, "TMEM holds 512 fp32 columns");
+
+  uint8_t* sA = smem;                                           // TILES x kA
+  uint8_t* sStage = sA + TILES * S::kA;                         // TILES x Ops::kStageBytes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + TILES * Ops::kStageBytes);
   uint64_t* w_full = bars;
   uint64_t* w_empty = bars + kRing;
   uint64_t* a_full = bars + 2 * kRing;
   uint64_t* d_full = bars + 2 * kRing + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::oBar + S::kBars * 8);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kRing + 2);
+  uint8_t* sW = reinterpret_cast<uint8_t*>(bars) + 512;
+  float* sBias = reinterpret_cast<float*>(sW + S::w_bytes(M));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int M = p.M;
-  const int T = p.T;
-  constexpr int NS = Plan::kStages;
 
   // ---- one-time setup
   for (int j = threadIdx.x; j < M * Plan::kBiasFloats; j += blockDim.x) {
@@ -119,12 +146,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_rollout(const __grid_constan
       sm100::mbar_init(&w_full[s], 1);
       sm100::mbar_init(&w_empty[s], 1);
     }
-    sm100::mbar_init(a_full, 4 * 32);
+    sm100::mbar_init(a_full, 128 * TILES);
     sm100::mbar_init(d_full, 1);
     sm100::fence_mbar_init();
   }
   if (warp == 1) {
-    sm100::tmem_alloc(tmem_slot, Plan::kHid <= 128 ? 128 : 256);
+    sm100::tmem_alloc(tmem_slot, kTmemCols);
     sm100::tmem_relinquish();
   }
   sm100::tc_fence_before();
@@ -161,18 +188,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_rollout(const __grid_constan
     // ============================ MMA issuer ============================
     if (lane == 0) {
       uint32_t it = 0, a_use = 0;
-      if (RESIDENT) {
-        sm100::mbar_wait(&w_full[0], 0);
-      }
-      const uint32_t xa = sm100::smem_u32(sX), ha = sm100::smem_u32(sH), wa = sm100::smem_u32(sW);
+      if (RESIDENT) sm100::mbar_wait(&w_full[0], 0);
+      const uint32_t aa = sm100::smem_u32(sA), wa = sm100::smem_u32(sW);
       for (int t = 0; t < T; ++t) {
         for (int m = 0; m < M; ++m) {
 #pragma unroll 1
           for (int l = 0; l < 3; ++l) {
             sm100::mbar_wait(a_full, a_use & 1);
             ++a_use;
+            FIN_TR(m == 0, t, 9 + 2 * l);
             sm100::tc_fence_after();
-            const uint32_t a_base = (l == 0) ? xa : ha;
             const uint32_t a_sbo = (uint32_t)(Plan::kdim(l) / 8) * 128u;
             const uint32_t idesc = sm100::make_idesc_bf16(kTileM, Plan::nrows(l));
             for (int s = Plan::first_stage(l); s < Plan::first_stage(l) + Plan::nstages(l); ++s) {
@@ -187,10 +212,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_rollout(const __grid_constan
               }
               const int j0 = Plan::j0_of(s), nks = Plan::nks_of(s);
               const uint32_t b_sbo = (uint32_t)(nks * 2) * 128u;  // Kt/8 * 128 with Kt = 16 nks
-              for (int j = 0; j < nks; ++j) {
-                const uint64_t ad = sm100::make_sdesc(a_base + (uint32_t)(j0 + j) * 256u, 128u, a_sbo);
-                const uint64_t bd = sm100::make_sdesc(b_base + (uint32_t)j * 256u, 128u, b_sbo);
-                sm100::mma_bf16(tmem, ad, bd, idesc, (j0 + j) > 0 ? 1u : 0u);
+#pragma unroll
+              for (int tile = 0; tile < TILES; ++tile) {
+                const uint32_t a_base = aa + (uint32_t)(tile * S::kA);
+                const uint32_t d_tmem = tmem + (uint32_t)(tile * Plan::kHid);
+                for (int j = 0; j < nks; ++j) {
+                  const uint64_t ad = sm100::make_sdesc(a_base + (uint32_t)(j0 + j) * 256u, 128u, a_sbo);
+                  const uint64_t bd = sm100::make_sdesc(b_base + (uint32_t)j * 256u, 128u, b_sbo);
+                  sm100::mma_bf16(d_tmem, ad, bd, idesc, (j0 + j) > 0 ? 1u : 0u);
+                }
               }
               if (!RESIDENT) {
                 sm100::mma_commit(&w_empty[it % kRing]);
@@ -198,65 +228,96 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_rollout(const __grid_constan
               }
             }
             sm100::mma_commit(d_full);
+            FIN_TR(m == 0, t, 10 + 2 * l);
           }
         }
       }
     }
     __syncwarp();
   } else {
-    // ============================ env warpgroup ============================
+    // ============================ env warpgroups ============================
+    const int tile = (warp - 2) >> 2;
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;          // env row of the tile == TMEM lane
-    const int env = blockIdx.x * kTileM + row;
-    const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
-    const uint32_t xa = sm100::smem_u32(sX), ha = sm100::smem_u32(sH);
+    const int gtid = (warp - 2 - tile * 4) * 32 + lane;   // thread index within the tile's warpgroup
+    const int env = (blockIdx.x * TILES + tile) * kTileM + row;
+    const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tile * Plan::kHid);
+    const uint32_t xa = sm100::smem_u32(sA + tile * S::kA);
+    uint8_t* stg = sStage + tile * Ops::kStageBytes;
+    const int bar_id = 1 + tile;
     typename Ops::State st;
     Ops::init(st, p, env, row);
     uint32_t d_use = 0;
     for (int t = 0; t < T; ++t) {
-      Ops::build_obs(st, p, env, row, t, xa);
-      sm100::fence_proxy_async_smem();
-      sm100::tc_fence_before();
-      sm100::mbar_arrive(a_full);
+      FIN_TR(row == 0 && tile == 0, t, 0);
+      Ops::stage(st, p, env, gtid, t, stg, bar_id);
       for (int m = 0; m < M; ++m) {
+        Ops::build_obs(st, p, env, row, t, m, xa, stg);
+        sm100::fence_proxy_async_smem();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(a_full);
+        FIN_TR(row == 0 && tile == 0 && m == 0, t, 1);
         const float* bias = sBias + m * Plan::kBiasFloats;
-        // hidden layers: D -> +bias -> ReLU -> bf16 -> H (K-major core matrices)
+        // hidden layers: D -> +bias -> ReLU -> bf16 -> A (K-major core matrices)
 #pragma unroll 1
         for (int l = 0; l < 2; ++l) {
           sm100::mbar_wait(d_full, d_use & 1);
           ++d_use;
+          FIN_TR(row == 0 && tile == 0 && m == 0, t, 2 + 2 * l);
           sm100::tc_fence_after();
           const float* bl = bias + l * Plan::kHid;
+          // factored layer 1: + shared-input term of the env's day (smem or global row)
+          const float* add = l == 0 ? Ops::l1_addend(st, p, m, stg) : nullptr;
           // debug / parity log of the bf16 hidden activations (teacher-forced layer checks)
           uint4* hlog = reinterpret_cast<uint4*>(Ops::hidden_ptr(st, p, env, t, m, l, Plan::kHid));
 #pragma unroll 1
           for (int c = 0; c < Plan::kHid / 32; ++c) {
             uint32_t v[32];
             sm100::tmem_ld32(t_lane + (uint32_t)(c * 32), v);
+            // addend b (+ z1s for the factored layer 1), 128-bit broadcast loads, issued
+            // while the TMEM load is in flight
+            float ad[32];
+            const float4* b4 = reinterpret_cast<const float4*>(bl + c * 32);
+#pragma unroll
+            for (int q4 = 0; q4 < 8; ++q4) {
+              const float4 x = b4[q4];
+              ad[4 * q4] = x.x; ad[4 * q4 + 1] = x.y; ad[4 * q4 + 2] = x.z; ad[4 * q4 + 3] = x.w;
+            }
+            if (add) {
+              const float4* a4 = reinterpret_cast<const float4*>(add + c * 32);
+#pragma unroll
+              for (int q4 = 0; q4 < 8; ++q4) {
+                const float4 y = a4[q4];
+                ad[4 * q4] += y.x; ad[4 * q4 + 1] += y.y; ad[4 * q4 + 2] += y.z; ad[4 * q4 + 3] += y.w;
+              }
+            }
             sm100::tmem_wait_ld();
             uint32_t pk[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              const float a0 = fmaxf(__uint_as_float(v[2 * j]) + bl[c * 32 + 2 * j], 0.f);
-              const float a1 = fmaxf(__uint_as_float(v[2 * j + 1]) + bl[c * 32 + 2 * j + 1], 0.f);
+              const float a0 = fmaxf(__uint_as_float(v[2 * j]) + ad[2 * j], 0.f);
+              const float a1 = fmaxf(__uint_as_float(v[2 * j + 1]) + ad[2 * j + 1], 0.f);
               pk[j] = sm100::pack_bf16(a0, a1);
             }
 #pragma unroll
             for (int g = 0; g < 4; ++g)
-              sm100::st_shared_v4(ha + cm_off(row, c * 4 + g, Plan::kHid / 8), pk[4 * g], pk[4 * g + 1],
-                                  pk[4 * g + 2], pk[4 * g + 3]);
+              sts128(xa + cm_off(row, c * 4 + g, Plan::kHid / 8), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2],
+                     pk[4 * g + 3]);
             if (hlog) {
 #pragma unroll
-              for (int g = 0; g < 4; ++g) hlog[c * 4 + g] = make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+              for (int g = 0; g < 4; ++g)
+                hlog[c * 4 + g] = make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
             }
           }
           sm100::fence_proxy_async_smem();
           sm100::tc_fence_before();
           sm100::mbar_arrive(a_full);
+          FIN_TR(row == 0 && tile == 0 && m == 0, t, 3 + 2 * l);
         }
         // output layer
         sm100::mbar_wait(d_full, d_use & 1);
         ++d_use;
+        FIN_TR(row == 0 && tile == 0 && m == 0, t, 6);
         sm100::tc_fence_after();
         float z[Plan::kOut];
 #pragma unroll
@@ -268,18 +329,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_rollout(const __grid_constan
           for (int j = 0; j < 16; ++j) z[c * 16 + j] = __uint_as_float(v[j]) + bias[2 * Plan::kHid + c * 16 + j];
         }
         sm100::tc_fence_before();
-        if (m + 1 < M) sm100::mbar_arrive(a_full);   // X stays valid for the next member
         Ops::consume(st, p, env, t, m, z);
+        FIN_TR(row == 0 && tile == 0 && m == 0, t, 7);
       }
-      Ops::finish_step(st, p, env, t);
+      Ops::finish_step(st, p, env, t, stg);
+      FIN_TR(row == 0 && tile == 0, t, 8);
     }
-    Ops::finalize(st, p, env);
+    Ops::finalize(st, p, env, gtid, bar_id, tile);
   }
   __syncthreads();
   if (warp == 1) {
     sm100::tc_fence_after();
-    sm100::tmem_dealloc(tmem, Plan::kHid <= 128 ? 128 : 256);
+    sm100::tmem_dealloc(tmem, kTmemCols);
   }
+}
+
+template <class Plan, bool RESIDENT, int TILES, class Ops>
+cudaError_t launch(const TcParams& p, int n_envs, cudaStream_t s) {
+  using Sm = Smem<Plan, RESIDENT, TILES, Ops>;
+  auto kern = k_tc_rollout<Plan, RESIDENT, TILES, Ops>;
+  const int bytes = Sm::total(p.M);
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (err != cudaSuccess) return err;
+  const int per_cta = kTileM * TILES;
+  kern<<<(n_envs + per_cta - 1) / per_cta, 64 + 128 * TILES, bytes, s>>>(p);
+  return cudaGetLastError();
 }
 
 }  // namespace tc

@@ -55,10 +55,33 @@ __host__ __device__ inline int tc_cm_offset(int n, int k, int kt) {
   return ((n / 8) * (kt / 8) + k / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
 }
 
+// Stock observation split ("layer-1 factorisation").  The stock
+// observation x = [b/b0, close_norm_d (K), h/max_trade (K), features_d (I*K)]
+// has 1 + K env-private entries (cash, holdings) and K + I*K entries that depend
+// only on the market day d.  Layer 1 is computed as
+//     z1 = W1_env x_env + z1s[d] + b1,   z1s[d] = W1_shared x_shared(d)
+// with W1_env = W1's private columns (a tcgen05 GEMM with K = 1 + K padded to 16) and
+// z1s precomputed once per rollout for every market day (float64 accumulation,
+// rounded once to fp32).  The result is the same linear map; only the rounding
+// order differs, inside the fp32 accumulation bound of the layered parity check.
+template <int KA, int IA>
+struct StockObs {
+  static constexpr int kIn = 1 + 2 * KA + IA * KA;      // 301 for C1
+  static constexpr int kEnv = 1 + KA;                   // private entries
+  static constexpr int kEnvPad = (kEnv + 15) / 16 * 16;  // UMMA K multiple
+  static constexpr int kShared = kIn - kEnv;             // 270 for C1
+  // full-observation column of private entry j (0 = cash, 1 + k = holding k)
+  __host__ __device__ static constexpr int env_col(int j) { return j == 0 ? 0 : KA + j; }
+  // full-observation column of shared entry s (close_norm first, then the features)
+  __host__ __device__ static constexpr int shared_col(int s) { return s < KA ? 1 + s : 1 + 2 * KA + (s - KA); }
+};
+
 // The network shapes compiled into libfinenv.so (fin_policy_create rejects others).
-//   stock C1 policy  301-256-256-30  -> (304, 256, 32)
-//   stock small test  25-128-128-4   -> ( 32, 128, 16)   (K = 4 assets, I = 4: C0-shaped env)
-//   crypto C3 Q-net  103-128-128-3   -> (112, 128, 16)
-using PlanStockC1 = TcPlan<304, 256, 32, 16384>;
-using PlanStockSmall = TcPlan<32, 128, 16, 16384>;
+//   stock C1 policy  301-256-256-30  -> factored layer 1 K = 32 (31 private inputs), (32, 256, 32)
+//   stock small test  25-128-128-4   -> factored layer 1 K = 16 (5 private inputs),   (16, 128, 16)
+//   crypto C3 Q-net  103-128-128-3   -> (112, 128, 16)   (every input is read from the step's row)
+using ObsC1 = StockObs<30, 8>;
+using ObsSmall = StockObs<4, 4>;
+using PlanStockC1 = TcPlan<ObsC1::kEnvPad, 256, 32, 16384>;
+using PlanStockSmall = TcPlan<ObsSmall::kEnvPad, 128, 16, 16384>;
 using PlanCrypto = TcPlan<112, 128, 16, 32768>;

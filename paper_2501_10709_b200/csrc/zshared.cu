@@ -1,0 +1,77 @@
+// zshared.cu -- the shared part of layer 1 for the factored stock policy:
+//     z1s[r][n] = sum_s W1_shared[n][s] * q(x_shared(r))[s]
+// for every market day r (rollouts) or every probe row r (fin_mlp_forward), in
+// float64 (bf16 x bf16 products are exact in float64), rounded once to fp32.
+// One CTA per row: the row's shared inputs are converted to bf16 once into shared
+// memory, then thread n accumulates output n over the transposed weights (coalesced).
+#include <cuda_bf16.h>
+
+#include "fin_internal.cuh"
+#include "tc_plan.cuh"
+
+namespace {
+
+template <class Obs>
+__device__ __forceinline__ float market_shared_value(const float* mrow, int kp, int s) {
+  constexpr int KA = (Obs::kEnv - 1);
+  // close_norm (channel 1) for s < K, then indicator-major features (channel 2 + j / K)
+  if (s < KA) return mrow[kp + s];
+  const int j = s - KA;
+  return mrow[(2 + j / KA) * kp + (j % KA)];
+}
+
+template <class Obs>
+__global__ void k_z1s_market(const float* __restrict__ w1s_t /*[S][H]*/, int H, const float* __restrict__ market,
+                             int row_floats, int kp, float* __restrict__ z1s /*[rows][H]*/) {
+  __shared__ double xs[Obs::kShared];
+  const int r = blockIdx.x;
+  const float* mrow = market + (size_t)r * row_floats;
+  for (int s = threadIdx.x; s < Obs::kShared; s += blockDim.x)
+    xs[s] = (double)__bfloat162float(__float2bfloat16_rn(market_shared_value<Obs>(mrow, kp, s)));
+  __syncthreads();
+  for (int n = threadIdx.x; n < H; n += blockDim.x) {
+    double acc = 0.0;
+    for (int s = 0; s < Obs::kShared; ++s) acc = fma((double)w1s_t[(size_t)s * H + n], xs[s], acc);
+    z1s[(size_t)r * H + n] = (float)acc;
+  }
+}
+
+template <class Obs>
+__global__ void k_z1s_probe(const float* __restrict__ w1s_t, int H, const uint16_t* __restrict__ x, int in_dim,
+                            float* __restrict__ z1s) {
+  __shared__ double xs[Obs::kShared];
+  const int r = blockIdx.x;
+  for (int s = threadIdx.x; s < Obs::kShared; s += blockDim.x) {
+    const int col = Obs::shared_col(s);
+    const uint16_t bits = col < in_dim ? x[(size_t)r * in_dim + col] : (uint16_t)0;
+    xs[s] = (double)__uint_as_float((uint32_t)bits << 16);
+  }
+  __syncthreads();
+  for (int n = threadIdx.x; n < H; n += blockDim.x) {
+    double acc = 0.0;
+    for (int s = 0; s < Obs::kShared; ++s) acc = fma((double)w1s_t[(size_t)s * H + n], xs[s], acc);
+    z1s[(size_t)r * H + n] = (float)acc;
+  }
+}
+
+}  // namespace
+
+namespace fin {
+
+// net 0 = C1 (K=30, I=8), net 1 = small (K=4, I=4)
+cudaError_t launch_z1s_market(int net, const float* w1s_t, int H, const EnvDev& e, float* z1s, cudaStream_t s) {
+  if (net == 0) k_z1s_market<ObsC1><<<e.rows, 256, 0, s>>>(w1s_t, H, e.market, e.row_floats, e.kp, z1s);
+  else if (net == 1) k_z1s_market<ObsSmall><<<e.rows, 128, 0, s>>>(w1s_t, H, e.market, e.row_floats, e.kp, z1s);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_z1s_probe(int net, const float* w1s_t, int H, const uint16_t* x, int B, int in_dim, float* z1s,
+                             cudaStream_t s) {
+  if (net == 0) k_z1s_probe<ObsC1><<<B, 256, 0, s>>>(w1s_t, H, x, in_dim, z1s);
+  else if (net == 1) k_z1s_probe<ObsSmall><<<B, 128, 0, s>>>(w1s_t, H, x, in_dim, z1s);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+}  // namespace fin

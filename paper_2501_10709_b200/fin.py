@@ -44,7 +44,7 @@ FIN_AGG_LEN = 8
 EXPORTS = ("fin_env_create", "fin_env_reset", "fin_env_step", "fin_env_get_state", "fin_env_set_state",
            "fin_env_check", "fin_env_destroy", "fin_policy_create", "fin_policy_destroy", "fin_rollout",
            "fin_rollout_actions", "fin_ensemble_act", "fin_episode_metrics", "fin_mlp_forward",
-           "fin_philox_normals", "fin_last_error", "fin_abi_version", "fin_device_check")
+           "fin_philox_normals", "fin_last_error", "fin_abi_version", "fin_device_check", "fin_debug_trace")
 
 
 class FinError(RuntimeError):
@@ -98,6 +98,7 @@ _sig = {
     "fin_last_error": ([], C.c_char_p),
     "fin_abi_version": ([], C.c_int),
     "fin_device_check": ([C.c_int32], C.c_int),
+    "fin_debug_trace": ([_P], C.c_int),
 }
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_lib, _name)
@@ -218,6 +219,12 @@ def fin_abi_version() -> int:
 
 def fin_device_check(ordinal: int = 0) -> None:
     _check(_lib.fin_device_check(ordinal), "fin_device_check")
+
+
+def fin_debug_trace(buf=None) -> None:
+    """Debug timeline of block 0 (u64 [T][16] CUDA tensor, int64 dtype) or None to disable."""
+    import torch
+    _check(_lib.fin_debug_trace(_ptr(buf, torch.int64, "trace")), "fin_debug_trace")
 
 
 def fin_last_error() -> str:

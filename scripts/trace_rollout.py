@@ -1,0 +1,36 @@
+"""Print the block-0 clock64 timeline of a fused rollout (fin_debug_trace), in cycles
+relative to the start of each step."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2501_10709_b200 import fin  # noqa: E402
+from synth import market  # noqa: E402
+from synth import policy as spol  # noqa: E402
+
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 128
+T = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+m = market.stock_c1(rows=1008)
+cfg = fin.env_config(num_envs=N, num_assets=30, num_indicators=8, num_rows=1008, episode_len=30, num_windows=195)
+env = fin.fin_env_create(cfg, m.market)
+pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, spol.kaiming_bf16(spol.STOCK_DIMS, 0))
+rew = torch.zeros((T, N), dtype=torch.float32, device="cuda")
+tr = fin.make_traj(reward=rew)
+nz = fin.make_noise(fin.FIN_NOISE_PHILOX, 7)
+fin.fin_rollout(env, [pol], T, nz, tr)
+buf = torch.zeros((T, 32), dtype=torch.int64, device="cuda")
+fin.fin_debug_trace(buf)
+fin.fin_rollout(env, [pol], T, nz, tr)
+torch.cuda.synchronize()
+fin.fin_debug_trace(None)
+b = buf.cpu().numpy().astype(np.int64)
+names = {0: "step", 23: "stg:d", 24: "stg:uni", 25: "stg:done", 1: "obs_done", 9: "mma:a1", 10: "mma:i1",
+         2: "d1", 3: "epi1", 11: "mma:a2", 12: "mma:i2", 4: "d2", 5: "epi2", 13: "mma:a3", 14: "mma:i3", 6: "d3",
+         16: "philox0", 7: "consume", 17: "fs:start", 19: "fs:body", 20: "fs:tx", 21: "fs:metric", 8: "env_done"}
+for t in range(T):
+    d = b[t] - b[t, 0]
+    order = sorted((int(d[i]), n) for i, n in names.items() if b[t, i] != 0)
+    print(f"t={t}: " + " ".join(f"{n}={v}" for v, n in order))
