@@ -38,7 +38,11 @@ K_ASSETS = 30
 N_IND = 8
 ROWS = 1008
 L_EP = 30
-FLOP_PER_ENV_STEP = 2 * (301 * 256 + 256 * 256 + 256 * 30)        # 300,544 (algorithmic, unpadded)
+MLP_FLOP_PER_ENV_STEP = 2 * (301 * 256 + 256 * 256 + 256 * 30)    # 300,544: the unfactored MLP
+# tensor-core work the fused kernel performs per env-step with the factored layer 1
+# (DESIGN.md §4.3): 31 env-private inputs in layer 1, layers 2 and 3 unchanged
+FLOP_PER_ENV_STEP = 2 * (31 * 256 + 256 * 256 + 256 * 30)          # 162,304
+Z1S_FLOP_PER_ROLLOUT = 2 * 270 * 256 * ROWS   # fp64 CUDA-core precompute of the per-day layer-1 term
 STEP_BYTES_PER_ENV = 8 + 60 + 4 + 4 + 60 + 8 + 60 + 4 + 4 + 1     # K1: state in/out + action + reward + done
 METRIC = "env-steps/sec (whole box) at 2048-65536 envs, 1/2/4/8 B200; % HBM roofline"
 WORKLOAD = "C1 30-stock env + 301-256-256-30 bf16 policy, 65536 envs/GPU, horizon 256, reset on done"
@@ -190,11 +194,10 @@ def run_ours(args):
     pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, spol.kaiming_bf16(spol.STOCK_DIMS, 0))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
-    def allreduce(agg):
-        if world > 1:
-            import torch.distributed as dist
-            dist.all_reduce(agg[:fin.FIN_AGG_NSUM], op=dist.ReduceOp.SUM)
-            dist.all_reduce(agg[fin.FIN_AGG_NSUM:], op=dist.ReduceOp.MIN)
+    from paper_2501_10709_b200 import dist as fdist
+
+    def allreduce(agg):   # the one collective of the path: per-rank FIN_AGG_* partials (NCCL)
+        fdist.allreduce_agg(agg)
 
     def barrier():
         if world > 1:
@@ -206,16 +209,11 @@ def run_ours(args):
     with ClockSampler(local) as cs:
         times, agg = time_rollouts(fin, torch, env, pol, N, T, args.steps, args.warmup, flush, allreduce)
     barrier()
-    total_ms = sum(times)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = fdist.max_over_ranks(sum(times), device="cuda")
     units = N * T * world * args.steps
     value = units / (total_ms / 1e3)
     ms_per_step = total_ms / args.steps
-    kern_ms = statistics.mean(times)
+    kern_ms = statistics.mean(times)      # whole fin_rollout call (z1s prep + rollout + agg): conservative
     flops = FLOP_PER_ENV_STEP * N * T
     pk = peaks()
     achieved = flops / (kern_ms / 1e3) / 1e12
@@ -226,11 +224,15 @@ def run_ours(args):
                       "global_envs": N * world, "parallelism": f"env-sharded dp{world}",
                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
                       "noise": "philox"},
-           "gpu_launches": 2 * args.steps,
+           "gpu_launches": 3 * args.steps,   # per rollout: z1s precompute, fused rollout, aggregate
            "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops_sustained"],
                         "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops_sustained"], "traffic": None,
                         "kernel": "k_tc_rollout<PlanStockC1> (fused rollout)",
-                        "flop_per_env_step": FLOP_PER_ENV_STEP, "peak_source": pk["source"] + " sustained"}}
+                        "flop_per_env_step": FLOP_PER_ENV_STEP,
+                        "note": "tensor FLOPs the kernel executes (factored layer 1, DESIGN.md 4.3); the "
+                                "unfactored MLP is %d FLOP/env-step = %.1f TFLOP/s equivalent"
+                                % (MLP_FLOP_PER_ENV_STEP, MLP_FLOP_PER_ENV_STEP * N * T / (kern_ms / 1e3) / 1e12),
+                        "peak_source": pk["source"] + " bf16 sustained"}}
     prof = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(prof):
         with open(prof) as f:

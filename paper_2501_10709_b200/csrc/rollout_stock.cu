@@ -433,6 +433,13 @@ int num_sms() {
 template <class Plan, bool RES, class Ops>
 cudaError_t launch_auto(const TcParams& p, int n_envs, int* tiles, cudaStream_t s) {
   const int n_tiles = (n_envs + tc::kTileM - 1) / tc::kTileM;
+  static const char* mode = getenv("FIN_TC_MODE");   // experiment switch: "dual" = 2 CTAs / SM
+  if constexpr (!RES) {
+    if (mode && mode[0] == 'd' && n_tiles > num_sms()) {
+      *tiles = 1;
+      return tc::launch<Plan, RES, 1, Ops, 2, 2>(p, n_envs, s);
+    }
+  }
   if (n_tiles > num_sms() && p.M <= tc::Smem<Plan, RES, 2, Ops>::max_members()) {
     *tiles = 2;
     return tc::launch<Plan, RES, 2, Ops>(p, n_envs, s);

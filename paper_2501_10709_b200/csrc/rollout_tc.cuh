@@ -31,7 +31,7 @@
 namespace tc {
 
 constexpr int kTileM = 128;
-constexpr int kRing = 4;
+constexpr int kRing = 4;   // max weight-ring slots (barrier storage); a launch may use fewer
 constexpr int kSmemLimit = 232448;  // 227 KB per CTA
 
 struct TcParams {
@@ -78,7 +78,7 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
 
 // Shared-memory carve-up (dynamic smem, 1024-B aligned base).  The bias region is
 // sized for the launch's member count.
-template <class Plan, bool RESIDENT, int TILES, class Ops>
+template <class Plan, bool RESIDENT, int TILES, class Ops, int RING = kRing>
 struct Smem {
   static constexpr int kA = kTileM * (Plan::kIn > Plan::kHid ? Plan::kIn : Plan::kHid) * 2;  // per tile
   static constexpr int kFixed = TILES * kA + TILES * Ops::kStageBytes + 512;  // + barriers, flags
@@ -91,7 +91,7 @@ struct Smem {
                       : FIN_MAX_MEMBERS)
                : FIN_MAX_MEMBERS;
   __host__ __device__ static constexpr int w_bytes(int M) {
-    return RESIDENT ? Plan::kMemberBytes * M : kRing * Plan::kStageBytes;
+    return RESIDENT ? Plan::kMemberBytes * M : RING * Plan::kStageBytes;
   }
   __host__ __device__ static constexpr int total(int M) { return kFixed + w_bytes(M) + M * kBiasPerMember; }
   __host__ __device__ static constexpr int max_members() {
@@ -112,9 +112,11 @@ struct Smem {
 //     finish_step(State&, p, env, t, stage_ptr)
 //     finalize(State&, p, env, group_tid, bar_id)
 //   };
-template <class Plan, bool RESIDENT, int TILES, class Ops>
-__global__ void __launch_bounds__(64 + 128 * TILES, 1) k_tc_rollout(const __grid_constant__ TcParams p) {
-  using S = Smem<Plan, RESIDENT, TILES, Ops>;
+// RING: weight-ring slots; MINB: CTAs per SM (MINB = 2 runs two independent tiles per
+// SM whose env phases overlap each other's MMA / weight-streaming phases).
+template <class Plan, bool RESIDENT, int TILES, class Ops, int RING = kRing, int MINB = 1>
+__global__ void __launch_bounds__(64 + 128 * TILES, MINB) k_tc_rollout(const __grid_constant__ TcParams p) {
+  using S = Smem<Plan, RESIDENT, TILES, Ops, RING>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int M = p.M;
   const int T = p.T;
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(64 + 128 * TILES, 1) k_tc_rollout(const __grid
         for (int t = 0; t < T; ++t)
           for (int m = 0; m < M; ++m)
             for (int s = 0; s < NS; ++s, ++it) {
-              const uint32_t slot = it % kRing, ph = (it / kRing) & 1;
+              const uint32_t slot = it % RING, ph = (it / RING) & 1;
               sm100::mbar_wait(&w_empty[slot], ph ^ 1);
               sm100::mbar_arrive_expect_tx(&w_full[slot], (uint32_t)Plan::bytes_of(s));
               sm100::bulk_g2s_hint(sW + slot * Plan::kStageBytes, p.wpack[m] + Plan::offset_of(s),
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(64 + 128 * TILES, 1) k_tc_rollout(const __grid
               if (RESIDENT) {
                 b_base = wa + (uint32_t)(m * Plan::kMemberBytes + Plan::offset_of(s));
               } else {
-                const uint32_t slot = it % kRing, ph = (it / kRing) & 1;
+                const uint32_t slot = it % RING, ph = (it / RING) & 1;
                 sm100::mbar_wait(&w_full[slot], ph);
                 sm100::tc_fence_after();
                 b_base = wa + slot * (uint32_t)Plan::kStageBytes;
@@ -216,14 +218,16 @@ __global__ void __launch_bounds__(64 + 128 * TILES, 1) k_tc_rollout(const __grid
               for (int tile = 0; tile < TILES; ++tile) {
                 const uint32_t a_base = aa + (uint32_t)(tile * S::kA);
                 const uint32_t d_tmem = tmem + (uint32_t)(tile * Plan::kHid);
-                for (int j = 0; j < nks; ++j) {
-                  const uint64_t ad = sm100::make_sdesc(a_base + (uint32_t)(j0 + j) * 256u, 128u, a_sbo);
-                  const uint64_t bd = sm100::make_sdesc(b_base + (uint32_t)j * 256u, 128u, b_sbo);
-                  sm100::mma_bf16(d_tmem, ad, bd, idesc, (j0 + j) > 0 ? 1u : 0u);
-                }
+                // descriptors of k-step 0; each further k-step advances both start
+                // addresses by 256 B = 16 units of the descriptor's address field
+                const uint64_t ad0 = sm100::make_sdesc(a_base + (uint32_t)j0 * 256u, 128u, a_sbo);
+                const uint64_t bd0 = sm100::make_sdesc(b_base, 128u, b_sbo);
+                for (int j = 0; j < nks; ++j)
+                  sm100::mma_bf16(d_tmem, ad0 + (uint64_t)(16 * j), bd0 + (uint64_t)(16 * j), idesc,
+                                  (j0 + j) > 0 ? 1u : 0u);
               }
               if (!RESIDENT) {
-                sm100::mma_commit(&w_empty[it % kRing]);
+                sm100::mma_commit(&w_empty[it % RING]);
                 ++it;
               }
             }
@@ -294,11 +298,9 @@ __global__ void __launch_bounds__(64 + 128 * TILES, 1) k_tc_rollout(const __grid
             sm100::tmem_wait_ld();
             uint32_t pk[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const float a0 = fmaxf(__uint_as_float(v[2 * j]) + ad[2 * j], 0.f);
-              const float a1 = fmaxf(__uint_as_float(v[2 * j + 1]) + ad[2 * j + 1], 0.f);
-              pk[j] = sm100::pack_bf16(a0, a1);
-            }
+            for (int j = 0; j < 16; ++j)   // ReLU + bf16 in one cvt.rn.relu.bf16x2
+              pk[j] = sm100::pack_bf16_relu(__uint_as_float(v[2 * j]) + ad[2 * j],
+                                            __uint_as_float(v[2 * j + 1]) + ad[2 * j + 1]);
 #pragma unroll
             for (int g = 0; g < 4; ++g)
               sts128(xa + cm_off(row, c * 4 + g, Plan::kHid / 8), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2],
@@ -344,11 +346,12 @@ __global__ void __launch_bounds__(64 + 128 * TILES, 1) k_tc_rollout(const __grid
   }
 }
 
-template <class Plan, bool RESIDENT, int TILES, class Ops>
+template <class Plan, bool RESIDENT, int TILES, class Ops, int RING = kRing, int MINB = 1>
 cudaError_t launch(const TcParams& p, int n_envs, cudaStream_t s) {
-  using Sm = Smem<Plan, RESIDENT, TILES, Ops>;
-  auto kern = k_tc_rollout<Plan, RESIDENT, TILES, Ops>;
+  using Sm = Smem<Plan, RESIDENT, TILES, Ops, RING>;
+  auto kern = k_tc_rollout<Plan, RESIDENT, TILES, Ops, RING, MINB>;
   const int bytes = Sm::total(p.M);
+  if (MINB > 1 && bytes * MINB > kSmemLimit) return cudaErrorInvalidConfiguration;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (err != cudaSuccess) return err;
   const int per_cta = kTileM * TILES;
