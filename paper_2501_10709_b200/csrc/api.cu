@@ -293,7 +293,8 @@ int fin_env_create(const fin_env_config* cfg, const float* market, int64_t marke
   size_t bytes = 7 * n8 * sizeof(double) / 8;   // 7 double arrays
   bytes += (size_t)FIN_MAX_MEMBERS * K * N * sizeof(float);
   bytes += N * 4 * sizeof(int32_t);              // t_ep, window, tau, m_n
-  bytes += K * N * sizeof(int16_t);
+  const size_t KO = (K + 7) / 8;                 // holdings: asset octets (hold_at)
+  bytes += KO * 8 * N * sizeof(int16_t);
   bytes += 256;
   cudaError_t e;
   if ((e = cudaMalloc(&env->state_mem, bytes)) != cudaSuccess) { delete env; return cuda_fail(e, "cudaMalloc(state)"); }
@@ -316,23 +317,39 @@ int fin_env_create(const fin_env_config* cfg, const float* market, int64_t marke
   d.window = reinterpret_cast<int32_t*>(take(N * 4));
   d.tau = reinterpret_cast<int32_t*>(take(N * 4));
   d.m_n = reinterpret_cast<int32_t*>(take(N * 4));
-  d.hold = reinterpret_cast<int16_t*>(take(K * N * 2));
+  d.hold = reinterpret_cast<int16_t*>(take(KO * 8 * N * 2));
   if ((size_t)(p - static_cast<uint8_t*>(env->state_mem)) > bytes) {
     cudaFree(env->state_mem);
     delete env;
     return fail(FIN_E_CONFIG, "internal: state layout overflow");
   }
-  // flags word + market copy
+  // market copy | flags word | (stock) f64 price table px[rows][2][kp]: close p and
+  // u = fl(p * (1 + c)), both exact host double operations (one rounding for u)
   const size_t mbytes = (size_t)c.num_rows * d.row_floats * sizeof(float);
-  if ((e = cudaMalloc(&env->market_mem, mbytes + 64)) != cudaSuccess) {
+  std::vector<double> px;
+  if (c.task == FIN_STOCK) {
+    px.assign((size_t)c.num_rows * 2 * d.kp, 0.0);
+    for (int r = 0; r < c.num_rows; ++r)
+      for (int k = 0; k < d.K; ++k) {
+        const double pk = (double)padded[(size_t)r * d.row_floats + k];
+        px[((size_t)r * 2 + 0) * d.kp + k] = pk;
+        px[((size_t)r * 2 + 1) * d.kp + k] = pk * d.up;
+      }
+  }
+  const size_t pxbytes = px.size() * sizeof(double);
+  if ((e = cudaMalloc(&env->market_mem, mbytes + 64 + pxbytes)) != cudaSuccess) {
     cudaFree(env->state_mem);
     delete env;
     return cuda_fail(e, "cudaMalloc(market)");
   }
   d.flags = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(env->market_mem) + mbytes);
   d.market = env->market_mem;
+  d.px = pxbytes ? reinterpret_cast<const double*>(reinterpret_cast<uint8_t*>(env->market_mem) + mbytes + 64)
+                 : nullptr;
   cudaStream_t s = S(stream);
   e = cudaMemcpyAsync(env->market_mem, upload, mbytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && pxbytes)
+    e = cudaMemcpyAsync(const_cast<double*>(d.px), px.data(), pxbytes, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(d.flags, 0, 64, s);
   env->d = d;
   if (e == cudaSuccess)

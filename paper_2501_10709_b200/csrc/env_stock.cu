@@ -2,11 +2,26 @@
 // (K4), state get/set.  PAPER.md §4.2: reset / step / reward over
 // all SubEnvs; the paper vmaps them in PyTorch on an A100, here each is
 // one hand-written sm_100a kernel over the SoA state.
+//
+// K1 / K4 layout of work: one env per thread, 128-thread blocks
+// (one window block of envs, so the block normally sits on one market day).
+//  * state: coalesced SoA loads; holdings as 16-byte asset octets (hold_at).
+//  * actions [N][K] int16 (caller layout, 60 B per env at K = 30): each warp copies
+//    its 32 contiguous rows into shared memory with 16-byte cp.async, then every
+//    thread reads its row as 32-bit words (stride K/2 words: conflict-free for odd
+//    K/2).  K4 double-buffers the copy of step s+1 under the arithmetic of step s.
+//  * prices: the three f64 rows a step needs (p_d, u_d, p_{d+1}) are staged in
+//    shared memory once per block and day (group_apply, group_stage.cuh).
+//  * arithmetic: exact f64 in the oracle's order, int -> f64 on the fp64 pipe.
 #include "env_stock.cuh"
+#include "group_stage.cuh"
+#include "sm100.cuh"
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;       // reset / get / set
+constexpr int kStep = 128;          // K1 / K4 block: 4 warps
+constexpr int kBar = 1;             // named barrier of group_apply (0 is __syncthreads)
 
 __device__ __forceinline__ MetricAcc load_metric(const EnvDev& e, int i) {
   MetricAcc m;
@@ -24,7 +39,8 @@ __global__ void k_stock_reset(EnvDev e, const uint8_t* __restrict__ mask) {
   if (i >= e.N) return;
   if (mask && !mask[i]) return;
   e.cash[i] = e.cash0;
-  for (int k = 0; k < e.K; ++k) e.hold[(size_t)k * e.N + i] = 0;
+  uint4* q = reinterpret_cast<uint4*>(e.hold);
+  for (int o = 0; o < (e.K + 7) / 8; ++o) q[(size_t)o * e.N + i] = make_uint4(0u, 0u, 0u, 0u);
   e.t_ep[i] = 0;
   e.window[i] = window_of(e, e.env_offset + i);
   for (int m = 0; m < FIN_MAX_MEMBERS; ++m)
@@ -34,154 +50,248 @@ __global__ void k_stock_reset(EnvDev e, const uint8_t* __restrict__ mask) {
   store_metric(e, i, a);
 }
 
-// K1: one step of every env with supplied actions [N][K].  One env per thread;
-// state SoA loads are coalesced; the two market rows are read through L1 (the
-// whole C1 market is 1.2 MB and stays L2-resident; envs of a warp share a row).
-template <int KP>
-__global__ void __launch_bounds__(kThreads) k_stock_step(EnvDev e, const int16_t* __restrict__ actions, TrajDev o) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= e.N) return;
-  const int K = e.K, N = e.N;
-  int t = e.t_ep[i];
-  const int w = e.window[i];
-  double b = e.cash[i];
-  int h[KP], a[KP], ex[KP];
-#pragma unroll
-  for (int k = 0; k < KP; ++k) {
-    h[k] = (k < K) ? (int)e.hold[(size_t)k * N + i] : 0;
-    a[k] = (k < K) ? (int)actions[(size_t)i * K + k] : 0;
+// ------------------------------------------------------------------ K1 / K4 pieces
+// KA: compile-time asset count (EXACT: KA == K) or bound (K <= KA, padding zeros).
+template <int KA>
+struct StepSmem {
+  double pr[3][KA];                         // staged day: p_d, u_d, p_{d+1}
+  GroupSlots gs;
+  alignas(16) int16_t act[2][4][32 * KA];   // [buffer][warp] action rows
+};
+
+// copy this warp's action rows [n_valid][K] (contiguous in the caller's [N][K]) to shared
+__device__ __forceinline__ void slab_load(int16_t* dst, const int16_t* src, int n_valid, int K, int lane, bool vec) {
+  const int elems = n_valid * K;
+  if (vec) {   // n_valid == 32 and src 16-B aligned: 64 K bytes = 4 K vectors
+    for (int j = lane; j < 4 * K; j += 32) sm100::cp_async16(dst + 8 * j, src + 8 * j);
+  } else {
+    for (int j = lane; j < elems; j += 32) dst[j] = src[j];
   }
-  if (t >= e.L) {  // done env, autoreset = 0: ignored
+  sm100::cp_async_commit();
+}
+
+template <int KA, bool EXACT>
+__device__ __forceinline__ void slab_read(const int16_t* slab, int lane, int K, bool live, int (&a)[KA]) {
+  if constexpr (EXACT && (KA % 2 == 0)) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(slab) + lane * (KA / 2);
+#pragma unroll
+    for (int j = 0; j < KA / 2; ++j) {
+      const uint32_t x = live ? w[j] : 0u;
+      a[2 * j] = (int)(int16_t)(x & 0xffffu);
+      a[2 * j + 1] = ((int)x) >> 16;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < KA; ++k) a[k] = (live && k < K) ? (int)slab[lane * K + k] : 0;
+  }
+}
+
+// stage p_d, u_d (row d) and p_{d+1} (row d+1) of the f64 price table
+template <int KA>
+__device__ __forceinline__ void stage_prices(const EnvDev& e, StepSmem<KA>& sm, int d, int tid) {
+  for (int j = tid; j < 3 * KA; j += kStep) {
+    const int r = j / KA, k = j - r * KA;
+    const int row = d + (r == 2 ? 1 : 0), ch = (r == 1 ? 1 : 0);
+    sm.pr[r][k] = k < e.kp ? e.px[((size_t)row * 2 + ch) * e.kp + k] : 0.0;
+  }
+}
+
+template <int KA>
+__device__ __forceinline__ void write_rows(const EnvDev& e, const TrajDev& o, size_t ti, const int (&h)[KA],
+                                           const int (&a)[KA]) {
+  if (o.hold || o.actions) {
+#pragma unroll
+    for (int k = 0; k < KA; ++k) {
+      if (k < e.K) {
+        if (o.hold) o.hold[ti * e.K + k] = (int16_t)h[k];
+        if (o.actions) o.actions[ti * e.K + k] = (int16_t)a[k];
+      }
+    }
+  }
+}
+
+// K1: one step of every env with supplied actions [N][K].
+template <int KA, bool EXACT>
+__global__ void __launch_bounds__(kStep) k_stock_step(EnvDev e, const int16_t* __restrict__ actions, TrajDev o,
+                                                      int vec_ok) {
+  __shared__ StepSmem<KA> sm;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int i = blockIdx.x * kStep + tid;
+  const bool live = i < e.N;
+  const int K = EXACT ? KA : e.K;
+  int t = 0, w = 0;
+  double b = 0.0;
+  int h[KA];
+#pragma unroll
+  for (int k = 0; k < KA; ++k) h[k] = 0;
+  if (live) {
+    t = e.t_ep[i];
+    w = e.window[i];
+    b = e.cash[i];
+    load_hold<KA>(e, i, h);
+  }
+  const int i0 = blockIdx.x * kStep + wid * 32;
+  const int nv = max(0, min(32, e.N - i0));
+  int16_t* slab = sm.act[0][wid];
+  if (nv > 0) slab_load(slab, actions + (size_t)i0 * K, nv, K, lane, vec_ok && nv == 32);
+  gs_init(&sm.gs, tid, kBar);
+  const bool stepping = live && t < e.L;
+  if (live && !stepping) {  // done env, autoreset = 0: ignored
     set_flag(e, FIN_FLAG_EPISODE_DONE);
     if (o.reward) o.reward[i] = 0.f;
     if (o.done) o.done[i] = 1;
-    return;
   }
   const int d = day_of(e, w, t);
-  if (d < 0 || d + 1 >= e.rows) {
-    set_flag(e, FIN_FLAG_BAD_INDEX);
-    return;
-  }
-  const float* p = e.market + (size_t)d * e.row_floats;  // channel 0 = close
-  const float* pn = p + e.row_floats;
-  double v, vn;
+  const bool bad = stepping && (d < 0 || d + 1 >= e.rows);
+  if (bad) set_flag(e, FIN_FLAG_BAD_INDEX);
+  sm100::cp_async_wait<0>();
+  __syncwarp();
+  int a[KA];
+  slab_read<KA, EXACT>(slab, lane, K, live, a);
   bool oor = false;
-  stock_transition<KP>(e, b, h, p, pn, a, v, vn, ex, oor);
+  int round = 0;
+  group_apply(
+      &sm.gs, round, d, stepping && !bad, tid, kBar, [&](int dd) { stage_prices<KA>(e, sm, dd, tid); },
+      [&]() {
+        const double v = stock_mark<KA>(b, h, sm.pr[0]);
+        stock_trade<KA>(e, b, h, sm.pr[0], sm.pr[1], a, oor);
+        const double vn = stock_mark<KA>(b, h, sm.pr[2]);
+        t += 1;
+        const bool done = (t == e.L);
+        if (o.reward) o.reward[i] = stock_reward(e, v, vn);
+        if (o.done) o.done[i] = done ? 1 : 0;
+        if (o.cash) o.cash[i] = b;
+        if (o.asset) o.asset[i] = vn;
+        write_rows<KA>(e, o, (size_t)i, h, a);
+        if (done && e.autoreset) {
+          b = e.cash0;
+#pragma unroll
+          for (int k = 0; k < KA; ++k) h[k] = 0;
+          t = 0;
+          if (e.wadv) w = (w + 1) % e.W;
+        }
+        e.cash[i] = b;
+        store_hold<KA>(e, i, h);
+        e.t_ep[i] = t;
+        if (e.wadv) e.window[i] = w;
+      });
   if (oor) set_flag(e, FIN_FLAG_ACTION_RANGE);
-  t += 1;
-  const bool done = (t == e.L);
-  if (o.reward) o.reward[i] = stock_reward(e, v, vn);
-  if (o.done) o.done[i] = done ? 1 : 0;
-  if (o.cash) o.cash[i] = b;
-  if (o.asset) o.asset[i] = vn;
-#pragma unroll
-  for (int k = 0; k < KP; ++k) {
-    if (k < K) {
-      if (o.hold) o.hold[(size_t)i * K + k] = (int16_t)h[k];
-      if (o.actions) o.actions[(size_t)i * K + k] = (int16_t)ex[k];
-    }
-  }
-  if (done && e.autoreset) {
-    b = e.cash0;
-#pragma unroll
-    for (int k = 0; k < KP; ++k) h[k] = 0;
-    t = 0;
-    if (e.wadv) e.window[i] = (w + 1) % e.W;
-  }
-  e.cash[i] = b;
-#pragma unroll
-  for (int k = 0; k < KP; ++k)
-    if (k < K) e.hold[(size_t)k * N + i] = (int16_t)h[k];
-  e.t_ep[i] = t;
 }
 
 // K4: T steps with supplied actions [T][N][K]; the env state (cash, holdings,
-// episode clock, window, metric accumulators) lives in registers for all T.
-template <int KP>
-__global__ void __launch_bounds__(kThreads) k_stock_replay(EnvDev e, const int16_t* __restrict__ actions, int T,
-                                                           TrajDev o) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+// episode clock, window, metric accumulators) lives in registers for all T, and the
+// pre-trade asset v of a step is the previous step's post-trade asset v' (the same
+// sum over the same holdings and prices), or b0 after a reset.
+template <int KA, bool EXACT>
+__global__ void __launch_bounds__(kStep) k_stock_replay(EnvDev e, const int16_t* __restrict__ actions, int T,
+                                                        TrajDev o, int vec_ok) {
+  __shared__ StepSmem<KA> sm;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int i = blockIdx.x * kStep + tid;
   const bool live = i < e.N;
-  const int K = e.K, N = e.N;
+  const int K = EXACT ? KA : e.K, N = e.N;
   AggAcc agg;
   agg_init(agg);
+  int t = 0, w = 0;
+  double b = 0.0;
+  int h[KA];
+#pragma unroll
+  for (int k = 0; k < KA; ++k) h[k] = 0;
+  MetricAcc m;
+  metric_start(m, 0.0);
   if (live) {
-    int t = e.t_ep[i];
-    int w = e.window[i];
-    double b = e.cash[i];
-    int h[KP], a[KP], ex[KP];
-#pragma unroll
-    for (int k = 0; k < KP; ++k) h[k] = (k < K) ? (int)e.hold[(size_t)k * N + i] : 0;
-    MetricAcc m = load_metric(e, i);
-    int cnt = 0;
-    double rsum = 0.0;
-    bool oor = false, bad = false;
-    for (int s = 0; s < T; ++s) {
-      const int16_t* ar = actions + ((size_t)s * N + i) * K;
-#pragma unroll
-      for (int k = 0; k < KP; ++k) a[k] = (k < K) ? (int)ar[k] : 0;
-      const size_t ti = (size_t)s * N + i;
-      if (t >= e.L) {
-        set_flag(e, FIN_FLAG_EPISODE_DONE);
-        if (o.reward) o.reward[ti] = 0.f;
-        if (o.done) o.done[ti] = 1;
-        continue;
-      }
-      const int d = day_of(e, w, t);
-      if (d < 0 || d + 1 >= e.rows) { bad = true; break; }
-      const float* p = e.market + (size_t)d * e.row_floats;
-      double v, vn;
-      stock_transition<KP>(e, b, h, p, p + e.row_floats, a, v, vn, ex, oor);
-      t += 1;
-      const bool done = (t == e.L);
-      const float r = stock_reward(e, v, vn);
-      rsum += (double)r;
-      if (o.reward) o.reward[ti] = r;
-      if (o.done) o.done[ti] = done ? 1 : 0;
-      if (o.cash) o.cash[ti] = b;
-      if (o.asset) o.asset[ti] = vn;
-      if (o.hold || o.actions) {
-#pragma unroll
-        for (int k = 0; k < KP; ++k) {
-          if (k < K) {
-            if (o.hold) o.hold[ti * K + k] = (int16_t)h[k];
-            if (o.actions) o.actions[ti * K + k] = (int16_t)ex[k];
-          }
-        }
-      }
-      metric_push(m, vn);
-      if (done) {
-        double em[3];
-        metric_finish(m, 252.0, 0.0, em);
-        if (o.ep_metrics && cnt < o.ep_capacity) {
-          double* dst = o.ep_metrics + ((size_t)cnt * N + i) * 3;
-          dst[0] = em[0]; dst[1] = em[1]; dst[2] = em[2];
-        }
-        ++cnt;
-        agg_episode(agg, em);
-        if (e.autoreset) {
-          b = e.cash0;
-#pragma unroll
-          for (int k = 0; k < KP; ++k) h[k] = 0;
-          t = 0;
-          if (e.wadv) w = (w + 1) % e.W;
-          metric_start(m, e.cash0);
-        }
-      }
+    t = e.t_ep[i];
+    w = e.window[i];
+    b = e.cash[i];
+    load_hold<KA>(e, i, h);
+    m = load_metric(e, i);
+  }
+  const int i0 = blockIdx.x * kStep + wid * 32;
+  const int nv = max(0, min(32, N - i0));
+  const bool vec = vec_ok && nv == 32;
+  if (nv > 0) slab_load(sm.act[0][wid], actions + (size_t)i0 * K, nv, K, lane, vec);
+  gs_init(&sm.gs, tid, kBar);
+  int cnt = 0, round = 0;
+  double rsum = 0.0, vc = 0.0;
+  bool have_v = false, oor = false, bad = false;
+  for (int s = 0; s < T; ++s) {
+    if (s + 1 < T && nv > 0)
+      slab_load(sm.act[(s + 1) & 1][wid], actions + ((size_t)(s + 1) * N + i0) * K, nv, K, lane, vec);
+    if (s + 1 < T && nv > 0) sm100::cp_async_wait<1>();
+    else sm100::cp_async_wait<0>();
+    __syncwarp();
+    int a[KA];
+    slab_read<KA, EXACT>(sm.act[s & 1][wid], lane, K, live, a);
+    const size_t ti = (size_t)s * N + i;
+    const bool stepping = live && !bad && t < e.L;
+    if (live && !bad && !stepping) {
+      set_flag(e, FIN_FLAG_EPISODE_DONE);
+      if (o.reward) o.reward[ti] = 0.f;
+      if (o.done) o.done[ti] = 1;
     }
+    const int d = day_of(e, w, t);
+    if (stepping && (d < 0 || d + 1 >= e.rows)) bad = true;
+    group_apply(
+        &sm.gs, round, d, stepping && !bad, tid, kBar, [&](int dd) { stage_prices<KA>(e, sm, dd, tid); },
+        [&]() {
+          if (!have_v) { vc = stock_mark<KA>(b, h, sm.pr[0]); have_v = true; }
+          const double v = vc;
+          stock_trade<KA>(e, b, h, sm.pr[0], sm.pr[1], a, oor);
+          const double vn = stock_mark<KA>(b, h, sm.pr[2]);
+          vc = vn;
+          t += 1;
+          const bool done = (t == e.L);
+          const float r = stock_reward(e, v, vn);
+          rsum += (double)r;
+          if (o.reward) o.reward[ti] = r;
+          if (o.done) o.done[ti] = done ? 1 : 0;
+          if (o.cash) o.cash[ti] = b;
+          if (o.asset) o.asset[ti] = vn;
+          write_rows<KA>(e, o, ti, h, a);
+          metric_push(m, vn);
+          if (done) {
+            double em[3];
+            metric_finish(m, 252.0, 0.0, em);
+            if (o.ep_metrics && cnt < o.ep_capacity) {
+              double* dst = o.ep_metrics + ((size_t)cnt * N + i) * 3;
+              dst[0] = em[0]; dst[1] = em[1]; dst[2] = em[2];
+            }
+            ++cnt;
+            agg_episode(agg, em);
+            if (e.autoreset) {
+              b = e.cash0;
+#pragma unroll
+              for (int k = 0; k < KA; ++k) h[k] = 0;
+              t = 0;
+              vc = e.cash0;
+              if (e.wadv) w = (w + 1) % e.W;
+              metric_start(m, e.cash0);
+            }
+          }
+        });
+  }
+  if (live) {
     if (oor) set_flag(e, FIN_FLAG_ACTION_RANGE);
     if (bad) set_flag(e, FIN_FLAG_BAD_INDEX);
-    agg.s[FIN_AGG_SUM_REWARD] = rsum;
     e.cash[i] = b;
-#pragma unroll
-    for (int k = 0; k < KP; ++k)
-      if (k < K) e.hold[(size_t)k * N + i] = (int16_t)h[k];
+    store_hold<KA>(e, i, h);
     e.t_ep[i] = t;
     e.window[i] = w;
     store_metric(e, i, m);
     if (o.ep_count) o.ep_count[i] = cnt;
   }
+  agg.s[FIN_AGG_SUM_REWARD] = rsum;
   if (o.agg_partial) agg_block_write(agg, o.agg_partial + (size_t)blockIdx.x * FIN_AGG_LEN);
+}
+
+// asset (v = b + sum h p at the env's current day) through the same f64 table
+__device__ __forceinline__ double asset_now(const EnvDev& e, int i) {
+  int d = day_of(e, e.window[i], e.t_ep[i]);
+  if (d >= e.rows) d = e.rows - 1;
+  const double* p = e.px + (size_t)d * 2 * e.kp;
+  double v = e.cash[i];
+  for (int k = 0; k < e.K; ++k) v = fadd64(v, fmul64(nn2d(e.hold[hold_at(e.N, k, i)]), p[k]));
+  return v;
 }
 
 __global__ void k_stock_get_state(EnvDev e, double* cash, int16_t* hold, double* asset, int32_t* t_ep,
@@ -189,21 +299,12 @@ __global__ void k_stock_get_state(EnvDev e, double* cash, int16_t* hold, double*
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= e.N) return;
   const int K = e.K;
-  double b = e.cash[i];
-  if (cash) cash[i] = b;
+  if (cash) cash[i] = e.cash[i];
   if (t_ep) t_ep[i] = e.t_ep[i];
   if (window) window[i] = e.window[i];
   if (hold)
-    for (int k = 0; k < K; ++k) hold[(size_t)i * K + k] = e.hold[(size_t)k * e.N + i];
-  if (asset) {
-    int t = e.t_ep[i];
-    int d = day_of(e, e.window[i], t);
-    if (d >= e.rows) d = e.rows - 1;
-    const float* p = e.market + (size_t)d * e.row_floats;
-    double v = b;
-    for (int k = 0; k < K; ++k) v = fadd64(v, fmul64((double)e.hold[(size_t)k * e.N + i], (double)p[k]));
-    asset[i] = v;
-  }
+    for (int k = 0; k < K; ++k) hold[(size_t)i * K + k] = e.hold[hold_at(e.N, k, i)];
+  if (asset) asset[i] = asset_now(e, i);
 }
 
 __global__ void k_stock_set_state(EnvDev e, const double* cash, const int16_t* hold, const int32_t* t_ep,
@@ -213,17 +314,12 @@ __global__ void k_stock_set_state(EnvDev e, const double* cash, const int16_t* h
   const int K = e.K;
   if (cash) e.cash[i] = cash[i];
   if (hold)
-    for (int k = 0; k < K; ++k) e.hold[(size_t)k * e.N + i] = hold[(size_t)i * K + k];
+    for (int k = 0; k < K; ++k) e.hold[hold_at(e.N, k, i)] = hold[(size_t)i * K + k];
   if (t_ep) e.t_ep[i] = t_ep[i];
   if (window) e.window[i] = window[i];
   // online metrics restart at the current equity
-  int d = day_of(e, e.window[i], e.t_ep[i]);
-  if (d >= e.rows) d = e.rows - 1;
-  const float* p = e.market + (size_t)d * e.row_floats;
-  double v = e.cash[i];
-  for (int k = 0; k < K; ++k) v = fadd64(v, fmul64((double)e.hold[(size_t)k * e.N + i], (double)p[k]));
   MetricAcc m;
-  metric_start(m, v);
+  metric_start(m, asset_now(e, i));
   store_metric(e, i, m);
 }
 
@@ -238,18 +334,27 @@ __global__ void k_agg_finalize(const double* __restrict__ partial, int n_blocks,
   agg[j] = s;
 }
 
-inline int blocks_for(int n) { return (n + kThreads - 1) / kThreads; }
+inline int blocks_for(int n, int threads = kThreads) { return (n + threads - 1) / threads; }
+
+// 16-byte cp.async of whole action rows needs a 16-B aligned base and, for the
+// per-step slabs of K4, a 16-B multiple per step (N K int16)
+inline int vec_ok(const void* p, long long elems_per_step) {
+  return ((reinterpret_cast<uintptr_t>(p) & 15u) == 0 && (elems_per_step % 8) == 0) ? 1 : 0;
+}
 
 }  // namespace
 
 namespace fin {
 
-#define FIN_DISPATCH_KP(K, KERNEL, GRID, BLOCK, STREAM, ...)                    \
-  do {                                                                          \
-    if ((K) <= 4) KERNEL<4><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);           \
-    else if ((K) <= 8) KERNEL<8><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);      \
-    else if ((K) <= 16) KERNEL<16><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);    \
-    else KERNEL<32><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);                   \
+// K = 30 (C1) and K = 4 (C0) are compiled exactly; any other K runs in the next
+// power-of-two bound with zero padding.
+#define FIN_DISPATCH_K(K, KERNEL, GRID, STREAM, ...)                                         \
+  do {                                                                                       \
+    if ((K) == 30) KERNEL<30, true><<<GRID, kStep, 0, STREAM>>>(__VA_ARGS__);                \
+    else if ((K) == 4) KERNEL<4, true><<<GRID, kStep, 0, STREAM>>>(__VA_ARGS__);             \
+    else if ((K) <= 8) KERNEL<8, false><<<GRID, kStep, 0, STREAM>>>(__VA_ARGS__);            \
+    else if ((K) <= 16) KERNEL<16, false><<<GRID, kStep, 0, STREAM>>>(__VA_ARGS__);          \
+    else KERNEL<32, false><<<GRID, kStep, 0, STREAM>>>(__VA_ARGS__);                         \
   } while (0)
 
 cudaError_t launch_stock_reset(const EnvDev& e, const uint8_t* mask, cudaStream_t s) {
@@ -258,14 +363,16 @@ cudaError_t launch_stock_reset(const EnvDev& e, const uint8_t* mask, cudaStream_
 }
 
 cudaError_t launch_stock_step(const EnvDev& e, const int16_t* actions, const TrajDev& o, cudaStream_t s) {
-  FIN_DISPATCH_KP(e.K, k_stock_step, blocks_for(e.N), kThreads, s, e, actions, o);
+  const int v = vec_ok(actions, 8);   // K1 reads one step: per-warp rows are 64 K bytes
+  FIN_DISPATCH_K(e.K, k_stock_step, blocks_for(e.N, kStep), s, e, actions, o, v);
   return cudaGetLastError();
 }
 
 cudaError_t launch_stock_replay(const EnvDev& e, const int16_t* actions, int T, const TrajDev& o, int* n_blocks,
                                 cudaStream_t s) {
-  *n_blocks = blocks_for(e.N);
-  FIN_DISPATCH_KP(e.K, k_stock_replay, blocks_for(e.N), kThreads, s, e, actions, T, o);
+  *n_blocks = blocks_for(e.N, kStep);
+  const int v = vec_ok(actions, (long long)e.N * e.K);
+  FIN_DISPATCH_K(e.K, k_stock_replay, blocks_for(e.N, kStep), s, e, actions, T, o, v);
   return cudaGetLastError();
 }
 

@@ -15,57 +15,57 @@
 #pragma once
 #include "fin_internal.cuh"
 
-// ``p`` / ``pn``: close prices of rows d and d+1 (fp32, widened exactly).
-// h[] holds int holdings (updated in place), a[] the requested deltas.
-// Returns via references: v (pre-trade asset at p), vn (post-trade asset at pn),
-// act[] the action after the clamp (R6); oor set when an action was clamped.
-template <int KP, typename PT>
-__device__ __forceinline__ void stock_transition(const EnvDev& e, double& b, int (&h)[KP],
-                                                 const PT* __restrict__ p, const PT* __restrict__ pn,
-                                                 const int (&a)[KP], double& v, double& vn,
-                                                 int (&act)[KP], bool& oor) {
-  const int K = e.K;
-  // 1. v = b + sum_k h_k p_k, ascending k (products are exact: h < 2^15, p has 24 bits)
+// P / U: row d of the f64 price table -- close p_k (exact widening of the fp32
+// market) and u_k = fl(p_k * up) -- in shared or global memory.  Padding assets
+// (k >= K) carry p = u = 0, h = 0 and a = 0, so every loop below runs to the
+// compile-time KA with no per-asset predicate: a padded asset adds +0 to the cash
+// (b is never -0) and to the sums, which leaves them bit-identical.
+
+// v = b + sum_k h_k p_k, ascending k (each product is exact: h < 2^15, p has 24 bits)
+template <int KA>
+__device__ __forceinline__ double stock_mark(double b, const int (&h)[KA], const double* P) {
   double acc = b;
 #pragma unroll
-  for (int k = 0; k < KP; ++k)
-    if (k < K) acc = fadd64(acc, fmul64((double)h[k], (double)p[k]));
-  v = acc;
-  // 2. clamp (R6)
-  int aa[KP];
+  for (int k = 0; k < KA; ++k) acc = fadd64(acc, fmul64(nn2d(h[k]), P[k]));
+  return acc;
+}
+
+// The trade of one step.  a[] holds the requested deltas on entry and the clamped
+// deltas (R6) on exit; h[] and b are updated in place.
+template <int KA>
+__device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)[KA], const double* P,
+                                            const double* U, int (&a)[KA], bool& oor) {
+  // 2. clamp (R6); any clamped entry sets the sticky range flag
+  int diff = 0;
 #pragma unroll
-  for (int k = 0; k < KP; ++k) {
-    int x = (k < K) ? a[k] : 0;
-    if (x > e.max_trade) { x = e.max_trade; oor = true; }
-    if (x < -e.max_trade) { x = -e.max_trade; oor = true; }
-    aa[k] = x;
-    act[k] = x;
+  for (int k = 0; k < KA; ++k) {
+    const int x = min(max(a[k], -e.max_trade), e.max_trade);
+    diff |= x ^ a[k];
+    a[k] = x;
   }
-  // 3. sells, clipped to holdings: b += (n p) (1 - c)
+  oor |= diff != 0;
+  // 3. sells, clipped to holdings: b += fl(fl(n p) (1 - c)); n = 0 adds +0
 #pragma unroll
-  for (int k = 0; k < KP; ++k) {
-    if (k < K && aa[k] < 0) {
-      int n = min(-aa[k], h[k]);
-      b = fadd64(b, fmul64(fmul64((double)n, (double)p[k]), e.dn));
-      h[k] -= n;
+  for (int k = 0; k < KA; ++k) {
+    const int n = max(min(-a[k], h[k]), 0);
+    b = fadd64(b, fmul64(fmul64(nn2d(n), P[k]), e.dn));
+    h[k] -= n;
+  }
+  // 4. buys, ascending k, each the largest affordable count at u (R5); the fast
+  //    path (the whole request is affordable) reuses the product it tested
+#pragma unroll
+  for (int k = 0; k < KA; ++k) {
+    const int want = max(min(a[k], FIN_HOLD_MAX - h[k]), 0);
+    const double u = U[k];
+    double c = fmul64(nn2d(want), u);
+    int n = want;
+    if (!(c <= b)) {
+      n = affordable_slow(b, u, want);
+      c = fmul64(nn2d(n), u);
     }
+    b = fsub64(b, c);
+    h[k] += n;
   }
-  // 4. buys, ascending k, each the largest affordable count at u = p (1 + c)
-#pragma unroll
-  for (int k = 0; k < KP; ++k) {
-    if (k < K && aa[k] > 0) {
-      double u = fmul64((double)p[k], e.up);
-      int n = affordable(b, u, min(aa[k], FIN_HOLD_MAX - h[k]));
-      b = fsub64(b, fmul64((double)n, u));
-      h[k] += n;
-    }
-  }
-  // 5. v' = b' + sum_k h'_k p'_k
-  acc = b;
-#pragma unroll
-  for (int k = 0; k < KP; ++k)
-    if (k < K) acc = fadd64(acc, fmul64((double)h[k], (double)pn[k]));
-  vn = acc;
 }
 
 // reward = (v' - v) * scale (exact power-of-two scale), stored fp32

@@ -27,9 +27,10 @@ struct EnvDev {
   int64_t env_offset;
   int64_t t_global;      // global step counter (Philox counter word), advanced per step
   const float* market;   // [rows][row_floats]
+  const double* px;      // stock: [rows][2][kp] f64 -- close p (exact widening), u = fl(p * up)
   // ---- state (library-owned device memory)
   double* cash;          // [N]
-  int16_t* hold;         // [K][N] (crypto: position in {-1,0,1}, K = 1)
+  int16_t* hold;         // stock: asset octets [ceil(K/8)][N][8] (hold_at); crypto: [N] position in {-1,0,1}
   int32_t* t_ep;         // [N]
   int32_t* window;       // [N]
   int32_t* tau;          // [N] crypto holding time
@@ -68,6 +69,48 @@ __device__ __forceinline__ double fadd64(double a, double b) { return __dadd_rn(
 __device__ __forceinline__ double fsub64(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double fmul64(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double fdiv64(double a, double b) { return __ddiv_rn(a, b); }
+
+// Exact int -> double for 0 <= n < 2^31 on the fp64 pipe: the bit pattern
+// 0x43300000:n is 2^52 + n exactly and subtracting 2^52 is exact.  Replaces the
+// I2F.F64 conversion, which runs on the narrow XU pipe (ncu round 1: XU was the
+// busiest pipe of the step kernels).
+__device__ __forceinline__ double nn2d(int n) {
+  return __dsub_rn(__hiloint2double(0x43300000, n), 4503599627370496.0);
+}
+
+// Stock holdings layout: asset octets, element (k, i) at ((k / 8) * N + i) * 8 + k % 8,
+// so one env's 8 assets are one 16-byte vector and a warp's octet row is 512
+// contiguous bytes.  Padding assets (k >= K) are kept at 0.
+__device__ __forceinline__ size_t hold_at(int N, int k, int i) {
+  return (((size_t)(k >> 3) * N + i) << 3) + (k & 7);
+}
+template <int KA>
+__device__ __forceinline__ void load_hold(const EnvDev& e, int i, int (&h)[KA]) {
+  const uint4* q = reinterpret_cast<const uint4*>(e.hold);
+#pragma unroll
+  for (int o = 0; o < (KA + 7) / 8; ++o) {
+    const uint4 v = q[(size_t)o * e.N + i];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (8 * o + j < KA) h[8 * o + j] = (int)((j & 1) ? (w[j >> 1] >> 16) : (w[j >> 1] & 0xffffu));
+  }
+}
+template <int KA>
+__device__ __forceinline__ void store_hold(const EnvDev& e, int i, const int (&h)[KA]) {
+  uint4* q = reinterpret_cast<uint4*>(e.hold);
+#pragma unroll
+  for (int o = 0; o < (KA + 7) / 8; ++o) {
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k0 = 8 * o + 2 * j, k1 = k0 + 1;
+      const uint32_t lo = k0 < KA ? (uint32_t)h[k0] : 0u, hi = k1 < KA ? (uint32_t)h[k1] : 0u;
+      w[j] = __byte_perm(lo, hi, 0x5410);
+    }
+    q[(size_t)o * e.N + i] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
 
 __device__ __forceinline__ void set_flag(const EnvDev& e, uint32_t bit) { atomicOr(e.flags, bit); }
 

@@ -54,9 +54,9 @@ struct StockOps {
   static constexpr int KT8 = Plan::kIn / 8;
   using Obs = StockObs<KA, IA>;
   static_assert(Obs::kEnvPad == Plan::kIn, "factored layer 1: the network input is the private part");
-  // staging: close_d, close_d+1 (f64) | z1s rows of day d per member (f32) | slots | broadcast
+  // staging: p_d, u_d, p_d+1 (f64) | z1s rows of day d per member (f32) | slots | broadcast
   static constexpr int kOffP = 0;
-  static constexpr int kOffZ = 2 * KP4 * 8;
+  static constexpr int kOffZ = 3 * KP4 * 8;
   static constexpr int kOffS = kOffZ + FIN_MAX_MEMBERS * Plan::kHid * 4;
   static constexpr int kOffB = kOffS + 16;
   static constexpr int kStageBytes = kOffB + 16;
@@ -65,6 +65,8 @@ struct StockOps {
     bool live;
     int gtid, bar_id, round;
     double b;
+    double vc;         // pre-trade asset of the next step (= last v', or b0 after a reset)
+    bool have_v;
     int h[KA];
     int t_ep, w, d;
     uint32_t b0bits;
@@ -86,11 +88,13 @@ struct StockOps {
     st.rsum = 0.0;
     st.oor = st.bad = st.nonfinite = false;
     st.d = 0;
+    st.have_v = false;
+    st.vc = 0.0;
     agg_init(st.agg);
     if (st.live) {
       st.b = e.cash[env];
 #pragma unroll
-      for (int k = 0; k < KA; ++k) st.h[k] = e.hold[(size_t)k * e.N + env];
+      load_hold<KA>(e, env, st.h);
       st.t_ep = e.t_ep[env];
       st.w = e.window[env];
       st.m.v0 = e.m_v0[env]; st.m.vprev = e.m_vprev[env]; st.m.peak = e.m_peak[env]; st.m.mdd = e.m_mdd[env];
@@ -111,14 +115,14 @@ struct StockOps {
     }
   }
 
-  // stage day k: fp64 close prices of rows k, k+1 and the members' z1s rows of day k
+  // stage day k: f64 price rows p_k, u_k, p_k+1 and the members' z1s rows of day k
   __device__ __noinline__ static void stage_row(const TcParams& p, int k, int gtid, uint8_t* stg) {
     const EnvDev& e = p.e;
-    const float* mrow = e.market + (size_t)k * e.row_floats;
     double* pd = reinterpret_cast<double*>(stg + kOffP);
-    if (gtid < 2 * KP4) {
+    if (gtid < 3 * KP4) {
       const int r = gtid / KP4, kk = gtid % KP4;
-      pd[gtid] = kk < KA ? (double)__ldg(mrow + r * e.row_floats + kk) : 0.0;
+      const int row = k + (r == 2 ? 1 : 0), ch = (r == 1 ? 1 : 0);
+      pd[gtid] = kk < e.kp ? __ldg(e.px + ((size_t)row * 2 + ch) * e.kp + kk) : 0.0;
     }
     float* zs = reinterpret_cast<float*>(stg + kOffZ);
     for (int j = gtid; j < p.M * Plan::kHid; j += 128) {
@@ -284,10 +288,15 @@ struct StockOps {
         gs, st.round, st.d, stepping, st.gtid, st.bar_id, [&](int k) { stage_row(p, k, st.gtid, stg); },
         [&]() {
           const double* pd = reinterpret_cast<const double*>(stg + kOffP);
-          int ex[KA];
-          double v, vn;
           FIN_TR(threadIdx.x == 128, t, 19);
-          stock_transition<KA>(e, st.b, st.h, pd, pd + KP4, a, v, vn, ex, st.oor);
+          if (!st.have_v) {   // first step of the call: v from the state; afterwards v = last v'
+            st.vc = stock_mark<KA>(st.b, st.h, pd);
+            st.have_v = true;
+          }
+          const double v = st.vc;
+          stock_trade<KA>(e, st.b, st.h, pd, pd + KP4, a, st.oor);   // a: clamped on return
+          const double vn = stock_mark<KA>(st.b, st.h, pd + 2 * KP4);
+          st.vc = vn;
           FIN_TR(threadIdx.x == 128, t, 20);
           st.t_ep += 1;
           const bool done = st.t_ep == e.L;
@@ -300,7 +309,7 @@ struct StockOps {
           if (p.o.actions || p.o.hold) {
 #pragma unroll
             for (int k = 0; k < KA; ++k) {
-              if (p.o.actions) p.o.actions[ti * KA + k] = (int16_t)ex[k];
+              if (p.o.actions) p.o.actions[ti * KA + k] = (int16_t)a[k];
               if (p.o.hold) p.o.hold[ti * KA + k] = (int16_t)st.h[k];
             }
           }
@@ -322,6 +331,7 @@ struct StockOps {
 #pragma unroll
               for (int k = 0; k < KOU; ++k) st.ou[k] = 0.f;
               st.t_ep = 0;
+              st.vc = e.cash0;
               if (e.wadv) st.w = (st.w + 1) % e.W;
               metric_start(st.m, e.cash0);
             }
@@ -335,8 +345,7 @@ struct StockOps {
     if (p.act_only) return;
     if (st.live) {
       e.cash[env] = st.b;
-#pragma unroll
-      for (int k = 0; k < KA; ++k) e.hold[(size_t)k * e.N + env] = (int16_t)st.h[k];
+      store_hold<KA>(e, env, st.h);
       e.t_ep[env] = st.t_ep;
       e.window[env] = st.w;
       e.m_v0[env] = st.m.v0; e.m_vprev[env] = st.m.vprev; e.m_peak[env] = st.m.peak; e.m_mdd[env] = st.m.mdd;
