@@ -54,7 +54,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
         o = os.path.join(BUILD, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            cmd = [nvcc(), *ARCH, *CFLAGS, "-c", s, "-o", o]
+            cmd = [nvcc(), *ARCH, *CFLAGS, *os.environ.get("FIN_NVCC_FLAGS", "").split(), "-c", s, "-o", o]
             if ptxas_v:
                 cmd += ["-Xptxas", "-v"]
             jobs.append(cmd)

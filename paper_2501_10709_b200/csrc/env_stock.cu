@@ -17,6 +17,8 @@
 #include "group_stage.cuh"
 #include "sm100.cuh"
 
+#include <algorithm>
+
 namespace {
 
 constexpr int kThreads = 256;       // reset / get / set
@@ -54,7 +56,8 @@ __global__ void k_stock_reset(EnvDev e, const uint8_t* __restrict__ mask) {
 // KA: compile-time asset count (EXACT: KA == K) or bound (K <= KA, padding zeros).
 template <int KA>
 struct StepSmem {
-  double pr[3][KA];                         // staged day: p_d, u_d, p_{d+1}
+  uint4 save[kStep][(KA + 7) / 8];          // per-thread post-sell holdings (exact buy redo)
+  double pr[kPriceRows][KA];                // staged day (env_stock.cuh: P U MP MU PN MPN)
   GroupSlots gs;
   alignas(16) int16_t act[2][4][32 * KA];   // [buffer][warp] action rows
 };
@@ -86,95 +89,160 @@ __device__ __forceinline__ void slab_read(const int16_t* slab, int lane, int K, 
   }
 }
 
-// stage p_d, u_d (row d) and p_{d+1} (row d+1) of the f64 price table
 template <int KA>
 __device__ __forceinline__ void stage_prices(const EnvDev& e, StepSmem<KA>& sm, int d, int tid) {
-  for (int j = tid; j < 3 * KA; j += kStep) {
-    const int r = j / KA, k = j - r * KA;
-    const int row = d + (r == 2 ? 1 : 0), ch = (r == 1 ? 1 : 0);
-    sm.pr[r][k] = k < e.kp ? e.px[((size_t)row * 2 + ch) * e.kp + k] : 0.0;
-  }
+  stage_price_rows(e, &sm.pr[0][0], KA, d, tid, kStep);
 }
 
 template <int KA>
-__device__ __forceinline__ void write_rows(const EnvDev& e, const TrajDev& o, size_t ti, const int (&h)[KA],
-                                           const int (&a)[KA]) {
-  if (o.hold || o.actions) {
+__device__ __forceinline__ void write_hold_row(const EnvDev& e, const TrajDev& o, size_t ti, const int (&h)[KA]) {
+  if (o.hold) {
 #pragma unroll
-    for (int k = 0; k < KA; ++k) {
-      if (k < e.K) {
-        if (o.hold) o.hold[ti * e.K + k] = (int16_t)h[k];
-        if (o.actions) o.actions[ti * e.K + k] = (int16_t)a[k];
-      }
-    }
+    for (int k = 0; k < KA; ++k)
+      if (k < e.K) o.hold[ti * e.K + k] = (int16_t)h[k];
   }
 }
 
 // K1: one step of every env with supplied actions [N][K].
+//
+// Persistent and software-pipelined: each block walks tiles of 128 envs (stride
+// gridDim.x).  While the block computes tile j, one thread has already issued the
+// 1-D bulk-TMA copies of tile j + gridDim.x's state (cash, clock, window, holdings
+// octets) and action rows into the other shared-memory buffer, completing on an
+// mbarrier -- so the HBM latency of the loads overlaps the arithmetic instead of
+// stalling every new block (round-1 ncu: long_scoreboard was the top stall).
+// Results go straight from registers to global memory (coalesced stores).
+template <int KA>
+struct K1Buf {
+  double cash[kStep];
+  int32_t t[kStep];
+  int32_t w[kStep];
+  uint4 hold[(KA + 7) / 8][kStep];
+  alignas(16) int16_t act[kStep * KA];
+};
+template <int KA>
+struct K1Smem {
+  K1Buf<KA> buf[2];
+  uint4 save[kStep][(KA + 7) / 8];
+  double pr[kPriceRows][KA];
+  GroupSlots gs;
+  uint64_t full[2];
+};
+
+template <int KA>
+__device__ __forceinline__ void k1_issue(const EnvDev& e, const int16_t* actions, int K, K1Buf<KA>& B,
+                                         uint64_t* bar, int i0) {
+  const int ko = (K + 7) / 8;
+  const uint32_t bytes = kStep * (8 + 4 + 4) + (uint32_t)ko * kStep * 16 + kStep * K * 2;
+  sm100::mbar_arrive_expect_tx(bar, bytes);
+  sm100::bulk_g2s(B.cash, e.cash + i0, kStep * 8, bar);
+  sm100::bulk_g2s(B.t, e.t_ep + i0, kStep * 4, bar);
+  sm100::bulk_g2s(B.w, e.window + i0, kStep * 4, bar);
+  const uint4* hq = reinterpret_cast<const uint4*>(e.hold);
+  for (int o = 0; o < ko; ++o) sm100::bulk_g2s(B.hold[o], hq + (size_t)o * e.N + i0, kStep * 16, bar);
+  sm100::bulk_g2s(B.act, actions + (size_t)i0 * K, kStep * K * 2, bar);
+}
+
+#ifndef FIN_K1_MINB
+#define FIN_K1_MINB 4   // resident K1 blocks per SM the register allocation must allow
+#endif
 template <int KA, bool EXACT>
-__global__ void __launch_bounds__(kStep) k_stock_step(EnvDev e, const int16_t* __restrict__ actions, TrajDev o,
-                                                      int vec_ok) {
-  __shared__ StepSmem<KA> sm;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int i = blockIdx.x * kStep + tid;
-  const bool live = i < e.N;
+__global__ void __launch_bounds__(kStep, FIN_K1_MINB) k_stock_step(EnvDev e, const int16_t* __restrict__ actions, TrajDev o,
+                                                      int tma_ok) {
+  __shared__ K1Smem<KA> sm;
+  const int tid = threadIdx.x;
   const int K = EXACT ? KA : e.K;
-  int t = 0, w = 0;
-  double b = 0.0;
-  int h[KA];
-#pragma unroll
-  for (int k = 0; k < KA; ++k) h[k] = 0;
-  if (live) {
-    t = e.t_ep[i];
-    w = e.window[i];
-    b = e.cash[i];
-    load_hold<KA>(e, i, h);
+  const int n_tiles = (e.N + kStep - 1) / kStep;
+  const int n_full = tma_ok ? e.N / kStep : 0;   // tiles served by the bulk-copy pipeline
+  if (tid == 0) {
+    sm100::mbar_init(&sm.full[0], 1);
+    sm100::mbar_init(&sm.full[1], 1);
+    sm100::fence_mbar_init();
   }
-  const int i0 = blockIdx.x * kStep + wid * 32;
-  const int nv = max(0, min(32, e.N - i0));
-  int16_t* slab = sm.act[0][wid];
-  if (nv > 0) slab_load(slab, actions + (size_t)i0 * K, nv, K, lane, vec_ok && nv == 32);
   gs_init(&sm.gs, tid, kBar);
-  const bool stepping = live && t < e.L;
-  if (live && !stepping) {  // done env, autoreset = 0: ignored
-    set_flag(e, FIN_FLAG_EPISODE_DONE);
-    if (o.reward) o.reward[i] = 0.f;
-    if (o.done) o.done[i] = 1;
-  }
-  const int d = day_of(e, w, t);
-  const bool bad = stepping && (d < 0 || d + 1 >= e.rows);
-  if (bad) set_flag(e, FIN_FLAG_BAD_INDEX);
-  sm100::cp_async_wait<0>();
-  __syncwarp();
-  int a[KA];
-  slab_read<KA, EXACT>(slab, lane, K, live, a);
+  __syncthreads();
+  if (tid == 0 && (int)blockIdx.x < n_full) k1_issue<KA>(e, actions, K, sm.buf[0], &sm.full[0], blockIdx.x * kStep);
+  uint32_t phase = 0;
   bool oor = false;
   int round = 0;
-  group_apply(
-      &sm.gs, round, d, stepping && !bad, tid, kBar, [&](int dd) { stage_prices<KA>(e, sm, dd, tid); },
-      [&]() {
-        const double v = stock_mark<KA>(b, h, sm.pr[0]);
-        stock_trade<KA>(e, b, h, sm.pr[0], sm.pr[1], a, oor);
-        const double vn = stock_mark<KA>(b, h, sm.pr[2]);
-        t += 1;
-        const bool done = (t == e.L);
-        if (o.reward) o.reward[i] = stock_reward(e, v, vn);
-        if (o.done) o.done[i] = done ? 1 : 0;
-        if (o.cash) o.cash[i] = b;
-        if (o.asset) o.asset[i] = vn;
-        write_rows<KA>(e, o, (size_t)i, h, a);
-        if (done && e.autoreset) {
-          b = e.cash0;
+  int it = 0;
+  for (int j = blockIdx.x; j < n_tiles; j += gridDim.x, ++it) {
+    const int sb = it & 1;
+    const int jn = j + gridDim.x;
+    if (tid == 0 && jn < n_full) k1_issue<KA>(e, actions, K, sm.buf[sb ^ 1], &sm.full[sb ^ 1], jn * kStep);
+    const int i = j * kStep + tid;
+    const bool live = i < e.N;
+    const bool tma = j < n_full;
+    int t = 0, w = 0;
+    double b = 0.0;
+    int h[KA], a[KA];
 #pragma unroll
-          for (int k = 0; k < KA; ++k) h[k] = 0;
-          t = 0;
-          if (e.wadv) w = (w + 1) % e.W;
-        }
-        e.cash[i] = b;
-        store_hold<KA>(e, i, h);
-        e.t_ep[i] = t;
-        if (e.wadv) e.window[i] = w;
-      });
+    for (int k = 0; k < KA; ++k) h[k] = 0;
+    K1Buf<KA>& B = sm.buf[sb];
+    if (tma) {
+      sm100::mbar_wait(&sm.full[sb], (phase >> sb) & 1u);
+      phase ^= 1u << sb;
+      t = B.t[tid];
+      w = B.w[tid];
+      b = B.cash[tid];
+#pragma unroll
+      for (int oc = 0; oc < (KA + 7) / 8; ++oc) {
+        const uint4 v = B.hold[oc][tid];
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (8 * oc + q < KA) h[8 * oc + q] = (int)((q & 1) ? (wv[q >> 1] >> 16) : (wv[q >> 1] & 0xffffu));
+      }
+      slab_read<KA, EXACT>(B.act, tid, K, true, a);
+    } else if (live) {   // ragged last tile / unaligned actions: direct loads
+      t = e.t_ep[i];
+      w = e.window[i];
+      b = e.cash[i];
+      load_hold<KA>(e, i, h);
+#pragma unroll
+      for (int k = 0; k < KA; ++k) a[k] = (k < K) ? (int)actions[(size_t)i * K + k] : 0;
+    } else {
+#pragma unroll
+      for (int k = 0; k < KA; ++k) a[k] = 0;
+    }
+    const bool stepping = live && t < e.L;
+    if (live && !stepping) {  // done env, autoreset = 0: ignored
+      set_flag(e, FIN_FLAG_EPISODE_DONE);
+      if (o.reward) o.reward[i] = 0.f;
+      if (o.done) o.done[i] = 1;
+    }
+    const int d = day_of(e, w, t);
+    const bool bad = stepping && (d < 0 || d + 1 >= e.rows);
+    if (bad) set_flag(e, FIN_FLAG_BAD_INDEX);
+    group_apply(
+        &sm.gs, round, d, stepping && !bad, tid, kBar,
+        [&](int dd) { stage_price_rows(e, &sm.pr[0][0], KA, dd, tid, kStep); },
+        [&]() {
+          const double v = stock_mark<KA>(b, h, sm.pr[kRowP], sm.pr[kRowMP]);
+          stock_trade<KA>(e, b, h, &sm.pr[0][0], KA, a, oor, sm.save[tid],
+                          o.actions ? o.actions + (size_t)i * K : nullptr);
+          const double vn = stock_mark<KA>(b, h, sm.pr[kRowPN], sm.pr[kRowMPN]);
+          t += 1;
+          const bool done = (t == e.L);
+          if (o.reward) o.reward[i] = stock_reward(e, v, vn);
+          if (o.done) o.done[i] = done ? 1 : 0;
+          if (o.cash) o.cash[i] = b;
+          if (o.asset) o.asset[i] = vn;
+          write_hold_row<KA>(e, o, (size_t)i, h);
+          if (done && e.autoreset) {
+            b = e.cash0;
+#pragma unroll
+            for (int k = 0; k < KA; ++k) h[k] = 0;
+            t = 0;
+            if (e.wadv) w = (w + 1) % e.W;
+          }
+          e.cash[i] = b;
+          store_hold<KA>(e, i, h);
+          e.t_ep[i] = t;
+          if (e.wadv) e.window[i] = w;
+        });
+    __syncthreads();   // buffer sb is refilled two tiles from now: everyone has read it
+  }
   if (oor) set_flag(e, FIN_FLAG_ACTION_RANGE);
 }
 
@@ -234,10 +302,11 @@ __global__ void __launch_bounds__(kStep) k_stock_replay(EnvDev e, const int16_t*
     group_apply(
         &sm.gs, round, d, stepping && !bad, tid, kBar, [&](int dd) { stage_prices<KA>(e, sm, dd, tid); },
         [&]() {
-          if (!have_v) { vc = stock_mark<KA>(b, h, sm.pr[0]); have_v = true; }
+          if (!have_v) { vc = stock_mark<KA>(b, h, sm.pr[kRowP], sm.pr[kRowMP]); have_v = true; }
           const double v = vc;
-          stock_trade<KA>(e, b, h, sm.pr[0], sm.pr[1], a, oor);
-          const double vn = stock_mark<KA>(b, h, sm.pr[2]);
+          stock_trade<KA>(e, b, h, &sm.pr[0][0], KA, a, oor, sm.save[tid],
+                          o.actions ? o.actions + ti * K : nullptr);
+          const double vn = stock_mark<KA>(b, h, sm.pr[kRowPN], sm.pr[kRowMPN]);
           vc = vn;
           t += 1;
           const bool done = (t == e.L);
@@ -247,7 +316,7 @@ __global__ void __launch_bounds__(kStep) k_stock_replay(EnvDev e, const int16_t*
           if (o.done) o.done[ti] = done ? 1 : 0;
           if (o.cash) o.cash[ti] = b;
           if (o.asset) o.asset[ti] = vn;
-          write_rows<KA>(e, o, ti, h, a);
+          write_hold_row<KA>(e, o, ti, h);
           metric_push(m, vn);
           if (done) {
             double em[3];
@@ -346,6 +415,8 @@ inline int vec_ok(const void* p, long long elems_per_step) {
 
 namespace fin {
 
+int num_sms();
+
 // K = 30 (C1) and K = 4 (C0) are compiled exactly; any other K runs in the next
 // power-of-two bound with zero padding.
 #define FIN_DISPATCH_K(K, KERNEL, GRID, STREAM, ...)                                         \
@@ -362,9 +433,27 @@ cudaError_t launch_stock_reset(const EnvDev& e, const uint8_t* mask, cudaStream_
   return cudaGetLastError();
 }
 
+// persistent grid for K1: resident blocks per SM (occupancy API) x SMs, capped by the tiles
+template <int KA, bool EXACT>
+int k1_grid(int N) {
+  static int per_sm = 0;
+  if (per_sm == 0 &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stock_step<KA, EXACT>, kStep, 0) != cudaSuccess)
+    per_sm = 1;
+  if (per_sm < 1) per_sm = 1;
+  const int tiles = (N + kStep - 1) / kStep;
+  return std::min(tiles, per_sm * num_sms());
+}
+
 cudaError_t launch_stock_step(const EnvDev& e, const int16_t* actions, const TrajDev& o, cudaStream_t s) {
-  const int v = vec_ok(actions, 8);   // K1 reads one step: per-warp rows are 64 K bytes
-  FIN_DISPATCH_K(e.K, k_stock_step, blocks_for(e.N, kStep), s, e, actions, o, v);
+  const int v = vec_ok(actions, 8);   // bulk copies of whole 128-env tiles: 256 K bytes each
+#define FIN_K1(KA, EX) k_stock_step<KA, EX><<<k1_grid<KA, EX>(e.N), kStep, 0, s>>>(e, actions, o, v)
+  if (e.K == 30) FIN_K1(30, true);
+  else if (e.K == 4) FIN_K1(4, true);
+  else if (e.K <= 8) FIN_K1(8, false);
+  else if (e.K <= 16) FIN_K1(16, false);
+  else FIN_K1(32, false);
+#undef FIN_K1
   return cudaGetLastError();
 }
 

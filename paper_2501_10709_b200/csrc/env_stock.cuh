@@ -15,26 +15,84 @@
 #pragma once
 #include "fin_internal.cuh"
 
-// P / U: row d of the f64 price table -- close p_k (exact widening of the fp32
-// market) and u_k = fl(p_k * up) -- in shared or global memory.  Padding assets
-// (k >= K) carry p = u = 0, h = 0 and a = 0, so every loop below runs to the
-// compile-time KA with no per-asset predicate: a padded asset adds +0 to the cash
-// (b is never -0) and to the sums, which leaves them bit-identical.
+// Price rows of one step, staged in shared memory (or read from global memory):
+//   P  = p_d   close of the execution day (exact widening of the fp32 market)
+//   U  = u_d   = fl(p_d * (1 + c)), the buy price per share
+//   MP = -2^52 p_d,  MU = -2^52 u_d   (exact scalings)
+//   RU = fl(1 / u_d)                  (estimate of the affordable count only)
+//   PN = p_d+1, MPN = -2^52 p_d+1     (marking day)
+// Products n * x with a non-negative int n are formed as fma(2^52 + n, x, -2^52 x):
+// the exact value is n * x, so the single rounding of the fma gives fl(n * x) --
+// the same bits as converting n and multiplying, with neither the XU-pipe I2F
+// conversion nor a separate subtract.  2^52 + n is the bit pattern 0x43300000:n.
+// Padding assets (k >= K) carry zeros in every row and in h and a, so every loop
+// runs to the compile-time KA with no per-asset predicate: a padded asset adds +0
+// to the cash (b is never -0) and to the sums, which leaves them bit-identical.
+enum { kRowP = 0, kRowU, kRowMP, kRowMU, kRowRU, kRowPN, kRowMPN, kPriceRows };
+
+// Register-pressure control.  Left alone, ptxas hoists all 2-3 x 30 f64 row loads of
+// a loop to its top (255 registers and spills).  The rows of asset chunk c+1 are
+// therefore addressed through an offset computed from the loop's running value at
+// the start of chunk c: (x >> 31) with x the high word of a non-negative double or a
+// non-negative int, which is 0 at run time but not provably so at compile time.  At
+// most two chunks of row values are live.
+constexpr int kChunk = 6;
+__device__ __forceinline__ int zdep(double x) { return __double2hiint(x) >> 31; }
+__device__ __forceinline__ int zdep(int x) { return x >> 31; }
+#define FIN_CHUNKED(KA, dep_expr, BODY)                                            \
+  {                                                                                \
+    int off_ = 0;                                                                  \
+    _Pragma("unroll") for (int c_ = 0; c_ < (KA); c_ += kChunk) {                  \
+      const int o_ = off_;                                                         \
+      off_ = zdep(dep_expr);                                                       \
+      _Pragma("unroll") for (int k = c_; k < (c_ + kChunk < (KA) ? c_ + kChunk : (KA)); ++k) { BODY } \
+    }                                                                              \
+  }
+
+__device__ __forceinline__ double nprod(int n, double x, double mx) {
+  return __fma_rn(__hiloint2double(0x43300000, n), x, mx);
+}
 
 // v = b + sum_k h_k p_k, ascending k (each product is exact: h < 2^15, p has 24 bits)
 template <int KA>
-__device__ __forceinline__ double stock_mark(double b, const int (&h)[KA], const double* P) {
+__device__ __forceinline__ double stock_mark(double b, const int (&h)[KA], const double* P, const double* MP) {
   double acc = b;
-#pragma unroll
-  for (int k = 0; k < KA; ++k) acc = fadd64(acc, fmul64(nn2d(h[k]), P[k]));
+  FIN_CHUNKED(KA, acc, acc = fadd64(acc, nprod(h[k], P[k + o_], MP[k + o_]));)
   return acc;
 }
 
-// The trade of one step.  a[] holds the requested deltas on entry and the clamped
-// deltas (R6) on exit; h[] and b are updated in place.
+// Buys of one step in the definition's order (R5): each asset the largest n <= want
+// with fl(n u) <= b.  Out of line: only the rare steps where some request is not
+// affordable come here.
+static __device__ __noinline__ double stock_buys_exact(double b, int* h, const int* a, int K, const double* U,
+                                                       const double* MU) {
+  for (int k = 0; k < K; ++k) {
+    const int want = max(min(a[k], FIN_HOLD_MAX - h[k]), 0);
+    double c = nprod(want, U[k], MU[k]);
+    int n = want;
+    if (!(c <= b)) {
+      n = affordable_slow(b, U[k], want);
+      c = nprod(n, U[k], MU[k]);
+    }
+    b = fsub64(b, c);
+    h[k] += n;
+  }
+  return b;
+}
+
+// The trade of one step; R[r * RS + k] is row r of the staged rows above.  a[]
+// holds the requested deltas on entry and the clamped deltas (R6) on exit; h[] and
+// b are updated in place.  ``save`` (16-B aligned, (KA+7)/8 uint4; shared or local
+// memory) receives the post-sell holdings for the rare exact redo of the buys;
+// ``act_out`` (nullable) the clamped actions.
 template <int KA>
-__device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)[KA], const double* P,
-                                            const double* U, int (&a)[KA], bool& oor) {
+__device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)[KA], const double* R, int RS,
+                                            int (&a)[KA], bool& oor, uint4* save, int16_t* act_out) {
+  const double* P = R + kRowP * RS;
+  const double* U = R + kRowU * RS;
+  const double* MP = R + kRowMP * RS;
+  const double* MU = R + kRowMU * RS;
+  const double* RU = R + kRowRU * RS;
   // 2. clamp (R6); any clamped entry sets the sticky range flag
   int diff = 0;
 #pragma unroll
@@ -42,32 +100,70 @@ __device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)
     const int x = min(max(a[k], -e.max_trade), e.max_trade);
     diff |= x ^ a[k];
     a[k] = x;
+    if (act_out) act_out[k] = (int16_t)x;
   }
   oor |= diff != 0;
   // 3. sells, clipped to holdings: b += fl(fl(n p) (1 - c)); n = 0 adds +0
-#pragma unroll
-  for (int k = 0; k < KA; ++k) {
+  FIN_CHUNKED(KA, b, {
     const int n = max(min(-a[k], h[k]), 0);
-    b = fadd64(b, fmul64(fmul64(nn2d(n), P[k]), e.dn));
+    b = fadd64(b, fmul64(nprod(n, P[k + o_], MP[k + o_]), e.dn));
     h[k] -= n;
-  }
-  // 4. buys, ascending k, each the largest affordable count at u (R5); the fast
-  //    path (the whole request is affordable) reuses the product it tested
+  })
+  // 4. buys, ascending k, each n = min(want, f) with f the largest count whose cost
+  //    fl(f u) fits the cash (R5).  Branch-free: f = floor(b * fl(1/u)) from one
+  //    round-down add (its bits are 2^52 + f, the biased operand nprod needs), then
+  //    the definition is verified on the chosen n -- fl(n u) <= b and, when the cash
+  //    binds, fl((n + 1) u) > b.  A failed check (x within ~1e-11 of an integer, NaN
+  //    cash) sends the step's buys to the exact out-of-line loop.
+  const double bpre = b;
 #pragma unroll
-  for (int k = 0; k < KA; ++k) {
-    const int want = max(min(a[k], FIN_HOLD_MAX - h[k]), 0);
-    const double u = U[k];
-    double c = fmul64(nn2d(want), u);
-    int n = want;
-    if (!(c <= b)) {
-      n = affordable_slow(b, u, want);
-      c = fmul64(nn2d(n), u);
+  for (int o = 0; o < (KA + 7) / 8; ++o) {   // post-sell holdings, packed, for the exact redo
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k0 = 8 * o + 2 * j, k1 = k0 + 1;
+      w[j] = __byte_perm(k0 < KA ? (uint32_t)h[k0] : 0u, k1 < KA ? (uint32_t)h[k1] : 0u, 0x5410);
     }
-    b = fsub64(b, c);
+    save[o] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  bool miss = false;
+  FIN_CHUNKED(KA, b, {
+    const int want = max(min(a[k], FIN_HOLD_MAX - h[k]), 0);
+    const double D = __dadd_rd(fmul64(b, RU[k + o_]), 4503599627370496.0);
+    const int f = (__double2hiint(D) == 0x43300000) ? __double2loint(D) : 0x7fffffff;
+    const int n = min(want, f);
+    const double cn = nprod(n, U[k + o_], MU[k + o_]);
+    const double cn1 = nprod(n + 1, U[k + o_], MU[k + o_]);
+    miss |= (!(cn <= b)) | ((n < want) & !(cn1 > b));
+    b = fsub64(b, cn);
     h[k] += n;
+  })
+  if (miss) {   // rare: arrays in local memory only on this path
+    int hh[KA], aa[KA];
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(save);
+#pragma unroll
+    for (int k = 0; k < KA; ++k) {
+      hh[k] = (int)((k & 1) ? (sw[k >> 1] >> 16) : (sw[k >> 1] & 0xffffu));
+      aa[k] = a[k];
+    }
+    b = stock_buys_exact(bpre, hh, aa, KA, U, MU);
+#pragma unroll
+    for (int k = 0; k < KA; ++k) h[k] = hh[k];
   }
 }
 
+// stage the price rows of day d from the f64 table px[rows][2][kp] into pr[kPriceRows][RS]
+// (threads tid = 0 .. nthr-1 of the staging group)
+__device__ __forceinline__ void stage_price_rows(const EnvDev& e, double* pr, int RS, int d, int tid, int nthr) {
+  for (int j = tid; j < kPriceRows * RS; j += nthr) {
+    const int r = j / RS, k = j - r * RS;
+    const int row = d + (r >= kRowPN ? 1 : 0), ch = (r == kRowU || r == kRowMU || r == kRowRU) ? 1 : 0;
+    const double x = k < e.kp ? e.px[((size_t)row * 2 + ch) * e.kp + k] : 0.0;
+    pr[j] = (r == kRowMP || r == kRowMU || r == kRowMPN) ? x * -4503599627370496.0
+            : (r == kRowRU)                          ? (x > 0.0 ? 1.0 / x : 0.0)
+                                                     : x;
+  }
+}
 // reward = (v' - v) * scale (exact power-of-two scale), stored fp32
 __device__ __forceinline__ float stock_reward(const EnvDev& e, double v, double vn) {
   return (float)fmul64(fsub64(vn, v), e.scale);

@@ -54,9 +54,9 @@ struct StockOps {
   static constexpr int KT8 = Plan::kIn / 8;
   using Obs = StockObs<KA, IA>;
   static_assert(Obs::kEnvPad == Plan::kIn, "factored layer 1: the network input is the private part");
-  // staging: p_d, u_d, p_d+1 (f64) | z1s rows of day d per member (f32) | slots | broadcast
+  // staging: price rows of day d (f64, env_stock.cuh) | z1s rows of day d per member (f32) | slots | broadcast
   static constexpr int kOffP = 0;
-  static constexpr int kOffZ = 3 * KP4 * 8;
+  static constexpr int kOffZ = kPriceRows * KP4 * 8;
   static constexpr int kOffS = kOffZ + FIN_MAX_MEMBERS * Plan::kHid * 4;
   static constexpr int kOffB = kOffS + 16;
   static constexpr int kStageBytes = kOffB + 16;
@@ -93,7 +93,6 @@ struct StockOps {
     agg_init(st.agg);
     if (st.live) {
       st.b = e.cash[env];
-#pragma unroll
       load_hold<KA>(e, env, st.h);
       st.t_ep = e.t_ep[env];
       st.w = e.window[env];
@@ -118,12 +117,7 @@ struct StockOps {
   // stage day k: f64 price rows p_k, u_k, p_k+1 and the members' z1s rows of day k
   __device__ __noinline__ static void stage_row(const TcParams& p, int k, int gtid, uint8_t* stg) {
     const EnvDev& e = p.e;
-    double* pd = reinterpret_cast<double*>(stg + kOffP);
-    if (gtid < 3 * KP4) {
-      const int r = gtid / KP4, kk = gtid % KP4;
-      const int row = k + (r == 2 ? 1 : 0), ch = (r == 1 ? 1 : 0);
-      pd[gtid] = kk < e.kp ? __ldg(e.px + ((size_t)row * 2 + ch) * e.kp + kk) : 0.0;
-    }
+    stage_price_rows(e, reinterpret_cast<double*>(stg + kOffP), KP4, k, gtid, 128);
     float* zs = reinterpret_cast<float*>(stg + kOffZ);
     for (int j = gtid; j < p.M * Plan::kHid; j += 128) {
       const int m = j / Plan::kHid, n = j % Plan::kHid;
@@ -290,12 +284,14 @@ struct StockOps {
           const double* pd = reinterpret_cast<const double*>(stg + kOffP);
           FIN_TR(threadIdx.x == 128, t, 19);
           if (!st.have_v) {   // first step of the call: v from the state; afterwards v = last v'
-            st.vc = stock_mark<KA>(st.b, st.h, pd);
+            st.vc = stock_mark<KA>(st.b, st.h, pd + kRowP * KP4, pd + kRowMP * KP4);
             st.have_v = true;
           }
           const double v = st.vc;
-          stock_trade<KA>(e, st.b, st.h, pd, pd + KP4, a, st.oor);   // a: clamped on return
-          const double vn = stock_mark<KA>(st.b, st.h, pd + 2 * KP4);
+          uint4 save[(KA + 7) / 8];   // local: read only by the rare exact buy redo
+          stock_trade<KA>(e, st.b, st.h, pd, KP4, a, st.oor, save,
+                          p.o.actions ? p.o.actions + ti * KA : nullptr);   // a: clamped on return
+          const double vn = stock_mark<KA>(st.b, st.h, pd + kRowPN * KP4, pd + kRowMPN * KP4);
           st.vc = vn;
           FIN_TR(threadIdx.x == 128, t, 20);
           st.t_ep += 1;
@@ -306,12 +302,9 @@ struct StockOps {
           if (p.o.done) p.o.done[ti] = done ? 1 : 0;
           if (p.o.cash) p.o.cash[ti] = st.b;
           if (p.o.asset) p.o.asset[ti] = vn;
-          if (p.o.actions || p.o.hold) {
+          if (p.o.hold) {
 #pragma unroll
-            for (int k = 0; k < KA; ++k) {
-              if (p.o.actions) p.o.actions[ti * KA + k] = (int16_t)a[k];
-              if (p.o.hold) p.o.hold[ti * KA + k] = (int16_t)st.h[k];
-            }
+            for (int k = 0; k < KA; ++k) p.o.hold[ti * KA + k] = (int16_t)st.h[k];
           }
           metric_push(st.m, vn);
           FIN_TR(threadIdx.x == 128, t, 21);

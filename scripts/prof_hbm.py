@@ -22,17 +22,36 @@ from synth import market  # noqa: E402
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+flush_r = torch.ones(256 << 18, dtype=torch.float32, device="cuda")
+
+
+def flush_l2():
+    """Write 256 MiB, then read another 256 MiB: the written lines are evicted (and
+    written back) by the read pass, so the timed kernel starts on a clean L2."""
+    flush.zero_()
+    flush_r.sum()
 M = market.stock_c1(rows=1008)
 res = {}
+
+
+MODE = os.environ.get("FIN_TIMING", "flush")   # flush | b2b
 
 
 def timed(fn, warm=3):
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
+    if MODE == "b2b":   # back-to-back launches over a working set far above L2
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
     ts = []
     for _ in range(reps):
-        flush.zero_()
+        flush_l2()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         fn()
