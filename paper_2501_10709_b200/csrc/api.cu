@@ -290,7 +290,7 @@ int fin_env_create(const fin_env_config* cfg, const float* market, int64_t marke
   const size_t N = (size_t)c.num_envs, K = (size_t)d.K;
   // one allocation for all state arrays (8-byte members first)
   const size_t n8 = N * 8;  // cash + 6 metric doubles
-  size_t bytes = 7 * n8 * sizeof(double) / 8;   // 7 double arrays
+  size_t bytes = 8 * n8 * sizeof(double) / 8;   // 8 double arrays
   bytes += (size_t)FIN_MAX_MEMBERS * K * N * sizeof(float);
   bytes += N * 4 * sizeof(int32_t);              // t_ep, window, tau, m_n
   const size_t KO = (K + 7) / 8;                 // holdings: asset octets (hold_at)
@@ -306,6 +306,7 @@ int fin_env_create(const fin_env_config* cfg, const float* market, int64_t marke
   uint8_t* p = static_cast<uint8_t*>(env->state_mem);
   auto take = [&](size_t b) { uint8_t* r = p; p += (b + 15) / 16 * 16; return r; };
   d.cash = reinterpret_cast<double*>(take(N * 8));
+  d.vcur = reinterpret_cast<double*>(take(N * 8));
   d.m_v0 = reinterpret_cast<double*>(take(N * 8));
   d.m_vprev = reinterpret_cast<double*>(take(N * 8));
   d.m_peak = reinterpret_cast<double*>(take(N * 8));
@@ -323,17 +324,27 @@ int fin_env_create(const fin_env_config* cfg, const float* market, int64_t marke
     delete env;
     return fail(FIN_E_CONFIG, "internal: state layout overflow");
   }
-  // market copy | flags word | (stock) f64 price table px[rows][2][kp]: close p and
-  // u = fl(p * (1 + c)), both exact host double operations (one rounding for u)
+  // market copy | flags word | (stock) f64 price rows px[rows][kPriceRows][kp]
+  // (fin_internal.cuh), each entry one IEEE double operation on the host: p exact,
+  // u = fl(p (1 + c)), the -2^52 scalings exact, fl(1 / u); padding assets stay 0
   const size_t mbytes = (size_t)c.num_rows * d.row_floats * sizeof(float);
   std::vector<double> px;
   if (c.task == FIN_STOCK) {
-    px.assign((size_t)c.num_rows * 2 * d.kp, 0.0);
+    const double m52 = -4503599627370496.0;
+    px.assign((size_t)c.num_rows * kPriceRows * d.kp, 0.0);
     for (int r = 0; r < c.num_rows; ++r)
       for (int k = 0; k < d.K; ++k) {
+        double* row = px.data() + (size_t)r * kPriceRows * d.kp;
         const double pk = (double)padded[(size_t)r * d.row_floats + k];
-        px[((size_t)r * 2 + 0) * d.kp + k] = pk;
-        px[((size_t)r * 2 + 1) * d.kp + k] = pk * d.up;
+        const double uk = pk * d.up;
+        const double pn = r + 1 < c.num_rows ? (double)padded[(size_t)(r + 1) * d.row_floats + k] : 0.0;
+        row[kRowP * d.kp + k] = pk;
+        row[kRowU * d.kp + k] = uk;
+        row[kRowMP * d.kp + k] = pk * m52;
+        row[kRowMU * d.kp + k] = uk * m52;
+        row[kRowRU * d.kp + k] = 1.0 / uk;
+        row[kRowPN * d.kp + k] = pn;
+        row[kRowMPN * d.kp + k] = pn * m52;
       }
   }
   const size_t pxbytes = px.size() * sizeof(double);

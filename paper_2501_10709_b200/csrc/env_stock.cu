@@ -41,6 +41,7 @@ __global__ void k_stock_reset(EnvDev e, const uint8_t* __restrict__ mask) {
   if (i >= e.N) return;
   if (mask && !mask[i]) return;
   e.cash[i] = e.cash0;
+  e.vcur[i] = e.cash0;
   uint4* q = reinterpret_cast<uint4*>(e.hold);
   for (int o = 0; o < (e.K + 7) / 8; ++o) q[(size_t)o * e.N + i] = make_uint4(0u, 0u, 0u, 0u);
   e.t_ep[i] = 0;
@@ -57,8 +58,10 @@ __global__ void k_stock_reset(EnvDev e, const uint8_t* __restrict__ mask) {
 template <int KA>
 struct StepSmem {
   uint4 save[kStep][(KA + 7) / 8];          // per-thread post-sell holdings (exact buy redo)
-  double pr[kPriceRows][KA];                // staged day (env_stock.cuh: P U MP MU PN MPN)
+  alignas(16) double pr[2][kPriceRows * ((KA + 3) / 4 * 4)];   // price rows, [buffer]
   GroupSlots gs;
+  uint64_t rows[2];
+  int pred[2];
   alignas(16) int16_t act[2][4][32 * KA];   // [buffer][warp] action rows
 };
 
@@ -90,11 +93,6 @@ __device__ __forceinline__ void slab_read(const int16_t* slab, int lane, int K, 
 }
 
 template <int KA>
-__device__ __forceinline__ void stage_prices(const EnvDev& e, StepSmem<KA>& sm, int d, int tid) {
-  stage_price_rows(e, &sm.pr[0][0], KA, d, tid, kStep);
-}
-
-template <int KA>
 __device__ __forceinline__ void write_hold_row(const EnvDev& e, const TrajDev& o, size_t ti, const int (&h)[KA]) {
   if (o.hold) {
 #pragma unroll
@@ -112,9 +110,15 @@ __device__ __forceinline__ void write_hold_row(const EnvDev& e, const TrajDev& o
 // mbarrier -- so the HBM latency of the loads overlaps the arithmetic instead of
 // stalling every new block (round-1 ncu: long_scoreboard was the top stall).
 // Results go straight from registers to global memory (coalesced stores).
+// The f64 price rows of a tile's day (kPriceRows x kp doubles, one contiguous block
+// of px) are prefetched the same way, one tile ahead, for the day PREDICTED from
+// the current tile (envs step in lockstep and their windows advance together, so
+// the next tile's window is its initial window shifted like this tile's).  A wrong
+// prediction only costs a restage (group_apply).
 template <int KA>
 struct K1Buf {
   double cash[kStep];
+  double v[kStep];
   int32_t t[kStep];
   int32_t w[kStep];
   uint4 hold[(KA + 7) / 8][kStep];
@@ -124,18 +128,41 @@ template <int KA>
 struct K1Smem {
   K1Buf<KA> buf[2];
   uint4 save[kStep][(KA + 7) / 8];
-  double pr[kPriceRows][KA];
-  GroupSlots gs;
-  uint64_t full[2];
+  alignas(16) double pr[2][kPriceRows * ((KA + 3) / 4 * 4)];
+  uint64_t full[2];    // state + actions of the buffer's tile landed (TMA)
+  uint64_t rows[2];    // price rows of the buffer's predicted day landed (TMA), or no prediction
+  uint64_t empty[2];   // the 4 warps are done with the buffer (state and rows)
+  int pred[2];
 };
+
+// day of the next tile predicted from (t0, w0) of global env g0 of this tile
+__device__ __forceinline__ int predict_day(const EnvDev& e, int t0, int w0, int64_t g0, int64_t gn) {
+  const int shift = ((w0 - window_of(e, g0)) % e.W + e.W) % e.W;
+  return day_of(e, (window_of(e, gn) + shift) % e.W, t0);
+}
+
+// thread 0: publish the prediction, then bulk-copy the price rows of day d into pr
+// (completing on bar); with no usable prediction the barrier phase completes at once
+__device__ __forceinline__ void rows_issue(const EnvDev& e, double* pr, uint64_t* bar, int* pred, int d) {
+  if (d >= 0 && d + 1 < e.rows) {
+    *pred = d;
+    const uint32_t bytes = kPriceRows * e.kp * 8;
+    sm100::mbar_arrive_expect_tx(bar, bytes);
+    sm100::bulk_g2s(pr, e.px + (size_t)d * kPriceRows * e.kp, bytes, bar);
+  } else {
+    *pred = -1;
+    sm100::mbar_arrive(bar);
+  }
+}
 
 template <int KA>
 __device__ __forceinline__ void k1_issue(const EnvDev& e, const int16_t* actions, int K, K1Buf<KA>& B,
                                          uint64_t* bar, int i0) {
   const int ko = (K + 7) / 8;
-  const uint32_t bytes = kStep * (8 + 4 + 4) + (uint32_t)ko * kStep * 16 + kStep * K * 2;
+  const uint32_t bytes = kStep * (8 + 8 + 4 + 4) + (uint32_t)ko * kStep * 16 + kStep * K * 2;
   sm100::mbar_arrive_expect_tx(bar, bytes);
   sm100::bulk_g2s(B.cash, e.cash + i0, kStep * 8, bar);
+  sm100::bulk_g2s(B.v, e.vcur + i0, kStep * 8, bar);
   sm100::bulk_g2s(B.t, e.t_ep + i0, kStep * 4, bar);
   sm100::bulk_g2s(B.w, e.window + i0, kStep * 4, bar);
   const uint4* hq = reinterpret_cast<const uint4*>(e.hold);
@@ -146,35 +173,44 @@ __device__ __forceinline__ void k1_issue(const EnvDev& e, const int16_t* actions
 #ifndef FIN_K1_MINB
 #define FIN_K1_MINB 4   // resident K1 blocks per SM the register allocation must allow
 #endif
+// No block-wide barrier inside the tile loop: warps are decoupled by the full / rows
+// / empty mbarriers, and an env whose day is not the predicted one reads its rows
+// from the (L2-resident) global table instead of a restaged copy.
 template <int KA, bool EXACT>
-__global__ void __launch_bounds__(kStep, FIN_K1_MINB) k_stock_step(EnvDev e, const int16_t* __restrict__ actions, TrajDev o,
-                                                      int tma_ok) {
-  __shared__ K1Smem<KA> sm;
-  const int tid = threadIdx.x;
+__global__ void __launch_bounds__(kStep, FIN_K1_MINB)
+    k_stock_step(EnvDev e, const int16_t* __restrict__ actions, TrajDev o, int tma_ok) {
+  extern __shared__ __align__(16) uint8_t k1_smem[];   // dynamic: > 48 KB static limit
+  K1Smem<KA>& sm = *reinterpret_cast<K1Smem<KA>*>(k1_smem);
+  const int tid = threadIdx.x, lane = tid & 31;
   const int K = EXACT ? KA : e.K;
   const int n_tiles = (e.N + kStep - 1) / kStep;
   const int n_full = tma_ok ? e.N / kStep : 0;   // tiles served by the bulk-copy pipeline
+  const int RS = EXACT ? (KA + 3) / 4 * 4 : e.kp;   // staged row stride (= kp)
   if (tid == 0) {
-    sm100::mbar_init(&sm.full[0], 1);
-    sm100::mbar_init(&sm.full[1], 1);
+    for (int q = 0; q < 2; ++q) {
+      sm100::mbar_init(&sm.full[q], 1);
+      sm100::mbar_init(&sm.rows[q], 1);
+      sm100::mbar_init(&sm.empty[q], kStep / 32);
+    }
     sm100::fence_mbar_init();
   }
-  gs_init(&sm.gs, tid, kBar);
   __syncthreads();
-  if (tid == 0 && (int)blockIdx.x < n_full) k1_issue<KA>(e, actions, K, sm.buf[0], &sm.full[0], blockIdx.x * kStep);
-  uint32_t phase = 0;
+  if (tid == 0 && (int)blockIdx.x < n_tiles) {
+    const int i0 = blockIdx.x * kStep;
+    if ((int)blockIdx.x < n_full) k1_issue<KA>(e, actions, K, sm.buf[0], &sm.full[0], i0);
+    rows_issue(e, sm.pr[0], &sm.rows[0], &sm.pred[0], day_of(e, __ldg(e.window + i0), __ldg(e.t_ep + i0)));
+  }
+  uint32_t phase = 0, rphase = 0, ephase = 0;
   bool oor = false;
-  int round = 0;
   int it = 0;
   for (int j = blockIdx.x; j < n_tiles; j += gridDim.x, ++it) {
     const int sb = it & 1;
     const int jn = j + gridDim.x;
-    if (tid == 0 && jn < n_full) k1_issue<KA>(e, actions, K, sm.buf[sb ^ 1], &sm.full[sb ^ 1], jn * kStep);
     const int i = j * kStep + tid;
     const bool live = i < e.N;
     const bool tma = j < n_full;
     int t = 0, w = 0;
-    double b = 0.0;
+    double b = 0.0, v = 0.0;
     int h[KA], a[KA];
 #pragma unroll
     for (int k = 0; k < KA; ++k) h[k] = 0;
@@ -185,6 +221,7 @@ __global__ void __launch_bounds__(kStep, FIN_K1_MINB) k_stock_step(EnvDev e, con
       t = B.t[tid];
       w = B.w[tid];
       b = B.cash[tid];
+      v = B.v[tid];
 #pragma unroll
       for (int oc = 0; oc < (KA + 7) / 8; ++oc) {
         const uint4 v = B.hold[oc][tid];
@@ -198,12 +235,24 @@ __global__ void __launch_bounds__(kStep, FIN_K1_MINB) k_stock_step(EnvDev e, con
       t = e.t_ep[i];
       w = e.window[i];
       b = e.cash[i];
+      v = e.vcur[i];
       load_hold<KA>(e, i, h);
 #pragma unroll
       for (int k = 0; k < KA; ++k) a[k] = (k < K) ? (int)actions[(size_t)i * K + k] : 0;
     } else {
 #pragma unroll
       for (int k = 0; k < KA; ++k) a[k] = 0;
+    }
+    // producer (thread 0): once the 4 warps are done with the other buffer (tile j - G),
+    // refill it with tile jn's state and the rows of its predicted day
+    if (tid == 0 && jn < n_tiles) {
+      if (it >= 1) {
+        sm100::mbar_wait(&sm.empty[sb ^ 1], (ephase >> (sb ^ 1)) & 1u);
+        ephase ^= 1u << (sb ^ 1);
+      }
+      if (jn < n_full) k1_issue<KA>(e, actions, K, sm.buf[sb ^ 1], &sm.full[sb ^ 1], jn * kStep);
+      rows_issue(e, sm.pr[sb ^ 1], &sm.rows[sb ^ 1], &sm.pred[sb ^ 1],
+                 predict_day(e, t, w, e.env_offset + (int64_t)j * kStep, e.env_offset + (int64_t)jn * kStep));
     }
     const bool stepping = live && t < e.L;
     if (live && !stepping) {  // done env, autoreset = 0: ignored
@@ -214,34 +263,37 @@ __global__ void __launch_bounds__(kStep, FIN_K1_MINB) k_stock_step(EnvDev e, con
     const int d = day_of(e, w, t);
     const bool bad = stepping && (d < 0 || d + 1 >= e.rows);
     if (bad) set_flag(e, FIN_FLAG_BAD_INDEX);
-    group_apply(
-        &sm.gs, round, d, stepping && !bad, tid, kBar,
-        [&](int dd) { stage_price_rows(e, &sm.pr[0][0], KA, dd, tid, kStep); },
-        [&]() {
-          const double v = stock_mark<KA>(b, h, sm.pr[kRowP], sm.pr[kRowMP]);
-          stock_trade<KA>(e, b, h, &sm.pr[0][0], KA, a, oor, sm.save[tid],
-                          o.actions ? o.actions + (size_t)i * K : nullptr);
-          const double vn = stock_mark<KA>(b, h, sm.pr[kRowPN], sm.pr[kRowMPN]);
-          t += 1;
-          const bool done = (t == e.L);
-          if (o.reward) o.reward[i] = stock_reward(e, v, vn);
-          if (o.done) o.done[i] = done ? 1 : 0;
-          if (o.cash) o.cash[i] = b;
-          if (o.asset) o.asset[i] = vn;
-          write_hold_row<KA>(e, o, (size_t)i, h);
-          if (done && e.autoreset) {
-            b = e.cash0;
+    sm100::mbar_wait(&sm.rows[sb], (rphase >> sb) & 1u);
+    rphase ^= 1u << sb;
+    if (stepping && !bad) {
+      const double* R = static_cast<const double*>(__builtin_assume_aligned(
+          (d == sm.pred[sb]) ? sm.pr[sb] : e.px + (size_t)d * kPriceRows * e.kp, 16));
+      stock_trade<KA>(e, b, h, R, RS, a, oor, sm.save[tid], o.actions ? o.actions + (size_t)i * K : nullptr);
+      const double vn = stock_mark<KA>(b, h, R + kRowPN * RS, R + kRowMPN * RS);
+      double vnext = vn;
+      t += 1;
+      const bool done = (t == e.L);
+      if (o.reward) o.reward[i] = stock_reward(e, v, vn);
+      if (o.done) o.done[i] = done ? 1 : 0;
+      if (o.cash) o.cash[i] = b;
+      if (o.asset) o.asset[i] = vn;
+      write_hold_row<KA>(e, o, (size_t)i, h);
+      if (done && e.autoreset) {
+        b = e.cash0;
+        vnext = e.cash0;
 #pragma unroll
-            for (int k = 0; k < KA; ++k) h[k] = 0;
-            t = 0;
-            if (e.wadv) w = (w + 1) % e.W;
-          }
-          e.cash[i] = b;
-          store_hold<KA>(e, i, h);
-          e.t_ep[i] = t;
-          if (e.wadv) e.window[i] = w;
-        });
-    __syncthreads();   // buffer sb is refilled two tiles from now: everyone has read it
+        for (int k = 0; k < KA; ++k) h[k] = 0;
+        t = 0;
+        if (e.wadv) w = (w + 1) % e.W;
+      }
+      e.cash[i] = b;
+      e.vcur[i] = vnext;
+      store_hold<KA>(e, i, h);
+      e.t_ep[i] = t;
+      if (e.wadv) e.window[i] = w;
+    }
+    __syncwarp();
+    if (lane == 0) sm100::mbar_arrive(&sm.empty[sb]);
   }
   if (oor) set_flag(e, FIN_FLAG_ACTION_RANGE);
 }
@@ -267,10 +319,12 @@ __global__ void __launch_bounds__(kStep) k_stock_replay(EnvDev e, const int16_t*
   for (int k = 0; k < KA; ++k) h[k] = 0;
   MetricAcc m;
   metric_start(m, 0.0);
+  double vc = 0.0;   // pre-trade asset of the next step (the cached v, then each post-trade v)
   if (live) {
     t = e.t_ep[i];
     w = e.window[i];
     b = e.cash[i];
+    vc = e.vcur[i];
     load_hold<KA>(e, i, h);
     m = load_metric(e, i);
   }
@@ -278,10 +332,20 @@ __global__ void __launch_bounds__(kStep) k_stock_replay(EnvDev e, const int16_t*
   const int nv = max(0, min(32, N - i0));
   const bool vec = vec_ok && nv == 32;
   if (nv > 0) slab_load(sm.act[0][wid], actions + (size_t)i0 * K, nv, K, lane, vec);
+  const int RS = EXACT ? (KA + 3) / 4 * 4 : e.kp;   // staged row stride (= kp)
+  if (tid == 0) {
+    sm100::mbar_init(&sm.rows[0], 1);
+    sm100::mbar_init(&sm.rows[1], 1);
+    sm100::fence_mbar_init();
+  }
   gs_init(&sm.gs, tid, kBar);
+  __syncthreads();
+  if (tid == 0) rows_issue(e, sm.pr[0], &sm.rows[0], &sm.pred[0], day_of(e, w, t));   // thread 0 is live
+  __syncthreads();
+  uint32_t rphase = 0;
   int cnt = 0, round = 0;
-  double rsum = 0.0, vc = 0.0;
-  bool have_v = false, oor = false, bad = false;
+  double rsum = 0.0;
+  bool oor = false, bad = false;
   for (int s = 0; s < T; ++s) {
     if (s + 1 < T && nv > 0)
       slab_load(sm.act[(s + 1) & 1][wid], actions + ((size_t)(s + 1) * N + i0) * K, nv, K, lane, vec);
@@ -299,14 +363,24 @@ __global__ void __launch_bounds__(kStep) k_stock_replay(EnvDev e, const int16_t*
     }
     const int d = day_of(e, w, t);
     if (stepping && (d < 0 || d + 1 >= e.rows)) bad = true;
+    const int sb = s & 1;
+    // rows of step s+1, predicted from thread 0's env (lockstep): the next day, or the
+    // first day of its (possibly advanced) window after a reset
+    if (tid == 0 && s + 1 < T) {
+      const int w1 = (e.wadv && t + 1 >= e.L) ? (w + 1) % e.W : w;
+      rows_issue(e, sm.pr[sb ^ 1], &sm.rows[sb ^ 1], &sm.pred[sb ^ 1],
+                 t + 1 < e.L ? d + 1 : (e.autoreset ? day_of(e, w1, 0) : -1));
+    }
+    double* pr = sm.pr[sb];
+    sm100::mbar_wait(&sm.rows[sb], (rphase >> sb) & 1u);   // rows landed (or no prediction)
+    rphase ^= 1u << sb;
+    if (tid == 0) sm.gs.staged = sm.pred[sb];
     group_apply(
-        &sm.gs, round, d, stepping && !bad, tid, kBar, [&](int dd) { stage_prices<KA>(e, sm, dd, tid); },
+        &sm.gs, round, d, stepping && !bad, tid, kBar, [&](int dd) { stage_price_rows(e, pr, dd, tid, kStep); },
         [&]() {
-          if (!have_v) { vc = stock_mark<KA>(b, h, sm.pr[kRowP], sm.pr[kRowMP]); have_v = true; }
           const double v = vc;
-          stock_trade<KA>(e, b, h, &sm.pr[0][0], KA, a, oor, sm.save[tid],
-                          o.actions ? o.actions + ti * K : nullptr);
-          const double vn = stock_mark<KA>(b, h, sm.pr[kRowPN], sm.pr[kRowMPN]);
+          stock_trade<KA>(e, b, h, pr, RS, a, oor, sm.save[tid], o.actions ? o.actions + ti * K : nullptr);
+          const double vn = stock_mark<KA>(b, h, pr + kRowPN * RS, pr + kRowMPN * RS);
           vc = vn;
           t += 1;
           const bool done = (t == e.L);
@@ -343,6 +417,7 @@ __global__ void __launch_bounds__(kStep) k_stock_replay(EnvDev e, const int16_t*
     if (oor) set_flag(e, FIN_FLAG_ACTION_RANGE);
     if (bad) set_flag(e, FIN_FLAG_BAD_INDEX);
     e.cash[i] = b;
+    e.vcur[i] = vc;
     store_hold<KA>(e, i, h);
     e.t_ep[i] = t;
     e.window[i] = w;
@@ -357,7 +432,7 @@ __global__ void __launch_bounds__(kStep) k_stock_replay(EnvDev e, const int16_t*
 __device__ __forceinline__ double asset_now(const EnvDev& e, int i) {
   int d = day_of(e, e.window[i], e.t_ep[i]);
   if (d >= e.rows) d = e.rows - 1;
-  const double* p = e.px + (size_t)d * 2 * e.kp;
+  const double* p = e.px + (size_t)d * kPriceRows * e.kp + kRowP * e.kp;
   double v = e.cash[i];
   for (int k = 0; k < e.K; ++k) v = fadd64(v, fmul64(nn2d(e.hold[hold_at(e.N, k, i)]), p[k]));
   return v;
@@ -386,9 +461,11 @@ __global__ void k_stock_set_state(EnvDev e, const double* cash, const int16_t* h
     for (int k = 0; k < K; ++k) e.hold[hold_at(e.N, k, i)] = hold[(size_t)i * K + k];
   if (t_ep) e.t_ep[i] = t_ep[i];
   if (window) e.window[i] = window[i];
-  // online metrics restart at the current equity
+  // cached asset and online metrics restart at the current equity
+  const double v = asset_now(e, i);
+  e.vcur[i] = v;
   MetricAcc m;
-  metric_start(m, asset_now(e, i));
+  metric_start(m, v);
   store_metric(e, i, m);
 }
 
@@ -437,9 +514,13 @@ cudaError_t launch_stock_reset(const EnvDev& e, const uint8_t* mask, cudaStream_
 template <int KA, bool EXACT>
 int k1_grid(int N) {
   static int per_sm = 0;
-  if (per_sm == 0 &&
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stock_step<KA, EXACT>, kStep, 0) != cudaSuccess)
-    per_sm = 1;
+  if (per_sm == 0) {
+    cudaFuncSetAttribute(k_stock_step<KA, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(K1Smem<KA>));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stock_step<KA, EXACT>, kStep,
+                                                      sizeof(K1Smem<KA>)) != cudaSuccess)
+      per_sm = 1;
+  }
   if (per_sm < 1) per_sm = 1;
   const int tiles = (N + kStep - 1) / kStep;
   return std::min(tiles, per_sm * num_sms());
@@ -447,7 +528,8 @@ int k1_grid(int N) {
 
 cudaError_t launch_stock_step(const EnvDev& e, const int16_t* actions, const TrajDev& o, cudaStream_t s) {
   const int v = vec_ok(actions, 8);   // bulk copies of whole 128-env tiles: 256 K bytes each
-#define FIN_K1(KA, EX) k_stock_step<KA, EX><<<k1_grid<KA, EX>(e.N), kStep, 0, s>>>(e, actions, o, v)
+#define FIN_K1(KA, EX) \
+  k_stock_step<KA, EX><<<k1_grid<KA, EX>(e.N), kStep, sizeof(K1Smem<KA>), s>>>(e, actions, o, v)
   if (e.K == 30) FIN_K1(30, true);
   else if (e.K == 4) FIN_K1(4, true);
   else if (e.K <= 8) FIN_K1(8, false);

@@ -15,20 +15,14 @@
 #pragma once
 #include "fin_internal.cuh"
 
-// Price rows of one step, staged in shared memory (or read from global memory):
-//   P  = p_d   close of the execution day (exact widening of the fp32 market)
-//   U  = u_d   = fl(p_d * (1 + c)), the buy price per share
-//   MP = -2^52 p_d,  MU = -2^52 u_d   (exact scalings)
-//   RU = fl(1 / u_d)                  (estimate of the affordable count only)
-//   PN = p_d+1, MPN = -2^52 p_d+1     (marking day)
-// Products n * x with a non-negative int n are formed as fma(2^52 + n, x, -2^52 x):
+// The price rows of one step (fin_internal.cuh: P U MP MU RU PN MPN) are staged in
+// shared memory.  Products n * x with a non-negative int n are formed as fma(2^52 + n, x, -2^52 x):
 // the exact value is n * x, so the single rounding of the fma gives fl(n * x) --
 // the same bits as converting n and multiplying, with neither the XU-pipe I2F
 // conversion nor a separate subtract.  2^52 + n is the bit pattern 0x43300000:n.
 // Padding assets (k >= K) carry zeros in every row and in h and a, so every loop
 // runs to the compile-time KA with no per-asset predicate: a padded asset adds +0
 // to the cash (b is never -0) and to the sums, which leaves them bit-identical.
-enum { kRowP = 0, kRowU, kRowMP, kRowMU, kRowRU, kRowPN, kRowMPN, kPriceRows };
 
 // Register-pressure control.  Left alone, ptxas hoists all 2-3 x 30 f64 row loads of
 // a loop to its top (255 registers and spills).  The rows of asset chunk c+1 are
@@ -44,7 +38,7 @@ __device__ __forceinline__ int zdep(int x) { return x >> 31; }
     int off_ = 0;                                                                  \
     _Pragma("unroll") for (int c_ = 0; c_ < (KA); c_ += kChunk) {                  \
       const int o_ = off_;                                                         \
-      off_ = zdep(dep_expr);                                                       \
+      off_ = 2 * zdep(dep_expr);  /* even: keeps 16-B row vectors aligned */       \
       _Pragma("unroll") for (int k = c_; k < (c_ + kChunk < (KA) ? c_ + kChunk : (KA)); ++k) { BODY } \
     }                                                                              \
   }
@@ -152,18 +146,13 @@ __device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)
   }
 }
 
-// stage the price rows of day d from the f64 table px[rows][2][kp] into pr[kPriceRows][RS]
+// copy the price rows of day d (px[d], kPriceRows x kp doubles) into pr[kPriceRows][kp]
 // (threads tid = 0 .. nthr-1 of the staging group)
-__device__ __forceinline__ void stage_price_rows(const EnvDev& e, double* pr, int RS, int d, int tid, int nthr) {
-  for (int j = tid; j < kPriceRows * RS; j += nthr) {
-    const int r = j / RS, k = j - r * RS;
-    const int row = d + (r >= kRowPN ? 1 : 0), ch = (r == kRowU || r == kRowMU || r == kRowRU) ? 1 : 0;
-    const double x = k < e.kp ? e.px[((size_t)row * 2 + ch) * e.kp + k] : 0.0;
-    pr[j] = (r == kRowMP || r == kRowMU || r == kRowMPN) ? x * -4503599627370496.0
-            : (r == kRowRU)                          ? (x > 0.0 ? 1.0 / x : 0.0)
-                                                     : x;
-  }
+__device__ __forceinline__ void stage_price_rows(const EnvDev& e, double* pr, int d, int tid, int nthr) {
+  const double* src = e.px + (size_t)d * kPriceRows * e.kp;
+  for (int j = tid; j < kPriceRows * e.kp; j += nthr) pr[j] = __ldg(src + j);
 }
+
 // reward = (v' - v) * scale (exact power-of-two scale), stored fp32
 __device__ __forceinline__ float stock_reward(const EnvDev& e, double v, double vn) {
   return (float)fmul64(fsub64(vn, v), e.scale);

@@ -27,9 +27,11 @@ struct EnvDev {
   int64_t env_offset;
   int64_t t_global;      // global step counter (Philox counter word), advanced per step
   const float* market;   // [rows][row_floats]
-  const double* px;      // stock: [rows][2][kp] f64 -- close p (exact widening), u = fl(p * up)
+  const double* px;      // stock: [rows][kPriceRows][kp] f64 price rows of each day (env_stock.cuh)
   // ---- state (library-owned device memory)
   double* cash;          // [N]
+  double* vcur;          // [N] stock: total asset v = b + sum_k h_k p_k at the env's current day
+                         //     (P:132), cached: a step's pre-trade v is the previous post-trade v
   int16_t* hold;         // stock: asset octets [ceil(K/8)][N][8] (hold_at); crypto: [N] position in {-1,0,1}
   int32_t* t_ep;         // [N]
   int32_t* window;       // [N]
@@ -69,6 +71,14 @@ __device__ __forceinline__ double fadd64(double a, double b) { return __dadd_rn(
 __device__ __forceinline__ double fsub64(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double fmul64(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double fdiv64(double a, double b) { return __ddiv_rn(a, b); }
+
+// Price rows of day d, precomputed on the host at create (px), staged per step:
+//   P  = p_d   close of the execution day (exact widening of the fp32 market)
+//   U  = u_d   = fl(p_d * (1 + c)), the buy price per share
+//   MP = -2^52 p_d,  MU = -2^52 u_d   (exact scalings)
+//   RU = fl(1 / u_d)                  (estimate of the affordable count only)
+//   PN = p_d+1, MPN = -2^52 p_d+1     (marking day; 0 on the last row)
+enum { kRowP = 0, kRowU, kRowMP, kRowMU, kRowRU, kRowPN, kRowMPN, kPriceRows };
 
 // Exact int -> double for 0 <= n < 2^31 on the fp64 pipe: the bit pattern
 // 0x43300000:n is 2^52 + n exactly and subtracting 2^52 is exact.  Replaces the

@@ -65,8 +65,7 @@ struct StockOps {
     bool live;
     int gtid, bar_id, round;
     double b;
-    double vc;         // pre-trade asset of the next step (= last v', or b0 after a reset)
-    bool have_v;
+    double vc;         // pre-trade asset of the next step (cached v, then the last post-trade v)
     int h[KA];
     int t_ep, w, d;
     uint32_t b0bits;
@@ -88,11 +87,11 @@ struct StockOps {
     st.rsum = 0.0;
     st.oor = st.bad = st.nonfinite = false;
     st.d = 0;
-    st.have_v = false;
     st.vc = 0.0;
     agg_init(st.agg);
     if (st.live) {
       st.b = e.cash[env];
+      st.vc = e.vcur[env];
       load_hold<KA>(e, env, st.h);
       st.t_ep = e.t_ep[env];
       st.w = e.window[env];
@@ -117,7 +116,7 @@ struct StockOps {
   // stage day k: f64 price rows p_k, u_k, p_k+1 and the members' z1s rows of day k
   __device__ __noinline__ static void stage_row(const TcParams& p, int k, int gtid, uint8_t* stg) {
     const EnvDev& e = p.e;
-    stage_price_rows(e, reinterpret_cast<double*>(stg + kOffP), KP4, k, gtid, 128);
+    stage_price_rows(e, reinterpret_cast<double*>(stg + kOffP), k, gtid, 128);
     float* zs = reinterpret_cast<float*>(stg + kOffZ);
     for (int j = gtid; j < p.M * Plan::kHid; j += 128) {
       const int m = j / Plan::kHid, n = j % Plan::kHid;
@@ -283,10 +282,6 @@ struct StockOps {
         [&]() {
           const double* pd = reinterpret_cast<const double*>(stg + kOffP);
           FIN_TR(threadIdx.x == 128, t, 19);
-          if (!st.have_v) {   // first step of the call: v from the state; afterwards v = last v'
-            st.vc = stock_mark<KA>(st.b, st.h, pd + kRowP * KP4, pd + kRowMP * KP4);
-            st.have_v = true;
-          }
           const double v = st.vc;
           uint4 save[(KA + 7) / 8];   // local: read only by the rare exact buy redo
           stock_trade<KA>(e, st.b, st.h, pd, KP4, a, st.oor, save,
@@ -338,6 +333,7 @@ struct StockOps {
     if (p.act_only) return;
     if (st.live) {
       e.cash[env] = st.b;
+      e.vcur[env] = st.vc;
       store_hold<KA>(e, env, st.h);
       e.t_ep[env] = st.t_ep;
       e.window[env] = st.w;
