@@ -76,19 +76,28 @@ __device__ __forceinline__ void slab_load(int16_t* dst, const int16_t* src, int 
   sm100::cp_async_commit();
 }
 
+// this thread's action row from shared memory, clamped (R6; sets oor, writes act_out)
 template <int KA, bool EXACT>
-__device__ __forceinline__ void slab_read(const int16_t* slab, int lane, int K, bool live, int (&a)[KA]) {
+__device__ __forceinline__ void slab_read(const EnvDev& e, const int16_t* slab, int lane, int K, bool live,
+                                          PackedActs<KA>& a, bool& oor, int16_t* act_out) {
   if constexpr (EXACT && (KA % 2 == 0)) {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(slab) + lane * (KA / 2);
+    const uint32_t mt2 = (uint32_t)e.max_trade * 0x10001u;
+    uint32_t diff = 0;
 #pragma unroll
     for (int j = 0; j < KA / 2; ++j) {
-      const uint32_t x = live ? w[j] : 0u;
-      a[2 * j] = (int)(int16_t)(x & 0xffffu);
-      a[2 * j + 1] = ((int)x) >> 16;
+      a.w[j] = clamp_pair(live ? w[j] : 0u, mt2, diff);
+      if (act_out) reinterpret_cast<uint32_t*>(act_out)[j] = a.w[j];   // K even: 4-B aligned rows
     }
+    oor |= diff != 0;
   } else {
+    int x[KA];
 #pragma unroll
-    for (int k = 0; k < KA; ++k) a[k] = (live && k < K) ? (int)slab[lane * K + k] : 0;
+    for (int k = 0; k < KA; ++k) x[k] = (live && k < K) ? (int)slab[lane * K + k] : 0;
+    clamp_actions<KA>(e, x, oor, nullptr);
+    if (act_out)
+      for (int k = 0; k < K; ++k) act_out[k] = (int16_t)x[k];
+    a = pack_acts<KA>(x);
   }
 }
 
@@ -171,7 +180,7 @@ __device__ __forceinline__ void k1_issue(const EnvDev& e, const int16_t* actions
 }
 
 #ifndef FIN_K1_MINB
-#define FIN_K1_MINB 4   // resident K1 blocks per SM the register allocation must allow
+#define FIN_K1_MINB 3   // resident K1 blocks per SM (measured best of 2, 3, 4: scripts/k1_sweep.sh)
 #endif
 // No block-wide barrier inside the tile loop: warps are decoupled by the full / rows
 // / empty mbarriers, and an env whose day is not the predicted one reads its rows
@@ -211,7 +220,8 @@ __global__ void __launch_bounds__(kStep, FIN_K1_MINB)
     const bool tma = j < n_full;
     int t = 0, w = 0;
     double b = 0.0, v = 0.0;
-    int h[KA], a[KA];
+    int h[KA];
+    PackedActs<KA> a;
 #pragma unroll
     for (int k = 0; k < KA; ++k) h[k] = 0;
     K1Buf<KA>& B = sm.buf[sb];
@@ -230,18 +240,23 @@ __global__ void __launch_bounds__(kStep, FIN_K1_MINB)
         for (int q = 0; q < 8; ++q)
           if (8 * oc + q < KA) h[8 * oc + q] = (int)((q & 1) ? (wv[q >> 1] >> 16) : (wv[q >> 1] & 0xffffu));
       }
-      slab_read<KA, EXACT>(B.act, tid, K, true, a);
+      slab_read<KA, EXACT>(e, B.act, tid, K, true, a, oor, o.actions ? o.actions + (size_t)i * K : nullptr);
     } else if (live) {   // ragged last tile / unaligned actions: direct loads
       t = e.t_ep[i];
       w = e.window[i];
       b = e.cash[i];
       v = e.vcur[i];
       load_hold<KA>(e, i, h);
+      int x[KA];
 #pragma unroll
-      for (int k = 0; k < KA; ++k) a[k] = (k < K) ? (int)actions[(size_t)i * K + k] : 0;
+      for (int k = 0; k < KA; ++k) x[k] = (k < K) ? (int)actions[(size_t)i * K + k] : 0;
+      clamp_actions<KA>(e, x, oor, nullptr);
+      if (o.actions)
+        for (int k = 0; k < K; ++k) o.actions[(size_t)i * K + k] = (int16_t)x[k];
+      a = pack_acts<KA>(x);
     } else {
 #pragma unroll
-      for (int k = 0; k < KA; ++k) a[k] = 0;
+      for (int j = 0; j < (KA + 1) / 2; ++j) a.w[j] = 0u;
     }
     // producer (thread 0): once the 4 warps are done with the other buffer (tile j - G),
     // refill it with tile jn's state and the rows of its predicted day
@@ -268,7 +283,7 @@ __global__ void __launch_bounds__(kStep, FIN_K1_MINB)
     if (stepping && !bad) {
       const double* R = static_cast<const double*>(__builtin_assume_aligned(
           (d == sm.pred[sb]) ? sm.pr[sb] : e.px + (size_t)d * kPriceRows * e.kp, 16));
-      stock_trade<KA>(e, b, h, R, RS, a, oor, sm.save[tid], o.actions ? o.actions + (size_t)i * K : nullptr);
+      stock_trade<KA>(e, b, h, R, RS, a, sm.save[tid]);
       const double vn = stock_mark<KA>(b, h, R + kRowPN * RS, R + kRowMPN * RS);
       double vnext = vn;
       t += 1;
@@ -302,8 +317,11 @@ __global__ void __launch_bounds__(kStep, FIN_K1_MINB)
 // episode clock, window, metric accumulators) lives in registers for all T, and the
 // pre-trade asset v of a step is the previous step's post-trade asset v' (the same
 // sum over the same holdings and prices), or b0 after a reset.
+#ifndef FIN_K4_MINB
+#define FIN_K4_MINB 3   // measured best of 2, 3, 4 (scripts/k4_sweep.sh)
+#endif
 template <int KA, bool EXACT>
-__global__ void __launch_bounds__(kStep) k_stock_replay(EnvDev e, const int16_t* __restrict__ actions, int T,
+__global__ void __launch_bounds__(kStep, FIN_K4_MINB) k_stock_replay(EnvDev e, const int16_t* __restrict__ actions, int T,
                                                         TrajDev o, int vec_ok) {
   __shared__ StepSmem<KA> sm;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -352,9 +370,10 @@ __global__ void __launch_bounds__(kStep) k_stock_replay(EnvDev e, const int16_t*
     if (s + 1 < T && nv > 0) sm100::cp_async_wait<1>();
     else sm100::cp_async_wait<0>();
     __syncwarp();
-    int a[KA];
-    slab_read<KA, EXACT>(sm.act[s & 1][wid], lane, K, live, a);
+    PackedActs<KA> a;
     const size_t ti = (size_t)s * N + i;
+    slab_read<KA, EXACT>(e, sm.act[s & 1][wid], lane, K, live, a, oor,
+                         (o.actions && live) ? o.actions + ti * K : nullptr);
     const bool stepping = live && !bad && t < e.L;
     if (live && !bad && !stepping) {
       set_flag(e, FIN_FLAG_EPISODE_DONE);
@@ -379,7 +398,7 @@ __global__ void __launch_bounds__(kStep) k_stock_replay(EnvDev e, const int16_t*
         &sm.gs, round, d, stepping && !bad, tid, kBar, [&](int dd) { stage_price_rows(e, pr, dd, tid, kStep); },
         [&]() {
           const double v = vc;
-          stock_trade<KA>(e, b, h, pr, RS, a, oor, sm.save[tid], o.actions ? o.actions + ti * K : nullptr);
+          stock_trade<KA>(e, b, h, pr, RS, a, sm.save[tid]);
           const double vn = stock_mark<KA>(b, h, pr + kRowPN * RS, pr + kRowMPN * RS);
           vc = vn;
           t += 1;

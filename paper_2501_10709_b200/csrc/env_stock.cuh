@@ -74,20 +74,10 @@ static __device__ __noinline__ double stock_buys_exact(double b, int* h, const i
   return b;
 }
 
-// The trade of one step; R[r * RS + k] is row r of the staged rows above.  a[]
-// holds the requested deltas on entry and the clamped deltas (R6) on exit; h[] and
-// b are updated in place.  ``save`` (16-B aligned, (KA+7)/8 uint4; shared or local
-// memory) receives the post-sell holdings for the rare exact redo of the buys;
-// ``act_out`` (nullable) the clamped actions.
+// Step 2 of the transition, clamp (R6): any clamped entry sets the sticky range flag;
+// ``act_out`` (nullable) receives the clamped actions.  Scalar form (policy actions).
 template <int KA>
-__device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)[KA], const double* R, int RS,
-                                            int (&a)[KA], bool& oor, uint4* save, int16_t* act_out) {
-  const double* P = R + kRowP * RS;
-  const double* U = R + kRowU * RS;
-  const double* MP = R + kRowMP * RS;
-  const double* MU = R + kRowMU * RS;
-  const double* RU = R + kRowRU * RS;
-  // 2. clamp (R6); any clamped entry sets the sticky range flag
+__device__ __forceinline__ void clamp_actions(const EnvDev& e, int (&a)[KA], bool& oor, int16_t* act_out) {
   int diff = 0;
 #pragma unroll
   for (int k = 0; k < KA; ++k) {
@@ -97,6 +87,45 @@ __device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)
     if (act_out) act_out[k] = (int16_t)x;
   }
   oor |= diff != 0;
+}
+// Packed form for supplied int16 actions: two assets per 32-bit word, 16-bit SIMD
+// min / max (max_trade <= 32767 fits a signed half).
+__device__ __forceinline__ uint32_t clamp_pair(uint32_t w, uint32_t mt2, uint32_t& diff) {
+  const uint32_t x = __vmins2(__vmaxs2(w, __vneg2(mt2)), mt2);
+  diff |= x ^ w;
+  return x;
+}
+
+// Clamped actions travel packed, two int16 per 32-bit word (asset 2j in the low
+// half): 15 registers instead of 30 for the C1 shapes.
+template <int KA>
+struct PackedActs {
+  uint32_t w[(KA + 1) / 2];
+  __device__ __forceinline__ int operator[](int k) const {
+    return (k & 1) ? ((int)w[k >> 1] >> 16) : (int)(int16_t)(w[k >> 1] & 0xffffu);
+  }
+};
+template <int KA>
+__device__ __forceinline__ PackedActs<KA> pack_acts(const int (&a)[KA]) {
+  PackedActs<KA> p;
+#pragma unroll
+  for (int j = 0; j < (KA + 1) / 2; ++j)
+    p.w[j] = __byte_perm((uint32_t)a[2 * j], 2 * j + 1 < KA ? (uint32_t)a[2 * j + 1] : 0u, 0x5410);
+  return p;
+}
+
+// Steps 3-4 of the transition (a already clamped); R[r * RS + k] is row r of the
+// staged rows above; h[] and b are updated in place.  ``save`` (16-B aligned,
+// (KA+7)/8 uint4; shared or local memory) receives the post-sell holdings for the
+// rare exact redo of the buys.
+template <int KA>
+__device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)[KA], const double* R, int RS,
+                                            const PackedActs<KA>& a, uint4* save) {
+  const double* P = R + kRowP * RS;
+  const double* U = R + kRowU * RS;
+  const double* MP = R + kRowMP * RS;
+  const double* MU = R + kRowMU * RS;
+  const double* RU = R + kRowRU * RS;
   // 3. sells, clipped to holdings: b += fl(fl(n p) (1 - c)); n = 0 adds +0
   FIN_CHUNKED(KA, b, {
     const int n = max(min(-a[k], h[k]), 0);
@@ -123,12 +152,13 @@ __device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)
   bool miss = false;
   FIN_CHUNKED(KA, b, {
     const int want = max(min(a[k], FIN_HOLD_MAX - h[k]), 0);
+    // floor(b / u) estimate; its low word is used even when x >= 2^32 or b is NaN:
+    // the checks below accept n only if it satisfies the definition itself
     const double D = __dadd_rd(fmul64(b, RU[k + o_]), 4503599627370496.0);
-    const int f = (__double2hiint(D) == 0x43300000) ? __double2loint(D) : 0x7fffffff;
-    const int n = min(want, f);
+    const int n = min(want, __double2loint(D));
     const double cn = nprod(n, U[k + o_], MU[k + o_]);
     const double cn1 = nprod(n + 1, U[k + o_], MU[k + o_]);
-    miss |= (!(cn <= b)) | ((n < want) & !(cn1 > b));
+    miss |= (!(cn <= b)) | ((n < want) & !(cn1 > b)) | (n < 0);
     b = fsub64(b, cn);
     h[k] += n;
   })
