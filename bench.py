@@ -43,7 +43,9 @@ MLP_FLOP_PER_ENV_STEP = 2 * (301 * 256 + 256 * 256 + 256 * 30)    # 300,544: the
 # (DESIGN.md §4.3): 31 env-private inputs in layer 1, layers 2 and 3 unchanged
 FLOP_PER_ENV_STEP = 2 * (31 * 256 + 256 * 256 + 256 * 30)          # 162,304
 Z1S_FLOP_PER_ROLLOUT = 2 * 270 * 256 * ROWS   # fp64 CUDA-core precompute of the per-day layer-1 term
-STEP_BYTES_PER_ENV = 8 + 60 + 4 + 4 + 60 + 8 + 60 + 4 + 4 + 1     # K1: state in/out + action + reward + done
+# K1 algorithmic bytes per env-step: read cash 8 + cached asset 8 + holdings 60 +
+# clock 4 + window 4 + action 60; write cash 8 + asset 8 + holdings 60 + clock 4 + reward 4 + done 1
+STEP_BYTES_PER_ENV = 8 + 8 + 60 + 4 + 4 + 60 + 8 + 8 + 60 + 4 + 4 + 1   # 229
 METRIC = "env-steps/sec (whole box) at 2048-65536 envs, 1/2/4/8 B200; % HBM roofline"
 WORKLOAD = "C1 30-stock env + 301-256-256-30 bf16 policy, 65536 envs/GPU, horizon 256, reset on done"
 
@@ -129,7 +131,7 @@ def _oracle_shard(args):
     return time.perf_counter() - t0
 
 
-def oracle_rate(n_envs_per_core=16, T=8, cores=None):
+def oracle_rate(n_envs_per_core=2048, T=30, cores=None):
     """Oracle env-steps/s on the host's cores (multiprocessing over env shards)."""
     import multiprocessing as mp
     for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
@@ -141,8 +143,8 @@ def oracle_rate(n_envs_per_core=16, T=8, cores=None):
         pool.map(_oracle_shard, [(n_envs_per_core, T, 128 * c) for c in range(cores)])
     wall = time.perf_counter() - t0
     steps = n_envs_per_core * T * cores
-    return steps / wall, cores, f"{cores} shards x {n_envs_per_core} envs x {T} steps of the headline workload " \
-                                f"(float64 oracle incl. 301-256-256-30 MLP), wall {wall:.1f}s"
+    return steps / wall, cores, f"{cores} shards x {n_envs_per_core} envs x {T} steps (one C1 episode) of the " \
+                                f"headline workload (float64 oracle incl. 301-256-256-30 MLP), wall {wall:.1f}s"
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -152,6 +154,20 @@ def make_env(fin, N, env_offset, T_ep=L_EP):
     cfg = fin.env_config(num_envs=N, num_assets=K_ASSETS, num_indicators=N_IND, num_rows=ROWS, episode_len=T_ep,
                          window_stride=5, num_windows=195, window_block=128, env_offset=env_offset, seed=23)
     return fin.fin_env_create(cfg, m.market)
+
+
+class L2Flush:
+    """Write 256 MiB, then read another 256 MiB: the written lines are evicted (and
+    written back) by the read pass, so the next timed region starts on a clean L2
+    that holds none of the step's inputs (126 MB L2)."""
+
+    def __init__(self, torch):
+        self.w = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        self.r = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
+
+    def zero_(self):
+        self.w.zero_()
+        self.r.sum()
 
 
 def time_rollouts(fin, torch, env, pol, N, T, steps, warmup, flush=None, allreduce=None, clocks_index=None):
@@ -192,7 +208,7 @@ def run_ours(args):
     N, T = N_HEAD, T_HEAD
     env = make_env(fin, N, env_offset=rank * N)
     pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, spol.kaiming_bf16(spol.STOCK_DIMS, 0))
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush(torch)
 
     from paper_2501_10709_b200 import dist as fdist
 
@@ -222,7 +238,7 @@ def run_ours(args):
            "vs_baseline": None, "dtype": "bf16 MLP (fp32 accum) + f64 env", "data": "synthetic",
            "config": {"workload": WORKLOAD, "envs_per_gpu": N, "horizon": T, "episode_len": L_EP,
                       "global_envs": N * world, "parallelism": f"env-sharded dp{world}",
-                      "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                      "l2": "flushed between timed steps (256 MiB write + 256 MiB read, outside the events)",
                       "noise": "philox"},
            "gpu_launches": 3 * args.steps,   # per rollout: z1s precompute, fused rollout, aggregate
            "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops_sustained"],
@@ -310,7 +326,7 @@ def extras(fin, torch, pol):
     the C4 sweep points, the exact configs[1] rollout (2048 envs, T = 30), and the
     HBM-bound step kernel K1 at N = 2^22 against the measured HBM copy bandwidth."""
     out = {"sweep_T256": {}}
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush(torch)
     for N in (1, 64, 2048, 16384):
         env = make_env(fin, N, 0)
         times, _ = time_rollouts(fin, torch, env, pol, N, T_HEAD, 5, 3, flush)
@@ -320,33 +336,66 @@ def extras(fin, torch, pol):
     times, _ = time_rollouts(fin, torch, env, pol, 2048, 30, 10, 3, flush)
     out["configs1_2048envs_T30"] = 2048 * 30 / (statistics.mean(times) / 1e3)
     del env
-    # K1 step kernel at N = 2^22 (877 MB working set >> 126 MB L2)
-    N = 1 << 22
-    env = make_env(fin, N, 0)
-    from synth import inputs
-    acts = torch.from_numpy(inputs.stock_actions(1, N, K_ASSETS, seed=5)[0]).cuda()
-    z = lambda s, d: torch.zeros(s, dtype=d, device="cuda")  # noqa: E731
-    rew, dn = z(N, torch.float32), z(N, torch.uint8)
-    tr = fin.make_traj(reward=rew, done=dn)
-    for _ in range(3):
-        fin.fin_env_step(env, acts, tr)
-    torch.cuda.synchronize()
-    ts = []
-    for _ in range(10):
-        flush.zero_()
+    out.update(hbm_kernels(fin, torch))
+    return out
+
+
+def hbm_kernels(fin, torch):
+    """The HBM-bound kernels at working sets far above the 126 MB L2, timed as 10
+    back-to-back launches between CUDA events (no flush needed): K1 fin_env_step
+    (N = 2^22), K4 fin_rollout_actions (N = 2^20, T = 32), K6 fin_episode_metrics
+    (T = 2048, N = 2^18).  achieved = algorithmic bytes / launch time."""
+    import statistics as st
+    pk = peaks()
+    res = {}
+
+    def b2b(fn, reps=10):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        fin.fin_env_step(env, acts, tr)
+        for _ in range(reps):
+            fn()
         b.record()
         torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
-    ms = statistics.mean(ts)
-    pk = peaks()
-    gbs = STEP_BYTES_PER_ENV * N / (ms / 1e3) / 1e9
-    out["step_kernel_hbm"] = {"kernel": "k_stock_step (K1)", "envs": N, "bytes_per_env_step": STEP_BYTES_PER_ENV,
-                              "env_steps_per_s": N / (ms / 1e3), "achieved_gbs": gbs, "peak_gbs": pk["hbm_gbs"],
-                              "frac": gbs / pk["hbm_gbs"], "frac_of_8tbs": gbs / 8000.0}
-    return out
+        return a.elapsed_time(b) / reps
+
+    def entry(name, kernel, units, bytes_, ms, note):
+        gbs = bytes_ / (ms / 1e3) / 1e9
+        res[name] = {"kernel": kernel, "env_steps": units, "ms": ms, "env_steps_per_s": units / (ms / 1e3),
+                     "bytes_per_launch": bytes_, "achieved_gbs": gbs, "peak_gbs": pk["hbm_gbs"],
+                     "frac": gbs / pk["hbm_gbs"], "frac_of_8tbs": gbs / 8000.0, "note": note}
+
+    g = torch.Generator(device="cuda").manual_seed(5)
+    z = lambda s, d: torch.zeros(s, dtype=d, device="cuda")  # noqa: E731
+    N = 1 << 22
+    env = make_env(fin, N, 0)
+    acts = torch.randint(-100, 101, (N, K_ASSETS), device="cuda", generator=g, dtype=torch.int16)
+    tr = fin.make_traj(reward=z(N, torch.float32), done=z(N, torch.uint8))
+    ms = b2b(lambda: fin.fin_env_step(env, acts, tr))
+    entry("step_kernel_hbm", "k_stock_step (K1)", N, STEP_BYTES_PER_ENV * N, ms,
+          "steady state: the same seeded U{-100..100} actions every step, so cash binds (exact affordability path)")
+    del env, acts, tr
+    N, T = 1 << 20, 32
+    env = make_env(fin, N, 0)
+    acts = torch.randint(-100, 101, (T, N, K_ASSETS), device="cuda", generator=g, dtype=torch.int16)
+    tr = fin.make_traj(reward=z((T, N), torch.float32), done=z((T, N), torch.uint8))
+    ms = b2b(lambda: fin.fin_rollout_actions(env, acts, T, tr))
+    state = 2 * (8 + 8 + 60 + 4 + 4 + 52)   # per env per call: cash, asset, holdings, clock, window, metrics
+    entry("replay_kernel_hbm", "k_stock_replay (K4)", N * T, N * T * 65 + N * state, ms,
+          "actions 60 + reward 4 + done 1 per env-step, state in/out once per call")
+    del env, acts, tr
+    T, N = 2048, 1 << 18
+    done = (torch.rand((T, N), device="cuda", generator=g) < 1 / 30).to(torch.uint8)
+    eq = 1e6 * torch.exp(torch.cumsum(0.01 * torch.randn((T + 1, N), device="cuda", generator=g,
+                                                         dtype=torch.float64), 0))
+    epm, cnt = z((160, N, 3), torch.float64), z(N, torch.int32)
+    ms = b2b(lambda: fin.fin_episode_metrics(eq, done, 1e6, ep_metrics=epm, ep_count=cnt))
+    entry("metrics_kernel_hbm", "k_pass_a/b/c (K6)", N * T,
+          T * N * 9 + N * 8 + int(cnt.sum().item()) * 24 + N * 4, ms,
+          "equity f64 + done u8 per env-step read, episode rows written")
+    return res
 
 
 def run_reference(args):
