@@ -45,6 +45,7 @@ struct fin_policy {
   int32_t dims[4];
   uint8_t* wpack;              // device, TcPlan layout (stock: layer 1 = private columns only)
   float* bias;                 // device, [HID + HID + OUT_PAD]
+  uint32_t bias_nz;            // bit l: layer l has a non-zero bias (an all-zero bias is skipped)
   float* w1s_t;                // stock: device [S][HID] shared columns of W1 (exact bf16 values), else null
 };
 
@@ -469,6 +470,11 @@ int fin_policy_create(int32_t kind, int32_t n_layers, const int32_t* dims, const
   if (!pol) return fail(FIN_E_CONFIG, "out of host memory");
   pol->kind = kind;
   pol->net = net;
+  pol->bias_nz = 0;
+  for (int l = 0; l < 3; ++l)
+    if (bias && bias[l])
+      for (int n = 0; n < dims[l + 1]; ++n)
+        if (bias[l][n] != 0.f) pol->bias_nz |= 1u << l;
   for (int l = 0; l < 4; ++l) pol->dims[l] = dims[l];
   cudaError_t e = cudaMalloc(&pol->wpack, wp.size());
   if (e == cudaSuccess) e = cudaMalloc(&pol->bias, bp.size() * sizeof(float));
@@ -512,6 +518,7 @@ int fill_members(const fin_env* env, const fin_policy* const* members, int32_t n
     net = members[m]->net;
     p.wpack[m] = members[m]->wpack;
     p.bias[m] = members[m]->bias;
+    p.bias_nz |= members[m]->bias_nz << (3 * m);
     p.kinds[m] = members[m]->kind;
     if (members[m]->kind == FIN_DDPG_OU) ++n_ddpg;
     p.mw[m] = member_w ? member_w[m] : 1.f;
@@ -690,6 +697,7 @@ int fin_mlp_forward(const fin_policy* pol, const uint16_t* x, int32_t B, float* 
   p.wpack[0] = pol->wpack;
   p.bias[0] = pol->bias;
   p.kinds[0] = pol->kind;
+  p.bias_nz = pol->bias_nz;
   p.M = 1;
   p.T = 1;
   p.x_in = x;

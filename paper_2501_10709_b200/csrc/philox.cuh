@@ -38,7 +38,7 @@ __device__ __forceinline__ void box_muller(float ur, float ua, float& z0, float&
 struct Normals8 {
   float4 a, b;
 };
-static __device__ __noinline__ Normals8 philox_normals8_v(uint64_t g, uint32_t t, uint32_t word2a, uint32_t word2b,
+__device__ __forceinline__ Normals8 philox_normals8_v(uint64_t g, uint32_t t, uint32_t word2a, uint32_t word2b,
                                                            uint64_t seed) {
   uint32_t ca[4] = {(uint32_t)g, t, word2a, 0u};
   uint32_t cb[4] = {(uint32_t)g, t, word2b, 0u};

@@ -54,10 +54,15 @@ struct StockOps {
   static constexpr int KT8 = Plan::kIn / 8;
   using Obs = StockObs<KA, IA>;
   static_assert(Obs::kEnvPad == Plan::kIn, "factored layer 1: the network input is the private part");
-  // staging: price rows of day d (f64, env_stock.cuh) | z1s rows of day d per member (f32) | slots | broadcast
+  // staging, two buffers: [price rows of a day (f64, fin_internal.cuh) | z1s rows of that
+  // day per member (f32)] x 2 | slots | broadcast.  The current step uses buffer sb;
+  // the other one receives, by cp.async under the step's work, the rows of the day
+  // predicted for the next step (the tile's first env: next day, or the first day of
+  // its window after a reset -- envs of a tile step in lockstep).
   static constexpr int kOffP = 0;
   static constexpr int kOffZ = kPriceRows * KP4 * 8;
-  static constexpr int kOffS = kOffZ + FIN_MAX_MEMBERS * Plan::kHid * 4;
+  static constexpr int kRegion = kOffZ + FIN_MAX_MEMBERS * Plan::kHid * 4;
+  static constexpr int kOffS = 2 * kRegion;
   static constexpr int kOffB = kOffS + 16;
   static constexpr int kStageBytes = kOffB + 16;
 
@@ -70,6 +75,9 @@ struct StockOps {
     int t_ep, w, d;
     uint32_t b0bits;
     bool zsm;          // this step's z1s rows are staged in shared memory
+    int sb;            // current staging buffer
+    int kcur, koth;    // day held by buffer sb / by buffer sb ^ 1 (-1: none)
+    int pend;          // day being prefetched into buffer sb ^ 1 (-1: none)
     float asum[KA];
     float ou[KOU];
     MetricAcc m;
@@ -88,6 +96,9 @@ struct StockOps {
     st.oor = st.bad = st.nonfinite = false;
     st.d = 0;
     st.vc = 0.0;
+    st.sb = 0;
+    st.kcur = st.koth = -1;
+    st.pend = -1;
     agg_init(st.agg);
     if (st.live) {
       st.b = e.cash[env];
@@ -113,16 +124,31 @@ struct StockOps {
     }
   }
 
-  // stage day k: f64 price rows p_k, u_k, p_k+1 and the members' z1s rows of day k
-  __device__ __noinline__ static void stage_row(const TcParams& p, int k, int gtid, uint8_t* stg) {
+  // stage day k into buffer region reg: f64 price rows of day k and the members' z1s rows
+  __device__ __noinline__ static void stage_row(const TcParams& p, int k, int gtid, uint8_t* reg) {
     const EnvDev& e = p.e;
-    stage_price_rows(e, reinterpret_cast<double*>(stg + kOffP), k, gtid, 128);
-    float* zs = reinterpret_cast<float*>(stg + kOffZ);
+    stage_price_rows(e, reinterpret_cast<double*>(reg + kOffP), k, gtid, 128);
+    float* zs = reinterpret_cast<float*>(reg + kOffZ);
     for (int j = gtid; j < p.M * Plan::kHid; j += 128) {
       const int m = j / Plan::kHid, n = j % Plan::kHid;
       zs[j] = __ldg(p.z1s + ((size_t)m * p.z1s_rows + k) * Plan::kHid + n);
     }
   }
+  // the same rows by cp.async (16-byte chunks, no wait): completed by the next stage()
+  __device__ __forceinline__ static void prefetch_row(const TcParams& p, int k, int gtid, uint8_t* reg) {
+    const EnvDev& e = p.e;
+    const int np = kPriceRows * e.kp / 2;                 // 16-B chunks of the price rows
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(e.px + (size_t)k * kPriceRows * e.kp);
+    for (int j = gtid; j < np; j += 128) sm100::cp_async16(reg + kOffP + 16 * j, src + 16 * j);
+    constexpr int nz = Plan::kHid / 4;                   // chunks per member z1s row
+    for (int j = gtid; j < p.M * nz; j += 128) {
+      const int m = j / nz, c = j % nz;
+      sm100::cp_async16(reg + kOffZ + (m * Plan::kHid + 4 * c) * 4,
+                        p.z1s + ((size_t)m * p.z1s_rows + k) * Plan::kHid + 4 * c);
+    }
+    sm100::cp_async_commit();
+  }
+  __device__ __forceinline__ static uint8_t* region(uint8_t* stg, int b) { return stg + b * kRegion; }
 
   // once per step, all 128 threads of the tile: day of every env; if the tile sits on
   // one day, stage that day once (prices, z1s rows) for the whole step
@@ -139,25 +165,49 @@ struct StockOps {
       if (st.d < 0 || st.d + 1 >= e.rows) { st.bad = true; st.d = 0; }
       st.b0bits = (uint32_t)__bfloat16_as_ushort(__double2bfloat16(fdiv64(st.b, e.cash0)));
     }
-    if (gtid == 0) bc[0] = st.live ? st.d : -1;
-    gs_bar(bar_id);
+    if (gtid == 0) {
+      bc[0] = st.live ? st.d : -1;
+      // predicted day of the next step (lockstep envs): from this thread's env
+      int dn = -1;
+      if (st.live && !st.bad) {
+        if (st.t_ep + 1 < e.L) dn = st.d + 1;
+        else if (e.autoreset) dn = day_of(e, e.wadv ? (st.w + 1) % e.W : st.w, 0);
+      }
+      bc[1] = (dn >= 0 && dn + 1 < e.rows) ? dn : -1;
+    }
+    sm100::cp_async_wait<0>();                 // this thread's part of the last prefetch
+    gs_bar(bar_id);                            // ... and everyone else's
     FIN_TR(threadIdx.x == 128, t, 23);
-    const int d0 = bc[0];
-    const int staged = gs->staged;            // read by all before thread 0 may rewrite it
+    if (st.pend >= 0) {                        // the prefetched buffer becomes current
+      st.sb ^= 1;
+      const int k = st.kcur;
+      st.kcur = st.koth;
+      st.koth = k;
+      st.pend = -1;
+    }
+    const int d0 = bc[0], dn = bc[1];
     const bool uni = !gs_bar_or(bar_id, st.live && st.d != d0) && d0 >= 0;
     FIN_TR(threadIdx.x == 128, t, 24);
     st.zsm = uni;
-    if (uni && d0 != staged) {
-      stage_row(p, d0, gtid, stg);
-      if (gtid == 0) gs->staged = d0;
+    if (uni && d0 != st.kcur) {
+      stage_row(p, d0, gtid, region(stg, st.sb));
+      st.kcur = d0;
       gs_bar(bar_id);
+    }
+    if (gtid == 0) gs->staged = st.kcur;   // for group_apply in finish_step (after its barrier)
+    // rows of the predicted next day into the other buffer, under this step's work
+    // (that buffer was last read in the previous step, before this step's barriers)
+    if (dn >= 0 && t + 1 < p.T && dn != st.kcur) {
+      prefetch_row(p, dn, gtid, region(stg, st.sb ^ 1));
+      st.koth = dn;
+      st.pend = dn;
     }
     FIN_TR(threadIdx.x == 128, t, 25);
   }
 
   // factored layer 1: the shared-input term of this env's day, member m
   __device__ __forceinline__ static const float* l1_addend(State& st, const TcParams& p, int m, uint8_t* stg) {
-    if (st.zsm) return reinterpret_cast<const float*>(stg + kOffZ) + m * Plan::kHid;
+    if (st.zsm) return reinterpret_cast<const float*>(region(stg, st.sb) + kOffZ) + m * Plan::kHid;
     return p.z1s + ((size_t)m * p.z1s_rows + st.d) * Plan::kHid;
   }
 
@@ -278,9 +328,13 @@ struct StockOps {
     }
     GroupSlots* gs = reinterpret_cast<GroupSlots*>(stg + kOffS);
     group_apply(
-        gs, st.round, st.d, stepping, st.gtid, st.bar_id, [&](int k) { stage_row(p, k, st.gtid, stg); },
+        gs, st.round, st.d, stepping, st.gtid, st.bar_id,
+        [&](int k) {
+          stage_row(p, k, st.gtid, region(stg, st.sb));
+          st.kcur = k;
+        },
         [&]() {
-          const double* pd = reinterpret_cast<const double*>(stg + kOffP);
+          const double* pd = reinterpret_cast<const double*>(region(stg, st.sb) + kOffP);
           FIN_TR(threadIdx.x == 128, t, 19);
           const double v = st.vc;
           uint4 save[(KA + 7) / 8];   // local: read only by the rare exact buy redo
@@ -353,7 +407,7 @@ struct StockOps {
     }
     st.agg.s[FIN_AGG_SUM_REWARD] = st.rsum;
     if (p.o.agg_partial)
-      agg_group_write(st.agg, p.o.agg_partial + ((size_t)blockIdx.x * (blockDim.x / 128) + tile) * FIN_AGG_LEN, gtid,
+      agg_group_write(st.agg, p.o.agg_partial + ((size_t)blockIdx.x * (blockDim.x / 128 - 1) + tile) * FIN_AGG_LEN, gtid,
                       bar_id, tile);
   }
 };

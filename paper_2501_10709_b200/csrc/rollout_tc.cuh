@@ -9,10 +9,12 @@
 // streamed weight stage feeds the MMAs of all TILES tiles, so L2 weight traffic
 // per env-step is divided by TILES.
 //
-// Warp roles (64 + 128 * TILES threads):
+// Warp roles (128 + 128 * TILES threads, whole warpgroups so registers can move
+// between them with setmaxnreg):
 //   warp 0        producer: streams weight stages global(L2) -> smem ring (cp.async.bulk)
 //   warp 1        TMEM allocator + MMA issuer (one elected lane)
-//   warps 2..     one "env" warpgroup per tile: per-tile staging of the shared market
+//   warps 2, 3    idle (complete the first warpgroup)
+//   warps 4..     one "env" warpgroup per tile: per-tile staging of the shared market
 //                 row, observation rows, TMEM epilogues (bias, ReLU, bf16), action
 //                 sampling / ensemble averaging, the env transition (trade, reward,
 //                 done / reset) and online metrics -- thread r of a warpgroup owns env
@@ -39,6 +41,9 @@ struct TcParams {
   TrajDev o;
   const uint8_t* wpack[FIN_MAX_MEMBERS];  // packed member weights (TcPlan layout)
   const float* bias[FIN_MAX_MEMBERS];     // [HID + HID + OUT_PAD] fp32 per member
+  uint32_t bias_nz;                       // bit 3m + l: member m, layer l has a non-zero bias.  Adding
+                                          // an exactly-zero bias is the identity (up to the sign of a
+                                          // zero), so the epilogue skips those loads and adds
   int32_t kinds[FIN_MAX_MEMBERS];
   float mw[FIN_MAX_MEMBERS];              // member weights (weighted mode)
   int32_t M;
@@ -115,7 +120,7 @@ struct Smem {
 // RING: weight-ring slots; MINB: CTAs per SM (MINB = 2 runs two independent tiles per
 // SM whose env phases overlap each other's MMA / weight-streaming phases).
 template <class Plan, bool RESIDENT, int TILES, class Ops, int RING = kRing, int MINB = 1>
-__global__ void __launch_bounds__(64 + 128 * TILES, MINB) k_tc_rollout(const __grid_constant__ TcParams p) {
+__global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __grid_constant__ TcParams p) {
   using S = Smem<Plan, RESIDENT, TILES, Ops, RING>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int M = p.M;
@@ -161,6 +166,13 @@ __global__ void __launch_bounds__(64 + 128 * TILES, MINB) k_tc_rollout(const __g
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // register split (one CTA per SM, two tiles): the producer / MMA warpgroup needs few
+  // registers, the env warpgroups hold each env's whole state for all T steps.  Each
+  // role's code sits inside the branch that resized its registers, so ptxas allocates
+  // it against the new budget.
+  constexpr bool kSplitRegs = TILES == 2 && MINB == 1;
+  if (warp < 4) {
+  if constexpr (kSplitRegs) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
   if (warp == 0) {
     // ============================ producer ============================
     if (lane == 0) {
@@ -238,12 +250,14 @@ __global__ void __launch_bounds__(64 + 128 * TILES, MINB) k_tc_rollout(const __g
       }
     }
     __syncwarp();
+  }
   } else {
+    if constexpr (kSplitRegs) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
     // ============================ env warpgroups ============================
-    const int tile = (warp - 2) >> 2;
+    const int tile = (warp - 4) >> 2;
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;          // env row of the tile == TMEM lane
-    const int gtid = (warp - 2 - tile * 4) * 32 + lane;   // thread index within the tile's warpgroup
+    const int gtid = (warp - 4 - tile * 4) * 32 + lane;   // thread index within the tile's warpgroup
     const int env = (blockIdx.x * TILES + tile) * kTileM + row;
     const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tile * Plan::kHid);
     const uint32_t xa = sm100::smem_u32(sA + tile * S::kA);
@@ -269,46 +283,60 @@ __global__ void __launch_bounds__(64 + 128 * TILES, MINB) k_tc_rollout(const __g
           ++d_use;
           FIN_TR(row == 0 && tile == 0 && m == 0, t, 2 + 2 * l);
           sm100::tc_fence_after();
-          const float* bl = bias + l * Plan::kHid;
+          const float* bl = ((p.bias_nz >> (3 * m + l)) & 1u) ? bias + l * Plan::kHid : nullptr;
           // factored layer 1: + shared-input term of the env's day (smem or global row)
           const float* add = l == 0 ? Ops::l1_addend(st, p, m, stg) : nullptr;
           // debug / parity log of the bf16 hidden activations (teacher-forced layer checks)
           uint4* hlog = reinterpret_cast<uint4*>(Ops::hidden_ptr(st, p, env, t, m, l, Plan::kHid));
+          // 16 columns per TMEM load: half the registers of 32-column chunks (the env
+          // state lives in registers across the whole rollout)
 #pragma unroll 1
-          for (int c = 0; c < Plan::kHid / 32; ++c) {
-            uint32_t v[32];
-            sm100::tmem_ld32(t_lane + (uint32_t)(c * 32), v);
+          for (int c = 0; c < Plan::kHid / 16; ++c) {
+            uint32_t v[16];
+            sm100::tmem_ld16(t_lane + (uint32_t)(c * 16), v);
             // addend b (+ z1s for the factored layer 1), 128-bit broadcast loads, issued
             // while the TMEM load is in flight
-            float ad[32];
-            const float4* b4 = reinterpret_cast<const float4*>(bl + c * 32);
+            float ad[16];
+            if (bl) {
+              const float4* b4 = reinterpret_cast<const float4*>(bl + c * 16);
 #pragma unroll
-            for (int q4 = 0; q4 < 8; ++q4) {
-              const float4 x = b4[q4];
-              ad[4 * q4] = x.x; ad[4 * q4 + 1] = x.y; ad[4 * q4 + 2] = x.z; ad[4 * q4 + 3] = x.w;
+              for (int q4 = 0; q4 < 4; ++q4) {
+                const float4 x = b4[q4];
+                ad[4 * q4] = x.x; ad[4 * q4 + 1] = x.y; ad[4 * q4 + 2] = x.z; ad[4 * q4 + 3] = x.w;
+              }
             }
             if (add) {
-              const float4* a4 = reinterpret_cast<const float4*>(add + c * 32);
+              const float4* a4 = reinterpret_cast<const float4*>(add + c * 16);
 #pragma unroll
-              for (int q4 = 0; q4 < 8; ++q4) {
+              for (int q4 = 0; q4 < 4; ++q4) {
                 const float4 y = a4[q4];
-                ad[4 * q4] += y.x; ad[4 * q4 + 1] += y.y; ad[4 * q4 + 2] += y.z; ad[4 * q4 + 3] += y.w;
+                if (bl) {
+                  ad[4 * q4] += y.x; ad[4 * q4 + 1] += y.y; ad[4 * q4 + 2] += y.z; ad[4 * q4 + 3] += y.w;
+                } else {
+                  ad[4 * q4] = y.x; ad[4 * q4 + 1] = y.y; ad[4 * q4 + 2] = y.z; ad[4 * q4 + 3] = y.w;
+                }
               }
             }
             sm100::tmem_wait_ld();
-            uint32_t pk[16];
+            uint32_t pk[8];
+            if (bl || add) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)   // ReLU + bf16 in one cvt.rn.relu.bf16x2
-              pk[j] = sm100::pack_bf16_relu(__uint_as_float(v[2 * j]) + ad[2 * j],
-                                            __uint_as_float(v[2 * j + 1]) + ad[2 * j + 1]);
+              for (int j = 0; j < 8; ++j)   // ReLU + bf16 in one cvt.rn.relu.bf16x2
+                pk[j] = sm100::pack_bf16_relu(__uint_as_float(v[2 * j]) + ad[2 * j],
+                                              __uint_as_float(v[2 * j + 1]) + ad[2 * j + 1]);
+            } else {
 #pragma unroll
-            for (int g = 0; g < 4; ++g)
-              sts128(xa + cm_off(row, c * 4 + g, Plan::kHid / 8), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2],
+              for (int j = 0; j < 8; ++j)
+                pk[j] = sm100::pack_bf16_relu(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+            }
+#pragma unroll
+            for (int g = 0; g < 2; ++g)
+              sts128(xa + cm_off(row, c * 2 + g, Plan::kHid / 8), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2],
                      pk[4 * g + 3]);
             if (hlog) {
 #pragma unroll
-              for (int g = 0; g < 4; ++g)
-                hlog[c * 4 + g] = make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+              for (int g = 0; g < 2; ++g)
+                hlog[c * 2 + g] = make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
             }
           }
           sm100::fence_proxy_async_smem();
@@ -327,8 +355,13 @@ __global__ void __launch_bounds__(64 + 128 * TILES, MINB) k_tc_rollout(const __g
           uint32_t v[16];
           sm100::tmem_ld16(t_lane + (uint32_t)(c * 16), v);
           sm100::tmem_wait_ld();
+          if ((p.bias_nz >> (3 * m + 2)) & 1u) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) z[c * 16 + j] = __uint_as_float(v[j]) + bias[2 * Plan::kHid + c * 16 + j];
+            for (int j = 0; j < 16; ++j) z[c * 16 + j] = __uint_as_float(v[j]) + bias[2 * Plan::kHid + c * 16 + j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) z[c * 16 + j] = __uint_as_float(v[j]);
+          }
         }
         sm100::tc_fence_before();
         Ops::consume(st, p, env, t, m, z);
@@ -355,7 +388,7 @@ cudaError_t launch(const TcParams& p, int n_envs, cudaStream_t s) {
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (err != cudaSuccess) return err;
   const int per_cta = kTileM * TILES;
-  kern<<<(n_envs + per_cta - 1) / per_cta, 64 + 128 * TILES, bytes, s>>>(p);
+  kern<<<(n_envs + per_cta - 1) / per_cta, 128 + 128 * TILES, bytes, s>>>(p);
   return cudaGetLastError();
 }
 

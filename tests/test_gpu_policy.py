@@ -213,6 +213,38 @@ def test_fused_rollout_deterministic_and_partition_invariant_philox():
     assert np.abs(res[0][0]).sum() > 0
 
 
+def test_two_tiles_per_cta_match_one_tile_per_cta():
+    """More tiles than SMs switches the fused rollout to two tiles per CTA (one weight
+    stream for both, a setmaxnreg register split); fewer tiles run one tile per CTA.
+    Both layouts must give the same bits: N = 19200 (150 tiles, two per CTA) against
+    the same envs as two handles of 9600 (75 tiles each), Philox noise, T = 35 with a
+    reset, full trajectory compared."""
+    import torch
+    fin = _fin()
+    m = market.stock_c1(rows=1008)
+    layers = spol.kaiming_bf16(spol.STOCK_DIMS, 0)
+    N, T, H = 19200, 35, 9600
+    kw = dict(num_assets=30, num_indicators=8, num_rows=1008, episode_len=30, num_windows=195, window_stride=5,
+              window_block=128)
+    res = []
+    for lo, hi in ((0, N), (0, H), (H, N)):
+        _, fcfg = stock_pair(num_envs=hi - lo, env_offset=lo, **kw)
+        env = fin.fin_env_create(fcfg, m.market)
+        pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, layers)
+        n = hi - lo
+        logs = dict(actions=zeros((T, n, 30), torch.int16), cash=zeros((T, n), torch.float64),
+                    reward=zeros((T, n), torch.float32), done=zeros((T, n), torch.uint8),
+                    ep_metrics=zeros((3, n, 3), torch.float64), ep_count=zeros(n, torch.int32))
+        fin.fin_rollout(env, [pol], T, fin.make_noise(fin.FIN_NOISE_PHILOX, 99), fin.make_traj(**logs))
+        assert fin.fin_env_check(env) == 0
+        res.append({k: host(v) for k, v in logs.items()})
+    for k in res[0]:
+        ax = 1 if res[0][k].ndim >= 2 and k != "ep_count" else 0
+        joined = np.concatenate([res[1][k], res[2][k]], axis=ax)
+        assert np.array_equal(res[0][k], joined, equal_nan=True), k
+    assert res[0]["done"].sum() == N and np.abs(res[0]["actions"]).sum() > 0
+
+
 def test_philox_normals_match_oracle_generator():
     import torch
     fin = _fin()
