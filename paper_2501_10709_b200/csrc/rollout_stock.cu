@@ -429,7 +429,9 @@ struct ProbeOps {
   __device__ __forceinline__ static void init(State& st, const TcParams& p, int env, int row) { st.b = env; }
   __device__ __forceinline__ static void stage(State&, const TcParams&, int, int, int, uint8_t*, int) {}
   __device__ __forceinline__ static const float* l1_addend(State& st, const TcParams& p, int m, uint8_t*) {
-    if constexpr (kFactored) return st.b < p.B ? p.z1s + (size_t)st.b * Plan::kHid : nullptr;
+    // never null for a factored net (the epilogue's addend branch must be warp-uniform):
+    // rows past B read row 0 and their outputs are dropped
+    if constexpr (kFactored) return p.z1s + (size_t)(st.b < p.B ? st.b : 0) * Plan::kHid;
     else return nullptr;
   }
   __device__ __forceinline__ static void build_obs(State& st, const TcParams& p, int env, int row, int t, int m,

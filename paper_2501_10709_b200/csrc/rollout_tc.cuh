@@ -26,6 +26,8 @@
 // layer's MMAs have completed when d_full fires), so the observation is rebuilt
 // for every ensemble member from the per-step staging area.
 #pragma once
+#include <type_traits>
+
 #include "fin_internal.cuh"
 #include "sm100.cuh"
 #include "tc_plan.cuh"
@@ -289,56 +291,59 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
           // debug / parity log of the bf16 hidden activations (teacher-forced layer checks)
           uint4* hlog = reinterpret_cast<uint4*>(Ops::hidden_ptr(st, p, env, t, m, l, Plan::kHid));
           // 16 columns per TMEM load: half the registers of 32-column chunks (the env
-          // state lives in registers across the whole rollout)
+          // state lives in registers across the whole rollout).  One loop per addend
+          // combination (uniform branch), so an absent addend costs no issue slots.
+          auto epilogue = [&](auto has_b, auto has_add) {
+            constexpr bool HB = decltype(has_b)::value, HA = decltype(has_add)::value;
 #pragma unroll 1
-          for (int c = 0; c < Plan::kHid / 16; ++c) {
-            uint32_t v[16];
-            sm100::tmem_ld16(t_lane + (uint32_t)(c * 16), v);
-            // addend b (+ z1s for the factored layer 1), 128-bit broadcast loads, issued
-            // while the TMEM load is in flight
-            float ad[16];
-            if (bl) {
-              const float4* b4 = reinterpret_cast<const float4*>(bl + c * 16);
+            for (int c = 0; c < Plan::kHid / 16; ++c) {
+              uint32_t v[16];
+              sm100::tmem_ld16(t_lane + (uint32_t)(c * 16), v);
+              // addend b (+ z1s for the factored layer 1), 128-bit broadcast loads, issued
+              // while the TMEM load is in flight
+              float ad[16];
 #pragma unroll
               for (int q4 = 0; q4 < 4; ++q4) {
-                const float4 x = b4[q4];
+                float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+                if constexpr (HB) x = reinterpret_cast<const float4*>(bl + c * 16)[q4];
+                if constexpr (HA) {
+                  const float4 y = reinterpret_cast<const float4*>(add + c * 16)[q4];
+                  if constexpr (HB) {
+                    x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
+                  } else {
+                    x = y;
+                  }
+                }
                 ad[4 * q4] = x.x; ad[4 * q4 + 1] = x.y; ad[4 * q4 + 2] = x.z; ad[4 * q4 + 3] = x.w;
               }
-            }
-            if (add) {
-              const float4* a4 = reinterpret_cast<const float4*>(add + c * 16);
+              sm100::tmem_wait_ld();
+              uint32_t pk[8];
 #pragma unroll
-              for (int q4 = 0; q4 < 4; ++q4) {
-                const float4 y = a4[q4];
-                if (bl) {
-                  ad[4 * q4] += y.x; ad[4 * q4 + 1] += y.y; ad[4 * q4 + 2] += y.z; ad[4 * q4 + 3] += y.w;
-                } else {
-                  ad[4 * q4] = y.x; ad[4 * q4 + 1] = y.y; ad[4 * q4 + 2] = y.z; ad[4 * q4 + 3] = y.w;
-                }
+              for (int j = 0; j < 8; ++j) {   // ReLU + bf16 in one cvt.rn.relu.bf16x2
+                if constexpr (HB || HA)
+                  pk[j] = sm100::pack_bf16_relu(__uint_as_float(v[2 * j]) + ad[2 * j],
+                                                __uint_as_float(v[2 * j + 1]) + ad[2 * j + 1]);
+                else
+                  pk[j] = sm100::pack_bf16_relu(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
               }
-            }
-            sm100::tmem_wait_ld();
-            uint32_t pk[8];
-            if (bl || add) {
-#pragma unroll
-              for (int j = 0; j < 8; ++j)   // ReLU + bf16 in one cvt.rn.relu.bf16x2
-                pk[j] = sm100::pack_bf16_relu(__uint_as_float(v[2 * j]) + ad[2 * j],
-                                              __uint_as_float(v[2 * j + 1]) + ad[2 * j + 1]);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 8; ++j)
-                pk[j] = sm100::pack_bf16_relu(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-            }
-#pragma unroll
-            for (int g = 0; g < 2; ++g)
-              sts128(xa + cm_off(row, c * 2 + g, Plan::kHid / 8), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2],
-                     pk[4 * g + 3]);
-            if (hlog) {
 #pragma unroll
               for (int g = 0; g < 2; ++g)
-                hlog[c * 2 + g] = make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+                sts128(xa + cm_off(row, c * 2 + g, Plan::kHid / 8), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2],
+                       pk[4 * g + 3]);
+              if (hlog) {
+#pragma unroll
+                for (int g = 0; g < 2; ++g)
+                  hlog[c * 2 + g] = make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+              }
             }
-          }
+          };
+          using T1 = std::true_type;
+          using F0 = std::false_type;
+          // (bl is uniform; add is null for every thread or for none -- Ops contract)
+          if (bl && add) epilogue(T1{}, T1{});
+          else if (bl) epilogue(T1{}, F0{});
+          else if (add) epilogue(F0{}, T1{});
+          else epilogue(F0{}, F0{});
           sm100::fence_proxy_async_smem();
           sm100::tc_fence_before();
           sm100::mbar_arrive(a_full);
