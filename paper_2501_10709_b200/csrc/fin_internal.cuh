@@ -176,15 +176,22 @@ __device__ __forceinline__ void metric_start(MetricAcc& m, double v) {
   m.v0 = v; m.vprev = v; m.peak = v; m.mdd = 0.0; m.mean = 0.0; m.m2 = 0.0; m.n = 0;
 }
 
+// One division per point (the return r = v / v_prev - 1 of the definition).  The
+// Welford mean update multiplies by the correctly rounded 1/n (within an ulp of the
+// division), and the drawdown v / peak - 1 is only divided out when v falls below
+// (1 + mdd) peak (checked by a multiply with a 1e-12 margin, so no new minimum is
+// missed): a new maximum drawdown is rare, a division per point is not.
 __device__ __forceinline__ void metric_push(MetricAcc& m, double v) {
   double r = fsub64(fdiv64(v, m.vprev), 1.0);
   m.n += 1;
   double delta = fsub64(r, m.mean);
-  m.mean = fadd64(m.mean, fdiv64(delta, (double)m.n));
+  m.mean = fadd64(m.mean, fmul64(delta, __drcp_rn(nn2d(m.n))));
   m.m2 = fadd64(m.m2, fmul64(delta, fsub64(r, m.mean)));
   if (v > m.peak) m.peak = v;
-  double dd = fsub64(fdiv64(v, m.peak), 1.0);
-  if (dd < m.mdd) m.mdd = dd;
+  if (v < fmul64(fadd64(m.mdd, 1.0 + 1e-12), m.peak)) {
+    const double dd = fsub64(fdiv64(v, m.peak), 1.0);
+    if (dd < m.mdd) m.mdd = dd;
+  }
   m.vprev = v;
 }
 

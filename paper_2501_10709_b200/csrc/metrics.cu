@@ -37,13 +37,15 @@ __device__ __forceinline__ void seg_push(Seg& s, double vp, double v) {
   double r = fsub64(fdiv64(v, vp), 1.0);
   s.n += 1;
   double delta = fsub64(r, s.mean);
-  s.mean = fadd64(s.mean, fdiv64(delta, (double)s.n));
+  s.mean = fadd64(s.mean, fmul64(delta, __drcp_rn(nn2d(s.n))));
   s.m2 = fadd64(s.m2, fmul64(delta, fsub64(r, s.mean)));
   if (s.n == 1) { s.vmax = v; s.vmin = v; s.mdd = 0.0; }
   else {
     if (v > s.vmax) s.vmax = v;
-    double dd = fsub64(fdiv64(v, s.vmax), 1.0);
-    if (dd < s.mdd) s.mdd = dd;
+    if (v < fmul64(fadd64(s.mdd, 1.0 + 1e-12), s.vmax)) {   // see metric_push
+      const double dd = fsub64(fdiv64(v, s.vmax), 1.0);
+      if (dd < s.mdd) s.mdd = dd;
+    }
     if (v < s.vmin) s.vmin = v;
   }
   s.vlast = v;
@@ -106,31 +108,66 @@ __global__ void k_pass_b(const double* __restrict__ eq, int N, int nchunks, doub
   }
 }
 
+// Pass C walks a chunk from its carried-in accumulator (carry == null: one chunk,
+// the single fused pass, starting at row 0).  The equity / done rows of the next U
+// steps are loaded ahead of the arithmetic of the current U (registers), so each
+// thread keeps 9 U bytes in flight.
 __global__ void k_pass_c(const double* __restrict__ eq, const uint8_t* __restrict__ done, int T, int N, int chunk,
                          double reset_eq, double ppy, double rf, const MetricAcc* __restrict__ carry,
                          const int32_t* __restrict__ base, double* __restrict__ ep, int cap,
                          int32_t* __restrict__ cnt_out, double* __restrict__ partial) {
+  constexpr int U = 8;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   AggAcc agg;
   agg_init(agg);
   if (i < N) {
     const int t0 = c * chunk, t1 = min(T, t0 + chunk);
-    MetricAcc m = carry[(size_t)c * N + i];
-    int k = base[(size_t)c * N + i];
-    for (int t = t0; t < t1; ++t) {
-      const double v = eq[(size_t)(t + 1) * N + i];
-      metric_push(m, v);
-      if (done[(size_t)t * N + i]) {
-        double em[3];
-        metric_finish(m, ppy, rf, em);
-        if (ep && k < cap) {
-          double* d = ep + ((size_t)k * N + i) * 3;
-          d[0] = em[0]; d[1] = em[1]; d[2] = em[2];
+    MetricAcc m;
+    int k = 0;
+    if (carry) {
+      m = carry[(size_t)c * N + i];
+      k = base[(size_t)c * N + i];
+    } else {
+      metric_start(m, __ldg(eq + i));
+    }
+    double vb[U];
+    uint8_t db[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      vb[u] = t0 + u < t1 ? __ldg(eq + (size_t)(t0 + u + 1) * N + i) : 0.0;
+      db[u] = t0 + u < t1 ? __ldg(done + (size_t)(t0 + u) * N + i) : 0;
+    }
+    for (int t = t0; t < t1; t += U) {
+      double vn[U];
+      uint8_t dn[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int tn = t + U + u;
+        vn[u] = tn < t1 ? __ldg(eq + (size_t)(tn + 1) * N + i) : 0.0;
+        dn[u] = tn < t1 ? __ldg(done + (size_t)tn * N + i) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (t + u < t1) {
+          metric_push(m, vb[u]);
+          if (db[u]) {
+            double em[3];
+            metric_finish(m, ppy, rf, em);
+            if (ep && k < cap) {
+              double* d = ep + ((size_t)k * N + i) * 3;
+              d[0] = em[0]; d[1] = em[1]; d[2] = em[2];
+            }
+            agg_episode(agg, em);
+            ++k;
+            metric_start(m, reset_eq);
+          }
         }
-        agg_episode(agg, em);
-        ++k;
-        metric_start(m, reset_eq);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        vb[u] = vn[u];
+        db[u] = dn[u];
       }
     }
     if (c == gridDim.y - 1 && cnt_out) cnt_out[i] = k;
@@ -162,6 +199,13 @@ cudaError_t launch_episode_metrics(const double* equity, const uint8_t* done, in
   if (nchunks > 4096) nchunks = 4096;
   const int chunk = (T + nchunks - 1) / nchunks > 0 ? (T + nchunks - 1) / nchunks : 1;
   nchunks = T > 0 ? (T + chunk - 1) / chunk : 1;
+  dim3 grid(env_blocks, nchunks);
+  *n_blocks = env_blocks * nchunks;
+  if (nchunks == 1) {   // enough envs to fill the GPU: one fused pass, each row read once
+    k_pass_c<<<grid, kThreads, 0, s>>>(equity, done, T, N, chunk, reset_eq, ppy, rf, nullptr, nullptr, ep, cap,
+                                        cnt, partial);
+    return cudaGetLastError();
+  }
   Seg* seg = nullptr;
   MetricAcc* carry = nullptr;
   int32_t* base = nullptr;
@@ -169,12 +213,10 @@ cudaError_t launch_episode_metrics(const double* equity, const uint8_t* done, in
   if ((err = cudaMallocAsync(&seg, sizeof(Seg) * (size_t)nchunks * N, s)) != cudaSuccess) return err;
   if ((err = cudaMallocAsync(&carry, sizeof(MetricAcc) * (size_t)nchunks * N, s)) != cudaSuccess) return err;
   if ((err = cudaMallocAsync(&base, sizeof(int32_t) * (size_t)nchunks * N, s)) != cudaSuccess) return err;
-  dim3 grid(env_blocks, nchunks);
   k_pass_a<<<grid, kThreads, 0, s>>>(equity, done, T, N, chunk, reset_eq, seg);
   k_pass_b<<<env_blocks, kThreads, 0, s>>>(equity, N, nchunks, reset_eq, seg, carry, base);
   k_pass_c<<<grid, kThreads, 0, s>>>(equity, done, T, N, chunk, reset_eq, ppy, rf, carry, base, ep, cap, cnt,
                                       partial);
-  *n_blocks = env_blocks * nchunks;
   cudaFreeAsync(seg, s);
   cudaFreeAsync(carry, s);
   cudaFreeAsync(base, s);

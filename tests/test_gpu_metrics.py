@@ -9,8 +9,12 @@ from oracle import metrics as omet
 pytestmark = [pytest.mark.gpu, needs_gpu]
 
 
-@pytest.mark.parametrize("T,N,p_done", [(64, 8, 0.05), (3000, 300, 0.01), (20000, 40, 0.0005), (7, 1, 0.5)])
+@pytest.mark.parametrize("T,N,p_done", [(64, 8, 0.05), (3000, 300, 0.01), (20000, 40, 0.0005), (7, 1, 0.5),
+                                         (45, 270000, 1 / 30)])
 def test_episode_metrics_parity(T, N, p_done):
+    """Chunked three-pass scans (small N) and the single fused pass (N >= 2048 x 128:
+    every row read once; checked on a seeded sample of 400 envs plus the first and
+    last env)."""
     import torch
     from paper_2501_10709_b200 import fin
     rng = np.random.default_rng(T + N)
@@ -24,7 +28,9 @@ def test_episode_metrics_parity(T, N, p_done):
     em, ec, agg = host(em), host(ec), host(agg)
     n = 0
     sh_sum = 0.0
-    for i in range(N):
+    full = N <= 1000
+    check = range(N) if full else sorted(set([0, N - 1] + list(rng.choice(N, 400, replace=False))))
+    for i in check:
         curves = []
         cur = [eq[0, i]]
         for t in range(T):
@@ -43,5 +49,8 @@ def test_episode_metrics_parity(T, N, p_done):
                 np.testing.assert_allclose(em[j, i, 1], sh, rtol=1e-7, atol=1e-9)
                 sh_sum += sh
             n += 1
-    assert agg[fin.FIN_AGG_EPISODES] == n
-    np.testing.assert_allclose(agg[fin.FIN_AGG_SUM_SHARPE], sh_sum, rtol=1e-7, atol=1e-9)
+    if full:
+        assert agg[fin.FIN_AGG_EPISODES] == n
+        np.testing.assert_allclose(agg[fin.FIN_AGG_SUM_SHARPE], sh_sum, rtol=1e-7, atol=1e-9)
+    else:
+        assert agg[fin.FIN_AGG_EPISODES] == ec.sum()
