@@ -387,14 +387,16 @@ def hbm_kernels(fin, torch):
           "actions 60 + reward 4 + done 1 per env-step, state in/out once per call")
     del env, acts, tr
     T, N = 2048, 1 << 18
-    done = (torch.rand((T, N), device="cuda", generator=g) < 1 / 30).to(torch.uint8)
+    # lockstep episodes of 30 steps, as the rollouts produce them (dones of a tile coincide)
+    done = torch.zeros((T, N), dtype=torch.uint8, device="cuda")
+    done[29::30] = 1
     eq = 1e6 * torch.exp(torch.cumsum(0.01 * torch.randn((T + 1, N), device="cuda", generator=g,
                                                          dtype=torch.float64), 0))
     epm, cnt = z((160, N, 3), torch.float64), z(N, torch.int32)
     ms = b2b(lambda: fin.fin_episode_metrics(eq, done, 1e6, ep_metrics=epm, ep_count=cnt))
     entry("metrics_kernel_hbm", "k_pass_a/b/c (K6)", N * T,
           T * N * 9 + N * 8 + int(cnt.sum().item()) * 24 + N * 4, ms,
-          "equity f64 + done u8 per env-step read, episode rows written")
+          "equity f64 + done u8 per env-step read, episode rows written; lockstep 30-step episodes")
     return res
 
 

@@ -196,13 +196,15 @@ __device__ __forceinline__ void metric_push(MetricAcc& m, double v) {
 }
 
 // (cum, sharpe, mdd) of a finished episode; Sharpe = sqrt(ppy) mean / std(ddof 1),
-// NaN when n < 2 or std == 0 (reading R21).
+// NaN when n < 2 or std == 0 (reading R21).  Reciprocals instead of divisions (each
+// within an ulp): when episodes end at different steps across a warp this runs
+// divergently on most steps, so its cost matters.
 __device__ __forceinline__ void metric_finish(const MetricAcc& m, double ppy, double rf, double out[3]) {
-  out[0] = fsub64(fdiv64(m.vprev, m.v0), 1.0);
+  out[0] = fsub64(fmul64(m.vprev, __drcp_rn(m.v0)), 1.0);
   double sh = __longlong_as_double(0x7ff8000000000000ULL);
   if (m.n >= 2) {
-    double sd = sqrt(fdiv64(m.m2, (double)(m.n - 1)));
-    if (sd > 0.0) sh = fdiv64(fmul64(sqrt(ppy), fsub64(m.mean, rf)), sd);
+    const double var = fmul64(m.m2, __drcp_rn(nn2d(m.n - 1)));
+    if (var > 0.0) sh = fmul64(fmul64(sqrt(ppy), fsub64(m.mean, rf)), rsqrt(var));
   }
   out[1] = sh;
   out[2] = m.mdd;
