@@ -6,12 +6,15 @@
 // online episode metrics.  All envs of the C3 workload read the same row t
 // (lockstep, reading R27): once per step a tile stages the bf16 factor part of the
 // observation and the two book rows in shared memory; a tile whose envs sit on
-// different rows takes the per-env path.
+// different rows takes the per-env path.  The market rows live in a 3-slot ring
+// (row k in slot k mod 3): during step t the tile cp.asyncs row t+2, so the C3 loop
+// never waits on HBM for its next row (276 MB series, streamed once).
 #include <cuda_bf16.h>
 
 #include "env_crypto.cuh"
 #include "philox.cuh"
 #include "rollout_tc.cuh"
+#include "sm100.cuh"
 
 namespace {
 
@@ -40,12 +43,15 @@ struct CryptoOps {
   static constexpr int IN = 2 + FIN_C_FACTORS;  // 103
   static constexpr int KT8 = PlanCrypto::kIn / 8;
   static constexpr int kOffX = 0;                               // bf16 obs row (112)
-  static constexpr int kOffR = 256;                             // rows t, t+1 (2 x 144 floats)
-  static constexpr int kOffT = kOffR + 2 * FIN_C_ROW * 4;
+  static constexpr int kOffR = 256;                             // ring of 3 rows (3 x 144 floats)
+  static constexpr int kOffT = kOffR + 3 * FIN_C_ROW * 4;
   static constexpr int kStageBytes = kOffT + 16;
 
   struct State {
     bool live, uniform;
+    int k0, k1, k2;    // market row held by ring slot 0 / 1 / 2 (-1: none); same in every thread
+    int pend;          // row being prefetched (-1: none)
+    int slot_t;        // ring slot of this step's row (uniform case)
     double b;
     int h, tau, t_ep;
     int act;
@@ -64,6 +70,9 @@ struct CryptoOps {
     st.rsum = 0.0;
     st.bad = st.nonfinite = false;
     st.act = 0;
+    st.k0 = st.k1 = st.k2 = -1;
+    st.pend = -1;
+    st.slot_t = 0;
     agg_init(st.agg);
     if (st.live) {
       st.b = e.cash[env];
@@ -85,19 +94,54 @@ struct CryptoOps {
     int tr = st.t_ep;
     if (st.live && (tr + 1 >= e.rows)) { st.bad = true; tr = 0; }
     if (gtid == 0) sr[0] = st.live ? tr : -1;
-    bar_sync128(bar_id);
+    sm100::cp_async_wait<0>();      // this thread's part of the last prefetch ...
+    bar_sync128(bar_id);            // ... and everyone else's
+    st.pend = -1;
     const int t0 = sr[0];
     const bool uni = bar_red_and(bar_id, !st.live || tr == t0) && t0 >= 0;
     st.uniform = uni;
     if (uni) {
-      const float* mrow = e.market + (size_t)t0 * FIN_C_ROW;
+      float* ring = reinterpret_cast<float*>(stg + kOffR);
+      // rows t0 and t0 + 1 must be in the ring; load whichever is missing
+      const bool have0 = held(st, t0), have1 = held(st, t0 + 1);
+      if (!have0 || !have1) {
+        for (int j = gtid; j < 2 * FIN_C_ROW; j += 128) {
+          const int r = t0 + (j >= FIN_C_ROW ? 1 : 0);
+          if ((r == t0 && !have0) || (r == t0 + 1 && !have1))
+            ring[(r % 3) * FIN_C_ROW + (j % FIN_C_ROW)] = __ldg(e.market + (size_t)r * FIN_C_ROW + (j % FIN_C_ROW));
+        }
+        set_held(st, t0);
+        set_held(st, t0 + 1);
+      }
+      st.slot_t = t0 % 3;
+      const float* mrow = ring + st.slot_t * FIN_C_ROW;
       uint16_t* xs = reinterpret_cast<uint16_t*>(stg + kOffX);
+      bar_sync128(bar_id);   // ring rows visible
       for (int idx = gtid; idx < PlanCrypto::kIn; idx += 128)
-        xs[idx] = (idx >= 2 && idx < IN) ? (uint16_t)bf16_bits(__ldg(mrow + FIN_C_F0 + idx - 2)) : (uint16_t)0;
-      float* rs = reinterpret_cast<float*>(stg + kOffR);
-      for (int j = gtid; j < 2 * FIN_C_ROW; j += 128) rs[j] = __ldg(mrow + j);
-      bar_sync128(bar_id);
+        xs[idx] = (idx >= 2 && idx < IN) ? (uint16_t)bf16_bits(mrow[FIN_C_F0 + idx - 2]) : (uint16_t)0;
+      // prefetch row t0 + 2 (the next step's marking row) into the third slot
+      const int r2 = t0 + 2;
+      if (r2 < e.rows && t + 1 < p.T && !held(st, r2)) {
+        const float* src = e.market + (size_t)r2 * FIN_C_ROW;
+        float* dst = ring + (r2 % 3) * FIN_C_ROW;
+        for (int j = gtid; j < FIN_C_ROW / 4; j += 128) sm100::cp_async16(dst + 4 * j, src + 4 * j);
+        sm100::cp_async_commit();
+        set_held(st, r2);
+        st.pend = r2;
+      }
+      bar_sync128(bar_id);   // xs visible
     }
+  }
+
+  __device__ __forceinline__ static bool held(const State& st, int r) {
+    const int s = r % 3;
+    return (s == 0 ? st.k0 : (s == 1 ? st.k1 : st.k2)) == r;
+  }
+  __device__ __forceinline__ static void set_held(State& st, int r) {
+    const int s = r % 3;
+    if (s == 0) st.k0 = r;
+    else if (s == 1) st.k1 = r;
+    else st.k2 = r;
   }
 
   __device__ __forceinline__ static void build_obs(State& st, const TcParams& p, int env, int row, int t, int m,
@@ -177,11 +221,12 @@ struct CryptoOps {
       if (p.o.done) p.o.done[ti] = 1;
       return;
     }
-    const float* row = st.uniform ? reinterpret_cast<const float*>(stg + kOffR)
-                                  : e.market + (size_t)st.t_ep * FIN_C_ROW;
+    const float* ring = reinterpret_cast<const float*>(stg + kOffR);
+    const float* row = st.uniform ? ring + st.slot_t * FIN_C_ROW : e.market + (size_t)st.t_ep * FIN_C_ROW;
+    const float* row_next = st.uniform ? ring + ((st.slot_t + 1) % 3) * FIN_C_ROW : row + FIN_C_ROW;
     double v, vn;
     int delta;
-    crypto_transition(e, st.b, st.h, st.tau, row, row + FIN_C_ROW, st.act, v, vn, delta);
+    crypto_transition(e, st.b, st.h, st.tau, row, row_next, st.act, v, vn, delta);
     st.t_ep += 1;
     const bool done = st.t_ep == e.L;
     const float r = (float)fmul64(fsub64(vn, v), e.scale);

@@ -137,8 +137,14 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
   uint64_t* w_full = bars;
   uint64_t* w_empty = bars + kRing;
   uint64_t* a_full = bars + 2 * kRing;
-  uint64_t* d_full = bars + 2 * kRing + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kRing + 2);
+  uint64_t* d_full = bars + 2 * kRing + 1;          // [TILES]: one per tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kRing + 1 + TILES);
+  // Resident weights: each tile's thread 0 issues its own MMAs right after the tile's
+  // epilogue barrier (the issue code sits in the env warps' hot path; a separate MMA
+  // warp woken per layer cost ~1,000 cycles per layer in the C3 timeline, mostly
+  // instruction fetch of a code path that runs once per layer).  Streamed weights keep
+  // the MMA warp: its stages feed both tiles.
+  constexpr bool kEnvIssue = RESIDENT;
   uint8_t* sW = reinterpret_cast<uint8_t*>(bars) + 512;
   float* sBias = reinterpret_cast<float*>(sW + S::w_bytes(M));
 
@@ -156,7 +162,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
       sm100::mbar_init(&w_empty[s], 1);
     }
     sm100::mbar_init(a_full, 128 * TILES);
-    sm100::mbar_init(d_full, 1);
+    for (int tl = 0; tl < TILES; ++tl) sm100::mbar_init(&d_full[tl], 1);
     sm100::fence_mbar_init();
   }
   if (warp == 1) {
@@ -202,7 +208,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
     __syncwarp();
   } else if (warp == 1) {
     // ============================ MMA issuer ============================
-    if (lane == 0) {
+    if (lane == 0 && !kEnvIssue) {
       uint32_t it = 0, a_use = 0;
       if (RESIDENT) sm100::mbar_wait(&w_full[0], 0);
       const uint32_t aa = sm100::smem_u32(sA), wa = sm100::smem_u32(sW);
@@ -245,7 +251,8 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
                 ++it;
               }
             }
-            sm100::mma_commit(d_full);
+            sm100::mma_commit(d_full);   // TILES == 1 or 2 share one phase when the MMA warp issues
+            if (TILES > 1) sm100::mma_commit(&d_full[1]);
             FIN_TR(m == 0, t, 10 + 2 * l);
           }
         }
@@ -268,20 +275,51 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
     typename Ops::State st;
     Ops::init(st, p, env, row);
     uint32_t d_use = 0;
+    bool w_ready = false;   // resident weights landed (env-issued MMAs)
+    // A operand of layer l of member m written by this thread: hand it to the tensor core
+    auto kick = [&](int m, int l) {
+      sm100::fence_proxy_async_smem();
+      sm100::tc_fence_before();
+      if constexpr (kEnvIssue) {
+        sm100::named_bar_sync(bar_id, 128);
+        if (gtid == 0) {
+          if (!w_ready) {
+            sm100::mbar_wait(&w_full[0], 0);
+            w_ready = true;
+          }
+          sm100::tc_fence_after();
+          const uint32_t a_sbo = (uint32_t)(Plan::kdim(l) / 8) * 128u;
+          const uint32_t idesc = sm100::make_idesc_bf16(kTileM, Plan::nrows(l));
+          const uint32_t a_base = sm100::smem_u32(sA) + (uint32_t)(tile * S::kA);
+          const uint32_t d_tmem = tmem + (uint32_t)(tile * Plan::kHid);
+          for (int s = Plan::first_stage(l); s < Plan::first_stage(l) + Plan::nstages(l); ++s) {
+            const uint32_t b_base = sm100::smem_u32(sW) + (uint32_t)(m * Plan::kMemberBytes + Plan::offset_of(s));
+            const int j0 = Plan::j0_of(s), nks = Plan::nks_of(s);
+            const uint32_t b_sbo = (uint32_t)(nks * 2) * 128u;
+            const uint64_t ad0 = sm100::make_sdesc(a_base + (uint32_t)j0 * 256u, 128u, a_sbo);
+            const uint64_t bd0 = sm100::make_sdesc(b_base, 128u, b_sbo);
+            for (int j = 0; j < nks; ++j)
+              sm100::mma_bf16(d_tmem, ad0 + (uint64_t)(16 * j), bd0 + (uint64_t)(16 * j), idesc,
+                              (j0 + j) > 0 ? 1u : 0u);
+          }
+          sm100::mma_commit(&d_full[tile]);
+        }
+      } else {
+        sm100::mbar_arrive(a_full);
+      }
+    };
     for (int t = 0; t < T; ++t) {
       FIN_TR(row == 0 && tile == 0, t, 0);
       Ops::stage(st, p, env, gtid, t, stg, bar_id);
       for (int m = 0; m < M; ++m) {
         Ops::build_obs(st, p, env, row, t, m, xa, stg);
-        sm100::fence_proxy_async_smem();
-        sm100::tc_fence_before();
-        sm100::mbar_arrive(a_full);
+        kick(m, 0);
         FIN_TR(row == 0 && tile == 0 && m == 0, t, 1);
         const float* bias = sBias + m * Plan::kBiasFloats;
         // hidden layers: D -> +bias -> ReLU -> bf16 -> A (K-major core matrices)
 #pragma unroll 1
         for (int l = 0; l < 2; ++l) {
-          sm100::mbar_wait(d_full, d_use & 1);
+          sm100::mbar_wait(&d_full[tile], d_use & 1);
           ++d_use;
           FIN_TR(row == 0 && tile == 0 && m == 0, t, 2 + 2 * l);
           sm100::tc_fence_after();
@@ -344,13 +382,11 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
           else if (bl) epilogue(T1{}, F0{});
           else if (add) epilogue(F0{}, T1{});
           else epilogue(F0{}, F0{});
-          sm100::fence_proxy_async_smem();
-          sm100::tc_fence_before();
-          sm100::mbar_arrive(a_full);
+          kick(m, l + 1);
           FIN_TR(row == 0 && tile == 0 && m == 0, t, 3 + 2 * l);
         }
         // output layer
-        sm100::mbar_wait(d_full, d_use & 1);
+        sm100::mbar_wait(&d_full[tile], d_use & 1);
         ++d_use;
         FIN_TR(row == 0 && tile == 0 && m == 0, t, 6);
         sm100::tc_fence_after();
