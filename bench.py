@@ -337,7 +337,42 @@ def extras(fin, torch, pol):
     out["configs1_2048envs_T30"] = 2048 * 30 / (statistics.mean(times) / 1e3)
     del env
     out.update(hbm_kernels(fin, torch))
+    out["crypto_c3"] = crypto_c3(fin, torch)
     return out
+
+
+def crypto_c3(fin, torch):
+    """BASELINE configs[3] at full length: 4096 envs x 480,000 one-second steps (one
+    episode), Q-net 103-128-128-3, epsilon-greedy 0.005 (Philox), in 10 calls of 48,000
+    steps; latency-bound (all envs advance in lockstep)."""
+    from synth import market
+    from synth import policy as spol
+    N, T, calls = 4096, 480000, 10
+    rows = market.crypto_market(T, seed=41)
+    cfg = fin.env_config(task=fin.FIN_CRYPTO, num_envs=N, num_assets=1, num_indicators=0, num_rows=T + 1,
+                         episode_len=T, reward_scale=1.0, cost_rate=0.0, epsilon=0.005, seed=43)
+    pol = fin.fin_policy_create(fin.FIN_Q_ARGMAX, spol.kaiming_bf16(spol.CRYPTO_DIMS, 4))
+    Tc = T // calls
+    z = lambda s, d: torch.zeros(s, dtype=d, device="cuda")  # noqa: E731
+    rew, done, agg = z((Tc, N), torch.float32), z((Tc, N), torch.uint8), z(8, torch.float64)
+    tr = fin.make_traj(reward=rew, done=done, agg=agg)
+    nz = fin.make_noise(fin.FIN_NOISE_PHILOX, 43)
+    warm = fin.fin_env_create(cfg, rows)
+    for _ in range(3):
+        fin.fin_rollout(warm, [pol], 1000, nz, fin.make_traj(reward=rew[:1000], done=done[:1000]))
+    del warm
+    env = fin.fin_env_create(cfg, rows)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(calls):
+        fin.fin_rollout(env, [pol], Tc, nz, tr)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    return {"envs": N, "steps": T, "ms": ms, "env_steps_per_s": N * T / (ms / 1e3),
+            "us_per_lockstep_step": 1e3 * ms / T, "episodes": int(done.sum().item()),
+            "note": "one 480,000-step episode per env (reading R27), latency-bound: 32 tiles of 128 envs"}
 
 
 def hbm_kernels(fin, torch):

@@ -346,6 +346,8 @@ int fin_env_create(const fin_env_config* cfg, const float* market, int64_t marke
         row[kRowRU * d.kp + k] = 1.0 / uk;
         row[kRowPN * d.kp + k] = pn;
         row[kRowMPN * d.kp + k] = pn * m52;
+        double& umin = row[kRowMeta * d.kp];
+        umin = (k == 0 || uk < umin) ? uk : umin;
       }
   }
   const size_t pxbytes = px.size() * sizeof(double);

@@ -150,7 +150,11 @@ __device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)
     save[o] = make_uint4(w[0], w[1], w[2], w[3]);
   }
   bool miss = false;
+  // once the cash of every env of the warp is below min_k u_k, no later asset can be
+  // bought (fl(n u) > b for every n >= 1): the rest of the loop is skipped.  Exact.
+  const double umin = R[kRowMeta * RS];
   FIN_CHUNKED(KA, b, {
+    if (k == c_ && c_ > 0 && __all_sync(__activemask(), !(b >= umin))) goto buys_done;
     const int want = max(min(a[k], FIN_HOLD_MAX - h[k]), 0);
     // floor(b / u) estimate; its low word is used even when x >= 2^32 or b is NaN:
     // the checks below accept n only if it satisfies the definition itself
@@ -162,6 +166,7 @@ __device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)
     b = fsub64(b, cn);
     h[k] += n;
   })
+buys_done:
   if (miss) {   // rare: arrays in local memory only on this path
     int hh[KA], aa[KA];
     const uint32_t* sw = reinterpret_cast<const uint32_t*>(save);

@@ -78,7 +78,8 @@ __device__ __forceinline__ double fdiv64(double a, double b) { return __ddiv_rn(
 //   MP = -2^52 p_d,  MU = -2^52 u_d   (exact scalings)
 //   RU = fl(1 / u_d)                  (estimate of the affordable count only)
 //   PN = p_d+1, MPN = -2^52 p_d+1     (marking day; 0 on the last row)
-enum { kRowP = 0, kRowU, kRowMP, kRowMU, kRowRU, kRowPN, kRowMPN, kPriceRows };
+//   META[0] = min_k u_k               (cash below it buys nothing more this step)
+enum { kRowP = 0, kRowU, kRowMP, kRowMU, kRowRU, kRowPN, kRowMPN, kRowMeta, kPriceRows };
 
 // Exact int -> double for 0 <= n < 2^31 on the fp64 pipe: the bit pattern
 // 0x43300000:n is 2^52 + n exactly and subtracting 2^52 is exact.  Replaces the
