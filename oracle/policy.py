@@ -77,3 +77,58 @@ def epsilon_greedy(q, eps: float, u_explore: float, u_action: float) -> int:
     if u_explore < eps:
         return min(int(u_action * n), n - 1)
     return argmax_lowest(q)
+
+
+# ------------------------------------------------------------------ SURVEY §8(f) NEXT-1 / NEXT-2
+# Stock ensemble weights (§5.2.1): members are validated on a 5-day
+# window, "agents with very low Sharpe ratios are discarded", the rest weighted by "a
+# softmax function applied to their Sharpe ratios" (Eq. 6 P:305-307 for the ratio).
+# Readings (DESIGN.md R-GATE, after SPEC S:496): discard Sharpe < threshold (default
+# 0.0; a NaN Sharpe is discarded); softmax at temperature tau over the retained ones;
+# if all are discarded, the best finite Sharpe keeps weight 1 (member 0 if none is
+# finite).
+def softmax_weights(sharpes, threshold: float = 0.0, temperature: float = 1.0):
+    keep = [s == s and s >= threshold for s in sharpes]
+    if not any(keep):
+        finite = [i for i, s in enumerate(sharpes) if s == s]
+        best = max(finite, key=lambda i: (sharpes[i], -i)) if finite else 0
+        return [1.0 if i == best else 0.0 for i in range(len(sharpes))]
+    top = max(s for s, k in zip(sharpes, keep) if k)
+    e = [math.exp((s - top) / temperature) if k else 0.0 for s, k in zip(sharpes, keep)]
+    tot = 0.0
+    for x in e:
+        tot = tot + x
+    return [x / tot for x in e]
+
+
+# Crypto ensemble (§5.2.2): "the majority action is selected as the
+# final ensemble action".  Plurality over the members' actions; ties go to the action
+# closest to 0 (hold), then to the lowest index (reading R-VOTE).
+def majority_vote(actions, values=(-1, 0, 1)) -> int:
+    counts = {v: 0 for v in values}
+    for a in actions:
+        counts[a] += 1
+    top = max(counts.values())
+    tied = [v for v in values if counts[v] == top]
+    return min(tied, key=lambda v: (abs(v), values.index(v)))
+
+
+# Dueling DQN head (Wang et al. 2016, the paper's third crypto member): Q_j = V + A_j -
+# mean_j A_j.  Its greedy action is argmax_j A_j (V and the mean do not depend on j).
+def dueling_q(a_head, v: float):
+    m = 0.0
+    for x in a_head:
+        m = m + x
+    m = m / len(a_head)
+    return [v + (x - m) for x in a_head]
+
+
+# Condorcet's jury theorem, Eq. 1: P(majority of n independent
+# voters, each right with probability p, is right) = sum_{k > n/2} C(n,k) p^k (1-p)^(n-k).
+def condorcet_probability(n: int, p: float) -> float:
+    if n < 1 or n % 2 == 0:
+        raise ValueError("n must be a positive odd integer")
+    tot = 0.0
+    for k in range(n // 2 + 1, n + 1):
+        tot = tot + math.comb(n, k) * p ** k * (1.0 - p) ** (n - k)
+    return tot
