@@ -70,8 +70,15 @@ enum {
 
 enum { FIN_STOCK = 0, FIN_CRYPTO = 1 };
 
-/* policy member kinds: C1 / C2 members (BASELINE configs[1,2]) and the C3 Q-net */
-enum { FIN_PPO_GAUSS = 0, FIN_SAC_SQUASH = 1, FIN_DDPG_OU = 2, FIN_Q_ARGMAX = 3 };
+/* policy member kinds: C1 / C2 members (BASELINE configs[1,2]) and the C3 Q-nets.
+ * FIN_Q_ARGMAX: DQN or Double DQN (identical at inference: greedy on Q), net
+ * 103-128-128-3; FIN_Q_DUELING: Dueling DQN, net 103-128-128-4 whose outputs
+ * are the advantage head A_0..A_2 then V (Q = V + A - mean A; its greedy action is the
+ * argmax of A). */
+enum { FIN_PPO_GAUSS = 0, FIN_SAC_SQUASH = 1, FIN_DDPG_OU = 2, FIN_Q_ARGMAX = 3, FIN_Q_DUELING = 4 };
+
+/* most ensemble members in one call (PAPER.md P:445 Ensemble-3: 30) */
+#define FIN_MAX_MEMBERS_API 32
 
 /* noise modes for fin_rollout / fin_ensemble_act */
 enum { FIN_NOISE_PHILOX = 0, FIN_NOISE_SUPPLIED = 1, FIN_NOISE_NONE = 2 };
@@ -214,10 +221,15 @@ typedef struct {
 
 /* Fused rollout of T steps (the producer of P:139-146 / P:241-278): per step the
  * members' MLPs on the current observation (tcgen05 tensor cores), sampling /
- * ensemble averaging (uniform mean, or member_w (host, M floats) weighted), trade
- * execution, reward, done / auto-reset, online episode metrics.  members (host
- * array) has n_members in [1, 4] policies of identical shape; stock: kinds
- * PPO/SAC/DDPG; crypto: exactly one FIN_Q_ARGMAX.  No host round-trip inside. */
+ * ensemble combination, trade execution, reward, done / auto-reset, online episode
+ * metrics.  members (host array) has n_members in [1, 32] policies of identical
+ * shape.  Stock: kinds PPO/SAC/DDPG, executed action = uniform mean of
+ * the members' continuous actions, or the member_w (host, M floats) weighted sum
+ * (the Sharpe-softmax weights of fin_member_weights); each DDPG member keeps its own
+ * OU state (slot i = the i-th DDPG member of the list).  Crypto: kinds
+ * Q_ARGMAX / Q_DUELING, executed action = plurality vote of the members' greedy
+ * actions (ties to hold, then the lowest index), then epsilon-greedy; member_w
+ * must be NULL.  mlp_out / mlp_hidden logs are [T][M][N][.].  No host round-trip. */
 int fin_rollout(fin_env* env, const fin_policy* const* members /*host*/, int32_t n_members,
                 const float* member_w /*host*/, int32_t T, const fin_noise* noise /*host*/,
                 const fin_traj* out /*host*/, void* stream);
@@ -254,6 +266,15 @@ int fin_mlp_forward(const fin_policy* policy, const uint16_t* x, int32_t B, floa
  * exactly as fin_rollout draws them (Philox4x32-10 + Box-Muller). */
 int fin_philox_normals(uint64_t seed, int64_t env_offset, int32_t N, int32_t K, int32_t member,
                        int64_t t_global, float* out, void* stream);
+
+/* Ensemble weights from validation statistics (Eq. 6; reading R-GATE):
+ * aggs f64 [M][FIN_AGG_LEN] = the aggregate vector of one validation fin_rollout per
+ * member (deterministic: FIN_NOISE_NONE), all-reduced over ranks.  Member Sharpe =
+ * aggs[m][FIN_AGG_SUM_SHARPE] / aggs[m][FIN_AGG_N_SHARPE] (NaN if that count is 0).  Members below ``threshold`` (or NaN) are discarded; the rest get
+ * softmax(Sharpe / temperature); if all are discarded the best finite Sharpe gets 1.
+ * Writes w f32 [M] (device) and, if non-NULL, sharpe f64 [M] (device). */
+int fin_member_weights(const double* aggs, int32_t M, double threshold, double temperature, float* w,
+                       double* sharpe, void* stream);
 
 /* Debug: record a clock64 timeline of block 0 of subsequent fin_rollout calls into
  * ``device_buffer`` (u64 [T][16]; NULL disables).  Not for production use. */

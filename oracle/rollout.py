@@ -32,22 +32,46 @@ def member_action(kind: int, z: float, eps: float, ou_x: float):
     raise ValueError(kind)
 
 
-def ensemble_shares(kinds, zs, eps, ou, max_trade: int = 100, weights=None):
-    """zs[m][K], eps[m][K], ou[K] (DDPG member state) -> (shares[K], abar[K], ou')."""
+def ensemble_shares_multi(kinds, zs, eps, ou_slots, max_trade: int = 100, weights=None):
+    """zs[m][K], eps[m][K], ou_slots[j][K] (state of the j-th DDPG member, in member
+    order) -> (shares[K], abar[K], ou_slots').  Executed action: the uniform mean of the
+    members' continuous actions (reading R20), or the weights' weighted sum (the
+    Sharpe-softmax weights of PAPER.md P:309, reading R-GATE)."""
     K = len(zs[0])
-    ou = list(ou)
+    ou_slots = [list(x) for x in ou_slots]
     out, abar = [], []
     for k in range(K):
         acts = []
+        j = 0
         for m, kind in enumerate(kinds):
-            a, x = member_action(kind, float(zs[m][k]), float(eps[m][k]), ou[k])
+            x_old = ou_slots[j][k] if kind == DDPG_OU else 0.0
+            a, x = member_action(kind, float(zs[m][k]), float(eps[m][k]), x_old)
             if kind == DDPG_OU:
-                ou[k] = x
+                ou_slots[j][k] = x
+                j += 1
             acts.append(a)
         mean = policy.ensemble_mean(acts) if weights is None else policy.weighted_mean(acts, weights)
         abar.append(mean)
         out.append(policy.shares(mean, max_trade))
-    return out, abar, ou
+    return out, abar, ou_slots
+
+
+def ensemble_shares(kinds, zs, eps, ou, max_trade: int = 100, weights=None):
+    """zs[m][K], eps[m][K], ou[K] (the single DDPG member's state) -> (shares[K], abar[K], ou')."""
+    out, abar, slots = ensemble_shares_multi(kinds, zs, eps, [list(ou)], max_trade, weights)
+    return out, abar, slots[0]
+
+
+def crypto_vote_action(qs, epsilon: float = 0.0, u_explore: float = 1.0, u_action: float = 0.0) -> int:
+    """Crypto ensemble: each member's greedy action (argmax of its
+    first 3 outputs -- Q for DQN / Double DQN, the advantage head for Dueling DQN) is a
+    vote; the plurality winner (ties to hold, then the lowest index) is then subject to
+    epsilon-greedy exploration like a single agent.  Returns the action in {-1, 0, 1}."""
+    votes = [policy.argmax_lowest(list(q[:3])) - 1 for q in qs]
+    a = policy.majority_vote(votes)
+    if u_explore < epsilon:
+        return min(int(u_action * 3), 2) - 1
+    return a
 
 
 def stock_policy_rollout(cfg: stock.StockEnvConfig, market, members, kinds, noise, T: int,

@@ -37,6 +37,7 @@ struct fin_env {
   size_t agg_cap;  // rows of FIN_AGG_LEN
   float* z1s;      // factored layer 1: per-member shared term of every market day [M][rows][HID]
   size_t z1s_cap;  // floats
+  float* ou_mem;   // DDPG OU state [ou_slots][K][N] (grown on demand)
 };
 
 struct fin_policy {
@@ -45,7 +46,7 @@ struct fin_policy {
   int32_t dims[4];
   uint8_t* wpack;              // device, TcPlan layout (stock: layer 1 = private columns only)
   float* bias;                 // device, [HID + HID + OUT_PAD]
-  uint32_t bias_nz;            // bit l: layer l has a non-zero bias (an all-zero bias is skipped)
+  uint8_t bias_nz;             // bit l: layer l has a non-zero bias (an all-zero bias is skipped)
   float* w1s_t;                // stock: device [S][HID] shared columns of W1 (exact bf16 values), else null
 };
 
@@ -119,7 +120,7 @@ int ensure_agg(fin_env* env, size_t rows) {
 int net_of(const int32_t* dims) {
   if (dims[0] == 301 && dims[1] == 256 && dims[2] == 256 && dims[3] == 30) return 0;
   if (dims[0] == 25 && dims[1] == 128 && dims[2] == 128 && dims[3] == 4) return 1;
-  if (dims[0] == 103 && dims[1] == 128 && dims[2] == 128 && dims[3] == 3) return 2;
+  if (dims[0] == 103 && dims[1] == 128 && dims[2] == 128 && (dims[3] == 3 || dims[3] == 4)) return 2;
   return -1;
 }
 
@@ -292,7 +293,6 @@ int fin_env_create(const fin_env_config* cfg, const float* market, int64_t marke
   // one allocation for all state arrays (8-byte members first)
   const size_t n8 = N * 8;  // cash + 6 metric doubles
   size_t bytes = 8 * n8 * sizeof(double) / 8;   // 8 double arrays
-  bytes += (size_t)FIN_MAX_MEMBERS * K * N * sizeof(float);
   bytes += N * 4 * sizeof(int32_t);              // t_ep, window, tau, m_n
   const size_t KO = (K + 7) / 8;                 // holdings: asset octets (hold_at)
   bytes += KO * 8 * N * sizeof(int16_t);
@@ -314,7 +314,8 @@ int fin_env_create(const fin_env_config* cfg, const float* market, int64_t marke
   d.m_mdd = reinterpret_cast<double*>(take(N * 8));
   d.m_mean = reinterpret_cast<double*>(take(N * 8));
   d.m_m2 = reinterpret_cast<double*>(take(N * 8));
-  d.ou = reinterpret_cast<float*>(take((size_t)FIN_MAX_MEMBERS * K * N * 4));
+  d.ou = nullptr;      // DDPG OU slots: allocated by the first rollout with DDPG members
+  d.ou_slots = 0;
   d.t_ep = reinterpret_cast<int32_t*>(take(N * 4));
   d.window = reinterpret_cast<int32_t*>(take(N * 4));
   d.tau = reinterpret_cast<int32_t*>(take(N * 4));
@@ -442,6 +443,7 @@ void fin_env_destroy(fin_env* env) {
   cudaStreamSynchronize(env->last_stream);
   if (env->agg_scratch) cudaFree(env->agg_scratch);
   if (env->z1s) cudaFree(env->z1s);
+  if (env->ou_mem) cudaFree(env->ou_mem);
   if (env->market_mem) cudaFree(env->market_mem);
   if (env->state_mem) cudaFree(env->state_mem);
   delete env;
@@ -451,15 +453,19 @@ int fin_policy_create(int32_t kind, int32_t n_layers, const int32_t* dims, const
                       const float* const* bias, void* stream, fin_policy** out) {
   if (!dims || !w_bf16 || !out) return fail(FIN_E_CONFIG, "fin_policy_create: null argument");
   *out = nullptr;
-  if (kind < FIN_PPO_GAUSS || kind > FIN_Q_ARGMAX) return fail(FIN_E_CONFIG, "unknown policy kind %d", kind);
+  if (kind < FIN_PPO_GAUSS || kind > FIN_Q_DUELING) return fail(FIN_E_CONFIG, "unknown policy kind %d", kind);
   if (n_layers != 3) return fail(FIN_E_UNSUPPORTED, "only 3-layer networks are compiled (got %d)", n_layers);
   for (int l = 0; l < 3; ++l)
     if (!w_bf16[l]) return fail(FIN_E_CONFIG, "weight %d is null", l);
   const int net = net_of(dims);
   if (net < 0)
-    return fail(FIN_E_UNSUPPORTED, "network %d-%d-%d-%d not compiled (have 301-256-256-30, 25-128-128-4, 103-128-128-3)",
-                dims[0], dims[1], dims[2], dims[3]);
-  if ((net == 2) != (kind == FIN_Q_ARGMAX)) return fail(FIN_E_CONFIG, "Q_ARGMAX pairs with the 103-128-128-3 Q-net");
+    return fail(FIN_E_UNSUPPORTED,
+                "network %d-%d-%d-%d not compiled (have 301-256-256-30, 25-128-128-4, 103-128-128-3 / -4)", dims[0],
+                dims[1], dims[2], dims[3]);
+  const bool qkind = kind == FIN_Q_ARGMAX || kind == FIN_Q_DUELING;
+  if ((net == 2) != qkind) return fail(FIN_E_CONFIG, "Q kinds pair with the 103-128-128 Q-nets");
+  if (kind == FIN_Q_ARGMAX && dims[3] != 3) return fail(FIN_E_CONFIG, "Q_ARGMAX needs 3 outputs");
+  if (kind == FIN_Q_DUELING && dims[3] != 4) return fail(FIN_E_CONFIG, "Q_DUELING needs 4 outputs (A0..A2, V)");
   for (int l = 0; l < 3; ++l) {
     if (bias && bias[l] && !finite_all(bias[l], dims[l + 1])) return fail(FIN_E_DATA, "bias %d non-finite", l);
   }
@@ -510,8 +516,26 @@ void fin_policy_destroy(fin_policy* pol) {
 
 namespace {
 
-int fill_members(const fin_env* env, const fin_policy* const* members, int32_t n, const float* member_w,
-                 tc::TcParams& p, int* net_out) {
+// DDPG OU state: one [K][N] slot per DDPG member, grown on demand (existing slots kept)
+int ensure_ou_slots(fin_env* env, int n, cudaStream_t s) {
+  if (n <= env->d.ou_slots) return FIN_OK;
+  const size_t slot = (size_t)env->d.K * env->d.N * sizeof(float);
+  float* mem = nullptr;
+  FIN_CUDA(cudaMalloc(&mem, n * slot));
+  FIN_CUDA(cudaMemsetAsync(mem, 0, n * slot, s));
+  if (env->ou_mem) {
+    FIN_CUDA(cudaMemcpyAsync(mem, env->ou_mem, env->d.ou_slots * slot, cudaMemcpyDeviceToDevice, s));
+    FIN_CUDA(cudaStreamSynchronize(s));
+    cudaFree(env->ou_mem);
+  }
+  env->ou_mem = mem;
+  env->d.ou = mem;
+  env->d.ou_slots = n;
+  return FIN_OK;
+}
+
+int fill_members(fin_env* env, const fin_policy* const* members, int32_t n, const float* member_w,
+                 tc::TcParams& p, int* net_out, cudaStream_t s) {
   if (!members || n < 1 || n > FIN_MAX_MEMBERS) return fail(FIN_E_CONFIG, "n_members must be in [1, %d]", FIN_MAX_MEMBERS);
   int net = -1, n_ddpg = 0;
   for (int m = 0; m < n; ++m) {
@@ -520,12 +544,16 @@ int fill_members(const fin_env* env, const fin_policy* const* members, int32_t n
     net = members[m]->net;
     p.wpack[m] = members[m]->wpack;
     p.bias[m] = members[m]->bias;
-    p.bias_nz |= members[m]->bias_nz << (3 * m);
+    p.bias_nz[m] = members[m]->bias_nz;
     p.kinds[m] = members[m]->kind;
-    if (members[m]->kind == FIN_DDPG_OU) ++n_ddpg;
+    p.ou_slot[m] = members[m]->kind == FIN_DDPG_OU ? (int8_t)(n_ddpg++) : (int8_t)-1;
     p.mw[m] = member_w ? member_w[m] : 1.f;
   }
-  if (n_ddpg > 1) return fail(FIN_E_UNSUPPORTED, "at most one DDPG member (OU state slot) per rollout");
+  p.n_ddpg = n_ddpg;
+  if (n_ddpg > 0) {
+    const int rc = ensure_ou_slots(env, n_ddpg, s);
+    if (rc != FIN_OK) return rc;
+  }
   if (env->d.task == FIN_STOCK) {
     if (net == 2) return fail(FIN_E_CONFIG, "stock env needs a stock policy");
     const int need_k = net == 0 ? 30 : 4, need_i = net == 0 ? 8 : 4;
@@ -533,7 +561,8 @@ int fill_members(const fin_env* env, const fin_policy* const* members, int32_t n
       return fail(FIN_E_UNSUPPORTED, "policy network expects K=%d, I=%d; env has K=%d, I=%d", need_k, need_i,
                   env->d.K, env->d.I);
   } else {
-    if (net != 2 || n != 1) return fail(FIN_E_CONFIG, "crypto env takes exactly one Q_ARGMAX member");
+    if (net != 2) return fail(FIN_E_CONFIG, "crypto env takes Q_ARGMAX / Q_DUELING members");
+    if (member_w) return fail(FIN_E_CONFIG, "crypto ensembles vote: member_w must be NULL");
   }
   p.M = n;
   p.weighted = member_w ? 1 : 0;
@@ -589,7 +618,7 @@ int fin_rollout(fin_env* env, const fin_policy* const* members, int32_t n_member
   tc::TcParams p;
   std::memset(&p, 0, sizeof(p));
   int net = -1;
-  int rc = fill_members(env, members, n_members, member_w, p, &net);
+  int rc = fill_members(env, members, n_members, member_w, p, &net, S(stream));
   if (rc != FIN_OK) return rc;
   rc = fill_noise(noise, p);
   if (rc != FIN_OK) return rc;
@@ -650,7 +679,7 @@ int fin_ensemble_act(fin_env* env, const fin_policy* const* members, int32_t n_m
   tc::TcParams p;
   std::memset(&p, 0, sizeof(p));
   int net = -1;
-  int rc = fill_members(env, members, n_members, member_w, p, &net);
+  int rc = fill_members(env, members, n_members, member_w, p, &net, S(stream));
   if (rc != FIN_OK) return rc;
   rc = fill_noise(noise, p);
   if (rc != FIN_OK) return rc;
@@ -699,7 +728,7 @@ int fin_mlp_forward(const fin_policy* pol, const uint16_t* x, int32_t B, float* 
   p.wpack[0] = pol->wpack;
   p.bias[0] = pol->bias;
   p.kinds[0] = pol->kind;
-  p.bias_nz = pol->bias_nz;
+  p.bias_nz[0] = pol->bias_nz;
   p.M = 1;
   p.T = 1;
   p.x_in = x;
@@ -719,6 +748,17 @@ int fin_mlp_forward(const fin_policy* pol, const uint16_t* x, int32_t B, float* 
   if (e == cudaSuccess) e = fin::launch_mlp_probe(pol->net, p, B, s);
   if (z1s) cudaFreeAsync(z1s, s);
   if (e != cudaSuccess) return cuda_fail(e, "fin_mlp_forward launch");
+  return FIN_OK;
+}
+
+int fin_member_weights(const double* aggs, int32_t M, double threshold, double temperature, float* w,
+                       double* sharpe, void* stream) {
+  if (!aggs || !w) return fail(FIN_E_CONFIG, "fin_member_weights: null argument");
+  if (M < 1 || M > FIN_MAX_MEMBERS) return fail(FIN_E_CONFIG, "M must be in [1, %d]", FIN_MAX_MEMBERS);
+  if (!(temperature > 0.0) || !std::isfinite(temperature)) return fail(FIN_E_CONFIG, "temperature must be > 0");
+  if (std::isnan(threshold)) return fail(FIN_E_CONFIG, "threshold is NaN");
+  cudaError_t e = fin::launch_member_weights(aggs, M, threshold, temperature, w, sharpe, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_member_weights launch");
   return FIN_OK;
 }
 

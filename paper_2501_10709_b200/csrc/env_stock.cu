@@ -46,7 +46,7 @@ __global__ void k_stock_reset(EnvDev e, const uint8_t* __restrict__ mask) {
   for (int o = 0; o < (e.K + 7) / 8; ++o) q[(size_t)o * e.N + i] = make_uint4(0u, 0u, 0u, 0u);
   e.t_ep[i] = 0;
   e.window[i] = window_of(e, e.env_offset + i);
-  for (int m = 0; m < FIN_MAX_MEMBERS; ++m)
+  for (int m = 0; m < e.ou_slots; ++m)
     for (int k = 0; k < e.K; ++k) e.ou[((size_t)m * e.K + k) * e.N + i] = 0.f;
   MetricAcc a;
   metric_start(a, e.cash0);

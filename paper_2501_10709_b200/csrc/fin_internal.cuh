@@ -9,7 +9,8 @@
 
 #define FIN_HOLD_MAX 32767   // holdings are int16 (reading R-HOLD)
 #define FIN_MAX_ASSETS 32
-#define FIN_MAX_MEMBERS 4
+#define FIN_MAX_MEMBERS 32   // ensemble members per rollout (Ensemble-3 = 30)
+#define FIN_STAGE_MEMBERS 4  // members whose bias / z1s rows live in shared memory (the rest: L2)
 
 // Flat, by-value kernel parameter block describing one env handle on the device.
 // Internal state is SoA: element [k][i] of a [K][N] array is at k*N + i.
@@ -36,7 +37,8 @@ struct EnvDev {
   int32_t* t_ep;         // [N]
   int32_t* window;       // [N]
   int32_t* tau;          // [N] crypto holding time
-  float* ou;             // [FIN_MAX_MEMBERS][K][N] DDPG OU noise state
+  float* ou;             // [ou_slots][K][N] DDPG OU noise state (slot i: the i-th DDPG member of a call)
+  int32_t ou_slots;      // allocated slots (grown on demand by fin_rollout)
   // online episode-metric state (persisted across calls)
   double* m_v0;          // equity at episode start
   double* m_vprev;       // last equity
@@ -320,6 +322,8 @@ cudaError_t launch_agg_finalize(const double* partial, int n_blocks, double* agg
 cudaError_t launch_episode_metrics(const double* equity, const uint8_t* done, int T, int N, double reset_eq,
                                    double ppy, double rf, double* ep, int cap, int32_t* cnt,
                                    double* partial, int* n_blocks, cudaStream_t s);
+cudaError_t launch_member_weights(const double* stats, int M, double thr, double tau, float* w, double* sharpe,
+                                  cudaStream_t s);
 cudaError_t launch_philox_normals(uint64_t seed, int64_t off, int N, int K, int member, int64_t t,
                                   float* out, cudaStream_t s);
 }  // namespace fin

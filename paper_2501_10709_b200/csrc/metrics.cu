@@ -185,9 +185,47 @@ __global__ void k_philox_normals(uint64_t seed, int64_t off, int N, int K, int m
   }
 }
 
+// Ensemble member weights from validation statistics (reading
+// R-GATE): Sharpe_m = sum_m / count_m; discard Sharpe < threshold or NaN; softmax at
+// temperature tau over the rest (shifted by the largest kept Sharpe); none kept -> the
+// best finite Sharpe (lowest index on ties; member 0 if none is finite) gets 1.
+__global__ void k_member_weights(const double* __restrict__ stats, int M, double thr, double tau, float* w,
+                                 double* sharpe) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double sh[FIN_MAX_MEMBERS];
+  bool keep[FIN_MAX_MEMBERS];
+  bool any = false;
+  double top = -__longlong_as_double(0x7ff0000000000000ULL);
+  int best = -1;
+  for (int m = 0; m < M; ++m) {
+    const double c = stats[m * FIN_AGG_LEN + FIN_AGG_N_SHARPE];
+    sh[m] = c > 0.0 ? stats[m * FIN_AGG_LEN + FIN_AGG_SUM_SHARPE] / c : __longlong_as_double(0x7ff8000000000000ULL);
+    if (sharpe) sharpe[m] = sh[m];
+    keep[m] = sh[m] == sh[m] && sh[m] >= thr;
+    if (keep[m]) { any = true; top = fmax(top, sh[m]); }
+    if (sh[m] == sh[m] && (best < 0 || sh[m] > sh[best])) best = m;
+  }
+  if (!any) {
+    for (int m = 0; m < M; ++m) w[m] = m == (best < 0 ? 0 : best) ? 1.f : 0.f;
+    return;
+  }
+  double ex[FIN_MAX_MEMBERS], tot = 0.0;
+  for (int m = 0; m < M; ++m) {
+    ex[m] = keep[m] ? exp((sh[m] - top) / tau) : 0.0;
+    tot += ex[m];
+  }
+  for (int m = 0; m < M; ++m) w[m] = (float)(ex[m] / tot);
+}
+
 }  // namespace
 
 namespace fin {
+
+cudaError_t launch_member_weights(const double* stats, int M, double thr, double tau, float* w, double* sharpe,
+                                  cudaStream_t s) {
+  k_member_weights<<<1, 32, 0, s>>>(stats, M, thr, tau, w, sharpe);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_episode_metrics(const double* equity, const uint8_t* done, int T, int N, double reset_eq,
                                    double ppy, double rf, double* ep, int cap, int32_t* cnt, double* partial,

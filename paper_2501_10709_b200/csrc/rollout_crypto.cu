@@ -4,7 +4,11 @@
 // argmax (lowest index on ties) with epsilon-greedy exploration ->
 // a in {-1, 0, 1} -> LOB-walk execution, reward, done / reset (env_crypto.cuh) ->
 // online episode metrics.  All envs of the C3 workload read the same row t
-// (lockstep, reading R27): once per step a tile stages the bf16 factor part of the
+// (lockstep, reading R27).  With several members (DQN / Double DQN / Dueling DQN,
+// PAPER.md §5.2.2) each member's greedy action is one vote and the
+// executed action is the plurality winner, ties to hold, then to the lowest index
+// (reading R-VOTE); a dueling member's greedy action is the argmax of its advantage
+// head (outputs 0..2; Q = V + A - mean A has the same argmax).  Once per step a tile stages the bf16 factor part of the
 // observation and the two book rows in shared memory; a tile whose envs sit on
 // different rows takes the per-env path.  The market rows live in a 3-slot ring
 // (row k in slot k mod 3): during step t the tile cp.asyncs row t+2, so the C3 loop
@@ -55,6 +59,7 @@ struct CryptoOps {
     double b;
     int h, tau, t_ep;
     int act;
+    int votes[3];
     MetricAcc m;
     AggAcc agg;
     int cnt;
@@ -184,20 +189,27 @@ struct CryptoOps {
   __device__ __forceinline__ static uint16_t* hidden_ptr(State& st, const TcParams& p, int env, int t, int m, int l,
                                                          int hid) {
     if (!st.live || !p.o.mlp_hidden) return nullptr;
-    return p.o.mlp_hidden + (((size_t)t * p.e.N + env) * 2 + l) * hid;
+    return p.o.mlp_hidden + ((((size_t)t * p.M + m) * p.e.N + env) * 2 + l) * hid;
   }
 
   __device__ __forceinline__ static void consume(State& st, const TcParams& p, int env, int t, int m, const float* z) {
     if (!st.live) return;
     const EnvDev& e = p.e;
     if (p.o.mlp_out) {
-      float* dst = p.o.mlp_out + ((size_t)t * e.N + env) * 3;
+      float* dst = p.o.mlp_out + (((size_t)t * p.M + m) * e.N + env) * 3;
       dst[0] = z[0]; dst[1] = z[1]; dst[2] = z[2];
     }
     int best = 0;
     if (z[1] > z[best]) best = 1;
     if (z[2] > z[best]) best = 2;
     if (!(isfinite(z[0]) && isfinite(z[1]) && isfinite(z[2]))) { st.nonfinite = true; best = 1; }
+    if (m == 0) st.votes[0] = st.votes[1] = st.votes[2] = 0;
+    st.votes[best] += 1;
+    if (m + 1 < p.M) return;
+    // plurality; ties to hold (index 1), then to the lowest index
+    best = 1;
+    if (st.votes[0] > st.votes[best]) best = 0;
+    if (st.votes[2] > st.votes[best]) best = 2;
     float u0 = 1.f, u1 = 0.f;
     if (p.noise_mode == FIN_NOISE_SUPPLIED) {
       const float* nz = p.noise + ((size_t)t * e.N + env) * 2;
@@ -285,12 +297,18 @@ int num_sms();
 // SMs first (one tile per CTA); pair tiles per CTA only when tiles outnumber SMs.
 cudaError_t launch_crypto_rollout(const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s) {
   const int n_tiles = (n_envs + tc::kTileM - 1) / tc::kTileM;
-  if (n_tiles > num_sms()) {
-    *tiles = 2;
-    return tc::launch<PlanCrypto, true, 2, CryptoOps>(p, n_envs, s);
+  const bool two = n_tiles > num_sms();
+  *tiles = two ? 2 : 1;
+  // the Q-nets stay resident in shared memory while they fit (60 KB each); a larger
+  // voting ensemble (9 or 30 members) streams them like the stock nets
+  if (two) {
+    if (p.M <= tc::Smem<PlanCrypto, true, 2, CryptoOps>::max_members())
+      return tc::launch<PlanCrypto, true, 2, CryptoOps>(p, n_envs, s);
+    return tc::launch<PlanCrypto, false, 2, CryptoOps>(p, n_envs, s);
   }
-  *tiles = 1;
-  return tc::launch<PlanCrypto, true, 1, CryptoOps>(p, n_envs, s);
+  if (p.M <= tc::Smem<PlanCrypto, true, 1, CryptoOps>::max_members())
+    return tc::launch<PlanCrypto, true, 1, CryptoOps>(p, n_envs, s);
+  return tc::launch<PlanCrypto, false, 1, CryptoOps>(p, n_envs, s);
 }
 
 }  // namespace fin

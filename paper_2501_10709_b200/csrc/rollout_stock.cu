@@ -61,7 +61,7 @@ struct StockOps {
   // its window after a reset -- envs of a tile step in lockstep).
   static constexpr int kOffP = 0;
   static constexpr int kOffZ = kPriceRows * KP4 * 8;
-  static constexpr int kRegion = kOffZ + FIN_MAX_MEMBERS * Plan::kHid * 4;
+  static constexpr int kRegion = kOffZ + FIN_STAGE_MEMBERS * Plan::kHid * 4;
   static constexpr int kOffS = 2 * kRegion;
   static constexpr int kOffB = kOffS + 16;
   static constexpr int kStageBytes = kOffB + 16;
@@ -108,11 +108,10 @@ struct StockOps {
       st.w = e.window[env];
       st.m.v0 = e.m_v0[env]; st.m.vprev = e.m_vprev[env]; st.m.peak = e.m_peak[env]; st.m.mdd = e.m_mdd[env];
       st.m.mean = e.m_mean[env]; st.m.m2 = e.m_m2[env]; st.m.n = e.m_n[env];
-      int slot = -1;  // OU state of the (single) DDPG member
-      for (int m = 0; m < p.M; ++m)
-        if (p.kinds[m] == FIN_DDPG_OU) slot = m;
+      // OU state of a single DDPG member lives in registers (slot 0); with several DDPG
+      // members every slot is read and written in global memory (L2) at its use
 #pragma unroll
-      for (int k = 0; k < KOU; ++k) st.ou[k] = (ENS && slot >= 0) ? e.ou[((size_t)slot * e.K + k) * e.N + env] : 0.f;
+      for (int k = 0; k < KOU; ++k) st.ou[k] = (ENS && p.n_ddpg == 1) ? e.ou[(size_t)k * e.N + env] : 0.f;
     } else {
       st.b = 0.0;
 #pragma unroll
@@ -129,7 +128,7 @@ struct StockOps {
     const EnvDev& e = p.e;
     stage_price_rows(e, reinterpret_cast<double*>(reg + kOffP), k, gtid, 128);
     float* zs = reinterpret_cast<float*>(reg + kOffZ);
-    for (int j = gtid; j < p.M * Plan::kHid; j += 128) {
+    for (int j = gtid; j < min(p.M, FIN_STAGE_MEMBERS) * Plan::kHid; j += 128) {
       const int m = j / Plan::kHid, n = j % Plan::kHid;
       zs[j] = __ldg(p.z1s + ((size_t)m * p.z1s_rows + k) * Plan::kHid + n);
     }
@@ -141,7 +140,7 @@ struct StockOps {
     const uint8_t* src = reinterpret_cast<const uint8_t*>(e.px + (size_t)k * kPriceRows * e.kp);
     for (int j = gtid; j < np; j += 128) sm100::cp_async16(reg + kOffP + 16 * j, src + 16 * j);
     constexpr int nz = Plan::kHid / 4;                   // chunks per member z1s row
-    for (int j = gtid; j < p.M * nz; j += 128) {
+    for (int j = gtid; j < min(p.M, FIN_STAGE_MEMBERS) * nz; j += 128) {
       const int m = j / nz, c = j % nz;
       sm100::cp_async16(reg + kOffZ + (m * Plan::kHid + 4 * c) * 4,
                         p.z1s + ((size_t)m * p.z1s_rows + k) * Plan::kHid + 4 * c);
@@ -207,7 +206,7 @@ struct StockOps {
 
   // factored layer 1: the shared-input term of this env's day, member m
   __device__ __forceinline__ static const float* l1_addend(State& st, const TcParams& p, int m, uint8_t* stg) {
-    if (st.zsm) return reinterpret_cast<const float*>(region(stg, st.sb) + kOffZ) + m * Plan::kHid;
+    if (st.zsm && m < FIN_STAGE_MEMBERS) return reinterpret_cast<const float*>(region(stg, st.sb) + kOffZ) + m * Plan::kHid;
     return p.z1s + ((size_t)m * p.z1s_rows + st.d) * Plan::kHid;
   }
 
@@ -289,9 +288,11 @@ struct StockOps {
         float post = se;
         if (ENS && ddpg) {
           const int ko = ENS ? k : 0;
-          post = __fadd_rn(__fadd_rn(st.ou[ko], __fmul_rn(e.ou_theta, __fsub_rn(0.f, st.ou[ko]))),
-                           __fmul_rn(e.ou_sigma, eps[j]));
-          st.ou[ko] = post;
+          float* gx = e.ou + ((size_t)p.ou_slot[m] * e.K + k) * e.N + env;
+          const float x = p.n_ddpg == 1 ? st.ou[ko] : *gx;
+          post = __fadd_rn(__fadd_rn(x, __fmul_rn(e.ou_theta, __fsub_rn(0.f, x))), __fmul_rn(e.ou_sigma, eps[j]));
+          if (p.n_ddpg == 1) st.ou[ko] = post;
+          else *gx = post;
         }
         const float th = tanh_f32(pre);
         float a = sac ? th : fminf(fmaxf(__fadd_rn(th, post), -1.f), 1.f);
@@ -372,6 +373,9 @@ struct StockOps {
               for (int k = 0; k < KA; ++k) st.h[k] = 0;
 #pragma unroll
               for (int k = 0; k < KOU; ++k) st.ou[k] = 0.f;
+              if (ENS && p.n_ddpg > 1)
+                for (int q = 0; q < p.n_ddpg; ++q)
+                  for (int k = 0; k < KA; ++k) e.ou[((size_t)q * e.K + k) * e.N + env] = 0.f;
               st.t_ep = 0;
               st.vc = e.cash0;
               if (e.wadv) st.w = (st.w + 1) % e.W;
@@ -393,12 +397,9 @@ struct StockOps {
       e.window[env] = st.w;
       e.m_v0[env] = st.m.v0; e.m_vprev[env] = st.m.vprev; e.m_peak[env] = st.m.peak; e.m_mdd[env] = st.m.mdd;
       e.m_mean[env] = st.m.mean; e.m_m2[env] = st.m.m2; e.m_n[env] = st.m.n;
-      int slot = -1;
-      for (int m = 0; m < p.M; ++m)
-        if (p.kinds[m] == FIN_DDPG_OU) slot = m;
-      if (ENS && slot >= 0) {
+      if (ENS && p.n_ddpg == 1) {
 #pragma unroll
-        for (int k = 0; k < KOU; ++k) e.ou[((size_t)slot * e.K + k) * e.N + env] = st.ou[k];
+        for (int k = 0; k < KOU; ++k) e.ou[(size_t)k * e.N + env] = st.ou[k];
       }
       if (p.o.ep_count) p.o.ep_count[env] = st.cnt;
       if (st.oor) set_flag(e, FIN_FLAG_ACTION_RANGE);

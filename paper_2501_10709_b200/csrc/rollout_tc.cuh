@@ -43,9 +43,11 @@ struct TcParams {
   TrajDev o;
   const uint8_t* wpack[FIN_MAX_MEMBERS];  // packed member weights (TcPlan layout)
   const float* bias[FIN_MAX_MEMBERS];     // [HID + HID + OUT_PAD] fp32 per member
-  uint32_t bias_nz;                       // bit 3m + l: member m, layer l has a non-zero bias.  Adding
-                                          // an exactly-zero bias is the identity (up to the sign of a
+  uint8_t bias_nz[FIN_MAX_MEMBERS];       // bit l: member m, layer l has a non-zero bias.  Adding an
+                                          // exactly-zero bias is the identity (up to the sign of a
                                           // zero), so the epilogue skips those loads and adds
+  int8_t ou_slot[FIN_MAX_MEMBERS];        // DDPG members: OU state slot (else -1)
+  int32_t n_ddpg;                         // DDPG members in this call
   int32_t kinds[FIN_MAX_MEMBERS];
   float mw[FIN_MAX_MEMBERS];              // member weights (weighted mode)
   int32_t M;
@@ -100,9 +102,11 @@ struct Smem {
   __host__ __device__ static constexpr int w_bytes(int M) {
     return RESIDENT ? Plan::kMemberBytes * M : RING * Plan::kStageBytes;
   }
-  __host__ __device__ static constexpr int total(int M) { return kFixed + w_bytes(M) + M * kBiasPerMember; }
-  __host__ __device__ static constexpr int max_members() {
-    return (kSmemLimit - kStaticSmem - kFixed - w_bytes(0)) / ((RESIDENT ? Plan::kMemberBytes : 0) + kBiasPerMember);
+  __host__ __device__ static constexpr int staged(int M) { return M < FIN_STAGE_MEMBERS ? M : FIN_STAGE_MEMBERS; }
+  __host__ __device__ static constexpr int total(int M) { return kFixed + w_bytes(M) + staged(M) * kBiasPerMember; }
+  __host__ __device__ static constexpr int max_members() {   // resident plans: weights of M members in smem
+    return RESIDENT ? (kSmemLimit - kStaticSmem - kFixed - FIN_STAGE_MEMBERS * kBiasPerMember) / Plan::kMemberBytes
+                    : FIN_MAX_MEMBERS;
   }
 };
 
@@ -152,7 +156,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
   const int lane = threadIdx.x & 31;
 
   // ---- one-time setup
-  for (int j = threadIdx.x; j < M * Plan::kBiasFloats; j += blockDim.x) {
+  for (int j = threadIdx.x; j < min(M, FIN_STAGE_MEMBERS) * Plan::kBiasFloats; j += blockDim.x) {
     const int m = j / Plan::kBiasFloats, q = j % Plan::kBiasFloats;
     sBias[j] = p.bias[m] ? p.bias[m][q] : 0.f;
   }
@@ -315,7 +319,8 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
         Ops::build_obs(st, p, env, row, t, m, xa, stg);
         kick(m, 0);
         FIN_TR(row == 0 && tile == 0 && m == 0, t, 1);
-        const float* bias = sBias + m * Plan::kBiasFloats;
+        // biases of the first FIN_STAGE_MEMBERS members in shared memory, the rest from L2
+        const float* bias = m < FIN_STAGE_MEMBERS ? sBias + m * Plan::kBiasFloats : p.bias[m];
         // hidden layers: D -> +bias -> ReLU -> bf16 -> A (K-major core matrices)
 #pragma unroll 1
         for (int l = 0; l < 2; ++l) {
@@ -323,7 +328,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
           ++d_use;
           FIN_TR(row == 0 && tile == 0 && m == 0, t, 2 + 2 * l);
           sm100::tc_fence_after();
-          const float* bl = ((p.bias_nz >> (3 * m + l)) & 1u) ? bias + l * Plan::kHid : nullptr;
+          const float* bl = ((p.bias_nz[m] >> l) & 1u) ? bias + l * Plan::kHid : nullptr;
           // factored layer 1: + shared-input term of the env's day (smem or global row)
           const float* add = l == 0 ? Ops::l1_addend(st, p, m, stg) : nullptr;
           // debug / parity log of the bf16 hidden activations (teacher-forced layer checks)
@@ -396,7 +401,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
           uint32_t v[16];
           sm100::tmem_ld16(t_lane + (uint32_t)(c * 16), v);
           sm100::tmem_wait_ld();
-          if ((p.bias_nz >> (3 * m + 2)) & 1u) {
+          if ((p.bias_nz[m] >> 2) & 1u) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) z[c * 16 + j] = __uint_as_float(v[j]) + bias[2 * Plan::kHid + c * 16 + j];
           } else {

@@ -32,6 +32,21 @@ def allreduce_agg(agg, group=None):
     return agg
 
 
+def allreduce_aggs(aggs, group=None):
+    """In-place all-reduce of an [M][FIN_AGG_LEN] float64 tensor (one aggregate row per
+    ensemble member, e.g. the validation statistics of fin_member_weights)."""
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return aggs
+    sums = aggs[:, :FIN_AGG_NSUM].contiguous()
+    mins = aggs[:, FIN_AGG_NSUM:].contiguous()
+    dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(mins, op=dist.ReduceOp.MIN, group=group)
+    aggs[:, :FIN_AGG_NSUM] = sums
+    aggs[:, FIN_AGG_NSUM:] = mins
+    return aggs
+
+
 def max_over_ranks(value: float, device=None, group=None) -> float:
     """Max of a host float over all ranks (the timing rule: slowest rank)."""
     import torch

@@ -31,7 +31,8 @@ FIN_OK, FIN_E_CONFIG, FIN_E_DATA, FIN_E_NUMERIC, FIN_E_CUDA, FIN_E_EPISODE_DONE,
     FIN_E_DEVICE_ASYNC = range(8)
 FIN_FLAG_ACTION_RANGE, FIN_FLAG_EPISODE_DONE, FIN_FLAG_NONFINITE, FIN_FLAG_BAD_INDEX = 1, 2, 4, 8
 FIN_STOCK, FIN_CRYPTO = 0, 1
-FIN_PPO_GAUSS, FIN_SAC_SQUASH, FIN_DDPG_OU, FIN_Q_ARGMAX = 0, 1, 2, 3
+FIN_PPO_GAUSS, FIN_SAC_SQUASH, FIN_DDPG_OU, FIN_Q_ARGMAX, FIN_Q_DUELING = 0, 1, 2, 3, 4
+FIN_MAX_MEMBERS = 32
 FIN_NOISE_PHILOX, FIN_NOISE_SUPPLIED, FIN_NOISE_NONE = 0, 1, 2
 FIN_AGG_EPISODES, FIN_AGG_SUM_CUM, FIN_AGG_SUM_SHARPE, FIN_AGG_N_SHARPE, FIN_AGG_SUM_MDD, \
     FIN_AGG_SUM_REWARD = range(6)
@@ -44,7 +45,8 @@ FIN_AGG_LEN = 8
 EXPORTS = ("fin_env_create", "fin_env_reset", "fin_env_step", "fin_env_get_state", "fin_env_set_state",
            "fin_env_check", "fin_env_destroy", "fin_policy_create", "fin_policy_destroy", "fin_rollout",
            "fin_rollout_actions", "fin_ensemble_act", "fin_episode_metrics", "fin_mlp_forward",
-           "fin_philox_normals", "fin_last_error", "fin_abi_version", "fin_device_check", "fin_debug_trace")
+           "fin_philox_normals", "fin_member_weights", "fin_last_error", "fin_abi_version", "fin_device_check",
+           "fin_debug_trace")
 
 
 class FinError(RuntimeError):
@@ -95,6 +97,7 @@ _sig = {
                              _P, _P], C.c_int),
     "fin_mlp_forward": ([_P, _P, C.c_int32, _P, _P, _P], C.c_int),
     "fin_philox_normals": ([C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int64, _P, _P], C.c_int),
+    "fin_member_weights": ([_P, C.c_int32, C.c_double, C.c_double, _P, _P, _P], C.c_int),
     "fin_last_error": ([], C.c_char_p),
     "fin_abi_version": ([], C.c_int),
     "fin_device_check": ([C.c_int32], C.c_int),
@@ -362,3 +365,13 @@ def fin_philox_normals(seed: int, env_offset: int, out, member: int, t_global: i
     N, K = int(out.shape[0]), int(out.shape[1])
     _check(_lib.fin_philox_normals(seed, env_offset, N, K, member, t_global, _ptr(out, torch.float32, "out"),
                                    _stream(stream)), "fin_philox_normals")
+
+
+def fin_member_weights(aggs, w, sharpe=None, threshold: float = 0.0, temperature: float = 1.0,
+                       stream=None) -> None:
+    """aggs f64 [M][FIN_AGG_LEN] (device) -> w f32 [M] (device), sharpe f64 [M] (device, optional)."""
+    import torch
+    M = int(aggs.shape[0])
+    _check(_lib.fin_member_weights(_ptr(aggs, torch.float64, "aggs"), M, float(threshold), float(temperature),
+                                   _ptr(w, torch.float32, "w"), _ptr(sharpe, torch.float64, "sharpe"),
+                                   _stream(stream)), "fin_member_weights")
