@@ -131,7 +131,7 @@ def _oracle_shard(args):
     return time.perf_counter() - t0
 
 
-def oracle_rate(n_envs_per_core=2048, T=30, cores=None):
+def oracle_rate(n_envs_per_core=2560, T=30, cores=None):
     """Oracle env-steps/s on the host's cores (multiprocessing over env shards)."""
     import multiprocessing as mp
     for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
@@ -338,7 +338,72 @@ def extras(fin, torch, pol):
     del env
     out.update(hbm_kernels(fin, torch))
     out["crypto_c3"] = crypto_c3(fin, torch)
+    out["ensembles"] = ensembles(fin, torch)
     return out
+
+
+def ensembles(fin, torch):
+    """Ensemble rollouts (§5.2, §6.3-6.4): the C2 config (PPO + SAC + DDPG with OU,
+    5-day test windows advancing on reset, uniform mean), the Sharpe-softmax weighted
+    Ensemble-2 / -3 (5 / 10 members of each kind: 15 / 30 MLPs per env-step) at 16,384 envs,
+    T = 30; and the crypto DQN / Double DQN / Dueling DQN vote at 4,096 envs."""
+    from synth import market
+    from synth import policy as spol
+    res = {}
+    flush = L2Flush(torch)
+    z = lambda s, d: torch.zeros(s, dtype=d, device="cuda")  # noqa: E731
+    m = market.stock_c1(rows=ROWS)
+    kinds = [fin.FIN_PPO_GAUSS, fin.FIN_SAC_SQUASH, fin.FIN_DDPG_OU]
+    for name, per_kind, N, T in (("c2_3_members", 1, 65536, 30), ("ensemble2_15_members", 5, 16384, 30),
+                                 ("ensemble3_30_members", 10, 16384, 30)):
+        M = 3 * per_kind
+        cfg = fin.env_config(num_envs=N, num_assets=K_ASSETS, num_indicators=N_IND, num_rows=ROWS, episode_len=5,
+                             window_stride=5, window_offset=35, num_windows=194, window_block=128,
+                             advance_window_on_reset=1, seed=23)
+        env = fin.fin_env_create(cfg, m.market)
+        pols = [fin.fin_policy_create(kinds[j % 3], spol.kaiming_bf16(spol.STOCK_DIMS, 1 + j)) for j in range(M)]
+        w = None if per_kind == 1 else [1.0 / M] * M
+        tr = fin.make_traj(reward=z((T, N), torch.float32), done=z((T, N), torch.uint8), agg=z(8, torch.float64))
+        nz = fin.make_noise(fin.FIN_NOISE_PHILOX, 33)
+        for _ in range(2):
+            fin.fin_rollout(env, pols, T, nz, tr, member_w=w)
+        ts = []
+        for _ in range(3):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fin.fin_rollout(env, pols, T, nz, tr, member_w=w)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        ms = statistics.median(ts)
+        res[name] = {"members": M, "envs": N, "T": T, "ms": ms, "env_steps_per_s": N * T / (ms / 1e3),
+                     "mlp_evals_per_s": M * N * T / (ms / 1e3),
+                     "combine": "uniform mean" if w is None else "weighted (member_w)"}
+        del env, pols
+    rows = market.crypto_market(4800, seed=41)
+    N, T = 4096, 4800
+    cfg = fin.env_config(task=fin.FIN_CRYPTO, num_envs=N, num_assets=1, num_indicators=0, num_rows=T + 1,
+                         episode_len=T, reward_scale=1.0, cost_rate=0.0, epsilon=0.005, seed=43)
+    qk = [fin.FIN_Q_ARGMAX, fin.FIN_Q_ARGMAX, fin.FIN_Q_DUELING]
+    pols = []
+    for j in range(3):
+        dims = spol.CRYPTO_DIMS if qk[j] == fin.FIN_Q_ARGMAX else tuple(spol.CRYPTO_DIMS[:-1]) + (4,)
+        pols.append(fin.fin_policy_create(qk[j], spol.kaiming_bf16(dims, 4 + j)))
+    tr = fin.make_traj(reward=z((T, N), torch.float32), done=z((T, N), torch.uint8))
+    nz = fin.make_noise(fin.FIN_NOISE_PHILOX, 43)
+    fin.fin_rollout(fin.fin_env_create(cfg, rows), pols, 500, nz, fin.make_traj(reward=z((500, N), torch.float32)))
+    env = fin.fin_env_create(cfg, rows)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    fin.fin_rollout(env, pols, T, nz, tr)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    res["crypto_vote_3_members"] = {"members": 3, "envs": N, "T": T, "ms": ms, "env_steps_per_s": N * T / (ms / 1e3),
+                                    "us_per_lockstep_step": 1e3 * ms / T}
+    return res
 
 
 def crypto_c3(fin, torch):

@@ -98,3 +98,55 @@ def test_gloo_world2_matches_single_process():
     assert tmax == 2.0
     s = fdist.summarize_agg(agg)
     assert s["episodes"] == ref[0]
+
+
+def _ens_worker(rank, world, port, n_global, M, result_q):
+    """Ensemble validation exchange: each rank validates every
+    member on its env shard (here: member m = its own seeded action stream replayed by the
+    oracle), all-reduces the [M][8] aggregate rows, and derives the softmax weights."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import policy as opol
+    from oracle import stock as ostock
+    from synth import inputs, market
+    m = market.stock_c1(rows=90)
+    off, n = fdist.shard(n_global, rank, world)
+    cfg = ostock.StockEnvConfig(num_envs=n, num_assets=30, num_indicators=8, num_rows=90, episode_len=5,
+                                num_windows=16, window_block=4, env_offset=off)
+    aggs = torch.zeros((M, 8), dtype=torch.float64)
+    for j in range(M):
+        acts = inputs.stock_actions(10, n_global, 30, seed=20 + j)
+        aggs[j] = torch.tensor(_agg_of(cfg, m.market, acts[:, off:off + n]), dtype=torch.float64)
+    fdist.allreduce_aggs(aggs)
+    sharpes = [float(a[2] / a[3]) if a[3] > 0 else math.nan for a in aggs]
+    w = opol.softmax_weights(sharpes, -10.0, 0.5)
+    if rank == 0:
+        result_q.put((aggs.numpy().tolist(), w))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world2_ensemble_weights_match_single_process():
+    from oracle import policy as opol
+    from oracle import stock as ostock
+    from synth import inputs, market
+    n_global, M = 9, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ens_worker, args=(r, 2, port, n_global, M, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    aggs, w = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    m = market.stock_c1(rows=90)
+    cfg = ostock.StockEnvConfig(num_envs=n_global, num_assets=30, num_indicators=8, num_rows=90, episode_len=5,
+                                num_windows=16, window_block=4)
+    ref = [_agg_of(cfg, m.market, inputs.stock_actions(10, n_global, 30, seed=20 + j)) for j in range(M)]
+    np.testing.assert_allclose(aggs, ref, rtol=1e-12)
+    sharpes = [a[2] / a[3] for a in ref]
+    np.testing.assert_allclose(w, opol.softmax_weights(sharpes, -10.0, 0.5), rtol=1e-12)
+    assert abs(sum(w) - 1.0) < 1e-12
