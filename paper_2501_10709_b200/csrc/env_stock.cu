@@ -57,7 +57,7 @@ __global__ void k_stock_reset(EnvDev e, const uint8_t* __restrict__ mask) {
 // KA: compile-time asset count (EXACT: KA == K) or bound (K <= KA, padding zeros).
 template <int KA>
 struct StepSmem {
-  uint4 save[kStep][(KA + 7) / 8];          // per-thread post-sell holdings (exact buy redo)
+  uint4 save[(KA + 7) / 8][kStep];          // per-thread post-sell holdings (exact buy redo)
   alignas(16) double pr[2][kPriceRows * ((KA + 3) / 4 * 4)];   // price rows, [buffer]
   GroupSlots gs;
   uint64_t rows[2];
@@ -136,7 +136,7 @@ struct K1Buf {
 template <int KA>
 struct K1Smem {
   K1Buf<KA> buf[2];
-  uint4 save[kStep][(KA + 7) / 8];
+  uint4 save[(KA + 7) / 8][kStep];   // [octet][thread]: conflict-free 16-B stores
   alignas(16) double pr[2][kPriceRows * ((KA + 3) / 4 * 4)];
   uint64_t full[2];    // state + actions of the buffer's tile landed (TMA)
   uint64_t rows[2];    // price rows of the buffer's predicted day landed (TMA), or no prediction
@@ -283,8 +283,8 @@ __global__ void __launch_bounds__(kStep, FIN_K1_MINB)
     if (stepping && !bad) {
       const double* R = static_cast<const double*>(__builtin_assume_aligned(
           (d == sm.pred[sb]) ? sm.pr[sb] : e.px + (size_t)d * kPriceRows * e.kp, 16));
-      stock_trade<KA>(e, b, h, R, RS, a, sm.save[tid]);
-      const double vn = stock_mark<KA>(b, h, R + kRowPN * RS, R + kRowMPN * RS);
+      stock_trade<KA>(e, b, h, R, RS, a, &sm.save[0][tid], kStep);
+      const double vn = stock_mark<KA>(b, h, R + kRowPN * RS);
       double vnext = vn;
       t += 1;
       const bool done = (t == e.L);
@@ -398,8 +398,8 @@ __global__ void __launch_bounds__(kStep, FIN_K4_MINB) k_stock_replay(EnvDev e, c
         &sm.gs, round, d, stepping && !bad, tid, kBar, [&](int dd) { stage_price_rows(e, pr, dd, tid, kStep); },
         [&]() {
           const double v = vc;
-          stock_trade<KA>(e, b, h, pr, RS, a, sm.save[tid]);
-          const double vn = stock_mark<KA>(b, h, pr + kRowPN * RS, pr + kRowMPN * RS);
+          stock_trade<KA>(e, b, h, pr, RS, a, &sm.save[0][tid], kStep);
+          const double vn = stock_mark<KA>(b, h, pr + kRowPN * RS);
           vc = vn;
           t += 1;
           const bool done = (t == e.L);

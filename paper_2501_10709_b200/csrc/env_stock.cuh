@@ -46,12 +46,18 @@ __device__ __forceinline__ int zdep(int x) { return x >> 31; }
 __device__ __forceinline__ double nprod(int n, double x, double mx) {
   return __fma_rn(__hiloint2double(0x43300000, n), x, mx);
 }
+// the same with -2^52 x formed by an exact multiply instead of a staged row: one fp64
+// op instead of one shared-memory row read (the K1 profile is bound by the shared
+// memory data path: broadcast 16-B row loads cost 4 wavefronts per warp instruction)
+__device__ __forceinline__ double nprodx(int n, double x) {
+  return __fma_rn(__hiloint2double(0x43300000, n), x, __dmul_rn(x, -4503599627370496.0));
+}
 
 // v = b + sum_k h_k p_k, ascending k (each product is exact: h < 2^15, p has 24 bits)
 template <int KA>
-__device__ __forceinline__ double stock_mark(double b, const int (&h)[KA], const double* P, const double* MP) {
+__device__ __forceinline__ double stock_mark(double b, const int (&h)[KA], const double* P) {
   double acc = b;
-  FIN_CHUNKED(KA, acc, acc = fadd64(acc, nprod(h[k], P[k + o_], MP[k + o_]));)
+  FIN_CHUNKED(KA, acc, acc = fadd64(acc, nprodx(h[k], P[k + o_]));)
   return acc;
 }
 
@@ -120,16 +126,15 @@ __device__ __forceinline__ PackedActs<KA> pack_acts(const int (&a)[KA]) {
 // rare exact redo of the buys.
 template <int KA>
 __device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)[KA], const double* R, int RS,
-                                            const PackedActs<KA>& a, uint4* save) {
+                                            const PackedActs<KA>& a, uint4* save, int save_stride) {
   const double* P = R + kRowP * RS;
   const double* U = R + kRowU * RS;
-  const double* MP = R + kRowMP * RS;
-  const double* MU = R + kRowMU * RS;
+  const double* MU = R + kRowMU * RS;   // only for the rare exact redo
   const double* RU = R + kRowRU * RS;
   // 3. sells, clipped to holdings: b += fl(fl(n p) (1 - c)); n = 0 adds +0
   FIN_CHUNKED(KA, b, {
     const int n = max(min(-a[k], h[k]), 0);
-    b = fadd64(b, fmul64(nprod(n, P[k + o_], MP[k + o_]), e.dn));
+    b = fadd64(b, fmul64(nprodx(n, P[k + o_]), e.dn));
     h[k] -= n;
   })
   // 4. buys, ascending k, each n = min(want, f) with f the largest count whose cost
@@ -147,7 +152,7 @@ __device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)
       const int k0 = 8 * o + 2 * j, k1 = k0 + 1;
       w[j] = __byte_perm(k0 < KA ? (uint32_t)h[k0] : 0u, k1 < KA ? (uint32_t)h[k1] : 0u, 0x5410);
     }
-    save[o] = make_uint4(w[0], w[1], w[2], w[3]);
+    save[o * save_stride] = make_uint4(w[0], w[1], w[2], w[3]);
   }
   bool miss = false;
   // once the cash of every env of the warp is below min_k u_k, no later asset can be
@@ -160,8 +165,9 @@ __device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)
     // the checks below accept n only if it satisfies the definition itself
     const double D = __dadd_rd(fmul64(b, RU[k + o_]), 4503599627370496.0);
     const int n = min(want, __double2loint(D));
-    const double cn = nprod(n, U[k + o_], MU[k + o_]);
-    const double cn1 = nprod(n + 1, U[k + o_], MU[k + o_]);
+    const double mu = __dmul_rn(U[k + o_], -4503599627370496.0);
+    const double cn = nprod(n, U[k + o_], mu);
+    const double cn1 = nprod(n + 1, U[k + o_], mu);
     miss |= (!(cn <= b)) | ((n < want) & !(cn1 > b)) | (n < 0);
     b = fsub64(b, cn);
     h[k] += n;
@@ -169,10 +175,12 @@ __device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)
 buys_done:
   if (miss) {   // rare: arrays in local memory only on this path
     int hh[KA], aa[KA];
-    const uint32_t* sw = reinterpret_cast<const uint32_t*>(save);
 #pragma unroll
     for (int k = 0; k < KA; ++k) {
-      hh[k] = (int)((k & 1) ? (sw[k >> 1] >> 16) : (sw[k >> 1] & 0xffffu));
+      const uint4 v = save[(k >> 3) * save_stride];
+      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+      const uint32_t x = wv[(k >> 1) & 3];
+      hh[k] = (int)((k & 1) ? (x >> 16) : (x & 0xffffu));
       aa[k] = a[k];
     }
     b = stock_buys_exact(bpre, hh, aa, KA, U, MU);

@@ -340,8 +340,8 @@ struct StockOps {
           const double v = st.vc;
           uint4 save[(KA + 7) / 8];   // local: read only by the rare exact buy redo
           clamp_actions<KA>(e, a, st.oor, p.o.actions ? p.o.actions + ti * KA : nullptr);
-          stock_trade<KA>(e, st.b, st.h, pd, KP4, pack_acts<KA>(a), save);
-          const double vn = stock_mark<KA>(st.b, st.h, pd + kRowPN * KP4, pd + kRowMPN * KP4);
+          stock_trade<KA>(e, st.b, st.h, pd, KP4, pack_acts<KA>(a), save, 1);
+          const double vn = stock_mark<KA>(st.b, st.h, pd + kRowPN * KP4);
           st.vc = vn;
           FIN_TR(threadIdx.x == 128, t, 20);
           st.t_ep += 1;
