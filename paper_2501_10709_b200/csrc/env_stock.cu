@@ -179,15 +179,22 @@ __device__ __forceinline__ void k1_issue(const EnvDev& e, const int16_t* actions
   sm100::bulk_g2s(B.act, actions + (size_t)i0 * K, kStep * K * 2, bar);
 }
 
-#ifndef FIN_K1_MINB
-#define FIN_K1_MINB 3   // resident K1 blocks per SM (measured best of 2, 3, 4: scripts/k1_sweep.sh)
+#ifndef FIN_K1_E
+#define FIN_K1_E 1      // envs per thread (2 and 4 measured slower: scripts/k1_sweep.sh)
 #endif
+#ifndef FIN_K1_MINB
+#define FIN_K1_MINB (FIN_K1_E == 1 ? 3 : 4)   // resident K1 blocks per SM
+#endif
+constexpr int kK1E = FIN_K1_E;
+constexpr int kK1Threads = kStep / kK1E;      // a block owns a 128-env tile per iteration
 // No block-wide barrier inside the tile loop: warps are decoupled by the full / rows
 // / empty mbarriers, and an env whose day is not the predicted one reads its rows
-// from the (L2-resident) global table instead of a restaged copy.
+// from the (L2-resident) global table instead of a restaged copy.  Thread r of the
+// block steps envs r, r + kK1Threads, ... of the tile.
 template <int KA, bool EXACT>
-__global__ void __launch_bounds__(kStep, FIN_K1_MINB)
+__global__ void __launch_bounds__(kK1Threads, FIN_K1_MINB)
     k_stock_step(EnvDev e, const int16_t* __restrict__ actions, TrajDev o, int tma_ok) {
+  constexpr int E = kK1E;
   extern __shared__ __align__(16) uint8_t k1_smem[];   // dynamic: > 48 KB static limit
   K1Smem<KA>& sm = *reinterpret_cast<K1Smem<KA>*>(k1_smem);
   const int tid = threadIdx.x, lane = tid & 31;
@@ -199,7 +206,7 @@ __global__ void __launch_bounds__(kStep, FIN_K1_MINB)
     for (int q = 0; q < 2; ++q) {
       sm100::mbar_init(&sm.full[q], 1);
       sm100::mbar_init(&sm.rows[q], 1);
-      sm100::mbar_init(&sm.empty[q], kStep / 32);
+      sm100::mbar_init(&sm.empty[q], kK1Threads / 32);
     }
     sm100::fence_mbar_init();
   }
@@ -215,50 +222,72 @@ __global__ void __launch_bounds__(kStep, FIN_K1_MINB)
   for (int j = blockIdx.x; j < n_tiles; j += gridDim.x, ++it) {
     const int sb = it & 1;
     const int jn = j + gridDim.x;
-    const int i = j * kStep + tid;
-    const bool live = i < e.N;
     const bool tma = j < n_full;
-    int t = 0, w = 0;
-    double b = 0.0, v = 0.0;
-    int h[KA];
-    PackedActs<KA> a;
-#pragma unroll
-    for (int k = 0; k < KA; ++k) h[k] = 0;
     K1Buf<KA>& B = sm.buf[sb];
     if (tma) {
       sm100::mbar_wait(&sm.full[sb], (phase >> sb) & 1u);
       phase ^= 1u << sb;
-      t = B.t[tid];
-      w = B.w[tid];
-      b = B.cash[tid];
-      v = B.v[tid];
-#pragma unroll
-      for (int oc = 0; oc < (KA + 7) / 8; ++oc) {
-        const uint4 v = B.hold[oc][tid];
-        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (8 * oc + q < KA) h[8 * oc + q] = (int)((q & 1) ? (wv[q >> 1] >> 16) : (wv[q >> 1] & 0xffffu));
-      }
-      slab_read<KA, EXACT>(e, B.act, tid, K, true, a, oor, o.actions ? o.actions + (size_t)i * K : nullptr);
-    } else if (live) {   // ragged last tile / unaligned actions: direct loads
-      t = e.t_ep[i];
-      w = e.window[i];
-      b = e.cash[i];
-      v = e.vcur[i];
-      load_hold<KA>(e, i, h);
-      int x[KA];
-#pragma unroll
-      for (int k = 0; k < KA; ++k) x[k] = (k < K) ? (int)actions[(size_t)i * K + k] : 0;
-      clamp_actions<KA>(e, x, oor, nullptr);
-      if (o.actions)
-        for (int k = 0; k < K; ++k) o.actions[(size_t)i * K + k] = (int16_t)x[k];
-      a = pack_acts<KA>(x);
-    } else {
-#pragma unroll
-      for (int j = 0; j < (KA + 1) / 2; ++j) a.w[j] = 0u;
     }
-    // producer (thread 0): once the 4 warps are done with the other buffer (tile j - G),
+    int t[E], w[E], d[E];
+    double b[E], v[E];
+    int h[E][KA];
+    PackedActs<KA> a[E];
+    bool live[E], go[E];
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      const int r = tid + q * kK1Threads;   // env row in the tile
+      const int i = j * kStep + r;
+      live[q] = i < e.N;
+      t[q] = 0; w[q] = 0; b[q] = 0.0; v[q] = 0.0;
+#pragma unroll
+      for (int k = 0; k < KA; ++k) h[q][k] = 0;
+      if (tma) {
+        t[q] = B.t[r];
+        w[q] = B.w[r];
+        b[q] = B.cash[r];
+        v[q] = B.v[r];
+#pragma unroll
+        for (int oc = 0; oc < (KA + 7) / 8; ++oc) {
+          const uint4 x = B.hold[oc][r];
+          const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            if (8 * oc + c < KA) h[q][8 * oc + c] = (int)((c & 1) ? (wv[c >> 1] >> 16) : (wv[c >> 1] & 0xffffu));
+        }
+        slab_read<KA, EXACT>(e, B.act, r, K, true, a[q], oor, o.actions ? o.actions + (size_t)i * K : nullptr);
+      } else if (live[q]) {   // ragged last tile / unaligned actions: direct loads
+        t[q] = e.t_ep[i];
+        w[q] = e.window[i];
+        b[q] = e.cash[i];
+        v[q] = e.vcur[i];
+        load_hold<KA>(e, i, h[q]);
+        int x[KA];
+#pragma unroll
+        for (int k = 0; k < KA; ++k) x[k] = (k < K) ? (int)actions[(size_t)i * K + k] : 0;
+        clamp_actions<KA>(e, x, oor, nullptr);
+        if (o.actions)
+          for (int k = 0; k < K; ++k) o.actions[(size_t)i * K + k] = (int16_t)x[k];
+        a[q] = pack_acts<KA>(x);
+      } else {
+#pragma unroll
+        for (int c = 0; c < (KA + 1) / 2; ++c) a[q].w[c] = 0u;
+      }
+      const bool stepping = live[q] && t[q] < e.L;
+      if (live[q] && !stepping) {  // done env, autoreset = 0: ignored
+        set_flag(e, FIN_FLAG_EPISODE_DONE);
+        if (o.reward) o.reward[i] = 0.f;
+        if (o.done) o.done[i] = 1;
+      }
+      d[q] = day_of(e, w[q], t[q]);
+      const bool bad = stepping && (d[q] < 0 || d[q] + 1 >= e.rows);
+      if (bad) set_flag(e, FIN_FLAG_BAD_INDEX);
+      go[q] = stepping && !bad;
+      if (!go[q]) {   // steps with no trade: leaves b and h untouched
+#pragma unroll
+        for (int c = 0; c < (KA + 1) / 2; ++c) a[q].w[c] = 0u;
+      }
+    }
+    // producer (thread 0): once the warps are done with the other buffer (tile j - G),
     // refill it with tile jn's state and the rows of its predicted day
     if (tid == 0 && jn < n_tiles) {
       if (it >= 1) {
@@ -267,45 +296,52 @@ __global__ void __launch_bounds__(kStep, FIN_K1_MINB)
       }
       if (jn < n_full) k1_issue<KA>(e, actions, K, sm.buf[sb ^ 1], &sm.full[sb ^ 1], jn * kStep);
       rows_issue(e, sm.pr[sb ^ 1], &sm.rows[sb ^ 1], &sm.pred[sb ^ 1],
-                 predict_day(e, t, w, e.env_offset + (int64_t)j * kStep, e.env_offset + (int64_t)jn * kStep));
+                 predict_day(e, t[0], w[0], e.env_offset + (int64_t)j * kStep, e.env_offset + (int64_t)jn * kStep));
     }
-    const bool stepping = live && t < e.L;
-    if (live && !stepping) {  // done env, autoreset = 0: ignored
-      set_flag(e, FIN_FLAG_EPISODE_DONE);
-      if (o.reward) o.reward[i] = 0.f;
-      if (o.done) o.done[i] = 1;
-    }
-    const int d = day_of(e, w, t);
-    const bool bad = stepping && (d < 0 || d + 1 >= e.rows);
-    if (bad) set_flag(e, FIN_FLAG_BAD_INDEX);
     sm100::mbar_wait(&sm.rows[sb], (rphase >> sb) & 1u);
     rphase ^= 1u << sb;
-    if (stepping && !bad) {
-      const double* R = static_cast<const double*>(__builtin_assume_aligned(
-          (d == sm.pred[sb]) ? sm.pr[sb] : e.px + (size_t)d * kPriceRows * e.kp, 16));
-      stock_trade<KA>(e, b, h, R, RS, a, &sm.save[0][tid], kStep);
-      const double vn = stock_mark<KA>(b, h, R + kRowPN * RS);
-      double vnext = vn;
-      t += 1;
-      const bool done = (t == e.L);
-      if (o.reward) o.reward[i] = stock_reward(e, v, vn);
+    const double* R[E];
+    uint4* sv[E];
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      R[q] = static_cast<const double*>(__builtin_assume_aligned(
+          (!go[q] || d[q] == sm.pred[sb]) ? sm.pr[sb] : e.px + (size_t)d[q] * kPriceRows * e.kp, 16));
+      sv[q] = &sm.save[0][tid + q * kK1Threads];
+    }
+    stock_trade_e<KA, E>(e, b, h, R, RS, a, sv, kStep);
+    double vn[E];
+    const double* PN[E];
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      vn[q] = b[q];
+      PN[q] = R[q] + kRowPN * RS;
+    }
+    stock_mark_e<KA, E>(vn, h, PN);
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      if (!go[q]) continue;
+      const int i = j * kStep + tid + q * kK1Threads;
+      double vnext = vn[q];
+      t[q] += 1;
+      const bool done = (t[q] == e.L);
+      if (o.reward) o.reward[i] = stock_reward(e, v[q], vn[q]);
       if (o.done) o.done[i] = done ? 1 : 0;
-      if (o.cash) o.cash[i] = b;
-      if (o.asset) o.asset[i] = vn;
-      write_hold_row<KA>(e, o, (size_t)i, h);
+      if (o.cash) o.cash[i] = b[q];
+      if (o.asset) o.asset[i] = vn[q];
+      write_hold_row<KA>(e, o, (size_t)i, h[q]);
       if (done && e.autoreset) {
-        b = e.cash0;
+        b[q] = e.cash0;
         vnext = e.cash0;
 #pragma unroll
-        for (int k = 0; k < KA; ++k) h[k] = 0;
-        t = 0;
-        if (e.wadv) w = (w + 1) % e.W;
+        for (int k = 0; k < KA; ++k) h[q][k] = 0;
+        t[q] = 0;
+        if (e.wadv) w[q] = (w[q] + 1) % e.W;
       }
-      e.cash[i] = b;
+      e.cash[i] = b[q];
       e.vcur[i] = vnext;
-      store_hold<KA>(e, i, h);
-      e.t_ep[i] = t;
-      if (e.wadv) e.window[i] = w;
+      store_hold<KA>(e, i, h[q]);
+      e.t_ep[i] = t[q];
+      if (e.wadv) e.window[i] = w[q];
     }
     __syncwarp();
     if (lane == 0) sm100::mbar_arrive(&sm.empty[sb]);
@@ -536,7 +572,7 @@ int k1_grid(int N) {
   if (per_sm == 0) {
     cudaFuncSetAttribute(k_stock_step<KA, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(K1Smem<KA>));
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stock_step<KA, EXACT>, kStep,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stock_step<KA, EXACT>, kK1Threads,
                                                       sizeof(K1Smem<KA>)) != cudaSuccess)
       per_sm = 1;
   }
@@ -548,7 +584,7 @@ int k1_grid(int N) {
 cudaError_t launch_stock_step(const EnvDev& e, const int16_t* actions, const TrajDev& o, cudaStream_t s) {
   const int v = vec_ok(actions, 8);   // bulk copies of whole 128-env tiles: 256 K bytes each
 #define FIN_K1(KA, EX) \
-  k_stock_step<KA, EX><<<k1_grid<KA, EX>(e.N), kStep, sizeof(K1Smem<KA>), s>>>(e, actions, o, v)
+  k_stock_step<KA, EX><<<k1_grid<KA, EX>(e.N), kK1Threads, sizeof(K1Smem<KA>), s>>>(e, actions, o, v)
   if (e.K == 30) FIN_K1(30, true);
   else if (e.K == 4) FIN_K1(4, true);
   else if (e.K <= 8) FIN_K1(8, false);

@@ -189,6 +189,93 @@ buys_done:
   }
 }
 
+// ---------------------------------------------------------------- E envs per thread
+// The same transition for E independent envs of one thread, interleaved asset by asset:
+// the serial cash chains of the envs overlap (K1 at E = 1 stalled mostly on fixed-
+// latency dependencies of one chain).  Identical arithmetic per env.
+template <int KA, int E>
+__device__ __forceinline__ void stock_mark_e(double (&acc)[E], const int (&h)[E][KA], const double* const (&P)[E]) {
+  FIN_CHUNKED(KA, acc[0], {
+#pragma unroll
+    for (int q = 0; q < E; ++q) acc[q] = fadd64(acc[q], nprodx(h[q][k], P[q][k + o_]));
+  })
+}
+
+template <int KA, int E>
+__device__ __forceinline__ void stock_trade_e(const EnvDev& e, double (&b)[E], int (&h)[E][KA],
+                                              const double* const (&R)[E], int RS, const PackedActs<KA> (&a)[E],
+                                              uint4* const (&save)[E], int save_stride) {
+  // 3. sells
+  FIN_CHUNKED(KA, b[0], {
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      const int n = max(min(-a[q][k], h[q][k]), 0);
+      b[q] = fadd64(b[q], fmul64(nprodx(n, R[q][kRowP * RS + k + o_]), e.dn));
+      h[q][k] -= n;
+    }
+  })
+  // 4. buys (see stock_trade)
+  double bpre[E];
+  bool miss[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) {
+    bpre[q] = b[q];
+    miss[q] = false;
+#pragma unroll
+    for (int o = 0; o < (KA + 7) / 8; ++o) {
+      uint32_t w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k0 = 8 * o + 2 * j, k1 = k0 + 1;
+        w[j] = __byte_perm(k0 < KA ? (uint32_t)h[q][k0] : 0u, k1 < KA ? (uint32_t)h[q][k1] : 0u, 0x5410);
+      }
+      save[q][o * save_stride] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+  double umin[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) umin[q] = R[q][kRowMeta * RS];
+  FIN_CHUNKED(KA, b[0], {
+    if (k == c_ && c_ > 0) {
+      bool poor = true;
+#pragma unroll
+      for (int q = 0; q < E; ++q) poor &= !(b[q] >= umin[q]);
+      if (__all_sync(__activemask(), poor)) goto buys_done_e;
+    }
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      const double u = R[q][kRowU * RS + k + o_];
+      const int want = max(min(a[q][k], FIN_HOLD_MAX - h[q][k]), 0);
+      const double D = __dadd_rd(fmul64(b[q], R[q][kRowRU * RS + k + o_]), 4503599627370496.0);
+      const int n = min(want, __double2loint(D));
+      const double mu = __dmul_rn(u, -4503599627370496.0);
+      const double cn = nprod(n, u, mu);
+      const double cn1 = nprod(n + 1, u, mu);
+      miss[q] |= (!(cn <= b[q])) | ((n < want) & !(cn1 > b[q])) | (n < 0);
+      b[q] = fsub64(b[q], cn);
+      h[q][k] += n;
+    }
+  })
+buys_done_e:
+#pragma unroll
+  for (int q = 0; q < E; ++q) {
+    if (miss[q]) {   // rare: arrays in local memory only on this path
+      int hh[KA], aa[KA];
+#pragma unroll
+      for (int k = 0; k < KA; ++k) {
+        const uint4 v = save[q][(k >> 3) * save_stride];
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+        const uint32_t x = wv[(k >> 1) & 3];
+        hh[k] = (int)((k & 1) ? (x >> 16) : (x & 0xffffu));
+        aa[k] = a[q][k];
+      }
+      b[q] = stock_buys_exact(bpre[q], hh, aa, KA, R[q] + kRowU * RS, R[q] + kRowMU * RS);
+#pragma unroll
+      for (int k = 0; k < KA; ++k) h[q][k] = hh[k];
+    }
+  }
+}
+
 // copy the price rows of day d (px[d], kPriceRows x kp doubles) into pr[kPriceRows][kp]
 // (threads tid = 0 .. nthr-1 of the staging group)
 __device__ __forceinline__ void stage_price_rows(const EnvDev& e, double* pr, int d, int tid, int nthr) {
