@@ -481,16 +481,20 @@ int num_sms() {
   return n;
 }
 
-// Tiles per CTA for a launch: two tiles share every streamed weight stage (halving
-// L2 weight traffic per env-step and doubling the env warps per SM) when there are
-// more tiles than SMs and the members' biases still fit in shared memory; otherwise
-// one tile per CTA (small N is latency-bound: use as many SMs as there are tiles).
+// CTA layout for a launch when there are more tiles than SMs.  Default ("dual"): two
+// CTAs per SM with one tile each -- each tile has its own weight stream (2-slot ring)
+// and MMA issuer, so one tile's tensor-core phases overlap the other's env work (with
+// two tiles sharing one stream they advance in lockstep and the tensor core idles
+// during every env phase); the env warpgroup still gets 216 registers (setmaxnreg).
+// "pair" (FIN_TC_MODE=pair): one CTA with two tiles sharing each streamed weight stage.
+// With fewer tiles than SMs: one tile per CTA (latency-bound: spread over the SMs).
 template <class Plan, bool RES, class Ops>
 cudaError_t launch_auto(const TcParams& p, int n_envs, int* tiles, cudaStream_t s) {
   const int n_tiles = (n_envs + tc::kTileM - 1) / tc::kTileM;
-  static const char* mode = getenv("FIN_TC_MODE");   // experiment switch: "dual" = 2 CTAs / SM
+  const char* mode = getenv("FIN_TC_MODE");   // read per launch (tests switch it)
+  const bool pair = mode && mode[0] == 'p';
   if constexpr (!RES) {
-    if (mode && mode[0] == 'd' && n_tiles > num_sms()) {
+    if (!pair && n_tiles > num_sms()) {
       *tiles = 1;
       return tc::launch<Plan, RES, 1, Ops, 2, 2>(p, n_envs, s);
     }

@@ -182,7 +182,10 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
   // registers, the env warpgroups hold each env's whole state for all T steps.  Each
   // role's code sits inside the branch that resized its registers, so ptxas allocates
   // it against the new budget.
-  constexpr bool kSplitRegs = TILES == 2 && MINB == 1;
+  // (two tiles, one CTA per SM: 4 x 40 + 8 x 232 warps' worth = 64 K registers; one tile, two
+  // CTAs per SM: each CTA 4 x 40 + 4 x 216 of its 128-per-thread launch allocation)
+  constexpr bool kSplitRegs = (TILES == 2 && MINB == 1) || (TILES == 1 && MINB == 2);
+  constexpr uint32_t kEnvRegs = TILES == 2 ? 232 : 216;
   if (warp < 4) {
   if constexpr (kSplitRegs) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
   if (warp == 0) {
@@ -265,7 +268,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
     __syncwarp();
   }
   } else {
-    if constexpr (kSplitRegs) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    if constexpr (kSplitRegs) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kEnvRegs) : "memory");
     // ============================ env warpgroups ============================
     const int tile = (warp - 4) >> 2;
     const int q = warp & 3;                 // TMEM lane quarter this warp may access

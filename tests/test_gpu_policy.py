@@ -213,14 +213,17 @@ def test_fused_rollout_deterministic_and_partition_invariant_philox():
     assert np.abs(res[0][0]).sum() > 0
 
 
-def test_two_tiles_per_cta_match_one_tile_per_cta():
-    """More tiles than SMs switches the fused rollout to two tiles per CTA (one weight
-    stream for both, a setmaxnreg register split); fewer tiles run one tile per CTA.
-    Both layouts must give the same bits: N = 19200 (150 tiles, two per CTA) against
-    the same envs as two handles of 9600 (75 tiles each), Philox noise, T = 35 with a
-    reset, full trajectory compared."""
+@pytest.mark.parametrize("mode", ["dual", "pair"])
+def test_two_tiles_per_cta_match_one_tile_per_cta(mode, monkeypatch):
+    """More tiles than SMs switches the fused rollout to two tiles per SM: "dual" (the
+    default: two CTAs per SM, one tile and one weight stream each, setmaxnreg split) or
+    "pair" (one CTA, two tiles sharing each weight stage); fewer tiles run one tile per
+    CTA.  All layouts must give the same bits: N = 19200 (150 tiles) against the same
+    envs as two handles of 9600 (75 tiles each), Philox noise, T = 35 with a reset, full
+    trajectory compared."""
     import torch
     fin = _fin()
+    monkeypatch.setenv("FIN_TC_MODE", mode)
     m = market.stock_c1(rows=1008)
     layers = spol.kaiming_bf16(spol.STOCK_DIMS, 0)
     N, T, H = 19200, 35, 9600
