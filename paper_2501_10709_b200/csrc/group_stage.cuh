@@ -43,28 +43,34 @@ __device__ __forceinline__ void gs_init(GroupSlots* s, int gtid, int bar_id) {
   gs_bar(bar_id);
 }
 
-// round counter lives in a register of each thread (identical across the tile)
+// round counter lives in a register of each thread (identical across the tile).
+// uni_key >= 0: the caller knows (tile-uniformly) that every pending thread has this
+// key and that its row is already staged -- one round, no barrier.
 template <class StageF, class BodyF>
 __device__ __forceinline__ void group_apply(GroupSlots* s, int& round, int key, bool pending, int gtid, int bar_id,
-                                            StageF&& stage, BodyF&& body) {
-  bool any = gs_bar_or(bar_id, pending);
+                                            StageF&& stage, BodyF&& body, int uni_key = -1) {
+  const bool fast = uni_key >= 0;
+  bool any = fast ? true : gs_bar_or(bar_id, pending);
   while (any) {
-    const int e = round & 1;
-    if (gtid == 0) s->elect[e ^ 1] = INT_MAX;   // next round's slot (everyone is past its last read)
-    if (pending) atomicMin(&s->elect[e], key);
-    gs_bar(bar_id);
-    const int k = s->elect[e];
-    ++round;
-    if (k != s->staged) {
-      gs_bar(bar_id);                              // everyone has read s->staged
-      stage(k);
-      if (gtid == 0) s->staged = k;
+    int k = uni_key;
+    if (!fast) {
+      const int e = round & 1;
+      if (gtid == 0) s->elect[e ^ 1] = INT_MAX;   // next round's slot (everyone is past its last read)
+      if (pending) atomicMin(&s->elect[e], key);
       gs_bar(bar_id);
+      k = s->elect[e];
+      ++round;
+      if (k != s->staged) {
+        gs_bar(bar_id);                              // everyone has read s->staged
+        stage(k);
+        if (gtid == 0) s->staged = k;
+        gs_bar(bar_id);
+      }
     }
     if (pending && key == k) {
       body();
       pending = false;
     }
-    any = gs_bar_or(bar_id, pending);
+    any = fast ? false : gs_bar_or(bar_id, pending);
   }
 }

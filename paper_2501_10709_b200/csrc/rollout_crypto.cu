@@ -192,6 +192,7 @@ struct CryptoOps {
     return p.o.mlp_hidden + ((((size_t)t * p.M + m) * p.e.N + env) * 2 + l) * hid;
   }
 
+  __device__ __forceinline__ static void prepare(State&, const TcParams&, int, int, int) {}
   __device__ __forceinline__ static void consume(State& st, const TcParams& p, int env, int t, int m, const float* z) {
     if (!st.live) return;
     const EnvDev& e = p.e;

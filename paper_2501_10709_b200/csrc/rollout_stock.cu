@@ -74,11 +74,13 @@ struct StockOps {
     int h[KA];
     int t_ep, w, d;
     uint32_t b0bits;
-    bool zsm;          // this step's z1s rows are staged in shared memory
+    bool zsm;          // every live env of the tile is on day d0, whose rows are staged
+    int d0;
     int sb;            // current staging buffer
     int kcur, koth;    // day held by buffer sb / by buffer sb ^ 1 (-1: none)
     int pend;          // day being prefetched into buffer sb ^ 1 (-1: none)
     float asum[KA];
+    float eps[KA];     // this member's noise of the step (prepare(), while layer 2 runs)
     float ou[KOU];
     MetricAcc m;
     AggAcc agg;
@@ -188,6 +190,7 @@ struct StockOps {
     const bool uni = !gs_bar_or(bar_id, st.live && st.d != d0) && d0 >= 0;
     FIN_TR(threadIdx.x == 128, t, 24);
     st.zsm = uni;
+    st.d0 = d0;
     if (uni && d0 != st.kcur) {
       stage_row(p, d0, gtid, region(stg, st.sb));
       st.kcur = d0;
@@ -246,17 +249,11 @@ struct StockOps {
     return p.o.mlp_hidden + ((((size_t)t * p.M + m) * p.e.N + env) * 2 + l) * hid;
   }
 
-  __device__ __forceinline__ static void consume(State& st, const TcParams& p, int env, int t, int m, const float* z) {
+  // the member's noise for this step: Philox4x32-10 + Box-Muller (R-NOISE) or the
+  // supplied normals; independent of the network output, so it runs while layer 2 does
+  __device__ __forceinline__ static void prepare(State& st, const TcParams& p, int env, int t, int m) {
     if (!st.live) return;
     const EnvDev& e = p.e;
-    const int kind = p.kinds[m];
-    const bool sac = kind == FIN_SAC_SQUASH, ddpg = kind == FIN_DDPG_OU;
-    if (p.o.mlp_out) {
-      float* dst = p.o.mlp_out + (((size_t)t * p.M + m) * e.N + env) * KA;
-#pragma unroll
-      for (int k = 0; k < KA; ++k) dst[k] = z[k];
-    }
-    const float wm = p.weighted ? p.mw[m] : 1.f;
     const float* nz = p.noise + (((size_t)t * p.M + m) * e.N + env) * KA;
     // noise in blocks of 8 assets: two Philox counters (blocks 2q, 2q+1) per call
 #pragma unroll
@@ -275,6 +272,28 @@ struct StockOps {
         for (int j = 0; j < 8; ++j)
           if (pb * 8 + j < KA) eps[j] = __ldg(nz + pb * 8 + j);
       }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (pb * 8 + j < KA) st.eps[pb * 8 + j] = eps[j];
+    }
+  }
+
+  __device__ __forceinline__ static void consume(State& st, const TcParams& p, int env, int t, int m, const float* z) {
+    if (!st.live) return;
+    const EnvDev& e = p.e;
+    const int kind = p.kinds[m];
+    const bool sac = kind == FIN_SAC_SQUASH, ddpg = kind == FIN_DDPG_OU;
+    if (p.o.mlp_out) {
+      float* dst = p.o.mlp_out + (((size_t)t * p.M + m) * e.N + env) * KA;
+#pragma unroll
+      for (int k = 0; k < KA; ++k) dst[k] = z[k];
+    }
+    const float wm = p.weighted ? p.mw[m] : 1.f;
+#pragma unroll
+    for (int pb = 0; pb < (KA + 7) / 8; ++pb) {
+      float eps[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) eps[j] = pb * 8 + j < KA ? st.eps[pb * 8 + j] : 0.f;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int k = pb * 8 + j;
@@ -382,7 +401,8 @@ struct StockOps {
               metric_start(st.m, e.cash0);
             }
           }
-        });
+        },
+        st.zsm ? st.d0 : -1);   // uniform tile: its day's rows were staged by stage()
   }
 
   __device__ __forceinline__ static void finalize(State& st, const TcParams& p, int env, int gtid, int bar_id,
@@ -458,6 +478,7 @@ struct ProbeOps {
     if (st.b >= p.B || !p.hid_out) return nullptr;
     return p.hid_out + ((size_t)st.b * 2 + l) * hid;
   }
+  __device__ __forceinline__ static void prepare(State&, const TcParams&, int, int, int) {}
   __device__ __forceinline__ static void consume(State& st, const TcParams& p, int env, int t, int m,
                                                  const float* z) {
     if (st.b >= p.B) return;

@@ -391,6 +391,9 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
           else if (add) epilogue(F0{}, T1{});
           else epilogue(F0{}, F0{});
           kick(m, l + 1);
+          // work that does not depend on the network output (e.g. the step's noise)
+          // overlaps the largest MMA (layer 2) instead of following the last one
+          if (l == 0) Ops::prepare(st, p, env, t, m);
           FIN_TR(row == 0 && tile == 0 && m == 0, t, 3 + 2 * l);
         }
         // output layer
