@@ -515,7 +515,9 @@ cudaError_t launch_auto(const TcParams& p, int n_envs, int* tiles, cudaStream_t 
   const char* mode = getenv("FIN_TC_MODE");   // read per launch (tests switch it)
   const bool pair = mode && mode[0] == 'p';
   if constexpr (!RES) {
-    if (!pair && n_tiles > num_sms()) {
+    // two CTAs must fit one SM's shared memory (the bias of up to 4 members is staged)
+    const bool fits = 2 * tc::Smem<Plan, RES, 1, Ops, 2>::total(p.M) <= tc::kSmemLimit;
+    if (!pair && fits && n_tiles > num_sms()) {
       *tiles = 1;
       return tc::launch<Plan, RES, 1, Ops, 2, 2>(p, n_envs, s);
     }
