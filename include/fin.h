@@ -267,6 +267,21 @@ int fin_mlp_forward(const fin_policy* policy, const uint16_t* x, int32_t B, floa
 int fin_philox_normals(uint64_t seed, int64_t env_offset, int32_t N, int32_t K, int32_t member,
                        int64_t t_global, float* out, void* stream);
 
+/* Market preparation on the device (the step before the rollout; P:290, P:338;
+ * readings R11, R12, R-PERTURB): from raw OHLCV f32 [D][5][K] (open, high, low, close,
+ * volume; the first ``warmup`` of the D days are hidden warm-up), build the stock market
+ * tensor f32 [D - warmup][2 + I][K] that fin_env_create takes: c = 0 close, c = 1
+ * close / close[first stored day], c = 2 + i indicator ``indicators[i]`` (host array of
+ * FIN_IND_*, I <= 16) z-scored per (asset, indicator) over the stored days.  Every
+ * price of asset k is first scaled by c_k = 1 + magnitude (2 u_k - 1), u_k a Philox
+ * uniform of (seed, k) (magnitude 0: no perturbation).  Float64 arithmetic in the
+ * definitions' order.  ``raw`` (f64 [I][K][D - warmup], caller scratch) receives the
+ * stored indicator series before the z-score; the call needs it (no allocation). */
+enum { FIN_IND_MACD = 0, FIN_IND_BOLL_UB = 1, FIN_IND_BOLL_LB = 2, FIN_IND_RSI30 = 3, FIN_IND_CCI30 = 4,
+       FIN_IND_DX30 = 5, FIN_IND_SMA30 = 6, FIN_IND_SMA60 = 7 };
+int fin_market_prepare(const float* ohlcv, int32_t D, int32_t K, int32_t warmup, const int32_t* indicators /*host*/,
+                       int32_t I, double magnitude, uint64_t seed, float* market, double* raw, void* stream);
+
 /* Ensemble weights from validation statistics (Eq. 6; reading R-GATE):
  * aggs f64 [M][FIN_AGG_LEN] = the aggregate vector of one validation fin_rollout per
  * member (deterministic: FIN_NOISE_NONE), all-reduced over ranks.  Member Sharpe =

@@ -751,6 +751,21 @@ int fin_mlp_forward(const fin_policy* pol, const uint16_t* x, int32_t B, float* 
   return FIN_OK;
 }
 
+int fin_market_prepare(const float* ohlcv, int32_t D, int32_t K, int32_t warmup, const int32_t* indicators,
+                       int32_t I, double magnitude, uint64_t seed, float* market, double* raw, void* stream) {
+  if (!ohlcv || !market || !raw || (I > 0 && !indicators)) return fail(FIN_E_CONFIG, "fin_market_prepare: null argument");
+  if (K < 1 || warmup < 0 || D - warmup < 1) return fail(FIN_E_CONFIG, "need K >= 1 and D > warmup >= 0");
+  if (I < 0 || I > 16) return fail(FIN_E_CONFIG, "I must be in [0, 16]");
+  for (int i = 0; i < I; ++i)
+    if (indicators[i] < FIN_IND_MACD || indicators[i] > FIN_IND_SMA60)
+      return fail(FIN_E_CONFIG, "unknown indicator id %d", indicators[i]);
+  if (!(magnitude >= 0.0 && magnitude <= 0.1)) return fail(FIN_E_CONFIG, "magnitude must be in [0, 0.1]");
+  cudaError_t e = fin::launch_market_prepare(ohlcv, D, K, warmup, indicators, I, magnitude, seed, market, raw,
+                                             S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_market_prepare launch");
+  return FIN_OK;
+}
+
 int fin_member_weights(const double* aggs, int32_t M, double threshold, double temperature, float* w,
                        double* sharpe, void* stream) {
   if (!aggs || !w) return fail(FIN_E_CONFIG, "fin_member_weights: null argument");

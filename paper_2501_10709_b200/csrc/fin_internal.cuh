@@ -322,6 +322,8 @@ cudaError_t launch_agg_finalize(const double* partial, int n_blocks, double* agg
 cudaError_t launch_episode_metrics(const double* equity, const uint8_t* done, int T, int N, double reset_eq,
                                    double ppy, double rf, double* ep, int cap, int32_t* cnt,
                                    double* partial, int* n_blocks, cudaStream_t s);
+cudaError_t launch_market_prepare(const float* ohlcv, int D, int K, int warmup, const int32_t* ind, int I,
+                                  double magnitude, uint64_t seed, float* market, double* raw, cudaStream_t s);
 cudaError_t launch_member_weights(const double* stats, int M, double thr, double tau, float* w, double* sharpe,
                                   cudaStream_t s);
 cudaError_t launch_philox_normals(uint64_t seed, int64_t off, int N, int K, int member, int64_t t,

@@ -17,8 +17,11 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32
   }
 }
 
+// fp32 value of ((x >> 8) + 0.5) 2^-24: the +0.5 rounds away for x >> 8 >= 2^23 (the exact
+// value needs 25 bits); the rollout's noise is compared with tolerances, and exact
+// consumers (fin_market_prepare) form the value in f64
 __device__ __forceinline__ float philox_u01(uint32_t x) {
-  return ((float)(x >> 8) + 0.5f) * 5.9604644775390625e-08f;  // 2^-24, exact
+  return ((float)(x >> 8) + 0.5f) * 5.9604644775390625e-08f;
 }
 
 // Box-Muller pair from (u_r, u_a): r = sqrt(-2 ln u_r) (accurate log: u_r can be

@@ -33,6 +33,9 @@ FIN_FLAG_ACTION_RANGE, FIN_FLAG_EPISODE_DONE, FIN_FLAG_NONFINITE, FIN_FLAG_BAD_I
 FIN_STOCK, FIN_CRYPTO = 0, 1
 FIN_PPO_GAUSS, FIN_SAC_SQUASH, FIN_DDPG_OU, FIN_Q_ARGMAX, FIN_Q_DUELING = 0, 1, 2, 3, 4
 FIN_MAX_MEMBERS = 32
+FIN_IND_MACD, FIN_IND_BOLL_UB, FIN_IND_BOLL_LB, FIN_IND_RSI30, FIN_IND_CCI30, FIN_IND_DX30, FIN_IND_SMA30, \
+    FIN_IND_SMA60 = range(8)
+FIN_IND_NAMES = ("macd", "boll_ub", "boll_lb", "rsi30", "cci30", "dx30", "sma30", "sma60")
 FIN_NOISE_PHILOX, FIN_NOISE_SUPPLIED, FIN_NOISE_NONE = 0, 1, 2
 FIN_AGG_EPISODES, FIN_AGG_SUM_CUM, FIN_AGG_SUM_SHARPE, FIN_AGG_N_SHARPE, FIN_AGG_SUM_MDD, \
     FIN_AGG_SUM_REWARD = range(6)
@@ -45,7 +48,7 @@ FIN_AGG_LEN = 8
 EXPORTS = ("fin_env_create", "fin_env_reset", "fin_env_step", "fin_env_get_state", "fin_env_set_state",
            "fin_env_check", "fin_env_destroy", "fin_policy_create", "fin_policy_destroy", "fin_rollout",
            "fin_rollout_actions", "fin_ensemble_act", "fin_episode_metrics", "fin_mlp_forward",
-           "fin_philox_normals", "fin_member_weights", "fin_last_error", "fin_abi_version", "fin_device_check",
+           "fin_philox_normals", "fin_member_weights", "fin_market_prepare", "fin_last_error", "fin_abi_version", "fin_device_check",
            "fin_debug_trace")
 
 
@@ -98,6 +101,8 @@ _sig = {
     "fin_mlp_forward": ([_P, _P, C.c_int32, _P, _P, _P], C.c_int),
     "fin_philox_normals": ([C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int64, _P, _P], C.c_int),
     "fin_member_weights": ([_P, C.c_int32, C.c_double, C.c_double, _P, _P, _P], C.c_int),
+    "fin_market_prepare": ([_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_double,
+                            C.c_uint64, _P, _P, _P], C.c_int),
     "fin_last_error": ([], C.c_char_p),
     "fin_abi_version": ([], C.c_int),
     "fin_device_check": ([C.c_int32], C.c_int),
@@ -375,3 +380,16 @@ def fin_member_weights(aggs, w, sharpe=None, threshold: float = 0.0, temperature
     _check(_lib.fin_member_weights(_ptr(aggs, torch.float64, "aggs"), M, float(threshold), float(temperature),
                                    _ptr(w, torch.float32, "w"), _ptr(sharpe, torch.float64, "sharpe"),
                                    _stream(stream)), "fin_member_weights")
+
+
+def fin_market_prepare(ohlcv, warmup: int, indicators, market, raw, magnitude: float = 0.0, seed: int = 0,
+                       stream=None) -> None:
+    """ohlcv f32 [D][5][K] (device) -> market f32 [D-warmup][2+I][K] (device); raw f64
+    [I][K][D-warmup] (device scratch).  indicators: FIN_IND_* ids or names."""
+    import torch
+    D, _, K = (int(v) for v in ohlcv.shape)
+    ids = [FIN_IND_NAMES.index(i) if isinstance(i, str) else int(i) for i in indicators]
+    arr = (C.c_int32 * max(1, len(ids)))(*ids)
+    _check(_lib.fin_market_prepare(_ptr(ohlcv, torch.float32, "ohlcv"), D, K, int(warmup), arr, len(ids),
+                                   float(magnitude), int(seed), _ptr(market, torch.float32, "market"),
+                                   _ptr(raw, torch.float64, "raw"), _stream(stream)), "fin_market_prepare")
