@@ -371,3 +371,53 @@ def test_zz_mlp_error_statistics():
         with open(path, "w") as f:
             json.dump({"p99_max_pairs": MLP_STATS,
                        "max": max(m for _, m in MLP_STATS), "p99_max": max(p for p, _ in MLP_STATS)}, f)
+
+
+def test_headline_config_sampled_envs():
+    """The bench's own workload and launch configuration (C1 env + policy, N = 65,536 envs
+    -> 512 tiles, two CTAs per SM, production Philox noise), T = 35 (one reset), checked on
+    a seeded sample of 24 envs against the oracle run env by env (env_offset = the env's
+    global id): the replayed trajectory bit-exact, each action from the GPU's network output
+    and the oracle's own Philox4x32-10 + Box-Muller noise, the network output against the
+    oracle's forward pass on the replayed observation."""
+    import torch
+    fin = _fin()
+    m = market.stock_c1(rows=1008)
+    layers = spol.kaiming_bf16(spol.STOCK_DIMS, 0)
+    N, T, K, seed = 65536, 35, 30, 1234
+    kw = dict(num_assets=30, num_indicators=8, num_rows=1008, episode_len=30, num_windows=195, window_stride=5,
+              window_block=128)
+    _, fcfg = stock_pair(num_envs=N, **kw)
+    env = fin.fin_env_create(fcfg, m.market)
+    pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, layers)
+    logs = dict(actions=zeros((T, N, K), torch.int16), cash=zeros((T, N), torch.float64),
+                mlp_out=zeros((T, 1, N, K), torch.float32), done=zeros((T, N), torch.uint8))
+    fin.fin_rollout(env, [pol], T, fin.make_noise(fin.FIN_NOISE_PHILOX, seed), fin.make_traj(**logs))
+    assert fin.fin_env_check(env) == 0
+    rng = np.random.default_rng(7)
+    sample = sorted(set([0, N - 1] + list(rng.choice(N, 22, replace=False))))
+    g = {k: v[:, :, sample] if k == "mlp_out" else v[:, sample] for k, v in ((k, host(t)) for k, t in logs.items())}
+    L64 = omlp.layers_f64(layers)
+    n_boundary = 0
+    zs, refs = [], []
+    for j, i in enumerate(sample):
+        ocfg = ostock.StockEnvConfig(num_envs=1, env_offset=int(i), **kw)
+        o, _ = ostock.run_actions(ocfg, m.market, g["actions"][:, j:j + 1])
+        assert np.array_equal(o["cash"][:, 0], g["cash"][:, j]) and np.array_equal(o["done"][:, 0], g["done"][:, j] > 0)
+        st = ostock.reset(ocfg)
+        for t in range(T):
+            X = orol.stock_obs_batch(ocfg, st, m.market)
+            z = g["mlp_out"][t, 0, j].astype(np.float64)
+            zs.append(z)
+            refs.append(omlp.forward(L64, X)[0])
+            eps = ophx.stock_noise(seed, int(i), t, 0, K)
+            for k in range(K):
+                a = orol.policy.gaussian_action(float(z[k]), eps[k])
+                sh = orol.policy.shares(a)
+                if sh != g["actions"][t, j, k]:
+                    y = 100.0 * a
+                    assert abs(abs(y - math.trunc(y)) - 0.5) < 2e-3, (t, i, k, y, g["actions"][t, j, k])
+                    n_boundary += 1
+            ostock.step(ocfg, st, m.market, g["actions"][t, j:j + 1])
+    _mlp_close(np.array(zs), np.array(refs))
+    assert n_boundary <= 3
