@@ -133,15 +133,19 @@ struct K1Buf {
   uint4 hold[(KA + 7) / 8][kStep];
   alignas(16) int16_t act[kStep * KA];
 };
+#ifndef FIN_K1_NBUF
+#define FIN_K1_NBUF 2   // tile buffers: NBUF - 1 tiles in flight ahead of the one being stepped
+#endif
+constexpr int kK1Buf = FIN_K1_NBUF;
 template <int KA>
 struct K1Smem {
-  K1Buf<KA> buf[2];
+  K1Buf<KA> buf[kK1Buf];
   uint4 save[(KA + 7) / 8][kStep];   // [octet][thread]: conflict-free 16-B stores
-  alignas(16) double pr[2][kPriceRows * ((KA + 3) / 4 * 4)];
-  uint64_t full[2];    // state + actions of the buffer's tile landed (TMA)
-  uint64_t rows[2];    // price rows of the buffer's predicted day landed (TMA), or no prediction
-  uint64_t empty[2];   // the 4 warps are done with the buffer (state and rows)
-  int pred[2];
+  alignas(16) double pr[kK1Buf][kPriceRows * ((KA + 3) / 4 * 4)];
+  uint64_t full[kK1Buf];    // state + actions of the buffer's tile landed (TMA)
+  uint64_t rows[kK1Buf];    // price rows of the buffer's predicted day landed (TMA), or no prediction
+  uint64_t empty[kK1Buf];   // the 4 warps are done with the buffer (state and rows)
+  int pred[kK1Buf];
 };
 
 // day of the next tile predicted from (t0, w0) of global env g0 of this tile
@@ -203,7 +207,7 @@ __global__ void __launch_bounds__(kK1Threads, FIN_K1_MINB)
   const int n_full = tma_ok ? e.N / kStep : 0;   // tiles served by the bulk-copy pipeline
   const int RS = EXACT ? (KA + 3) / 4 * 4 : e.kp;   // staged row stride (= kp)
   if (tid == 0) {
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < kK1Buf; ++q) {
       sm100::mbar_init(&sm.full[q], 1);
       sm100::mbar_init(&sm.rows[q], 1);
       sm100::mbar_init(&sm.empty[q], kK1Threads / 32);
@@ -211,23 +215,26 @@ __global__ void __launch_bounds__(kK1Threads, FIN_K1_MINB)
     sm100::fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0 && (int)blockIdx.x < n_tiles) {
-    const int i0 = blockIdx.x * kStep;
-    if ((int)blockIdx.x < n_full) k1_issue<KA>(e, actions, K, sm.buf[0], &sm.full[0], i0);
-    rows_issue(e, sm.pr[0], &sm.rows[0], &sm.pred[0], day_of(e, __ldg(e.window + i0), __ldg(e.t_ep + i0)));
+  // prologue: the block's first NBUF - 1 tiles, rows of each tile's actual day
+  if (tid == 0) {
+    for (int q = 0; q + 1 < kK1Buf; ++q) {
+      const int jq = blockIdx.x + q * gridDim.x;
+      if (jq >= n_tiles) break;
+      const int i0 = jq * kStep;
+      if (jq < n_full) k1_issue<KA>(e, actions, K, sm.buf[q], &sm.full[q], i0);
+      rows_issue(e, sm.pr[q], &sm.rows[q], &sm.pred[q], day_of(e, __ldg(e.window + i0), __ldg(e.t_ep + i0)));
+    }
   }
-  uint32_t phase = 0, rphase = 0, ephase = 0;
   bool oor = false;
   int it = 0;
   for (int j = blockIdx.x; j < n_tiles; j += gridDim.x, ++it) {
-    const int sb = it & 1;
-    const int jn = j + gridDim.x;
+    const int sb = it % kK1Buf;
+    const uint32_t par = (uint32_t)(it / kK1Buf) & 1u;   // phase of slot sb's current use
+    const int jn = j + (kK1Buf - 1) * gridDim.x;          // tile refilled this iteration
+    const int sn = (it + kK1Buf - 1) % kK1Buf;            // ... into the slot of tile j - G
     const bool tma = j < n_full;
     K1Buf<KA>& B = sm.buf[sb];
-    if (tma) {
-      sm100::mbar_wait(&sm.full[sb], (phase >> sb) & 1u);
-      phase ^= 1u << sb;
-    }
+    if (tma) sm100::mbar_wait(&sm.full[sb], par);
     int t[E], w[E], d[E];
     double b[E], v[E];
     int h[E][KA];
@@ -287,19 +294,15 @@ __global__ void __launch_bounds__(kK1Threads, FIN_K1_MINB)
         for (int c = 0; c < (KA + 1) / 2; ++c) a[q].w[c] = 0u;
       }
     }
-    // producer (thread 0): once the warps are done with the other buffer (tile j - G),
-    // refill it with tile jn's state and the rows of its predicted day
+    // producer (thread 0): once the warps are done with tile j - G's buffer, refill it
+    // with tile jn's state and the rows of its predicted day
     if (tid == 0 && jn < n_tiles) {
-      if (it >= 1) {
-        sm100::mbar_wait(&sm.empty[sb ^ 1], (ephase >> (sb ^ 1)) & 1u);
-        ephase ^= 1u << (sb ^ 1);
-      }
-      if (jn < n_full) k1_issue<KA>(e, actions, K, sm.buf[sb ^ 1], &sm.full[sb ^ 1], jn * kStep);
-      rows_issue(e, sm.pr[sb ^ 1], &sm.rows[sb ^ 1], &sm.pred[sb ^ 1],
+      if (it >= 1) sm100::mbar_wait(&sm.empty[sn], (uint32_t)((it - 1) / kK1Buf) & 1u);
+      if (jn < n_full) k1_issue<KA>(e, actions, K, sm.buf[sn], &sm.full[sn], jn * kStep);
+      rows_issue(e, sm.pr[sn], &sm.rows[sn], &sm.pred[sn],
                  predict_day(e, t[0], w[0], e.env_offset + (int64_t)j * kStep, e.env_offset + (int64_t)jn * kStep));
     }
-    sm100::mbar_wait(&sm.rows[sb], (rphase >> sb) & 1u);
-    rphase ^= 1u << sb;
+    sm100::mbar_wait(&sm.rows[sb], par);
     const double* R[E];
     uint4* sv[E];
 #pragma unroll

@@ -16,6 +16,7 @@
 // drawdown (max, min, mdd) with mdd(A.B) = min(A.mdd, B.mdd, B.min/A.max - 1).
 #include "fin_internal.cuh"
 #include "philox.cuh"
+#include "sm100.cuh"
 
 namespace {
 
@@ -175,6 +176,270 @@ __global__ void k_pass_c(const double* __restrict__ eq, const uint8_t* __restric
   if (partial) agg_block_write(agg, partial + ((size_t)c * gridDim.x + blockIdx.x) * FIN_AGG_LEN);
 }
 
+// ------------------------------------------------------------ single fused pass
+// When the envs alone fill the GPU (one chunk), every thread walks its env's whole
+// log once.  The accumulator is cheaper than MetricAcc's Welford form (K6 was bound
+// by fp64 issue, not HBM: a correctly rounded division and reciprocal per point):
+//   r_t  = (v_t - v_{t-1}) * rcp(v_{t-1})   -- v_t - v_{t-1} is exact (Sterbenz) and
+//          rcp(v) (MUFU seed + 2 Newton steps, <= 1 ulp) is computed once per point,
+//          when v becomes the previous point: r within ~2 ulp of v_t / v_{t-1} - 1
+//   shifted sums S1 = sum (r - r_1), S2 = sum (r - r_1)^2 with the episode's first
+//          return r_1 as the shift: var = (S2 - S1^2 / n) / (n - 1), relative error
+//          O(n eps (1 + (mean - r_1)^2 / var)); identical returns give S1 = S2 = 0, so
+//          a flat equity curve still yields std = 0 -> NaN (reading R21)
+//   drawdown (v - peak) * rcp(peak), rcp(peak) = rcp(v) of the point that set the peak
+//          (~2 ulp relative, exactly 0 at a peak).
+// Tolerances of the parity tests (rel 1e-9 cum / MDD, 1e-7 Sharpe) hold with room.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = __fma_rn(-x, y, 1.0);
+  y = __fma_rn(y, e, y);
+  e = __fma_rn(-x, y, 1.0);
+  return __fma_rn(y, e, y);
+}
+
+struct FastAcc {
+  double v0, vprev, rinv, peak, rpeak, mdd, k, s1, s2;
+  int32_t n;
+};
+
+__device__ __forceinline__ void fast_start(FastAcc& a, double v) {
+  a.v0 = v; a.vprev = v; a.rinv = rcp_nr(v); a.peak = v; a.rpeak = a.rinv; a.mdd = 0.0;
+  a.k = 0.0; a.s1 = 0.0; a.s2 = 0.0; a.n = 0;
+}
+
+// branch-free: the drawdown (v - peak) * rcp(peak) reuses rcp(v) of the new peak (a
+// data-dependent division branch was taken by some env of nearly every warp)
+__device__ __forceinline__ void fast_push(FastAcc& a, double v) {
+  const double r = fmul64(fsub64(v, a.vprev), a.rinv);
+  const double rv = rcp_nr(v);
+  a.rinv = rv;
+  a.vprev = v;
+  a.k = a.n == 0 ? r : a.k;
+  const double x = fsub64(r, a.k);
+  a.s1 = fadd64(a.s1, x);
+  a.s2 = __fma_rn(x, x, a.s2);
+  a.n += 1;
+  const bool up = v > a.peak;
+  a.peak = up ? v : a.peak;
+  a.rpeak = up ? rv : a.rpeak;
+  a.mdd = fmin(a.mdd, fmul64(fsub64(v, a.peak), a.rpeak));
+}
+
+__device__ __forceinline__ void fast_finish(const FastAcc& a, double ppy, double rf, double out[3]) {
+  out[0] = fmul64(fsub64(a.vprev, a.v0), rcp_nr(a.v0));   // exact 0 for a flat curve
+  double sh = __longlong_as_double(0x7ff8000000000000ULL);
+  if (a.n >= 2) {
+    const double rn = rcp_nr(nn2d(a.n));
+    const double mean = fadd64(a.k, fmul64(a.s1, rn));
+    const double var = fmul64(fsub64(a.s2, fmul64(fmul64(a.s1, a.s1), rn)), rcp_nr(nn2d(a.n - 1)));
+    if (var > 0.0) sh = fmul64(fmul64(sqrt(ppy), fsub64(mean, rf)), rsqrt(var));
+  }
+  out[1] = sh;
+  out[2] = a.mdd;
+}
+
+// Episode end: metrics row, per-thread aggregate (shared memory, touched only here).
+#ifndef FIN_K6_MINB
+#define FIN_K6_MINB 6
+#endif
+#ifndef FIN_K6_NOINLINE
+#define FIN_K6_NOINLINE 0
+#endif
+#if FIN_K6_NOINLINE
+#define FIN_K6_EP_ATTR __noinline__
+#else
+#define FIN_K6_EP_ATTR __forceinline__
+#endif
+__device__ FIN_K6_EP_ATTR void fast_episode(FastAcc& a, double ppy, double rf, double* ep, int cap, int N, int i,
+                                            int k, double* sagg, double reset_eq) {
+  double em[3];
+  fast_finish(a, ppy, rf, em);
+  if (ep && k < cap) {
+    double* d = ep + ((size_t)k * N + i) * 3;
+    d[0] = em[0]; d[1] = em[1]; d[2] = em[2];
+  }
+  AggAcc g;   // the thread's aggregate partial lives in shared memory (touched once per episode)
+#pragma unroll
+  for (int j = 0; j < FIN_AGG_LEN; ++j) g.s[j] = sagg[j * kThreads];
+  agg_episode(g, em);
+#pragma unroll
+  for (int j = 0; j < FIN_AGG_LEN; ++j) sagg[j * kThreads] = g.s[j];
+  fast_start(a, reset_eq);
+}
+
+__device__ __forceinline__ void sagg_init(double* sagg) {
+  AggAcc g;
+  agg_init(g);
+#pragma unroll
+  for (int j = 0; j < FIN_AGG_LEN; ++j) sagg[j * kThreads] = g.s[j];
+}
+
+// one thread per env, the whole log; the next U rows are loaded under the arithmetic
+// of the current U.  Up to 8 blocks of 128 per SM (<= 64 registers): 32 warps in
+// flight; the aggregate lives in shared memory.
+__global__ void __launch_bounds__(kThreads, FIN_K6_MINB)
+    k_metrics_fused(const double* __restrict__ eq, const uint8_t* __restrict__ done, int T, int N, double reset_eq,
+                    double ppy, double rf, double* __restrict__ ep, int cap, int32_t* __restrict__ cnt_out,
+                    double* __restrict__ partial) {
+  constexpr int U = 8;
+  __shared__ double s_agg[FIN_AGG_LEN * kThreads];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  sagg_init(s_agg + threadIdx.x);
+  if (i < N) {
+    FastAcc a;
+    fast_start(a, __ldg(eq + i));
+    int k = 0;
+    double vb[U];
+    uint32_t db = 0;   // done bits of the current U rows
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      vb[u] = u < T ? __ldg(eq + (size_t)(u + 1) * N + i) : 0.0;
+      db |= (u < T ? (uint32_t)__ldg(done + (size_t)u * N + i) : 0u) << u;
+    }
+    for (int t = 0; t < T; t += U) {
+      double vn[U];
+      uint32_t dn = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int tn = t + U + u;
+        vn[u] = tn < T ? __ldg(eq + (size_t)(tn + 1) * N + i) : 0.0;
+        dn |= (tn < T ? (uint32_t)__ldg(done + (size_t)tn * N + i) : 0u) << u;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (t + u < T) {
+          fast_push(a, vb[u]);
+          if ((db >> u) & 1u) {
+            fast_episode(a, ppy, rf, ep, cap, N, i, k, s_agg + threadIdx.x, reset_eq);
+            ++k;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) vb[u] = vn[u];
+      db = dn;
+    }
+    if (cnt_out) cnt_out[i] = k;
+  }
+  if (partial) {
+    AggAcc g;
+#pragma unroll
+    for (int j = 0; j < FIN_AGG_LEN; ++j) g.s[j] = s_agg[j * kThreads + threadIdx.x];
+    agg_block_write(g, partial + (size_t)blockIdx.x * FIN_AGG_LEN);
+  }
+}
+
+// TMA-staged variant of the fused pass (N % 16 == 0, 16-B aligned logs): a producer
+// warp streams, per 128-env block, chunks of R rows of the equity log (1 KB per row)
+// and of the done log (128 B per row) into an S-slot shared-memory ring with 1-D bulk
+// copies (cp.async.bulk, complete_tx on the slot's mbarrier), so S - 1 chunks are in
+// flight per block without holding them in registers; the 4 consumer warps walk the
+// rows out of shared memory (conflict-free 8-B / 1-B loads).
+#ifndef FIN_K6_S
+#define FIN_K6_S 3
+#endif
+#ifndef FIN_K6_R
+#define FIN_K6_R 8
+#endif
+#ifndef FIN_K6_TMINB
+#define FIN_K6_TMINB 5
+#endif
+constexpr int kK6S = FIN_K6_S, kK6R = FIN_K6_R;
+struct K6Smem {
+  double eq[kK6S][kK6R][kThreads];
+  uint8_t dn[kK6S][kK6R][kThreads];
+  double agg[FIN_AGG_LEN * kThreads];
+  uint64_t full[kK6S], empty[kK6S];
+};
+
+__global__ void __launch_bounds__(kThreads + 32, FIN_K6_TMINB)
+    k_metrics_tma(const double* __restrict__ eq, const uint8_t* __restrict__ done, int T, int N, double reset_eq,
+                  double ppy, double rf, double* __restrict__ ep, int cap, int32_t* __restrict__ cnt_out,
+                  double* __restrict__ partial) {
+  extern __shared__ __align__(128) uint8_t k6_smem[];
+  K6Smem& sm = *reinterpret_cast<K6Smem*>(k6_smem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int i0 = blockIdx.x * kThreads;
+  const int nb = min(kThreads, N - i0);           // envs of this block (multiple of 16)
+  const int nchunks = (T + kK6R - 1) / kK6R;
+  if (tid == 0) {
+    for (int q = 0; q < kK6S; ++q) {
+      sm100::mbar_init(&sm.full[q], 1);
+      sm100::mbar_init(&sm.empty[q], kThreads / 32);
+    }
+    sm100::fence_mbar_init();
+  }
+  if (tid < kThreads) sagg_init(sm.agg + tid);
+  __syncthreads();
+  if (warp == kThreads / 32) {
+    // ---- producer
+    if (lane == 0) {
+      for (int c = 0; c < nchunks; ++c) {
+        const int slot = c % kK6S;
+        if (c >= kK6S) sm100::mbar_wait(&sm.empty[slot], (uint32_t)(c / kK6S - 1) & 1u);
+        const int rows = min(kK6R, T - c * kK6R);
+        sm100::mbar_arrive_expect_tx(&sm.full[slot], (uint32_t)(rows * nb * 9));
+        for (int r = 0; r < rows; ++r) {
+          const size_t t = (size_t)c * kK6R + r;
+          sm100::bulk_g2s(sm.eq[slot][r], eq + (t + 1) * N + i0, (uint32_t)nb * 8, &sm.full[slot]);
+          sm100::bulk_g2s(sm.dn[slot][r], done + t * N + i0, (uint32_t)nb, &sm.full[slot]);
+        }
+      }
+    }
+  } else {
+    // ---- consumers: thread tid owns env i0 + tid
+    const bool live = tid < nb;
+    const int i = i0 + tid;
+    FastAcc a;
+    fast_start(a, live ? __ldg(eq + i) : 1.0);
+    int k = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int slot = c % kK6S;
+      sm100::mbar_wait(&sm.full[slot], (uint32_t)(c / kK6S) & 1u);
+      const int rows = min(kK6R, T - c * kK6R);
+      if (live) {
+        if (rows == kK6R) {
+          double v[kK6R];
+          uint8_t d[kK6R];
+#pragma unroll
+          for (int r = 0; r < kK6R; ++r) { v[r] = sm.eq[slot][r][tid]; d[r] = sm.dn[slot][r][tid]; }
+#pragma unroll
+          for (int r = 0; r < kK6R; ++r) {
+            fast_push(a, v[r]);
+            if (d[r]) {
+              fast_episode(a, ppy, rf, ep, cap, N, i, k, sm.agg + tid, reset_eq);
+              ++k;
+            }
+          }
+        } else {
+          for (int r = 0; r < rows; ++r) {
+            fast_push(a, sm.eq[slot][r][tid]);
+            if (sm.dn[slot][r][tid]) {
+              fast_episode(a, ppy, rf, ep, cap, N, i, k, sm.agg + tid, reset_eq);
+              ++k;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&sm.empty[slot]);
+    }
+    if (live && cnt_out) cnt_out[i] = k;
+  }
+  __syncthreads();
+  if (partial) {   // every thread takes part (agg_block_write synchronises the block); the
+    AggAcc g;      // producer warp contributes the neutral element
+    agg_init(g);
+    if (tid < kThreads) {
+#pragma unroll
+      for (int j = 0; j < FIN_AGG_LEN; ++j) g.s[j] = sm.agg[j * kThreads + tid];
+    }
+    agg_block_write(g, partial + (size_t)blockIdx.x * FIN_AGG_LEN);
+  }
+}
+
 __global__ void k_philox_normals(uint64_t seed, int64_t off, int N, int K, int member, int64_t t, float* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
@@ -240,8 +505,23 @@ cudaError_t launch_episode_metrics(const double* equity, const uint8_t* done, in
   dim3 grid(env_blocks, nchunks);
   *n_blocks = env_blocks * nchunks;
   if (nchunks == 1) {   // enough envs to fill the GPU: one fused pass, each row read once
+#ifdef FIN_K6_OLD
     k_pass_c<<<grid, kThreads, 0, s>>>(equity, done, T, N, chunk, reset_eq, ppy, rf, nullptr, nullptr, ep, cap,
                                         cnt, partial);
+#else
+    const bool tma = N % 16 == 0 && ((uintptr_t)equity & 15) == 0 && ((uintptr_t)done & 15) == 0 && !getenv("FIN_K6_NOTMA");
+    if (tma) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_metrics_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K6Smem));
+        attr = true;
+      }
+      k_metrics_tma<<<env_blocks, kThreads + 32, sizeof(K6Smem), s>>>(equity, done, T, N, reset_eq, ppy, rf, ep, cap,
+                                                                      cnt, partial);
+    } else {
+      k_metrics_fused<<<env_blocks, kThreads, 0, s>>>(equity, done, T, N, reset_eq, ppy, rf, ep, cap, cnt, partial);
+    }
+#endif
     return cudaGetLastError();
   }
   Seg* seg = nullptr;

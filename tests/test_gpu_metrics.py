@@ -10,11 +10,12 @@ pytestmark = [pytest.mark.gpu, needs_gpu]
 
 
 @pytest.mark.parametrize("T,N,p_done", [(64, 8, 0.05), (3000, 300, 0.01), (20000, 40, 0.0005), (7, 1, 0.5),
-                                         (45, 270000, 1 / 30)])
+                                         (45, 270000, 1 / 30), (45, 262150, 1 / 30)])
 def test_episode_metrics_parity(T, N, p_done):
     """Chunked three-pass scans (small N) and the single fused pass (N >= 2048 x 128:
     every row read once; checked on a seeded sample of 400 envs plus the first and
-    last env)."""
+    last env) -- TMA-staged when N % 16 == 0 (270,000: a ragged last block of 48 envs,
+    T = 45 a ragged last chunk of rows), register-prefetched otherwise (262,150)."""
     import torch
     from paper_2501_10709_b200 import fin
     rng = np.random.default_rng(T + N)
@@ -54,3 +55,21 @@ def test_episode_metrics_parity(T, N, p_done):
         np.testing.assert_allclose(agg[fin.FIN_AGG_SUM_SHARPE], sh_sum, rtol=1e-7, atol=1e-9)
     else:
         assert agg[fin.FIN_AGG_EPISODES] == ec.sum()
+
+
+def test_episode_metrics_flat_equity():
+    """A flat equity curve (zero actions) has zero returns: cum = MDD = 0 and
+    Sharpe = NaN (std = 0, reading R21), on both fused-pass variants."""
+    import torch
+    from paper_2501_10709_b200 import fin
+    for N in (262144, 262146):
+        T = 60
+        eq = torch.full((T + 1, N), 1e6, dtype=torch.float64, device="cuda")
+        done = torch.zeros((T, N), dtype=torch.uint8, device="cuda")
+        done[29::30] = 1
+        em, ec = zeros((2, N, 3), torch.float64), zeros(N, torch.int32)
+        fin.fin_episode_metrics(eq, done, 1e6, 252.0, 0.0, em, ec)
+        em, ec = host(em), host(ec)
+        assert (ec == 2).all()
+        assert (em[:, :, 0] == 0).all() and (em[:, :, 2] == 0).all()
+        assert np.isnan(em[:, :, 1]).all()
