@@ -509,6 +509,10 @@ int num_sms() {
 // during every env phase); the env warpgroup still gets 216 registers (setmaxnreg).
 // "pair" (FIN_TC_MODE=pair): one CTA with two tiles sharing each streamed weight stage.
 // With fewer tiles than SMs: one tile per CTA (latency-bound: spread over the SMs).
+#ifndef FIN_DUAL_RING
+#define FIN_DUAL_RING 2   // weight-ring slots per CTA in the dual layout
+#endif
+constexpr int kDualRing = FIN_DUAL_RING;
 template <class Plan, bool RES, class Ops>
 cudaError_t launch_auto(const TcParams& p, int n_envs, int* tiles, cudaStream_t s) {
   const int n_tiles = (n_envs + tc::kTileM - 1) / tc::kTileM;
@@ -516,10 +520,10 @@ cudaError_t launch_auto(const TcParams& p, int n_envs, int* tiles, cudaStream_t 
   const bool pair = mode && mode[0] == 'p';
   if constexpr (!RES) {
     // two CTAs must fit one SM's shared memory (the bias of up to 4 members is staged)
-    const bool fits = 2 * tc::Smem<Plan, RES, 1, Ops, 2>::total(p.M) <= tc::kSmemLimit;
+    const bool fits = 2 * tc::Smem<Plan, RES, 1, Ops, kDualRing>::total(p.M) <= tc::kSmemLimit;
     if (!pair && fits && n_tiles > num_sms()) {
       *tiles = 1;
-      return tc::launch<Plan, RES, 1, Ops, 2, 2>(p, n_envs, s);
+      return tc::launch<Plan, RES, 1, Ops, kDualRing, 2>(p, n_envs, s);
     }
   }
   if (n_tiles > num_sms() && p.M <= tc::Smem<Plan, RES, 2, Ops>::max_members()) {

@@ -205,7 +205,9 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
           for (int m = 0; m < M; ++m)
             for (int s = 0; s < NS; ++s, ++it) {
               const uint32_t slot = it % RING, ph = (it / RING) & 1;
-              sm100::mbar_wait(&w_empty[slot], ph ^ 1);
+              sm100::mbar_wait_fast(&w_empty[slot], ph ^ 1);
+              FIN_TR(m == 0 && (s == 0 || s == NS - 1), t, s == 0 ? 30 : 31);
+              FIN_TR(m == 0 && s < 16, T + t, 16 + s);   // per-stage detail rows (trace [2T][32])
               sm100::mbar_arrive_expect_tx(&w_full[slot], (uint32_t)Plan::bytes_of(s));
               sm100::bulk_g2s_hint(sW + slot * Plan::kStageBytes, p.wpack[m] + Plan::offset_of(s),
                                    (uint32_t)Plan::bytes_of(s), &w_full[slot], pol);
@@ -223,7 +225,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
         for (int m = 0; m < M; ++m) {
 #pragma unroll 1
           for (int l = 0; l < 3; ++l) {
-            sm100::mbar_wait(a_full, a_use & 1);
+            sm100::mbar_wait_fast(a_full, a_use & 1);
             ++a_use;
             FIN_TR(m == 0, t, 9 + 2 * l);
             sm100::tc_fence_after();
@@ -235,7 +237,11 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
                 b_base = wa + (uint32_t)(m * Plan::kMemberBytes + Plan::offset_of(s));
               } else {
                 const uint32_t slot = it % RING, ph = (it / RING) & 1;
-                sm100::mbar_wait(&w_full[slot], ph);
+                FIN_TR(m == 0 && s < 16, 2 * T + t, s);
+                sm100::mbar_wait_fast(&w_full[slot], ph);
+                FIN_TR(m == 0 && s == Plan::first_stage(l), t, 26 + l);
+                FIN_TR(m == 0 && l == 1 && s == Plan::first_stage(1) + Plan::nstages(1) - 1, t, 29);
+                FIN_TR(m == 0 && s < 16, T + t, s);
                 sm100::tc_fence_after();
                 b_base = wa + slot * (uint32_t)Plan::kStageBytes;
               }
@@ -253,6 +259,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
                   sm100::mma_bf16(d_tmem, ad0 + (uint64_t)(16 * j), bd0 + (uint64_t)(16 * j), idesc,
                                   (j0 + j) > 0 ? 1u : 0u);
               }
+              FIN_TR(m == 0 && s < 16, 2 * T + t, 16 + s);
               if (!RESIDENT) {
                 sm100::mma_commit(&w_empty[it % RING]);
                 ++it;

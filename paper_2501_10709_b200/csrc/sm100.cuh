@@ -2,6 +2,9 @@
 // fused rollout uses: mbarrier, 1-D bulk TMA (cp.async.bulk), tcgen05 TMEM
 // alloc / MMA / commit / load, proxy fences.  No CUTLASS / CuTe.
 #pragma once
+#ifndef FIN_MBAR_FAST
+#define FIN_MBAR_FAST 0
+#endif
 #include <stdint.h>
 
 namespace sm100 {
@@ -41,6 +44,27 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
+}
+// try_wait without a suspend-time hint (the hardware's default time limit): for the
+// single-lane producer / MMA roles whose wake-up latency is on the critical path
+__device__ __forceinline__ bool mbar_try_wait_nh(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_fast(uint64_t* bar, uint32_t parity) {
+#if FIN_MBAR_FAST
+  while (!mbar_try_wait_nh(bar, parity)) {
+  }
+#else
+  mbar_wait(bar, parity);
+#endif
 }
 
 // ------------------------------------------------------------------ bulk TMA (1-D)

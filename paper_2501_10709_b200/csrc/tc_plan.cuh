@@ -82,6 +82,9 @@ struct StockObs {
 //   crypto C3 Q-net  103-128-128-3   -> (112, 128, 16)   (every input is read from the step's row)
 using ObsC1 = StockObs<30, 8>;
 using ObsSmall = StockObs<4, 4>;
-using PlanStockC1 = TcPlan<ObsC1::kEnvPad, 256, 32, 16384>;
+#ifndef FIN_C1_STAGE
+#define FIN_C1_STAGE 16384   // weight-stage bytes of the streamed C1 plan
+#endif
+using PlanStockC1 = TcPlan<ObsC1::kEnvPad, 256, 32, FIN_C1_STAGE>;
 using PlanStockSmall = TcPlan<ObsSmall::kEnvPad, 128, 16, 16384>;
 using PlanCrypto = TcPlan<112, 128, 16, 32768>;

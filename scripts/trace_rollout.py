@@ -21,7 +21,7 @@ rew = torch.zeros((T, N), dtype=torch.float32, device="cuda")
 tr = fin.make_traj(reward=rew)
 nz = fin.make_noise(fin.FIN_NOISE_PHILOX, 7)
 fin.fin_rollout(env, [pol], T, nz, tr)
-buf = torch.zeros((T, 32), dtype=torch.int64, device="cuda")
+buf = torch.zeros((3 * T, 32), dtype=torch.int64, device="cuda")
 fin.fin_debug_trace(buf)
 fin.fin_rollout(env, [pol], T, nz, tr)
 torch.cuda.synchronize()
@@ -29,8 +29,16 @@ fin.fin_debug_trace(None)
 b = buf.cpu().numpy().astype(np.int64)
 names = {0: "step", 23: "stg:d", 24: "stg:uni", 25: "stg:done", 1: "obs_done", 9: "mma:a1", 10: "mma:i1",
          2: "d1", 3: "epi1", 11: "mma:a2", 12: "mma:i2", 4: "d2", 5: "epi2", 13: "mma:a3", 14: "mma:i3", 6: "d3",
-         16: "philox0", 7: "consume", 17: "fs:start", 19: "fs:body", 20: "fs:tx", 21: "fs:metric", 8: "env_done"}
+         16: "philox0", 7: "consume", 26: "w1rdy", 27: "w2rdy", 28: "w3rdy", 29: "w2last", 30: "p:l1", 31: "p:l3", 17: "fs:start", 19: "fs:body", 20: "fs:tx", 21: "fs:metric", 8: "env_done"}
 for t in range(T):
     d = b[t] - b[t, 0]
     order = sorted((int(d[i]), n) for i, n in names.items() if b[t, i] != 0)
     print(f"t={t}: " + " ".join(f"{n}={v}" for v, n in order))
+
+# per-stage detail: MMA warp after each stage's w_full wait (m) / producer after each w_empty wait (p)
+for t in range(T):
+    d = b[T + t] - b[t, 0]
+    print(f"t={t} stages: " + " ".join(f"m{s}={int(d[s])}" for s in range(16) if b[T + t, s] != 0))
+    print(f"t={t} produce: " + " ".join(f"p{s}={int(d[16 + s])}" for s in range(16) if b[T + t, 16 + s] != 0))
+    d = b[2 * T + t] - b[t, 0]
+    print(f"t={t} mma before-wait/after-issue: " + " ".join(f"s{s}={int(d[s])}/{int(d[16 + s])}" for s in range(16) if b[2 * T + t, s] != 0))
