@@ -19,7 +19,7 @@ namespace fin {
 // n_envs rows; *tiles receives the tiles per CTA the launch used (agg partial rows
 // = ceil(n_envs / (128 * tiles)) * tiles)
 cudaError_t launch_stock_rollout(int net, const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s);
-cudaError_t launch_crypto_rollout(const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s);
+cudaError_t launch_crypto_rollout(int net, const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s);
 cudaError_t launch_mlp_probe(int net, const tc::TcParams& p, int n_rows, cudaStream_t s);
 cudaError_t launch_z1s_market(int net, const float* w1s_t, int H, const EnvDev& e, float* z1s, cudaStream_t s);
 cudaError_t launch_z1s_probe(int net, const float* w1s_t, int H, const uint16_t* x, int B, int in_dim, float* z1s,
@@ -42,10 +42,11 @@ struct fin_env {
 
 struct fin_policy {
   int32_t kind;
-  int32_t net;                 // 0 stock C1, 1 stock small, 2 crypto
-  int32_t dims[4];
+  int32_t net;                 // 0 stock C1, 1 stock small, 2 crypto, 3 stock paper net, 4 crypto paper net
+  int32_t n_layers;            // 3 or 4
+  int32_t dims[5];
   uint8_t* wpack;              // device, TcPlan layout (stock: layer 1 = private columns only)
-  float* bias;                 // device, [HID + HID + OUT_PAD]
+  float* bias;                 // device, [H1 | H2 | (H3) | OUT_PAD] (TcPlan::bias_off)
   uint8_t bias_nz;             // bit l: layer l has a non-zero bias (an all-zero bias is skipped)
   float* w1s_t;                // stock: device [S][HID] shared columns of W1 (exact bf16 values), else null
 };
@@ -116,11 +117,17 @@ int ensure_agg(fin_env* env, size_t rows) {
   return FIN_OK;
 }
 
-// network id from dims, -1 if not compiled
-int net_of(const int32_t* dims) {
-  if (dims[0] == 301 && dims[1] == 256 && dims[2] == 256 && dims[3] == 30) return 0;
-  if (dims[0] == 25 && dims[1] == 128 && dims[2] == 128 && dims[3] == 4) return 1;
-  if (dims[0] == 103 && dims[1] == 128 && dims[2] == 128 && (dims[3] == 3 || dims[3] == 4)) return 2;
+// network id from (n_layers, dims), -1 if not compiled
+int net_of(int n_layers, const int32_t* dims) {
+  if (n_layers == 3) {
+    if (dims[0] == 301 && dims[1] == 256 && dims[2] == 256 && dims[3] == 30) return 0;
+    if (dims[0] == 25 && dims[1] == 128 && dims[2] == 128 && dims[3] == 4) return 1;
+    if (dims[0] == 103 && dims[1] == 128 && dims[2] == 128 && (dims[3] == 3 || dims[3] == 4)) return 2;
+    if (dims[0] == 301 && dims[1] == 64 && dims[2] == 32 && dims[3] == 30) return 3;
+  }
+  if (n_layers == 4 && dims[0] == 103 && dims[1] == 128 && dims[2] == 128 && dims[3] == 128 &&
+      (dims[4] == 3 || dims[4] == 4))
+    return 4;
   return -1;
 }
 
@@ -158,8 +165,8 @@ void pack_member(const int32_t* dims, const uint16_t* const* w, const float* con
       }
   }
   bp.assign(Plan::kBiasFloats, 0.f);
-  for (int l = 0; l < 3; ++l) {
-    const int off = l == 0 ? 0 : (l == 1 ? Plan::kHid : 2 * Plan::kHid);
+  for (int l = 0; l < Plan::kNL; ++l) {
+    const int off = Plan::bias_off(l);
     if (bias && bias[l])
       for (int n = 0; n < dims[l + 1]; ++n) bp[off + n] = bias[l][n];
   }
@@ -454,36 +461,43 @@ int fin_policy_create(int32_t kind, int32_t n_layers, const int32_t* dims, const
   if (!dims || !w_bf16 || !out) return fail(FIN_E_CONFIG, "fin_policy_create: null argument");
   *out = nullptr;
   if (kind < FIN_PPO_GAUSS || kind > FIN_Q_DUELING) return fail(FIN_E_CONFIG, "unknown policy kind %d", kind);
-  if (n_layers != 3) return fail(FIN_E_UNSUPPORTED, "only 3-layer networks are compiled (got %d)", n_layers);
-  for (int l = 0; l < 3; ++l)
+  if (n_layers != 3 && n_layers != 4)
+    return fail(FIN_E_UNSUPPORTED, "only 3- and 4-layer networks are compiled (got %d)", n_layers);
+  for (int l = 0; l < n_layers; ++l)
     if (!w_bf16[l]) return fail(FIN_E_CONFIG, "weight %d is null", l);
-  const int net = net_of(dims);
+  const int net = net_of(n_layers, dims);
   if (net < 0)
     return fail(FIN_E_UNSUPPORTED,
-                "network %d-%d-%d-%d not compiled (have 301-256-256-30, 25-128-128-4, 103-128-128-3 / -4)", dims[0],
-                dims[1], dims[2], dims[3]);
+                "network %d-%d-%d-%d%s not compiled (have 301-256-256-30, 301-64-32-30, 25-128-128-4, "
+                "103-128-128-3 / -4, 103-128-128-128-3 / -4)",
+                dims[0], dims[1], dims[2], dims[3], n_layers == 4 ? "-.." : "");
   const bool qkind = kind == FIN_Q_ARGMAX || kind == FIN_Q_DUELING;
-  if ((net == 2) != qkind) return fail(FIN_E_CONFIG, "Q kinds pair with the 103-128-128 Q-nets");
-  if (kind == FIN_Q_ARGMAX && dims[3] != 3) return fail(FIN_E_CONFIG, "Q_ARGMAX needs 3 outputs");
-  if (kind == FIN_Q_DUELING && dims[3] != 4) return fail(FIN_E_CONFIG, "Q_DUELING needs 4 outputs (A0..A2, V)");
-  for (int l = 0; l < 3; ++l) {
+  const bool qnet = net == 2 || net == 4;
+  const int n_out = dims[n_layers];
+  if (qnet != qkind) return fail(FIN_E_CONFIG, "Q kinds pair with the 103-128-.. Q-nets");
+  if (kind == FIN_Q_ARGMAX && n_out != 3) return fail(FIN_E_CONFIG, "Q_ARGMAX needs 3 outputs");
+  if (kind == FIN_Q_DUELING && n_out != 4) return fail(FIN_E_CONFIG, "Q_DUELING needs 4 outputs (A0..A2, V)");
+  for (int l = 0; l < n_layers; ++l) {
     if (bias && bias[l] && !finite_all(bias[l], dims[l + 1])) return fail(FIN_E_DATA, "bias %d non-finite", l);
   }
   std::vector<uint8_t> wp;
   std::vector<float> bp, w1s;
   if (net == 0) pack_member<PlanStockC1, ObsC1>(dims, w_bf16, bias, wp, bp, &w1s);
   else if (net == 1) pack_member<PlanStockSmall, ObsSmall>(dims, w_bf16, bias, wp, bp, &w1s);
+  else if (net == 3) pack_member<PlanStockPaper, ObsC1>(dims, w_bf16, bias, wp, bp, &w1s);
+  else if (net == 4) pack_member<PlanCryptoPaper, void>(dims, w_bf16, bias, wp, bp, nullptr);
   else pack_member<PlanCrypto, void>(dims, w_bf16, bias, wp, bp, nullptr);
   fin_policy* pol = new (std::nothrow) fin_policy();
   if (!pol) return fail(FIN_E_CONFIG, "out of host memory");
   pol->kind = kind;
   pol->net = net;
+  pol->n_layers = n_layers;
   pol->bias_nz = 0;
-  for (int l = 0; l < 3; ++l)
+  for (int l = 0; l < n_layers; ++l)
     if (bias && bias[l])
       for (int n = 0; n < dims[l + 1]; ++n)
         if (bias[l][n] != 0.f) pol->bias_nz |= 1u << l;
-  for (int l = 0; l < 4; ++l) pol->dims[l] = dims[l];
+  for (int l = 0; l < 5; ++l) pol->dims[l] = l <= n_layers ? dims[l] : 0;
   cudaError_t e = cudaMalloc(&pol->wpack, wp.size());
   if (e == cudaSuccess) e = cudaMalloc(&pol->bias, bp.size() * sizeof(float));
   if (e == cudaSuccess && !w1s.empty()) e = cudaMalloc(&pol->w1s_t, w1s.size() * sizeof(float));
@@ -555,13 +569,13 @@ int fill_members(fin_env* env, const fin_policy* const* members, int32_t n, cons
     if (rc != FIN_OK) return rc;
   }
   if (env->d.task == FIN_STOCK) {
-    if (net == 2) return fail(FIN_E_CONFIG, "stock env needs a stock policy");
-    const int need_k = net == 0 ? 30 : 4, need_i = net == 0 ? 8 : 4;
+    if (net == 2 || net == 4) return fail(FIN_E_CONFIG, "stock env needs a stock policy");
+    const int need_k = net == 1 ? 4 : 30, need_i = net == 1 ? 4 : 8;
     if (env->d.K != need_k || env->d.I != need_i)
       return fail(FIN_E_UNSUPPORTED, "policy network expects K=%d, I=%d; env has K=%d, I=%d", need_k, need_i,
                   env->d.K, env->d.I);
   } else {
-    if (net != 2) return fail(FIN_E_CONFIG, "crypto env takes Q_ARGMAX / Q_DUELING members");
+    if (net != 2 && net != 4) return fail(FIN_E_CONFIG, "crypto env takes Q_ARGMAX / Q_DUELING members");
     if (member_w) return fail(FIN_E_CONFIG, "crypto ensembles vote: member_w must be NULL");
   }
   p.M = n;
@@ -637,7 +651,7 @@ int fin_rollout(fin_env* env, const fin_policy* const* members, int32_t n_member
   env->last_stream = S(stream);
   int tiles = 1;
   cudaError_t e = env->d.task == FIN_STOCK ? fin::launch_stock_rollout(net, p, env->d.N, &tiles, S(stream))
-                                           : fin::launch_crypto_rollout(p, env->d.N, &tiles, S(stream));
+                                           : fin::launch_crypto_rollout(net, p, env->d.N, &tiles, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fin_rollout launch");
   if (out && out->agg) {
     const int rows = (env->d.N + tc::kTileM * tiles - 1) / (tc::kTileM * tiles) * tiles;
@@ -736,7 +750,7 @@ int fin_mlp_forward(const fin_policy* pol, const uint16_t* x, int32_t B, float* 
   p.hid_out = hidden;
   p.B = B;
   p.in_dim = pol->dims[0];
-  p.out_dim = pol->dims[3];
+  p.out_dim = pol->dims[pol->n_layers];
   float* z1s = nullptr;
   cudaStream_t s = S(stream);
   cudaError_t e = cudaSuccess;

@@ -43,9 +43,12 @@ __device__ __forceinline__ void bar_sync128(int bar_id) {
   asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
 }
 
+// Plan: PlanCrypto (BASELINE configs[3]: 103-128-128-3/-4) or PlanCryptoPaper (the
+// paper's three 128-unit hidden layers); both take the same 112-wide input.
+template <class Plan>
 struct CryptoOps {
   static constexpr int IN = 2 + FIN_C_FACTORS;  // 103
-  static constexpr int KT8 = PlanCrypto::kIn / 8;
+  static constexpr int KT8 = Plan::kIn / 8;
   static constexpr int kOffX = 0;                               // bf16 obs row (112)
   static constexpr int kOffR = 256;                             // ring of 3 rows (3 x 144 floats)
   static constexpr int kOffT = kOffR + 3 * FIN_C_ROW * 4;
@@ -122,7 +125,7 @@ struct CryptoOps {
       const float* mrow = ring + st.slot_t * FIN_C_ROW;
       uint16_t* xs = reinterpret_cast<uint16_t*>(stg + kOffX);
       bar_sync128(bar_id);   // ring rows visible
-      for (int idx = gtid; idx < PlanCrypto::kIn; idx += 128)
+      for (int idx = gtid; idx < Plan::kIn; idx += 128)
         xs[idx] = (idx >= 2 && idx < IN) ? (uint16_t)bf16_bits(mrow[FIN_C_F0 + idx - 2]) : (uint16_t)0;
       // prefetch row t0 + 2 (the next step's marking row) into the third slot
       const int r2 = t0 + 2;
@@ -189,7 +192,7 @@ struct CryptoOps {
   __device__ __forceinline__ static uint16_t* hidden_ptr(State& st, const TcParams& p, int env, int t, int m, int l,
                                                          int hid) {
     if (!st.live || !p.o.mlp_hidden) return nullptr;
-    return p.o.mlp_hidden + ((((size_t)t * p.M + m) * p.e.N + env) * 2 + l) * hid;
+    return p.o.mlp_hidden + ((((size_t)t * p.M + m) * p.e.N + env) * Plan::kNH + l) * hid;
   }
 
   __device__ __forceinline__ static void prepare(State&, const TcParams&, int, int, int) {}
@@ -296,20 +299,28 @@ int num_sms();
 
 // The C3 loop is latency-bound (one lockstep step at a time): spread tiles over the
 // SMs first (one tile per CTA); pair tiles per CTA only when tiles outnumber SMs.
-cudaError_t launch_crypto_rollout(const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s) {
+template <class Plan>
+cudaError_t launch_crypto_plan(const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s) {
+  using Ops = CryptoOps<Plan>;
   const int n_tiles = (n_envs + tc::kTileM - 1) / tc::kTileM;
   const bool two = n_tiles > num_sms();
   *tiles = two ? 2 : 1;
-  // the Q-nets stay resident in shared memory while they fit (60 KB each); a larger
-  // voting ensemble (9 or 30 members) streams them like the stock nets
+  // the Q-nets stay resident in shared memory while they fit (60 KB each, 92 KB for the
+  // paper's 3 x 128 net); a larger voting ensemble (9 or 30 members)
+  // streams them like the stock nets
   if (two) {
-    if (p.M <= tc::Smem<PlanCrypto, true, 2, CryptoOps>::max_members())
-      return tc::launch<PlanCrypto, true, 2, CryptoOps>(p, n_envs, s);
-    return tc::launch<PlanCrypto, false, 2, CryptoOps>(p, n_envs, s);
+    if (p.M <= tc::Smem<Plan, true, 2, Ops>::max_members()) return tc::launch<Plan, true, 2, Ops>(p, n_envs, s);
+    return tc::launch<Plan, false, 2, Ops>(p, n_envs, s);
   }
-  if (p.M <= tc::Smem<PlanCrypto, true, 1, CryptoOps>::max_members())
-    return tc::launch<PlanCrypto, true, 1, CryptoOps>(p, n_envs, s);
-  return tc::launch<PlanCrypto, false, 1, CryptoOps>(p, n_envs, s);
+  if (p.M <= tc::Smem<Plan, true, 1, Ops>::max_members()) return tc::launch<Plan, true, 1, Ops>(p, n_envs, s);
+  return tc::launch<Plan, false, 1, Ops>(p, n_envs, s);
+}
+
+// net: 2 = PlanCrypto, 4 = PlanCryptoPaper
+cudaError_t launch_crypto_rollout(int net, const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s) {
+  if (net == 2) return launch_crypto_plan<PlanCrypto>(p, n_envs, tiles, s);
+  if (net == 4) return launch_crypto_plan<PlanCryptoPaper>(p, n_envs, tiles, s);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace fin

@@ -61,7 +61,7 @@ struct StockOps {
   // its window after a reset -- envs of a tile step in lockstep).
   static constexpr int kOffP = 0;
   static constexpr int kOffZ = kPriceRows * KP4 * 8;
-  static constexpr int kRegion = kOffZ + FIN_STAGE_MEMBERS * Plan::kHid * 4;
+  static constexpr int kRegion = kOffZ + FIN_STAGE_MEMBERS * Plan::kH1 * 4;
   static constexpr int kOffS = 2 * kRegion;
   static constexpr int kOffB = kOffS + 16;
   static constexpr int kStageBytes = kOffB + 16;
@@ -130,9 +130,9 @@ struct StockOps {
     const EnvDev& e = p.e;
     stage_price_rows(e, reinterpret_cast<double*>(reg + kOffP), k, gtid, 128);
     float* zs = reinterpret_cast<float*>(reg + kOffZ);
-    for (int j = gtid; j < min(p.M, FIN_STAGE_MEMBERS) * Plan::kHid; j += 128) {
-      const int m = j / Plan::kHid, n = j % Plan::kHid;
-      zs[j] = __ldg(p.z1s + ((size_t)m * p.z1s_rows + k) * Plan::kHid + n);
+    for (int j = gtid; j < min(p.M, FIN_STAGE_MEMBERS) * Plan::kH1; j += 128) {
+      const int m = j / Plan::kH1, n = j % Plan::kH1;
+      zs[j] = __ldg(p.z1s + ((size_t)m * p.z1s_rows + k) * Plan::kH1 + n);
     }
   }
   // the same rows by cp.async (16-byte chunks, no wait): completed by the next stage()
@@ -141,11 +141,11 @@ struct StockOps {
     const int np = kPriceRows * e.kp / 2;                 // 16-B chunks of the price rows
     const uint8_t* src = reinterpret_cast<const uint8_t*>(e.px + (size_t)k * kPriceRows * e.kp);
     for (int j = gtid; j < np; j += 128) sm100::cp_async16(reg + kOffP + 16 * j, src + 16 * j);
-    constexpr int nz = Plan::kHid / 4;                   // chunks per member z1s row
+    constexpr int nz = Plan::kH1 / 4;                   // chunks per member z1s row
     for (int j = gtid; j < min(p.M, FIN_STAGE_MEMBERS) * nz; j += 128) {
       const int m = j / nz, c = j % nz;
-      sm100::cp_async16(reg + kOffZ + (m * Plan::kHid + 4 * c) * 4,
-                        p.z1s + ((size_t)m * p.z1s_rows + k) * Plan::kHid + 4 * c);
+      sm100::cp_async16(reg + kOffZ + (m * Plan::kH1 + 4 * c) * 4,
+                        p.z1s + ((size_t)m * p.z1s_rows + k) * Plan::kH1 + 4 * c);
     }
     sm100::cp_async_commit();
   }
@@ -209,8 +209,8 @@ struct StockOps {
 
   // factored layer 1: the shared-input term of this env's day, member m
   __device__ __forceinline__ static const float* l1_addend(State& st, const TcParams& p, int m, uint8_t* stg) {
-    if (st.zsm && m < FIN_STAGE_MEMBERS) return reinterpret_cast<const float*>(region(stg, st.sb) + kOffZ) + m * Plan::kHid;
-    return p.z1s + ((size_t)m * p.z1s_rows + st.d) * Plan::kHid;
+    if (st.zsm && m < FIN_STAGE_MEMBERS) return reinterpret_cast<const float*>(region(stg, st.sb) + kOffZ) + m * Plan::kH1;
+    return p.z1s + ((size_t)m * p.z1s_rows + st.d) * Plan::kH1;
   }
 
   // the env-private observation entries [b/b0, h_k/max_trade, 0 pad] -> X (bf16)
@@ -246,7 +246,7 @@ struct StockOps {
   __device__ __forceinline__ static uint16_t* hidden_ptr(State& st, const TcParams& p, int env, int t, int m, int l,
                                                          int hid) {
     if (!st.live || !p.o.mlp_hidden) return nullptr;
-    return p.o.mlp_hidden + ((((size_t)t * p.M + m) * p.e.N + env) * 2 + l) * hid;
+    return p.o.mlp_hidden + ((((size_t)t * p.M + m) * p.e.N + env) * Plan::kNH + l) * hid;
   }
 
   // the member's noise for this step: Philox4x32-10 + Box-Muller (R-NOISE) or the
@@ -452,7 +452,7 @@ struct ProbeOps {
   __device__ __forceinline__ static const float* l1_addend(State& st, const TcParams& p, int m, uint8_t*) {
     // never null for a factored net (the epilogue's addend branch must be warp-uniform):
     // rows past B read row 0 and their outputs are dropped
-    if constexpr (kFactored) return p.z1s + (size_t)(st.b < p.B ? st.b : 0) * Plan::kHid;
+    if constexpr (kFactored) return p.z1s + (size_t)(st.b < p.B ? st.b : 0) * Plan::kH1;
     else return nullptr;
   }
   __device__ __forceinline__ static void build_obs(State& st, const TcParams& p, int env, int row, int t, int m,
@@ -476,7 +476,7 @@ struct ProbeOps {
   __device__ __forceinline__ static uint16_t* hidden_ptr(State& st, const TcParams& p, int env, int t, int m, int l,
                                                          int hid) {
     if (st.b >= p.B || !p.hid_out) return nullptr;
-    return p.hid_out + ((size_t)st.b * 2 + l) * hid;
+    return p.hid_out + ((size_t)st.b * Plan::kNH + l) * hid;
   }
   __device__ __forceinline__ static void prepare(State&, const TcParams&, int, int, int) {}
   __device__ __forceinline__ static void consume(State& st, const TcParams& p, int env, int t, int m,
@@ -534,22 +534,28 @@ cudaError_t launch_auto(const TcParams& p, int n_envs, int* tiles, cudaStream_t 
   return tc::launch<Plan, RES, 1, Ops>(p, n_envs, s);
 }
 
-// net: 0 = PlanStockC1 (K=30, I=8), 1 = PlanStockSmall (K=4, I=4)
+// net: 0 = PlanStockC1 (K=30, I=8), 1 = PlanStockSmall (K=4, I=4), 3 = PlanStockPaper (K=30, I=8;
+// the paper's 64-32 net, 10 KB of weights: resident in shared memory, env-issued MMAs)
 cudaError_t launch_stock_rollout(int net, const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s) {
   const bool single = p.M == 1 && p.kinds[0] != FIN_DDPG_OU;
   if (net == 0 && single)
     return launch_auto<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false>>(p, n_envs, tiles, s);
   if (net == 0) return launch_auto<PlanStockC1, false, StockOps<30, 8, PlanStockC1, true>>(p, n_envs, tiles, s);
+  if (net == 3 && single)
+    return launch_auto<PlanStockPaper, true, StockOps<30, 8, PlanStockPaper, false>>(p, n_envs, tiles, s);
+  if (net == 3) return launch_auto<PlanStockPaper, true, StockOps<30, 8, PlanStockPaper, true>>(p, n_envs, tiles, s);
   if (net == 1) return launch_auto<PlanStockSmall, true, StockOps<4, 4, PlanStockSmall, true>>(p, n_envs, tiles, s);
   return cudaErrorInvalidValue;
 }
 
-// net: 0 = PlanStockC1, 1 = PlanStockSmall, 2 = PlanCrypto
+// net: 0 = PlanStockC1, 1 = PlanStockSmall, 2 = PlanCrypto, 3 = PlanStockPaper, 4 = PlanCryptoPaper
 cudaError_t launch_mlp_probe(int net, const tc::TcParams& p, int n_rows, cudaStream_t s) {
   int tiles = 0;
   if (net == 0) return launch_auto<PlanStockC1, false, ProbeOps<PlanStockC1, ObsC1>>(p, n_rows, &tiles, s);
   if (net == 1) return launch_auto<PlanStockSmall, true, ProbeOps<PlanStockSmall, ObsSmall>>(p, n_rows, &tiles, s);
   if (net == 2) return launch_auto<PlanCrypto, true, ProbeOps<PlanCrypto, void>>(p, n_rows, &tiles, s);
+  if (net == 3) return launch_auto<PlanStockPaper, true, ProbeOps<PlanStockPaper, ObsC1>>(p, n_rows, &tiles, s);
+  if (net == 4) return launch_auto<PlanCryptoPaper, true, ProbeOps<PlanCryptoPaper, void>>(p, n_rows, &tiles, s);
   return cudaErrorInvalidValue;
 }
 

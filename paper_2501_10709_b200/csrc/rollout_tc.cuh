@@ -89,7 +89,7 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
 // sized for the launch's member count.
 template <class Plan, bool RESIDENT, int TILES, class Ops, int RING = kRing>
 struct Smem {
-  static constexpr int kA = kTileM * (Plan::kIn > Plan::kHid ? Plan::kIn : Plan::kHid) * 2;  // per tile
+  static constexpr int kA = kTileM * (Plan::kIn > Plan::kHidMax ? Plan::kIn : Plan::kHidMax) * 2;  // per tile
   static constexpr int kFixed = TILES * kA + TILES * Ops::kStageBytes + 512;  // + barriers, flags
   static constexpr int kBiasPerMember = Plan::kBiasFloats * 4;
   static constexpr int kStaticSmem = 512;  // agg_group_write scratch etc.
@@ -132,8 +132,9 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
   const int M = p.M;
   const int T = p.T;
   constexpr int NS = Plan::kStages;
-  constexpr uint32_t kTmemCols = (TILES * Plan::kHid <= 128) ? 128 : (TILES * Plan::kHid <= 256 ? 256 : 512);
-  static_assert(TILES * Plan::kHid <= 512, "TMEM holds 512 fp32 columns");
+  constexpr int kTc = Plan::kHidMax > Plan::kOut ? Plan::kHidMax : Plan::kOut;   // TMEM columns per tile
+  constexpr uint32_t kTmemCols = (TILES * kTc <= 128) ? 128 : (TILES * kTc <= 256 ? 256 : 512);
+  static_assert(TILES * kTc <= 512, "TMEM holds 512 fp32 columns");
 
   uint8_t* sA = smem;                                           // TILES x kA
   uint8_t* sStage = sA + TILES * S::kA;                         // TILES x Ops::kStageBytes
@@ -203,7 +204,8 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
         uint32_t it = 0;
         for (int t = 0; t < T; ++t)
           for (int m = 0; m < M; ++m)
-            for (int s = 0; s < NS; ++s, ++it) {
+#pragma unroll
+            for (int s = 0; s < NS; ++s, ++it) {   // unrolled: per-stage plan values fold to constants
               const uint32_t slot = it % RING, ph = (it / RING) & 1;
               sm100::mbar_wait_fast(&w_empty[slot], ph ^ 1);
               FIN_TR(m == 0 && (s == 0 || s == NS - 1), t, s == 0 ? 30 : 31);
@@ -223,14 +225,15 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
       const uint32_t aa = sm100::smem_u32(sA), wa = sm100::smem_u32(sW);
       for (int t = 0; t < T; ++t) {
         for (int m = 0; m < M; ++m) {
-#pragma unroll 1
-          for (int l = 0; l < 3; ++l) {
+#pragma unroll
+          for (int l = 0; l < Plan::kNL; ++l) {
             sm100::mbar_wait_fast(a_full, a_use & 1);
             ++a_use;
             FIN_TR(m == 0, t, 9 + 2 * l);
             sm100::tc_fence_after();
             const uint32_t a_sbo = (uint32_t)(Plan::kdim(l) / 8) * 128u;
             const uint32_t idesc = sm100::make_idesc_bf16(kTileM, Plan::nrows(l));
+#pragma unroll
             for (int s = Plan::first_stage(l); s < Plan::first_stage(l) + Plan::nstages(l); ++s) {
               uint32_t b_base;
               if (RESIDENT) {
@@ -250,7 +253,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
 #pragma unroll
               for (int tile = 0; tile < TILES; ++tile) {
                 const uint32_t a_base = aa + (uint32_t)(tile * S::kA);
-                const uint32_t d_tmem = tmem + (uint32_t)(tile * Plan::kHid);
+                const uint32_t d_tmem = tmem + (uint32_t)(tile * kTc);
                 // descriptors of k-step 0; each further k-step advances both start
                 // addresses by 256 B = 16 units of the descriptor's address field
                 const uint64_t ad0 = sm100::make_sdesc(a_base + (uint32_t)j0 * 256u, 128u, a_sbo);
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
     const int row = q * 32 + lane;          // env row of the tile == TMEM lane
     const int gtid = (warp - 4 - tile * 4) * 32 + lane;   // thread index within the tile's warpgroup
     const int env = (blockIdx.x * TILES + tile) * kTileM + row;
-    const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tile * Plan::kHid);
+    const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tile * kTc);
     const uint32_t xa = sm100::smem_u32(sA + tile * S::kA);
     uint8_t* stg = sStage + tile * Ops::kStageBytes;
     const int bar_id = 1 + tile;
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
           const uint32_t a_sbo = (uint32_t)(Plan::kdim(l) / 8) * 128u;
           const uint32_t idesc = sm100::make_idesc_bf16(kTileM, Plan::nrows(l));
           const uint32_t a_base = sm100::smem_u32(sA) + (uint32_t)(tile * S::kA);
-          const uint32_t d_tmem = tmem + (uint32_t)(tile * Plan::kHid);
+          const uint32_t d_tmem = tmem + (uint32_t)(tile * kTc);
           for (int s = Plan::first_stage(l); s < Plan::first_stage(l) + Plan::nstages(l); ++s) {
             const uint32_t b_base = sm100::smem_u32(sW) + (uint32_t)(m * Plan::kMemberBytes + Plan::offset_of(s));
             const int j0 = Plan::j0_of(s), nks = Plan::nks_of(s);
@@ -333,23 +336,27 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
         const float* bias = m < FIN_STAGE_MEMBERS ? sBias + m * Plan::kBiasFloats : p.bias[m];
         // hidden layers: D -> +bias -> ReLU -> bf16 -> A (K-major core matrices)
 #pragma unroll 1
-        for (int l = 0; l < 2; ++l) {
+        for (int l = 0; l < Plan::kNH; ++l) {
           sm100::mbar_wait(&d_full[tile], d_use & 1);
           ++d_use;
           FIN_TR(row == 0 && tile == 0 && m == 0, t, 2 + 2 * l);
           sm100::tc_fence_after();
-          const float* bl = ((p.bias_nz[m] >> l) & 1u) ? bias + l * Plan::kHid : nullptr;
+          const float* bl = ((p.bias_nz[m] >> l) & 1u) ? bias + Plan::bias_off(l) : nullptr;
+          // this layer's width = the next layer's K (a compile-time constant when all hidden
+          // layers have one width, as in the BASELINE nets: the runtime bound cost ~10%)
+          constexpr bool kUniformHid = Plan::hid(0) == Plan::hid(1) && (Plan::kNH < 3 || Plan::hid(2) == Plan::hid(0));
+          const int ncol = kUniformHid ? Plan::kH1 : Plan::nrows(l);
           // factored layer 1: + shared-input term of the env's day (smem or global row)
           const float* add = l == 0 ? Ops::l1_addend(st, p, m, stg) : nullptr;
           // debug / parity log of the bf16 hidden activations (teacher-forced layer checks)
-          uint4* hlog = reinterpret_cast<uint4*>(Ops::hidden_ptr(st, p, env, t, m, l, Plan::kHid));
+          uint4* hlog = reinterpret_cast<uint4*>(Ops::hidden_ptr(st, p, env, t, m, l, Plan::kHidMax));
           // 16 columns per TMEM load: half the registers of 32-column chunks (the env
           // state lives in registers across the whole rollout).  One loop per addend
           // combination (uniform branch), so an absent addend costs no issue slots.
           auto epilogue = [&](auto has_b, auto has_add) {
             constexpr bool HB = decltype(has_b)::value, HA = decltype(has_add)::value;
 #pragma unroll 1
-            for (int c = 0; c < Plan::kHid / 16; ++c) {
+            for (int c = 0; c < ncol / 16; ++c) {
               uint32_t v[16];
               sm100::tmem_ld16(t_lane + (uint32_t)(c * 16), v);
               // addend b (+ z1s for the factored layer 1), 128-bit broadcast loads, issued
@@ -381,7 +388,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
               }
 #pragma unroll
               for (int g = 0; g < 2; ++g)
-                sts128(xa + cm_off(row, c * 2 + g, Plan::kHid / 8), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2],
+                sts128(xa + cm_off(row, c * 2 + g, ncol / 8), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2],
                        pk[4 * g + 3]);
               if (hlog) {
 #pragma unroll
@@ -414,9 +421,10 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
           uint32_t v[16];
           sm100::tmem_ld16(t_lane + (uint32_t)(c * 16), v);
           sm100::tmem_wait_ld();
-          if ((p.bias_nz[m] >> 2) & 1u) {
+          if ((p.bias_nz[m] >> Plan::kNH) & 1u) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) z[c * 16 + j] = __uint_as_float(v[j]) + bias[2 * Plan::kHid + c * 16 + j];
+            for (int j = 0; j < 16; ++j)
+              z[c * 16 + j] = __uint_as_float(v[j]) + bias[Plan::bias_off(Plan::kNH) + c * 16 + j];
           } else {
 #pragma unroll
             for (int j = 0; j < 16; ++j) z[c * 16 + j] = __uint_as_float(v[j]);

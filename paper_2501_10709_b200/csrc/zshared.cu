@@ -58,9 +58,9 @@ __global__ void k_z1s_probe(const float* __restrict__ w1s_t, int H, const uint16
 
 namespace fin {
 
-// net 0 = C1 (K=30, I=8), net 1 = small (K=4, I=4)
+// net 0 = C1 (K=30, I=8), 3 = the paper's 301-64-32-30 on the C1 env, net 1 = small (K=4, I=4)
 cudaError_t launch_z1s_market(int net, const float* w1s_t, int H, const EnvDev& e, float* z1s, cudaStream_t s) {
-  if (net == 0) k_z1s_market<ObsC1><<<e.rows, 256, 0, s>>>(w1s_t, H, e.market, e.row_floats, e.kp, z1s);
+  if (net == 0 || net == 3) k_z1s_market<ObsC1><<<e.rows, 256, 0, s>>>(w1s_t, H, e.market, e.row_floats, e.kp, z1s);
   else if (net == 1) k_z1s_market<ObsSmall><<<e.rows, 128, 0, s>>>(w1s_t, H, e.market, e.row_floats, e.kp, z1s);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
@@ -68,7 +68,7 @@ cudaError_t launch_z1s_market(int net, const float* w1s_t, int H, const EnvDev& 
 
 cudaError_t launch_z1s_probe(int net, const float* w1s_t, int H, const uint16_t* x, int B, int in_dim, float* z1s,
                              cudaStream_t s) {
-  if (net == 0) k_z1s_probe<ObsC1><<<B, 256, 0, s>>>(w1s_t, H, x, in_dim, z1s);
+  if (net == 0 || net == 3) k_z1s_probe<ObsC1><<<B, 256, 0, s>>>(w1s_t, H, x, in_dim, z1s);
   else if (net == 1) k_z1s_probe<ObsSmall><<<B, 128, 0, s>>>(w1s_t, H, x, in_dim, z1s);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();

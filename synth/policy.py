@@ -13,6 +13,10 @@ import numpy as np
 
 STOCK_DIMS = (301, 256, 256, 30)
 CRYPTO_DIMS = (103, 128, 128, 3)
+# the paper's own networks (two hidden layers of 64 and 32 units;
+# three 128-unit hidden layers), built as the NEXT-3 / NEXT-2 variants
+STOCK_PAPER_DIMS = (301, 64, 32, 30)
+CRYPTO_PAPER_DIMS = (103, 128, 128, 128, 3)
 
 
 def f64_to_bf16_bits(x: np.ndarray) -> np.ndarray:

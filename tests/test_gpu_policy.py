@@ -51,8 +51,20 @@ def _mlp_close(g, o, rel=2e-3, strict=False):
     assert np.mean(ratio > rel) <= 1e-2 or (ratio > rel).sum() <= 1, f"{(ratio > rel).sum()} rows outside {rel}"
 
 
+def _kind_for(fin, dims):
+    if dims[0] != 103:
+        return fin.FIN_PPO_GAUSS
+    return fin.FIN_Q_ARGMAX if dims[-1] == 3 else fin.FIN_Q_DUELING
+
+
+def _hid_shape(dims):
+    """(hidden layers, widest hidden layer) of the device's hidden-activation log."""
+    return len(dims) - 2, max(dims[1:-1])
+
+
 # ------------------------------------------------------------------ K7 standalone MLP
-@pytest.mark.parametrize("dims", [(301, 256, 256, 30), (25, 128, 128, 4), (103, 128, 128, 3)])
+@pytest.mark.parametrize("dims", [(301, 256, 256, 30), (25, 128, 128, 4), (103, 128, 128, 3), (301, 64, 32, 30),
+                                  (103, 128, 128, 128, 3), (103, 128, 128, 128, 4)])
 def test_mlp_dyadic_bit_exact(dims):
     """Dyadic weights / inputs: every product and partial sum is exact in fp32, so the
     tcgen05 result must equal the oracle bit for bit -- this pins the smem
@@ -66,8 +78,7 @@ def test_mlp_dyadic_bit_exact(dims):
         w = rng.choice(vals, (fo, fi))
         b = rng.choice(np.array([0.0, 0.25, -0.75]), fo).astype(np.float32)
         layers.append((spol.f64_to_bf16_bits(w), b))
-    kind = fin.FIN_Q_ARGMAX if dims[0] == 103 else fin.FIN_PPO_GAUSS
-    pol = fin.fin_policy_create(kind, layers)
+    pol = fin.fin_policy_create(_kind_for(fin, dims), layers)
     B = 300
     x = rng.choice(np.array([0.0, 0.5, -0.5, 1.0, -1.0, 0.25]), (B, dims[0]))
     xb = spol.f64_to_bf16_bits(x).view(np.int16)
@@ -77,19 +88,18 @@ def test_mlp_dyadic_bit_exact(dims):
     assert np.array_equal(host(z).astype(np.float64), o)
 
 
-@pytest.mark.parametrize("dims", [(301, 256, 256, 30), (103, 128, 128, 3)])
+@pytest.mark.parametrize("dims", [(301, 256, 256, 30), (103, 128, 128, 3), (301, 64, 32, 30), (103, 128, 128, 128, 3)])
 def test_mlp_kaiming_rel_2e3(dims):
     import torch
     fin = _fin()
     layers = spol.random_bias(spol.kaiming_bf16(dims, 0), 99)
-    kind = fin.FIN_Q_ARGMAX if dims[0] == 103 else fin.FIN_PPO_GAUSS
-    pol = fin.fin_policy_create(kind, layers)
+    pol = fin.fin_policy_create(_kind_for(fin, dims), layers)
     rng = np.random.default_rng(1)
     B = 1000
     x = rng.standard_normal((B, dims[0])) * 2.0
     xq = omlp.bf16_bits_to_f64(spol.f64_to_bf16_bits(x))
     z = zeros((B, dims[-1]), torch.float32)
-    hid = zeros((B, 2, dims[1]), torch.int16)
+    hid = zeros((B, *_hid_shape(dims)), torch.int16)
     fin.fin_mlp_forward(pol, dev(spol.f64_to_bf16_bits(x).view(np.int16)), z, hid)
     L64 = omlp.layers_f64(layers)
     amb, tot = omlp.teacher_forced_layers(L64, xq, host(hid), host(z))
@@ -98,7 +108,7 @@ def test_mlp_kaiming_rel_2e3(dims):
 
 
 # ------------------------------------------------------------------ fused stock rollout
-def _stock_fused(N, T, members_spec, L, rows=150, seed_noise=23, **env_kw):
+def _stock_fused(N, T, members_spec, L, rows=150, seed_noise=23, dims=spol.STOCK_DIMS, **env_kw):
     """Run fin_rollout with supplied noise; return logs + the oracle pieces."""
     import torch
     fin = _fin()
@@ -110,7 +120,7 @@ def _stock_fused(N, T, members_spec, L, rows=150, seed_noise=23, **env_kw):
     kw["num_windows"] = (rows - 1 - L - kw.get("window_offset", 0)) // 5 + 1
     ocfg, fcfg = stock_pair(**kw)
     env = fin.fin_env_create(fcfg, m.market)
-    layers = [spol.kaiming_bf16(spol.STOCK_DIMS, s) for s, _ in members_spec]
+    layers = [spol.kaiming_bf16(dims, s) for s, _ in members_spec]
     kinds = [k for _, k in members_spec]
     pols = [fin.fin_policy_create(k, L_) for k, L_ in zip(kinds, layers)]
     M = len(pols)
@@ -119,7 +129,7 @@ def _stock_fused(N, T, members_spec, L, rows=150, seed_noise=23, **env_kw):
     logs = dict(reward=zeros((T, N), torch.float32), done=zeros((T, N), torch.uint8),
                 actions=zeros((T, N, K), torch.int16), cash=zeros((T, N), torch.float64),
                 hold=zeros((T, N, K), torch.int16), asset=zeros((T, N), torch.float64),
-                mlp_out=zeros((T, M, N, K), torch.float32), mlp_hidden=zeros((T, M, N, 2, 256), torch.int16),
+                mlp_out=zeros((T, M, N, K), torch.float32), mlp_hidden=zeros((T, M, N, *_hid_shape(dims)), torch.int16),
                 ep_metrics=zeros((E, N, 3), torch.float64),
                 ep_count=zeros(N, torch.int32), agg=zeros(8, torch.float64))
     fin.fin_rollout(env, pols, T, fin.make_noise(fin.FIN_NOISE_SUPPLIED, 0, dev(noise)), fin.make_traj(**logs))
@@ -187,6 +197,23 @@ def test_fused_c2_ensemble_teacher_forced():
     spec = [(1, fin.FIN_PPO_GAUSS), (2, fin.FIN_SAC_SQUASH), (3, fin.FIN_DDPG_OU)]
     g, ocfg, mk, layers, kinds, noise = _stock_fused(200, 12, spec, L=5, window_offset=30,
                                                      advance_window_on_reset=True, seed_noise=33)
+    _teacher_forced_stock(g, ocfg, mk, layers, kinds, noise)
+
+
+def test_fused_paper_net_rollout_teacher_forced():
+    """The paper's own stock policy net (hidden layers of 64 and 32 units) on the
+    C1 env: 10 KB of weights resident in shared memory, env-issued tcgen05 MMAs; a single
+    PPO member over a reset (N=300, T=35), then the PPO / SAC / DDPG ensemble on 5-day
+    test windows."""
+    fin = _fin()
+    g, ocfg, mk, layers, kinds, noise = _stock_fused(300, 35, [(0, fin.FIN_PPO_GAUSS)], L=30,
+                                                     dims=spol.STOCK_PAPER_DIMS)
+    _teacher_forced_stock(g, ocfg, mk, layers, kinds, noise)
+    assert g["agg"][fin.FIN_AGG_EPISODES] == 300
+    spec = [(1, fin.FIN_PPO_GAUSS), (2, fin.FIN_SAC_SQUASH), (3, fin.FIN_DDPG_OU)]
+    g, ocfg, mk, layers, kinds, noise = _stock_fused(200, 12, spec, L=5, window_offset=30,
+                                                     advance_window_on_reset=True, seed_noise=33,
+                                                     dims=spol.STOCK_PAPER_DIMS)
     _teacher_forced_stock(g, ocfg, mk, layers, kinds, noise)
 
 
@@ -311,9 +338,11 @@ def test_ensemble_act_matches_rollout_first_step():
 
 
 # ------------------------------------------------------------------ crypto Q rollout
-def test_fused_crypto_rollout_teacher_forced():
-    """BASELINE configs[3] shape on a short series: Q-net 103-128-128-3, argmax,
-    epsilon-greedy 0.005 with supplied uniforms, position +-1, max hold 120."""
+@pytest.mark.parametrize("dims", [spol.CRYPTO_DIMS, spol.CRYPTO_PAPER_DIMS])
+def test_fused_crypto_rollout_teacher_forced(dims):
+    """BASELINE configs[3] shape on a short series: Q-net 103-128-128-3 (and the paper's
+    three 128-unit hidden layers), argmax, epsilon-greedy 0.005 with supplied
+    uniforms, position +-1, max hold 120."""
     import torch
     fin = _fin()
     T, N = 400, 300
@@ -323,13 +352,13 @@ def test_fused_crypto_rollout_teacher_forced():
     fcfg = fin.env_config(task=fin.FIN_CRYPTO, num_envs=N, num_assets=1, num_indicators=0, num_rows=T + 1,
                           episode_len=T, reward_scale=1.0, cost_rate=0.0, epsilon=eps)
     env = fin.fin_env_create(fcfg, rows)
-    layers = spol.random_bias(spol.kaiming_bf16(spol.CRYPTO_DIMS, 4), 5)
+    layers = spol.random_bias(spol.kaiming_bf16(dims, 4), 5)
     pol = fin.fin_policy_create(fin.FIN_Q_ARGMAX, layers)
     uni = inputs.crypto_uniforms(T, N, seed=43)
     logs = dict(actions=zeros((T, N, 1), torch.int16), hold=zeros((T, N, 1), torch.int16),
                 cash=zeros((T, N), torch.float64), asset=zeros((T, N), torch.float64),
                 reward=zeros((T, N), torch.float32), done=zeros((T, N), torch.uint8),
-                mlp_out=zeros((T, N, 3), torch.float32), mlp_hidden=zeros((T, N, 2, 128), torch.int16),
+                mlp_out=zeros((T, N, 3), torch.float32), mlp_hidden=zeros((T, N, *_hid_shape(dims)), torch.int16),
                 ep_metrics=zeros((2, N, 3), torch.float64),
                 ep_count=zeros(N, torch.int32))
     fin.fin_rollout(env, [pol], T, fin.make_noise(fin.FIN_NOISE_SUPPLIED, 0, dev(uni)), fin.make_traj(**logs))
