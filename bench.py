@@ -360,7 +360,50 @@ def extras(fin, torch, pol):
     out.update(hbm_kernels(fin, torch))
     out["crypto_c3"] = crypto_c3(fin, torch)
     out["ensembles"] = ensembles(fin, torch)
+    out["paper_nets"] = paper_nets(fin, torch)
     return out
+
+
+def paper_nets(fin, torch):
+    """The paper's own network shapes (NEXT-3 / NEXT-2 variants): the stock PPO policy with
+    hidden layers of 64 and 32 units on the headline workload (C1 env, 65,536 envs,
+    T = 256, Philox noise; weights resident in shared memory), and the crypto Q-net with
+    three 128-unit hidden layers on the C3 env (4,096 envs, 48,000 steps)."""
+    from synth import market
+    from synth import policy as spol
+    res = {}
+    flush = L2Flush(torch)
+    N = N_HEAD
+    env = make_env(fin, N, 0)
+    pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, spol.kaiming_bf16(spol.STOCK_PAPER_DIMS, 0))
+    times, _ = time_rollouts(fin, torch, env, pol, N, T_HEAD, 5, 3, flush)
+    ms = statistics.mean(times)
+    d = spol.STOCK_PAPER_DIMS
+    res["stock_64_32"] = {"dims": list(d), "envs": N, "T": T_HEAD, "ms": ms, "env_steps_per_s": N * T_HEAD / (ms / 1e3),
+                          "flop_per_env_step_executed": 2 * (64 * 32 + 32 * 64 + 32 * 32),
+                          "flop_per_env_step_unfactored": 2 * sum(a * b for a, b in zip(d[:-1], d[1:])),
+                          "note": "10 KB of weights resident in shared memory; env-side bound (trade, noise, obs)"}
+    del env, pol
+    z = lambda s, dt: torch.zeros(s, dtype=dt, device="cuda")  # noqa: E731
+    N, T = 4096, 48000
+    rows = market.crypto_market(T, seed=41)
+    cfg = fin.env_config(task=fin.FIN_CRYPTO, num_envs=N, num_assets=1, num_indicators=0, num_rows=T + 1,
+                         episode_len=T, reward_scale=1.0, cost_rate=0.0, epsilon=0.005, seed=43)
+    pol = fin.fin_policy_create(fin.FIN_Q_ARGMAX, spol.kaiming_bf16(spol.CRYPTO_PAPER_DIMS, 4))
+    nz = fin.make_noise(fin.FIN_NOISE_PHILOX, 43)
+    fin.fin_rollout(fin.fin_env_create(cfg, rows), [pol], 1000, nz, fin.make_traj(reward=z((1000, N), torch.float32)))
+    env = fin.fin_env_create(cfg, rows)
+    tr = fin.make_traj(reward=z((T, N), torch.float32), done=z((T, N), torch.uint8))
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    fin.fin_rollout(env, [pol], T, nz, tr)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    res["crypto_3x128"] = {"dims": list(spol.CRYPTO_PAPER_DIMS), "envs": N, "T": T, "ms": ms,
+                           "env_steps_per_s": N * T / (ms / 1e3), "us_per_lockstep_step": 1e3 * ms / T}
+    return res
 
 
 def ensembles(fin, torch):

@@ -69,11 +69,19 @@ struct TcParams {
   int32_t B, in_dim, out_dim;
 };
 
-// debug timeline (fin_debug_trace): block 0 only, one slot per event
+// debug timeline (fin_debug_trace): block 0 only, one slot per event.  Compiled in only
+// with -DFIN_TRACE (FIN_NVCC_FLAGS=-DFIN_TRACE): the per-event predicates alone cost ~4%
+// of the headline rollout (A/B, round 1), so production builds carry none.
+#ifndef FIN_TRACE
+#define FIN_TR(cond, t, slot) \
+  do {                        \
+  } while (0)
+#else
 #define FIN_TR(cond, t, slot)                                                                  \
   do {                                                                                         \
     if (p.trace && blockIdx.x == 0 && (cond)) p.trace[(size_t)(t) * 32 + (slot)] = clock64(); \
   } while (0)
+#endif
 
 __device__ __forceinline__ uint32_t cm_off(int r, int kchunk, int kt8) {
   return (uint32_t)(((r >> 3) * kt8 + kchunk) * 128 + (r & 7) * 16);

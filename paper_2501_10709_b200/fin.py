@@ -18,7 +18,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfinenv.so")
+LIB_PATH = os.environ.get("FIN_LIB_PATH") or os.path.join(_HERE, "libfinenv.so")   # override: A/B runs
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -1,4 +1,6 @@
-"""Block-0 clock64 timeline of the fused crypto rollout (fin_debug_trace), cycles
+"""Needs a build with the timeline compiled in:
+    FIN_NVCC_FLAGS=-DFIN_TRACE python -m paper_2501_10709_b200.build --force
+Block-0 clock64 timeline of the fused crypto rollout (fin_debug_trace), cycles
 relative to the start of each step."""
 import os
 import sys

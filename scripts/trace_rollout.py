@@ -1,4 +1,6 @@
-"""Print the block-0 clock64 timeline of a fused rollout (fin_debug_trace), in cycles
+"""Needs a build with the timeline compiled in:
+    FIN_NVCC_FLAGS=-DFIN_TRACE python -m paper_2501_10709_b200.build --force
+Print the block-0 clock64 timeline of a fused rollout (fin_debug_trace), in cycles
 relative to the start of each step."""
 import os
 import sys
