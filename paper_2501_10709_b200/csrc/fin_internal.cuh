@@ -179,22 +179,29 @@ __device__ __forceinline__ void metric_start(MetricAcc& m, double v) {
   m.v0 = v; m.vprev = v; m.peak = v; m.mdd = 0.0; m.mean = 0.0; m.m2 = 0.0; m.n = 0;
 }
 
-// One division per point (the return r = v / v_prev - 1 of the definition).  The
-// Welford mean update multiplies by the correctly rounded 1/n (within an ulp of the
-// division), and the drawdown v / peak - 1 is only divided out when v falls below
-// (1 + mdd) peak (checked by a multiply with a 1e-12 margin, so no new minimum is
-// missed): a new maximum drawdown is rare, a division per point is not.
+// 1 / x from the MUFU seed and two Newton steps (<= 1 ulp): a fraction of the cost of a
+// correctly rounded division or __drcp_rn
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = __fma_rn(-x, y, 1.0);
+  y = __fma_rn(y, e, y);
+  e = __fma_rn(-x, y, 1.0);
+  return __fma_rn(y, e, y);
+}
+
+// Branch-free, no division: r = (v - v_prev) * rcp(v_prev) (v - v_prev exact, within
+// ~2 ulp of v / v_prev - 1), Welford with rcp(n), drawdown (v - peak) * rcp(peak) with
+// the running peak (exactly 0 at a peak).  The earlier form divided, and its "new
+// maximum drawdown" branch was taken by some env of nearly every warp.
 __device__ __forceinline__ void metric_push(MetricAcc& m, double v) {
-  double r = fsub64(fdiv64(v, m.vprev), 1.0);
+  const double r = fmul64(fsub64(v, m.vprev), rcp_nr(m.vprev));
   m.n += 1;
-  double delta = fsub64(r, m.mean);
-  m.mean = fadd64(m.mean, fmul64(delta, __drcp_rn(nn2d(m.n))));
+  const double delta = fsub64(r, m.mean);
+  m.mean = fadd64(m.mean, fmul64(delta, rcp_nr(nn2d(m.n))));
   m.m2 = fadd64(m.m2, fmul64(delta, fsub64(r, m.mean)));
-  if (v > m.peak) m.peak = v;
-  if (v < fmul64(fadd64(m.mdd, 1.0 + 1e-12), m.peak)) {
-    const double dd = fsub64(fdiv64(v, m.peak), 1.0);
-    if (dd < m.mdd) m.mdd = dd;
-  }
+  m.peak = fmax(m.peak, v);
+  m.mdd = fmin(m.mdd, fmul64(fsub64(v, m.peak), rcp_nr(m.peak)));
   m.vprev = v;
 }
 
@@ -203,10 +210,10 @@ __device__ __forceinline__ void metric_push(MetricAcc& m, double v) {
 // within an ulp): when episodes end at different steps across a warp this runs
 // divergently on most steps, so its cost matters.
 __device__ __forceinline__ void metric_finish(const MetricAcc& m, double ppy, double rf, double out[3]) {
-  out[0] = fsub64(fmul64(m.vprev, __drcp_rn(m.v0)), 1.0);
+  out[0] = fmul64(fsub64(m.vprev, m.v0), rcp_nr(m.v0));   // exactly 0 for a flat curve
   double sh = __longlong_as_double(0x7ff8000000000000ULL);
   if (m.n >= 2) {
-    const double var = fmul64(m.m2, __drcp_rn(nn2d(m.n - 1)));
+    const double var = fmul64(m.m2, rcp_nr(nn2d(m.n - 1)));
     if (var > 0.0) sh = fmul64(fmul64(sqrt(ppy), fsub64(m.mean, rf)), rsqrt(var));
   }
   out[1] = sh;

@@ -190,15 +190,6 @@ __global__ void k_pass_c(const double* __restrict__ eq, const uint8_t* __restric
 //   drawdown (v - peak) * rcp(peak), rcp(peak) = rcp(v) of the point that set the peak
 //          (~2 ulp relative, exactly 0 at a peak).
 // Tolerances of the parity tests (rel 1e-9 cum / MDD, 1e-7 Sharpe) hold with room.
-__device__ __forceinline__ double rcp_nr(double x) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = __fma_rn(-x, y, 1.0);
-  y = __fma_rn(y, e, y);
-  e = __fma_rn(-x, y, 1.0);
-  return __fma_rn(y, e, y);
-}
-
 struct FastAcc {
   double v0, vprev, rinv, peak, rpeak, mdd, k, s1, s2;
   int32_t n;

@@ -45,8 +45,11 @@ __device__ __forceinline__ float tanh_f32(float x) {
 }
 
 // ENS = false: the single-policy (C1) specialisation -- one non-DDPG member, no OU
-// state kept in registers.
-template <int KA, int IA, class Plan, bool ENS = true>
+// state kept in registers.  LOG = false: no optional trajectory logs (actions, cash,
+// asset, holdings, network outputs / hidden activations) and no fin_ensemble_act mode
+// -- the production rollout (reward, done, episode metrics, aggregate) carries none of
+// their per-step branches.
+template <int KA, int IA, class Plan, bool ENS = true, bool LOG = true>
 struct StockOps {
   static constexpr int KOU = ENS ? KA : 1;
   static constexpr int KP4 = (KA + 3) / 4 * 4;
@@ -245,7 +248,7 @@ struct StockOps {
 
   __device__ __forceinline__ static uint16_t* hidden_ptr(State& st, const TcParams& p, int env, int t, int m, int l,
                                                          int hid) {
-    if (!st.live || !p.o.mlp_hidden) return nullptr;
+    if (!LOG || !st.live || !p.o.mlp_hidden) return nullptr;
     return p.o.mlp_hidden + ((((size_t)t * p.M + m) * p.e.N + env) * Plan::kNH + l) * hid;
   }
 
@@ -283,7 +286,7 @@ struct StockOps {
     const EnvDev& e = p.e;
     const int kind = p.kinds[m];
     const bool sac = kind == FIN_SAC_SQUASH, ddpg = kind == FIN_DDPG_OU;
-    if (p.o.mlp_out) {
+    if (LOG && p.o.mlp_out) {
       float* dst = p.o.mlp_out + (((size_t)t * p.M + m) * e.N + env) * KA;
 #pragma unroll
       for (int k = 0; k < KA; ++k) dst[k] = z[k];
@@ -331,9 +334,9 @@ struct StockOps {
     for (int k = 0; k < KA; ++k) {
       const float abar = (!ENS || p.M == 1 || p.weighted) ? st.asum[k] : __fmul_rn(st.asum[k], inv_m);
       a[k] = rha_f32(__fmul_rn((float)e.max_trade, abar));
-      if (st.live && p.act_only && p.mean_out) p.mean_out[(size_t)env * KA + k] = abar;
+      if (LOG && st.live && p.act_only && p.mean_out) p.mean_out[(size_t)env * KA + k] = abar;
     }
-    if (p.act_only) {  // fin_ensemble_act: report the action, leave the env untouched
+    if (LOG && p.act_only) {  // fin_ensemble_act: report the action, leave the env untouched
       if (st.live && p.o.actions) {
 #pragma unroll
         for (int k = 0; k < KA; ++k) p.o.actions[(size_t)env * KA + k] = (int16_t)a[k];
@@ -358,7 +361,7 @@ struct StockOps {
           FIN_TR(threadIdx.x == 128, t, 19);
           const double v = st.vc;
           uint4 save[(KA + 7) / 8];   // local: read only by the rare exact buy redo
-          clamp_actions<KA>(e, a, st.oor, p.o.actions ? p.o.actions + ti * KA : nullptr);
+          clamp_actions<KA>(e, a, st.oor, (LOG && p.o.actions) ? p.o.actions + ti * KA : nullptr);
           stock_trade<KA>(e, st.b, st.h, pd, KP4, pack_acts<KA>(a), save, 1);
           const double vn = stock_mark<KA>(st.b, st.h, pd + kRowPN * KP4);
           st.vc = vn;
@@ -369,9 +372,9 @@ struct StockOps {
           st.rsum += (double)r;
           if (p.o.reward) p.o.reward[ti] = r;
           if (p.o.done) p.o.done[ti] = done ? 1 : 0;
-          if (p.o.cash) p.o.cash[ti] = st.b;
-          if (p.o.asset) p.o.asset[ti] = vn;
-          if (p.o.hold) {
+          if (LOG && p.o.cash) p.o.cash[ti] = st.b;
+          if (LOG && p.o.asset) p.o.asset[ti] = vn;
+          if (LOG && p.o.hold) {
 #pragma unroll
             for (int k = 0; k < KA; ++k) p.o.hold[ti * KA + k] = (int16_t)st.h[k];
           }
@@ -408,7 +411,7 @@ struct StockOps {
   __device__ __forceinline__ static void finalize(State& st, const TcParams& p, int env, int gtid, int bar_id,
                                                   int tile) {
     const EnvDev& e = p.e;
-    if (p.act_only) return;
+    if (LOG && p.act_only) return;
     if (st.live) {
       e.cash[env] = st.b;
       e.vcur[env] = st.vc;
@@ -538,9 +541,14 @@ cudaError_t launch_auto(const TcParams& p, int n_envs, int* tiles, cudaStream_t 
 // the paper's 64-32 net, 10 KB of weights: resident in shared memory, env-issued MMAs)
 cudaError_t launch_stock_rollout(int net, const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s) {
   const bool single = p.M == 1 && p.kinds[0] != FIN_DDPG_OU;
+  const bool logs = p.act_only || p.o.mlp_out || p.o.mlp_hidden || p.o.cash || p.o.asset || p.o.hold || p.o.actions;
+  if (net == 0 && single && !logs)
+    return launch_auto<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false, false>>(p, n_envs, tiles, s);
   if (net == 0 && single)
     return launch_auto<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false>>(p, n_envs, tiles, s);
   if (net == 0) return launch_auto<PlanStockC1, false, StockOps<30, 8, PlanStockC1, true>>(p, n_envs, tiles, s);
+  if (net == 3 && single && !logs)
+    return launch_auto<PlanStockPaper, true, StockOps<30, 8, PlanStockPaper, false, false>>(p, n_envs, tiles, s);
   if (net == 3 && single)
     return launch_auto<PlanStockPaper, true, StockOps<30, 8, PlanStockPaper, false>>(p, n_envs, tiles, s);
   if (net == 3) return launch_auto<PlanStockPaper, true, StockOps<30, 8, PlanStockPaper, true>>(p, n_envs, tiles, s);

@@ -450,3 +450,38 @@ def test_headline_config_sampled_envs():
             ostock.step(ocfg, st, m.market, g["actions"][t, j:j + 1])
     _mlp_close(np.array(zs), np.array(refs))
     assert n_boundary <= 3
+
+
+def test_production_variant_matches_logged_variant():
+    """The bench launches the log-free kernel variant (StockOps LOG = false: no optional
+    logs, fewer per-step branches).  On the headline launch configuration (65,536 envs,
+    dual layout, Philox noise, T = 35 with a reset) its reward / done / episode metrics /
+    aggregate and final env state must equal, bit for bit, those of the logged variant
+    that the sampled-env oracle test above checks."""
+    import torch
+    fin = _fin()
+    m = market.stock_c1(rows=1008)
+    layers = spol.kaiming_bf16(spol.STOCK_DIMS, 0)
+    N, T, K = 65536, 35, 30
+    kw = dict(num_assets=30, num_indicators=8, num_rows=1008, episode_len=30, num_windows=195, window_stride=5,
+              window_block=128)
+    _, fcfg = stock_pair(num_envs=N, **kw)
+    res = []
+    for logged in (False, True):
+        env = fin.fin_env_create(fcfg, m.market)
+        pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, layers)
+        logs = dict(reward=zeros((T, N), torch.float32), done=zeros((T, N), torch.uint8),
+                    ep_metrics=zeros((2, N, 3), torch.float64), ep_count=zeros(N, torch.int32),
+                    agg=zeros(8, torch.float64))
+        if logged:
+            logs["actions"] = zeros((T, N, K), torch.int16)
+        fin.fin_rollout(env, [pol], T, fin.make_noise(fin.FIN_NOISE_PHILOX, 1234), fin.make_traj(**logs))
+        assert fin.fin_env_check(env) == 0
+        cash, hold = zeros(N, torch.float64), zeros((N, K), torch.int16)
+        fin.fin_env_get_state(env, cash=cash, hold=hold)
+        out = {k: host(v) for k, v in logs.items() if k != "actions"}
+        out["cash"], out["hold"] = host(cash), host(hold)
+        res.append(out)
+    for k in res[0]:
+        assert np.array_equal(res[0][k], res[1][k], equal_nan=True), k
+    assert res[0]["done"].sum() == N
