@@ -361,7 +361,42 @@ def extras(fin, torch, pol):
     out["crypto_c3"] = crypto_c3(fin, torch)
     out["ensembles"] = ensembles(fin, torch)
     out["paper_nets"] = paper_nets(fin, torch)
+    out["market_prep"] = market_prep(fin, torch)
     return out
+
+
+def market_prep(fin, torch):
+    """The step before the rollout on the device (NEXT-3): fin_market_prepare at the C1
+    shape (30 assets, 64 warm-up + 1,008 stored days, 8 indicator families, +-1% price-scale
+    perturbation) and fin_crypto_market at the C3 length (480,000 steps x 144 f32)."""
+    import numpy as np
+    from synth import market
+    res = {}
+    m = market.stock_c1()
+    x = np.stack([m.open_all, m.high_all, m.low_all, m.close_all, m.volume_all], axis=1).astype(np.float32)
+    D, K = x.shape[0], x.shape[2]
+    xd = torch.from_numpy(x).cuda()
+    ind = list(range(8))
+    mk = torch.zeros((D - market.WARMUP_DAYS, 10, K), dtype=torch.float32, device="cuda")
+    raw = torch.zeros((8, K, D - market.WARMUP_DAYS), dtype=torch.float64, device="cuda")
+
+    def ev(fn):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
+
+    ms = ev(lambda: fin.fin_market_prepare(xd, market.WARMUP_DAYS, ind, mk, raw, magnitude=0.01, seed=7))
+    res["stock_prepare_c1"] = {"assets": K, "days": D, "indicators": 8, "ms": ms}
+    steps = 480000
+    rows = torch.zeros((steps + 1, 144), dtype=torch.float32, device="cuda")
+    ms = ev(lambda: fin.fin_crypto_market(steps, 43, rows))
+    res["crypto_market_c3"] = {"steps": steps, "ms": ms, "bytes_written": (steps + 1) * 144 * 4}
+    return res
 
 
 def paper_nets(fin, torch):

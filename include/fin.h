@@ -282,6 +282,18 @@ enum { FIN_IND_MACD = 0, FIN_IND_BOLL_UB = 1, FIN_IND_BOLL_LB = 2, FIN_IND_RSI30
 int fin_market_prepare(const float* ohlcv, int32_t D, int32_t K, int32_t warmup, const int32_t* indicators /*host*/,
                        int32_t I, double magnitude, uint64_t seed, float* market, double* raw, void* stream);
 
+/* Crypto market generation on the device (the synthetic stand-in
+ * for the paper's BTC LOB series, with the shapes of BASELINE configs[3]; reading
+ * R-CGEN, formulas in oracle/crypto_market.py): writes ``rows`` (device, f32
+ * [steps + 1][144], the layout fin_env_create takes for FIN_CRYPTO: mid, ask px / size,
+ * bid px / size over 10 levels, 101 factors, 2 pad) for steps 0 .. steps of a GBM mid
+ * (``sigma`` per step from ``m0``), a 10-level book (lognormal half-spread and level
+ * gaps, Exp(1) sizes) and 101 stationary AR(1) factors (coefficient ``phi``), all drawn
+ * from Philox4x32-10 keyed by ``seed``.  Float64 arithmetic, one f32 rounding per value.
+ * Needs steps >= 1, sigma >= 0, m0 > 0, 0 <= phi < 1.  Allocates stream-ordered scratch
+ * (8 (steps + 1) bytes + chunk carries) and frees it on the stream. */
+int fin_crypto_market(int64_t steps, uint64_t seed, double sigma, double m0, double phi, float* rows, void* stream);
+
 /* Ensemble weights from validation statistics (Eq. 6; reading R-GATE):
  * aggs f64 [M][FIN_AGG_LEN] = the aggregate vector of one validation fin_rollout per
  * member (deterministic: FIN_NOISE_NONE), all-reduced over ranks.  Member Sharpe =

@@ -60,3 +60,24 @@ def stock_noise(seed: int, g: int, t: int, member: int, K: int) -> list:
 def crypto_uniforms(seed: int, g: int, t: int):
     x = philox4x32_10((g, t, 0xFFFF0000, 0), (seed & MASK, (seed >> 32) & MASK))
     return uniform(x[0]), uniform(x[1])
+
+
+def philox4x32_10_np(c0, c1, c2, c3, k0: int, k1: int):
+    """The same Philox4x32-10 on NumPy arrays of counters (uint64 holding 32-bit values):
+    the element-wise restatement of ``philox4x32_10`` for the full-length sampled checks
+    (pinned against the scalar function and the known-answer vectors in the tests)."""
+    import numpy as np
+    m32 = np.uint64(MASK)
+    c0, c1, c2, c3 = (np.asarray(x, dtype=np.uint64) & m32 for x in (c0, c1, c2, c3))
+    c0, c1, c2, c3 = np.broadcast_arrays(c0, c1, c2, c3)
+    k0, k1 = k0 & MASK, k1 & MASK
+    for r in range(10):
+        if r > 0:
+            k0 = (k0 + W0) & MASK
+            k1 = (k1 + W1) & MASK
+        p0 = np.uint64(M0) * c0
+        p1 = np.uint64(M1) * c2
+        hi0, lo0 = p0 >> np.uint64(32), p0 & m32
+        hi1, lo1 = p1 >> np.uint64(32), p1 & m32
+        c0, c1, c2, c3 = (hi1 ^ c1 ^ np.uint64(k0)), lo1, (hi0 ^ c3 ^ np.uint64(k1)), lo0
+    return c0, c1, c2, c3

@@ -19,6 +19,8 @@ namespace fin {
 // n_envs rows; *tiles receives the tiles per CTA the launch used (agg partial rows
 // = ceil(n_envs / (128 * tiles)) * tiles)
 cudaError_t launch_stock_rollout(int net, const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s);
+cudaError_t launch_crypto_market(int64_t steps, uint64_t seed, double sigma, double m0, double phi, float* rows,
+                                 cudaStream_t s);
 cudaError_t launch_crypto_rollout(int net, const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s);
 cudaError_t launch_mlp_probe(int net, const tc::TcParams& p, int n_rows, cudaStream_t s);
 cudaError_t launch_z1s_market(int net, const float* w1s_t, int H, const EnvDev& e, float* z1s, cudaStream_t s);
@@ -777,6 +779,17 @@ int fin_market_prepare(const float* ohlcv, int32_t D, int32_t K, int32_t warmup,
   cudaError_t e = fin::launch_market_prepare(ohlcv, D, K, warmup, indicators, I, magnitude, seed, market, raw,
                                              S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fin_market_prepare launch");
+  return FIN_OK;
+}
+
+int fin_crypto_market(int64_t steps, uint64_t seed, double sigma, double m0, double phi, float* rows, void* stream) {
+  if (!rows) return fail(FIN_E_CONFIG, "fin_crypto_market: null rows");
+  if (steps < 1 || steps > (int64_t)1 << 31) return fail(FIN_E_CONFIG, "steps must be in [1, 2^31]");
+  if (!(sigma >= 0.0) || !std::isfinite(sigma)) return fail(FIN_E_CONFIG, "sigma must be finite and >= 0");
+  if (!(m0 > 0.0) || !std::isfinite(m0)) return fail(FIN_E_CONFIG, "m0 must be finite and > 0");
+  if (!(phi >= 0.0 && phi < 1.0)) return fail(FIN_E_CONFIG, "phi must be in [0, 1)");
+  cudaError_t e = fin::launch_crypto_market(steps, seed, sigma, m0, phi, rows, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_crypto_market launch");
   return FIN_OK;
 }
 

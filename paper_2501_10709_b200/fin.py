@@ -48,7 +48,7 @@ FIN_AGG_LEN = 8
 EXPORTS = ("fin_env_create", "fin_env_reset", "fin_env_step", "fin_env_get_state", "fin_env_set_state",
            "fin_env_check", "fin_env_destroy", "fin_policy_create", "fin_policy_destroy", "fin_rollout",
            "fin_rollout_actions", "fin_ensemble_act", "fin_episode_metrics", "fin_mlp_forward",
-           "fin_philox_normals", "fin_member_weights", "fin_market_prepare", "fin_last_error", "fin_abi_version", "fin_device_check",
+           "fin_philox_normals", "fin_member_weights", "fin_market_prepare", "fin_crypto_market", "fin_last_error", "fin_abi_version", "fin_device_check",
            "fin_debug_trace")
 
 
@@ -101,6 +101,7 @@ _sig = {
     "fin_mlp_forward": ([_P, _P, C.c_int32, _P, _P, _P], C.c_int),
     "fin_philox_normals": ([C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int64, _P, _P], C.c_int),
     "fin_member_weights": ([_P, C.c_int32, C.c_double, C.c_double, _P, _P, _P], C.c_int),
+    "fin_crypto_market": ([C.c_int64, C.c_uint64, C.c_double, C.c_double, C.c_double, _P, _P], C.c_int),
     "fin_market_prepare": ([_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_double,
                             C.c_uint64, _P, _P, _P], C.c_int),
     "fin_last_error": ([], C.c_char_p),
@@ -393,3 +394,13 @@ def fin_market_prepare(ohlcv, warmup: int, indicators, market, raw, magnitude: f
     _check(_lib.fin_market_prepare(_ptr(ohlcv, torch.float32, "ohlcv"), D, K, int(warmup), arr, len(ids),
                                    float(magnitude), int(seed), _ptr(market, torch.float32, "market"),
                                    _ptr(raw, torch.float64, "raw"), _stream(stream)), "fin_market_prepare")
+
+
+def fin_crypto_market(steps: int, seed: int, rows, sigma: float = 1e-4, m0: float = 5e4, phi: float = 0.9,
+                      stream=None) -> None:
+    """Generate the crypto market tensor rows f32 [steps + 1][144] (device) on the GPU."""
+    import torch
+    if tuple(rows.shape) != (steps + 1, 144):
+        raise ValueError("rows must be [steps + 1][144]")
+    _check(_lib.fin_crypto_market(int(steps), int(seed), float(sigma), float(m0), float(phi),
+                                  _ptr(rows, torch.float32, "rows"), _stream(stream)), "fin_crypto_market")

@@ -58,3 +58,58 @@ def test_market_prepare_c0_subset_and_env():
     for e, c in zip(envs, cash):
         fin.fin_env_get_state(e, cash=c)
     assert np.array_equal(host(cash[0]), host(cash[1]))
+
+
+# ------------------------------------------------------------- crypto market generation
+def _close_f32(g, o):
+    """Float64 on both sides, one f32 rounding each: equal up to 2 f32 ulps (the device's
+    libm and chunked running sums differ from the oracle's in the last f64 bits, which
+    can move a value across an f32 rounding boundary)."""
+    g = g.astype(np.float64)
+    o = o.astype(np.float64)
+    tol = 2.0 * np.abs(o) * 2.0 ** -23 + 1e-30
+    bad = np.abs(g - o) > tol
+    assert not bad.any(), f"{int(bad.sum())} values beyond 2 ulp; first {np.argwhere(bad)[0].tolist()}"
+
+
+def test_crypto_market_matches_oracle_small():
+    """700 steps (three chunks of 256, the last ragged): every value against the oracle's
+    plain loops."""
+    import torch
+    from oracle import crypto_market as ocm
+    from paper_2501_10709_b200 import fin
+    steps = 700
+    rows = zeros((steps + 1, 144), torch.float32)
+    fin.fin_crypto_market(steps, 41, rows)
+    _close_f32(host(rows), ocm.generate(steps, 41))
+
+
+def test_crypto_market_full_length_sampled():
+    """BASELINE configs[3] length (480,000 steps): sampled rows (chunk edges, the ends)
+    against the oracle's element-wise path; structural invariants on every row."""
+    import torch
+    from oracle import crypto_market as ocm
+    from paper_2501_10709_b200 import fin
+    steps = 480000
+    rows = zeros((steps + 1, 144), torch.float32)
+    fin.fin_crypto_market(steps, 43, rows)
+    g = host(rows)
+    sample = [0, 1, 255, 256, 257, 4097, 123457, 479999, 480000]
+    _close_f32(g[sample], ocm.sampled_rows(steps, 43, sample))
+    mid, ask, bid = g[:, 0], g[:, 1:11], g[:, 21:31]
+    assert np.all(ask[:, 0] > mid) and np.all(bid[:, 0] < mid)
+    assert np.all(np.diff(ask, axis=1) > 0) and np.all(np.diff(bid, axis=1) < 0)
+    assert np.all(g[:, 11:21] > 0) and np.all(g[:, 142:] == 0)
+    f = g[:, 41:142].astype(np.float64)
+    assert abs(f.var(axis=0).mean() - 1.0) < 0.02
+
+
+def test_crypto_market_rejects_bad_arguments():
+    import torch
+    from paper_2501_10709_b200 import fin
+    rows = zeros((1, 144), torch.float32)
+    with pytest.raises(Exception):
+        fin.fin_crypto_market(0, 1, rows)
+    rows = zeros((11, 144), torch.float32)
+    with pytest.raises(Exception):
+        fin.fin_crypto_market(10, 1, rows, phi=1.0)

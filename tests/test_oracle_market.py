@@ -81,3 +81,67 @@ def test_perturbation_properties():
             scaled = name in ("macd", "boll_ub", "boll_lb", "sma30", "sma60")
             ref = raw0[:, i, k] * (ck if scaled else 1.0)
             np.testing.assert_allclose(raw1[:, i, k], ref, rtol=1e-9, atol=1e-7)
+
+
+# ------------------------------------------------------------- crypto market oracle (NEXT-3)
+def test_vectorized_philox_matches_scalar():
+    from oracle import philox
+    rng = np.random.default_rng(3)
+    ctr = rng.integers(0, 2**32, size=(200, 4), dtype=np.uint64)
+    key = (0x9E3779B9, 0x0BADF00D)
+    v = philox.philox4x32_10_np(ctr[:, 0], ctr[:, 1], ctr[:, 2], ctr[:, 3], *key)
+    for i in range(200):
+        assert tuple(int(x[i]) for x in v) == philox.philox4x32_10(tuple(int(c) for c in ctr[i]), key)
+
+
+def test_crypto_generator_special_cases():
+    """sigma = 0: the mid stays at m0 exactly; phi = 0: each factor is its innovation
+    N(t, 7, k) exactly; row 0 holds f_0 = N(0, 7, k) and mid m0."""
+    from oracle import crypto_market as ocm
+    g = ocm.generate(40, 5, sigma=0.0, m0=123.5)
+    assert np.all(g[:, 0] == np.float32(123.5))
+    g = ocm.generate(12, 9, phi=0.0)
+    for t in (0, 1, 7, 12):
+        for k in (0, 3, 50, 100):
+            assert g[t, 41 + k] == np.float32(ocm.normal(9, t, ocm.S_FACTOR, k))
+    assert g[0, 0] == np.float32(5e4)
+
+
+def test_crypto_generator_book_structure_and_sampled_rows():
+    """Book invariants on every row (ask_0 > mid > bid_0, asks strictly increasing, bids
+    strictly decreasing, sizes > 0, pad 0) and the element-wise full-length path equal to
+    the plain loops on the rows they share."""
+    from oracle import crypto_market as ocm
+    g = ocm.generate(400, 41)
+    mid, ask, bid = g[:, 0], g[:, 1:11], g[:, 21:31]
+    assert np.all(ask[:, 0] > mid) and np.all(bid[:, 0] < mid)
+    assert np.all(np.diff(ask, axis=1) > 0) and np.all(np.diff(bid, axis=1) < 0)
+    assert np.all(g[:, 11:21] > 0) and np.all(g[:, 31:41] > 0) and np.all(g[:, 142:] == 0)
+    rows = [0, 1, 2, 255, 256, 399, 400]
+    assert np.array_equal(ocm.sampled_rows(400, 41, rows), g[rows])
+
+
+def test_crypto_generator_distributions():
+    """Moments of the drawn series against their definitions (3,000 steps): GBM log
+    returns (drift -sigma^2/2, visible at sigma = 0.5; std sigma), lognormal spread and
+    gaps (log-ratio mean 0, std 0.5), Exp(1) sizes, stationary AR(1) factors (variance 1,
+    lag-1 autocorrelation phi)."""
+    from oracle import crypto_market as ocm
+    g = ocm.generate(1000, 77, sigma=0.5, m0=1e30).astype(np.float64)   # stays inside f32 range
+    lr = np.diff(np.log(g[:, 0]))
+    assert abs(lr.mean() - (-0.125)) < 4 * 0.5 / np.sqrt(1000) and abs(lr.std() - 0.5) < 0.04
+    n = 3000
+    g = ocm.generate(n, 78).astype(np.float64)
+    lr = np.diff(np.log(g[:, 0]))
+    assert abs(lr.std() - 1e-4) < 0.05e-4
+    mid = g[:, 0]
+    ls = np.log((g[:, 1] - mid) / (mid * 1e-4))
+    assert abs(ls.mean()) < 0.05 and abs(ls.std() - 0.5) < 0.03
+    lg = np.log(np.diff(g[:, 1:11], axis=1) / (mid[:, None] * 0.5e-4))
+    assert abs(lg.mean()) < 0.03 and abs(lg.std() - 0.5) < 0.02
+    sz = np.concatenate([g[:, 11:21].ravel(), g[:, 31:41].ravel()])
+    assert abs(sz.mean() - 1.0) < 0.02 and abs(sz.std() - 1.0) < 0.03
+    f = g[:, 41:142]
+    assert abs(f.var(axis=0).mean() - 1.0) < 0.1
+    ac = np.mean([np.corrcoef(f[:-1, k], f[1:, k])[0, 1] for k in range(101)])
+    assert abs(ac - 0.9) < 0.02
