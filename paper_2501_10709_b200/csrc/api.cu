@@ -9,6 +9,7 @@
 #include <new>
 #include <string>
 #include <type_traits>
+#include <atomic>
 #include <vector>
 
 #include "fin_internal.cuh"
@@ -39,6 +40,7 @@ struct fin_env {
   size_t agg_cap;  // rows of FIN_AGG_LEN
   float* z1s;      // factored layer 1: per-member shared term of every market day [M][rows][HID]
   size_t z1s_cap;  // floats
+  std::vector<uint64_t> z1s_key;   // uids of the members z1s holds (empty: none)
   float* ou_mem;   // DDPG OU state [ou_slots][K][N] (grown on demand)
 };
 
@@ -51,6 +53,7 @@ struct fin_policy {
   float* bias;                 // device, [H1 | H2 | (H3) | OUT_PAD] (TcPlan::bias_off)
   uint8_t bias_nz;             // bit l: layer l has a non-zero bias (an all-zero bias is skipped)
   float* w1s_t;                // stock: device [S][HID] shared columns of W1 (exact bf16 values), else null
+  uint64_t uid;                // process-unique id (keys the env's z1s cache; addresses can be reused)
 };
 
 namespace {
@@ -491,6 +494,8 @@ int fin_policy_create(int32_t kind, int32_t n_layers, const int32_t* dims, const
   else pack_member<PlanCrypto, void>(dims, w_bf16, bias, wp, bp, nullptr);
   fin_policy* pol = new (std::nothrow) fin_policy();
   if (!pol) return fail(FIN_E_CONFIG, "out of host memory");
+  static std::atomic<uint64_t> next_uid{1};
+  pol->uid = next_uid.fetch_add(1);
   pol->kind = kind;
   pol->net = net;
   pol->n_layers = n_layers;
@@ -587,11 +592,20 @@ int fill_members(fin_env* env, const fin_policy* const* members, int32_t n, cons
 }
 
 // Factored stock layer 1: the shared-input term of every market day for every member
-// (z1s = W1_shared q(x_shared(d)), tc_plan.cuh), recomputed at each rollout so it
-// always matches the members and the market it is used with (1008 x 270 x 256 FMAs).
+// (z1s = W1_shared q(x_shared(d)), tc_plan.cuh; 1008 x 270 x 256 FMAs).  Kept per env
+// and recomputed only when the member list changes (policies and the env's market copy
+// are immutable after creation; policies are keyed by their process-unique uid).
 int prepare_z1s(fin_env* env, const fin_policy* const* members, int n, int net, tc::TcParams& p, cudaStream_t s) {
   if (env->d.task != FIN_STOCK) return FIN_OK;
   const int H = members[0]->dims[1];
+  std::vector<uint64_t> key(n);
+  for (int m = 0; m < n; ++m) key[m] = members[m]->uid;
+  if (env->z1s && key == env->z1s_key) {
+    p.z1s = env->z1s;
+    p.z1s_rows = env->d.rows;
+    return FIN_OK;
+  }
+  env->z1s_key.clear();
   const size_t need = (size_t)n * env->d.rows * H;
   if (env->z1s_cap < need) {
     if (env->z1s) cudaFree(env->z1s);
@@ -604,6 +618,7 @@ int prepare_z1s(fin_env* env, const fin_policy* const* members, int n, int net, 
     cudaError_t e = fin::launch_z1s_market(net, members[m]->w1s_t, H, env->d, env->z1s + (size_t)m * env->d.rows * H, s);
     if (e != cudaSuccess) return cuda_fail(e, "z1s precompute");
   }
+  env->z1s_key = key;
   p.z1s = env->z1s;
   p.z1s_rows = env->d.rows;
   return FIN_OK;

@@ -527,15 +527,24 @@ __global__ void k_stock_set_state(EnvDev e, const double* cash, const int16_t* h
   store_metric(e, i, m);
 }
 
+// One warp per aggregate component: lanes stride over the partial rows, then a fixed
+// shuffle tree (deterministic order) -- the serial per-component loop cost ~36 us per
+// rollout (512 partial rows of dependent-chain loads).
 __global__ void k_agg_finalize(const double* __restrict__ partial, int n_blocks, double* agg) {
-  const int j = threadIdx.x;
+  const int j = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (j >= FIN_AGG_LEN) return;
-  double s = (j < FIN_AGG_NSUM) ? 0.0 : __longlong_as_double(0x7ff0000000000000ULL);
-  for (int b = 0; b < n_blocks; ++b) {
-    double x = partial[(size_t)b * FIN_AGG_LEN + j];
-    s = (j < FIN_AGG_NSUM) ? s + x : fmin(s, x);
+  const bool sum = j < FIN_AGG_NSUM;
+  double s = sum ? 0.0 : __longlong_as_double(0x7ff0000000000000ULL);
+  for (int b = lane; b < n_blocks; b += 32) {
+    const double x = __ldg(partial + (size_t)b * FIN_AGG_LEN + j);
+    s = sum ? s + x : fmin(s, x);
   }
-  agg[j] = s;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double o = __shfl_down_sync(0xffffffffu, s, off);
+    s = sum ? s + o : fmin(s, o);
+  }
+  if (lane == 0) agg[j] = s;
 }
 
 inline int blocks_for(int n, int threads = kThreads) { return (n + threads - 1) / threads; }
@@ -618,7 +627,7 @@ cudaError_t launch_stock_set_state(const EnvDev& e, const double* cash, const in
 }
 
 cudaError_t launch_agg_finalize(const double* partial, int n_blocks, double* agg, cudaStream_t s) {
-  k_agg_finalize<<<1, 32, 0, s>>>(partial, n_blocks, agg);
+  k_agg_finalize<<<1, 32 * FIN_AGG_LEN, 0, s>>>(partial, n_blocks, agg);
   return cudaGetLastError();
 }
 

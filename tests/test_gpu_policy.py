@@ -485,3 +485,29 @@ def test_production_variant_matches_logged_variant():
     for k in res[0]:
         assert np.array_equal(res[0][k], res[1][k], equal_nan=True), k
     assert res[0]["done"].sum() == N
+
+
+def test_z1s_cache_follows_the_member_list():
+    """The factored layer-1 term is cached per env and keyed by the members' ids: acting
+    with A, then B, then A again on one env gives, each time, the actions of a fresh env
+    (the cache is refilled whenever the member list changes)."""
+    import torch
+    fin = _fin()
+    m = market.stock_c1(rows=80)
+    N = 150
+    _, fcfg = stock_pair(num_envs=N, num_assets=30, num_indicators=8, num_rows=80, episode_len=5, num_windows=10)
+    pa = fin.fin_policy_create(fin.FIN_PPO_GAUSS, spol.kaiming_bf16(spol.STOCK_DIMS, 11))
+    pb = fin.fin_policy_create(fin.FIN_PPO_GAUSS, spol.kaiming_bf16(spol.STOCK_DIMS, 12))
+    nz = fin.make_noise(fin.FIN_NOISE_NONE, 0)
+
+    def act(env, pols):
+        a = zeros((N, 30), torch.int16)
+        fin.fin_ensemble_act(env, pols, a, None, nz)
+        return host(a)
+
+    env = fin.fin_env_create(fcfg, m.market)
+    seq = [act(env, [pa]), act(env, [pb]), act(env, [pa]), act(env, [pa, pb])]
+    ref = [act(fin.fin_env_create(fcfg, m.market), p) for p in ([pa], [pb], [pa], [pa, pb])]
+    for x, y in zip(seq, ref):
+        assert np.array_equal(x, y)
+    assert not np.array_equal(seq[0], seq[1])
