@@ -49,6 +49,7 @@ template <class Plan>
 struct CryptoOps {
   static constexpr int IN = 2 + FIN_C_FACTORS;  // 103
   static constexpr int KT8 = Plan::kIn / 8;
+  static constexpr bool kSplitOK = true;        // column-split epilogues (no layer-1 addend)
   static constexpr int kOffX = 0;                               // bf16 obs row (112)
   static constexpr int kOffR = 256;                             // ring of 3 rows (3 x 144 floats)
   static constexpr int kOffT = kOffR + 3 * FIN_C_ROW * 4;
@@ -195,6 +196,13 @@ struct CryptoOps {
     return p.o.mlp_hidden + ((((size_t)t * p.M + m) * p.e.N + env) * Plan::kNH + l) * hid;
   }
 
+  // the hidden-activation log row of env ``env`` for an epilogue helper warpgroup
+  __device__ __forceinline__ static uint16_t* helper_hidden_ptr(const TcParams& p, int env, int t, int m, int l,
+                                                                int hid) {
+    if (env >= p.e.N || !p.o.mlp_hidden) return nullptr;
+    return p.o.mlp_hidden + ((((size_t)t * p.M + m) * p.e.N + env) * Plan::kNH + l) * hid;
+  }
+
   __device__ __forceinline__ static void prepare(State&, const TcParams&, int, int, int) {}
   __device__ __forceinline__ static void consume(State& st, const TcParams& p, int env, int t, int m, const float* z) {
     if (!st.live) return;
@@ -299,6 +307,11 @@ int num_sms();
 
 // The C3 loop is latency-bound (one lockstep step at a time): spread tiles over the
 // SMs first (one tile per CTA); pair tiles per CTA only when tiles outnumber SMs.
+#ifndef FIN_CRYPTO_SPLIT
+#define FIN_CRYPTO_SPLIT 2   // warpgroups sharing each hidden-layer epilogue (one tile per CTA)
+#endif
+constexpr int kCryptoSplit = FIN_CRYPTO_SPLIT;
+
 template <class Plan>
 cudaError_t launch_crypto_plan(const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s) {
   using Ops = CryptoOps<Plan>;
@@ -312,7 +325,8 @@ cudaError_t launch_crypto_plan(const tc::TcParams& p, int n_envs, int* tiles, cu
     if (p.M <= tc::Smem<Plan, true, 2, Ops>::max_members()) return tc::launch<Plan, true, 2, Ops>(p, n_envs, s);
     return tc::launch<Plan, false, 2, Ops>(p, n_envs, s);
   }
-  if (p.M <= tc::Smem<Plan, true, 1, Ops>::max_members()) return tc::launch<Plan, true, 1, Ops>(p, n_envs, s);
+  if (p.M <= tc::Smem<Plan, true, 1, Ops>::max_members())
+    return tc::launch<Plan, true, 1, Ops, tc::kRing, 1, kCryptoSplit>(p, n_envs, s);
   return tc::launch<Plan, false, 1, Ops>(p, n_envs, s);
 }
 

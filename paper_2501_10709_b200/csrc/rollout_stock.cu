@@ -52,6 +52,7 @@ __device__ __forceinline__ float tanh_f32(float x) {
 template <int KA, int IA, class Plan, bool ENS = true, bool LOG = true>
 struct StockOps {
   static constexpr int KOU = ENS ? KA : 1;
+  static constexpr bool kSplitOK = false;
   static constexpr int KP4 = (KA + 3) / 4 * 4;
   static constexpr int IN = 1 + 2 * KA + IA * KA;
   static constexpr int KT8 = Plan::kIn / 8;
@@ -442,6 +443,7 @@ struct StockOps {
 template <class Plan, class Obs>
 struct ProbeOps {
   static constexpr int kStageBytes = 16;
+  static constexpr bool kSplitOK = false;
   static constexpr bool kFactored = !std::is_void<Obs>::value;
   struct State {
     int b;

@@ -133,8 +133,13 @@ struct Smem {
 //   };
 // RING: weight-ring slots; MINB: CTAs per SM (MINB = 2 runs two independent tiles per
 // SM whose env phases overlap each other's MMA / weight-streaming phases).
-template <class Plan, bool RESIDENT, int TILES, class Ops, int RING = kRing, int MINB = 1>
-__global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __grid_constant__ TcParams p) {
+// SPLIT > 1 (resident plans, one tile per CTA: the latency-bound crypto rollout): SPLIT
+// warpgroups share each hidden layer's epilogue by columns (warpgroup w takes chunk
+// range w of the layer's 16-column chunks); the first runs everything else.
+template <class Plan, bool RESIDENT, int TILES, class Ops, int RING = kRing, int MINB = 1, int SPLIT = 1>
+__global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(const __grid_constant__ TcParams p) {
+  static_assert(SPLIT == 1 || (TILES == 1 && RESIDENT && Ops::kSplitOK), "column-split epilogues: resident, 1 tile");
+  static_assert((Plan::kHidMax / 16) % SPLIT == 0, "chunks must divide among the warpgroups");
   using S = Smem<Plan, RESIDENT, TILES, Ops, RING>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int M = p.M;
@@ -288,15 +293,109 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
   } else {
     if constexpr (kSplitRegs) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kEnvRegs) : "memory");
     // ============================ env warpgroups ============================
-    const int tile = (warp - 4) >> 2;
+    const int part = SPLIT > 1 ? ((warp - 4) >> 2) : 0;   // column share of the epilogues (SPLIT > 1)
+    const int tile = SPLIT > 1 ? 0 : ((warp - 4) >> 2);
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;          // env row of the tile == TMEM lane
-    const int gtid = (warp - 4 - tile * 4) * 32 + lane;   // thread index within the tile's warpgroup
+    const int gtid = (warp - 4 - (tile + part) * 4) * 32 + lane;   // thread index within its warpgroup
     const int env = (blockIdx.x * TILES + tile) * kTileM + row;
     const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tile * kTc);
     const uint32_t xa = sm100::smem_u32(sA + tile * S::kA);
     uint8_t* stg = sStage + tile * Ops::kStageBytes;
     const int bar_id = 1 + tile;
+    constexpr int kSplitBar = 1 + TILES;     // the warpgroups of a column-split tile meet here
+    // Hidden-layer epilogue of chunks [c0, c1): D -> +bias (+ addend) -> ReLU -> bf16 -> A
+    // (K-major core matrices).  16 columns per TMEM load: half the registers of 32-column
+    // chunks (the env state lives in registers across the whole rollout).  One loop per
+    // addend combination (uniform branch), so an absent addend costs no issue slots.
+    auto epi = [&](auto has_b, auto has_add, const float* bl, const float* add, uint4* hlog, int ncol, int c0,
+                   int c1) {
+      constexpr bool HB = decltype(has_b)::value, HA = decltype(has_add)::value;
+#pragma unroll 1
+      for (int c = c0; c < c1; ++c) {
+        uint32_t v[16];
+        sm100::tmem_ld16(t_lane + (uint32_t)(c * 16), v);
+        // addend b (+ z1s for the factored layer 1), 128-bit broadcast loads, issued
+        // while the TMEM load is in flight
+        float ad[16];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+          if constexpr (HB) x = reinterpret_cast<const float4*>(bl + c * 16)[q4];
+          if constexpr (HA) {
+            const float4 y = reinterpret_cast<const float4*>(add + c * 16)[q4];
+            if constexpr (HB) {
+              x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
+            } else {
+              x = y;
+            }
+          }
+          ad[4 * q4] = x.x; ad[4 * q4 + 1] = x.y; ad[4 * q4 + 2] = x.z; ad[4 * q4 + 3] = x.w;
+        }
+        sm100::tmem_wait_ld();
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {   // ReLU + bf16 in one cvt.rn.relu.bf16x2
+          if constexpr (HB || HA)
+            pk[j] = sm100::pack_bf16_relu(__uint_as_float(v[2 * j]) + ad[2 * j],
+                                          __uint_as_float(v[2 * j + 1]) + ad[2 * j + 1]);
+          else
+            pk[j] = sm100::pack_bf16_relu(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+        }
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+          sts128(xa + cm_off(row, c * 2 + g, ncol / 8), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+        if (hlog) {
+#pragma unroll
+          for (int g = 0; g < 2; ++g)
+            hlog[c * 2 + g] = make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+        }
+      }
+    };
+    auto run_epi = [&](const float* bl, const float* add, uint4* hlog, int ncol, int c0, int c1) {
+      using T1 = std::true_type;
+      using F0 = std::false_type;
+      // (bl is uniform; add is null for every thread or for none -- Ops contract)
+      if (bl && add) epi(T1{}, T1{}, bl, add, hlog, ncol, c0, c1);
+      else if (bl) epi(T1{}, F0{}, bl, add, hlog, ncol, c0, c1);
+      else if (add) epi(F0{}, T1{}, bl, add, hlog, ncol, c0, c1);
+      else epi(F0{}, F0{}, bl, add, hlog, ncol, c0, c1);
+    };
+    // this layer's width = the next layer's K (a compile-time constant when all hidden
+    // layers have one width, as in the BASELINE nets: the runtime bound cost ~10%)
+    constexpr bool kUniformHid = Plan::hid(0) == Plan::hid(1) && (Plan::kNH < 3 || Plan::hid(2) == Plan::hid(0));
+    bool is_helper = false;
+    if constexpr (SPLIT > 1) {
+    if (part > 0) {
+      // ======================= epilogue helper (column share `part`) =======================
+      is_helper = true;
+      uint32_t d_use = 0;
+      for (int t = 0; t < T; ++t) {
+        for (int m = 0; m < M; ++m) {
+          const float* bias = m < FIN_STAGE_MEMBERS ? sBias + m * Plan::kBiasFloats : p.bias[m];
+#pragma unroll 1
+          for (int l = 0; l < Plan::kNH; ++l) {
+            sm100::mbar_wait(&d_full[0], d_use & 1);
+            ++d_use;
+            sm100::tc_fence_after();
+            const float* bl = ((p.bias_nz[m] >> l) & 1u) ? bias + Plan::bias_off(l) : nullptr;
+            const int ncol = kUniformHid ? Plan::kH1 : Plan::nrows(l);
+            const int cpp = (ncol / 16) / SPLIT;
+            uint4* hlog = reinterpret_cast<uint4*>(Ops::helper_hidden_ptr(p, env, t, m, l, Plan::kHidMax));
+            run_epi(bl, nullptr, hlog, ncol, part * cpp, (part + 1) * cpp);
+            sm100::fence_proxy_async_smem();
+            sm100::tc_fence_before();
+            sm100::named_bar_sync(kSplitBar, 128 * SPLIT);
+          }
+          // the output layer's phase (read by the first warpgroup only) must still be waited
+          // for: parity waits only tell the current phase from the previous one
+          sm100::mbar_wait(&d_full[0], d_use & 1);
+          ++d_use;
+        }
+      }
+    }
+    }
+    if (!is_helper) {
     typename Ops::State st;
     Ops::init(st, p, env, row);
     uint32_t d_use = 0;
@@ -306,7 +405,8 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
       sm100::fence_proxy_async_smem();
       sm100::tc_fence_before();
       if constexpr (kEnvIssue) {
-        sm100::named_bar_sync(bar_id, 128);
+        if (SPLIT > 1 && l > 0) sm100::named_bar_sync(kSplitBar, 128 * SPLIT);   // the helpers' columns too
+        else sm100::named_bar_sync(bar_id, 128);
         if (gtid == 0) {
           if (!w_ready) {
             sm100::mbar_wait(&w_full[0], 0);
@@ -350,68 +450,12 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
           FIN_TR(row == 0 && tile == 0 && m == 0, t, 2 + 2 * l);
           sm100::tc_fence_after();
           const float* bl = ((p.bias_nz[m] >> l) & 1u) ? bias + Plan::bias_off(l) : nullptr;
-          // this layer's width = the next layer's K (a compile-time constant when all hidden
-          // layers have one width, as in the BASELINE nets: the runtime bound cost ~10%)
-          constexpr bool kUniformHid = Plan::hid(0) == Plan::hid(1) && (Plan::kNH < 3 || Plan::hid(2) == Plan::hid(0));
           const int ncol = kUniformHid ? Plan::kH1 : Plan::nrows(l);
           // factored layer 1: + shared-input term of the env's day (smem or global row)
           const float* add = l == 0 ? Ops::l1_addend(st, p, m, stg) : nullptr;
           // debug / parity log of the bf16 hidden activations (teacher-forced layer checks)
           uint4* hlog = reinterpret_cast<uint4*>(Ops::hidden_ptr(st, p, env, t, m, l, Plan::kHidMax));
-          // 16 columns per TMEM load: half the registers of 32-column chunks (the env
-          // state lives in registers across the whole rollout).  One loop per addend
-          // combination (uniform branch), so an absent addend costs no issue slots.
-          auto epilogue = [&](auto has_b, auto has_add) {
-            constexpr bool HB = decltype(has_b)::value, HA = decltype(has_add)::value;
-#pragma unroll 1
-            for (int c = 0; c < ncol / 16; ++c) {
-              uint32_t v[16];
-              sm100::tmem_ld16(t_lane + (uint32_t)(c * 16), v);
-              // addend b (+ z1s for the factored layer 1), 128-bit broadcast loads, issued
-              // while the TMEM load is in flight
-              float ad[16];
-#pragma unroll
-              for (int q4 = 0; q4 < 4; ++q4) {
-                float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-                if constexpr (HB) x = reinterpret_cast<const float4*>(bl + c * 16)[q4];
-                if constexpr (HA) {
-                  const float4 y = reinterpret_cast<const float4*>(add + c * 16)[q4];
-                  if constexpr (HB) {
-                    x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
-                  } else {
-                    x = y;
-                  }
-                }
-                ad[4 * q4] = x.x; ad[4 * q4 + 1] = x.y; ad[4 * q4 + 2] = x.z; ad[4 * q4 + 3] = x.w;
-              }
-              sm100::tmem_wait_ld();
-              uint32_t pk[8];
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {   // ReLU + bf16 in one cvt.rn.relu.bf16x2
-                if constexpr (HB || HA)
-                  pk[j] = sm100::pack_bf16_relu(__uint_as_float(v[2 * j]) + ad[2 * j],
-                                                __uint_as_float(v[2 * j + 1]) + ad[2 * j + 1]);
-                else
-                  pk[j] = sm100::pack_bf16_relu(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-              }
-#pragma unroll
-              for (int g = 0; g < 2; ++g)
-                sts128(xa + cm_off(row, c * 2 + g, ncol / 8), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2],
-                       pk[4 * g + 3]);
-              if (hlog) {
-#pragma unroll
-                for (int g = 0; g < 2; ++g)
-                  hlog[c * 2 + g] = make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
-              }
-            }
-          };
-          using T1 = std::true_type;
-          using F0 = std::false_type;
-          // (bl is uniform; add is null for every thread or for none -- Ops contract)
-          if (bl && add) epilogue(T1{}, T1{});
-          else if (bl) epilogue(T1{}, F0{});
-          else if (add) epilogue(F0{}, T1{});
-          else epilogue(F0{}, F0{});
+          run_epi(bl, add, hlog, ncol, 0, (ncol / 16) / SPLIT);
           kick(m, l + 1);
           // work that does not depend on the network output (e.g. the step's noise)
           // overlaps the largest MMA (layer 2) instead of following the last one
@@ -446,6 +490,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
       FIN_TR(row == 0 && tile == 0, t, 8);
     }
     Ops::finalize(st, p, env, gtid, bar_id, tile);
+    }   // first warpgroup
   }
   __syncthreads();
   if (warp == 1) {
@@ -454,16 +499,16 @@ __global__ void __launch_bounds__(128 + 128 * TILES, MINB) k_tc_rollout(const __
   }
 }
 
-template <class Plan, bool RESIDENT, int TILES, class Ops, int RING = kRing, int MINB = 1>
+template <class Plan, bool RESIDENT, int TILES, class Ops, int RING = kRing, int MINB = 1, int SPLIT = 1>
 cudaError_t launch(const TcParams& p, int n_envs, cudaStream_t s) {
   using Sm = Smem<Plan, RESIDENT, TILES, Ops, RING>;
-  auto kern = k_tc_rollout<Plan, RESIDENT, TILES, Ops, RING, MINB>;
+  auto kern = k_tc_rollout<Plan, RESIDENT, TILES, Ops, RING, MINB, SPLIT>;
   const int bytes = Sm::total(p.M);
   if (MINB > 1 && bytes * MINB > kSmemLimit) return cudaErrorInvalidConfiguration;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (err != cudaSuccess) return err;
   const int per_cta = kTileM * TILES;
-  kern<<<(n_envs + per_cta - 1) / per_cta, 128 + 128 * TILES, bytes, s>>>(p);
+  kern<<<(n_envs + per_cta - 1) / per_cta, 128 + 128 * TILES * SPLIT, bytes, s>>>(p);
   return cudaGetLastError();
 }
 
