@@ -362,7 +362,51 @@ def extras(fin, torch, pol):
     out["ensembles"] = ensembles(fin, torch)
     out["paper_nets"] = paper_nets(fin, torch)
     out["market_prep"] = market_prep(fin, torch)
+    out["consumer"] = consumer(fin, torch)
     return out
+
+
+def consumer(fin, torch):
+    """The consumer's first steps on the rollout's tensors (NEXT-4): GAE over the headline
+    trajectory shape (65,536 envs x 256 steps; 17 B per env-step: reward f32 + done u8 +
+    value f32 read, advantage + return f32 written), with and without batch normalisation,
+    and the Eq. 5 KL term of three members over 65,536 states."""
+    pk = peaks()
+    N, T = N_HEAD, T_HEAD
+    g = torch.Generator(device="cuda").manual_seed(4)
+    rew = torch.randn((T, N), device="cuda", generator=g)
+    val = torch.randn((T + 1, N), device="cuda", generator=g)
+    done = torch.zeros((T, N), dtype=torch.uint8, device="cuda")
+    done[29::30] = 1
+    adv, ret = torch.empty_like(rew), torch.empty_like(rew)
+    res = {}
+    for norm in (False, True):
+        for _ in range(3):
+            fin.fin_gae(rew, val, done, adv, ret, normalise=norm)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(10):
+            fin.fin_gae(rew, val, done, adv, ret, normalise=norm)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / 10
+        byts = T * N * 17 + N * 4 + (T * N * 8 if norm else 0)
+        gbs = byts / (ms / 1e3) / 1e9
+        res["gae" + ("_normalised" if norm else "")] = {
+            "envs": N, "T": T, "ms": ms, "env_steps_per_s": N * T / (ms / 1e3), "bytes_per_launch": byts,
+            "achieved_gbs": gbs, "frac": gbs / pk["hbm_gbs"]}
+    out = torch.tanh(torch.randn((3, N, 30), device="cuda", generator=g))
+    D = torch.zeros((3, 3), dtype=torch.float64, device="cuda")
+    fin.fin_kl_diversity(out, D)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    fin.fin_kl_diversity(out, D)
+    b.record()
+    torch.cuda.synchronize()
+    res["kl_diversity_3x65536x30"] = {"ms": a.elapsed_time(b)}
+    return res
 
 
 def market_prep(fin, torch):

@@ -294,6 +294,27 @@ int fin_market_prepare(const float* ohlcv, int32_t D, int32_t K, int32_t warmup,
  * (8 (steps + 1) bytes + chunk carries) and frees it on the stream. */
 int fin_crypto_market(int64_t steps, uint64_t seed, double sigma, double m0, double phi, float* rows, void* stream);
 
+/* Generalised advantage estimation over a rollout's trajectory (
+ * SPEC S:392-395; reading R-GAE, formulas in oracle/learn.py): from reward f32 [T][N],
+ * value f32 [T+1][N] (row T = the bootstrap value of the last state) and done u8 [T][N]
+ * (device), writes adv and ret f32 [T][N] (device): delta_t = r_t + gamma V_{t+1} (1 - d_t)
+ * - V_t, A_t = delta_t + gamma lambda (1 - d_t) A_{t+1}, A_T = 0, R_t = A_t + V_t, float64
+ * per env in this order (bit-identical to the oracle before the f32 rounding).
+ * ``normalise`` != 0: adv is then replaced by (A - mean) / std over all T N entries
+ * (population std of the float64 advantages, deterministic merge; A - mean if std = 0);
+ * ret keeps the unnormalised A + V.  Needs T >= 1, N >= 1, 0 <= gamma, lambda <= 1. */
+int fin_gae(const float* reward, const float* value, const uint8_t* done, int32_t T, int32_t N, double gamma,
+            double lambda, int32_t normalise, float* adv, float* ret, void* stream);
+
+/* The KL diversity term of Eq. 5: from M
+ * members' outputs f32 [M][B][K] on the same B states (device) writes D f64 [M][M]
+ * (device), D[i][j] = mean over the states of KL(pi_j || pi_i) (D[i][i] = 0); member i's
+ * loss term is lambda sum_{j != i} D[i][j].  kind 0: diagonal Gaussians N(out, sigma^2)
+ * (PPO, and DDPG wrapped with sigma): sum_k (mu_j - mu_i)^2 / (2 sigma^2); kind 1:
+ * categorical softmax(out) (the DQN family's Q-values).  Float64, deterministic. */
+int fin_kl_diversity(const float* outputs, int32_t M, int32_t B, int32_t K, int32_t kind, double sigma, double* D,
+                     void* stream);
+
 /* Ensemble weights from validation statistics (Eq. 6; reading R-GATE):
  * aggs f64 [M][FIN_AGG_LEN] = the aggregate vector of one validation fin_rollout per
  * member (deterministic: FIN_NOISE_NONE), all-reduced over ranks.  Member Sharpe =

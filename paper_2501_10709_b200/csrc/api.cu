@@ -22,6 +22,10 @@ namespace fin {
 cudaError_t launch_stock_rollout(int net, const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s);
 cudaError_t launch_crypto_market(int64_t steps, uint64_t seed, double sigma, double m0, double phi, float* rows,
                                  cudaStream_t s);
+cudaError_t launch_gae(const float* rew, const float* val, const uint8_t* done, int T, int N, double gamma,
+                       double lam, int normalise, float* adv, float* ret, cudaStream_t s);
+cudaError_t launch_kl_diversity(const float* out, int M, int B, int K, int kind, double sigma, double* D,
+                                cudaStream_t s);
 cudaError_t launch_crypto_rollout(int net, const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s);
 cudaError_t launch_mlp_probe(int net, const tc::TcParams& p, int n_rows, cudaStream_t s);
 cudaError_t launch_z1s_market(int net, const float* w1s_t, int H, const EnvDev& e, float* z1s, cudaStream_t s);
@@ -805,6 +809,28 @@ int fin_crypto_market(int64_t steps, uint64_t seed, double sigma, double m0, dou
   if (!(phi >= 0.0 && phi < 1.0)) return fail(FIN_E_CONFIG, "phi must be in [0, 1)");
   cudaError_t e = fin::launch_crypto_market(steps, seed, sigma, m0, phi, rows, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fin_crypto_market launch");
+  return FIN_OK;
+}
+
+int fin_gae(const float* reward, const float* value, const uint8_t* done, int32_t T, int32_t N, double gamma,
+            double lambda, int32_t normalise, float* adv, float* ret, void* stream) {
+  if (!reward || !value || !done || !adv || !ret) return fail(FIN_E_CONFIG, "fin_gae: null argument");
+  if (T < 1 || N < 1) return fail(FIN_E_CONFIG, "fin_gae: need T >= 1 and N >= 1");
+  if (!(gamma >= 0.0 && gamma <= 1.0) || !(lambda >= 0.0 && lambda <= 1.0))
+    return fail(FIN_E_CONFIG, "fin_gae: gamma and lambda must be in [0, 1]");
+  cudaError_t e = fin::launch_gae(reward, value, done, T, N, gamma, lambda, normalise, adv, ret, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_gae launch");
+  return FIN_OK;
+}
+
+int fin_kl_diversity(const float* outputs, int32_t M, int32_t B, int32_t K, int32_t kind, double sigma, double* D,
+                     void* stream) {
+  if (!outputs || !D) return fail(FIN_E_CONFIG, "fin_kl_diversity: null argument");
+  if (M < 1 || M > FIN_MAX_MEMBERS || B < 1 || K < 1) return fail(FIN_E_CONFIG, "fin_kl_diversity: bad sizes");
+  if (kind != 0 && kind != 1) return fail(FIN_E_CONFIG, "fin_kl_diversity: kind must be 0 or 1");
+  if (kind == 0 && !(sigma > 0.0 && std::isfinite(sigma))) return fail(FIN_E_CONFIG, "fin_kl_diversity: sigma > 0");
+  cudaError_t e = fin::launch_kl_diversity(outputs, M, B, K, kind, sigma, D, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_kl_diversity launch");
   return FIN_OK;
 }
 

@@ -48,7 +48,7 @@ FIN_AGG_LEN = 8
 EXPORTS = ("fin_env_create", "fin_env_reset", "fin_env_step", "fin_env_get_state", "fin_env_set_state",
            "fin_env_check", "fin_env_destroy", "fin_policy_create", "fin_policy_destroy", "fin_rollout",
            "fin_rollout_actions", "fin_ensemble_act", "fin_episode_metrics", "fin_mlp_forward",
-           "fin_philox_normals", "fin_member_weights", "fin_market_prepare", "fin_crypto_market", "fin_last_error", "fin_abi_version", "fin_device_check",
+           "fin_philox_normals", "fin_member_weights", "fin_market_prepare", "fin_crypto_market", "fin_gae", "fin_kl_diversity", "fin_last_error", "fin_abi_version", "fin_device_check",
            "fin_debug_trace")
 
 
@@ -101,6 +101,8 @@ _sig = {
     "fin_mlp_forward": ([_P, _P, C.c_int32, _P, _P, _P], C.c_int),
     "fin_philox_normals": ([C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int64, _P, _P], C.c_int),
     "fin_member_weights": ([_P, C.c_int32, C.c_double, C.c_double, _P, _P, _P], C.c_int),
+    "fin_gae": ([_P, _P, _P, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_int32, _P, _P, _P], C.c_int),
+    "fin_kl_diversity": ([_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, _P, _P], C.c_int),
     "fin_crypto_market": ([C.c_int64, C.c_uint64, C.c_double, C.c_double, C.c_double, _P, _P], C.c_int),
     "fin_market_prepare": ([_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_double,
                             C.c_uint64, _P, _P, _P], C.c_int),
@@ -404,3 +406,23 @@ def fin_crypto_market(steps: int, seed: int, rows, sigma: float = 1e-4, m0: floa
         raise ValueError("rows must be [steps + 1][144]")
     _check(_lib.fin_crypto_market(int(steps), int(seed), float(sigma), float(m0), float(phi),
                                   _ptr(rows, torch.float32, "rows"), _stream(stream)), "fin_crypto_market")
+
+
+def fin_gae(reward, value, done, adv, ret, gamma: float = 0.99, lam: float = 0.95, normalise: bool = False,
+            stream=None) -> None:
+    """GAE over reward / done [T][N] and value [T+1][N] (device) -> adv, ret [T][N] (device)."""
+    import torch
+    T, N = int(reward.shape[0]), int(reward.shape[1])
+    if tuple(value.shape) != (T + 1, N) or tuple(done.shape) != (T, N):
+        raise ValueError("value must be [T+1][N] and done [T][N]")
+    _check(_lib.fin_gae(_ptr(reward, torch.float32, "reward"), _ptr(value, torch.float32, "value"),
+                        _ptr(done, torch.uint8, "done"), T, N, float(gamma), float(lam), int(bool(normalise)),
+                        _ptr(adv, torch.float32, "adv"), _ptr(ret, torch.float32, "ret"), _stream(stream)), "fin_gae")
+
+
+def fin_kl_diversity(outputs, D, kind: int = 0, sigma: float = 0.1, stream=None) -> None:
+    """outputs f32 [M][B][K] (device) -> D f64 [M][M] (device), D[i][j] = mean KL(pi_j || pi_i)."""
+    import torch
+    M, B, K = (int(x) for x in outputs.shape)
+    _check(_lib.fin_kl_diversity(_ptr(outputs, torch.float32, "outputs"), M, B, K, int(kind), float(sigma),
+                                 _ptr(D, torch.float64, "D"), _stream(stream)), "fin_kl_diversity")
