@@ -133,6 +133,9 @@ struct K1Buf {
   uint4 hold[(KA + 7) / 8][kStep];
   alignas(16) int16_t act[kStep * KA];
 };
+#ifndef FIN_K1_LDS
+#define FIN_K1_LDS 1   // shared-typed trade path when every env of the warp is on the predicted day
+#endif
 #ifndef FIN_K1_NBUF
 #define FIN_K1_NBUF 2   // tile buffers: NBUF - 1 tiles in flight ahead of the one being stepped
 #endif
@@ -305,21 +308,42 @@ __global__ void __launch_bounds__(kK1Threads, FIN_K1_MINB)
     sm100::mbar_wait(&sm.rows[sb], par);
     const double* R[E];
     uint4* sv[E];
+    bool staged = true;
 #pragma unroll
     for (int q = 0; q < E; ++q) {
+      staged &= !go[q] || d[q] == sm.pred[sb];
       R[q] = static_cast<const double*>(__builtin_assume_aligned(
           (!go[q] || d[q] == sm.pred[sb]) ? sm.pr[sb] : e.px + (size_t)d[q] * kPriceRows * e.kp, 16));
       sv[q] = &sm.save[0][tid + q * kK1Threads];
     }
-    stock_trade_e<KA, E>(e, b, h, R, RS, a, sv, kStep);
     double vn[E];
-    const double* PN[E];
+#if FIN_K1_LDS
+    // the normal case (every env of the warp on the predicted day): the rows are addressed
+    // from the shared array itself, so they are read with shared loads, not generic ones
+    if (__all_sync(0xffffffffu, staged)) {
+      const double* Rs[E];
+      const double* PNs[E];
 #pragma unroll
-    for (int q = 0; q < E; ++q) {
-      vn[q] = b[q];
-      PN[q] = R[q] + kRowPN * RS;
+      for (int q = 0; q < E; ++q) Rs[q] = sm.pr[sb];
+      stock_trade_e<KA, E>(e, b, h, Rs, RS, a, sv, kStep);
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        vn[q] = b[q];
+        PNs[q] = sm.pr[sb] + kRowPN * RS;
+      }
+      stock_mark_e<KA, E>(vn, h, PNs);
+    } else
+#endif
+    {
+      stock_trade_e<KA, E>(e, b, h, R, RS, a, sv, kStep);
+      const double* PN[E];
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        vn[q] = b[q];
+        PN[q] = R[q] + kRowPN * RS;
+      }
+      stock_mark_e<KA, E>(vn, h, PN);
     }
-    stock_mark_e<KA, E>(vn, h, PN);
 #pragma unroll
     for (int q = 0; q < E; ++q) {
       if (!go[q]) continue;
