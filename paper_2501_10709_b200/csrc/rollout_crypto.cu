@@ -64,6 +64,7 @@ struct CryptoOps {
     int h, tau, t_ep;
     int act;
     int votes[3];
+    float u0, u1;      // the step's epsilon-greedy uniforms (drawn in prepare(), under layer 2)
     MetricAcc m;
     AggAcc agg;
     int cnt;
@@ -203,7 +204,21 @@ struct CryptoOps {
     return p.o.mlp_hidden + ((((size_t)t * p.M + m) * p.e.N + env) * Plan::kNH + l) * hid;
   }
 
-  __device__ __forceinline__ static void prepare(State&, const TcParams&, int, int, int) {}
+  // the step's epsilon-greedy uniforms do not depend on the network: drawn while layer 2 runs
+  __device__ __forceinline__ static void prepare(State& st, const TcParams& p, int env, int t, int m) {
+    if (!st.live || m != 0) return;
+    const EnvDev& e = p.e;
+    st.u0 = 1.f;
+    st.u1 = 0.f;
+    if (p.noise_mode == FIN_NOISE_SUPPLIED) {
+      const float* nz = p.noise + ((size_t)t * e.N + env) * 2;
+      st.u0 = __ldg(nz); st.u1 = __ldg(nz + 1);
+    } else if (p.noise_mode == FIN_NOISE_PHILOX) {
+      float u[2];
+      philox_uniform2((uint64_t)(e.env_offset + env), (uint32_t)(e.t_global + t), p.noise_seed, u);
+      st.u0 = u[0]; st.u1 = u[1];
+    }
+  }
   __device__ __forceinline__ static void consume(State& st, const TcParams& p, int env, int t, int m, const float* z) {
     if (!st.live) return;
     const EnvDev& e = p.e;
@@ -222,16 +237,7 @@ struct CryptoOps {
     best = 1;
     if (st.votes[0] > st.votes[best]) best = 0;
     if (st.votes[2] > st.votes[best]) best = 2;
-    float u0 = 1.f, u1 = 0.f;
-    if (p.noise_mode == FIN_NOISE_SUPPLIED) {
-      const float* nz = p.noise + ((size_t)t * e.N + env) * 2;
-      u0 = __ldg(nz); u1 = __ldg(nz + 1);
-    } else if (p.noise_mode == FIN_NOISE_PHILOX) {
-      float u[2];
-      philox_uniform2((uint64_t)(e.env_offset + env), (uint32_t)(e.t_global + t), p.noise_seed, u);
-      u0 = u[0]; u1 = u[1];
-    }
-    if (u0 < e.eps) best = min((int)((double)u1 * 3.0), 2);   // exact product, as the oracle
+    if (st.u0 < e.eps) best = min((int)((double)st.u1 * 3.0), 2);   // exact product, as the oracle
     st.act = best - 1;
   }
 
@@ -294,7 +300,7 @@ struct CryptoOps {
     }
     st.agg.s[FIN_AGG_SUM_REWARD] = st.rsum;
     if (p.o.agg_partial)
-      agg_group_write(st.agg, p.o.agg_partial + ((size_t)blockIdx.x * (blockDim.x / 128 - 1) + tile) * FIN_AGG_LEN, gtid,
+      agg_group_write(st.agg, p.o.agg_partial + ((size_t)blockIdx.x * p.tiles_per_cta + tile) * FIN_AGG_LEN, gtid,
                       bar_id, tile);
   }
 };

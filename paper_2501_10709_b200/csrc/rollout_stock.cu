@@ -432,7 +432,7 @@ struct StockOps {
     }
     st.agg.s[FIN_AGG_SUM_REWARD] = st.rsum;
     if (p.o.agg_partial)
-      agg_group_write(st.agg, p.o.agg_partial + ((size_t)blockIdx.x * (blockDim.x / 128 - 1) + tile) * FIN_AGG_LEN, gtid,
+      agg_group_write(st.agg, p.o.agg_partial + ((size_t)blockIdx.x * p.tiles_per_cta + tile) * FIN_AGG_LEN, gtid,
                       bar_id, tile);
   }
 };

@@ -67,6 +67,7 @@ struct TcParams {
   const uint16_t* x_in;
   float* z_out;
   int32_t B, in_dim, out_dim;
+  int32_t tiles_per_cta;                  // set by launch(): aggregate partial rows per CTA
 };
 
 // debug timeline (fin_debug_trace): block 0 only, one slot per event.  Compiled in only
@@ -508,7 +509,9 @@ cudaError_t launch(const TcParams& p, int n_envs, cudaStream_t s) {
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (err != cudaSuccess) return err;
   const int per_cta = kTileM * TILES;
-  kern<<<(n_envs + per_cta - 1) / per_cta, 128 + 128 * TILES * SPLIT, bytes, s>>>(p);
+  TcParams q = p;
+  q.tiles_per_cta = TILES;
+  kern<<<(n_envs + per_cta - 1) / per_cta, 128 + 128 * TILES * SPLIT, bytes, s>>>(q);
   return cudaGetLastError();
 }
 

@@ -360,7 +360,7 @@ def test_fused_crypto_rollout_teacher_forced(dims):
                 reward=zeros((T, N), torch.float32), done=zeros((T, N), torch.uint8),
                 mlp_out=zeros((T, N, 3), torch.float32), mlp_hidden=zeros((T, N, *_hid_shape(dims)), torch.int16),
                 ep_metrics=zeros((2, N, 3), torch.float64),
-                ep_count=zeros(N, torch.int32))
+                ep_count=zeros(N, torch.int32), agg=zeros(8, torch.float64))
     fin.fin_rollout(env, [pol], T, fin.make_noise(fin.FIN_NOISE_SUPPLIED, 0, dev(uni)), fin.make_traj(**logs))
     g = {k: host(v) for k, v in logs.items()}
     assert fin.fin_env_check(env) == 0
@@ -386,6 +386,9 @@ def test_fused_crypto_rollout_teacher_forced(dims):
         assert np.array_equal(np.array(o["cash"]), g["cash"][t]) and np.array_equal(np.array(o["asset"]), g["asset"][t])
         np.testing.assert_allclose(g["reward"][t], np.array(o["reward"]), rtol=1e-5, atol=1e-3)
     assert g["done"][-1].all() and np.all(g["ep_count"] == 1)
+    # the per-rank aggregate (one partial row per tile, also with column-split epilogues)
+    assert g["agg"][fin.FIN_AGG_EPISODES] == N
+    np.testing.assert_allclose(g["agg"][fin.FIN_AGG_SUM_REWARD], g["reward"].astype(np.float64).sum(), rtol=1e-9)
     for i in range(0, N, 37):
         eq = [1e6] + list(g["asset"][:, i])
         np.testing.assert_allclose(g["ep_metrics"][0, i], omet.episode_metrics(eq), rtol=1e-7, atol=1e-12)
