@@ -310,6 +310,7 @@ int fin_env_create(const fin_env_config* cfg, const float* market, int64_t marke
   const size_t n8 = N * 8;  // cash + 6 metric doubles
   size_t bytes = 8 * n8 * sizeof(double) / 8;   // 8 double arrays
   bytes += N * 4 * sizeof(int32_t);              // t_ep, window, tau, m_n
+  bytes += N * FIN_AGG_LEN * sizeof(double) + 16; // per-env aggregate partials
   const size_t KO = (K + 7) / 8;                 // holdings: asset octets (hold_at)
   bytes += KO * 8 * N * sizeof(int16_t);
   bytes += 256;
@@ -337,6 +338,7 @@ int fin_env_create(const fin_env_config* cfg, const float* market, int64_t marke
   d.tau = reinterpret_cast<int32_t*>(take(N * 4));
   d.m_n = reinterpret_cast<int32_t*>(take(N * 4));
   d.hold = reinterpret_cast<int16_t*>(take(KO * 8 * N * 2));
+  d.agg_env = reinterpret_cast<double*>(take(N * FIN_AGG_LEN * 8));
   if ((size_t)(p - static_cast<uint8_t*>(env->state_mem)) > bytes) {
     cudaFree(env->state_mem);
     delete env;

@@ -47,6 +47,8 @@ struct EnvDev {
   double* m_mean;        // Welford mean of returns
   double* m_m2;          // Welford M2
   int32_t* m_n;          // number of returns
+  double* agg_env;       // [FIN_AGG_LEN][N] per-env aggregate partials of the running rollout (fused
+                         // stock rollout: touched once per episode, kept out of the registers)
   uint32_t* flags;       // sticky device error word
 };
 
@@ -239,6 +241,22 @@ __device__ __forceinline__ void agg_episode(AggAcc& a, const double m[3]) {
   a.s[FIN_AGG_SUM_MDD] += m[2];
   a.s[FIN_AGG_MIN_MDD] = fmin(a.s[FIN_AGG_MIN_MDD], m[2]);
   a.s[7] = fmin(a.s[7], m[0]);
+}
+
+// the same accumulator kept in global memory, element j of env i at base[j * stride]
+__device__ __forceinline__ void agg_init_g(double* base, size_t stride) {
+  AggAcc a;
+  agg_init(a);
+#pragma unroll
+  for (int j = 0; j < FIN_AGG_LEN; ++j) base[j * stride] = a.s[j];
+}
+__device__ __forceinline__ void agg_episode_g(double* base, size_t stride, const double m[3]) {
+  AggAcc a;
+#pragma unroll
+  for (int j = 0; j < FIN_AGG_LEN; ++j) a.s[j] = base[j * stride];
+  agg_episode(a, m);
+#pragma unroll
+  for (int j = 0; j < FIN_AGG_LEN; ++j) base[j * stride] = a.s[j];
 }
 
 // Block-wide deterministic reduction (blockDim.x a multiple of 32, <= 1024).

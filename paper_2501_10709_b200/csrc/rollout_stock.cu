@@ -86,8 +86,7 @@ struct StockOps {
     float asum[KA];
     float eps[KA];     // this member's noise of the step (prepare(), while layer 2 runs)
     float ou[KOU];
-    MetricAcc m;
-    AggAcc agg;
+    MetricAcc m;       // (the aggregate partials live in e.agg_env: touched once per episode)
     int cnt;
     double rsum;
     bool oor, bad, nonfinite;
@@ -105,7 +104,7 @@ struct StockOps {
     st.sb = 0;
     st.kcur = st.koth = -1;
     st.pend = -1;
-    agg_init(st.agg);
+    if (st.live) agg_init_g(e.agg_env + env, (size_t)e.N);
     if (st.live) {
       st.b = e.cash[env];
       st.vc = e.vcur[env];
@@ -389,7 +388,7 @@ struct StockOps {
               dst[0] = em[0]; dst[1] = em[1]; dst[2] = em[2];
             }
             ++st.cnt;
-            agg_episode(st.agg, em);
+            agg_episode_g(e.agg_env + env, (size_t)e.N, em);
             if (e.autoreset) {
               st.b = e.cash0;
 #pragma unroll
@@ -430,9 +429,15 @@ struct StockOps {
       if (st.bad) set_flag(e, FIN_FLAG_BAD_INDEX);
       if (st.nonfinite) set_flag(e, FIN_FLAG_NONFINITE);
     }
-    st.agg.s[FIN_AGG_SUM_REWARD] = st.rsum;
+    AggAcc agg;
+    agg_init(agg);
+    if (st.live) {
+#pragma unroll
+      for (int j = 0; j < FIN_AGG_LEN; ++j) agg.s[j] = e.agg_env[(size_t)j * e.N + env];
+    }
+    agg.s[FIN_AGG_SUM_REWARD] = st.rsum;
     if (p.o.agg_partial)
-      agg_group_write(st.agg, p.o.agg_partial + ((size_t)blockIdx.x * p.tiles_per_cta + tile) * FIN_AGG_LEN, gtid,
+      agg_group_write(agg, p.o.agg_partial + ((size_t)blockIdx.x * p.tiles_per_cta + tile) * FIN_AGG_LEN, gtid,
                       bar_id, tile);
   }
 };
