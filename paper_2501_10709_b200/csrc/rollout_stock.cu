@@ -34,6 +34,10 @@ __device__ __forceinline__ uint32_t bf16_bits(float v) {
   return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v));
 }
 
+#ifndef FIN_NOISE_LATE
+#define FIN_NOISE_LATE 1   // draw the step's noise inside consume (1), or under layer 2 (0: 3.6% slower, A/B round 1)
+#endif
+
 // tanh(x) = sign(x) (1 - 2 / (exp(2|x|) + 1)) with the fast exp / reciprocal: absolute
 // error ~1e-7 (the sampled share count 100 a moves by ~1e-5, well inside the 1e-4
 // rounding-boundary allowance of the parity check); ~8 instructions instead of the
@@ -255,6 +259,9 @@ struct StockOps {
   // the member's noise for this step: Philox4x32-10 + Box-Muller (R-NOISE) or the
   // supplied normals; independent of the network output, so it runs while layer 2 does
   __device__ __forceinline__ static void prepare(State& st, const TcParams& p, int env, int t, int m) {
+#if FIN_NOISE_LATE
+    return;   // drawn inside consume (no noise registers live across the layer-2 epilogue)
+#endif
     if (!st.live) return;
     const EnvDev& e = p.e;
     const float* nz = p.noise + (((size_t)t * p.M + m) * e.N + env) * KA;
@@ -295,8 +302,28 @@ struct StockOps {
 #pragma unroll
     for (int pb = 0; pb < (KA + 7) / 8; ++pb) {
       float eps[8];
+#if FIN_NOISE_LATE
+      {
+        const float* nz = p.noise + (((size_t)t * p.M + m) * e.N + env) * KA;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) eps[j] = 0.f;
+        if (p.noise_mode == FIN_NOISE_PHILOX) {
+          const Normals8 nv =
+              philox_normals8_v((uint64_t)(e.env_offset + env), (uint32_t)(e.t_global + t),
+                                ((uint32_t)m << 16) | (uint32_t)(2 * pb), ((uint32_t)m << 16) | (uint32_t)(2 * pb + 1),
+                                p.noise_seed);
+          eps[0] = nv.a.x; eps[1] = nv.a.y; eps[2] = nv.a.z; eps[3] = nv.a.w;
+          eps[4] = nv.b.x; eps[5] = nv.b.y; eps[6] = nv.b.z; eps[7] = nv.b.w;
+        } else if (p.noise_mode == FIN_NOISE_SUPPLIED) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (pb * 8 + j < KA) eps[j] = __ldg(nz + pb * 8 + j);
+        }
+      }
+#else
 #pragma unroll
       for (int j = 0; j < 8; ++j) eps[j] = pb * 8 + j < KA ? st.eps[pb * 8 + j] : 0.f;
+#endif
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int k = pb * 8 + j;
