@@ -70,6 +70,10 @@ struct TcParams {
   int32_t tiles_per_cta;                  // set by launch(): aggregate partial rows per CTA
 };
 
+#ifndef FIN_PREPARE_LAYER
+#define FIN_PREPARE_LAYER 0   // Ops::prepare runs after the kick of layer FIN_PREPARE_LAYER + 1
+#endif
+
 // debug timeline (fin_debug_trace): block 0 only, one slot per event.  Compiled in only
 // with -DFIN_TRACE (FIN_NVCC_FLAGS=-DFIN_TRACE): the per-event predicates alone cost ~4%
 // of the headline rollout (A/B, round 1), so production builds carry none.
@@ -200,9 +204,14 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
   // (two tiles, one CTA per SM: 4 x 40 + 8 x 232 warps' worth = 64 K registers; one tile, two
   // CTAs per SM: each CTA 4 x 40 + 4 x 216 of its 128-per-thread launch allocation)
   constexpr bool kSplitRegs = (TILES == 2 && MINB == 1) || (TILES == 1 && MINB == 2);
-  constexpr uint32_t kEnvRegs = TILES == 2 ? 232 : 216;
+#ifndef FIN_DUAL_LOW_REGS
+#define FIN_DUAL_LOW_REGS 40   // producer / MMA warpgroup registers in the dual layout
+#endif
+  // dual layout (one tile, two CTAs per SM): 128 x (low + env) = 32 K registers per CTA
+  constexpr uint32_t kLowRegs = TILES == 2 ? 40 : FIN_DUAL_LOW_REGS;
+  constexpr uint32_t kEnvRegs = TILES == 2 ? 232 : 256 - kLowRegs;
   if (warp < 4) {
-  if constexpr (kSplitRegs) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+  if constexpr (kSplitRegs) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kLowRegs) : "memory");
   if (warp == 0) {
     // ============================ producer ============================
     if (lane == 0) {
@@ -460,7 +469,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
           kick(m, l + 1);
           // work that does not depend on the network output (e.g. the step's noise)
           // overlaps the largest MMA (layer 2) instead of following the last one
-          if (l == 0) Ops::prepare(st, p, env, t, m);
+          if (l == (Plan::kNH > FIN_PREPARE_LAYER ? FIN_PREPARE_LAYER : Plan::kNH - 1)) Ops::prepare(st, p, env, t, m);
           FIN_TR(row == 0 && tile == 0 && m == 0, t, 3 + 2 * l);
         }
         // output layer
