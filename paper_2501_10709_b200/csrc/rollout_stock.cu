@@ -57,6 +57,7 @@ template <int KA, int IA, class Plan, bool ENS = true, bool LOG = true>
 struct StockOps {
   static constexpr int KOU = ENS ? KA : 1;
   static constexpr bool kSplitOK = false;
+  static constexpr bool kEpiPipe = false;
   static constexpr int KP4 = (KA + 3) / 4 * 4;
   static constexpr int IN = 1 + 2 * KA + IA * KA;
   static constexpr int KT8 = Plan::kIn / 8;
@@ -476,6 +477,7 @@ template <class Plan, class Obs>
 struct ProbeOps {
   static constexpr int kStageBytes = 16;
   static constexpr bool kSplitOK = false;
+  static constexpr bool kEpiPipe = false;
   static constexpr bool kFactored = !std::is_void<Obs>::value;
   struct State {
     int b;
