@@ -212,3 +212,82 @@ def test_crypto_step_parity():
         assert np.array_equal(host(d).astype(bool), np.array(o["done"]))
         np.testing.assert_allclose(host(r), np.array(o["reward"]), rtol=1e-5, atol=1e-3)
     assert fin.fin_env_check(env) == 0
+
+
+def _bench_cfg(fin, N):
+    """The env of bench.py's HBM runs (C1 market, 1008 rows, 30-step episodes, 195 windows)."""
+    kw = dict(num_envs=N, num_assets=30, num_indicators=8, num_rows=1008, episode_len=30, window_stride=5,
+              num_windows=195, window_block=128)
+    return stock_pair(**kw)
+
+
+def _sample(N, n, seed):
+    rng = np.random.default_rng(seed)
+    return sorted(set([0, 127, 128, N - 1] + list(rng.choice(N, n, replace=False))))
+
+
+def test_k1_bench_size_sampled():
+    """K1 in the bench's launch configuration (N = 2^22 envs, persistent grid, TMA tile
+    pipeline), 35 steps with a reset, fresh seeded actions every step: sampled envs
+    (tile edges included) against the oracle run env by env -- holdings, done, cash
+    bit-exact, reward within tolerance, final state."""
+    import torch
+    fin = _fin()
+    N, T, K = 1 << 22, 35, 30
+    m = market.stock_c1(rows=1008)
+    ocfg, fcfg = _bench_cfg(fin, N)
+    env = fin.fin_env_create(fcfg, m.market)
+    cols = _sample(N, 40, 3)
+    idx = torch.tensor(cols, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(11)
+    acts, rew, done, cash = [], [], [], []
+    for t in range(T):
+        a = torch.randint(-100, 101, (N, K), device="cuda", generator=g, dtype=torch.int16)
+        r, d, c = zeros(N, torch.float32), zeros(N, torch.uint8), zeros(N, torch.float64)
+        fin.fin_env_step(env, a, fin.make_traj(reward=r, done=d, cash=c))
+        acts.append(host(a[idx]))
+        rew.append(host(r[idx])); done.append(host(d[idx])); cash.append(host(c[idx]))
+    hold = zeros((N, K), torch.int16)
+    fin.fin_env_get_state(env, hold=hold)
+    hold = host(hold[idx])
+    assert fin.fin_env_check(env) == 0
+    acts, rew, done, cash = (np.stack(x) for x in (acts, rew, done, cash))
+    for j, i in enumerate(cols):
+        oc = ostock.StockEnvConfig(num_envs=1, env_offset=int(i), num_assets=30, num_indicators=8, num_rows=1008,
+                                   episode_len=30, window_stride=5, num_windows=195, window_block=128)
+        o, st = ostock.run_actions(oc, m.market, acts[:, j:j + 1])
+        assert np.array_equal(o["done"][:, 0], done[:, j] > 0)
+        assert np.array_equal(o["cash"][:, 0], cash[:, j])
+        err = np.abs(rew[:, j].astype(np.float64) - o["reward"][:, 0])
+        assert np.all(err <= 1e-5 * np.abs(o["reward"][:, 0]) + 1e-5 * 2.0 ** -12 * 1e4)
+        assert np.array_equal(np.asarray(st.hold)[0], hold[j])
+
+
+def test_k4_bench_size_sampled():
+    """K4 replay in the bench's configuration (N = 2^20 envs, T = 32, actions [T][N][K]
+    resident in HBM): sampled envs against the oracle."""
+    import torch
+    fin = _fin()
+    N, T, K = 1 << 20, 32, 30
+    m = market.stock_c1(rows=1008)
+    ocfg, fcfg = _bench_cfg(fin, N)
+    env = fin.fin_env_create(fcfg, m.market)
+    g = torch.Generator(device="cuda").manual_seed(12)
+    acts = torch.randint(-100, 101, (T, N, K), device="cuda", generator=g, dtype=torch.int16)
+    rew, done = zeros((T, N), torch.float32), zeros((T, N), torch.uint8)
+    fin.fin_rollout_actions(env, acts, T, fin.make_traj(reward=rew, done=done))
+    assert fin.fin_env_check(env) == 0
+    cols = _sample(N, 40, 4)
+    idx = torch.tensor(cols, device="cuda")
+    a, r, d = host(acts[:, idx]), host(rew[:, idx]), host(done[:, idx])
+    cash = zeros(N, torch.float64)
+    fin.fin_env_get_state(env, cash=cash)
+    cash = host(cash[idx])
+    for j, i in enumerate(cols):
+        oc = ostock.StockEnvConfig(num_envs=1, env_offset=int(i), num_assets=30, num_indicators=8, num_rows=1008,
+                                   episode_len=30, window_stride=5, num_windows=195, window_block=128)
+        o, st = ostock.run_actions(oc, m.market, a[:, j:j + 1])
+        assert np.array_equal(o["done"][:, 0], d[:, j] > 0)
+        err = np.abs(r[:, j].astype(np.float64) - o["reward"][:, 0])
+        assert np.all(err <= 1e-5 * np.abs(o["reward"][:, 0]) + 1e-5 * 2.0 ** -12 * 1e4)
+        assert np.asarray(st.cash)[0] == cash[j]
