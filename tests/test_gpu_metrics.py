@@ -73,3 +73,36 @@ def test_episode_metrics_flat_equity():
         assert (ec == 2).all()
         assert (em[:, :, 0] == 0).all() and (em[:, :, 2] == 0).all()
         assert np.isnan(em[:, :, 1]).all()
+
+
+def test_episode_metrics_bench_size_sampled():
+    """K6 in the bench's configuration (T = 2048, N = 2^18, lockstep 30-step episodes, the
+    TMA-staged fused pass): sampled envs against the oracle's two-pass metrics."""
+    import torch
+    from paper_2501_10709_b200 import fin
+    T, N = 2048, 1 << 18
+    g = torch.Generator(device="cuda").manual_seed(5)
+    done = torch.zeros((T, N), dtype=torch.uint8, device="cuda")
+    done[29::30] = 1
+    eq = 1e6 * torch.exp(torch.cumsum(0.01 * torch.randn((T + 1, N), device="cuda", generator=g,
+                                                         dtype=torch.float64), 0))
+    E = T // 30 + 1
+    em, ec = zeros((E, N, 3), torch.float64), zeros(N, torch.int32)
+    fin.fin_episode_metrics(eq, done, 1e6, 252.0, 0.0, em, ec)
+    rng = np.random.default_rng(6)
+    cols = sorted(set([0, 127, 128, N - 1] + list(rng.choice(N, 28, replace=False))))
+    idx = torch.tensor(cols, device="cuda")
+    e_h, d_h, em_h, ec_h = host(eq[:, idx]), host(done[:, idx]), host(em[:, idx]), host(ec[idx])
+    for j in range(len(cols)):
+        # episodes after the first restart from the reset equity 1e6
+        curves = []
+        cur = [float(e_h[0, j])]
+        for t in range(T):
+            cur.append(float(e_h[t + 1, j]))
+            if d_h[t, j]:
+                curves.append(cur)
+                cur = [1e6]
+        assert ec_h[j] == len(curves)
+        for k, cv in enumerate(curves):
+            cum, sh, mdd = omet.episode_metrics(cv)
+            np.testing.assert_allclose(em_h[k, j], [cum, sh, mdd], rtol=1e-7, atol=1e-12)
