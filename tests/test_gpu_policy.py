@@ -514,3 +514,42 @@ def test_z1s_cache_follows_the_member_list():
     for x, y in zip(seq, ref):
         assert np.array_equal(x, y)
     assert not np.array_equal(seq[0], seq[1])
+
+
+def test_crypto_bench_call_sampled():
+    """One call of the C3 bench (4,096 envs, 48,000 one-second steps, Philox epsilon-greedy,
+    the column-split resident-weight kernel): on sampled envs every executed action equals
+    the oracle's epsilon-greedy rule applied to the GPU's Q-values with the oracle's own
+    Philox uniforms, the oracle env replays the actions with cash / position bit-exact,
+    and the Q-values match the oracle's forward pass on its replayed observations."""
+    import torch
+    fin = _fin()
+    N, T = 4096, 48000
+    rows = market.crypto_market(T, seed=41)
+    eps = float(np.float32(0.005))
+    fcfg = fin.env_config(task=fin.FIN_CRYPTO, num_envs=N, num_assets=1, num_indicators=0, num_rows=T + 1,
+                          episode_len=T, reward_scale=1.0, cost_rate=0.0, epsilon=eps)
+    env = fin.fin_env_create(fcfg, rows)
+    layers = spol.kaiming_bf16(spol.CRYPTO_DIMS, 4)
+    pol = fin.fin_policy_create(fin.FIN_Q_ARGMAX, layers)
+    logs = dict(actions=zeros((T, N, 1), torch.int16), cash=zeros((T, N), torch.float64),
+                hold=zeros((T, N, 1), torch.int16), mlp_out=zeros((T, N, 3), torch.float32))
+    fin.fin_rollout(env, [pol], T, fin.make_noise(fin.FIN_NOISE_PHILOX, 43), fin.make_traj(**logs))
+    assert fin.fin_env_check(env) == 0
+    cols = [0, 1234, N - 1]
+    idx = torch.tensor(cols, device="cuda")
+    g = {k: host(v[:, idx]) for k, v in logs.items()}
+    L64 = omlp.layers_f64(layers)
+    for j, i in enumerate(cols):
+        ocfg = ocry.CryptoEnvConfig(num_envs=1, episode_len=T)
+        st = ocry.reset(ocfg)
+        for t in range(T):
+            q = g["mlp_out"][t, j].astype(np.float64)
+            u0, u1 = ophx.crypto_uniforms(43, i, t)
+            a = opol.epsilon_greedy(list(q), eps, u0, u1) - 1
+            assert a == g["actions"][t, j, 0], (i, t)
+            if t in (0, 24000, T - 1):
+                X = orol.crypto_obs_batch(ocfg, st, rows)
+                _mlp_close(q[None, :], omlp.forward(L64, X))
+            o = ocry.step(ocfg, st, rows, [a])
+            assert o["pos"][0] == g["hold"][t, j, 0] and o["cash"][0] == g["cash"][t, j], (i, t)
