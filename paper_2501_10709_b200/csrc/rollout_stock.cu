@@ -35,7 +35,7 @@ __device__ __forceinline__ uint32_t bf16_bits(float v) {
 }
 
 #ifndef FIN_NOISE_LATE
-#define FIN_NOISE_LATE 1   // draw the step's noise inside consume (1), or under layer 2 (0: 3.6% slower, A/B round 1)
+#define FIN_NOISE_LATE 1   // 1: noise in consume for the single policy, under layer 2 for ensembles
 #endif
 
 // tanh(x) = sign(x) (1 - 2 / (exp(2|x|) + 1)) with the fast exp / reciprocal: absolute
@@ -58,6 +58,10 @@ struct StockOps {
   static constexpr int KOU = ENS ? KA : 1;
   static constexpr bool kSplitOK = false;
   static constexpr bool kEpiPipe = false;
+  // where the step's noise is drawn: inside consume for the single policy (+3.6%: no noise
+  // registers live across the layer-2 epilogue), under layer 2 for ensembles (FIN_NOISE_LATE
+  // overrides: 0 never late, 2 always late)
+  static constexpr bool kNoiseLate = FIN_NOISE_LATE == 2 || (FIN_NOISE_LATE == 1 && !ENS);
   static constexpr int KP4 = (KA + 3) / 4 * 4;
   static constexpr int IN = 1 + 2 * KA + IA * KA;
   static constexpr int KT8 = Plan::kIn / 8;
@@ -260,9 +264,7 @@ struct StockOps {
   // the member's noise for this step: Philox4x32-10 + Box-Muller (R-NOISE) or the
   // supplied normals; independent of the network output, so it runs while layer 2 does
   __device__ __forceinline__ static void prepare(State& st, const TcParams& p, int env, int t, int m) {
-#if FIN_NOISE_LATE
-    return;   // drawn inside consume (no noise registers live across the layer-2 epilogue)
-#endif
+    if constexpr (kNoiseLate) return;   // drawn inside consume (no noise registers live across epilogues)
     if (!st.live) return;
     const EnvDev& e = p.e;
     const float* nz = p.noise + (((size_t)t * p.M + m) * e.N + env) * KA;
@@ -303,8 +305,7 @@ struct StockOps {
 #pragma unroll
     for (int pb = 0; pb < (KA + 7) / 8; ++pb) {
       float eps[8];
-#if FIN_NOISE_LATE
-      {
+      if constexpr (kNoiseLate) {
         const float* nz = p.noise + (((size_t)t * p.M + m) * e.N + env) * KA;
 #pragma unroll
         for (int j = 0; j < 8; ++j) eps[j] = 0.f;
@@ -320,11 +321,10 @@ struct StockOps {
           for (int j = 0; j < 8; ++j)
             if (pb * 8 + j < KA) eps[j] = __ldg(nz + pb * 8 + j);
         }
-      }
-#else
+      } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) eps[j] = pb * 8 + j < KA ? st.eps[pb * 8 + j] : 0.f;
-#endif
+        for (int j = 0; j < 8; ++j) eps[j] = pb * 8 + j < KA ? st.eps[pb * 8 + j] : 0.f;
+      }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int k = pb * 8 + j;
