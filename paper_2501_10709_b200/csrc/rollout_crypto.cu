@@ -64,7 +64,7 @@ struct CryptoOps {
     double b;
     int h, tau, t_ep;
     int act;
-    int votes[3];
+    int vote0, vote1, vote2;   // (scalars: a dynamically indexed array would live in local memory)
     float u0, u1;      // the step's epsilon-greedy uniforms (drawn in prepare(), under layer 2)
     MetricAcc m;
     AggAcc agg;
@@ -227,17 +227,23 @@ struct CryptoOps {
       float* dst = p.o.mlp_out + (((size_t)t * p.M + m) * e.N + env) * 3;
       dst[0] = z[0]; dst[1] = z[1]; dst[2] = z[2];
     }
+    // argmax, lowest index on ties (no dynamic indexing of z: it would go to local memory)
+    const float z0 = z[0], z1 = z[1], z2 = z[2];
     int best = 0;
-    if (z[1] > z[best]) best = 1;
-    if (z[2] > z[best]) best = 2;
-    if (!(isfinite(z[0]) && isfinite(z[1]) && isfinite(z[2]))) { st.nonfinite = true; best = 1; }
-    if (m == 0) st.votes[0] = st.votes[1] = st.votes[2] = 0;
-    st.votes[best] += 1;
+    float bv = z0;
+    if (z1 > bv) { best = 1; bv = z1; }
+    if (z2 > bv) best = 2;
+    if (!(isfinite(z0) && isfinite(z1) && isfinite(z2))) { st.nonfinite = true; best = 1; }
+    if (m == 0) st.vote0 = st.vote1 = st.vote2 = 0;
+    st.vote0 += best == 0;
+    st.vote1 += best == 1;
+    st.vote2 += best == 2;
     if (m + 1 < p.M) return;
     // plurality; ties to hold (index 1), then to the lowest index
     best = 1;
-    if (st.votes[0] > st.votes[best]) best = 0;
-    if (st.votes[2] > st.votes[best]) best = 2;
+    int bc = st.vote1;
+    if (st.vote0 > bc) { best = 0; bc = st.vote0; }
+    if (st.vote2 > bc) best = 2;
     if (st.u0 < e.eps) best = min((int)((double)st.u1 * 3.0), 2);   // exact product, as the oracle
     st.act = best - 1;
   }
