@@ -559,7 +559,7 @@ cudaError_t launch_auto(const TcParams& p, int n_envs, int* tiles, cudaStream_t 
   const bool pair = mode && mode[0] == 'p';
   if constexpr (!RES) {
     // two CTAs must fit one SM's shared memory (the bias of up to 4 members is staged)
-    const bool fits = 2 * tc::Smem<Plan, RES, 1, Ops, kDualRing>::total(p.M) <= tc::kSmemLimit;
+    const bool fits = 2 * tc::Smem<Plan, RES, 1, Ops, kDualRing>::total(p.M, p.n_bias_staged) <= tc::kSmemLimit;
     if (!pair && fits && n_tiles > num_sms()) {
       *tiles = 1;
       return tc::launch<Plan, RES, 1, Ops, kDualRing, 2>(p, n_envs, s);

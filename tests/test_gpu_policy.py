@@ -553,3 +553,33 @@ def test_crypto_bench_call_sampled():
                 _mlp_close(q[None, :], omlp.forward(L64, X))
             o = ocry.step(ocfg, st, rows, [a])
             assert o["pos"][0] == g["hold"][t, j, 0] and o["cash"][0] == g["cash"][t, j], (i, t)
+
+
+def test_ensemble_dual_layout_matches_one_tile_per_cta():
+    """The C2 ensemble (PPO / SAC / DDPG, zero biases: nothing staged for them) runs in the
+    dual layout once tiles outnumber SMs; N = 19,200 (150 tiles), 5-day test windows that
+    advance, Philox noise, T = 12: bitwise equal to the same envs as two handles of 9,600
+    (75 tiles each, one tile per CTA -- the path the teacher-forced C2 test checks)."""
+    import torch
+    fin = _fin()
+    m = market.stock_c1(rows=1008)
+    spec = [(1, fin.FIN_PPO_GAUSS), (2, fin.FIN_SAC_SQUASH), (3, fin.FIN_DDPG_OU)]
+    pols = [fin.fin_policy_create(k, spol.kaiming_bf16(spol.STOCK_DIMS, s)) for s, k in spec]
+    N, T, H = 19200, 12, 9600
+    kw = dict(num_assets=30, num_indicators=8, num_rows=1008, episode_len=5, window_stride=5, window_offset=35,
+              num_windows=194, window_block=128, advance_window_on_reset=True)
+    res = []
+    for lo, hi in ((0, N), (0, H), (H, N)):
+        _, fcfg = stock_pair(num_envs=hi - lo, env_offset=lo, **kw)
+        env = fin.fin_env_create(fcfg, m.market)
+        n = hi - lo
+        logs = dict(actions=zeros((T, n, 30), torch.int16), cash=zeros((T, n), torch.float64),
+                    reward=zeros((T, n), torch.float32), done=zeros((T, n), torch.uint8),
+                    ep_metrics=zeros((3, n, 3), torch.float64), ep_count=zeros(n, torch.int32))
+        fin.fin_rollout(env, pols, T, fin.make_noise(fin.FIN_NOISE_PHILOX, 33), fin.make_traj(**logs))
+        assert fin.fin_env_check(env) == 0
+        res.append({k: host(v) for k, v in logs.items()})
+    for k in res[0]:
+        ax = 1 if res[0][k].ndim >= 2 and k != "ep_count" else 0
+        assert np.array_equal(res[0][k], np.concatenate([res[1][k], res[2][k]], axis=ax), equal_nan=True), k
+    assert res[0]["done"].sum() == 2 * N and np.abs(res[0]["actions"]).sum() > 0
