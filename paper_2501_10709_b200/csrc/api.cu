@@ -577,9 +577,6 @@ int fill_members(fin_env* env, const fin_policy* const* members, int32_t n, cons
     p.mw[m] = member_w ? member_w[m] : 1.f;
   }
   p.n_ddpg = n_ddpg;
-  bool any_bias = false;
-  for (int m = 0; m < n; ++m) any_bias |= members[m]->bias_nz != 0;
-  p.n_bias_staged = any_bias ? (n < FIN_STAGE_MEMBERS ? n : FIN_STAGE_MEMBERS) : 0;
   if (n_ddpg > 0) {
     const int rc = ensure_ou_slots(env, n_ddpg, s);
     if (rc != FIN_OK) return rc;
@@ -771,7 +768,6 @@ int fin_mlp_forward(const fin_policy* pol, const uint16_t* x, int32_t B, float* 
   p.bias_nz[0] = pol->bias_nz;
   p.M = 1;
   p.T = 1;
-  p.n_bias_staged = pol->bias_nz ? 1 : 0;
   p.x_in = x;
   p.z_out = z;
   p.hid_out = hidden;

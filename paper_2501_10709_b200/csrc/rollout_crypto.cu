@@ -51,6 +51,7 @@ struct CryptoOps {
   static constexpr int KT8 = Plan::kIn / 8;
   static constexpr bool kSplitOK = true;        // column-split epilogues (no layer-1 addend)
   static constexpr bool kEpiPipe = true;        // double-buffered TMEM loads in the epilogues
+  static constexpr bool kStageBias = true;
   static constexpr int kOffX = 0;                               // bf16 obs row (112)
   static constexpr int kOffR = 256;                             // ring of 3 rows (3 x 144 floats)
   static constexpr int kOffT = kOffR + 3 * FIN_C_ROW * 4;

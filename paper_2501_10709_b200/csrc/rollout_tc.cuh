@@ -68,8 +68,6 @@ struct TcParams {
   float* z_out;
   int32_t B, in_dim, out_dim;
   int32_t tiles_per_cta;                  // set by launch(): aggregate partial rows per CTA
-  int32_t n_bias_staged;                  // members whose biases are staged in shared memory (0 when
-                                          // every bias is zero: the epilogues skip them, no smem needed)
 };
 
 #ifndef FIN_PREPARE_LAYER
@@ -117,10 +115,12 @@ struct Smem {
   __host__ __device__ static constexpr int w_bytes(int M) {
     return RESIDENT ? Plan::kMemberBytes * M : RING * Plan::kStageBytes;
   }
-  __host__ __device__ static constexpr int staged(int M) { return M < FIN_STAGE_MEMBERS ? M : FIN_STAGE_MEMBERS; }
-  // nb: members with staged biases (TcParams::n_bias_staged)
-  __host__ __device__ static constexpr int total(int M, int nb) { return kFixed + w_bytes(M) + nb * kBiasPerMember; }
-  __host__ __device__ static constexpr int total(int M) { return total(M, staged(M)); }
+  // members whose biases are staged in shared memory (Ops::kStageBias = false: none, the
+  // epilogues read them from L2 -- the ensemble kernels, where the smem is needed elsewhere)
+  __host__ __device__ static constexpr int staged(int M) {
+    return !Ops::kStageBias ? 0 : (M < FIN_STAGE_MEMBERS ? M : FIN_STAGE_MEMBERS);
+  }
+  __host__ __device__ static constexpr int total(int M) { return kFixed + w_bytes(M) + staged(M) * kBiasPerMember; }
   __host__ __device__ static constexpr int max_members() {   // resident plans: weights of M members in smem
     return RESIDENT ? (kSmemLimit - kStaticSmem - kFixed - FIN_STAGE_MEMBERS * kBiasPerMember) / Plan::kMemberBytes
                     : FIN_MAX_MEMBERS;
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
   const int lane = threadIdx.x & 31;
 
   // ---- one-time setup
-  for (int j = threadIdx.x; j < p.n_bias_staged * Plan::kBiasFloats; j += blockDim.x) {
+  for (int j = threadIdx.x; j < S::staged(M) * Plan::kBiasFloats; j += blockDim.x) {
     const int m = j / Plan::kBiasFloats, q = j % Plan::kBiasFloats;
     sBias[j] = p.bias[m] ? p.bias[m][q] : 0.f;
   }
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
       uint32_t d_use = 0;
       for (int t = 0; t < T; ++t) {
         for (int m = 0; m < M; ++m) {
-          const float* bias = m < p.n_bias_staged ? sBias + m * Plan::kBiasFloats : p.bias[m];
+          const float* bias = (Ops::kStageBias && m < FIN_STAGE_MEMBERS) ? sBias + m * Plan::kBiasFloats : p.bias[m];
 #pragma unroll 1
           for (int l = 0; l < Plan::kNH; ++l) {
             sm100::mbar_wait(&d_full[0], d_use & 1);
@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
         kick(m, 0);
         FIN_TR(row == 0 && tile == 0 && m == 0, t, 1);
         // biases of the first FIN_STAGE_MEMBERS members in shared memory, the rest from L2
-        const float* bias = m < p.n_bias_staged ? sBias + m * Plan::kBiasFloats : p.bias[m];
+        const float* bias = (Ops::kStageBias && m < FIN_STAGE_MEMBERS) ? sBias + m * Plan::kBiasFloats : p.bias[m];
         // hidden layers: D -> +bias -> ReLU -> bf16 -> A (K-major core matrices)
 #pragma unroll 1
         for (int l = 0; l < Plan::kNH; ++l) {
@@ -546,7 +546,7 @@ template <class Plan, bool RESIDENT, int TILES, class Ops, int RING = kRing, int
 cudaError_t launch(const TcParams& p, int n_envs, cudaStream_t s) {
   using Sm = Smem<Plan, RESIDENT, TILES, Ops, RING>;
   auto kern = k_tc_rollout<Plan, RESIDENT, TILES, Ops, RING, MINB, SPLIT>;
-  const int bytes = Sm::total(p.M, p.n_bias_staged);
+  const int bytes = Sm::total(p.M);
   if (MINB > 1 && bytes * MINB > kSmemLimit) return cudaErrorInvalidConfiguration;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (err != cudaSuccess) return err;
