@@ -52,8 +52,11 @@ struct CryptoOps {
   static constexpr bool kSplitOK = true;        // column-split epilogues (no layer-1 addend)
   static constexpr bool kEpiPipe = true;        // double-buffered TMEM loads in the epilogues
   static constexpr bool kStageBias = true;
+  static constexpr bool kL1Bcast = true;        // uniform tiles: shared layer-1 inputs read with SBO = 0
+  static constexpr int kBcastKG = KT8 - 2;      // k-groups 2.. (columns 16..) of the observation
   static constexpr int kOffX = 0;                               // bf16 obs row (112)
-  static constexpr int kOffR = 256;                             // ring of 3 rows (3 x 144 floats)
+  static constexpr int kOffB = 256;                             // kBcastKG core matrices of 8 equal rows
+  static constexpr int kOffR = kOffB + kBcastKG * 128;          // ring of 3 rows (3 x 144 floats)
   static constexpr int kOffT = kOffR + 3 * FIN_C_ROW * 4;
   static constexpr int kStageBytes = kOffT + 16;
 
@@ -131,6 +134,19 @@ struct CryptoOps {
       bar_sync128(bar_id);   // ring rows visible
       for (int idx = gtid; idx < Plan::kIn; idx += 128)
         xs[idx] = (idx >= 2 && idx < IN) ? (uint16_t)bf16_bits(mrow[FIN_C_F0 + idx - 2]) : (uint16_t)0;
+      // the same columns 16.. as core matrices of 8 identical rows (the broadcast layer-1 operand)
+      if (gtid < kBcastKG * 8) {
+        const int c0 = 8 * (2 + (gtid >> 3));
+        uint32_t w4[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i0 = c0 + 2 * j;
+          const uint32_t lo = i0 < IN ? bf16_bits(mrow[FIN_C_F0 + i0 - 2]) : 0u;
+          const uint32_t hi = i0 + 1 < IN ? bf16_bits(mrow[FIN_C_F0 + i0 - 1]) : 0u;
+          w4[j] = lo | (hi << 16);
+        }
+        reinterpret_cast<uint4*>(stg + kOffB)[gtid] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+      }
       // prefetch row t0 + 2 (the next step's marking row) into the third slot
       const int r2 = t0 + 2;
       if (r2 < e.rows && t + 1 < p.T && !held(st, r2)) {
@@ -189,6 +205,29 @@ struct CryptoOps {
         tc::sts128(xa + tc::cm_off(row, c, KT8), w4[0], w4[1], w4[2], w4[3]);
       }
     }
+  }
+
+  // resident (env-issued) layer 1: a uniform tile writes only its private k-groups 0 and 1;
+  // the MMA reads columns 16.. from the broadcast core matrices (l1_bcast)
+  __device__ __forceinline__ static void build_obs_bcast(State& st, const TcParams& p, int env, int row, int t,
+                                                         int m, uint32_t xa, uint8_t* stg) {
+    if (!st.uniform) {
+      build_obs(st, p, env, row, t, m, xa, stg);
+      return;
+    }
+    const EnvDev& e = p.e;
+    const uint4* xs = reinterpret_cast<const uint4*>(stg + kOffX);
+    const uint4 v0 = xs[0], v1 = xs[1];
+    uint32_t priv = 0u;
+    if (st.live) {
+      const float den = (float)e.max_hold;
+      priv = bf16_bits((float)st.h) | (bf16_bits(div_int_f32(st.tau, den, __frcp_rn(den))) << 16);
+    }
+    tc::sts128(xa + tc::cm_off(row, 0, KT8), priv, v0.y, v0.z, v0.w);
+    tc::sts128(xa + tc::cm_off(row, 1, KT8), v1.x, v1.y, v1.z, v1.w);
+  }
+  __device__ __forceinline__ static uint32_t l1_bcast(const State& st, uint8_t* stg) {
+    return st.uniform ? sm100::smem_u32(stg + kOffB) : 0u;
   }
 
   __device__ __forceinline__ static const float* l1_addend(State&, const TcParams&, int, uint8_t*) { return nullptr; }

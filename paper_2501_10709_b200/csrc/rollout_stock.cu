@@ -57,6 +57,7 @@ template <int KA, int IA, class Plan, bool ENS = true, bool LOG = true>
 struct StockOps {
   static constexpr int KOU = ENS ? KA : 1;
   static constexpr bool kSplitOK = false;
+  static constexpr bool kL1Bcast = false;   // (crypto only: broadcast layer-1 A operand)
   static constexpr bool kEpiPipe = false;
   // ensembles read biases from L2 (no staged copy): the C2 ensemble then fits the dual layout
   // (two CTAs per SM), 6.1e8 -> 6.8e8 env-steps/s; the single policy keeps its staged copy
@@ -481,6 +482,7 @@ struct ProbeOps {
   static constexpr int kStageBytes = 16;
   static constexpr bool kStageBias = true;
   static constexpr bool kSplitOK = false;
+  static constexpr bool kL1Bcast = false;   // (crypto only: broadcast layer-1 A operand)
   static constexpr bool kEpiPipe = false;
   static constexpr bool kFactored = !std::is_void<Obs>::value;
   struct State {

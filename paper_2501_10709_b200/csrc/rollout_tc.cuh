@@ -460,15 +460,22 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
           const uint32_t idesc = sm100::make_idesc_bf16(kTileM, Plan::nrows(l));
           const uint32_t a_base = sm100::smem_u32(sA) + (uint32_t)(tile * S::kA);
           const uint32_t d_tmem = tmem + (uint32_t)(tile * kTc);
+          // layer 1 of a tile whose envs share the step's row (Ops::kL1Bcast): k-steps >= 1 read
+          // one 8-row core-matrix column per k-group with SBO = 0, so every 8-row group of the
+          // tile sees the same shared inputs (same operand values, same MMA sequence)
+          uint32_t bc = 0;
+          if constexpr (Ops::kL1Bcast) bc = l == 0 ? Ops::l1_bcast(st, stg) : 0u;
           for (int s = Plan::first_stage(l); s < Plan::first_stage(l) + Plan::nstages(l); ++s) {
             const uint32_t b_base = sm100::smem_u32(sW) + (uint32_t)(m * Plan::kMemberBytes + Plan::offset_of(s));
             const int j0 = Plan::j0_of(s), nks = Plan::nks_of(s);
             const uint32_t b_sbo = (uint32_t)(nks * 2) * 128u;
             const uint64_t ad0 = sm100::make_sdesc(a_base + (uint32_t)j0 * 256u, 128u, a_sbo);
             const uint64_t bd0 = sm100::make_sdesc(b_base, 128u, b_sbo);
-            for (int j = 0; j < nks; ++j)
-              sm100::mma_bf16(d_tmem, ad0 + (uint64_t)(16 * j), bd0 + (uint64_t)(16 * j), idesc,
-                              (j0 + j) > 0 ? 1u : 0u);
+            for (int j = 0; j < nks; ++j) {
+              uint64_t ad = ad0 + (uint64_t)(16 * j);
+              if (bc && j0 + j > 0) ad = sm100::make_sdesc(bc + (uint32_t)(j0 + j - 1) * 256u, 128u, 0u);
+              sm100::mma_bf16(d_tmem, ad, bd0 + (uint64_t)(16 * j), idesc, (j0 + j) > 0 ? 1u : 0u);
+            }
           }
           sm100::mma_commit(&d_full[tile]);
         }
@@ -480,7 +487,8 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
       FIN_TR(row == 0 && tile == 0, t, 0);
       Ops::stage(st, p, env, gtid, t, stg, bar_id);
       for (int m = 0; m < M; ++m) {
-        Ops::build_obs(st, p, env, row, t, m, xa, stg);
+        if constexpr (Ops::kL1Bcast && kEnvIssue) Ops::build_obs_bcast(st, p, env, row, t, m, xa, stg);
+        else Ops::build_obs(st, p, env, row, t, m, xa, stg);
         kick(m, 0);
         FIN_TR(row == 0 && tile == 0 && m == 0, t, 1);
         // biases of the first FIN_STAGE_MEMBERS members in shared memory, the rest from L2
