@@ -111,10 +111,12 @@ struct CryptoOps {
     if (gtid == 0) sr[0] = st.live ? tr : -1;
     sm100::cp_async_wait<0>();      // this thread's part of the last prefetch ...
     bar_sync128(bar_id);            // ... and everyone else's
+    FIN_TR(gtid == 0, t, 20);
     st.pend = -1;
     const int t0 = sr[0];
     const bool uni = bar_red_and(bar_id, !st.live || tr == t0) && t0 >= 0;
     st.uniform = uni;
+    FIN_TR(gtid == 0, t, 21);
     if (uni) {
       float* ring = reinterpret_cast<float*>(stg + kOffR);
       // rows t0 and t0 + 1 must be in the ring; load whichever is missing
@@ -132,6 +134,7 @@ struct CryptoOps {
       const float* mrow = ring + st.slot_t * FIN_C_ROW;
       uint16_t* xs = reinterpret_cast<uint16_t*>(stg + kOffX);
       bar_sync128(bar_id);   // ring rows visible
+      FIN_TR(gtid == 0, t, 22);
       for (int idx = gtid; idx < Plan::kIn; idx += 128)
         xs[idx] = (idx >= 2 && idx < IN) ? (uint16_t)bf16_bits(mrow[FIN_C_F0 + idx - 2]) : (uint16_t)0;
       // the same columns 16.. as core matrices of 8 identical rows (the broadcast layer-1 operand)
@@ -147,6 +150,7 @@ struct CryptoOps {
         }
         reinterpret_cast<uint4*>(stg + kOffB)[gtid] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
       }
+      FIN_TR(gtid == 0, t, 27);
       // prefetch row t0 + 2 (the next step's marking row) into the third slot
       const int r2 = t0 + 2;
       if (r2 < e.rows && t + 1 < p.T && !held(st, r2)) {
@@ -157,7 +161,9 @@ struct CryptoOps {
         set_held(st, r2);
         st.pend = r2;
       }
+      FIN_TR(gtid == 0, t, 23);
       bar_sync128(bar_id);   // xs visible
+      FIN_TR(gtid == 0, t, 24);
     }
   }
 

@@ -443,6 +443,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
     Ops::init(st, p, env, row);
     uint32_t d_use = 0;
     bool w_ready = false;   // resident weights landed (env-issued MMAs)
+    int t_cur = 0;          // (the timeline's step index inside kick)
     // A operand of layer l of member m written by this thread: hand it to the tensor core
     auto kick = [&](int m, int l) {
       sm100::fence_proxy_async_smem();
@@ -451,6 +452,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
         if (SPLIT > 1 && l > 0) sm100::named_bar_sync(kSplitBar, 128 * SPLIT);   // the helpers' columns too
         else sm100::named_bar_sync(bar_id, 128);
         if (gtid == 0) {
+          FIN_TR(tile == 0 && m == 0 && l == 0, t_cur, 25);
           if (!w_ready) {
             sm100::mbar_wait(&w_full[0], 0);
             w_ready = true;
@@ -477,6 +479,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
               sm100::mma_bf16(d_tmem, ad, bd0 + (uint64_t)(16 * j), idesc, (j0 + j) > 0 ? 1u : 0u);
             }
           }
+          FIN_TR(tile == 0 && m == 0 && l == 0, t_cur, 26);
           sm100::mma_commit(&d_full[tile]);
         }
       } else {
@@ -484,6 +487,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
       }
     };
     for (int t = 0; t < T; ++t) {
+      t_cur = t;
       FIN_TR(row == 0 && tile == 0, t, 0);
       Ops::stage(st, p, env, gtid, t, stg, bar_id);
       for (int m = 0; m < M; ++m) {

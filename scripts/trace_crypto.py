@@ -31,7 +31,8 @@ torch.cuda.synchronize()
 fin.fin_debug_trace(None)
 b = buf.cpu().numpy().astype(np.int64)
 names = {0: "step", 1: "obs_done", 9: "mma:a1", 10: "mma:i1", 2: "d1", 3: "epi1", 11: "mma:a2", 12: "mma:i2",
-         4: "d2", 5: "epi2", 13: "mma:a3", 14: "mma:i3", 6: "d3", 7: "consume", 8: "env_done"}
+         4: "d2", 5: "epi2", 13: "mma:a3", 14: "mma:i3", 6: "d3", 7: "consume", 8: "env_done",
+         20: "st:wait+bar", 21: "st:red", 22: "st:ring", 27: "st:bcast", 23: "st:prefetch", 24: "st:bar", 25: "kick:bar", 26: "kick:mma"}
 for t in range(T):
     d = b[t] - b[t, 0]
     order = sorted((int(d[i]), n) for i, n in names.items() if b[t, i] != 0)

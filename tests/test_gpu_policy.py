@@ -583,3 +583,33 @@ def test_ensemble_dual_layout_matches_one_tile_per_cta():
         ax = 1 if res[0][k].ndim >= 2 and k != "ep_count" else 0
         assert np.array_equal(res[0][k], np.concatenate([res[1][k], res[2][k]], axis=ax), equal_nan=True), k
     assert res[0]["done"].sum() == 2 * N and np.abs(res[0]["actions"]).sum() > 0
+
+
+def test_crypto_tile_composition_invariance():
+    """An env's crypto rollout does not depend on its tile-mates.  Tile 0 of 4,096 envs is made
+    non-uniform (env 0 starts at row 7, its 127 tile-mates at row 0: per-env observation rows,
+    the full layer-1 issue); every other tile stays on the shared row (broadcast layer-1 operand,
+    next-step shared k-steps issued early).  Envs 1..127 must equal, bit for bit, the same envs
+    of a run where every env starts at row 0 (Philox noise keyed by the global env id)."""
+    import torch
+    fin = _fin()
+    N, T = 4096, 64
+    rows = market.crypto_market(400, seed=41)
+    cfg = fin.env_config(task=fin.FIN_CRYPTO, num_envs=N, num_assets=1, num_indicators=0, num_rows=401,
+                         episode_len=400, reward_scale=1.0, cost_rate=0.0, epsilon=0.05, seed=43)
+    pol = fin.fin_policy_create(fin.FIN_Q_ARGMAX, spol.kaiming_bf16(spol.CRYPTO_DIMS, 4))
+    out = []
+    for shifted in (False, True):
+        env = fin.fin_env_create(cfg, rows)
+        if shifted:
+            t_ep = torch.zeros(N, dtype=torch.int32, device="cuda")
+            t_ep[0] = 7
+            fin.fin_env_set_state(env, t_ep=t_ep)
+        logs = dict(actions=zeros((T, N, 1), torch.int16), cash=zeros((T, N), torch.float64),
+                    reward=zeros((T, N), torch.float32), mlp_out=zeros((T, N, 3), torch.float32))
+        fin.fin_rollout(env, [pol], T, fin.make_noise(fin.FIN_NOISE_PHILOX, 5), fin.make_traj(**logs))
+        assert fin.fin_env_check(env) == 0
+        out.append({k: host(v) for k, v in logs.items()})
+    for k in out[0]:
+        assert np.array_equal(out[0][k][:, 1:], out[1][k][:, 1:]), k
+    assert not np.array_equal(out[0]["mlp_out"][:, 0], out[1]["mlp_out"][:, 0])
