@@ -65,6 +65,7 @@ struct CryptoOps {
     int k0, k1, k2;    // market row held by ring slot 0 / 1 / 2 (-1: none); same in every thread
     int pend;          // row being prefetched (-1: none)
     int slot_t;        // ring slot of this step's row (uniform case)
+    int tprev;         // the last uniform step's row (-1: none); same in every thread
     double b;
     int h, tau, t_ep;
     int act;
@@ -88,6 +89,7 @@ struct CryptoOps {
     st.k0 = st.k1 = st.k2 = -1;
     st.pend = -1;
     st.slot_t = 0;
+    st.tprev = -1;
     agg_init(st.agg);
     if (st.live) {
       st.b = e.cash[env];
@@ -108,14 +110,23 @@ struct CryptoOps {
     int* sr = reinterpret_cast<int*>(stg + kOffT);
     int tr = st.t_ep;
     if (st.live && (tr + 1 >= e.rows)) { st.bad = true; tr = 0; }
-    if (gtid == 0) sr[0] = st.live ? tr : -1;
     sm100::cp_async_wait<0>();      // this thread's part of the last prefetch ...
-    bar_sync128(bar_id);            // ... and everyone else's
+    // Lockstep prediction: the row after the last uniform step's.  One barrier-reduction both
+    // checks it and publishes everyone's part of the prefetch; otherwise thread 0's row is
+    // exchanged through shared memory and checked.
+    const int tp = st.tprev >= 0 && st.tprev + 2 < e.rows ? st.tprev + 1 : -1;   // same in every thread
+    int t0 = tp;
+    bool uni = tp >= 0 && bar_red_and(bar_id, !st.live || tr == tp);
+    if (!uni) {
+      if (gtid == 0) sr[0] = st.live ? tr : -1;
+      bar_sync128(bar_id);            // ... and everyone else's
+      t0 = sr[0];
+      uni = bar_red_and(bar_id, !st.live || tr == t0) && t0 >= 0;
+    }
     FIN_TR(gtid == 0, t, 20);
     st.pend = -1;
-    const int t0 = sr[0];
-    const bool uni = bar_red_and(bar_id, !st.live || tr == t0) && t0 >= 0;
     st.uniform = uni;
+    st.tprev = uni ? t0 : -1;
     FIN_TR(gtid == 0, t, 21);
     if (uni) {
       float* ring = reinterpret_cast<float*>(stg + kOffR);
