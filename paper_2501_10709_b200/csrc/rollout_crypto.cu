@@ -140,11 +140,11 @@ struct CryptoOps {
         }
         set_held(st, t0);
         set_held(st, t0 + 1);
+        bar_sync128(bar_id);   // ring rows visible (prefetched rows: since the barrier above)
       }
       st.slot_t = t0 % 3;
       const float* mrow = ring + st.slot_t * FIN_C_ROW;
       uint16_t* xs = reinterpret_cast<uint16_t*>(stg + kOffX);
-      bar_sync128(bar_id);   // ring rows visible
       FIN_TR(gtid == 0, t, 22);
       for (int idx = gtid; idx < Plan::kIn; idx += 128)
         xs[idx] = (idx >= 2 && idx < IN) ? (uint16_t)bf16_bits(mrow[FIN_C_F0 + idx - 2]) : (uint16_t)0;
