@@ -112,6 +112,45 @@ def dist_info():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_launch(args) -> int | None:
+    """``--gpus N`` (N > 1) outside a torch.distributed launcher: re-exec this script as
+    N ranks (one process per GPU) under torch.distributed.run on 127.0.0.1 and return its
+    exit code.  Inside a launcher, WORLD_SIZE must equal N.  Returns None when this
+    process is a rank (or N = 1) and should run the benchmark itself."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None:
+        if int(world_env) != args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}\n")
+            return 2
+        return None
+    if args.gpus <= 1:
+        return None
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but {have} CUDA devices visible",
+                          "n_gpus": args.gpus}), flush=True)
+        return 1
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def nccl_env():
+    """NCCL's own INIT log (communicator size, transports, NVLS) on every rank's output."""
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+
+
 # ------------------------------------------------------------------ oracle (CPU) timing
 _SHARD_CACHE = {}
 
@@ -206,8 +245,12 @@ def run_ours(args):
     rank, world, local = dist_info()
     torch.cuda.set_device(local)
     if world > 1:
+        import datetime
+
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        nccl_env()
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=datetime.timedelta(minutes=30))
     from paper_2501_10709_b200 import fin
     from synth import policy as spol
     fin.fin_device_check(local)
@@ -261,13 +304,16 @@ def run_ours(args):
         with open(prof) as f:
             out["roofline"]["traffic"] = json.load(f).get("rollout_bytes_per_launch")
     out["clocks"] = cs.summary()
-    # ---- e2e through the C ABI with host buffers
-    if rank == 0 or world > 1:
-        out["e2e"] = e2e(fin, torch, env, pol, N, T, max(4, args.steps), allreduce, world)
-    if rank == 0 and not args.no_extras:
-        out["extras"] = extras(fin, torch, pol)
+    if world > 1:
+        out["nccl"] = nccl_info(torch, world)
+    # ---- e2e through the C ABI with host buffers (every rank, max over ranks)
+    out["e2e"] = e2e(fin, torch, env, pol, N, T, max(4, args.steps), allreduce, world)
     del env
-    if rank == 0:
+    # ---- the C4 sweep at this G (every rank, max over ranks)
+    out["c4_sweep"] = c4_sweep(fin, torch, pol, world, allreduce, barrier)
+    if rank == 0 and world == 1 and not args.no_extras:
+        out["extras"] = extras(fin, torch, pol)
+    if rank == 0 and world == 1:
         rate, cores, sample = oracle_rate()
         out["cpu_baseline"] = {"value": rate, "unit": "env-steps/s", "cores": cores, "kind": "oracle", "sample": sample}
         out["paper_context"] = {"note": "paper numbers are from one NVIDIA A100 with real data and PPO/DQN training "
@@ -277,7 +323,43 @@ def run_ours(args):
         print(json.dumps(out), flush=True)
     if world > 1:
         import torch.distributed as dist
+        dist.barrier()
         dist.destroy_process_group()
+
+
+def nccl_info(torch, world):
+    """The communicator as NCCL and torch see it after the timed all-reduces."""
+    import torch.distributed as dist
+    info = {"backend": dist.get_backend(), "world_size": dist.get_world_size(), "nccl_version":
+            ".".join(str(v) for v in torch.cuda.nccl.version()), "nccl_debug": os.environ.get("NCCL_DEBUG")}
+    ranks = torch.tensor([dist.get_rank()], dtype=torch.int64, device="cuda")
+    seen = [torch.zeros_like(ranks) for _ in range(world)]
+    dist.all_gather(seen, ranks)
+    info["ranks_seen"] = [int(s.item()) for s in seen]
+    return info
+
+
+def c4_sweep(fin, torch, pol, world, allreduce, barrier):
+    """BASELINE configs[4]: N/GPU in {1, 64, 2048, 16384, 65536} at T = 256 on this box's G
+    GPUs (G = world size): every rank runs its shard (env_offset = rank * N), the per-rollout
+    aggregate is all-reduced, and the rate is N * T * G / the slowest rank's time."""
+    from paper_2501_10709_b200 import dist as fdist
+    rank = int(os.environ.get("RANK", 0))
+    res = {"G": world, "T": T_HEAD, "env_steps_per_s": {}}
+    flush = L2Flush(torch)
+    for N in (1, 64, 2048, 16384, 65536):
+        env = make_env(fin, N, rank * N)
+        barrier()
+        times, _ = time_rollouts(fin, torch, env, pol, N, T_HEAD, 5, 3, flush, allreduce)
+        barrier()
+        ms = fdist.max_over_ranks(statistics.mean(times), device="cuda")
+        res["env_steps_per_s"][str(N)] = N * T_HEAD * world / (ms / 1e3)
+        del env
+    r = res["env_steps_per_s"]
+    res["same_gpu_scaling_2048_vs_1"] = r["2048"] / r["1"]
+    res["paper_same_gpu_scaling_2048_vs_1"] = {"crypto_dqn_A100": 1746.25, "stock_ppo_A100": 47.73,
+                                               "note": "P:380: GPU(2048 envs) / GPU(1 env) on one A100; context"}
+    return res
 
 
 def e2e(fin, torch, env, pol, N, T, steps, allreduce, world):
@@ -351,15 +433,10 @@ def e2e(fin, torch, env, pol, N, T, steps, allreduce, world):
 
 def extras(fin, torch, pol):
     """Secondary measurements printed inside the same JSON line (rank 0, N = 1 GPU):
-    the C4 sweep points, the exact configs[1] rollout (2048 envs, T = 30), and the
-    HBM-bound step kernel K1 at N = 2^22 against the measured HBM copy bandwidth."""
-    out = {"sweep_T256": {}}
+    the exact configs[1] rollout (2048 envs, T = 30), the HBM-bound kernels against
+    the measured HBM copy bandwidth, the crypto, ensemble and paper-net variants."""
+    out = {}
     flush = L2Flush(torch)
-    for N in (1, 64, 2048, 16384):
-        env = make_env(fin, N, 0)
-        times, _ = time_rollouts(fin, torch, env, pol, N, T_HEAD, 5, 3, flush)
-        out["sweep_T256"][str(N)] = N * T_HEAD / (statistics.mean(times) / 1e3)
-        del env
     env = make_env(fin, 2048, 0)
     times, _ = time_rollouts(fin, torch, env, pol, 2048, 30, 10, 3, flush)
     out["configs1_2048envs_T30"] = 2048 * 30 / (statistics.mean(times) / 1e3)
@@ -695,6 +772,10 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if args.impl == "ours":
+        rc = self_launch(args)
+        if rc is not None:
+            sys.exit(rc)
     if args.impl == "reference":
         run_reference(args)
     else:

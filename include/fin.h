@@ -195,6 +195,14 @@ int fin_env_set_state(fin_env* env, const double* cash, const int16_t* hold, con
  * flag is set (written to *flags, host, may be NULL); clears the word. */
 int fin_env_check(fin_env* env, uint32_t* flags /*host*/);
 
+/* Event counters of the handle (host array counters[FIN_CTR_LEN], u32; synchronises the
+ * handle's last stream; clear != 0 zeroes them afterwards):
+ *   [0] stock steps whose buys took the exact out-of-line affordability path (R5: the
+ *       fast floor estimate failed its check -- cash at or within ~1e-11 of a multiple
+ *       of the unit cost); for tests, which prove the slow path ran; the rest reserved. */
+enum { FIN_CTR_LEN = 4 };
+int fin_env_counters(fin_env* env, uint32_t* counters /*host*/, int32_t clear);
+
 void fin_env_destroy(fin_env* env);
 
 /* Create a policy / Q network (BASELINE configs[1,3]).
@@ -207,6 +215,9 @@ void fin_env_destroy(fin_env* env);
 int fin_policy_create(int32_t kind, int32_t n_layers, const int32_t* dims /*host*/,
                       const uint16_t* const* w_bf16 /*host*/, const float* const* bias /*host*/,
                       void* stream, fin_policy** out /*host*/);
+/* Waits for the policy's last use (the event recorded on the stream of the most recent
+ * call that read it; not a device-wide synchronisation), then frees it.  A caller that
+ * used one policy on several streams concurrently synchronises those streams first. */
 void fin_policy_destroy(fin_policy* policy);
 
 /* Noise source.  PHILOX: counter-based Philox4x32-10 keyed by ``seed`` and the
@@ -241,11 +252,16 @@ int fin_rollout_actions(fin_env* env, const int16_t* actions, int32_t T, const f
 
 /* Ensemble action on the current state without stepping: writes
  * actions i16 [N][K] and, if non-NULL, mean_action f32 [N][K] (the averaged
- * continuous action before rounding).  Noise uses step index t_global of the env.
- * Advances the DDPG OU state like a rollout step would only if commit_ou != 0. */
+ * continuous action before rounding).  Noise uses step index t_global of the env
+ * (supplied noise is read as [1][M][N][K]).  The env (cash, holdings, clock, metrics)
+ * is never modified.  Each DDPG member's OU state x (R19, R-OU-M) is updated-then-used
+ * for the action as in a rollout step; the updated x is written back to the env only
+ * if commit_ou != 0 (commit_ou = 0: the call is a pure function of the env state, so
+ * repeated calls return the same actions).  Same behaviour for one or several DDPG
+ * members. */
 int fin_ensemble_act(fin_env* env, const fin_policy* const* members /*host*/, int32_t n_members,
                      const float* member_w /*host*/, const fin_noise* noise /*host*/,
-                     int16_t* actions, float* mean_action, void* stream);
+                     int16_t* actions, float* mean_action, int32_t commit_ou, void* stream);
 
 /* Episode metrics from a stored equity log (Eq. 6): equity f64 [T+1][N]
  * (row 0 = equity at the start, row t = v' of transition t), done u8 [T][N] (an

@@ -46,7 +46,7 @@ def forward(layers64, x: np.ndarray) -> np.ndarray:
 FP32_ACC_BOUND = 2.0 ** -17   # reading R-TOL: fp32 accumulation error, relative to sum |w x|
 
 
-def teacher_forced_layers(layers64, x, hidden_bits, z_dev):
+def teacher_forced_layers(layers64, x, hidden_bits, z_dev, row_mask: bool = False):
     """Layer-by-layer check of a device forward pass (reading R-TOL).
 
     ``x`` [B][in] float64 unquantised observation (the oracle's own), ``hidden_bits``
@@ -60,13 +60,15 @@ def teacher_forced_layers(layers64, x, hidden_bits, z_dev):
       boundary is ambiguous (both neighbours are correct); such cases are counted.
     * output: |z_dev - z| <= delta.
     Layer 1's input is q(x) computed by the oracle, so the observation encoding is
-    checked bit-exactly through it.  Returns (n_ambiguous, n_hidden_total).
+    checked bit-exactly through it.  Returns (n_ambiguous, n_hidden_total), plus with
+    ``row_mask`` the [B] boolean mask of the rows that hold an ambiguous activation.
     """
     from .quant import bf16_fast
     h = bf16_fast(np.asarray(x, dtype=np.float64))
     hid = bf16_bits_to_f64(np.asarray(hidden_bits).view(np.uint16))
     n_amb = 0
     n_tot = 0
+    rows = np.zeros(h.shape[0], dtype=bool)
     n = len(layers64)
     for li, (w, b) in enumerate(layers64):
         z = h @ w.T + b
@@ -84,6 +86,7 @@ def teacher_forced_layers(layers64, x, hidden_bits, z_dev):
                     f"layer {li}: {int(bad.sum())} activations differ beyond the fp32 bound; first at "
                     f"{np.argwhere(bad)[0].tolist()}")
                 n_amb += int(diff.sum())
+                rows |= diff.any(axis=1)
             n_tot += dev.size
             h = dev          # teacher forcing: the next layer consumes the device's activations
         else:   # z_dev may hold the first c outputs only (a logged head)
@@ -92,7 +95,28 @@ def teacher_forced_layers(layers64, x, hidden_bits, z_dev):
             err = np.abs(zd - z[:, :c])
             bad = err > delta[:, :c]
             assert not bad.any(), f"output: {int(bad.sum())} beyond the fp32 bound, worst {float((err / delta).max()):.2f}x"
+    if row_mask:
+        return n_amb, n_tot, rows
     return n_amb, n_tot
+
+
+def ambiguous_rows(layers64, x) -> np.ndarray:
+    """[B] mask of the rows whose free-running float64 forward has a hidden pre-activation
+    within the fp32 accumulation bound delta = 2^-17 (|W| |h| + |b|) of a bf16 rounding
+    decision (bf16(ReLU(z - delta)) != bf16(ReLU(z + delta))): there a device that
+    accumulates in fp32 may correctly round the other way (reading R-TOL), and the rest of
+    that row's forward differs by one bf16 step of that activation.  For checks where the
+    device's hidden activations are not logged."""
+    h = bf16_fast(np.asarray(x, dtype=np.float64))
+    rows = np.zeros(h.shape[0], dtype=bool)
+    for w, b in layers64[:-1]:
+        z = h @ w.T + b
+        delta = FP32_ACC_BOUND * (np.abs(h) @ np.abs(w).T + np.abs(b)) + 1e-30
+        lo = bf16_fast(np.maximum(z - delta, 0.0))
+        hi = bf16_fast(np.maximum(z + delta, 0.0))
+        rows |= (lo != hi).any(axis=1)
+        h = bf16_fast(np.maximum(z, 0.0))
+    return rows
 
 
 def forward_loops(layers64, x) -> list:

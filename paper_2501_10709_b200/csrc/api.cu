@@ -58,6 +58,7 @@ struct fin_policy {
   uint8_t bias_nz;             // bit l: layer l has a non-zero bias (an all-zero bias is skipped)
   float* w1s_t;                // stock: device [S][HID] shared columns of W1 (exact bf16 values), else null
   uint64_t uid;                // process-unique id (keys the env's z1s cache; addresses can be reused)
+  cudaEvent_t used;            // recorded on the stream of every call that reads the policy (destroy waits on it)
 };
 
 namespace {
@@ -456,6 +457,15 @@ int fin_env_check(fin_env* env, uint32_t* flags) {
   return FIN_OK;
 }
 
+int fin_env_counters(fin_env* env, uint32_t* counters, int32_t clear) {
+  if (!env || !counters) return fail(FIN_E_CONFIG, "fin_env_counters: null argument");
+  FIN_CUDA(cudaStreamSynchronize(env->last_stream));
+  FIN_CUDA(cudaMemcpy(counters, env->d.flags + FIN_CTR_EXACT_REDO, FIN_CTR_LEN * sizeof(uint32_t),
+                      cudaMemcpyDeviceToHost));
+  if (clear) FIN_CUDA(cudaMemset(env->d.flags + FIN_CTR_EXACT_REDO, 0, FIN_CTR_LEN * sizeof(uint32_t)));
+  return FIN_OK;
+}
+
 void fin_env_destroy(fin_env* env) {
   if (!env) return;
   cudaStreamSynchronize(env->last_stream);
@@ -519,6 +529,7 @@ int fin_policy_create(int32_t kind, int32_t n_layers, const int32_t* dims, const
   if (e == cudaSuccess && !w1s.empty())
     e = cudaMemcpyAsync(pol->w1s_t, w1s.data(), w1s.size() * 4, cudaMemcpyHostToDevice, S(stream));
   if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pol->used, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     if (pol->wpack) cudaFree(pol->wpack);
     if (pol->bias) cudaFree(pol->bias);
@@ -532,7 +543,10 @@ int fin_policy_create(int32_t kind, int32_t n_layers, const int32_t* dims, const
 
 void fin_policy_destroy(fin_policy* pol) {
   if (!pol) return;
-  cudaDeviceSynchronize();
+  if (pol->used) {   // wait for the last call that read the weights (not for the whole device)
+    cudaEventSynchronize(pol->used);
+    cudaEventDestroy(pol->used);
+  }
   cudaFree(pol->wpack);
   cudaFree(pol->bias);
   if (pol->w1s_t) cudaFree(pol->w1s_t);
@@ -542,6 +556,12 @@ void fin_policy_destroy(fin_policy* pol) {
 }  // extern "C"
 
 namespace {
+
+// every policy of a call records its `used` event on the call's stream after the launch
+void mark_used(const fin_policy* const* members, int n, cudaStream_t s) {
+  for (int m = 0; m < n; ++m)
+    if (members[m] && members[m]->used) cudaEventRecord(members[m]->used, s);
+}
 
 // DDPG OU state: one [K][N] slot per DDPG member, grown on demand (existing slots kept)
 int ensure_ou_slots(fin_env* env, int n, cudaStream_t s) {
@@ -675,6 +695,7 @@ int fin_rollout(fin_env* env, const fin_policy* const* members, int32_t n_member
   int tiles = 1;
   cudaError_t e = env->d.task == FIN_STOCK ? fin::launch_stock_rollout(net, p, env->d.N, &tiles, S(stream))
                                            : fin::launch_crypto_rollout(net, p, env->d.N, &tiles, S(stream));
+  mark_used(members, n_members, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fin_rollout launch");
   if (out && out->agg) {
     const int rows = (env->d.N + tc::kTileM * tiles - 1) / (tc::kTileM * tiles) * tiles;
@@ -710,7 +731,8 @@ int fin_rollout_actions(fin_env* env, const int16_t* actions, int32_t T, const f
 }
 
 int fin_ensemble_act(fin_env* env, const fin_policy* const* members, int32_t n_members, const float* member_w,
-                     const fin_noise* noise, int16_t* actions, float* mean_action, void* stream) {
+                     const fin_noise* noise, int16_t* actions, float* mean_action, int32_t commit_ou,
+                     void* stream) {
   if (!env || !actions) return fail(FIN_E_CONFIG, "fin_ensemble_act: null argument");
   if (env->d.task != FIN_STOCK) return fail(FIN_E_UNSUPPORTED, "fin_ensemble_act: stock envs only");
   tc::TcParams p;
@@ -725,11 +747,13 @@ int fin_ensemble_act(fin_env* env, const fin_policy* const* members, int32_t n_m
   p.e = env->d;   // supplied noise is read as [1][M][N][K]; Philox uses the env's current step
   p.T = 1;
   p.act_only = 1;
+  p.commit_ou = commit_ou != 0;
   p.mean_out = mean_action;
   p.o.actions = actions;
   env->last_stream = S(stream);
   int tiles = 1;
   cudaError_t e = fin::launch_stock_rollout(net, p, env->d.N, &tiles, S(stream));
+  mark_used(members, n_members, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fin_ensemble_act launch");
   return FIN_OK;
 }
@@ -783,6 +807,7 @@ int fin_mlp_forward(const fin_policy* pol, const uint16_t* x, int32_t B, float* 
     p.z1s = z1s;
   }
   if (e == cudaSuccess) e = fin::launch_mlp_probe(pol->net, p, B, s);
+  if (pol->used) cudaEventRecord(pol->used, s);
   if (z1s) cudaFreeAsync(z1s, s);
   if (e != cudaSuccess) return cuda_fail(e, "fin_mlp_forward launch");
   return FIN_OK;

@@ -174,6 +174,7 @@ __device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)
   })
 buys_done:
   if (miss) {   // rare: arrays in local memory only on this path
+    atomicAdd(e.flags + FIN_CTR_EXACT_REDO, 1u);
     int hh[KA], aa[KA];
 #pragma unroll
     for (int k = 0; k < KA; ++k) {
@@ -260,6 +261,7 @@ buys_done_e:
 #pragma unroll
   for (int q = 0; q < E; ++q) {
     if (miss[q]) {   // rare: arrays in local memory only on this path
+      atomicAdd(e.flags + FIN_CTR_EXACT_REDO, 1u);
       int hh[KA], aa[KA];
 #pragma unroll
       for (int k = 0; k < KA; ++k) {

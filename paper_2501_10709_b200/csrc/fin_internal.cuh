@@ -49,8 +49,10 @@ struct EnvDev {
   int32_t* m_n;          // number of returns
   double* agg_env;       // [FIN_AGG_LEN][N] per-env aggregate partials of the running rollout (fused
                          // stock rollout: touched once per episode, kept out of the registers)
-  uint32_t* flags;       // sticky device error word
+  uint32_t* flags;       // sticky device error word; flags[FIN_CTR_*] are event counters (fin_env_counters)
 };
+// counters after the flags word (same 64-B block)
+#define FIN_CTR_EXACT_REDO 4   // stock: steps whose buys took the exact out-of-line affordability path
 
 struct TrajDev {
   float* reward;

@@ -346,7 +346,7 @@ struct StockOps {
           const float x = p.n_ddpg == 1 ? st.ou[ko] : *gx;
           post = __fadd_rn(__fadd_rn(x, __fmul_rn(e.ou_theta, __fsub_rn(0.f, x))), __fmul_rn(e.ou_sigma, eps[j]));
           if (p.n_ddpg == 1) st.ou[ko] = post;
-          else *gx = post;
+          else if (!(LOG && p.act_only) || p.commit_ou) *gx = post;   // act-only: commit on request
         }
         const float th = tanh_f32(pre);
         float a = sac ? th : fminf(fmaxf(__fadd_rn(th, post), -1.f), 1.f);
@@ -443,7 +443,13 @@ struct StockOps {
   __device__ __forceinline__ static void finalize(State& st, const TcParams& p, int env, int gtid, int bar_id,
                                                   int tile) {
     const EnvDev& e = p.e;
-    if (LOG && p.act_only) return;
+    if (LOG && p.act_only) {   // fin_ensemble_act: only the single-DDPG register state may be committed
+      if (ENS && p.commit_ou && p.n_ddpg == 1 && st.live) {
+#pragma unroll
+        for (int k = 0; k < KOU; ++k) e.ou[(size_t)k * e.N + env] = st.ou[k];
+      }
+      return;
+    }
     if (st.live) {
       e.cash[env] = st.b;
       e.vcur[env] = st.vc;

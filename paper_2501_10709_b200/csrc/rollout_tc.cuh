@@ -58,6 +58,7 @@ struct TcParams {
   const float* noise;                     // supplied noise
   // fin_ensemble_act: compute the (ensemble) action only, no env transition
   int32_t act_only;
+  int32_t commit_ou;                      // fin_ensemble_act: advance the DDPG OU states (else left untouched)
   float* mean_out;                        // [N][K] averaged continuous action
   uint16_t* hid_out;                      // bf16 hidden activations (probe [B][2][HID])
   const float* z1s;                       // factored layer 1: shared term [M][rows][HID] (or probe [B][HID])

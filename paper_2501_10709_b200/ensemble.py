@@ -27,22 +27,36 @@ def validate_and_weight(env_val, members, T_val: int, threshold: float = 0.0, te
 
     env_val: a stock handle whose windows are the validation windows (e.g. window_offset
     = 30 after 30-day training windows, episode_len = 5, advance_window_on_reset).  It is
-    reset before each member, so every member sees the same validation episodes."""
+    reset before each member, so every member sees the same validation episodes.
+
+    Every step -- the zeroing of ``aggs``, the rollouts, the all-reduce and the weights --
+    is enqueued on ``stream`` (default: the current stream), so the collective reads the
+    aggregate rows only after the rollouts that write them."""
+    import contextlib
+
     import torch
-    M = len(members)
-    aggs = torch.zeros((M, fin.FIN_AGG_LEN), dtype=torch.float64, device="cuda")
-    for m, pol in enumerate(members):
-        fin.fin_env_reset(env_val, stream=stream)
-        fin.fin_rollout(env_val, [pol], T_val, fin.make_noise(fin.FIN_NOISE_NONE), fin.make_traj(agg=aggs[m]),
-                        stream=stream)
-    fdist.allreduce_aggs(aggs, group)
-    w = torch.empty(M, dtype=torch.float32, device="cuda")
-    sharpe = torch.empty(M, dtype=torch.float64, device="cuda")
-    fin.fin_member_weights(aggs, w, sharpe, threshold, temperature, stream=stream)
+    ctx = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+    with ctx:
+        M = len(members)
+        aggs = torch.zeros((M, fin.FIN_AGG_LEN), dtype=torch.float64, device="cuda")
+        for m, pol in enumerate(members):
+            fin.fin_env_reset(env_val)
+            fin.fin_rollout(env_val, [pol], T_val, fin.make_noise(fin.FIN_NOISE_NONE), fin.make_traj(agg=aggs[m]))
+        fdist.allreduce_aggs(aggs, group)
+        w = torch.empty(M, dtype=torch.float32, device="cuda")
+        sharpe = torch.empty(M, dtype=torch.float64, device="cuda")
+        fin.fin_member_weights(aggs, w, sharpe, threshold, temperature)
     return w, sharpe, aggs
 
 
 def weighted_rollout(env, members, w, T: int, noise=None, traj=None, stream=None):
     """Trade T steps with the weighted ensemble (fin_rollout's member_w is a host array:
-    the M weights are read back once, outside the rollout)."""
-    return fin.fin_rollout(env, members, T, noise, traj, member_w=w.float().cpu().numpy(), stream=stream)
+    the M weights are read back once, outside the rollout; the read-back is ordered after
+    the work of ``stream`` that produced them)."""
+    import contextlib
+
+    import torch
+    ctx = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+    with ctx:
+        wh = w.float().cpu().numpy()          # synchronises with the current (= given) stream
+        return fin.fin_rollout(env, members, T, noise, traj, member_w=wh)

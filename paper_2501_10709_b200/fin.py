@@ -8,7 +8,9 @@ of the library; there is no CPU fallback -- importing this module on a machine
 without the built library raises.
 
 PyTorch is used only for device memory and streams (tensors are allocated by the
-caller, see ``paper_2501_10709_b200.runtime`` for the conveniences built on it).
+caller).  Before a call, the binding checks that every tensor it passes is at least
+as large as the call's shapes require (include/fin.h states them), so a short tensor
+raises ValueError instead of becoming an out-of-bounds device write.
 """
 from __future__ import annotations
 
@@ -49,7 +51,7 @@ EXPORTS = ("fin_env_create", "fin_env_reset", "fin_env_step", "fin_env_get_state
            "fin_env_check", "fin_env_destroy", "fin_policy_create", "fin_policy_destroy", "fin_rollout",
            "fin_rollout_actions", "fin_ensemble_act", "fin_episode_metrics", "fin_mlp_forward",
            "fin_philox_normals", "fin_member_weights", "fin_market_prepare", "fin_crypto_market", "fin_gae", "fin_kl_diversity", "fin_last_error", "fin_abi_version", "fin_device_check",
-           "fin_debug_trace")
+           "fin_debug_trace", "fin_env_counters")
 
 
 class FinError(RuntimeError):
@@ -89,13 +91,15 @@ _sig = {
     "fin_env_set_state": ([_P, _P, _P, _P, _P, _P, _P], C.c_int),
     "fin_env_check": ([_P, C.POINTER(C.c_uint32)], C.c_int),
     "fin_env_destroy": ([_P], None),
+    "fin_env_counters": ([_P, _P, C.c_int32], C.c_int),
     "fin_policy_create": ([C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(_P), C.POINTER(_P), _P,
                            C.POINTER(_P)], C.c_int),
     "fin_policy_destroy": ([_P], None),
     "fin_rollout": ([_P, C.POINTER(_P), C.c_int32, _P, C.c_int32, C.POINTER(fin_noise), C.POINTER(fin_traj), _P],
                     C.c_int),
     "fin_rollout_actions": ([_P, _P, C.c_int32, C.POINTER(fin_traj), _P], C.c_int),
-    "fin_ensemble_act": ([_P, C.POINTER(_P), C.c_int32, _P, C.POINTER(fin_noise), _P, _P, _P], C.c_int),
+    "fin_ensemble_act": ([_P, C.POINTER(_P), C.c_int32, _P, C.POINTER(fin_noise), _P, _P, C.c_int32, _P],
+                         C.c_int),
     "fin_episode_metrics": ([_P, _P, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double, _P, C.c_int32, _P,
                              _P, _P], C.c_int),
     "fin_mlp_forward": ([_P, _P, C.c_int32, _P, _P, _P], C.c_int),
@@ -164,6 +168,9 @@ def make_traj(reward=None, done=None, actions=None, cash=None, hold=None, asset=
     tr.ep_count = _ptr(ep_count, torch.int32, "ep_count")
     tr.ep_capacity = int(ep_metrics.shape[0]) if ep_metrics is not None else 0
     tr.agg = _ptr(agg, torch.float64, "agg")
+    # the tensors stay referenced by the struct (lifetime) and are size-checked per call
+    tr._t = dict(reward=reward, done=done, actions=actions, cash=cash, hold=hold, asset=asset, mlp_out=mlp_out,
+                 mlp_hidden=mlp_hidden, ep_metrics=ep_metrics, ep_count=ep_count, agg=agg)
     return tr
 
 
@@ -173,7 +180,45 @@ def make_noise(mode: int = FIN_NOISE_NONE, seed: int = 0, supplied=None) -> fin_
     n.mode = mode
     n.seed = seed
     n.supplied = _ptr(supplied, torch.float32, "noise") if supplied is not None else None
+    if mode == FIN_NOISE_SUPPLIED and supplied is None:
+        raise ValueError("FIN_NOISE_SUPPLIED needs a supplied tensor")
+    n._supplied = supplied
     return n
+
+
+def _need(t, numel: int, what: str):
+    """Raise ValueError if tensor ``t`` (None = not passed) holds fewer than ``numel`` elements."""
+    if t is not None and t.numel() < numel:
+        raise ValueError(f"{what}: tensor has {t.numel()} elements, the call writes/reads {numel}")
+
+
+def _need_noise(nz: fin_noise, T: int, M: int, N: int, K: int, crypto: bool = False):
+    if nz.mode == FIN_NOISE_SUPPLIED:
+        s = getattr(nz, "_supplied", None)
+        if s is None:
+            raise ValueError("supplied noise: build the fin_noise with make_noise(..., supplied=tensor)")
+        _need(s, T * N * 2 if crypto else T * M * N * K, "supplied noise " + ("[T][N][2]" if crypto else "[T][M][N][K]"))
+
+
+def _need_traj(tr: fin_traj, T: int, N: int, K: int, M: int = 1, out_dim: int = 0, hid: int = 0):
+    """Size checks of the trajectory tensors against fin.h's [T][N][...] shapes."""
+    t = getattr(tr, "_t", None)
+    if t is None:
+        if any(getattr(tr, f) for f, _ in fin_traj._fields_ if f != "ep_capacity"):
+            raise ValueError("fin_traj must be built with make_traj (its tensors are size-checked)")
+        return
+    _need(t["reward"], T * N, "reward [T][N]")
+    _need(t["done"], T * N, "done [T][N]")
+    _need(t["actions"], T * N * K, "actions [T][N][K]")
+    _need(t["cash"], T * N, "cash [T][N]")
+    _need(t["hold"], T * N * K, "hold [T][N][K]")
+    _need(t["asset"], T * N, "asset [T][N]")
+    _need(t["mlp_out"], T * M * N * out_dim, "mlp_out [T][M][N][Kout]")
+    _need(t["mlp_hidden"], T * M * N * 2 * hid, "mlp_hidden [T][M][N][2][HID]")
+    _need(t["ep_metrics"], int(t["ep_metrics"].shape[0]) * N * 3 if t["ep_metrics"] is not None else 0,
+          "ep_metrics [E][N][3]")
+    _need(t["ep_count"], N, "ep_count [N]")
+    _need(t["agg"], FIN_AGG_LEN, "agg [FIN_AGG_LEN]")
 
 
 def env_config(**kw) -> fin_env_config:
@@ -258,6 +303,8 @@ def fin_env_reset(env: Env, mask=None, stream=None) -> None:
 def fin_env_step(env: Env, actions, traj: fin_traj | None = None, stream=None) -> None:
     import torch
     tr = traj if traj is not None else fin_traj()
+    _need(actions, env.N * env.K, "actions [N][K]")
+    _need_traj(tr, 1, env.N, env.K)
     _check(_lib.fin_env_step(env.handle, _ptr(actions, torch.int16, "actions"), C.byref(tr), _stream(stream)),
            "fin_env_step")
 
@@ -283,6 +330,14 @@ def fin_env_check(env: Env) -> int:
     if rc not in (FIN_OK, FIN_E_DEVICE_ASYNC):
         _check(rc, "fin_env_check")
     return int(f.value)
+
+
+def fin_env_counters(env: Env, clear: bool = False) -> dict:
+    """Event counters of the handle (synchronises): exact_redo = stock steps whose buys
+    took the exact out-of-line affordability path."""
+    c = (C.c_uint32 * 4)()
+    _check(_lib.fin_env_counters(env.handle, C.cast(c, _P), int(bool(clear))), "fin_env_counters")
+    return {"exact_redo": int(c[0])}
 
 
 def fin_env_destroy(env: Env) -> None:
@@ -316,10 +371,12 @@ def _members(members):
     return arr
 
 
-def _weights(member_w):
+def _weights(member_w, n_members: int):
     if member_w is None:
         return None, None
-    w = np.ascontiguousarray(member_w, dtype=np.float32)
+    w = np.ascontiguousarray(member_w, dtype=np.float32).reshape(-1)
+    if w.size != n_members:
+        raise ValueError(f"member_w has {w.size} weights for {n_members} members")
     return w, w.ctypes.data_as(_P)
 
 
@@ -327,7 +384,13 @@ def fin_rollout(env: Env, members, T: int, noise: fin_noise | None = None, traj:
                 member_w=None, stream=None) -> None:
     nz = noise if noise is not None else make_noise(FIN_NOISE_NONE)
     tr = traj if traj is not None else fin_traj()
-    keep, wp = _weights(member_w)
+    keep, wp = _weights(member_w, len(members))
+    crypto = env.cfg.task == FIN_CRYPTO
+    M = len(members)
+    if M:
+        d = members[0].dims
+        _need_traj(tr, T, env.N, env.K, M, out_dim=d[-1], hid=d[1])
+    _need_noise(nz, T, M, env.N, env.K, crypto)
     _check(_lib.fin_rollout(env.handle, _members(members), len(members), wp, T, C.byref(nz), C.byref(tr),
                             _stream(stream)), "fin_rollout")
 
@@ -335,18 +398,24 @@ def fin_rollout(env: Env, members, T: int, noise: fin_noise | None = None, traj:
 def fin_rollout_actions(env: Env, actions, T: int, traj: fin_traj | None = None, stream=None) -> None:
     import torch
     tr = traj if traj is not None else fin_traj()
+    _need(actions, T * env.N * env.K, "actions [T][N][K]")
+    _need_traj(tr, T, env.N, env.K)
     _check(_lib.fin_rollout_actions(env.handle, _ptr(actions, torch.int16, "actions"), T, C.byref(tr),
                                     _stream(stream)), "fin_rollout_actions")
 
 
 def fin_ensemble_act(env: Env, members, actions, mean_action=None, noise: fin_noise | None = None, member_w=None,
-                     stream=None) -> None:
+                     commit_ou: bool = False, stream=None) -> None:
     import torch
     nz = noise if noise is not None else make_noise(FIN_NOISE_NONE)
-    keep, wp = _weights(member_w)
+    keep, wp = _weights(member_w, len(members))
+    N, K = env.N, env.K
+    _need(actions, N * K, "actions [N][K]")
+    _need(mean_action, N * K, "mean_action [N][K]")
+    _need_noise(nz, 1, len(members), N, K)
     _check(_lib.fin_ensemble_act(env.handle, _members(members), len(members), wp, C.byref(nz),
                                  _ptr(actions, torch.int16, "actions"), _ptr(mean_action, torch.float32, "mean"),
-                                 _stream(stream)), "fin_ensemble_act")
+                                 int(bool(commit_ou)), _stream(stream)), "fin_ensemble_act")
 
 
 def fin_episode_metrics(equity, done, reset_equity: float, periods_per_year: float = 252.0, rf: float = 0.0,

@@ -45,6 +45,14 @@ def host(t):
     return t.cpu().numpy()
 
 
+def crypto_reward_tol(o_reward, pos_after, mid, mid_next, scale=1.0, fees=0.0):
+    """SURVEY c.8's reward tolerance for the crypto env: 1e-5 |o| + 1e-5 S (|h'| |m' - m| + fees),
+    h' the position after the trade (+-1 or 0)."""
+    o = np.asarray(o_reward, dtype=np.float64)
+    cond = np.abs(np.asarray(pos_after, dtype=np.float64)) * abs(float(mid_next) - float(mid)) + fees
+    return 1e-5 * np.abs(o) + 1e-5 * scale * cond + 1e-30
+
+
 def reward_tol(o_reward, o_hold, p, pn, scale=2.0 ** -12, cost_notional=None):
     """SURVEY c.8 reward tolerance: 1e-5 |o| + 1e-5 S (sum_k h'_k |p'_k - p_k| + fees)."""
     cond = np.abs(o_hold * np.abs(pn - p)).sum(axis=-1)

@@ -6,7 +6,7 @@ kernels mirror the oracle's operation order so equality is expected); reward
 import numpy as np
 import pytest
 
-from gpu_util import dev, host, needs_gpu, stock_pair, zeros
+from gpu_util import crypto_reward_tol, dev, host, needs_gpu, stock_pair, zeros
 from oracle import crypto as ocry
 from oracle import metrics as omet
 from oracle import stock as ostock
@@ -75,6 +75,65 @@ def test_c1_shape_step_parity_ragged_windows_resets():
     g = _step_loop(fin, env, acts, 30)
     _compare_stock(g, o, m.market, ocfg)
     assert fin.fin_env_check(env) & fin.FIN_FLAG_ACTION_RANGE
+
+
+def _redo_case(K=30, N=3000, cost=1e-3):
+    """Envs whose cash sits exactly at, or one ulp around, the cost of q shares of one
+    asset: cash = fl(q u) + {-1, 0, +1} ulp, u = fl(p (1 + c)), with dyadic and
+    non-dyadic prices; each env asks for q + 3 shares of its asset, so the cash binds
+    exactly at the affordability boundary of reading R5."""
+    prices = np.array([0.75, 1.5, 64.0, 100.0, 0.1, 99.37, 33.3, 12.34, 250.5, 7.77] * 3, dtype=np.float32)[:K]
+    mk = np.zeros((3, 3, K), dtype=np.float32)
+    mk[:, 0, :] = prices[None, :]
+    mk[:, 1, :] = 1.0
+    u = prices.astype(np.float64) * (1.0 + cost)
+    cash = np.empty(N)
+    acts = np.zeros((N, K), dtype=np.int16)
+    for i in range(N):
+        k, q, v = i % K, 1 + (i // K) % 97, (i // (K * 97)) % 3 - 1
+        b = q * u[k]
+        cash[i] = np.nextafter(b, np.inf) if v > 0 else np.nextafter(b, -np.inf) if v < 0 else b
+        acts[i, k] = q + 3
+    return mk, cash, acts
+
+
+@pytest.mark.parametrize("cost", [1e-3, 0.0])
+def test_exact_affordability_redo_path(cost):
+    """The exact out-of-line buy path (env_stock.cuh stock_buys_exact, reached only when
+    the fast floor estimate fails its check) runs -- the handle's event counter proves
+    it -- and gives cash and holdings bitwise equal to the oracle's definition (R5), in
+    K1 (fin_env_step) and K4 (fin_rollout_actions).  Control: unbinding buys never take it."""
+    import torch
+    fin = _fin()
+    K, N = 30, 3000
+    mk, cash, acts = _redo_case(K, N, cost)
+    ocfg, fcfg = stock_pair(num_envs=N, num_assets=K, num_indicators=1, num_rows=3, episode_len=2,
+                            cost_rate=cost, window_block=N)
+    p, pn = [float(x) for x in mk[0, 0]], [float(x) for x in mk[1, 0]]
+    want_b, want_h = np.empty(N), np.zeros((N, K), dtype=np.int64)
+    for i in range(N):
+        b, h, _, _, _, _, _ = ostock.step_one(ocfg, float(cash[i]), [0] * K, p, pn, [int(x) for x in acts[i]])
+        want_b[i], want_h[i] = b, h
+    for path in ("k1", "k4"):
+        env = fin.fin_env_create(fcfg, mk)
+        fin.fin_env_set_state(env, cash=dev(cash), hold=zeros((N, K), torch.int16), t_ep=zeros(N, torch.int32))
+        fin.fin_env_counters(env, clear=True)
+        c, h = zeros((1, N), torch.float64), zeros((1, N, K), torch.int16)
+        if path == "k1":
+            fin.fin_env_step(env, dev(acts), fin.make_traj(cash=c, hold=h))
+        else:
+            fin.fin_rollout_actions(env, dev(acts[None]), 1, fin.make_traj(cash=c, hold=h))
+        redo = fin.fin_env_counters(env)["exact_redo"]
+        assert redo > 0, path
+        assert np.array_equal(host(c)[0].view(np.uint64), want_b.view(np.uint64)), path
+        assert np.array_equal(host(h)[0], want_h), path
+        assert (want_b >= 0).all()
+    # control: cash far from binding -> the fast path alone
+    env = fin.fin_env_create(fcfg, mk)
+    small = (acts > 0).astype(np.int16)
+    c = zeros((1, N), torch.float64)
+    fin.fin_env_step(env, dev(small), fin.make_traj(cash=c))
+    assert fin.fin_env_counters(env)["exact_redo"] == 0
 
 
 def test_replay_rollout_parity_and_episode_metrics():
@@ -210,7 +269,8 @@ def test_crypto_step_parity():
         assert np.array_equal(host(c), np.array(o["cash"]))
         assert np.array_equal(host(v), np.array(o["asset"]))
         assert np.array_equal(host(d).astype(bool), np.array(o["done"]))
-        np.testing.assert_allclose(host(r), np.array(o["reward"]), rtol=1e-5, atol=1e-3)
+        err = np.abs(host(r).astype(np.float64) - np.array(o["reward"]))
+        assert np.all(err <= crypto_reward_tol(o["reward"], o["pos"], rows[t, 0], rows[t + 1, 0])), t
     assert fin.fin_env_check(env) == 0
 
 

@@ -13,7 +13,7 @@ import math
 import numpy as np
 import pytest
 
-from gpu_util import dev, host, needs_gpu, stock_pair, zeros
+from gpu_util import crypto_reward_tol, dev, host, needs_gpu, stock_pair, zeros
 from oracle import crypto as ocry
 from oracle import metrics as omet
 from oracle import mlp as omlp
@@ -35,20 +35,22 @@ def _fin():
 MLP_STATS = []
 
 
-def _mlp_close(g, o, rel=2e-3, strict=False):
+def _mlp_close(g, o, amb_rows, rel=2e-3):
     """End-to-end comparison with the free-running float64 forward: norm-wise relative
-    error of each output vector, max_k |g - o| / max_k |o| (reading R-TOL).
-    The gate is the layer-by-layer teacher-forced check (oracle.mlp.teacher_forced_layers);
-    end to end, a single bf16 rounding flip of one hidden activation (fp32 vs float64
-    pre-activation on the two sides of a rounding boundary) moves the outputs by
-    ~2^-8 |a| |w|, so this is recorded, and asserted at 2e-3 for 99% of rows."""
+    error of each output vector, max_k |g - o| / max_k |o| <= rel (BASELINE north_star:
+    rel 2e-3 on MLP outputs; reading R-TOL).  The only rows allowed beyond it
+    are those in ``amb_rows``: rows where the layer-by-layer check
+    (oracle.mlp.teacher_forced_layers(..., row_mask=True)) accepted an ambiguous bf16
+    rounding of a hidden activation (fp32 vs float64 pre-activation on the two sides of
+    a rounding boundary, within the fp32 accumulation bound) -- there the free-running
+    float64 forward legitimately takes the other activation, one bf16 step (~2^-8 |a|)
+    away -- or, where hidden activations are not logged, oracle.mlp.ambiguous_rows."""
     err = np.abs(g - o).max(axis=-1)
     scale = np.abs(o).max(axis=-1)
     ratio = err / np.maximum(scale, 1e-6)
     MLP_STATS.append((float(np.percentile(ratio, 99)), float(ratio.max())))
-    if strict:
-        assert np.all(ratio <= rel), f"{(ratio > rel).sum()} of {ratio.size} rows outside {rel}"
-    assert np.mean(ratio > rel) <= 1e-2 or (ratio > rel).sum() <= 1, f"{(ratio > rel).sum()} rows outside {rel}"
+    bad = (ratio > rel) & ~np.asarray(amb_rows, dtype=bool)
+    assert not bad.any(), f"{int(bad.sum())} of {ratio.size} rows outside {rel} without an ambiguous activation"
 
 
 def _kind_for(fin, dims):
@@ -102,9 +104,9 @@ def test_mlp_kaiming_rel_2e3(dims):
     hid = zeros((B, *_hid_shape(dims)), torch.int16)
     fin.fin_mlp_forward(pol, dev(spol.f64_to_bf16_bits(x).view(np.int16)), z, hid)
     L64 = omlp.layers_f64(layers)
-    amb, tot = omlp.teacher_forced_layers(L64, xq, host(hid), host(z))
-    assert amb <= 1e-3 * tot
-    _mlp_close(host(z).astype(np.float64), omlp.forward(L64, xq), strict=False)
+    n_amb, tot, amb = omlp.teacher_forced_layers(L64, xq, host(hid), host(z), row_mask=True)
+    assert n_amb <= 1e-3 * tot
+    _mlp_close(host(z).astype(np.float64), omlp.forward(L64, xq), amb)
 
 
 # ------------------------------------------------------------------ fused stock rollout
@@ -155,16 +157,17 @@ def _teacher_forced_stock(g, ocfg, mk, layers, kinds, noise):
     for t in range(T):
         X = orol.stock_obs_batch(ocfg, st, mk)
         for mi, L_ in enumerate(L64):
-            omlp.teacher_forced_layers(L_, X, g["mlp_hidden"][t, mi], g["mlp_out"][t, mi])
-            _mlp_close(g["mlp_out"][t, mi].astype(np.float64), omlp.forward(L_, X))
+            _, _, amb = omlp.teacher_forced_layers(L_, X, g["mlp_hidden"][t, mi], g["mlp_out"][t, mi], row_mask=True)
+            _mlp_close(g["mlp_out"][t, mi].astype(np.float64), omlp.forward(L_, X), amb)
         # (3) actions from the GPU's z and the supplied noise (f64 rule of oracle.policy)
         for i in range(N):
             zs = [g["mlp_out"][t, mi, i].astype(np.float64) for mi in range(len(kinds))]
-            sh, abar, ou_new = orol.ensemble_shares(kinds, zs, noise[t, :, i].astype(np.float64), list(ou[i]))
+            sh, abar, ou_new = orol.ensemble_shares(kinds, zs, noise[t, :, i].astype(np.float64), list(ou[i]),
+                                                    max_trade=ocfg.max_trade)
             ou[i] = ou_new
             for k in range(K):
                 if sh[k] != g["actions"][t, i, k]:
-                    y = 100.0 * abar[k]
+                    y = ocfg.max_trade * abar[k]
                     assert abs(abs(y - math.trunc(y)) - 0.5) < 1e-4, (t, i, k, y, g["actions"][t, i, k])
                     n_boundary += 1
         ostock.step(ocfg, st, mk, g["actions"][t])
@@ -188,6 +191,16 @@ def test_fused_c1_rollout_teacher_forced():
     g, ocfg, mk, layers, kinds, noise = _stock_fused(300, 35, [(0, fin.FIN_PPO_GAUSS)], L=30)
     _teacher_forced_stock(g, ocfg, mk, layers, kinds, noise)
     assert g["agg"][fin.FIN_AGG_EPISODES] == 300
+
+
+def test_fused_c1_rollout_max_trade_50():
+    """max_trade = 50: the observation's holdings entries are h / max_trade (reading R13,
+    pinned on the CPU by tests/test_oracle_obs.py) and actions rha(50 a) -- teacher forced
+    through the layered MLP check, so a kernel that scaled holdings by 1/100 fails layer 1."""
+    fin = _fin()
+    g, ocfg, mk, layers, kinds, noise = _stock_fused(300, 35, [(0, fin.FIN_PPO_GAUSS)], L=30, max_trade=50)
+    assert ocfg.max_trade == 50 and np.abs(g["actions"]).max() <= 50 and g["hold"].max() > 0
+    _teacher_forced_stock(g, ocfg, mk, layers, kinds, noise)
 
 
 def test_fused_c2_ensemble_teacher_forced():
@@ -308,8 +321,8 @@ def test_fused_small_net_c0_market():
     L64 = omlp.layers_f64(layers)
     for t in range(T):
         X = orol.stock_obs_batch(ocfg, st, mkt.market)
-        omlp.teacher_forced_layers(L64, X, g["mlp_hidden"][t, 0], g["mlp_out"][t, 0])
-        _mlp_close(g["mlp_out"][t, 0].astype(np.float64), omlp.forward(L64, X))
+        _, _, amb = omlp.teacher_forced_layers(L64, X, g["mlp_hidden"][t, 0], g["mlp_out"][t, 0], row_mask=True)
+        _mlp_close(g["mlp_out"][t, 0].astype(np.float64), omlp.forward(L64, X), amb)
         ostock.step(ocfg, st, mkt.market, g["actions"][t])
 
 
@@ -335,6 +348,103 @@ def test_ensemble_act_matches_rollout_first_step():
     t_ep = zeros(N, torch.int32)
     fin.fin_env_get_state(env_a, t_ep=t_ep)
     assert np.all(host(t_ep) == 0)
+
+
+def _zero_net(dims):
+    return [(np.zeros((o, i), dtype=np.uint16), None) for i, o in zip(dims[:-1], dims[1:])]
+
+
+@pytest.mark.parametrize("n_ddpg", [1, 2])
+def test_ensemble_act_ou_commit(n_ddpg):
+    """fin_ensemble_act's OU contract (include/fin.h): without commit_ou the call is a pure
+    function of the env (same actions twice; a following rollout step is unchanged);
+    with commit_ou the updated OU state is written back, so the next call starts from it.
+    Same behaviour for one DDPG member (state in registers) and two (state in global
+    memory).  Zero networks make every member's action a closed form of the supplied
+    noise (z = 0: PPO clip(0.1 eps), DDPG clip(x) with x <- ou_update(x, eps)), so the
+    mean action is checked against the oracle's policy rules (f32 vs f64: 2e-6)."""
+    import torch
+    fin = _fin()
+    m = market.stock_c1(rows=80)
+    N, K = 130, 30
+    kw = dict(num_envs=N, num_assets=K, num_indicators=8, num_rows=80, episode_len=5, num_windows=10)
+    _, fcfg = stock_pair(**kw)
+    kinds = [fin.FIN_DDPG_OU, fin.FIN_PPO_GAUSS] + ([fin.FIN_DDPG_OU] if n_ddpg == 2 else [])
+    M = len(kinds)
+    pols = [fin.fin_policy_create(k, _zero_net(spol.STOCK_DIMS)) for k in kinds]
+    eps = inputs.supplied_noise(1, M, N, K, seed=5)
+    nz = fin.make_noise(fin.FIN_NOISE_SUPPLIED, 0, dev(eps))
+    env = fin.fin_env_create(fcfg, m.market)
+
+    def act(commit):
+        a, mean = zeros((N, K), torch.int16), zeros((N, K), torch.float32)
+        fin.fin_ensemble_act(env, pols, a, mean, nz, commit_ou=commit)
+        return host(a), host(mean).astype(np.float64)
+
+    def expected(x_in):
+        """mean action and the OU states after the update, from OU states x_in [M][N][K]."""
+        mean = np.zeros((N, K))
+        x_out = x_in.copy()
+        for i in range(N):
+            for k in range(K):
+                acts = []
+                for j, kind in enumerate(kinds):
+                    e = float(eps[0, j, i, k])
+                    if kind == fin.FIN_DDPG_OU:
+                        x_out[j, i, k] = opol.ou_update(float(x_in[j, i, k]), e)
+                        acts.append(opol.ddpg_action(0.0, x_out[j, i, k]))
+                    else:
+                        acts.append(opol.gaussian_action(0.0, e))
+                mean[i, k] = opol.ensemble_mean(acts)
+        return mean, x_out
+
+    x0 = np.zeros((M, N, K))
+    e1, x1 = expected(x0)
+    a0, m0 = act(False)
+    a1, m1 = act(False)
+    assert np.array_equal(a0, a1) and np.array_equal(m0, m1)      # no commit: pure
+    np.testing.assert_allclose(m0, e1, atol=2e-6, rtol=0)
+    a2, m2 = act(True)                                             # commit: same action, state advances
+    assert np.array_equal(a2, a0) and np.array_equal(m2, m0)
+    e2, _ = expected(x1)
+    a3, m3 = act(False)
+    np.testing.assert_allclose(m3, e2, atol=4e-6, rtol=0)
+    assert not np.array_equal(m3, m0)
+    # an uncommitted call leaves the OU state as the rollout expects it: a rollout step after
+    # two act-only calls equals the same step on a fresh env
+    env_b, env_c = fin.fin_env_create(fcfg, m.market), fin.fin_env_create(fcfg, m.market)
+    for _ in range(2):
+        fin.fin_ensemble_act(env_b, pols, zeros((N, K), torch.int16), None, nz)
+    ab, ac = zeros((1, N, K), torch.int16), zeros((1, N, K), torch.int16)
+    fin.fin_rollout(env_b, pols, 1, nz, fin.make_traj(actions=ab))
+    fin.fin_rollout(env_c, pols, 1, nz, fin.make_traj(actions=ac))
+    assert np.array_equal(host(ab), host(ac))
+
+
+def test_binding_rejects_short_tensors():
+    """The binding checks tensor sizes against the call's shapes before launching."""
+    import torch
+    fin = _fin()
+    m = market.stock_c1(rows=80)
+    N, K, T = 130, 30, 4
+    _, fcfg = stock_pair(num_envs=N, num_assets=K, num_indicators=8, num_rows=80, episode_len=5, num_windows=10)
+    env = fin.fin_env_create(fcfg, m.market)
+    pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, spol.kaiming_bf16(spol.STOCK_DIMS, 0))
+    with pytest.raises(ValueError):
+        fin.fin_rollout(env, [pol], T, None, fin.make_traj(reward=zeros((T - 1, N), torch.float32)))
+    with pytest.raises(ValueError):
+        fin.fin_rollout(env, [pol], T, None, fin.make_traj(actions=zeros((T, N, K - 1), torch.int16)))
+    with pytest.raises(ValueError):
+        fin.fin_rollout(env, [pol], T, fin.make_noise(fin.FIN_NOISE_SUPPLIED, 0, zeros((T, 1, N, K - 1),
+                                                                                      torch.float32)))
+    with pytest.raises(ValueError):
+        fin.fin_rollout(env, [pol, pol], T, None, None, member_w=[1.0])
+    with pytest.raises(ValueError):
+        fin.fin_rollout_actions(env, zeros((T, N, K), torch.int16), T + 1)
+    with pytest.raises(ValueError):
+        fin.fin_env_step(env, zeros((N - 1, K), torch.int16))
+    fin.fin_rollout(env, [pol], T, None, fin.make_traj(reward=zeros((T, N), torch.float32)))   # right size: ok
+    torch.cuda.synchronize()
 
 
 # ------------------------------------------------------------------ crypto Q rollout
@@ -370,8 +480,8 @@ def test_fused_crypto_rollout_teacher_forced(dims):
     for t in range(T):
         X = orol.crypto_obs_batch(ocfg, st, rows)
         q = omlp.forward(L64, X)
-        omlp.teacher_forced_layers(L64, X, g["mlp_hidden"][t], g["mlp_out"][t])
-        _mlp_close(g["mlp_out"][t].astype(np.float64), q)
+        _, _, amb = omlp.teacher_forced_layers(L64, X, g["mlp_hidden"][t], g["mlp_out"][t], row_mask=True)
+        _mlp_close(g["mlp_out"][t].astype(np.float64), q, amb)
         for i in range(N):
             qg = g["mlp_out"][t, i].astype(np.float64)
             j = opol.epsilon_greedy(list(qg), eps, float(uni[t, i, 0]), float(uni[t, i, 1]))
@@ -384,7 +494,8 @@ def test_fused_crypto_rollout_teacher_forced(dims):
         o = ocry.step(ocfg, st, rows, g["actions"][t, :, 0])
         assert np.array_equal(np.array(o["pos"]), g["hold"][t, :, 0])
         assert np.array_equal(np.array(o["cash"]), g["cash"][t]) and np.array_equal(np.array(o["asset"]), g["asset"][t])
-        np.testing.assert_allclose(g["reward"][t], np.array(o["reward"]), rtol=1e-5, atol=1e-3)
+        err = np.abs(g["reward"][t].astype(np.float64) - np.array(o["reward"]))
+        assert np.all(err <= crypto_reward_tol(o["reward"], o["pos"], rows[t, 0], rows[t + 1, 0])), t
     assert g["done"][-1].all() and np.all(g["ep_count"] == 1)
     # the per-rank aggregate (one partial row per tile, also with column-split epilogues)
     assert g["agg"][fin.FIN_AGG_EPISODES] == N
@@ -423,15 +534,18 @@ def test_headline_config_sampled_envs():
     env = fin.fin_env_create(fcfg, m.market)
     pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, layers)
     logs = dict(actions=zeros((T, N, K), torch.int16), cash=zeros((T, N), torch.float64),
-                mlp_out=zeros((T, 1, N, K), torch.float32), done=zeros((T, N), torch.uint8))
+                mlp_out=zeros((T, 1, N, K), torch.float32), done=zeros((T, N), torch.uint8),
+                mlp_hidden=zeros((T, 1, N, 2, 256), torch.int16))
     fin.fin_rollout(env, [pol], T, fin.make_noise(fin.FIN_NOISE_PHILOX, seed), fin.make_traj(**logs))
     assert fin.fin_env_check(env) == 0
     rng = np.random.default_rng(7)
-    sample = sorted(set([0, N - 1] + list(rng.choice(N, 22, replace=False))))
-    g = {k: v[:, :, sample] if k == "mlp_out" else v[:, sample] for k, v in ((k, host(t)) for k, t in logs.items())}
+    sample = sorted(set([0, 127, 128, N - 1] + list(rng.choice(N, 22, replace=False))))
+    idx = torch.tensor(sample, device="cuda")
+    g = {k: host(v.index_select(2 if k in ("mlp_out", "mlp_hidden") else 1, idx)) for k, v in logs.items()}
+    del logs
     L64 = omlp.layers_f64(layers)
     n_boundary = 0
-    zs, refs = [], []
+    zs, refs, ambs = [], [], []
     for j, i in enumerate(sample):
         ocfg = ostock.StockEnvConfig(num_envs=1, env_offset=int(i), **kw)
         o, _ = ostock.run_actions(ocfg, m.market, g["actions"][:, j:j + 1])
@@ -440,19 +554,23 @@ def test_headline_config_sampled_envs():
         for t in range(T):
             X = orol.stock_obs_batch(ocfg, st, m.market)
             z = g["mlp_out"][t, 0, j].astype(np.float64)
+            # layer by layer from the GPU's own hidden activations (reading R-TOL)
+            _, _, amb = omlp.teacher_forced_layers(L64, X, g["mlp_hidden"][t, 0, j:j + 1], z[None, :],
+                                                   row_mask=True)
             zs.append(z)
             refs.append(omlp.forward(L64, X)[0])
+            ambs.append(bool(amb[0]))
             eps = ophx.stock_noise(seed, int(i), t, 0, K)
             for k in range(K):
                 a = orol.policy.gaussian_action(float(z[k]), eps[k])
                 sh = orol.policy.shares(a)
                 if sh != g["actions"][t, j, k]:
+                    # the GPU's f32 tanh / Box-Muller vs the oracle's f64: only a .5 boundary may differ
                     y = 100.0 * a
-                    assert abs(abs(y - math.trunc(y)) - 0.5) < 2e-3, (t, i, k, y, g["actions"][t, j, k])
+                    assert abs(abs(y - math.trunc(y)) - 0.5) < 1e-4, (t, i, k, y, g["actions"][t, j, k])
                     n_boundary += 1
             ostock.step(ocfg, st, m.market, g["actions"][t, j:j + 1])
-    _mlp_close(np.array(zs), np.array(refs))
-    assert n_boundary <= 3
+    _mlp_close(np.array(zs), np.array(refs), np.array(ambs))
 
 
 def test_production_variant_matches_logged_variant():
@@ -550,7 +668,7 @@ def test_crypto_bench_call_sampled():
             assert a == g["actions"][t, j, 0], (i, t)
             if t in (0, 24000, T - 1):
                 X = orol.crypto_obs_batch(ocfg, st, rows)
-                _mlp_close(q[None, :], omlp.forward(L64, X))
+                _mlp_close(q[None, :], omlp.forward(L64, X), omlp.ambiguous_rows(L64, X))
             o = ocry.step(ocfg, st, rows, [a])
             assert o["pos"][0] == g["hold"][t, j, 0] and o["cash"][0] == g["cash"][t, j], (i, t)
 

@@ -194,3 +194,28 @@ def test_teacher_forced_layers_accepts_fp32_and_rejects_corruption():
     # an observation-encoding error (input not what the oracle encodes) is caught at layer 1
     with pytest.raises(AssertionError):
         mlp.teacher_forced_layers(layers, x * 1.01, hid, z)
+
+
+def test_ambiguous_rows_and_row_mask():
+    """oracle.mlp.ambiguous_rows flags exactly the rows where a hidden pre-activation sits
+    within the fp32 bound of a bf16 rounding decision: a 1-input identity-like net whose
+    pre-activation is the midpoint between two bf16 neighbours is flagged, one on a bf16
+    value is not.  teacher_forced_layers(row_mask=True) marks the rows it accepted an
+    ambiguous activation in, and only those."""
+    one = 1.0
+    mid = 1.0 + 2.0 ** -8              # halfway between bf16 1.0 and 1.0 + 2^-7
+    w1 = np.array([[one]])
+    layers = [(w1, np.zeros(1)), (np.array([[one]]), np.zeros(1))]
+    x = np.array([[1.0], [1.0]])
+    # move row 0's pre-activation to the midpoint via the bias (x = 1 exactly in bf16)
+    layers_mid = [(w1, np.array([mid - 1.0])), layers[1]]
+    rows = mlp.ambiguous_rows(layers_mid, x)
+    assert rows.all()
+    assert not mlp.ambiguous_rows(layers, x).any()
+    # row mask: a device that rounded row 1's midpoint up (legal) is flagged in row 1 only
+    hid = np.zeros((2, 2, 1), dtype=np.uint16)
+    lo_bits, hi_bits = spol.f64_to_bf16_bits(np.array([1.0, 1.0 + 2.0 ** -7]))
+    hid[0, 0, 0], hid[1, 0, 0] = lo_bits, hi_bits      # RNE of the midpoint is 1.0 (even)
+    z = np.array([[1.0], [1.0 + 2.0 ** -7]])
+    amb, tot, mask = mlp.teacher_forced_layers(layers_mid, x, hid, z, row_mask=True)
+    assert amb == 1 and mask.tolist() == [False, True]
