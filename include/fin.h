@@ -199,7 +199,10 @@ int fin_env_check(fin_env* env, uint32_t* flags /*host*/);
  * handle's last stream; clear != 0 zeroes them afterwards):
  *   [0] stock steps whose buys took the exact out-of-line affordability path (R5: the
  *       fast floor estimate failed its check -- cash at or within ~1e-11 of a multiple
- *       of the unit cost); for tests, which prove the slow path ran; the rest reserved. */
+ *       of the unit cost); for tests, which prove the slow path ran;
+ *   [1] fused stock rollouts launched with the balanced persistent schedule;
+ *   [2] rollouts where that cooperative launch was refused and one tile per CTA ran instead;
+ *   [3] the cudaError_t of the last refusal (0: none). */
 enum { FIN_CTR_LEN = 4 };
 int fin_env_counters(fin_env* env, uint32_t* counters /*host*/, int32_t clear);
 

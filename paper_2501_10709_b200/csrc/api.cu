@@ -20,6 +20,7 @@ namespace fin {
 // n_envs rows; *tiles receives the tiles per CTA the launch used (agg partial rows
 // = ceil(n_envs / (128 * tiles)) * tiles)
 cudaError_t launch_stock_rollout(int net, const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s);
+int stock_seg_grid(int net, const tc::TcParams& p, int n_envs);
 cudaError_t launch_crypto_market(int64_t steps, uint64_t seed, double sigma, double m0, double phi, float* rows,
                                  cudaStream_t s);
 cudaError_t launch_gae(const float* rew, const float* val, const uint8_t* done, int T, int N, double gamma,
@@ -46,6 +47,11 @@ struct fin_env {
   size_t z1s_cap;  // floats
   std::vector<uint64_t> z1s_key;   // uids of the members z1s holds (empty: none)
   float* ou_mem;   // DDPG OU state [ou_slots][K][N] (grown on demand)
+  // dynamic chunk schedule of the fused stock rollout (rollout_tc.cuh TcParams::q_ctr)
+  uint32_t* q_ctr;      // work-item counter (zeroed before each launch)
+  uint32_t seg_epoch;   // per-call value of the tiles' progress flags
+  uint32_t ctr_seg, ctr_seg_fallback;   // rollouts launched with the chunk schedule / refused
+  int seg_fallback_err;                 // cudaError_t of the last refusal
 };
 
 struct fin_policy {
@@ -312,6 +318,8 @@ int fin_env_create(const fin_env_config* cfg, const float* market, int64_t marke
   size_t bytes = 8 * n8 * sizeof(double) / 8;   // 8 double arrays
   bytes += N * 4 * sizeof(int32_t);              // t_ep, window, tau, m_n
   bytes += N * FIN_AGG_LEN * sizeof(double) + 16; // per-env aggregate partials
+  bytes += N * (sizeof(int32_t) + sizeof(double)) + 32;   // seg_cnt, seg_rsum
+  bytes += ((N + 127) / 128) * sizeof(uint32_t) + 16;      // seg_flag
   const size_t KO = (K + 7) / 8;                 // holdings: asset octets (hold_at)
   bytes += KO * 8 * N * sizeof(int16_t);
   bytes += 256;
@@ -340,6 +348,9 @@ int fin_env_create(const fin_env_config* cfg, const float* market, int64_t marke
   d.m_n = reinterpret_cast<int32_t*>(take(N * 4));
   d.hold = reinterpret_cast<int16_t*>(take(KO * 8 * N * 2));
   d.agg_env = reinterpret_cast<double*>(take(N * FIN_AGG_LEN * 8));
+  d.seg_rsum = reinterpret_cast<double*>(take(N * 8));
+  d.seg_cnt = reinterpret_cast<int32_t*>(take(N * 4));
+  d.seg_flag = reinterpret_cast<uint32_t*>(take(((N + 127) / 128) * 4));
   if ((size_t)(p - static_cast<uint8_t*>(env->state_mem)) > bytes) {
     cudaFree(env->state_mem);
     delete env;
@@ -462,13 +473,20 @@ int fin_env_counters(fin_env* env, uint32_t* counters, int32_t clear) {
   FIN_CUDA(cudaStreamSynchronize(env->last_stream));
   FIN_CUDA(cudaMemcpy(counters, env->d.flags + FIN_CTR_EXACT_REDO, FIN_CTR_LEN * sizeof(uint32_t),
                       cudaMemcpyDeviceToHost));
-  if (clear) FIN_CUDA(cudaMemset(env->d.flags + FIN_CTR_EXACT_REDO, 0, FIN_CTR_LEN * sizeof(uint32_t)));
+  counters[1] = env->ctr_seg;
+  counters[2] = env->ctr_seg_fallback;
+  counters[3] = (uint32_t)env->seg_fallback_err;
+  if (clear) {
+    FIN_CUDA(cudaMemset(env->d.flags + FIN_CTR_EXACT_REDO, 0, FIN_CTR_LEN * sizeof(uint32_t)));
+    env->ctr_seg = env->ctr_seg_fallback = 0;
+  }
   return FIN_OK;
 }
 
 void fin_env_destroy(fin_env* env) {
   if (!env) return;
   cudaStreamSynchronize(env->last_stream);
+  if (env->q_ctr) cudaFree(env->q_ctr);
   if (env->agg_scratch) cudaFree(env->agg_scratch);
   if (env->z1s) cudaFree(env->z1s);
   if (env->ou_mem) cudaFree(env->ou_mem);
@@ -650,6 +668,42 @@ int prepare_z1s(fin_env* env, const fin_policy* const* members, int n, int net, 
   return FIN_OK;
 }
 
+// The dynamic chunk schedule (rollout_tc.cuh TcParams::q_ctr): the T steps
+// of every tile are cut into chunks of decreasing length -- a quarter of the remaining
+// steps, between 8 and max(64, T / 8) -- so the last rounds of work items are short and
+// the CTAs (whose speeds differ by a few percent) finish together.
+int chunk_plan(int T, int32_t* t0, int max_chunks) {
+  int n = 0, pos = 0;
+  const int cap = T / 8 > 64 ? T / 8 : 64;
+  while (pos < T && n < max_chunks - 1) {
+    const int rem = T - pos;
+    int c = rem / 4;
+    c = c < 8 ? 8 : (c > cap ? cap : c);
+    if (c > rem) c = rem;
+    t0[n++] = pos;
+    pos += c;
+  }
+  if (pos < T) t0[n++] = pos;   // (cap reached: one last chunk takes the rest)
+  t0[n] = T;
+  return n;
+}
+
+int prepare_chunks(fin_env* env, int n_tiles, int T, int grid, tc::TcParams& p) {
+  if (!env->q_ctr) FIN_CUDA(cudaMalloc(&env->q_ctr, 64));
+  p.n_chunks = chunk_plan(T, p.chunk_t0, 17);
+  p.n_tiles = n_tiles;
+  p.q_ctr = env->q_ctr;
+  p.seg_flag = env->d.seg_flag;
+  if (++env->seg_epoch >= (1u << 24)) {   // epoch << 8 would wrap: clear the flags, restart at 1
+    FIN_CUDA(cudaMemsetAsync(env->d.seg_flag, 0, ((env->d.N + 127) / 128) * sizeof(uint32_t), env->last_stream));
+    env->seg_epoch = 1;
+  }
+  p.seg_epoch = env->seg_epoch;
+  p.seg_grid = grid;
+  FIN_CUDA(cudaMemsetAsync(env->q_ctr, 0, sizeof(uint32_t), env->last_stream));
+  return FIN_OK;
+}
+
 int fill_noise(const fin_noise* noise, tc::TcParams& p) {
   if (!noise) {
     p.noise_mode = FIN_NOISE_NONE;
@@ -692,9 +746,42 @@ int fin_rollout(fin_env* env, const fin_policy* const* members, int32_t n_member
     p.o.agg_partial = env->agg_scratch;
   }
   env->last_stream = S(stream);
+  if (env->d.task == FIN_STOCK) {
+    const int grid = fin::stock_seg_grid(net, p, env->d.N);
+    if (grid > 0) {
+      rc = prepare_chunks(env, n_tiles, T, grid, p);
+      if (rc != FIN_OK) return rc;
+    }
+    if (getenv("FIN_SEG_PROF")) {
+      p.seg_grid = grid > 0 ? grid : n_tiles;
+      FIN_CUDA(cudaMalloc(&p.seg_prof, (size_t)p.seg_grid * 16 * 8));
+      FIN_CUDA(cudaMemset(p.seg_prof, 0, (size_t)p.seg_grid * 16 * 8));
+    }
+  }
   int tiles = 1;
   cudaError_t e = env->d.task == FIN_STOCK ? fin::launch_stock_rollout(net, p, env->d.N, &tiles, S(stream))
                                            : fin::launch_crypto_rollout(net, p, env->d.N, &tiles, S(stream));
+  if (p.seg_prof) {   // debug: per-CTA segment timeline -> file FIN_SEG_PROF
+    cudaStreamSynchronize(S(stream));
+    std::vector<unsigned long long> h((size_t)p.seg_grid * 16);
+    cudaMemcpy(h.data(), p.seg_prof, h.size() * 8, cudaMemcpyDeviceToHost);
+    cudaFree(p.seg_prof);
+    if (FILE* f = fopen(getenv("FIN_SEG_PROF"), "wb")) {
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+  }
+  if (p.q_ctr) {
+    if (e == cudaSuccess) {
+      ++env->ctr_seg;
+    } else {   // the balanced grid is not co-resident (cooperative launch refused): one tile per CTA
+      (void)cudaGetLastError();
+      ++env->ctr_seg_fallback;
+      env->seg_fallback_err = (int)e;
+      p.q_ctr = nullptr;
+      e = fin::launch_stock_rollout(net, p, env->d.N, &tiles, S(stream));
+    }
+  }
   mark_used(members, n_members, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fin_rollout launch");
   if (out && out->agg) {

@@ -49,6 +49,9 @@ struct EnvDev {
   int32_t* m_n;          // number of returns
   double* agg_env;       // [FIN_AGG_LEN][N] per-env aggregate partials of the running rollout (fused
                          // stock rollout: touched once per episode, kept out of the registers)
+  int32_t* seg_cnt;      // [N] balanced schedule: episodes completed so far in this call (head -> tail)
+  double* seg_rsum;      // [N] balanced schedule: reward sum so far in this call (head -> tail)
+  uint32_t* seg_flag;    // [ceil(N / 128)] balanced schedule: epoch of the last published head per tile
   uint32_t* flags;       // sticky device error word; flags[FIN_CTR_*] are event counters (fin_env_counters)
 };
 // counters after the flags word (same 64-B block)

@@ -50,6 +50,7 @@ struct CryptoOps {
   static constexpr int IN = 2 + FIN_C_FACTORS;  // 103
   static constexpr int KT8 = Plan::kIn / 8;
   static constexpr bool kSplitOK = true;        // column-split epilogues (no layer-1 addend)
+  static constexpr bool kSegments = false;
   static constexpr bool kEpiPipe = true;        // double-buffered TMEM loads in the epilogues
   static constexpr bool kStageBias = true;
   static constexpr bool kL1Bcast = true;        // uniform tiles: shared layer-1 inputs read with SBO = 0

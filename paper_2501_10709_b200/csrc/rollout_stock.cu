@@ -57,6 +57,7 @@ template <int KA, int IA, class Plan, bool ENS = true, bool LOG = true>
 struct StockOps {
   static constexpr int KOU = ENS ? KA : 1;
   static constexpr bool kSplitOK = false;
+  static constexpr bool kSegments = true;   // balanced persistent schedule (init_seg / finalize_seg)
   static constexpr bool kL1Bcast = false;   // (crypto only: broadcast layer-1 A operand)
   static constexpr bool kEpiPipe = false;
   // ensembles read biases from L2 (no staged copy): the C2 ensemble then fits the dual layout
@@ -78,7 +79,10 @@ struct StockOps {
   // its window after a reset -- envs of a tile step in lockstep).
   static constexpr int kOffP = 0;
   static constexpr int kOffZ = kPriceRows * KP4 * 8;
-  static constexpr int kRegion = kOffZ + FIN_STAGE_MEMBERS * Plan::kH1 * 4;
+  // z1s rows staged for up to kStageM members (the single policy: 1 -- 6 KB less shared
+  // memory per CTA, so two CTAs per SM also pass the cooperative launch's occupancy check)
+  static constexpr int kStageM = ENS ? FIN_STAGE_MEMBERS : 1;
+  static constexpr int kRegion = kOffZ + kStageM * Plan::kH1 * 4;
   static constexpr int kOffS = 2 * kRegion;
   static constexpr int kOffB = kOffS + 16;
   static constexpr int kStageBytes = kOffB + 16;
@@ -102,22 +106,30 @@ struct StockOps {
     MetricAcc m;       // (the aggregate partials live in e.agg_env: touched once per episode)
     int cnt;
     double rsum;
+    int t_begin, t_end;   // steps of this segment (whole call: 0, T)
     bool oor, bad, nonfinite;
   };
 
   __device__ __forceinline__ static void init(State& st, const TcParams& p, int env, int row) {
+    init_seg(st, p, env, row, 0, p.T);
+  }
+  // steps [t0, t1) of the call; a tail (t0 > 0) continues the episode count and reward sum
+  // its head left in seg_cnt / seg_rsum and the aggregate partials in agg_env
+  __device__ __forceinline__ static void init_seg(State& st, const TcParams& p, int env, int row, int t0, int t1) {
     const EnvDev& e = p.e;
     st.live = env < e.N;
+    st.t_begin = t0;
+    st.t_end = t1;
     st.round = 0;
-    st.cnt = 0;
-    st.rsum = 0.0;
+    st.cnt = (t0 > 0 && st.live) ? e.seg_cnt[env] : 0;
+    st.rsum = (t0 > 0 && st.live) ? e.seg_rsum[env] : 0.0;
     st.oor = st.bad = st.nonfinite = false;
     st.d = 0;
     st.vc = 0.0;
     st.sb = 0;
     st.kcur = st.koth = -1;
     st.pend = -1;
-    if (st.live) agg_init_g(e.agg_env + env, (size_t)e.N);
+    if (st.live && t0 == 0) agg_init_g(e.agg_env + env, (size_t)e.N);
     if (st.live) {
       st.b = e.cash[env];
       st.vc = e.vcur[env];
@@ -146,7 +158,7 @@ struct StockOps {
     const EnvDev& e = p.e;
     stage_price_rows(e, reinterpret_cast<double*>(reg + kOffP), k, gtid, 128);
     float* zs = reinterpret_cast<float*>(reg + kOffZ);
-    for (int j = gtid; j < min(p.M, FIN_STAGE_MEMBERS) * Plan::kH1; j += 128) {
+    for (int j = gtid; j < min(p.M, kStageM) * Plan::kH1; j += 128) {
       const int m = j / Plan::kH1, n = j % Plan::kH1;
       zs[j] = __ldg(p.z1s + ((size_t)m * p.z1s_rows + k) * Plan::kH1 + n);
     }
@@ -158,7 +170,7 @@ struct StockOps {
     const uint8_t* src = reinterpret_cast<const uint8_t*>(e.px + (size_t)k * kPriceRows * e.kp);
     for (int j = gtid; j < np; j += 128) sm100::cp_async16(reg + kOffP + 16 * j, src + 16 * j);
     constexpr int nz = Plan::kH1 / 4;                   // chunks per member z1s row
-    for (int j = gtid; j < min(p.M, FIN_STAGE_MEMBERS) * nz; j += 128) {
+    for (int j = gtid; j < min(p.M, kStageM) * nz; j += 128) {
       const int m = j / nz, c = j % nz;
       sm100::cp_async16(reg + kOffZ + (m * Plan::kH1 + 4 * c) * 4,
                         p.z1s + ((size_t)m * p.z1s_rows + k) * Plan::kH1 + 4 * c);
@@ -176,7 +188,7 @@ struct StockOps {
     st.bar_id = bar_id;
     GroupSlots* gs = reinterpret_cast<GroupSlots*>(stg + kOffS);
     int* bc = reinterpret_cast<int*>(stg + kOffB);
-    if (t == 0) gs_init(gs, gtid, bar_id);
+    if (t == st.t_begin) gs_init(gs, gtid, bar_id);
     if (st.live) {
       st.d = day_of(e, st.w, st.t_ep);
       if (st.d < 0 || st.d + 1 >= e.rows) { st.bad = true; st.d = 0; }
@@ -215,7 +227,7 @@ struct StockOps {
     if (gtid == 0) gs->staged = st.kcur;   // for group_apply in finish_step (after its barrier)
     // rows of the predicted next day into the other buffer, under this step's work
     // (that buffer was last read in the previous step, before this step's barriers)
-    if (dn >= 0 && t + 1 < p.T && dn != st.kcur) {
+    if (dn >= 0 && t + 1 < st.t_end && dn != st.kcur) {
       prefetch_row(p, dn, gtid, region(stg, st.sb ^ 1));
       st.koth = dn;
       st.pend = dn;
@@ -225,7 +237,7 @@ struct StockOps {
 
   // factored layer 1: the shared-input term of this env's day, member m
   __device__ __forceinline__ static const float* l1_addend(State& st, const TcParams& p, int m, uint8_t* stg) {
-    if (st.zsm && m < FIN_STAGE_MEMBERS) return reinterpret_cast<const float*>(region(stg, st.sb) + kOffZ) + m * Plan::kH1;
+    if (st.zsm && m < kStageM) return reinterpret_cast<const float*>(region(stg, st.sb) + kOffZ) + m * Plan::kH1;
     return p.z1s + ((size_t)m * p.z1s_rows + st.d) * Plan::kH1;
   }
 
@@ -442,6 +454,21 @@ struct StockOps {
 
   __device__ __forceinline__ static void finalize(State& st, const TcParams& p, int env, int gtid, int bar_id,
                                                   int tile) {
+    finalize_rows(st, p, env, gtid, bar_id, tile, blockIdx.x * p.tiles_per_cta + tile, true);
+  }
+  // end of a segment of the balanced schedule: the state goes back to the env; the tile's
+  // aggregate row (indexed by the tile, as in the one-tile-per-CTA layout) only at its end
+  __device__ __forceinline__ static void finalize_seg(State& st, const TcParams& p, int env, int gtid, int bar_id,
+                                                      int tile, int t1) {
+    const bool last = t1 == p.T;
+    if (!last && st.live && !(LOG && p.act_only)) {
+      p.e.seg_cnt[env] = st.cnt;
+      p.e.seg_rsum[env] = st.rsum;
+    }
+    finalize_rows(st, p, env, gtid, bar_id, 0, tile, last);
+  }
+  __device__ __forceinline__ static void finalize_rows(State& st, const TcParams& p, int env, int gtid, int bar_id,
+                                                       int group, int agg_row, bool last) {
     const EnvDev& e = p.e;
     if (LOG && p.act_only) {   // fin_ensemble_act: only the single-DDPG register state may be committed
       if (ENS && p.commit_ou && p.n_ddpg == 1 && st.live) {
@@ -467,6 +494,7 @@ struct StockOps {
       if (st.bad) set_flag(e, FIN_FLAG_BAD_INDEX);
       if (st.nonfinite) set_flag(e, FIN_FLAG_NONFINITE);
     }
+    if (!last) return;
     AggAcc agg;
     agg_init(agg);
     if (st.live) {
@@ -475,8 +503,7 @@ struct StockOps {
     }
     agg.s[FIN_AGG_SUM_REWARD] = st.rsum;
     if (p.o.agg_partial)
-      agg_group_write(agg, p.o.agg_partial + ((size_t)blockIdx.x * p.tiles_per_cta + tile) * FIN_AGG_LEN, gtid,
-                      bar_id, tile);
+      agg_group_write(agg, p.o.agg_partial + (size_t)agg_row * FIN_AGG_LEN, gtid, bar_id, group);
   }
 };
 
@@ -488,6 +515,7 @@ struct ProbeOps {
   static constexpr int kStageBytes = 16;
   static constexpr bool kStageBias = true;
   static constexpr bool kSplitOK = false;
+  static constexpr bool kSegments = false;
   static constexpr bool kL1Bcast = false;   // (crypto only: broadcast layer-1 A operand)
   static constexpr bool kEpiPipe = false;
   static constexpr bool kFactored = !std::is_void<Obs>::value;
@@ -574,7 +602,7 @@ cudaError_t launch_auto(const TcParams& p, int n_envs, int* tiles, cudaStream_t 
     const bool fits = 2 * tc::Smem<Plan, RES, 1, Ops, kDualRing>::total(p.M) <= tc::kSmemLimit;
     if (!pair && fits && n_tiles > num_sms()) {
       *tiles = 1;
-      return tc::launch<Plan, RES, 1, Ops, kDualRing, 2>(p, n_envs, s);
+      return tc::launch<Plan, RES, 1, Ops, kDualRing, 2>(p, n_envs, s, p.q_ctr ? p.seg_grid : 0);
     }
   }
   if (n_tiles > num_sms() && p.M <= tc::Smem<Plan, RES, 2, Ops>::max_members()) {
@@ -585,23 +613,64 @@ cudaError_t launch_auto(const TcParams& p, int n_envs, int* tiles, cudaStream_t 
   return tc::launch<Plan, RES, 1, Ops>(p, n_envs, s);
 }
 
+// The balanced persistent schedule of a dual-layout launch: the grid of
+// resident CTAs (2 per SM) when there are more tiles than that, else 0 (one tile per CTA).
+// FIN_SEG=0 disables it (A/B runs).
+template <class Plan, bool RES, class Ops>
+int seg_grid_auto(const TcParams& p, int n_envs) {
+  if constexpr (RES || !Ops::kSegments) {
+    return 0;
+  } else {
+    const char* mode = getenv("FIN_TC_MODE");
+    const char* seg = getenv("FIN_SEG");
+    if ((mode && mode[0] == 'p') || (seg && seg[0] == '0') || p.act_only) return 0;
+    const int n_tiles = (n_envs + tc::kTileM - 1) / tc::kTileM;
+    if (2 * tc::Smem<Plan, RES, 1, Ops, kDualRing>::total(p.M) > tc::kSmemLimit || n_tiles <= num_sms()) return 0;
+    // two CTAs per SM (the dual layout's __launch_bounds__ minimum and shared-memory fit);
+    // the cooperative launch verifies that all of them are resident (else: plain grid)
+    const int grid = 2 * num_sms();
+    return n_tiles > grid ? grid : 0;
+  }
+}
+
+template <class Plan, bool RES, class Ops>
+struct StockKernel {
+  using P = Plan;
+  static constexpr bool R = RES;
+  using O = Ops;
+};
+
 // net: 0 = PlanStockC1 (K=30, I=8), 1 = PlanStockSmall (K=4, I=4), 3 = PlanStockPaper (K=30, I=8;
 // the paper's 64-32 net, 10 KB of weights: resident in shared memory, env-issued MMAs)
-cudaError_t launch_stock_rollout(int net, const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s) {
+template <class F>
+auto dispatch_stock(int net, const tc::TcParams& p, F&& f) -> decltype(f(StockKernel<PlanStockC1, false,
+                                                                            StockOps<30, 8, PlanStockC1, false>>{})) {
   const bool single = p.M == 1 && p.kinds[0] != FIN_DDPG_OU;
   const bool logs = p.act_only || p.o.mlp_out || p.o.mlp_hidden || p.o.cash || p.o.asset || p.o.hold || p.o.actions;
-  if (net == 0 && single && !logs)
-    return launch_auto<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false, false>>(p, n_envs, tiles, s);
-  if (net == 0 && single)
-    return launch_auto<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false>>(p, n_envs, tiles, s);
-  if (net == 0) return launch_auto<PlanStockC1, false, StockOps<30, 8, PlanStockC1, true>>(p, n_envs, tiles, s);
+  if (net == 0 && single && !logs) return f(StockKernel<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false, false>>{});
+  if (net == 0 && single) return f(StockKernel<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false>>{});
+  if (net == 0) return f(StockKernel<PlanStockC1, false, StockOps<30, 8, PlanStockC1, true>>{});
   if (net == 3 && single && !logs)
-    return launch_auto<PlanStockPaper, true, StockOps<30, 8, PlanStockPaper, false, false>>(p, n_envs, tiles, s);
-  if (net == 3 && single)
-    return launch_auto<PlanStockPaper, true, StockOps<30, 8, PlanStockPaper, false>>(p, n_envs, tiles, s);
-  if (net == 3) return launch_auto<PlanStockPaper, true, StockOps<30, 8, PlanStockPaper, true>>(p, n_envs, tiles, s);
-  if (net == 1) return launch_auto<PlanStockSmall, true, StockOps<4, 4, PlanStockSmall, true>>(p, n_envs, tiles, s);
-  return cudaErrorInvalidValue;
+    return f(StockKernel<PlanStockPaper, true, StockOps<30, 8, PlanStockPaper, false, false>>{});
+  if (net == 3 && single) return f(StockKernel<PlanStockPaper, true, StockOps<30, 8, PlanStockPaper, false>>{});
+  if (net == 3) return f(StockKernel<PlanStockPaper, true, StockOps<30, 8, PlanStockPaper, true>>{});
+  return f(StockKernel<PlanStockSmall, true, StockOps<4, 4, PlanStockSmall, true>>{});
+}
+
+cudaError_t launch_stock_rollout(int net, const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s) {
+  if (net != 0 && net != 1 && net != 3) return cudaErrorInvalidValue;
+  return dispatch_stock(net, p, [&](auto k) {
+    using K = decltype(k);
+    return launch_auto<typename K::P, K::R, typename K::O>(p, n_envs, tiles, s);
+  });
+}
+
+int stock_seg_grid(int net, const tc::TcParams& p, int n_envs) {
+  if (net != 0 && net != 1 && net != 3) return 0;
+  return dispatch_stock(net, p, [&](auto k) {
+    using K = decltype(k);
+    return seg_grid_auto<typename K::P, K::R, typename K::O>(p, n_envs);
+  });
 }
 
 // net: 0 = PlanStockC1, 1 = PlanStockSmall, 2 = PlanCrypto, 3 = PlanStockPaper, 4 = PlanCryptoPaper

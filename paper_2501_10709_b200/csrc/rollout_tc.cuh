@@ -26,6 +26,8 @@
 // layer's MMAs have completed when d_full fires), so the observation is rebuilt
 // for every ensemble member from the per-step staging area.
 #pragma once
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "fin_internal.cuh"
@@ -69,6 +71,22 @@ struct TcParams {
   float* z_out;
   int32_t B, in_dim, out_dim;
   int32_t tiles_per_cta;                  // set by launch(): aggregate partial rows per CTA
+  // Dynamic chunk schedule (Ops::kSegments, one tile per CTA).  The T
+  // steps of every tile are cut into n_chunks chunks [chunk_t0[k], chunk_t0[k + 1]) of
+  // decreasing length; work item i = chunk i / n_tiles of tile i % n_tiles (chunk-major).
+  // Each CTA's producer warp claims items with one atomicAdd on q_ctr (zeroed before the
+  // launch) and hands them to the MMA warp and the env warpgroup through a 2-slot
+  // shared-memory queue; an item (tile, k > 0) starts once seg_flag[tile] says chunk k - 1
+  // is done (flag = epoch << 8 | chunks done).  Blocking chains strictly decrease in claim
+  // order, so the schedule cannot deadlock, resident or not.  q_ctr null: one tile per CTA,
+  // all T steps.
+  uint32_t* q_ctr;
+  uint32_t* seg_flag;
+  uint32_t seg_epoch;
+  int32_t n_tiles, n_chunks;
+  int32_t chunk_t0[17];
+  int32_t seg_grid;                       // CTAs of the chunk schedule (2 per SM)
+  unsigned long long* seg_prof;           // debug (FIN_SEG_PROF): [grid][16] globaltimer stamps, or null
 };
 
 #ifndef FIN_PREPARE_LAYER
@@ -167,6 +185,9 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
   uint64_t* a_full = bars + 2 * kRing;
   uint64_t* d_full = bars + 2 * kRing + 1;          // [TILES]: one per tile
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kRing + 1 + TILES);
+  uint64_t* q_full = bars + 16;                                  // [2] item published (1 arrival)
+  uint64_t* q_empty = bars + 18;                                 // [2] item read (MMA warp + env group)
+  int4* q_item = reinterpret_cast<int4*>(bars + 32);             // [2] {tile, t0, t1, k} (tile < 0: end)
   // Resident weights: each tile's thread 0 issues its own MMAs right after the tile's
   // epilogue barrier (the issue code sits in the env warps' hot path; a separate MMA
   // warp woken per layer cost ~1,000 cycles per layer in the C3 timeline, mostly
@@ -178,6 +199,9 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // dynamic chunk schedule: item queue in shared memory (2 slots), filled by the producer
+  constexpr bool kSeg = Ops::kSegments && TILES == 1 && SPLIT == 1;
+  const bool segd = kSeg && p.q_ctr != nullptr;
 
   // ---- one-time setup
   for (int j = threadIdx.x; j < S::staged(M) * Plan::kBiasFloats; j += blockDim.x) {
@@ -191,6 +215,10 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
     }
     sm100::mbar_init(a_full, 128 * TILES);
     for (int tl = 0; tl < TILES; ++tl) sm100::mbar_init(&d_full[tl], 1);
+    for (int s = 0; s < 2; ++s) {
+      sm100::mbar_init(&q_full[s], 1);
+      sm100::mbar_init(&q_empty[s], 2);
+    }
     sm100::fence_mbar_init();
   }
   if (warp == 1) {
@@ -230,18 +258,39 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
       } else {
         const uint64_t pol = sm100::l2_policy_evict_last();
         uint32_t it = 0;
-        for (int t = 0; t < T; ++t)
-          for (int m = 0; m < M; ++m)
-#pragma unroll
-            for (int s = 0; s < NS; ++s, ++it) {   // unrolled: per-stage plan values fold to constants
-              const uint32_t slot = it % RING, ph = (it / RING) & 1;
-              sm100::mbar_wait_fast(&w_empty[slot], ph ^ 1);
-              FIN_TR(m == 0 && (s == 0 || s == NS - 1), t, s == 0 ? 30 : 31);
-              FIN_TR(m == 0 && s < 16, T + t, 16 + s);   // per-stage detail rows (trace [2T][32])
-              sm100::mbar_arrive_expect_tx(&w_full[slot], (uint32_t)Plan::bytes_of(s));
-              sm100::bulk_g2s_hint(sW + slot * Plan::kStageBytes, p.wpack[m] + Plan::offset_of(s),
-                                   (uint32_t)Plan::bytes_of(s), &w_full[slot], pol);
+        uint32_t qi = 0;
+        for (;;) {
+          int n_steps = T;
+          if (segd) {   // claim the next work item and publish it to the MMA warp and the env group
+            const uint32_t i = atomicAdd(p.q_ctr, 1u);
+            const uint32_t n_items = (uint32_t)p.n_tiles * (uint32_t)p.n_chunks;
+            int4 item = make_int4(-1, 0, 0, 0);
+            if (i < n_items) {
+              const int k = (int)(i / (uint32_t)p.n_tiles), tl = (int)(i % (uint32_t)p.n_tiles);
+              item = make_int4(tl, p.chunk_t0[k], p.chunk_t0[k + 1], k);
             }
+            const uint32_t qs = qi & 1u;
+            sm100::mbar_wait(&q_empty[qs], ((qi >> 1) & 1u) ^ 1u);
+            q_item[qs] = item;
+            sm100::mbar_arrive(&q_full[qs]);   // (release: the item store is visible to the waiters)
+            ++qi;
+            if (item.x < 0) break;
+            n_steps = item.z - item.y;
+          }
+          for (int t = 0; t < n_steps; ++t)
+            for (int m = 0; m < M; ++m)
+#pragma unroll
+              for (int s = 0; s < NS; ++s, ++it) {   // unrolled: per-stage plan values fold to constants
+                const uint32_t slot = it % RING, ph = (it / RING) & 1;
+                sm100::mbar_wait_fast(&w_empty[slot], ph ^ 1);
+                FIN_TR(m == 0 && (s == 0 || s == NS - 1), t, s == 0 ? 30 : 31);
+                FIN_TR(m == 0 && s < 16, T + t, 16 + s);   // per-stage detail rows (trace [2T][32])
+                sm100::mbar_arrive_expect_tx(&w_full[slot], (uint32_t)Plan::bytes_of(s));
+                sm100::bulk_g2s_hint(sW + slot * Plan::kStageBytes, p.wpack[m] + Plan::offset_of(s),
+                                     (uint32_t)Plan::bytes_of(s), &w_full[slot], pol);
+              }
+          if (!segd) break;
+        }
       }
     }
     __syncwarp();
@@ -251,7 +300,19 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
       uint32_t it = 0, a_use = 0;
       if (RESIDENT) sm100::mbar_wait(&w_full[0], 0);
       const uint32_t aa = sm100::smem_u32(sA), wa = sm100::smem_u32(sW);
-      for (int t = 0; t < T; ++t) {
+      uint32_t qi = 0;
+      for (;;) {
+      int n_steps = T;
+      if (segd) {
+        const uint32_t qs = qi & 1u;
+        sm100::mbar_wait(&q_full[qs], (qi >> 1) & 1u);
+        const int4 item = q_item[qs];
+        sm100::mbar_arrive(&q_empty[qs]);
+        ++qi;
+        if (item.x < 0) break;
+        n_steps = item.z - item.y;
+      }
+      for (int t = 0; t < n_steps; ++t) {
         for (int m = 0; m < M; ++m) {
 #pragma unroll
           for (int l = 0; l < Plan::kNL; ++l) {
@@ -301,6 +362,8 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
             FIN_TR(m == 0, t, 10 + 2 * l);
           }
         }
+      }
+      if (!segd) break;
       }
     }
     __syncwarp();
@@ -441,7 +504,6 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
     }
     if (!is_helper) {
     typename Ops::State st;
-    Ops::init(st, p, env, row);
     uint32_t d_use = 0;
     bool w_ready = false;   // resident weights landed (env-issued MMAs)
     int t_cur = 0;          // (the timeline's step index inside kick)
@@ -487,7 +549,48 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
         sm100::mbar_arrive(a_full);
       }
     };
-    for (int t = 0; t < T; ++t) {
+    // one work item = steps [t_begin, t_end) of one tile (without the chunk schedule: this
+    // CTA's tile, all T steps)
+    uint32_t qi = 0;
+    for (int si = 0;; ++si) {
+    int4 sg = make_int4(blockIdx.x * TILES + tile, 0, T, 0);
+    if constexpr (kSeg) {
+      if (segd) {
+        const uint32_t qs = qi & 1u;
+        sm100::mbar_wait(&q_full[qs], (qi >> 1) & 1u);
+        sg = q_item[qs];
+        ++qi;
+        sm100::named_bar_sync(bar_id, 128);          // every thread has read the slot
+        if (gtid == 0) sm100::mbar_arrive(&q_empty[qs]);
+        if (sg.x < 0) break;
+      }
+    }
+    const int env = sg.x * kTileM + row;
+    const int t_begin = sg.y, t_end = sg.z;
+    if constexpr (kSeg) {
+      if (p.seg_prof && gtid == 0 && si < 5) {
+        p.seg_prof[blockIdx.x * 16 + 3 * si] = sm100::globaltimer();
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.seg_prof[blockIdx.x * 16 + 15] = smid;
+      }
+      if (segd) {
+        if (sg.w > 0) {   // chunk k > 0: wait until the tile's chunk k - 1 is written back
+          if (gtid == 0) {
+            const uint32_t need = (p.seg_epoch << 8) | (uint32_t)sg.w;
+            while (sm100::ld_acquire_gpu(p.seg_flag + sg.x) < need) __nanosleep(128);
+          }
+          sm100::named_bar_sync(bar_id, 128);
+        }
+        Ops::init_seg(st, p, env, row, t_begin, t_end);
+      } else {
+        Ops::init(st, p, env, row);
+      }
+      if (p.seg_prof && gtid == 0 && si < 5) p.seg_prof[blockIdx.x * 16 + 3 * si + 1] = sm100::globaltimer();
+    } else {
+      Ops::init(st, p, env, row);
+    }
+    for (int t = t_begin; t < t_end; ++t) {
       t_cur = t;
       FIN_TR(row == 0 && tile == 0, t, 0);
       Ops::stage(st, p, env, gtid, t, stg, bar_id);
@@ -545,7 +648,25 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
       Ops::finish_step(st, p, env, t, stg);
       FIN_TR(row == 0 && tile == 0, t, 8);
     }
-    Ops::finalize(st, p, env, gtid, bar_id, tile);
+    if constexpr (kSeg) {
+      if (p.seg_prof && gtid == 0 && si < 5) p.seg_prof[blockIdx.x * 16 + 3 * si + 2] = sm100::globaltimer();
+      if (segd) {
+        Ops::finalize_seg(st, p, env, gtid, bar_id, sg.x, t_end);
+        if (t_end < T) {   // publish the tile's state for the item that runs its next chunk
+          sm100::named_bar_sync(bar_id, 128);
+          if (gtid == 0) {
+            __threadfence();
+            sm100::st_release_gpu(p.seg_flag + sg.x, (p.seg_epoch << 8) | (uint32_t)(sg.w + 1));
+          }
+        }
+      } else {
+        Ops::finalize(st, p, env, gtid, bar_id, tile);
+      }
+    } else {
+      Ops::finalize(st, p, env, gtid, bar_id, tile);
+    }
+    if (!segd) break;
+    }   // work items
     }   // first warpgroup
   }
   __syncthreads();
@@ -556,16 +677,26 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
 }
 
 template <class Plan, bool RESIDENT, int TILES, class Ops, int RING = kRing, int MINB = 1, int SPLIT = 1>
-cudaError_t launch(const TcParams& p, int n_envs, cudaStream_t s) {
+cudaError_t launch(const TcParams& p, int n_envs, cudaStream_t s, int seg_grid = 0) {
   using Sm = Smem<Plan, RESIDENT, TILES, Ops, RING>;
   auto kern = k_tc_rollout<Plan, RESIDENT, TILES, Ops, RING, MINB, SPLIT>;
   const int bytes = Sm::total(p.M);
   if (MINB > 1 && bytes * MINB > kSmemLimit) return cudaErrorInvalidConfiguration;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (err != cudaSuccess) return err;
+  // all of the SM's shared memory as shared memory (the occupancy that cooperative launches
+  // check assumes the function's preferred carveout; MINB CTAs need the maximum)
+  err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (err != cudaSuccess) return err;
   const int per_cta = kTileM * TILES;
   TcParams q = p;
   q.tiles_per_cta = TILES;
+  if (seg_grid > 0 && p.q_ctr) {
+    // chunk schedule: MINB CTAs per SM pull work items until the queue is empty
+    kern<<<seg_grid, 128 + 128 * TILES * SPLIT, bytes, s>>>(q);
+    return cudaGetLastError();
+  }
+  q.q_ctr = nullptr;
   kern<<<(n_envs + per_cta - 1) / per_cta, 128 + 128 * TILES * SPLIT, bytes, s>>>(q);
   return cudaGetLastError();
 }

@@ -703,6 +703,46 @@ def test_ensemble_dual_layout_matches_one_tile_per_cta():
     assert res[0]["done"].sum() == 2 * N and np.abs(res[0]["actions"]).sum() > 0
 
 
+@pytest.mark.parametrize("ens", [False, True])
+def test_chunk_schedule_matches_one_tile_per_cta(ens, monkeypatch):
+    """The dynamic chunk schedule (more tiles than resident CTAs: work items of 8-17 steps
+    pulled from a queue, a tile's state handed from chunk to chunk through global memory,
+    DESIGN.md 4.3) is bitwise equal to one tile per CTA for all T steps (FIN_SEG=0): N =
+    38,450 (301 tiles, the last ragged), T = 70 (chunk boundaries inside episodes of 30
+    steps, resets, windows), Philox noise -- rewards, done flags, episode metrics and
+    counts, the aggregate vector, the final env state; single policy (log-free production
+    kernel) and the PPO / SAC / DDPG ensemble."""
+    import torch
+    fin = _fin()
+    m = market.stock_c1(rows=1008)
+    spec = [(1, fin.FIN_PPO_GAUSS), (2, fin.FIN_SAC_SQUASH), (3, fin.FIN_DDPG_OU)] if ens else \
+        [(0, fin.FIN_PPO_GAUSS)]
+    pols = [fin.fin_policy_create(k, spol.kaiming_bf16(spol.STOCK_DIMS, s)) for s, k in spec]
+    N, T = 38450, 70
+    _, fcfg = stock_pair(num_envs=N, num_assets=30, num_indicators=8, num_rows=1008, episode_len=30,
+                         window_stride=5, num_windows=195, window_block=128)
+    res = []
+    for seg in ("1", "0"):
+        monkeypatch.setenv("FIN_SEG", seg)
+        env = fin.fin_env_create(fcfg, m.market)
+        fin.fin_env_counters(env, clear=True)
+        logs = dict(reward=zeros((T, N), torch.float32), done=zeros((T, N), torch.uint8),
+                    ep_metrics=zeros((3, N, 3), torch.float64), ep_count=zeros(N, torch.int32),
+                    agg=zeros(8, torch.float64))
+        fin.fin_rollout(env, pols, T, fin.make_noise(fin.FIN_NOISE_PHILOX, 77), fin.make_traj(**logs))
+        c = fin.fin_env_counters(env)
+        assert c["balanced_rollouts"] == (1 if seg == "1" else 0), c
+        assert fin.fin_env_check(env) == 0
+        cash, hold = zeros(N, torch.float64), zeros((N, 30), torch.int16)
+        fin.fin_env_get_state(env, cash=cash, hold=hold)
+        r = {k: host(v) for k, v in logs.items()}
+        r["cash_end"], r["hold_end"] = host(cash), host(hold)
+        res.append(r)
+    for k in res[0]:
+        assert np.array_equal(res[0][k].view(np.uint8), res[1][k].view(np.uint8)), k
+    assert res[0]["done"].sum() == 2 * N and np.all(res[0]["ep_count"] == 2)
+
+
 def test_crypto_tile_composition_invariance():
     """An env's crypto rollout does not depend on its tile-mates.  Tile 0 of 4,096 envs is made
     non-uniform (env 0 starts at row 7, its 127 tile-mates at row 0: per-env observation rows,
