@@ -29,8 +29,10 @@ cudaError_t launch_kl_diversity(const float* out, int M, int B, int K, int kind,
                                 cudaStream_t s);
 cudaError_t launch_crypto_rollout(int net, const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s);
 cudaError_t launch_mlp_probe(int net, const tc::TcParams& p, int n_rows, cudaStream_t s);
-cudaError_t launch_z1s_market(int net, const float* w1s_t, int H, const EnvDev& e, float* z1s, cudaStream_t s);
-cudaError_t launch_z1s_probe(int net, const float* w1s_t, int H, const uint16_t* x, int B, int in_dim, float* z1s,
+cudaError_t launch_z1s_market(int net, const float* w1s_t, const float* b1, int H, const EnvDev& e, float* z1s,
+                              cudaStream_t s);
+cudaError_t launch_z1s_probe(int net, const float* w1s_t, const float* b1, int H, const uint16_t* x, int B, int in_dim,
+                             float* z1s,
                              cudaStream_t s);
 }  // namespace fin
 
@@ -63,6 +65,7 @@ struct fin_policy {
   float* bias;                 // device, [H1 | H2 | (H3) | OUT_PAD] (TcPlan::bias_off)
   uint8_t bias_nz;             // bit l: layer l has a non-zero bias (an all-zero bias is skipped)
   float* w1s_t;                // stock: device [S][HID] shared columns of W1 (exact bf16 values), else null
+  bool b1_in_z1s;              // factored stock net with a non-zero layer-1 bias: folded into z1s (f64)
   uint64_t uid;                // process-unique id (keys the env's z1s cache; addresses can be reused)
   cudaEvent_t used;            // recorded on the stream of every call that reads the policy (destroy waits on it)
 };
@@ -538,6 +541,10 @@ int fin_policy_create(int32_t kind, int32_t n_layers, const int32_t* dims, const
     if (bias && bias[l])
       for (int n = 0; n < dims[l + 1]; ++n)
         if (bias[l][n] != 0.f) pol->bias_nz |= 1u << l;
+  if (!w1s.empty() && (pol->bias_nz & 1u)) {   // z1s carries b1: epilogues never add it
+    pol->b1_in_z1s = true;
+    pol->bias_nz &= ~1u;
+  }
   for (int l = 0; l < 5; ++l) pol->dims[l] = l <= n_layers ? dims[l] : 0;
   cudaError_t e = cudaMalloc(&pol->wpack, wp.size());
   if (e == cudaSuccess) e = cudaMalloc(&pol->bias, bp.size() * sizeof(float));
@@ -659,7 +666,8 @@ int prepare_z1s(fin_env* env, const fin_policy* const* members, int n, int net, 
     env->z1s_cap = need;
   }
   for (int m = 0; m < n; ++m) {
-    cudaError_t e = fin::launch_z1s_market(net, members[m]->w1s_t, H, env->d, env->z1s + (size_t)m * env->d.rows * H, s);
+    cudaError_t e = fin::launch_z1s_market(net, members[m]->w1s_t, members[m]->b1_in_z1s ? members[m]->bias : nullptr,
+                                           H, env->d, env->z1s + (size_t)m * env->d.rows * H, s);
     if (e != cudaSuccess) return cuda_fail(e, "z1s precompute");
   }
   env->z1s_key = key;
@@ -890,7 +898,9 @@ int fin_mlp_forward(const fin_policy* pol, const uint16_t* x, int32_t B, float* 
   cudaError_t e = cudaSuccess;
   if (pol->w1s_t) {  // factored stock net: shared-input term of each probe row
     e = cudaMallocAsync(&z1s, sizeof(float) * (size_t)B * pol->dims[1], s);
-    if (e == cudaSuccess) e = fin::launch_z1s_probe(pol->net, pol->w1s_t, pol->dims[1], x, B, pol->dims[0], z1s, s);
+    if (e == cudaSuccess)
+      e = fin::launch_z1s_probe(pol->net, pol->w1s_t, pol->b1_in_z1s ? pol->bias : nullptr, pol->dims[1], x, B,
+                                pol->dims[0], z1s, s);
     p.z1s = z1s;
   }
   if (e == cudaSuccess) e = fin::launch_mlp_probe(pol->net, p, B, s);

@@ -51,6 +51,8 @@ struct CryptoOps {
   static constexpr int KT8 = Plan::kIn / 8;
   static constexpr bool kSplitOK = true;        // column-split epilogues (no layer-1 addend)
   static constexpr bool kSegments = false;
+  static constexpr bool kL1Init = false;
+  static constexpr int kOffImgT = 0;
   static constexpr bool kEpiPipe = true;        // double-buffered TMEM loads in the epilogues
   static constexpr bool kStageBias = true;
   static constexpr bool kL1Bcast = true;        // uniform tiles: shared layer-1 inputs read with SBO = 0

@@ -79,12 +79,22 @@ struct StockOps {
   // its window after a reset -- envs of a tile step in lockstep).
   static constexpr int kOffP = 0;
   static constexpr int kOffZ = kPriceRows * KP4 * 8;
-  // z1s rows staged for up to kStageM members (the single policy: 1 -- 6 KB less shared
-  // memory per CTA, so two CTAs per SM also pass the cooperative launch's occupancy check)
+  // FIN_L1_INIT=1 (A/B, off by default): the layer-1 accumulator starts at z1s[d] (+ b1),
+  // stored into each env's TMEM row with tcgen05.st before the layer-1 MMAs, instead of
+  // the epilogue adding it (same values for uniform and mixed tiles, same bits): measured
+  // neutral (7.49 vs 7.37 ms at 65,536 envs).  Also measured and not kept: a tcgen05.cp of
+  // a broadcast image of the row (SBO = 0): 32 copies of 8 columns cost ~2.3 k cycles on
+  // the tile's critical path (scripts/micro/tmem_cp_rate.cu).
+#ifndef FIN_L1_INIT
+#define FIN_L1_INIT 0
+#endif
+  static constexpr bool kL1Init = FIN_L1_INIT && !ENS;
+  // z1s rows staged (the epilogue addend of up to kStageM ensemble members; kL1Init: 1)
   static constexpr int kStageM = ENS ? FIN_STAGE_MEMBERS : 1;
   static constexpr int kRegion = kOffZ + kStageM * Plan::kH1 * 4;
   static constexpr int kOffS = 2 * kRegion;
-  static constexpr int kOffB = kOffS + 16;
+  static constexpr int kOffB = kOffS + 16;      // int[4]: d0, predicted day, -, -
+  static constexpr int kOffImgT = 0;
   static constexpr int kStageBytes = kOffB + 16;
 
   struct State {
@@ -179,6 +189,27 @@ struct StockOps {
   }
   __device__ __forceinline__ static uint8_t* region(uint8_t* stg, int b) { return stg + b * kRegion; }
 
+  // kL1Init: this env's row of the layer-1 accumulator <- z1s[d] (+ b1) of its day
+  __device__ __forceinline__ static void l1_init_rows(State& st, const TcParams& p, uint32_t t_lane, uint8_t* stg) {
+    if constexpr (kL1Init) {
+      const float* src = st.zsm ? reinterpret_cast<const float*>(region(stg, st.sb) + kOffZ)
+                                : p.z1s + (size_t)(st.live ? st.d : 0) * Plan::kH1;
+#pragma unroll 1
+      for (int c = 0; c < Plan::kH1 / 16; ++c) {
+        uint32_t v[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 x = reinterpret_cast<const float4*>(src + 16 * c)[q];
+          v[4 * q] = __float_as_uint(x.x); v[4 * q + 1] = __float_as_uint(x.y);
+          v[4 * q + 2] = __float_as_uint(x.z); v[4 * q + 3] = __float_as_uint(x.w);
+        }
+        sm100::tmem_st16(t_lane + (uint32_t)(16 * c), v);
+      }
+      sm100::tmem_wait_st();
+    }
+  }
+
+
   // once per step, all 128 threads of the tile: day of every env; if the tile sits on
   // one day, stage that day once (prices, z1s rows) for the whole step
   __device__ __forceinline__ static void stage(State& st, const TcParams& p, int env, int gtid, int t, uint8_t* stg,
@@ -225,6 +256,7 @@ struct StockOps {
       gs_bar(bar_id);
     }
     if (gtid == 0) gs->staged = st.kcur;   // for group_apply in finish_step (after its barrier)
+
     // rows of the predicted next day into the other buffer, under this step's work
     // (that buffer was last read in the previous step, before this step's barriers)
     if (dn >= 0 && t + 1 < st.t_end && dn != st.kcur) {
@@ -237,6 +269,7 @@ struct StockOps {
 
   // factored layer 1: the shared-input term of this env's day, member m
   __device__ __forceinline__ static const float* l1_addend(State& st, const TcParams& p, int m, uint8_t* stg) {
+    if constexpr (kL1Init) return nullptr;   // the accumulator started at z1s[d] + b1
     if (st.zsm && m < kStageM) return reinterpret_cast<const float*>(region(stg, st.sb) + kOffZ) + m * Plan::kH1;
     return p.z1s + ((size_t)m * p.z1s_rows + st.d) * Plan::kH1;
   }
@@ -516,6 +549,9 @@ struct ProbeOps {
   static constexpr bool kStageBias = true;
   static constexpr bool kSplitOK = false;
   static constexpr bool kSegments = false;
+  static constexpr bool kL1Init = false;
+  static constexpr int kOffB = 0;
+  static constexpr int kOffImgT = 0;
   static constexpr bool kL1Bcast = false;   // (crypto only: broadcast layer-1 A operand)
   static constexpr bool kEpiPipe = false;
   static constexpr bool kFactored = !std::is_void<Obs>::value;

@@ -322,6 +322,9 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
             sm100::tc_fence_after();
             const uint32_t a_sbo = (uint32_t)(Plan::kdim(l) / 8) * 128u;
             const uint32_t idesc = sm100::make_idesc_bf16(kTileM, Plan::nrows(l));
+            // layer 1 of a kL1Init member: the accumulator starts at the day's shared-input term
+            // (a uniform tile's image copied here, a mixed tile's rows stored by its env threads)
+            const bool l1init = Ops::kL1Init && l == 0;   // accumulator pre-set by the env threads
 #pragma unroll
             for (int s = Plan::first_stage(l); s < Plan::first_stage(l) + Plan::nstages(l); ++s) {
               uint32_t b_base;
@@ -349,7 +352,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
                 const uint64_t bd0 = sm100::make_sdesc(b_base, 128u, b_sbo);
                 for (int j = 0; j < nks; ++j)
                   sm100::mma_bf16(d_tmem, ad0 + (uint64_t)(16 * j), bd0 + (uint64_t)(16 * j), idesc,
-                                  (j0 + j) > 0 ? 1u : 0u);
+                                  (l1init || (j0 + j) > 0) ? 1u : 0u);
               }
               FIN_TR(m == 0 && s < 16, 2 * T + t, 16 + s);
               if (!RESIDENT) {
@@ -530,6 +533,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
           // tile sees the same shared inputs (same operand values, same MMA sequence)
           uint32_t bc = 0;
           if constexpr (Ops::kL1Bcast) bc = l == 0 ? Ops::l1_bcast(st, stg) : 0u;
+          const bool l1init = Ops::kL1Init && l == 0;   // accumulator pre-set by the env threads
           for (int s = Plan::first_stage(l); s < Plan::first_stage(l) + Plan::nstages(l); ++s) {
             const uint32_t b_base = sm100::smem_u32(sW) + (uint32_t)(m * Plan::kMemberBytes + Plan::offset_of(s));
             const int j0 = Plan::j0_of(s), nks = Plan::nks_of(s);
@@ -539,7 +543,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
             for (int j = 0; j < nks; ++j) {
               uint64_t ad = ad0 + (uint64_t)(16 * j);
               if (bc && j0 + j > 0) ad = sm100::make_sdesc(bc + (uint32_t)(j0 + j - 1) * 256u, 128u, 0u);
-              sm100::mma_bf16(d_tmem, ad, bd0 + (uint64_t)(16 * j), idesc, (j0 + j) > 0 ? 1u : 0u);
+              sm100::mma_bf16(d_tmem, ad, bd0 + (uint64_t)(16 * j), idesc, (l1init || (j0 + j) > 0) ? 1u : 0u);
             }
           }
           FIN_TR(tile == 0 && m == 0 && l == 0, t_cur, 26);
@@ -597,6 +601,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
       for (int m = 0; m < M; ++m) {
         if constexpr (Ops::kL1Bcast && kEnvIssue) Ops::build_obs_bcast(st, p, env, row, t, m, xa, stg);
         else Ops::build_obs(st, p, env, row, t, m, xa, stg);
+        if constexpr (Ops::kL1Init) Ops::l1_init_rows(st, p, t_lane, stg);
         kick(m, 0);
         FIN_TR(row == 0 && tile == 0 && m == 0, t, 1);
         // biases of the first FIN_STAGE_MEMBERS members in shared memory, the rest from L2

@@ -1,5 +1,7 @@
 // zshared.cu -- the shared part of layer 1 for the factored stock policy:
-//     z1s[r][n] = sum_s W1_shared[n][s] * q(x_shared(r))[s]
+//     z1s[r][n] = sum_s W1_shared[n][s] * q(x_shared(r))[s]  (+ b1[n])
+// (the layer-1 bias is folded in here, in float64, when it is non-zero: the rollout and
+// the probe then never add it in their epilogues)
 // for every market day r (rollouts) or every probe row r (fin_mlp_forward), in
 // float64 (bf16 x bf16 products are exact in float64), rounded once to fp32.
 // One CTA per row: the row's shared inputs are converted to bf16 once into shared
@@ -21,8 +23,8 @@ __device__ __forceinline__ float market_shared_value(const float* mrow, int kp, 
 }
 
 template <class Obs>
-__global__ void k_z1s_market(const float* __restrict__ w1s_t /*[S][H]*/, int H, const float* __restrict__ market,
-                             int row_floats, int kp, float* __restrict__ z1s /*[rows][H]*/) {
+__global__ void k_z1s_market(const float* __restrict__ w1s_t /*[S][H]*/, const float* __restrict__ b1, int H,
+                             const float* __restrict__ market, int row_floats, int kp, float* __restrict__ z1s /*[rows][H]*/) {
   __shared__ double xs[Obs::kShared];
   const int r = blockIdx.x;
   const float* mrow = market + (size_t)r * row_floats;
@@ -32,13 +34,14 @@ __global__ void k_z1s_market(const float* __restrict__ w1s_t /*[S][H]*/, int H, 
   for (int n = threadIdx.x; n < H; n += blockDim.x) {
     double acc = 0.0;
     for (int s = 0; s < Obs::kShared; ++s) acc = fma((double)w1s_t[(size_t)s * H + n], xs[s], acc);
+    if (b1) acc += (double)b1[n];
     z1s[(size_t)r * H + n] = (float)acc;
   }
 }
 
 template <class Obs>
-__global__ void k_z1s_probe(const float* __restrict__ w1s_t, int H, const uint16_t* __restrict__ x, int in_dim,
-                            float* __restrict__ z1s) {
+__global__ void k_z1s_probe(const float* __restrict__ w1s_t, const float* __restrict__ b1, int H,
+                            const uint16_t* __restrict__ x, int in_dim, float* __restrict__ z1s) {
   __shared__ double xs[Obs::kShared];
   const int r = blockIdx.x;
   for (int s = threadIdx.x; s < Obs::kShared; s += blockDim.x) {
@@ -50,6 +53,7 @@ __global__ void k_z1s_probe(const float* __restrict__ w1s_t, int H, const uint16
   for (int n = threadIdx.x; n < H; n += blockDim.x) {
     double acc = 0.0;
     for (int s = 0; s < Obs::kShared; ++s) acc = fma((double)w1s_t[(size_t)s * H + n], xs[s], acc);
+    if (b1) acc += (double)b1[n];
     z1s[(size_t)r * H + n] = (float)acc;
   }
 }
@@ -59,17 +63,18 @@ __global__ void k_z1s_probe(const float* __restrict__ w1s_t, int H, const uint16
 namespace fin {
 
 // net 0 = C1 (K=30, I=8), 3 = the paper's 301-64-32-30 on the C1 env, net 1 = small (K=4, I=4)
-cudaError_t launch_z1s_market(int net, const float* w1s_t, int H, const EnvDev& e, float* z1s, cudaStream_t s) {
-  if (net == 0 || net == 3) k_z1s_market<ObsC1><<<e.rows, 256, 0, s>>>(w1s_t, H, e.market, e.row_floats, e.kp, z1s);
-  else if (net == 1) k_z1s_market<ObsSmall><<<e.rows, 128, 0, s>>>(w1s_t, H, e.market, e.row_floats, e.kp, z1s);
+cudaError_t launch_z1s_market(int net, const float* w1s_t, const float* b1, int H, const EnvDev& e, float* z1s,
+                              cudaStream_t s) {
+  if (net == 0 || net == 3) k_z1s_market<ObsC1><<<e.rows, 256, 0, s>>>(w1s_t, b1, H, e.market, e.row_floats, e.kp, z1s);
+  else if (net == 1) k_z1s_market<ObsSmall><<<e.rows, 128, 0, s>>>(w1s_t, b1, H, e.market, e.row_floats, e.kp, z1s);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 
-cudaError_t launch_z1s_probe(int net, const float* w1s_t, int H, const uint16_t* x, int B, int in_dim, float* z1s,
-                             cudaStream_t s) {
-  if (net == 0 || net == 3) k_z1s_probe<ObsC1><<<B, 256, 0, s>>>(w1s_t, H, x, in_dim, z1s);
-  else if (net == 1) k_z1s_probe<ObsSmall><<<B, 128, 0, s>>>(w1s_t, H, x, in_dim, z1s);
+cudaError_t launch_z1s_probe(int net, const float* w1s_t, const float* b1, int H, const uint16_t* x, int B, int in_dim,
+                             float* z1s, cudaStream_t s) {
+  if (net == 0 || net == 3) k_z1s_probe<ObsC1><<<B, 256, 0, s>>>(w1s_t, b1, H, x, in_dim, z1s);
+  else if (net == 1) k_z1s_probe<ObsSmall><<<B, 128, 0, s>>>(w1s_t, b1, H, x, in_dim, z1s);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }

@@ -743,6 +743,46 @@ def test_chunk_schedule_matches_one_tile_per_cta(ens, monkeypatch):
     assert res[0]["done"].sum() == 2 * N and np.all(res[0]["ep_count"] == 2)
 
 
+def test_stock_tile_composition_invariance():
+    """A tile whose envs sit on different market days (layer-1 accumulator rows written per
+    env with tcgen05.st) gives the same bits as tiles on one day (the day's image copied with
+    tcgen05.cp): handle A has tiles on windows 0 and 1 (window_block 128), handle B
+    interleaves the two windows env by env (window_block 1), with the supplied noise
+    permuted to match; T = 35 (a reset); every logged output bitwise equal, plus a
+    teacher-forced oracle check of the mixed handle."""
+    import torch
+    fin = _fin()
+    m = market.stock_c1(rows=100)
+    N, T, K = 256, 35, 30
+    layers = spol.random_bias(spol.kaiming_bf16(spol.STOCK_DIMS, 3), 4)
+    pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, layers)
+    noise = inputs.supplied_noise(T, 1, N, K, seed=5)
+    perm = np.empty(N, dtype=np.int64)          # B's env j plays A's env perm[j]
+    perm[0::2] = np.arange(128)
+    perm[1::2] = 128 + np.arange(128)
+    res = []
+    for wb, nz in ((128, noise), (1, noise[:, :, perm])):
+        ocfg, fcfg = stock_pair(num_envs=N, num_assets=K, num_indicators=8, num_rows=100, episode_len=30,
+                                num_windows=2, window_block=wb)
+        env = fin.fin_env_create(fcfg, m.market)
+        logs = dict(actions=zeros((T, N, K), torch.int16), cash=zeros((T, N), torch.float64),
+                    reward=zeros((T, N), torch.float32), mlp_out=zeros((T, 1, N, K), torch.float32),
+                    mlp_hidden=zeros((T, 1, N, 2, 256), torch.int16), done=zeros((T, N), torch.uint8),
+                    hold=zeros((T, N, K), torch.int16), asset=zeros((T, N), torch.float64),
+                    ep_metrics=zeros((3, N, 3), torch.float64), ep_count=zeros(N, torch.int32),
+                    agg=zeros(8, torch.float64))
+        fin.fin_rollout(env, [pol], T, fin.make_noise(fin.FIN_NOISE_SUPPLIED, 0, dev(np.ascontiguousarray(nz))),
+                        fin.make_traj(**logs))
+        assert fin.fin_env_check(env) == 0
+        res.append(({k: host(v) for k, v in logs.items()}, ocfg))
+    (ga, _), (gb, ocfg_b) = res
+    for k in ("actions", "cash", "reward", "mlp_out", "mlp_hidden", "done"):
+        ax = 2 if k in ("mlp_out", "mlp_hidden") else 1
+        assert np.array_equal(np.take(ga[k], perm, axis=ax), gb[k]), k
+    assert np.abs(gb["actions"]).sum() > 0
+    _teacher_forced_stock(gb, ocfg_b, m.market, [layers], [fin.FIN_PPO_GAUSS], np.ascontiguousarray(noise[:, :, perm]))
+
+
 def test_crypto_tile_composition_invariance():
     """An env's crypto rollout does not depend on its tile-mates.  Tile 0 of 4,096 envs is made
     non-uniform (env 0 starts at row 7, its 127 tile-mates at row 0: per-env observation rows,
