@@ -289,6 +289,7 @@ __global__ void __launch_bounds__(kK1Threads, FIN_K1_MINB)
         if (o.done) o.done[i] = 1;
       }
       d[q] = day_of(e, w[q], t[q]);
+      FIN_CHECK(!live[q] || (i >= 0 && i < e.N && w[q] >= 0 && w[q] < e.W));
       const bool bad = stepping && (d[q] < 0 || d[q] + 1 >= e.rows);
       if (bad) set_flag(e, FIN_FLAG_BAD_INDEX);
       go[q] = stepping && !bad;
@@ -435,6 +436,7 @@ __global__ void __launch_bounds__(kStep, FIN_K4_MINB) k_stock_replay(EnvDev e, c
     __syncwarp();
     PackedActs<KA> a;
     const size_t ti = (size_t)s * N + i;
+    FIN_CHECK(s >= 0 && s < T && (!live || i < N));
     slab_read<KA, EXACT>(e, sm.act[s & 1][wid], lane, K, live, a, oor,
                          (o.actions && live) ? o.actions + ti * K : nullptr);
     const bool stepping = live && !bad && t < e.L;

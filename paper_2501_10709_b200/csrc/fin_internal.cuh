@@ -4,6 +4,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include "../../include/fin.h"
 
@@ -11,6 +12,28 @@
 #define FIN_MAX_ASSETS 32
 #define FIN_MAX_MEMBERS 32   // ensemble members per rollout (Ensemble-3 = 30)
 #define FIN_STAGE_MEMBERS 4  // members whose bias / z1s rows live in shared memory (the rest: L2)
+
+// Device-side bounds checks (compute-sanitizer is closed on this pool): a build with
+// FIN_NVCC_FLAGS=-DFIN_CHECKS=1 traps on any violated index assumption of the hot kernels
+// (trajectory rows, market days, work items, shared-memory staging); production builds
+// compile them out.
+#ifndef FIN_CHECKS
+#define FIN_CHECKS 0
+#endif
+#if FIN_CHECKS
+#define FIN_CHECK(cond)                                                                          \
+  do {                                                                                           \
+    if (!(cond)) {                                                                               \
+      printf("FIN_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,     \
+             (int)blockIdx.x, (int)threadIdx.x);                                                 \
+      asm volatile("trap;");                                                                     \
+    }                                                                                            \
+  } while (0)
+#else
+#define FIN_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
 
 // Flat, by-value kernel parameter block describing one env handle on the device.
 // Internal state is SoA: element [k][i] of a [K][N] array is at k*N + i.

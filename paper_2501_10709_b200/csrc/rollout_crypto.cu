@@ -312,6 +312,7 @@ struct CryptoOps {
     if (!st.live) return;
     const EnvDev& e = p.e;
     const size_t ti = (size_t)t * e.N + env;
+    FIN_CHECK(t >= 0 && t < p.T && env >= 0 && env < e.N);
     if (st.t_ep >= e.L || st.t_ep + 1 >= e.rows) {
       st.bad = true;
       if (p.o.reward) p.o.reward[ti] = 0.f;

@@ -166,6 +166,7 @@ struct StockOps {
   // stage day k into buffer region reg: f64 price rows of day k and the members' z1s rows
   __device__ __noinline__ static void stage_row(const TcParams& p, int k, int gtid, uint8_t* reg) {
     const EnvDev& e = p.e;
+    FIN_CHECK(k >= 0 && k < e.rows && k < p.z1s_rows);
     stage_price_rows(e, reinterpret_cast<double*>(reg + kOffP), k, gtid, 128);
     float* zs = reinterpret_cast<float*>(reg + kOffZ);
     for (int j = gtid; j < min(p.M, kStageM) * Plan::kH1; j += 128) {
@@ -176,6 +177,7 @@ struct StockOps {
   // the same rows by cp.async (16-byte chunks, no wait): completed by the next stage()
   __device__ __forceinline__ static void prefetch_row(const TcParams& p, int k, int gtid, uint8_t* reg) {
     const EnvDev& e = p.e;
+    FIN_CHECK(k >= 0 && k < e.rows && k < p.z1s_rows);
     const int np = kPriceRows * e.kp / 2;                 // 16-B chunks of the price rows
     const uint8_t* src = reinterpret_cast<const uint8_t*>(e.px + (size_t)k * kPriceRows * e.kp);
     for (int j = gtid; j < np; j += 128) sm100::cp_async16(reg + kOffP + 16 * j, src + 16 * j);
@@ -404,6 +406,8 @@ struct StockOps {
   __device__ __forceinline__ static void finish_step(State& st, const TcParams& p, int env, int t, uint8_t* stg) {
     const EnvDev& e = p.e;
     const size_t ti = (size_t)t * e.N + env;
+    FIN_CHECK(!st.live || (t >= 0 && t < p.T && env >= 0 && env < e.N));
+    FIN_CHECK(!st.live || st.bad || (st.d >= 0 && st.d + 1 < e.rows));
     int a[KA];
     FIN_TR(threadIdx.x == 128, t, 17);
     const float inv_m = 1.f / (float)p.M;   // uniform mean (R20); the weighted sum is already scaled

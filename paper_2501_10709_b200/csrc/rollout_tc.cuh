@@ -571,6 +571,8 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
     }
     const int env = sg.x * kTileM + row;
     const int t_begin = sg.y, t_end = sg.z;
+    FIN_CHECK(!segd || (sg.x >= 0 && sg.x < p.n_tiles && sg.w >= 0 && sg.w < p.n_chunks));
+    FIN_CHECK(0 <= t_begin && t_begin < t_end && t_end <= T);
     if constexpr (kSeg) {
       if (p.seg_prof && gtid == 0 && si < 5) {
         p.seg_prof[blockIdx.x * 16 + 3 * si] = sm100::globaltimer();
