@@ -43,9 +43,13 @@ MLP_FLOP_PER_ENV_STEP = 2 * (301 * 256 + 256 * 256 + 256 * 30)    # 300,544: the
 # (DESIGN.md §4.3): 31 env-private inputs in layer 1, layers 2 and 3 unchanged
 FLOP_PER_ENV_STEP = 2 * (31 * 256 + 256 * 256 + 256 * 30)          # 162,304
 Z1S_FLOP_PER_ROLLOUT = 2 * 270 * 256 * ROWS   # fp64 CUDA-core precompute of the per-day layer-1 term
-# K1 algorithmic bytes per env-step: read cash 8 + cached asset 8 + holdings 60 +
-# clock 4 + window 4 + action 60; write cash 8 + asset 8 + holdings 60 + clock 4 + reward 4 + done 1
-STEP_BYTES_PER_ENV = 8 + 8 + 60 + 4 + 4 + 60 + 8 + 8 + 60 + 4 + 4 + 1   # 229
+# K1 algorithmic bytes per env-step: read cash 8 + holdings 60 + clock 4 + action 60,
+# write cash 8 + holdings 60 + clock 4 + reward 4 + done 1 = 209 B.  The kernel moves 229 B: it also
+# reads and writes the cached asset v (8 + 8) and reads the window (4) -- DESIGN.md 4.2.
+STEP_BYTES_ALGO = 8 + 60 + 4 + 60 + 8 + 60 + 4 + 4 + 1                  # 209
+STEP_BYTES_MOVED = STEP_BYTES_ALGO + 8 + 8 + 4                            # 229
+# K3 HBM bytes per env-step the fused rollout must write (reward f32 + done u8; state is on chip)
+ROLLOUT_HBM_BYTES = 5
 METRIC = "env-steps/sec (whole box) at 2048-65536 envs, 1/2/4/8 B200; % HBM roofline"
 WORKLOAD = "C1 30-stock env + 301-256-256-30 bf16 policy, 65536 envs/GPU, horizon 256, reset on done"
 
@@ -176,6 +180,53 @@ def _oracle_shard(args):
     return time.perf_counter() - t0
 
 
+def _oracle_c0(_):
+    """C0 in full (SURVEY d.5 (i)): K=4, I=4, 8 envs x 64 steps of supplied actions, no policy."""
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import stock as ostock
+    from synth import inputs, market
+    m = market.stock_c0()
+    cfg = ostock.StockEnvConfig(num_envs=8, num_assets=4, num_indicators=4, num_rows=m.rows, episode_len=64)
+    acts = inputs.stock_actions(64, 8, 4, seed=12)
+    t0 = time.perf_counter()
+    ostock.run_actions(cfg, m.market, acts)
+    return time.perf_counter() - t0
+
+
+def _oracle_c3(args):
+    """A C3 slice (SURVEY d.5 (iii)): n envs x T steps of the crypto env with the f64 Q-net."""
+    n_envs, T = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import crypto as ocry
+    from oracle import rollout as orol
+    from synth import market
+    from synth import policy as spol
+    rows = market.crypto_market(T, seed=41)
+    cfg = ocry.CryptoEnvConfig(num_envs=n_envs, episode_len=T)
+    layers = spol.kaiming_bf16(spol.CRYPTO_DIMS, 4)
+    t0 = time.perf_counter()
+    orol.crypto_q_rollout(cfg, rows, layers, T)
+    return time.perf_counter() - t0
+
+
+def oracle_slices():
+    """the oracle on ONE core -- the C1 slice (64 envs x 30 steps with the
+    f64 MLP), C0 in full, a C3 slice -- env-steps/s each."""
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[v] = "1"
+    import multiprocessing as mp
+    res = {"cores": 1}
+    with mp.get_context("spawn").Pool(1) as pool:
+        pool.map(_oracle_c0, [0])   # worker start-up and imports, not timed
+        s = pool.map(_oracle_shard, [(64, 30, 0)])[0]
+        res["c1_slice_64envs_x_30"] = 64 * 30 / s
+        s = pool.map(_oracle_c0, [0])[0]
+        res["c0_full_8envs_x_64"] = 8 * 64 / s
+        s = pool.map(_oracle_c3, [(64, 1000)])[0]
+        res["c3_slice_64envs_x_1000"] = 64 * 1000 / s
+    return res
+
+
 def oracle_rate(n_envs_per_core=2560, T=30, cores=None):
     """Oracle env-steps/s on the host's cores (multiprocessing over env shards)."""
     import multiprocessing as mp
@@ -289,16 +340,26 @@ def run_ours(args):
                       "global_envs": N * world, "parallelism": f"env-sharded dp{world}",
                       "l2": "flushed between timed steps (256 MiB write + 256 MiB read, outside the events)",
                       "noise": "philox"},
-           "gpu_launches": 2 * args.steps,   # per rollout: fused rollout + aggregate finalize (the layer-1
+           "gpu_launches": 2 * args.steps,   # per rollout: fused rollout + aggregate finalize, plus one
+                                             # memset of the chunk queue's counter (the layer-1
                                              # shared term is cached per env: computed by the first call)
-           "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops_sustained"],
-                        "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops_sustained"], "traffic": None,
+           "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"],
+                        "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops"], "traffic": None,
                         "kernel": "k_tc_rollout<PlanStockC1> (fused rollout)",
                         "flop_per_env_step": FLOP_PER_ENV_STEP,
+                        "frac_of_sustained": achieved / pk["bf16_tflops_sustained"],
                         "note": "tensor FLOPs the kernel executes (factored layer 1, DESIGN.md 4.3); the "
-                                "unfactored MLP is %d FLOP/env-step = %.1f TFLOP/s equivalent"
+                                "unfactored MLP is %d FLOP/env-step = %.1f TFLOP/s equivalent. Peak: the burst "
+                                "bf16 figure (one ~7 ms launch at the max SM clock between L2 flushes)"
                                 % (MLP_FLOP_PER_ENV_STEP, MLP_FLOP_PER_ENV_STEP * N * T / (kern_ms / 1e3) / 1e12),
-                        "peak_source": pk["source"] + " bf16 sustained"}}
+                        "peak_source": pk["source"] + " bf16 burst",
+                        "hbm": {"bytes_per_env_step": ROLLOUT_HBM_BYTES,
+                                "achieved_gbs": ROLLOUT_HBM_BYTES * N * T / (kern_ms / 1e3) / 1e9,
+                                "peak_gbs": pk["hbm_gbs"],
+                                "frac": ROLLOUT_HBM_BYTES * N * T / (kern_ms / 1e3) / 1e9 / pk["hbm_gbs"],
+                                "note": "BASELINE metric's % HBM roofline for the fused rollout: it writes reward "
+                                        "+ done (5 B/env-step), env state stays on chip; the HBM-bound kernels "
+                                        "are in extras (K1 / K4 / K6)"}}}
     prof = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(prof):
         with open(prof) as f:
@@ -315,7 +376,12 @@ def run_ours(args):
         out["extras"] = extras(fin, torch, pol)
     if rank == 0 and world == 1:
         rate, cores, sample = oracle_rate()
-        out["cpu_baseline"] = {"value": rate, "unit": "env-steps/s", "cores": cores, "kind": "oracle", "sample": sample}
+        out["cpu_baseline"] = {"value": rate, "unit": "env-steps/s", "cores": cores, "kind": "oracle", "sample": sample,
+                               "one_core": oracle_slices()}
+        out["cpu_baseline"]["gpu_over_oracle"] = {"all_cores": value / rate,
+                                                  "one_core_c1": value / out["cpu_baseline"]["one_core"]["c1_slice_64envs_x_30"],
+                                                  "note": "GPU / oracle speedups, labelled (the oracle is a deliberately "
+                                                          "plain float64 program)"}
         out["paper_context"] = {"note": "paper numbers are from one NVIDIA A100 with real data and PPO/DQN training "
                                         "(P:380, P:336); context only",
                                 "stock_samples_per_s_2048_envs_A100": 8813.81, "stock_speedup_2048_vs_1": 47.73,
@@ -441,6 +507,7 @@ def extras(fin, torch, pol):
     times, _ = time_rollouts(fin, torch, env, pol, 2048, 30, 10, 3, flush)
     out["configs1_2048envs_T30"] = 2048 * 30 / (statistics.mean(times) / 1e3)
     del env
+    out["z1s_precompute"] = z1s_cost(fin, torch)
     out.update(hbm_kernels(fin, torch))
     out["crypto_c3"] = crypto_c3(fin, torch)
     out["ensembles"] = ensembles(fin, torch)
@@ -448,6 +515,38 @@ def extras(fin, torch, pol):
     out["market_prep"] = market_prep(fin, torch)
     out["consumer"] = consumer(fin, torch)
     return out
+
+
+def z1s_cost(fin, torch):
+    """The per-day shared layer-1 term z1s (1008 days x 270 x 256 float64 FMAs) is cached per env
+    and recomputed only when the member list changes, so the headline's timed calls do not
+    include it (its first call does).  A training loop that updates the weights before every
+    rollout pays it each time: alternate two policies (every call recomputes) vs one policy."""
+    from synth import policy as spol
+    N, T = N_HEAD, T_HEAD
+    env = make_env(fin, N, 0)
+    pa = fin.fin_policy_create(fin.FIN_PPO_GAUSS, spol.kaiming_bf16(spol.STOCK_DIMS, 0))
+    pb = fin.fin_policy_create(fin.FIN_PPO_GAUSS, spol.kaiming_bf16(spol.STOCK_DIMS, 1))
+    z = lambda s, d: torch.zeros(s, dtype=d, device="cuda")  # noqa: E731
+    tr = fin.make_traj(reward=z((T, N), torch.float32), done=z((T, N), torch.uint8), agg=z(8, torch.float64))
+    nz = fin.make_noise(fin.FIN_NOISE_PHILOX, 3)
+
+    def timed(pols):
+        for q in pols[:2]:
+            fin.fin_rollout(env, [q], T, nz, tr)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for q in pols:
+            fin.fin_rollout(env, [q], T, nz, tr)
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / len(pols)
+
+    same = timed([pa] * 6)
+    alt = timed([pa, pb] * 3)
+    return {"ms_per_rollout_same_policy": same, "ms_per_rollout_new_weights_each_call": alt,
+            "z1s_ms": alt - same, "note": "excluded from the headline (cached); paid once per weight update"}
 
 
 def consumer(fin, torch):
@@ -701,8 +800,10 @@ def hbm_kernels(fin, torch):
     acts = torch.randint(-100, 101, (N, K_ASSETS), device="cuda", generator=g, dtype=torch.int16)
     tr = fin.make_traj(reward=z(N, torch.float32), done=z(N, torch.uint8))
     ms = b2b(lambda: fin.fin_env_step(env, acts, tr))
-    entry("step_kernel_hbm", "k_stock_step (K1)", N, STEP_BYTES_PER_ENV * N, ms,
-          "steady state: the same seeded U{-100..100} actions every step, so cash binds (exact affordability path)")
+    entry("step_kernel_hbm", "k_stock_step (K1)", N, STEP_BYTES_ALGO * N, ms,
+          "SURVEY d.3's 209 B/env-step (the kernel moves 229 B: cached asset and window too); steady state: "
+          "the same seeded U{-100..100} actions every step, so the cash binds in most steps")
+    res["step_kernel_hbm"]["moved_gbs"] = STEP_BYTES_MOVED * N / (ms / 1e3) / 1e9
     del env, acts, tr
     N, T = 1 << 20, 32
     env = make_env(fin, N, 0)
