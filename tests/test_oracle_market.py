@@ -145,3 +145,78 @@ def test_crypto_generator_distributions():
     assert abs(f.var(axis=0).mean() - 1.0) < 0.1
     ac = np.mean([np.corrcoef(f[:-1, k], f[1:, k])[0, 1] for k in range(101)])
     assert abs(ac - 0.9) < 0.02
+
+
+# ---------------------------------------------------------------- stock OHLCV generator (R-SGEN)
+from oracle import stock_market as osm  # noqa: E402
+
+
+def test_stock_gen_sigma0_closed_form():
+    """sigma = 0: the close is the deterministic GBM path S_{-1} e^{mu (d + 1)} (exact GBM step,
+    dt = 1); high = max(open, close) and low = min(open, close) exactly (the |Z| terms vanish)."""
+    D, K, mu = 40, 5, 3e-3
+    x = osm.generate(D, K, seed=9, mu=mu, sigma=0.0)
+    s_init = np.array([50.0 + 100.0 * osm.uniform(9, 0, osm.S_INIT, k) for k in range(K)])
+    d = np.arange(D)[:, None]
+    np.testing.assert_allclose(x[:, osm.CLOSE].astype(np.float64), s_init[None, :] * np.exp(mu * (d + 1)), rtol=3e-7)
+    np.testing.assert_allclose(x[:, osm.OPEN].astype(np.float64), s_init[None, :] * np.exp(mu * d), rtol=3e-7)
+    assert np.array_equal(x[:, osm.HIGH], np.maximum(x[:, osm.OPEN], x[:, osm.CLOSE]))
+    assert np.array_equal(x[:, osm.LOW], np.minimum(x[:, osm.OPEN], x[:, osm.CLOSE]))
+
+
+def test_stock_gen_flat_when_mu_sigma_zero():
+    x = osm.generate(12, 3, seed=4, mu=0.0, sigma=0.0)
+    for c in (osm.OPEN, osm.HIGH, osm.LOW, osm.CLOSE):
+        assert np.array_equal(x[:, c], np.broadcast_to(x[0, osm.CLOSE], x[:, c].shape))
+
+
+def test_stock_gen_bar_invariants_and_continuity():
+    """S:36 bar invariants L <= min(O, C) <= max(O, C) <= H, positive prices and volumes; the
+    open of day d is the close of day d - 1 (O_d = S_{d-1}, c.1); S0 in [50, 150)."""
+    x = osm.generate(60, 6, seed=21)
+    o, h, lo, c, v = (x[:, j] for j in range(5))
+    assert np.all(lo <= np.minimum(o, c)) and np.all(np.maximum(o, c) <= h)
+    assert np.all(lo > 0) and np.all(v > 0)
+    assert np.array_equal(o[1:], c[:-1])
+    assert np.all(o[0] >= 50.0 * (1 - 1e-6)) and np.all(o[0] < 150.0 * (1 + 1e-6))
+
+
+def test_stock_gen_vectorised_equals_loops():
+    """generate_np (element-wise Philox, for the C1 sizes) reproduces the plain loops: every
+    value within one float32 ulp (NumPy's and libm's exp / log may differ in the last float64
+    bit before the single f32 rounding)."""
+    a = osm.generate(30, 7, seed=5)
+    b = osm.generate_np(30, 7, seed=5)
+    ulp = np.spacing(np.abs(a))
+    assert np.all(np.abs(a.astype(np.float64) - b.astype(np.float64)) <= ulp)
+    assert np.mean(a == b) > 0.99
+
+
+def test_stock_gen_moments():
+    """The drawn series have the distributions the generator states: daily log returns with
+    mean mu - sigma^2 / 2 and std sigma (BASELINE configs[0]: GBM mu = 2e-4, sigma = 0.02 per
+    day), the high / low excursions (0.5 sigma) |Z| with E|Z| = sqrt(2 / pi), log volumes with
+    mean ln 1e6 and std 0.5; initial prices uniform on [50, 150)."""
+    D, K, mu, sigma = 3000, 32, 2e-4, 0.02
+    x = osm.generate_np(D, K, seed=77, mu=mu, sigma=sigma).astype(np.float64)
+    o, h, lo, c, v = (x[:, j] for j in range(5))
+    r = np.log(c[1:] / c[:-1]).ravel()
+    n = r.size
+    assert abs(r.mean() - (mu - 0.5 * sigma * sigma)) < 4 * sigma / math.sqrt(n)
+    assert abs(r.std(ddof=1) / sigma - 1) < 0.03
+    zh = (h / np.maximum(o, c) - 1) / (0.5 * sigma)
+    zl = (1 - lo / np.minimum(o, c)) / (0.5 * sigma)
+    for zz in (zh, zl):
+        assert abs(zz.mean() / math.sqrt(2 / math.pi) - 1) < 0.03
+    lv = np.log(v)
+    assert abs(lv.mean() - math.log(1e6)) < 4 * 0.5 / math.sqrt(lv.size)
+    assert abs(lv.std() / 0.5 - 1) < 0.03
+    s0 = osm.generate_np(1, 4096, seed=3)[0, osm.OPEN].astype(np.float64)
+    assert s0.min() >= 50.0 * (1 - 1e-6) and s0.max() < 150.0 * (1 + 1e-6)
+    assert abs(s0.mean() - 100.0) < 4 * 100 / math.sqrt(12 * 4096)
+
+
+def test_stock_gen_seeded():
+    a = osm.generate(5, 3, seed=1)
+    assert np.array_equal(a, osm.generate(5, 3, seed=1))
+    assert not np.array_equal(a, osm.generate(5, 3, seed=2))
