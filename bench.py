@@ -619,6 +619,9 @@ def market_prep(fin, torch):
 
     ms = ev(lambda: fin.fin_market_prepare(xd, market.WARMUP_DAYS, ind, mk, raw, magnitude=0.01, seed=7))
     res["stock_prepare_c1"] = {"assets": K, "days": D, "indicators": 8, "ms": ms}
+    og = torch.zeros((D, 5, K), dtype=torch.float32, device="cuda")
+    ms = ev(lambda: fin.fin_stock_market(D, K, 21, og))
+    res["stock_generate_c1"] = {"assets": K, "days": D, "ms": ms, "note": "GBM close + OHLV (R-SGEN)"}
     steps = 480000
     rows = torch.zeros((steps + 1, 144), dtype=torch.float32, device="cuda")
     ms = ev(lambda: fin.fin_crypto_market(steps, 43, rows))

@@ -313,6 +313,18 @@ int fin_market_prepare(const float* ohlcv, int32_t D, int32_t K, int32_t warmup,
  * (8 (steps + 1) bytes + chunk carries) and frees it on the stream. */
 int fin_crypto_market(int64_t steps, uint64_t seed, double sigma, double m0, double phi, float* rows, void* stream);
 
+/* Stock OHLCV generation on the device (the synthetic stand-in for the
+ * paper's daily bars, with BASELINE configs[0]'s GBM; reading R-SGEN, formulas in
+ * oracle/stock_market.py): writes ``ohlcv`` (device, f32 [days][5][K]: open, high, low,
+ * close, volume -- the input of fin_market_prepare) for a GBM close per asset, S0 ~
+ * U(s0_lo, s0_hi), drift mu and volatility sigma per day, open = previous close, high / low =
+ * max / min(open, close) (1 +- (0.5 sigma)|Z|), volume LogNormal(ln 1e6, 0.5); random numbers
+ * from Philox4x32-10 keyed by ``seed`` (streams 11..15).  Float64 arithmetic, one f32 rounding
+ * per value.  Needs days >= 1, 1 <= K <= 4096, sigma >= 0, 0 < s0_lo < s0_hi.  Allocates
+ * stream-ordered scratch (16 (days + 1) K bytes) and frees it on the stream. */
+int fin_stock_market(int32_t days, int32_t K, uint64_t seed, double mu, double sigma, double s0_lo, double s0_hi,
+                     float* ohlcv, void* stream);
+
 /* Generalised advantage estimation over a rollout's trajectory (
  * SPEC S:392-395; reading R-GAE, formulas in oracle/learn.py): from reward f32 [T][N],
  * value f32 [T+1][N] (row T = the bootstrap value of the last state) and done u8 [T][N]

@@ -23,6 +23,8 @@ cudaError_t launch_stock_rollout(int net, const tc::TcParams& p, int n_envs, int
 int stock_seg_grid(int net, const tc::TcParams& p, int n_envs);
 cudaError_t launch_crypto_market(int64_t steps, uint64_t seed, double sigma, double m0, double phi, float* rows,
                                  cudaStream_t s);
+cudaError_t launch_stock_market(int D, int K, uint64_t seed, double mu, double sigma, double s0_lo, double s0_hi,
+                                float* ohlcv, cudaStream_t s);
 cudaError_t launch_gae(const float* rew, const float* val, const uint8_t* done, int T, int N, double gamma,
                        double lam, int normalise, float* adv, float* ret, cudaStream_t s);
 cudaError_t launch_kl_diversity(const float* out, int M, int B, int K, int kind, double sigma, double* D,
@@ -933,6 +935,20 @@ int fin_crypto_market(int64_t steps, uint64_t seed, double sigma, double m0, dou
   if (!(phi >= 0.0 && phi < 1.0)) return fail(FIN_E_CONFIG, "phi must be in [0, 1)");
   cudaError_t e = fin::launch_crypto_market(steps, seed, sigma, m0, phi, rows, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fin_crypto_market launch");
+  return FIN_OK;
+}
+
+int fin_stock_market(int32_t days, int32_t K, uint64_t seed, double mu, double sigma, double s0_lo, double s0_hi,
+                     float* ohlcv, void* stream) {
+  if (!ohlcv) return fail(FIN_E_CONFIG, "fin_stock_market: null ohlcv");
+  if (days < 1 || days > (1 << 24)) return fail(FIN_E_CONFIG, "days must be in [1, 2^24]");
+  if (K < 1 || K > 4096) return fail(FIN_E_CONFIG, "K must be in [1, 4096]");
+  if (!std::isfinite(mu)) return fail(FIN_E_CONFIG, "mu must be finite");
+  if (!(sigma >= 0.0) || !std::isfinite(sigma)) return fail(FIN_E_CONFIG, "sigma must be finite and >= 0");
+  if (!(s0_lo > 0.0 && s0_lo < s0_hi) || !std::isfinite(s0_hi))
+    return fail(FIN_E_CONFIG, "need 0 < s0_lo < s0_hi < inf");
+  cudaError_t e = fin::launch_stock_market(days, K, seed, mu, sigma, s0_lo, s0_hi, ohlcv, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_stock_market launch");
   return FIN_OK;
 }
 

@@ -14,6 +14,16 @@
 // serially over the chunks (one thread per stream), pass C re-runs each chunk from its
 // true carry-in and writes the rows.  The book columns of a step depend only on its mid:
 // one thread per step.  Float64 throughout, one f32 rounding per stored value.
+//
+// Stock OHLCV generation (fin_stock_market, reading R-SGEN, oracle/stock_market.py): the
+// synthetic stand-in for the paper's daily bars with BASELINE configs[0]'s GBM
+// (S0 ~ U(lo, hi), mu, sigma per day) and OHLV around the close, as the [D][5][K] f32
+// tensor fin_market_prepare takes.  Streams 11..15 of the same counter scheme (d, s, k / 4):
+//   l_{-1} = ln(lo + (hi - lo) U(0, 11, k));  l_d = l_{d-1} + ((mu - (0.5 sigma) sigma) + sigma N(d, 12, k))
+//   open = exp(l_{d-1}), close = exp(l_d), high = max (1 + (0.5 sigma)|N(d, 13, k)|),
+//   low = min (1 - (0.5 sigma)|N(d, 14, k)|), volume = exp(ln 1e6 + 0.5 N(d, 15, k)).
+// Pass 1 draws the increments (one thread per day and block of 4 assets), pass 2 runs the
+// running sum left to right (one thread per asset), pass 3 writes the bars.
 #include "fin_internal.cuh"
 #include "philox.cuh"
 
@@ -182,9 +192,88 @@ __global__ void k_book(GenParams g, const double* __restrict__ mid, float* __res
   r[143] = 0.f;
 }
 
+// ---- stock OHLCV (R-SGEN)
+enum { kSInit = 11, kSClose = 12, kSHigh = 13, kSLow = 14, kSVol = 15 };
+struct SGen {
+  int D, K;
+  uint64_t seed;
+  double drift, sigma, hs, lo, span, lv0;
+};
+__global__ void k_sgen_inc(SGen g, double* __restrict__ inc /*[D][K]*/) {
+  const int nb = (g.K + 3) >> 2;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.D * nb) return;
+  const int d = i / nb, b = i % nb;
+  double z[4];
+  normals4_f64(draw(g.seed, d, kSClose, (uint32_t)b), z);
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (4 * b + j < g.K) inc[(size_t)d * g.K + 4 * b + j] = fadd64(g.drift, fmul64(g.sigma, z[j]));
+}
+__global__ void k_sgen_scan(SGen g, const double* __restrict__ inc, double* __restrict__ lp /*[D + 1][K]*/) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= g.K) return;
+  const Words w = draw(g.seed, 0, kSInit, (uint32_t)(k >> 2));
+  double l = log(fadd64(g.lo, fmul64(g.span, u01_f64(w.w[k & 3]))));
+  lp[k] = l;
+  for (int d = 0; d < g.D; ++d) {   // left to right, as the definition
+    l = fadd64(l, inc[(size_t)d * g.K + k]);
+    lp[(size_t)(d + 1) * g.K + k] = l;
+  }
+}
+__global__ void k_sgen_bars(SGen g, const double* __restrict__ lp, float* __restrict__ out /*[D][5][K]*/) {
+  const int nb = (g.K + 3) >> 2;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.D * nb) return;
+  const int d = i / nb, b = i % nb;
+  double zh[4], zl[4], zv[4];
+  normals4_f64(draw(g.seed, d, kSHigh, (uint32_t)b), zh);
+  normals4_f64(draw(g.seed, d, kSLow, (uint32_t)b), zl);
+  normals4_f64(draw(g.seed, d, kSVol, (uint32_t)b), zv);
+  float* row = out + (size_t)d * 5 * g.K;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int k = 4 * b + j;
+    if (k >= g.K) break;
+    const double o = exp(lp[(size_t)d * g.K + k]), c = exp(lp[(size_t)(d + 1) * g.K + k]);
+    row[k] = (float)o;
+    row[g.K + k] = (float)fmul64(fmax(o, c), fadd64(1.0, fmul64(g.hs, fabs(zh[j]))));
+    row[2 * g.K + k] = (float)fmul64(fmin(o, c), fsub64(1.0, fmul64(g.hs, fabs(zl[j]))));
+    row[3 * g.K + k] = (float)c;
+    row[4 * g.K + k] = (float)exp(fadd64(g.lv0, fmul64(0.5, zv[j])));
+  }
+}
+
 }  // namespace
 
 namespace fin {
+
+cudaError_t launch_stock_market(int D, int K, uint64_t seed, double mu, double sigma, double s0_lo, double s0_hi,
+                                float* ohlcv, cudaStream_t s) {
+  SGen g;
+  g.D = D;
+  g.K = K;
+  g.seed = seed;
+  g.sigma = sigma;
+  g.drift = mu - (0.5 * sigma) * sigma;
+  g.hs = 0.5 * sigma;
+  g.lo = s0_lo;
+  g.span = s0_hi - s0_lo;
+  g.lv0 = log(1e6);
+  double *inc = nullptr, *lp = nullptr;
+  cudaError_t e = cudaMallocAsync(&inc, sizeof(double) * (size_t)D * K, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&lp, sizeof(double) * (size_t)(D + 1) * K, s);
+  if (e != cudaSuccess) return e;
+  const int n = D * ((K + 3) / 4);
+  k_sgen_inc<<<(n + 127) / 128, 128, 0, s>>>(g, inc);
+  k_sgen_scan<<<(K + 31) / 32, 32, 0, s>>>(g, inc, lp);
+  k_sgen_bars<<<(n + 127) / 128, 128, 0, s>>>(g, lp, ohlcv);
+  e = cudaGetLastError();
+  cudaFreeAsync(inc, s);
+  cudaFreeAsync(lp, s);
+  return e;
+}
+
 
 cudaError_t launch_crypto_market(int64_t steps, uint64_t seed, double sigma, double m0, double phi, float* rows,
                                  cudaStream_t s) {

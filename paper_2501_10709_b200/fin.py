@@ -51,7 +51,7 @@ EXPORTS = ("fin_env_create", "fin_env_reset", "fin_env_step", "fin_env_get_state
            "fin_env_check", "fin_env_destroy", "fin_policy_create", "fin_policy_destroy", "fin_rollout",
            "fin_rollout_actions", "fin_ensemble_act", "fin_episode_metrics", "fin_mlp_forward",
            "fin_philox_normals", "fin_member_weights", "fin_market_prepare", "fin_crypto_market", "fin_gae", "fin_kl_diversity", "fin_last_error", "fin_abi_version", "fin_device_check",
-           "fin_debug_trace", "fin_env_counters")
+           "fin_debug_trace", "fin_env_counters", "fin_stock_market")
 
 
 class FinError(RuntimeError):
@@ -108,6 +108,8 @@ _sig = {
     "fin_gae": ([_P, _P, _P, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_int32, _P, _P, _P], C.c_int),
     "fin_kl_diversity": ([_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, _P, _P], C.c_int),
     "fin_crypto_market": ([C.c_int64, C.c_uint64, C.c_double, C.c_double, C.c_double, _P, _P], C.c_int),
+    "fin_stock_market": ([C.c_int32, C.c_int32, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_double, _P, _P],
+                         C.c_int),
     "fin_market_prepare": ([_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_double,
                             C.c_uint64, _P, _P, _P], C.c_int),
     "fin_last_error": ([], C.c_char_p),
@@ -477,6 +479,16 @@ def fin_crypto_market(steps: int, seed: int, rows, sigma: float = 1e-4, m0: floa
         raise ValueError("rows must be [steps + 1][144]")
     _check(_lib.fin_crypto_market(int(steps), int(seed), float(sigma), float(m0), float(phi),
                                   _ptr(rows, torch.float32, "rows"), _stream(stream)), "fin_crypto_market")
+
+
+def fin_stock_market(days: int, K: int, seed: int, ohlcv, mu: float = 2e-4, sigma: float = 0.02,
+                     s0_lo: float = 50.0, s0_hi: float = 150.0, stream=None) -> None:
+    """Generate the stock OHLCV tensor ohlcv f32 [days][5][K] (device) on the GPU."""
+    import torch
+    if tuple(ohlcv.shape) != (days, 5, K):
+        raise ValueError("ohlcv must be [days][5][K]")
+    _check(_lib.fin_stock_market(int(days), int(K), int(seed), float(mu), float(sigma), float(s0_lo), float(s0_hi),
+                                 _ptr(ohlcv, torch.float32, "ohlcv"), _stream(stream)), "fin_stock_market")
 
 
 def fin_gae(reward, value, done, adv, ret, gamma: float = 0.99, lam: float = 0.95, normalise: bool = False,

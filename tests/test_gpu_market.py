@@ -113,3 +113,67 @@ def test_crypto_market_rejects_bad_arguments():
     rows = zeros((11, 144), torch.float32)
     with pytest.raises(Exception):
         fin.fin_crypto_market(10, 1, rows, phi=1.0)
+
+
+# ---------------------------------------------------------------- stock OHLCV generation (R-SGEN)
+def _within_ulps(g, o, n):
+    g64, o64 = g.astype(np.float64), o.astype(np.float64)
+    return np.all(np.abs(g64 - o64) <= n * np.spacing(np.abs(o).astype(np.float32)).astype(np.float64))
+
+
+@pytest.mark.parametrize("D,K,seed,mu,sigma", [(120, 7, 3, 2e-4, 0.02), (50, 30, 11, 1e-3, 0.05), (9, 1, 2, 0.0, 0.0)])
+def test_stock_market_matches_oracle_loops(D, K, seed, mu, sigma):
+    """fin_stock_market against oracle/stock_market.generate (plain loops): every value within
+    2 float32 ulps (float64 on both sides, device exp / log / sincos vs libm, one f32 rounding);
+    the open of day d equals the close of day d - 1 bit for bit; bar invariants hold."""
+    import torch
+    from oracle import stock_market as osm
+    from paper_2501_10709_b200 import fin
+    x = zeros((D, 5, K), torch.float32)
+    fin.fin_stock_market(D, K, seed, x, mu=mu, sigma=sigma)
+    g = host(x)
+    o = osm.generate(D, K, seed, mu=mu, sigma=sigma)
+    assert _within_ulps(g, o, 2)
+    assert np.array_equal(g[1:, osm.OPEN], g[:-1, osm.CLOSE])
+    assert np.all(g[:, osm.LOW] <= np.minimum(g[:, osm.OPEN], g[:, osm.CLOSE]))
+    assert np.all(np.maximum(g[:, osm.OPEN], g[:, osm.CLOSE]) <= g[:, osm.HIGH])
+
+
+def test_stock_market_c1_size_and_chain():
+    """The C1 shape (64 warm-up + 1008 stored days, 30 assets) against the oracle's
+    element-wise path (all values within 2 f32 ulps), then the whole device pipeline:
+    fin_stock_market -> fin_market_prepare -> fin_env_create -> a short fused rollout,
+    the prepared tensor bit-identical to oracle/market.py on the GPU's own OHLCV (3 assets)."""
+    import torch
+    from oracle import stock_market as osm
+    from paper_2501_10709_b200 import fin
+    from synth import policy as spol
+    D, K = sm.WARMUP_DAYS + 1008, 30
+    x = zeros((D, 5, K), torch.float32)
+    fin.fin_stock_market(D, K, 21, x)
+    g = host(x)
+    assert _within_ulps(g, osm.generate_np(D, K, 21), 2)
+    ind = list(om.INDICATORS)
+    mk = zeros((1008, 2 + len(ind), K), torch.float32)
+    raw = zeros((len(ind), K, 1008), torch.float64)
+    fin.fin_market_prepare(x, sm.WARMUP_DAYS, ind, mk, raw)
+    o_mk, _ = om.prepare_stock_market(g[:, :, :3], sm.WARMUP_DAYS, ind)   # assets are independent: 3 of 30
+    assert np.array_equal(host(mk)[:, :, :3], o_mk)
+    cfg = fin.env_config(num_envs=300, num_assets=30, num_indicators=8, num_rows=1008, episode_len=30,
+                         num_windows=195)
+    env = fin.fin_env_create(cfg, host(mk))
+    pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, spol.kaiming_bf16(spol.STOCK_DIMS, 0))
+    rew = zeros((40, 300), torch.float32)
+    fin.fin_rollout(env, [pol], 40, fin.make_noise(fin.FIN_NOISE_PHILOX, 1), fin.make_traj(reward=rew))
+    assert fin.fin_env_check(env) == 0 and np.isfinite(host(rew)).all()
+
+
+def test_stock_market_rejects_bad_arguments():
+    import torch
+    from paper_2501_10709_b200 import fin
+    x = zeros((10, 5, 4), torch.float32)
+    for kw in (dict(sigma=-1.0), dict(s0_lo=0.0), dict(s0_lo=5.0, s0_hi=5.0), dict(mu=float("nan"))):
+        with pytest.raises(fin.FinError):
+            fin.fin_stock_market(10, 4, 1, x, **kw)
+    with pytest.raises(ValueError):
+        fin.fin_stock_market(10, 5, 1, x)
