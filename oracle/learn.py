@@ -1,7 +1,9 @@
 """Consumer-side oracle pieces (test infrastructure only).
 
 The learner consumes the rollout's T x N x D tensors.
-Two of its steps act on those tensors directly, with no backward pass:
+Two of its steps act on those tensors directly, with no backward pass (the policy-gradient
+step of Eq. 3-4 with the PPO surrogate, its backward pass through the MLP and Adam follow
+further down):
 
 * Generalised advantage estimation (the paper names PPO, whose
   standard estimator this is -- reading R-GAE):
@@ -22,6 +24,7 @@ Plain float64 loops in the order written.
 from __future__ import annotations
 
 import math
+import numpy as np
 
 
 def gae(rewards, values, dones, gamma: float, lam: float):
@@ -112,3 +115,117 @@ def kl_diversity(outputs, sigma: float, categorical: bool = False):
                       else kl_gaussian(outputs[j][b], outputs[i][b], sigma))
             D[i][j] = s / B
     return D
+
+
+# ---------------------------------------------------------------- the policy-gradient step
+# PAPER.md Eq. 3-4: grad J = E[sum_t R grad log pi(a_t | s_t)], estimated by Monte
+# Carlo over the N trajectories of the rollout.  The PPO member replaces R by advantages
+# and the likelihood-ratio term by the clipped surrogate (reading R-PPO):
+#   log pi(a | s) = sum_k -(a_k - mu_k)^2 / (2 sigma^2) - K ln(sigma sqrt(2 pi)),  mu = tanh(z3(s))
+#                   (the Gaussian member of R17: fixed std sigma around the tanh mean, a the
+#                   pre-clip continuous action the rollout drew)
+#   rho = exp(log pi_new - log pi_old)
+#   L   = (1/B) sum_s min(rho_s A_s, clip(rho_s, 1 - eps, 1 + eps) A_s)        (maximised)
+#   dL/dtheta = (1/B) sum_s c_s grad log pi(a_s | s_s),  c_s = rho_s A_s when the unclipped term
+#               is the minimum (not (A > 0 and rho > 1 + eps), not (A < 0 and rho < 1 - eps)),
+#               else 0;  d log pi / d z3 = ((a - mu) / sigma^2) (1 - mu^2)
+# The loss the optimiser minimises is -L; its gradient flows back through the MLP of oracle.mlp
+# (ReLU hidden layers) with the hidden activations given (straight-through for the bf16 rounding
+# the rollout applies: the same activations the device forward produced).
+
+def ppo_head(z3, a, logp_old, adv, sigma: float = 0.1, eps: float = 0.2):
+    """Per sample s (rows of z3 / a [B][K], logp_old / adv [B]): returns
+    (logp_new [B], rho [B], coef [B], g3 [B][K] = d(-L)/dz3, L) in float64 with plain loops."""
+    B, K = len(z3), len(z3[0])
+    const = K * math.log(sigma * math.sqrt(2.0 * math.pi))
+    logp, rho, coef = [0.0] * B, [0.0] * B, [0.0] * B
+    g3 = [[0.0] * K for _ in range(B)]
+    L = 0.0
+    for s in range(B):
+        mu = [math.tanh(float(z3[s][k])) for k in range(K)]
+        q = 0.0
+        for k in range(K):
+            d = float(a[s][k]) - mu[k]
+            q += d * d
+        logp[s] = -q / (2.0 * sigma * sigma) - const
+        rho[s] = math.exp(logp[s] - float(logp_old[s]))
+        A = float(adv[s])
+        clipped = min(max(rho[s], 1.0 - eps), 1.0 + eps)
+        L += min(rho[s] * A, clipped * A)
+        active = not ((A > 0.0 and rho[s] > 1.0 + eps) or (A < 0.0 and rho[s] < 1.0 - eps))
+        coef[s] = rho[s] * A if active else 0.0
+        for k in range(K):
+            g3[s][k] = -coef[s] / B * ((float(a[s][k]) - mu[k]) / (sigma * sigma)) * (1.0 - mu[k] * mu[k])
+    return logp, rho, coef, g3, L / B
+
+
+def mlp_backward(layers64, x, hidden, g_out):
+    """Gradients of sum_s g_out[s] . z_out(s) for the 3-layer ReLU MLP of oracle.mlp, given the
+    input x [B][in], the hidden activations hidden [B][2][H] (the values each next layer consumed)
+    and g_out [B][out] = d loss / d z_out.  Returns [(dW_l [out][in], db_l [out]) for l = 1..3],
+    float64, plain loops over samples and units (small B only; ``mlp_backward_np`` is the
+    vectorised restatement pinned against it)."""
+    (w1, _), (w2, _), (w3, _) = layers64
+    H1, H2, O = w1.shape[0], w2.shape[0], w3.shape[0]
+    B = len(x)
+    dW = [np.zeros_like(w1), np.zeros_like(w2), np.zeros_like(w3)]
+    db = [np.zeros(H1), np.zeros(H2), np.zeros(O)]
+    for s in range(B):
+        h1 = [float(v) for v in hidden[s][0][:H1]]
+        h2 = [float(v) for v in hidden[s][1][:H2]]
+        g3 = [float(v) for v in g_out[s]]
+        g2 = [0.0] * H2
+        for j in range(H2):
+            if h2[j] > 0.0:
+                acc = 0.0
+                for o in range(O):
+                    acc += g3[o] * w3[o, j]
+                g2[j] = acc
+        g1 = [0.0] * H1
+        for i in range(H1):
+            if h1[i] > 0.0:
+                acc = 0.0
+                for j in range(H2):
+                    acc += g2[j] * w2[j, i]
+                g1[i] = acc
+        for o in range(O):
+            db[2][o] += g3[o]
+            for j in range(H2):
+                dW[2][o, j] += g3[o] * h2[j]
+        for j in range(H2):
+            db[1][j] += g2[j]
+            for i in range(H1):
+                dW[1][j, i] += g2[j] * h1[i]
+        xs = [float(v) for v in x[s]]
+        for i in range(H1):
+            db[0][i] += g1[i]
+            for c in range(w1.shape[1]):
+                dW[0][i, c] += g1[i] * xs[c]
+    return [(dW[l], db[l]) for l in range(3)]
+
+
+def mlp_backward_np(layers64, x, hidden, g_out):
+    """The same gradients with NumPy matrix products (library primitive ``@``)."""
+    (w1, _), (w2, _), (w3, _) = layers64
+    H1, H2 = w1.shape[0], w2.shape[0]
+    x = np.asarray(x, dtype=np.float64)
+    h1 = np.asarray(hidden, dtype=np.float64)[:, 0, :H1]
+    h2 = np.asarray(hidden, dtype=np.float64)[:, 1, :H2]
+    g3 = np.asarray(g_out, dtype=np.float64)
+    g2 = (g3 @ w3) * (h2 > 0)
+    g1 = (g2 @ w2) * (h1 > 0)
+    return [(g1.T @ x, g1.sum(0)), (g2.T @ h1, g2.sum(0)), (g3.T @ h2, g3.sum(0))]
+
+
+def adam(theta, m, v, g, step: int, lr: float = 3e-4, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8):
+    """One Adam step (Kingma & Ba) on flat float64 lists, ``step`` >= 1 the 1-based count:
+    m <- b1 m + (1 - b1) g; v <- b2 v + (1 - b2) g^2; theta <- theta - lr mhat / (sqrt(vhat) + eps)
+    with mhat = m / (1 - b1^step), vhat = v / (1 - b2^step).  Returns new (theta, m, v)."""
+    c1 = 1.0 - beta1 ** step
+    c2 = 1.0 - beta2 ** step
+    th, mm, vv = list(theta), list(m), list(v)
+    for i in range(len(th)):
+        mm[i] = beta1 * mm[i] + (1.0 - beta1) * g[i]
+        vv[i] = beta2 * vv[i] + (1.0 - beta2) * g[i] * g[i]
+        th[i] = th[i] - lr * (mm[i] / c1) / (math.sqrt(vv[i] / c2) + eps)
+    return th, mm, vv

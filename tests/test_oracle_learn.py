@@ -73,3 +73,104 @@ def test_kl_terms():
     assert np.all(np.array(learn.kl_diversity(same, 0.1)) == 0)
     G = np.array(learn.kl_diversity(out, 0.1))
     np.testing.assert_allclose(G, G.T, rtol=1e-12)            # equal-std Gaussians: symmetric
+
+
+# ---------------------------------------------------------------- PPO / policy-gradient step (R-PPO)
+def _tiny_net(rng, dims=(5, 6, 4, 3)):
+    return [(rng.normal(0, 0.7, (o, i)), rng.normal(0, 0.1, o)) for i, o in zip(dims[:-1], dims[1:])]
+
+
+def _forward64(layers, x):
+    """Unquantised float64 forward of the 3-layer ReLU MLP: (z3, hidden [B][2][H])."""
+    (w1, b1), (w2, b2), (w3, b3) = layers
+    h1 = np.maximum(x @ w1.T + b1, 0.0)
+    h2 = np.maximum(h1 @ w2.T + b2, 0.0)
+    H = max(h1.shape[1], h2.shape[1])
+    hid = np.zeros((x.shape[0], 2, H))
+    hid[:, 0, :h1.shape[1]] = h1
+    hid[:, 1, :h2.shape[1]] = h2
+    return h2 @ w3.T + b3, hid
+
+
+def _loss(layers, x, a, logp_old, adv):
+    z3, _ = _forward64(layers, x)
+    return -learn.ppo_head(z3.tolist(), a.tolist(), logp_old.tolist(), adv.tolist())[4]
+
+
+def test_ppo_head_spec_examples():
+    """rho = 1 everywhere -> the surrogate is the mean advantage; A > 0, rho = 2,
+    clip 0.2 -> the sample contributes 1.2 A; zero advantages -> zero gradient; and the Gaussian
+    log-density against its closed form at a = mu (the normalising constant only)."""
+    z3 = [[0.3, -0.2], [0.0, 0.5]]
+    mu = np.tanh(np.array(z3))
+    a = (mu + 0.01).tolist()
+    logp, _, _, _, _ = learn.ppo_head(z3, a, [0.0, 0.0], [0.0, 0.0])
+    adv = [1.5, -0.5]
+    _, rho, coef, g, L = learn.ppo_head(z3, a, logp, adv)
+    assert rho == [1.0, 1.0] and L == pytest.approx(np.mean(adv), rel=1e-15)
+    _, rho, _, _, L = learn.ppo_head(z3[:1], a[:1], [logp[0] - math.log(2.0)], [2.0])
+    assert rho[0] == pytest.approx(2.0, rel=1e-14) and L == pytest.approx(1.2 * 2.0, rel=1e-14)
+    _, _, coef, g, L = learn.ppo_head(z3, a, logp, [0.0, 0.0])
+    assert L == 0.0 and np.all(np.array(g) == 0.0)
+    lp, _, _, _, _ = learn.ppo_head([[0.2, 0.1, -0.3]], np.tanh([[0.2, 0.1, -0.3]]).tolist(), [0.0], [0.0])
+    assert lp[0] == pytest.approx(-3 * math.log(0.1 * math.sqrt(2 * math.pi)), rel=1e-14)
+
+
+def test_ppo_head_clipping_cases():
+    """The clipped branch has zero gradient exactly when it is the minimum."""
+    z3, a = [[0.1]], [[0.15]]
+    lp, _, _, _, _ = learn.ppo_head(z3, a, [0.0], [0.0])
+    for A, ratio, active in ((1.0, 1.5, False), (1.0, 0.5, True), (-1.0, 0.5, False), (-1.0, 1.5, True),
+                             (1.0, 1.1, True), (-1.0, 0.9, True)):
+        _, rho, coef, _, _ = learn.ppo_head(z3, a, [lp[0] - math.log(ratio)], [A])
+        assert (coef[0] != 0.0) == active, (A, ratio)
+        if active:
+            assert coef[0] == pytest.approx(ratio * A, rel=1e-13)
+
+
+def test_ppo_gradient_against_finite_differences():
+    """d(-L)/dtheta from ppo_head + mlp_backward against central finite differences of the
+    float64 loss, for every weight and bias of a small MLP, with a mix of clipped and unclipped
+    samples; the vectorised backward equals the loops."""
+    rng = np.random.default_rng(11)
+    layers = _tiny_net(rng)
+    B = 7
+    x = rng.normal(size=(B, 5))
+    z3, hid = _forward64(layers, x)
+    a = np.tanh(z3) + 0.1 * rng.normal(size=z3.shape)
+    logp_true, _, _, _, _ = learn.ppo_head(z3.tolist(), a.tolist(), [0.0] * B, [0.0] * B)
+    logp_old = np.array(logp_true) + rng.normal(0, 0.3, B)      # ratios spread across the clip range
+    adv = rng.normal(size=B)
+    _, rho, coef, g3, _ = learn.ppo_head(z3.tolist(), a.tolist(), logp_old.tolist(), adv.tolist())
+    assert any(c == 0.0 for c in coef) and any(c != 0.0 for c in coef)
+    grads = learn.mlp_backward(layers, x.tolist(), hid.tolist(), g3)
+    gnp = learn.mlp_backward_np(layers, x, hid, g3)
+    for (dw, db), (dw2, db2) in zip(grads, gnp):
+        np.testing.assert_allclose(dw, dw2, rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(db, db2, rtol=1e-12, atol=1e-14)
+    h = 1e-6
+    for li in range(3):
+        for which in (0, 1):
+            p = layers[li][which]
+            for idx in np.ndindex(p.shape):
+                old = p[idx]
+                p[idx] = old + h
+                lp = _loss(layers, x, a, logp_old, adv)
+                p[idx] = old - h
+                lm = _loss(layers, x, a, logp_old, adv)
+                p[idx] = old
+                fd = (lp - lm) / (2 * h)
+                an = grads[li][which][idx]
+                assert abs(fd - an) <= 1e-6 * max(1.0, abs(fd)), (li, which, idx, fd, an)
+
+
+def test_adam_first_steps_closed_form():
+    """Step 1: mhat = g, vhat = g^2, so theta moves by -lr g / (|g| + eps) (= -lr sign g for
+    |g| >> eps); a zero gradient leaves theta; step 2 with the same g moves by the same amount."""
+    g = [0.5, -2.0, 0.0, 1e-3]
+    th, m, v = learn.adam([1.0, 1.0, 1.0, 1.0], [0.0] * 4, [0.0] * 4, g, 1, lr=0.1)
+    for t, gi in zip(th, g):
+        assert t == pytest.approx(1.0 - 0.1 * gi / (abs(gi) + 1e-8), rel=1e-12, abs=1e-15)
+    th2, _, _ = learn.adam(th, m, v, g, 2, lr=0.1)
+    for t2, t, gi in zip(th2, th, g):
+        assert (t2 - t) == pytest.approx(-0.1 * gi / (abs(gi) + 1e-8), rel=1e-9, abs=1e-12)
