@@ -589,7 +589,61 @@ def consumer(fin, torch):
     b.record()
     torch.cuda.synchronize()
     res["kl_diversity_3x65536x30"] = {"ms": a.elapsed_time(b)}
+    res["ppo_step"] = ppo_step(fin, torch)
     return res
+
+
+def ppo_step(fin, torch, B=65536):
+    """The policy-gradient step (Eq. 3-4, PPO surrogate; NEXT-4) on a minibatch of B samples of
+    the C1 policy: the tcgen05 forward (fin_mlp_forward), fin_ppo_grad (float64 head, fp32 CUDA-core
+    contractions) and one Adam step over the 150,304 parameters.  FLOPs: forward 2 B (301 256 +
+    256 256 + 256 30), backward 2 B (30 256 + 256 256) for the propagated deltas and 2 B (30 256 +
+    256 256 + 256 301) for the weight gradients; the contractions' bound is the fp32 CUDA-core
+    peak 148 SMs x 128 lanes x 2 FLOP x 1.965 GHz = 74.4 TFLOP/s (alu)."""
+    import numpy as np
+    from synth import policy as spol
+    layers = spol.kaiming_bf16(spol.STOCK_DIMS, 0)
+    pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, layers)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.randn((B, 301), device="cuda", generator=g).to(torch.bfloat16).view(torch.int16)
+    z = torch.empty((B, 30), dtype=torch.float32, device="cuda")
+    hid = torch.empty((B, 2, 256), dtype=torch.int16, device="cuda")
+    a = torch.randn((B, 30), device="cuda", generator=g) * 0.1
+    logp_old = torch.zeros(B, device="cuda")
+    adv = torch.randn(B, device="cuda", generator=g)
+    ws = [torch.from_numpy((w.astype(np.uint32) << 16).view(np.float32)).cuda() for w, _ in layers]
+    grads = [(torch.empty_like(w), torch.empty(w.shape[0], device="cuda")) for w in ws]
+    stats = torch.empty(4, dtype=torch.float64, device="cuda")
+    n = sum(w.numel() + w.shape[0] for w in ws)
+    theta, m, v, gflat = (torch.zeros(n, device="cuda") for _ in range(4))
+
+    def step():
+        fin.fin_mlp_forward(pol, x, z, hid)
+        a.add_(0)   # (inputs stay resident)
+        fin.fin_ppo_grad(x, hid, z, a, logp_old, adv, ws[1], ws[2], grads, stats)
+        fin.fin_adam_step(theta, m, v, gflat, 1)
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        fin.fin_ppo_grad(x, hid, z, a, logp_old, adv, ws[1], ws[2], grads, stats)
+    e1.record()
+    torch.cuda.synchronize()
+    ms_grad = e0.elapsed_time(e1) / 5
+    e0.record()
+    for _ in range(5):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms_step = e0.elapsed_time(e1) / 5
+    flop_grad = 2 * B * (30 * 256 + 256 * 256) + 2 * B * (30 * 256 + 256 * 256 + 256 * 301)
+    return {"samples": B, "ms_forward_grad_adam": ms_step, "ms_grad": ms_grad,
+            "samples_per_s": B / (ms_step / 1e3), "grad_tflops": flop_grad / (ms_grad / 1e3) / 1e12,
+            "grad_frac_of_fp32_simt_peak": flop_grad / (ms_grad / 1e3) / 1e12 / 74.4,
+            "note": "fp32 CUDA-core contractions (first slice); the tensor-core backward is not built"}
 
 
 def market_prep(fin, torch):

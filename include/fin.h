@@ -325,6 +325,32 @@ int fin_crypto_market(int64_t steps, uint64_t seed, double sigma, double m0, dou
 int fin_stock_market(int32_t days, int32_t K, uint64_t seed, double mu, double sigma, double s0_lo, double s0_hi,
                      float* ohlcv, void* stream);
 
+/* The learner's policy-gradient step (Eq. 3-4, P:176-195 -- the
+ * Monte-Carlo gradient estimate grad J = (1/N) sum_i sum_t R grad log pi(a_t | s_t) -- in PPO's
+ * clipped-surrogate form; reading R-PPO, formulas in oracle/learn.py) for the
+ * Gaussian policy of a 3-layer ReLU MLP (mean tanh(z), fixed std ``sigma``).  Per sample s of
+ * the batch (device arrays): x bf16 bits [B][in_dim] the observation, hidden bf16 bits
+ * [B][2][max(h1, h2)] and z f32 [B][k_out] the hidden activations and outputs of the CURRENT
+ * weights (fin_mlp_forward), a f32 [B][k_out] the pre-clip continuous action the rollout drew,
+ * logp_old f32 [B] its log-density under the rollout's policy, adv f32 [B] its advantage (e.g.
+ * fin_gae, normalised).  Weights (device f32, the values the forward used, [out][in]): w2
+ * [h2][h1], w3 [k_out][h2].  Writes the gradients of the loss -L (L = the mean clipped surrogate,
+ * ratio clip 1 +- clip_eps) to dw1 [h1][in_dim], db1 [h1], dw2 [h2][h1], db2 [h2], dw3
+ * [k_out][h2], db3 [k_out] (device f32) and stats (device f64 [4]: L, mean ratio, clipped
+ * fraction, B).  float64 head, fp32 contractions, deterministic.  Allocates stream-ordered
+ * scratch (~4 B (k_out + h1 + h2) + split partials) and frees it on the stream. */
+int fin_ppo_grad(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t k_out, const uint16_t* x,
+                 const uint16_t* hidden, const float* z, const float* a, const float* logp_old, const float* adv,
+                 double sigma, double clip_eps, const float* w2, const float* w3, float* dw1, float* db1, float* dw2,
+                 float* db2, float* dw3, float* db3, double* stats, void* stream);
+
+/* One Adam step (Kingma & Ba) on n parameters (device f32 theta, m, v updated in place; grad the
+ * loss gradient): m = b1 m + (1 - b1) g, v = b2 v + (1 - b2) g^2, theta -= lr mhat / (sqrt(vhat) +
+ * eps), mhat / vhat bias-corrected with the 1-based ``step``.  Needs n >= 1, step >= 1, 0 <= b1, b2
+ * < 1, eps > 0, lr >= 0. */
+int fin_adam_step(int64_t n, float* theta, float* m, float* v, const float* grad, int32_t step, double lr,
+                  double beta1, double beta2, double eps, void* stream);
+
 /* Generalised advantage estimation over a rollout's trajectory (
  * SPEC S:392-395; reading R-GAE, formulas in oracle/learn.py): from reward f32 [T][N],
  * value f32 [T+1][N] (row T = the bootstrap value of the last state) and done u8 [T][N]

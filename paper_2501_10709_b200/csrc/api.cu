@@ -25,6 +25,12 @@ cudaError_t launch_crypto_market(int64_t steps, uint64_t seed, double sigma, dou
                                  cudaStream_t s);
 cudaError_t launch_stock_market(int D, int K, uint64_t seed, double mu, double sigma, double s0_lo, double s0_hi,
                                 float* ohlcv, cudaStream_t s);
+cudaError_t launch_ppo_grad(int B, int in, int H1, int H2, int K, const uint16_t* x, const uint16_t* hid,
+                            const float* z, const float* a, const float* logp_old, const float* adv, double sigma,
+                            double eps, const float* w2, const float* w3, float* dw1, float* db1, float* dw2,
+                            float* db2, float* dw3, float* db3, double* stats, cudaStream_t s);
+cudaError_t launch_adam(int64_t n, float* th, float* m, float* v, const float* g, int step, double lr, double b1,
+                        double b2, double eps, cudaStream_t s);
 cudaError_t launch_gae(const float* rew, const float* val, const uint8_t* done, int T, int N, double gamma,
                        double lam, int normalise, float* adv, float* ret, cudaStream_t s);
 cudaError_t launch_kl_diversity(const float* out, int M, int B, int K, int kind, double sigma, double* D,
@@ -949,6 +955,34 @@ int fin_stock_market(int32_t days, int32_t K, uint64_t seed, double mu, double s
     return fail(FIN_E_CONFIG, "need 0 < s0_lo < s0_hi < inf");
   cudaError_t e = fin::launch_stock_market(days, K, seed, mu, sigma, s0_lo, s0_hi, ohlcv, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fin_stock_market launch");
+  return FIN_OK;
+}
+
+int fin_ppo_grad(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t k_out, const uint16_t* x,
+                 const uint16_t* hidden, const float* z, const float* a, const float* logp_old, const float* adv,
+                 double sigma, double clip_eps, const float* w2, const float* w3, float* dw1, float* db1, float* dw2,
+                 float* db2, float* dw3, float* db3, double* stats, void* stream) {
+  if (!x || !hidden || !z || !a || !logp_old || !adv || !w2 || !w3 || !dw1 || !db1 || !dw2 || !db2 || !dw3 || !db3 ||
+      !stats)
+    return fail(FIN_E_CONFIG, "fin_ppo_grad: null argument");
+  if (B < 1 || in_dim < 1 || in_dim > 4096 || h1 < 1 || h1 > 1024 || h2 < 1 || h2 > 1024 || k_out < 1 || k_out > 64)
+    return fail(FIN_E_CONFIG, "fin_ppo_grad: bad sizes");
+  if (!(sigma > 0.0) || !std::isfinite(sigma) || !(clip_eps >= 0.0 && clip_eps < 1.0))
+    return fail(FIN_E_CONFIG, "fin_ppo_grad: need sigma > 0 and 0 <= clip_eps < 1");
+  cudaError_t e = fin::launch_ppo_grad(B, in_dim, h1, h2, k_out, x, hidden, z, a, logp_old, adv, sigma, clip_eps, w2, w3,
+                                       dw1, db1, dw2, db2, dw3, db3, stats, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_ppo_grad launch");
+  return FIN_OK;
+}
+
+int fin_adam_step(int64_t n, float* theta, float* m, float* v, const float* grad, int32_t step, double lr,
+                  double beta1, double beta2, double eps, void* stream) {
+  if (!theta || !m || !v || !grad) return fail(FIN_E_CONFIG, "fin_adam_step: null argument");
+  if (n < 1 || step < 1) return fail(FIN_E_CONFIG, "fin_adam_step: need n >= 1 and step >= 1");
+  if (!(beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 && beta2 < 1.0 && eps > 0.0 && lr >= 0.0))
+    return fail(FIN_E_CONFIG, "fin_adam_step: bad hyper-parameters");
+  cudaError_t e = fin::launch_adam(n, theta, m, v, grad, step, lr, beta1, beta2, eps, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_adam_step launch");
   return FIN_OK;
 }
 

@@ -1,0 +1,272 @@
+// ppo.cu -- the learner's policy-gradient step (Eq. 3-4, P:176-195;
+// PPO's clipped surrogate; reading R-PPO; oracle/learn.py states every formula):
+//   head:     per sample s, float64: mu = tanh(z3), log pi = -sum (a - mu)^2 / (2 sigma^2) - K ln(sigma
+//             sqrt(2 pi)), rho = exp(log pi - log pi_old), c = rho A unless the clipped term is the
+//             minimum (then 0), g3 = d(-L)/dz3 = -(c / B) ((a - mu) / sigma^2) (1 - mu^2)  -> f32
+//   backward: g2 = (g3 W3) * [h2 > 0],  g1 = (g2 W2) * [h1 > 0]   (rows = samples)
+//             dW3 = g3^T h2, dW2 = g2^T h1, dW1 = g1^T x, db_l = column sums of g_l
+//   Adam:     m, v, theta updates of the flat parameter vector (fin_adam_step)
+// The contractions run as fp32 CUDA-core GEMMs (64 x 64 tiles, 4 x 4 per thread, split-K over the
+// samples with partial sums reduced in a fixed order: deterministic); the hidden activations and
+// inputs are the bf16 values the device forward (fin_mlp_forward) produced and consumed.
+#include "fin_internal.cuh"
+
+namespace {
+
+constexpr int kTile = 64, kBK = 16, kThr = 256;
+
+__device__ __forceinline__ float bf16_at(const uint16_t* p, size_t i) {
+  return __uint_as_float((uint32_t)p[i] << 16);
+}
+
+// ---- head: one thread per sample; stats partials per block [4]: sum L, sum rho, clipped, n
+__global__ void k_ppo_head(int B, int K, const float* __restrict__ z, const float* __restrict__ a,
+                           const float* __restrict__ logp_old, const float* __restrict__ adv, double sigma,
+                           double eps, float* __restrict__ g3, double* __restrict__ part) {
+  __shared__ double red[4][kThr / 32];
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  double st[4] = {0.0, 0.0, 0.0, 0.0};
+  if (s < B) {
+    const double inv_s2 = 1.0 / (sigma * sigma);
+    const double cst = (double)K * log(sigma * sqrt(2.0 * 3.141592653589793));
+    double q = 0.0;
+    for (int k = 0; k < K; ++k) {
+      const double mu = tanh((double)z[(size_t)s * K + k]);
+      const double d = (double)a[(size_t)s * K + k] - mu;
+      q += d * d;
+    }
+    const double logp = -q * 0.5 * inv_s2 - cst;
+    const double rho = exp(logp - (double)logp_old[s]);
+    const double A = (double)adv[s];
+    const double clipped = fmin(fmax(rho, 1.0 - eps), 1.0 + eps);
+    const bool active = !((A > 0.0 && rho > 1.0 + eps) || (A < 0.0 && rho < 1.0 - eps));
+    const double c = active ? rho * A : 0.0;
+    const double scale = -c / (double)B * inv_s2;
+    for (int k = 0; k < K; ++k) {
+      const double mu = tanh((double)z[(size_t)s * K + k]);
+      g3[(size_t)s * K + k] = (float)(scale * ((double)a[(size_t)s * K + k] - mu) * (1.0 - mu * mu));
+    }
+    st[0] = fmin(rho * A, clipped * A);
+    st[1] = rho;
+    st[2] = active ? 0.0 : 1.0;
+    st[3] = 1.0;
+  }
+  for (int j = 0; j < 4; ++j) {
+    double v = st[j];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[j][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double v = 0.0;
+    for (int w = 0; w < kThr / 32; ++w) v += red[threadIdx.x][w];
+    part[(size_t)blockIdx.x * 4 + threadIdx.x] = v;
+  }
+}
+
+__global__ void k_stats_final(const double* __restrict__ part, int nb, double* __restrict__ stats) {
+  if (threadIdx.x < 4) {
+    double v = 0.0;
+    for (int b = 0; b < nb; ++b) v += part[(size_t)b * 4 + threadIdx.x];
+    stats[threadIdx.x] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {   // -> L (mean surrogate), mean rho, clipped fraction, B
+    const double n = stats[3];
+    stats[0] /= n;
+    stats[1] /= n;
+    stats[2] /= n;
+  }
+}
+
+// ---- g2 = (g3 W3) * [h2 > 0]: one thread per (sample, unit); K3 <= 32 terms
+__global__ void k_back_out(int B, int K, int H2, int Hs, const float* __restrict__ g3, const float* __restrict__ w3,
+                           const uint16_t* __restrict__ hid, float* __restrict__ g2) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (size_t)B * H2) return;
+  const int s = (int)(i / H2), j = (int)(i % H2);
+  float acc = 0.f;
+  if (bf16_at(hid, ((size_t)s * 2 + 1) * Hs + j) > 0.f)
+    for (int o = 0; o < K; ++o) acc = fmaf(g3[(size_t)s * K + o], w3[(size_t)o * H2 + j], acc);
+  g2[i] = acc;
+}
+
+// ---- generic fp32 GEMM: C[m][n] = sum_k A(m, k) B(k, n) over k in this split's range
+//   A(m, k) = AKM ? A[k * lda + m] : A[m * lda + k]           (f32)
+//   B(k, n) = BBF ? bf16 Bh[k * ldb + n] : Bf[k * ldb + n]
+//   out: part[split][M][N] (or C when splits == 1), optional mask (bf16 > 0) of C(m, n) at
+//   mask[m * ldm + n] applied when splits == 1
+template <bool AKM, bool BBF>
+__global__ void __launch_bounds__(kThr) k_gemm(int M, int N, int Ktot, int kchunk, const float* __restrict__ A,
+                                               int lda, const float* __restrict__ Bf, const uint16_t* __restrict__ Bh,
+                                               int ldb, float* __restrict__ out, const uint16_t* __restrict__ mask,
+                                               int ldm) {
+  __shared__ float As[kBK][kTile + 4];
+  __shared__ float Bs[kBK][kTile + 4];
+  const int m0 = blockIdx.y * kTile, n0 = blockIdx.x * kTile;
+  const int k0 = blockIdx.z * kchunk, k1 = min(Ktot, k0 + kchunk);
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  float acc[4][4] = {};
+  for (int kb = k0; kb < k1; kb += kBK) {
+    for (int e = threadIdx.x; e < kBK * kTile; e += kThr) {
+      const int kk = e / kTile, mm = e % kTile;   // consecutive threads: consecutive m (AKM) / n
+      const int k = kb + kk;
+      float av = 0.f, bv = 0.f;
+      if (AKM) {
+        if (k < k1 && m0 + mm < M) av = A[(size_t)k * lda + m0 + mm];
+        As[kk][mm] = av;
+      }
+      if (k < k1 && n0 + mm < N) bv = BBF ? bf16_at(Bh, (size_t)k * ldb + n0 + mm) : Bf[(size_t)k * ldb + n0 + mm];
+      Bs[kk][mm] = bv;
+    }
+    if (!AKM) {   // A row-major [M][lda]: consecutive threads read consecutive k of one row
+      for (int e = threadIdx.x; e < kBK * kTile; e += kThr) {
+        const int mm = e / kBK, kk = e % kBK;
+        const int k = kb + kk;
+        As[kk][mm] = (k < k1 && m0 + mm < M) ? A[(size_t)(m0 + mm) * lda + k] : 0.f;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kBK; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) av[r] = As[kk][ty * 4 + r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) bv[c] = Bs[kk][tx * 4 + c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(av[r], bv[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+  float* dst = out + (size_t)blockIdx.z * M * N;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int m = m0 + ty * 4 + r;
+    if (m >= M) continue;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int n = n0 + tx * 4 + c;
+      if (n >= N) continue;
+      float v = acc[r][c];
+      if (mask && !(bf16_at(mask, (size_t)m * ldm + n) > 0.f)) v = 0.f;
+      dst[(size_t)m * N + n] = v;
+    }
+  }
+}
+
+// fixed-order sum of the split partials: C[i] = sum_z part[z][i]
+__global__ void k_sum_splits(const float* __restrict__ part, int splits, size_t n, float* __restrict__ C) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float v = 0.f;
+  for (int z = 0; z < splits; ++z) v += part[(size_t)z * n + i];
+  C[i] = v;
+}
+
+// column sums of g [B][H] (bias gradients): one thread per column, fixed order over rows
+__global__ void k_colsum(int B, int H, const float* __restrict__ g, float* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= H) return;
+  float v = 0.f;
+  for (int s = 0; s < B; ++s) v += g[(size_t)s * H + j];
+  out[j] = v;
+}
+
+__global__ void k_adam(int64_t n, float* __restrict__ th, float* __restrict__ m, float* __restrict__ v,
+                       const float* __restrict__ g, float b1, float b2, float lr_c, float inv_c2, float eps) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float gi = g[i];
+  const float mi = fmaf(b1, m[i], (1.f - b1) * gi);
+  const float vi = fmaf(b2, v[i], (1.f - b2) * gi * gi);
+  m[i] = mi;
+  v[i] = vi;
+  th[i] -= lr_c * mi / (sqrtf(vi * inv_c2) + eps);
+}
+
+int splits_for(int M, int N, int K) {
+  const int tiles = ((M + kTile - 1) / kTile) * ((N + kTile - 1) / kTile);
+  int s = (2 * 148 + tiles - 1) / tiles;                  // ~2 waves of blocks
+  const int maxs = (K + 4 * kBK - 1) / (4 * kBK);          // >= 64 rows of K per split
+  if (s > maxs) s = maxs;
+  return s < 1 ? 1 : s;
+}
+
+// C[M][N] (= sum over K of A^T-ish products) with split-K and deterministic reduction
+template <bool AKM, bool BBF>
+cudaError_t gemm(int M, int N, int K, const float* A, int lda, const float* Bf, const uint16_t* Bh, int ldb, float* C,
+                 const uint16_t* mask, int ldm, float* scratch, cudaStream_t s) {
+  const int splits = mask ? 1 : splits_for(M, N, K);
+  const int kchunk = ((K + splits - 1) / splits + kBK - 1) / kBK * kBK;
+  const int used = (K + kchunk - 1) / kchunk;
+  dim3 grid((N + kTile - 1) / kTile, (M + kTile - 1) / kTile, used);
+  float* out = used == 1 ? C : scratch;
+  k_gemm<AKM, BBF><<<grid, kThr, 0, s>>>(M, N, K, kchunk, A, lda, Bf, Bh, ldb, out, mask, ldm);
+  if (used > 1) {
+    const size_t n = (size_t)M * N;
+    k_sum_splits<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(scratch, used, n, C);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+namespace fin {
+
+cudaError_t launch_ppo_grad(int B, int in, int H1, int H2, int K, const uint16_t* x, const uint16_t* hid,
+                            const float* z, const float* a, const float* logp_old, const float* adv, double sigma,
+                            double eps, const float* w2, const float* w3, float* dw1, float* db1, float* dw2,
+                            float* db2, float* dw3, float* db3, double* stats, cudaStream_t s) {
+  const int Hs = H1 > H2 ? H1 : H2;   // hidden log row width ([B][2][Hs], fin_mlp_forward)
+  const int nb = (B + kThr - 1) / kThr;
+  float *g3 = nullptr, *g2 = nullptr, *g1 = nullptr, *scr = nullptr;
+  double* part = nullptr;
+  auto part_n = [](int M, int N, int Kk) {   // split partials of one weight-gradient GEMM
+    const int sp = splits_for(M, N, Kk);
+    const int kc = ((Kk + sp - 1) / sp + kBK - 1) / kBK * kBK;
+    const int used = (Kk + kc - 1) / kc;
+    return used > 1 ? (size_t)used * M * N : (size_t)1;
+  };
+  size_t scr_n = part_n(K, H2, B);
+  if (part_n(H2, H1, B) > scr_n) scr_n = part_n(H2, H1, B);
+  if (part_n(H1, in, B) > scr_n) scr_n = part_n(H1, in, B);
+  cudaError_t e = cudaMallocAsync(&g3, sizeof(float) * (size_t)B * K, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&g2, sizeof(float) * (size_t)B * H2, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&g1, sizeof(float) * (size_t)B * H1, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&scr, sizeof(float) * scr_n, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&part, sizeof(double) * 4 * (size_t)nb, s);
+  if (e != cudaSuccess) return e;
+  k_ppo_head<<<nb, kThr, 0, s>>>(B, K, z, a, logp_old, adv, sigma, eps, g3, part);
+  k_stats_final<<<1, 32, 0, s>>>(part, nb, stats);
+  const size_t n2 = (size_t)B * H2;
+  k_back_out<<<(unsigned)((n2 + 255) / 256), 256, 0, s>>>(B, K, H2, Hs, g3, w3, hid, g2);
+  // g1 = (g2 W2) * [h1 > 0]: A = g2 [B][H2] row-major, B = W2 [H2][H1], mask = h1 (row stride 2 Hs)
+  e = gemm<false, false>(B, H1, H2, g2, H2, w2, nullptr, H1, g1, hid, 2 * Hs, scr, s);
+  // weight gradients: A = g_l [B][M] (k = sample: AKM), B = activations [B][N]
+  if (e == cudaSuccess) e = gemm<true, true>(K, H2, B, g3, K, nullptr, hid + Hs, 2 * Hs, dw3, nullptr, 0, scr, s);
+  if (e == cudaSuccess) e = gemm<true, true>(H2, H1, B, g2, H2, nullptr, hid, 2 * Hs, dw2, nullptr, 0, scr, s);
+  if (e == cudaSuccess) e = gemm<true, true>(H1, in, B, g1, H1, nullptr, x, in, dw1, nullptr, 0, scr, s);
+  k_colsum<<<(K + 127) / 128, 128, 0, s>>>(B, K, g3, db3);
+  k_colsum<<<(H2 + 127) / 128, 128, 0, s>>>(B, H2, g2, db2);
+  k_colsum<<<(H1 + 127) / 128, 128, 0, s>>>(B, H1, g1, db1);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  cudaFreeAsync(g3, s);
+  cudaFreeAsync(g2, s);
+  cudaFreeAsync(g1, s);
+  cudaFreeAsync(scr, s);
+  cudaFreeAsync(part, s);
+  return e;
+}
+
+cudaError_t launch_adam(int64_t n, float* th, float* m, float* v, const float* g, int step, double lr, double b1,
+                        double b2, double eps, cudaStream_t s) {
+  const double c1 = 1.0 - pow(b1, (double)step), c2 = 1.0 - pow(b2, (double)step);
+  k_adam<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, th, m, v, g, (float)b1, (float)b2, (float)(lr / c1),
+                                                     (float)(1.0 / c2), (float)eps);
+  return cudaGetLastError();
+}
+
+}  // namespace fin

@@ -51,7 +51,7 @@ EXPORTS = ("fin_env_create", "fin_env_reset", "fin_env_step", "fin_env_get_state
            "fin_env_check", "fin_env_destroy", "fin_policy_create", "fin_policy_destroy", "fin_rollout",
            "fin_rollout_actions", "fin_ensemble_act", "fin_episode_metrics", "fin_mlp_forward",
            "fin_philox_normals", "fin_member_weights", "fin_market_prepare", "fin_crypto_market", "fin_gae", "fin_kl_diversity", "fin_last_error", "fin_abi_version", "fin_device_check",
-           "fin_debug_trace", "fin_env_counters", "fin_stock_market")
+           "fin_debug_trace", "fin_env_counters", "fin_stock_market", "fin_ppo_grad", "fin_adam_step")
 
 
 class FinError(RuntimeError):
@@ -108,6 +108,9 @@ _sig = {
     "fin_gae": ([_P, _P, _P, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_int32, _P, _P, _P], C.c_int),
     "fin_kl_diversity": ([_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, _P, _P], C.c_int),
     "fin_crypto_market": ([C.c_int64, C.c_uint64, C.c_double, C.c_double, C.c_double, _P, _P], C.c_int),
+    "fin_ppo_grad": ([C.c_int32] * 5 + [_P] * 6 + [C.c_double, C.c_double] + [_P] * 10, C.c_int),
+    "fin_adam_step": ([C.c_int64, _P, _P, _P, _P, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double, _P],
+                      C.c_int),
     "fin_stock_market": ([C.c_int32, C.c_int32, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_double, _P, _P],
                          C.c_int),
     "fin_market_prepare": ([_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_double,
@@ -489,6 +492,45 @@ def fin_stock_market(days: int, K: int, seed: int, ohlcv, mu: float = 2e-4, sigm
         raise ValueError("ohlcv must be [days][5][K]")
     _check(_lib.fin_stock_market(int(days), int(K), int(seed), float(mu), float(sigma), float(s0_lo), float(s0_hi),
                                  _ptr(ohlcv, torch.float32, "ohlcv"), _stream(stream)), "fin_stock_market")
+
+
+def fin_ppo_grad(x_bf16_bits, hidden, z, a, logp_old, adv, w2, w3, grads, stats, sigma: float = 0.1,
+                 clip_eps: float = 0.2, stream=None) -> None:
+    """PPO policy-gradient step (include/fin.h): grads = [(dw1, db1), (dw2, db2), (dw3, db3)] f32
+    device tensors receive d(-L)/dtheta; stats f64 [4] (L, mean ratio, clipped fraction, B)."""
+    import torch
+    B, in_dim = int(x_bf16_bits.shape[0]), int(x_bf16_bits.shape[1])
+    k_out = int(z.shape[1])
+    h2, h1 = int(w2.shape[0]), int(w2.shape[1])
+    if tuple(w3.shape) != (k_out, h2) or tuple(a.shape) != (B, k_out) or int(hidden.shape[0]) != B:
+        raise ValueError("fin_ppo_grad: inconsistent shapes")
+    _need(hidden, B * 2 * max(h1, h2), "hidden [B][2][H]")
+    _need(logp_old, B, "logp_old [B]")
+    _need(adv, B, "adv [B]")
+    shapes = [((h1, in_dim), (h1,)), ((h2, h1), (h2,)), ((k_out, h2), (k_out,))]
+    for (dw, db), (sw, sb) in zip(grads, shapes):
+        if tuple(dw.shape) != sw or tuple(db.shape) != sb:
+            raise ValueError(f"fin_ppo_grad: gradient shapes must be {shapes}")
+    f32 = torch.float32
+    p = [_ptr(t, f32, "grad") for pair in grads for t in pair]
+    _check(_lib.fin_ppo_grad(B, in_dim, h1, h2, k_out, _ptr(x_bf16_bits, torch.int16, "x"),
+                             _ptr(hidden, torch.int16, "hidden"), _ptr(z, f32, "z"), _ptr(a, f32, "a"),
+                             _ptr(logp_old, f32, "logp_old"), _ptr(adv, f32, "adv"), float(sigma), float(clip_eps),
+                             _ptr(w2, f32, "w2"), _ptr(w3, f32, "w3"), *p, _ptr(stats, torch.float64, "stats"),
+                             _stream(stream)), "fin_ppo_grad")
+
+
+def fin_adam_step(theta, m, v, grad, step: int, lr: float = 3e-4, beta1: float = 0.9, beta2: float = 0.999,
+                  eps: float = 1e-8, stream=None) -> None:
+    """One Adam step on flat f32 device tensors (theta, m, v updated in place)."""
+    import torch
+    n = int(theta.numel())
+    for t, w in ((m, "m"), (v, "v"), (grad, "grad")):
+        _need(t, n, w)
+    f32 = torch.float32
+    _check(_lib.fin_adam_step(n, _ptr(theta, f32, "theta"), _ptr(m, f32, "m"), _ptr(v, f32, "v"),
+                              _ptr(grad, f32, "grad"), int(step), float(lr), float(beta1), float(beta2), float(eps),
+                              _stream(stream)), "fin_adam_step")
 
 
 def fin_gae(reward, value, done, adv, ret, gamma: float = 0.99, lam: float = 0.95, normalise: bool = False,
