@@ -619,7 +619,6 @@ def ppo_step(fin, torch, B=65536):
 
     def step():
         fin.fin_mlp_forward(pol, x, z, hid)
-        a.add_(0)   # (inputs stay resident)
         fin.fin_ppo_grad(x, hid, z, a, logp_old, adv, ws[1], ws[2], grads, stats)
         fin.fin_adam_step(theta, m, v, gflat, 1)
 
