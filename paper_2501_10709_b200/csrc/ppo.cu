@@ -166,12 +166,30 @@ __global__ void k_sum_splits(const float* __restrict__ part, int splits, size_t 
   C[i] = v;
 }
 
-// column sums of g [B][H] (bias gradients): one thread per column, fixed order over rows
-__global__ void k_colsum(int B, int H, const float* __restrict__ g, float* __restrict__ out) {
+// column sums of g [B][H] (bias gradients), deterministic: block (column group of 32, row chunk)
+// -> 8 row-strided partials per column reduced in a fixed order -> part[chunk][H]; then the chunks
+// summed in order
+constexpr int kColRows = 2048;
+__global__ void k_colsum_part(int B, int H, const float* __restrict__ g, float* __restrict__ part) {
+  __shared__ float red[8][33];
+  const int j = blockIdx.x * 32 + (threadIdx.x & 31), r = threadIdx.x >> 5;
+  const int s0 = blockIdx.y * kColRows, s1 = min(B, s0 + kColRows);
+  float v = 0.f;
+  if (j < H)
+    for (int s = s0 + r; s < s1; s += 8) v += g[(size_t)s * H + j];
+  red[r][threadIdx.x & 31] = v;
+  __syncthreads();
+  if (r == 0 && j < H) {
+    float t = 0.f;
+    for (int q = 0; q < 8; ++q) t += red[q][threadIdx.x & 31];
+    part[(size_t)blockIdx.y * H + j] = t;
+  }
+}
+__global__ void k_colsum_final(int chunks, int H, const float* __restrict__ part, float* __restrict__ out) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= H) return;
   float v = 0.f;
-  for (int s = 0; s < B; ++s) v += g[(size_t)s * H + j];
+  for (int c = 0; c < chunks; ++c) v += part[(size_t)c * H + j];
   out[j] = v;
 }
 
@@ -230,7 +248,8 @@ cudaError_t launch_ppo_grad(int B, int in, int H1, int H2, int K, const uint16_t
     const int used = (Kk + kc - 1) / kc;
     return used > 1 ? (size_t)used * M * N : (size_t)1;
   };
-  size_t scr_n = part_n(K, H2, B);
+  size_t scr_n = (size_t)((B + 2047) / 2048) * (H1 > H2 ? (H1 > K ? H1 : K) : (H2 > K ? H2 : K));   // bias partials
+  if (part_n(K, H2, B) > scr_n) scr_n = part_n(K, H2, B);
   if (part_n(H2, H1, B) > scr_n) scr_n = part_n(H2, H1, B);
   if (part_n(H1, in, B) > scr_n) scr_n = part_n(H1, in, B);
   cudaError_t e = cudaMallocAsync(&g3, sizeof(float) * (size_t)B * K, s);
@@ -249,9 +268,14 @@ cudaError_t launch_ppo_grad(int B, int in, int H1, int H2, int K, const uint16_t
   if (e == cudaSuccess) e = gemm<true, true>(K, H2, B, g3, K, nullptr, hid + Hs, 2 * Hs, dw3, nullptr, 0, scr, s);
   if (e == cudaSuccess) e = gemm<true, true>(H2, H1, B, g2, H2, nullptr, hid, 2 * Hs, dw2, nullptr, 0, scr, s);
   if (e == cudaSuccess) e = gemm<true, true>(H1, in, B, g1, H1, nullptr, x, in, dw1, nullptr, 0, scr, s);
-  k_colsum<<<(K + 127) / 128, 128, 0, s>>>(B, K, g3, db3);
-  k_colsum<<<(H2 + 127) / 128, 128, 0, s>>>(B, H2, g2, db2);
-  k_colsum<<<(H1 + 127) / 128, 128, 0, s>>>(B, H1, g1, db1);
+  const int chunks = (B + kColRows - 1) / kColRows;
+  const float* gs[3] = {g3, g2, g1};
+  float* bs[3] = {db3, db2, db1};
+  const int hs[3] = {K, H2, H1};
+  for (int l = 0; l < 3; ++l) {   // (scr is free again: the split partials were reduced above)
+    k_colsum_part<<<dim3((hs[l] + 31) / 32, chunks), 256, 0, s>>>(B, hs[l], gs[l], scr);
+    k_colsum_final<<<(hs[l] + 127) / 128, 128, 0, s>>>(chunks, hs[l], scr, bs[l]);
+  }
   if (e == cudaSuccess) e = cudaGetLastError();
   cudaFreeAsync(g3, s);
   cudaFreeAsync(g2, s);
