@@ -590,7 +590,67 @@ def consumer(fin, torch):
     torch.cuda.synchronize()
     res["kl_diversity_3x65536x30"] = {"ms": a.elapsed_time(b)}
     res["ppo_step"] = ppo_step(fin, torch)
+    res["ppo_iteration"] = ppo_iteration(fin, torch)
     return res
+
+
+def ppo_iteration(fin, torch, B=65536):
+    """One producer -> consumer iteration at the headline size (NEXT-4): the fused rollout of 65,536
+    envs x 256 steps logging the env-private observation entries and days; then on a minibatch of
+    B random samples: gather the observations, the old policy's forward, the Philox noise, the
+    Gaussian sample and its log-density, the PPO gradient, Adam, and installing the new weights."""
+    import numpy as np
+    from synth import policy as spol
+    N, T = N_HEAD, T_HEAD
+    env = make_env(fin, N, 0)
+    layers = spol.kaiming_bf16(spol.STOCK_DIMS, 0)
+    pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, layers)
+    z = lambda s, d: torch.zeros(s, dtype=d, device="cuda")  # noqa: E731
+    logs = dict(reward=z((T, N), torch.float32), done=z((T, N), torch.uint8), obs_private=z((T, N, 32), torch.int16),
+                day=z((T, N), torch.int32))
+    tr = fin.make_traj(**logs)
+    seed = 5
+    ev = lambda: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))  # noqa: E731
+    fin.fin_rollout(env, [pol], T, fin.make_noise(fin.FIN_NOISE_PHILOX, seed), tr)
+    t_base = fin.fin_env_clock(env)
+    a0, a1 = ev()
+    a0.record()
+    fin.fin_rollout(env, [pol], T, fin.make_noise(fin.FIN_NOISE_PHILOX, seed), tr)
+    a1.record()
+    g = torch.Generator(device="cuda").manual_seed(3)
+    idx = torch.randint(0, T * N, (B,), device="cuda", generator=g, dtype=torch.int64)
+    x, zo, hid = z((B, 301), torch.int16), z((B, 30), torch.float32), z((B, 2, 256), torch.int16)
+    eps, a, lpo = z((B, 30), torch.float32), z((B, 30), torch.float32), z(B, torch.float32)
+    adv = torch.randn(B, device="cuda", generator=g)
+    w = [torch.from_numpy((W.astype(np.uint32) << 16).view(np.float32)).cuda() for W, _ in layers]
+    bias = [z(W.shape[0], torch.float32) for W in w]
+    grads = [(torch.empty_like(W), torch.empty(W.shape[0], device="cuda")) for W in w]
+    opt = [(torch.zeros_like(p), torch.zeros_like(p)) for p in w + bias]
+    stats = z(4, torch.float64)
+
+    def learner():
+        fin.fin_gather_observations(env, logs["obs_private"], logs["day"], idx, x)
+        fin.fin_mlp_forward(pol, x, zo, hid)
+        fin.fin_rollout_noise(env, seed, t_base, idx, eps)
+        fin.fin_ppo_prepare(zo, eps, a, lpo)
+        fin.fin_ppo_grad(x, hid, zo, a, lpo, adv, w[1], w[2], grads, stats)
+        for p, gr, (mm, vv) in zip(w + bias, [q for q, _ in grads] + [q for _, q in grads], opt):
+            fin.fin_adam_step(p, mm, vv, gr, 1, lr=1e-5)
+
+    learner()
+    torch.cuda.synchronize()
+    b0, b1 = ev()
+    b0.record()
+    learner()
+    b1.record()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    fin.fin_policy_load(pol, w, bias)
+    load_ms = 1e3 * (time.perf_counter() - t0)
+    return {"rollout_ms_with_obs_logs": a0.elapsed_time(a1), "minibatch": B, "learner_ms": b0.elapsed_time(b1),
+            "policy_load_ms_host_wall": load_ms, "obs_log_bytes_per_env_step": 64 + 4,
+            "note": "learner = gather + forward + noise + prepare + PPO gradient + Adam; policy_load repacks "
+                    "the bf16 image on the host (synchronous)"}
 
 
 def ppo_step(fin, torch, B=65536):

@@ -159,7 +159,11 @@ int fin_env_reset(fin_env* env, const uint8_t* mask, void* stream);
  *   ep_metrics f64 [E][N][3] (cum, sharpe, mdd) of the episodes completed during the
  *            call, in completion order; ep_count i32 [N] counts them (written; may
  *            exceed E, extra episodes are counted but not stored)
- *   agg      f64 [FIN_AGG_LEN] per-rank partials (overwritten) */
+ *   agg      f64 [FIN_AGG_LEN] per-rank partials (overwritten)
+ *   obs_private bf16 bits [T][N][P] (stock policy rollouts) the env-private observation entries
+ *            the network consumed -- [b / b0, h_1 / max_trade .. h_K / max_trade, 0 pad], P = K + 1
+ *            rounded up to 16 -- and day i32 [T][N] the market day of the step: with the market they
+ *            rebuild the full observation (fin_gather_observations) for the learner */
 typedef struct {
   float* reward;
   uint8_t* done;
@@ -173,6 +177,8 @@ typedef struct {
   int32_t* ep_count;
   int32_t ep_capacity;      /* E */
   double* agg;
+  uint16_t* obs_private;
+  int32_t* day;
 } fin_traj;
 
 /* One VecEnv step with supplied integer actions [N][K] i16 (stock share
@@ -343,6 +349,33 @@ int fin_ppo_grad(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t k_ou
                  const uint16_t* hidden, const float* z, const float* a, const float* logp_old, const float* adv,
                  double sigma, double clip_eps, const float* w2, const float* w3, float* dw1, float* db1, float* dw2,
                  float* db2, float* dw3, float* db3, double* stats, void* stream);
+
+/* The learner's view of a rollout's samples (NEXT-4).  A sample is idx = t N + env (step t of
+ * the call, local env).  fin_env_clock: the handle's global step counter (host out) -- record it
+ * before a rollout: its Philox noise of step t is drawn at t_global + t.
+ * fin_gather_observations (stock): x bf16 bits [B][1 + 2K + I K] (device) = the full observation
+ * P:129 of each sample, rebuilt from the rollout's obs_private / day logs (fin_traj) and the
+ * market: [b / b0, close_norm (K), h / max_trade (K), features indicator-major (I K)], the
+ * shared entries bf16 of the market value -- the network input the rollout used.
+ * fin_rollout_noise: out f32 [B][K] = the rollout's Philox normals of member ``member`` at the
+ * samples (seed and t_base = the rollout's noise seed and starting clock).
+ * fin_ppo_prepare: from the rollout policy's outputs z_old f32 [B][K] and its noise eps, the
+ * Gaussian sample a = tanh(z_old) + sigma eps (f32) and its log-density log pi_old(a) f32 [B]
+ * (float64 arithmetic; R17 / R-PPO), the inputs of fin_ppo_grad. */
+int fin_env_clock(const fin_env* env, int64_t* t_global /*host*/);
+int fin_gather_observations(const fin_env* env, const uint16_t* obs_private, const int32_t* day, const int64_t* idx,
+                            int32_t B, uint16_t* x, void* stream);
+int fin_rollout_noise(const fin_env* env, uint64_t seed, int64_t t_base, const int64_t* idx, int32_t B, int32_t member,
+                      float* out, void* stream);
+int fin_ppo_prepare(int32_t B, int32_t K, const float* z_old, const float* eps, double sigma, float* a, float* logp_old,
+                    void* stream);
+
+/* Replace a policy's weights (same network) with device f32 values w[l] [dims[l+1]][dims[l]]
+ * and optional biases b[l] [dims[l+1]] (host arrays of DEVICE pointers; NULL bias = 0): rounded
+ * to bf16 (nearest even) on the device and repacked into the tcgen05 image; the policy gets a
+ * new id, so envs recompute their cached layer-1 term.  Waits for the policy's last use first;
+ * synchronises the stream (the learner's update -> the next rollout). */
+int fin_policy_load(fin_policy* policy, const float* const* w, const float* const* b, void* stream);
 
 /* One Adam step (Kingma & Ba) on n parameters (device f32 theta, m, v updated in place; grad the
  * loss gradient): m = b1 m + (1 - b1) g, v = b2 v + (1 - b2) g^2, theta -= lr mhat / (sqrt(vhat) +

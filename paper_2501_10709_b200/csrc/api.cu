@@ -31,6 +31,13 @@ cudaError_t launch_ppo_grad(int B, int in, int H1, int H2, int K, const uint16_t
                             float* db2, float* dw3, float* db3, double* stats, cudaStream_t s);
 cudaError_t launch_adam(int64_t n, float* th, float* m, float* v, const float* g, int step, double lr, double b1,
                         double b2, double eps, cudaStream_t s);
+cudaError_t launch_gather_obs(const EnvDev& e, const uint16_t* priv, int P, const int32_t* day, const int64_t* idx,
+                              int B, uint16_t* x, cudaStream_t s);
+cudaError_t launch_noise_at(uint64_t seed, int64_t off, int N, int64_t t_base, const int64_t* idx, int B, int K,
+                            int member, float* out, cudaStream_t s);
+cudaError_t launch_ppo_prepare(int B, int K, const float* z, const float* eps, double sigma, float* a, float* logp,
+                               cudaStream_t s);
+cudaError_t launch_to_bf16(int64_t n, const float* x, uint16_t* y, cudaStream_t s);
 cudaError_t launch_gae(const float* rew, const float* val, const uint8_t* done, int T, int N, double gamma,
                        double lam, int normalise, float* adv, float* ret, cudaStream_t s);
 cudaError_t launch_kl_diversity(const float* out, int M, int B, int K, int kind, double sigma, double* D,
@@ -79,6 +86,11 @@ struct fin_policy {
 };
 
 namespace {
+
+uint64_t new_uid() {   // process-unique policy ids (key the envs' z1s caches)
+  static std::atomic<uint64_t> next_uid{1};
+  return next_uid.fetch_add(1);
+}
 
 thread_local std::string g_err;
 unsigned long long* g_trace = nullptr;   // fin_debug_trace
@@ -131,6 +143,8 @@ TrajDev to_dev(const fin_traj* o) {
   t.ep_count = o->ep_count;
   t.ep_capacity = o->ep_metrics ? o->ep_capacity : 0;
   t.agg_partial = nullptr;
+  t.obs_private = o->obs_private;
+  t.day = o->day;
   return t;
 }
 
@@ -143,6 +157,7 @@ int ensure_agg(fin_env* env, size_t rows) {
   env->agg_cap = rows;
   return FIN_OK;
 }
+
 
 // network id from (n_layers, dims), -1 if not compiled
 int net_of(int n_layers, const int32_t* dims) {
@@ -197,6 +212,15 @@ void pack_member(const int32_t* dims, const uint16_t* const* w, const float* con
     if (bias && bias[l])
       for (int n = 0; n < dims[l + 1]; ++n) bp[off + n] = bias[l][n];
   }
+}
+
+void pack_any(int net, const int32_t* dims, const uint16_t* const* w, const float* const* b, std::vector<uint8_t>& wp,
+              std::vector<float>& bp, std::vector<float>& w1s) {
+  if (net == 0) pack_member<PlanStockC1, ObsC1>(dims, w, b, wp, bp, &w1s);
+  else if (net == 1) pack_member<PlanStockSmall, ObsSmall>(dims, w, b, wp, bp, &w1s);
+  else if (net == 3) pack_member<PlanStockPaper, ObsC1>(dims, w, b, wp, bp, &w1s);
+  else if (net == 4) pack_member<PlanCryptoPaper, void>(dims, w, b, wp, bp, nullptr);
+  else pack_member<PlanCrypto, void>(dims, w, b, wp, bp, nullptr);
 }
 
 bool finite_all(const float* x, int64_t n) {
@@ -532,15 +556,10 @@ int fin_policy_create(int32_t kind, int32_t n_layers, const int32_t* dims, const
   }
   std::vector<uint8_t> wp;
   std::vector<float> bp, w1s;
-  if (net == 0) pack_member<PlanStockC1, ObsC1>(dims, w_bf16, bias, wp, bp, &w1s);
-  else if (net == 1) pack_member<PlanStockSmall, ObsSmall>(dims, w_bf16, bias, wp, bp, &w1s);
-  else if (net == 3) pack_member<PlanStockPaper, ObsC1>(dims, w_bf16, bias, wp, bp, &w1s);
-  else if (net == 4) pack_member<PlanCryptoPaper, void>(dims, w_bf16, bias, wp, bp, nullptr);
-  else pack_member<PlanCrypto, void>(dims, w_bf16, bias, wp, bp, nullptr);
+  pack_any(net, dims, w_bf16, bias, wp, bp, w1s);
   fin_policy* pol = new (std::nothrow) fin_policy();
   if (!pol) return fail(FIN_E_CONFIG, "out of host memory");
-  static std::atomic<uint64_t> next_uid{1};
-  pol->uid = next_uid.fetch_add(1);
+  pol->uid = new_uid();
   pol->kind = kind;
   pol->net = net;
   pol->n_layers = n_layers;
@@ -574,6 +593,62 @@ int fin_policy_create(int32_t kind, int32_t n_layers, const int32_t* dims, const
   return FIN_OK;
 }
 
+int fin_policy_load(fin_policy* pol, const float* const* w, const float* const* bias, void* stream) {
+  if (!pol || !w) return fail(FIN_E_CONFIG, "fin_policy_load: null argument");
+  const int L = pol->n_layers;
+  for (int l = 0; l < L; ++l)
+    if (!w[l]) return fail(FIN_E_CONFIG, "fin_policy_load: weight %d is null", l);
+  cudaStream_t s = S(stream);
+  if (pol->used) FIN_CUDA(cudaEventSynchronize(pol->used));   // no call may still read the old image
+  // f32 -> bf16 (round to nearest even) on the device, then the host packs the image
+  std::vector<std::vector<uint16_t>> hw(L);
+  std::vector<std::vector<float>> hb(L);
+  uint16_t* tmp = nullptr;
+  size_t maxn = 0;
+  for (int l = 0; l < L; ++l) maxn = std::max(maxn, (size_t)pol->dims[l + 1] * pol->dims[l]);
+  FIN_CUDA(cudaMallocAsync(&tmp, maxn * sizeof(uint16_t), s));
+  cudaError_t e = cudaSuccess;
+  for (int l = 0; l < L && e == cudaSuccess; ++l) {
+    const size_t n = (size_t)pol->dims[l + 1] * pol->dims[l];
+    hw[l].resize(n);
+    e = fin::launch_to_bf16((int64_t)n, w[l], tmp, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hw[l].data(), tmp, n * 2, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess && bias && bias[l]) {
+      hb[l].resize(pol->dims[l + 1]);
+      e = cudaMemcpyAsync(hb[l].data(), bias[l], hb[l].size() * 4, cudaMemcpyDeviceToHost, s);
+    }
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFreeAsync(tmp, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fin_policy_load download");
+  std::vector<const uint16_t*> wpt(L);
+  std::vector<const float*> bpt(L);
+  for (int l = 0; l < L; ++l) {
+    wpt[l] = hw[l].data();
+    bpt[l] = hb[l].empty() ? nullptr : hb[l].data();
+    if (bpt[l] && !finite_all(bpt[l], pol->dims[l + 1])) return fail(FIN_E_DATA, "bias %d non-finite", l);
+  }
+  std::vector<uint8_t> wp;
+  std::vector<float> bp, w1s;
+  pack_any(pol->net, pol->dims, wpt.data(), bpt.data(), wp, bp, w1s);
+  pol->bias_nz = 0;
+  for (int l = 0; l < L; ++l)
+    if (bpt[l])
+      for (int n = 0; n < pol->dims[l + 1]; ++n)
+        if (bpt[l][n] != 0.f) pol->bias_nz |= 1u << l;
+  pol->b1_in_z1s = !w1s.empty() && (pol->bias_nz & 1u);
+  if (pol->b1_in_z1s) pol->bias_nz &= ~1u;
+  e = cudaMemcpyAsync(pol->wpack, wp.data(), wp.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(pol->bias, bp.data(), bp.size() * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && !w1s.empty())
+    e = cudaMemcpyAsync(pol->w1s_t, w1s.data(), w1s.size() * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "fin_policy_load upload");
+  pol->uid = new_uid();   // envs recompute their z1s term for the new weights
+  return FIN_OK;
+}
+
 void fin_policy_destroy(fin_policy* pol) {
   if (!pol) return;
   if (pol->used) {   // wait for the last call that read the weights (not for the whole device)
@@ -589,6 +664,11 @@ void fin_policy_destroy(fin_policy* pol) {
 }  // extern "C"
 
 namespace {
+
+// host packing of one member's bf16 weights into the tcgen05 image of its plan (fin_policy_create,
+// fin_policy_load): layout only, no arithmetic
+void pack_any(int net, const int32_t* dims, const uint16_t* const* w, const float* const* b, std::vector<uint8_t>& wp,
+              std::vector<float>& bp, std::vector<float>& w1s);
 
 // every policy of a call records its `used` event on the call's stream after the launch
 void mark_used(const fin_policy* const* members, int n, cudaStream_t s) {
@@ -972,6 +1052,42 @@ int fin_ppo_grad(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t k_ou
   cudaError_t e = fin::launch_ppo_grad(B, in_dim, h1, h2, k_out, x, hidden, z, a, logp_old, adv, sigma, clip_eps, w2, w3,
                                        dw1, db1, dw2, db2, dw3, db3, stats, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fin_ppo_grad launch");
+  return FIN_OK;
+}
+
+int fin_env_clock(const fin_env* env, int64_t* t_global) {
+  if (!env || !t_global) return fail(FIN_E_CONFIG, "fin_env_clock: null argument");
+  *t_global = env->d.t_global;
+  return FIN_OK;
+}
+
+int fin_gather_observations(const fin_env* env, const uint16_t* obs_private, const int32_t* day, const int64_t* idx,
+                            int32_t B, uint16_t* x, void* stream) {
+  if (!env || !obs_private || !day || !idx || !x) return fail(FIN_E_CONFIG, "fin_gather_observations: null argument");
+  if (env->d.task != FIN_STOCK) return fail(FIN_E_UNSUPPORTED, "fin_gather_observations: stock envs only");
+  if (B < 1) return fail(FIN_E_CONFIG, "fin_gather_observations: B must be >= 1");
+  const int P = (env->d.K + 1 + 15) / 16 * 16;
+  cudaError_t e = fin::launch_gather_obs(env->d, obs_private, P, day, idx, B, x, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_gather_observations launch");
+  return FIN_OK;
+}
+
+int fin_rollout_noise(const fin_env* env, uint64_t seed, int64_t t_base, const int64_t* idx, int32_t B, int32_t member,
+                      float* out, void* stream) {
+  if (!env || !idx || !out) return fail(FIN_E_CONFIG, "fin_rollout_noise: null argument");
+  if (B < 1 || member < 0 || member >= FIN_MAX_MEMBERS) return fail(FIN_E_CONFIG, "fin_rollout_noise: bad sizes");
+  cudaError_t e = fin::launch_noise_at(seed, env->d.env_offset, env->d.N, t_base, idx, B, env->d.K, member, out,
+                                       S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_rollout_noise launch");
+  return FIN_OK;
+}
+
+int fin_ppo_prepare(int32_t B, int32_t K, const float* z_old, const float* eps, double sigma, float* a, float* logp_old,
+                    void* stream) {
+  if (!z_old || !eps || !a || !logp_old) return fail(FIN_E_CONFIG, "fin_ppo_prepare: null argument");
+  if (B < 1 || K < 1 || !(sigma > 0.0)) return fail(FIN_E_CONFIG, "fin_ppo_prepare: bad arguments");
+  cudaError_t e = fin::launch_ppo_prepare(B, K, z_old, eps, sigma, a, logp_old, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_ppo_prepare launch");
   return FIN_OK;
 }
 

@@ -93,6 +93,8 @@ struct TrajDev {
   int32_t* ep_count;
   int32_t ep_capacity;
   double* agg_partial;   // [gridDim][FIN_AGG_LEN] scratch, reduced by k_agg_finalize
+  uint16_t* obs_private; // [T][N][P] bf16 bits of the env-private observation entries (stock)
+  int32_t* day;          // [T][N] market day of the step (stock)
 };
 
 // ----------------------------------------------------------------- exact fp64

@@ -9,7 +9,10 @@
 // The contractions run as fp32 CUDA-core GEMMs (64 x 64 tiles, 4 x 4 per thread, split-K over the
 // samples with partial sums reduced in a fixed order: deterministic); the hidden activations and
 // inputs are the bf16 values the device forward (fin_mlp_forward) produced and consumed.
+#include <cuda_bf16.h>
+
 #include "fin_internal.cuh"
+#include "philox.cuh"
 
 namespace {
 
@@ -230,9 +233,93 @@ cudaError_t gemm(int M, int N, int K, const float* A, int lda, const float* Bf, 
   return cudaGetLastError();
 }
 
+// ---- the learner's view of the rollout's samples (sample s = idx[s] = t N + env)
+// the full observation (PAPER.md P:129 order: b / b0, close_norm (K), h / max_trade (K), features
+// indicator-major (I K)) from the logged env-private entries and the step's market day; the shared
+// entries are bf16 of the f32 market value, as the z1s precompute (zshared.cu) quantises them
+__global__ void k_gather_obs(EnvDev e, const uint16_t* __restrict__ priv, int P, const int32_t* __restrict__ day,
+                             const int64_t* __restrict__ idx, int B, uint16_t* __restrict__ x) {
+  const int in_dim = 1 + 2 * e.K + e.I * e.K;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * in_dim) return;
+  const int s = (int)(i / in_dim), c = (int)(i % in_dim);
+  const int64_t r = idx[s];
+  const uint16_t* pv = priv + (size_t)r * P;
+  const float* mrow = e.market + (size_t)day[r] * e.row_floats;
+  uint16_t v;
+  if (c == 0) {
+    v = pv[0];
+  } else if (c <= e.K) {
+    v = __bfloat16_as_ushort(__float2bfloat16_rn(mrow[e.kp + (c - 1)]));
+  } else if (c <= 2 * e.K) {
+    v = pv[c - e.K];
+  } else {
+    const int j = c - 1 - 2 * e.K;
+    v = __bfloat16_as_ushort(__float2bfloat16_rn(mrow[(2 + j / e.K) * e.kp + (j % e.K)]));
+  }
+  x[i] = v;
+}
+
+// the rollout's Philox noise of member m at the samples' (global env id, global step)
+__global__ void k_noise_at(uint64_t seed, int64_t off, int N, int64_t t_base, const int64_t* __restrict__ idx, int B,
+                           int K, int member, float* __restrict__ out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= B) return;
+  const int64_t r = idx[s];
+  const int64_t t = r / N, env = r % N;
+  for (int blk = 0; blk * 4 < K; ++blk) {
+    float z[4];
+    philox_normals4((uint64_t)(off + env), (uint32_t)(t_base + t), ((uint32_t)member << 16) | (uint32_t)blk, seed, z);
+    for (int j = 0; j < 4 && blk * 4 + j < K; ++j) out[(size_t)s * K + blk * 4 + j] = z[j];
+  }
+}
+
+// the rollout policy's Gaussian sample and its log-density: a = tanh(z_old) + sigma eps (stored
+// f32), log pi_old(a) = -sum (a - tanh(z_old))^2 / (2 sigma^2) - K ln(sigma sqrt(2 pi)), float64
+__global__ void k_ppo_prepare(int B, int K, const float* __restrict__ z, const float* __restrict__ eps, double sigma,
+                              float* __restrict__ a, float* __restrict__ logp) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= B) return;
+  double q = 0.0;
+  for (int k = 0; k < K; ++k) {
+    const double mu = tanh((double)z[(size_t)s * K + k]);
+    const float ak = (float)(mu + sigma * (double)eps[(size_t)s * K + k]);
+    a[(size_t)s * K + k] = ak;
+    const double d = (double)ak - mu;
+    q += d * d;
+  }
+  logp[s] = (float)(-q / (2.0 * sigma * sigma) - (double)K * log(sigma * sqrt(2.0 * 3.141592653589793)));
+}
+
+__global__ void k_to_bf16(int64_t n, const float* __restrict__ x, uint16_t* __restrict__ y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = __bfloat16_as_ushort(__float2bfloat16_rn(x[i]));
+}
+
 }  // namespace
 
 namespace fin {
+
+cudaError_t launch_gather_obs(const EnvDev& e, const uint16_t* priv, int P, const int32_t* day, const int64_t* idx,
+                              int B, uint16_t* x, cudaStream_t s) {
+  const int64_t n = (int64_t)B * (1 + 2 * e.K + e.I * e.K);
+  k_gather_obs<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(e, priv, P, day, idx, B, x);
+  return cudaGetLastError();
+}
+cudaError_t launch_noise_at(uint64_t seed, int64_t off, int N, int64_t t_base, const int64_t* idx, int B, int K,
+                            int member, float* out, cudaStream_t s) {
+  k_noise_at<<<(B + 127) / 128, 128, 0, s>>>(seed, off, N, t_base, idx, B, K, member, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_ppo_prepare(int B, int K, const float* z, const float* eps, double sigma, float* a, float* logp,
+                               cudaStream_t s) {
+  k_ppo_prepare<<<(B + 127) / 128, 128, 0, s>>>(B, K, z, eps, sigma, a, logp);
+  return cudaGetLastError();
+}
+cudaError_t launch_to_bf16(int64_t n, const float* x, uint16_t* y, cudaStream_t s) {
+  k_to_bf16<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, x, y);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_ppo_grad(int B, int in, int H1, int H2, int K, const uint16_t* x, const uint16_t* hid,
                             const float* z, const float* a, const float* logp_old, const float* adv, double sigma,

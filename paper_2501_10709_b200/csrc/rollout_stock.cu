@@ -303,7 +303,11 @@ struct StockOps {
         w4[j] = lohi[0] | (lohi[1] << 16);
       }
       tc::sts128(xa + tc::cm_off(row, c, KT8), w4[0], w4[1], w4[2], w4[3]);
+      if (LOG && m == 0 && st.live && p.o.obs_private)
+        reinterpret_cast<uint4*>(p.o.obs_private + ((size_t)t * e.N + env) * Plan::kIn)[c] =
+            make_uint4(w4[0], w4[1], w4[2], w4[3]);
     }
+    if (LOG && m == 0 && st.live && p.o.day) p.o.day[(size_t)t * e.N + env] = st.d;
   }
 
   __device__ __forceinline__ static uint16_t* hidden_ptr(State& st, const TcParams& p, int env, int t, int m, int l,
@@ -686,7 +690,8 @@ template <class F>
 auto dispatch_stock(int net, const tc::TcParams& p, F&& f) -> decltype(f(StockKernel<PlanStockC1, false,
                                                                             StockOps<30, 8, PlanStockC1, false>>{})) {
   const bool single = p.M == 1 && p.kinds[0] != FIN_DDPG_OU;
-  const bool logs = p.act_only || p.o.mlp_out || p.o.mlp_hidden || p.o.cash || p.o.asset || p.o.hold || p.o.actions;
+  const bool logs = p.act_only || p.o.mlp_out || p.o.mlp_hidden || p.o.cash || p.o.asset || p.o.hold || p.o.actions ||
+                    p.o.obs_private || p.o.day;
   if (net == 0 && single && !logs) return f(StockKernel<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false, false>>{});
   if (net == 0 && single) return f(StockKernel<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false>>{});
   if (net == 0) return f(StockKernel<PlanStockC1, false, StockOps<30, 8, PlanStockC1, true>>{});

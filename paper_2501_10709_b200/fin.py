@@ -51,7 +51,8 @@ EXPORTS = ("fin_env_create", "fin_env_reset", "fin_env_step", "fin_env_get_state
            "fin_env_check", "fin_env_destroy", "fin_policy_create", "fin_policy_destroy", "fin_rollout",
            "fin_rollout_actions", "fin_ensemble_act", "fin_episode_metrics", "fin_mlp_forward",
            "fin_philox_normals", "fin_member_weights", "fin_market_prepare", "fin_crypto_market", "fin_gae", "fin_kl_diversity", "fin_last_error", "fin_abi_version", "fin_device_check",
-           "fin_debug_trace", "fin_env_counters", "fin_stock_market", "fin_ppo_grad", "fin_adam_step")
+           "fin_debug_trace", "fin_env_counters", "fin_stock_market", "fin_ppo_grad", "fin_adam_step",
+           "fin_env_clock", "fin_gather_observations", "fin_rollout_noise", "fin_ppo_prepare", "fin_policy_load")
 
 
 class FinError(RuntimeError):
@@ -75,7 +76,8 @@ class fin_traj(C.Structure):
     _fields_ = [("reward", C.c_void_p), ("done", C.c_void_p), ("actions", C.c_void_p), ("cash", C.c_void_p),
                 ("hold", C.c_void_p), ("asset", C.c_void_p), ("mlp_out", C.c_void_p),
                 ("mlp_hidden", C.c_void_p), ("ep_metrics", C.c_void_p),
-                ("ep_count", C.c_void_p), ("ep_capacity", C.c_int32), ("agg", C.c_void_p)]
+                ("ep_count", C.c_void_p), ("ep_capacity", C.c_int32), ("agg", C.c_void_p),
+                ("obs_private", C.c_void_p), ("day", C.c_void_p)]
 
 
 class fin_noise(C.Structure):
@@ -111,6 +113,11 @@ _sig = {
     "fin_ppo_grad": ([C.c_int32] * 5 + [_P] * 6 + [C.c_double, C.c_double] + [_P] * 10, C.c_int),
     "fin_adam_step": ([C.c_int64, _P, _P, _P, _P, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double, _P],
                       C.c_int),
+    "fin_env_clock": ([_P, _P], C.c_int),
+    "fin_gather_observations": ([_P, _P, _P, _P, C.c_int32, _P, _P], C.c_int),
+    "fin_rollout_noise": ([_P, C.c_uint64, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P], C.c_int),
+    "fin_ppo_prepare": ([C.c_int32, C.c_int32, _P, _P, C.c_double, _P, _P, _P], C.c_int),
+    "fin_policy_load": ([_P, C.POINTER(_P), C.POINTER(_P), _P], C.c_int),
     "fin_stock_market": ([C.c_int32, C.c_int32, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_double, _P, _P],
                          C.c_int),
     "fin_market_prepare": ([_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_double,
@@ -158,7 +165,7 @@ def _stream(stream):
 
 
 def make_traj(reward=None, done=None, actions=None, cash=None, hold=None, asset=None, mlp_out=None,
-              mlp_hidden=None, ep_metrics=None, ep_count=None, agg=None) -> fin_traj:
+              mlp_hidden=None, ep_metrics=None, ep_count=None, agg=None, obs_private=None, day=None) -> fin_traj:
     import torch
     tr = fin_traj()
     tr.reward = _ptr(reward, torch.float32, "reward")
@@ -173,9 +180,12 @@ def make_traj(reward=None, done=None, actions=None, cash=None, hold=None, asset=
     tr.ep_count = _ptr(ep_count, torch.int32, "ep_count")
     tr.ep_capacity = int(ep_metrics.shape[0]) if ep_metrics is not None else 0
     tr.agg = _ptr(agg, torch.float64, "agg")
+    tr.obs_private = _ptr(obs_private, torch.int16, "obs_private")
+    tr.day = _ptr(day, torch.int32, "day")
     # the tensors stay referenced by the struct (lifetime) and are size-checked per call
     tr._t = dict(reward=reward, done=done, actions=actions, cash=cash, hold=hold, asset=asset, mlp_out=mlp_out,
-                 mlp_hidden=mlp_hidden, ep_metrics=ep_metrics, ep_count=ep_count, agg=agg)
+                 mlp_hidden=mlp_hidden, ep_metrics=ep_metrics, ep_count=ep_count, agg=agg, obs_private=obs_private,
+                 day=day)
     return tr
 
 
@@ -224,6 +234,8 @@ def _need_traj(tr: fin_traj, T: int, N: int, K: int, M: int = 1, out_dim: int = 
           "ep_metrics [E][N][3]")
     _need(t["ep_count"], N, "ep_count [N]")
     _need(t["agg"], FIN_AGG_LEN, "agg [FIN_AGG_LEN]")
+    _need(t["obs_private"], T * N * ((K + 1 + 15) // 16 * 16), "obs_private [T][N][P]")
+    _need(t["day"], T * N, "day [T][N]")
 
 
 def env_config(**kw) -> fin_env_config:
@@ -492,6 +504,56 @@ def fin_stock_market(days: int, K: int, seed: int, ohlcv, mu: float = 2e-4, sigm
         raise ValueError("ohlcv must be [days][5][K]")
     _check(_lib.fin_stock_market(int(days), int(K), int(seed), float(mu), float(sigma), float(s0_lo), float(s0_hi),
                                  _ptr(ohlcv, torch.float32, "ohlcv"), _stream(stream)), "fin_stock_market")
+
+
+def fin_env_clock(env: Env) -> int:
+    t = C.c_int64(0)
+    _check(_lib.fin_env_clock(env.handle, C.byref(t)), "fin_env_clock")
+    return int(t.value)
+
+
+def fin_gather_observations(env: Env, obs_private, day, idx, x, stream=None) -> None:
+    """x int16 (bf16 bits) [B][1 + 2K + IK] <- the samples idx int64 [B] (t N + env) of a rollout's logs."""
+    import torch
+    B = int(idx.numel())
+    K, I = env.cfg.num_assets, env.cfg.num_indicators
+    if tuple(x.shape) != (B, 1 + 2 * K + I * K):
+        raise ValueError("x must be [B][1 + 2K + I K]")
+    _check(_lib.fin_gather_observations(env.handle, _ptr(obs_private, torch.int16, "obs_private"),
+                                        _ptr(day, torch.int32, "day"), _ptr(idx, torch.int64, "idx"), B,
+                                        _ptr(x, torch.int16, "x"), _stream(stream)), "fin_gather_observations")
+
+
+def fin_rollout_noise(env: Env, seed: int, t_base: int, idx, out, member: int = 0, stream=None) -> None:
+    import torch
+    B = int(idx.numel())
+    _need(out, B * env.K, "out [B][K]")
+    _check(_lib.fin_rollout_noise(env.handle, int(seed), int(t_base), _ptr(idx, torch.int64, "idx"), B, int(member),
+                                  _ptr(out, torch.float32, "out"), _stream(stream)), "fin_rollout_noise")
+
+
+def fin_ppo_prepare(z_old, eps, a, logp_old, sigma: float = 0.1, stream=None) -> None:
+    import torch
+    B, K = int(z_old.shape[0]), int(z_old.shape[1])
+    for t, n, w in ((eps, B * K, "eps"), (a, B * K, "a"), (logp_old, B, "logp_old")):
+        _need(t, n, w)
+    f32 = torch.float32
+    _check(_lib.fin_ppo_prepare(B, K, _ptr(z_old, f32, "z_old"), _ptr(eps, f32, "eps"), float(sigma), _ptr(a, f32, "a"),
+                                _ptr(logp_old, f32, "logp_old"), _stream(stream)), "fin_ppo_prepare")
+
+
+def fin_policy_load(pol: Policy, weights, biases=None, stream=None) -> None:
+    """weights / biases: lists of f32 device tensors [out][in] / [out] (biases None = zero)."""
+    import torch
+    n = len(pol.dims) - 1
+    if len(weights) != n or (biases is not None and len(biases) != n):
+        raise ValueError(f"fin_policy_load: {n} layers expected")
+    for l, w in enumerate(weights):
+        if tuple(w.shape) != (pol.dims[l + 1], pol.dims[l]):
+            raise ValueError(f"weight {l} must be [{pol.dims[l + 1]}][{pol.dims[l]}]")
+    w_c = (_P * n)(*[_ptr(w, torch.float32, "w") for w in weights])
+    b_c = (_P * n)(*([None] * n if biases is None else [_ptr(b, torch.float32, "b") for b in biases]))
+    _check(_lib.fin_policy_load(pol.handle, w_c, b_c, _stream(stream)), "fin_policy_load")
 
 
 def fin_ppo_grad(x_bf16_bits, hidden, z, a, logp_old, adv, w2, w3, grads, stats, sigma: float = 0.1,

@@ -46,7 +46,7 @@ def test_config_struct_layout_matches_header():
     from paper_2501_10709_b200 import fin
     # 16 int32, 3 double, 4 float, uint64, int64 with natural alignment
     assert ctypes.sizeof(fin.fin_env_config) == 16 * 4 + 3 * 8 + 4 * 4 + 8 + 8
-    assert ctypes.sizeof(fin.fin_traj) == 11 * 8 + 8
+    assert ctypes.sizeof(fin.fin_traj) == 13 * 8 + 8   # 13 pointers + ep_capacity (padded)
     assert ctypes.sizeof(fin.fin_noise) == 24
 
 

@@ -157,3 +157,115 @@ def test_adam_step_matches_oracle():
     np.testing.assert_allclose(host(dm), o_m, rtol=2e-6, atol=1e-7)
     np.testing.assert_allclose(host(dv), o_v, rtol=2e-6, atol=1e-7)
     np.testing.assert_allclose(host(dt), o_th, rtol=2e-6, atol=2e-7)
+
+
+def test_ppo_iteration_end_to_end():
+    """One producer -> consumer iteration on the device: a fused rollout with Philox
+    noise logs the env-private observation entries and market days; the learner rebuilds every
+    sample's observation (bitwise the oracle's bf16 observation of the replayed state), the old
+    policy's forward on it reproduces the rollout's network outputs bit for bit, the regenerated
+    Philox noise reproduces the executed share counts, GAE gives the advantages, fin_ppo_prepare /
+    fin_ppo_grad the gradient (ratio 1 at the old weights up to the f32 log pi_old; gradients against
+    the oracle),
+    Adam steps the float32 master weights, fin_policy_load installs them (the new forward passes
+    the layered check against the oracle with the new bf16 weights; the surrogate at the new weights
+    is finite -- its sign is not asserted: one Adam step moves every bf16 weight by about one
+    rounding step, far outside the first-order regime of a sigma = 0.1 Gaussian), and the next
+    rollout runs on the new policy."""
+    import math
+
+    import torch
+    from gpu_util import stock_pair
+    from oracle import learn as olearn
+    from oracle import mlp as omlp
+    from oracle import rollout as orol
+    from oracle import stock as ostock
+    from paper_2501_10709_b200 import fin
+    from synth import market, policy as spol
+    m = market.stock_c1(rows=150)
+    N, T, K, seed = 300, 35, 30, 77
+    ocfg, fcfg = stock_pair(num_envs=N, num_assets=K, num_indicators=8, num_rows=150, episode_len=30,
+                            num_windows=20, window_block=128)
+    env = fin.fin_env_create(fcfg, m.market)
+    layers = spol.random_bias(spol.kaiming_bf16(spol.STOCK_DIMS, 7), 8)
+    pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, layers)
+    t_base = fin.fin_env_clock(env)
+    logs = dict(actions=zeros((T, N, K), torch.int16), reward=zeros((T, N), torch.float32),
+                done=zeros((T, N), torch.uint8), mlp_out=zeros((T, 1, N, K), torch.float32),
+                obs_private=zeros((T, N, 32), torch.int16), day=zeros((T, N), torch.int32))
+    fin.fin_rollout(env, [pol], T, fin.make_noise(fin.FIN_NOISE_PHILOX, seed), fin.make_traj(**logs))
+    assert fin.fin_env_clock(env) == t_base + T
+    B = T * N
+    idx = torch.arange(B, dtype=torch.int64, device="cuda")
+    x = zeros((B, 301), torch.int16)
+    fin.fin_gather_observations(env, logs["obs_private"], logs["day"], idx, x)
+    xb = host(x).view(np.uint16).reshape(T, N, 301)
+    # (a) the observations are the oracle's, bf16-quantised, on the replayed states
+    acts = host(logs["actions"])
+    st = ostock.reset(ocfg)
+    for t in range(T):
+        X = orol.stock_obs_batch(ocfg, st, m.market)
+        assert np.array_equal(xb[t], spol.f64_to_bf16_bits(X)), t
+        ostock.step(ocfg, st, m.market, acts[t])
+    # (b) the old policy's forward reproduces the rollout's outputs bit for bit
+    z_old = zeros((B, K), torch.float32)
+    hid = zeros((B, 2, 256), torch.int16)
+    fin.fin_mlp_forward(pol, x, z_old, hid)
+    assert np.array_equal(host(z_old).reshape(T, N, K), host(logs["mlp_out"])[:, 0])
+    # (c) the regenerated Philox noise reproduces the executed actions (up to .5 roundings)
+    eps = zeros((B, K), torch.float32)
+    fin.fin_rollout_noise(env, seed, t_base, idx, eps)
+    zg, eg = host(z_old).astype(np.float64), host(eps).astype(np.float64)
+    y = 100.0 * np.clip(np.tanh(zg) + 0.1 * eg, -1, 1)
+    rha = np.sign(y) * np.floor(np.abs(y) + 0.5)
+    bad = rha != acts.reshape(B, K)
+    assert np.all(np.abs(np.abs(y[bad] - np.trunc(y[bad])) - 0.5) < 1e-4)
+    # (d) advantages (no critic: V = 0) and the gradient at the old weights
+    adv2 = zeros((T, N), torch.float32)
+    ret = zeros((T, N), torch.float32)
+    fin.fin_gae(logs["reward"], zeros((T + 1, N), torch.float32), logs["done"], adv2, ret, normalise=True)
+    adv = adv2.reshape(B)
+    a = zeros((B, K), torch.float32)
+    logp_old = zeros(B, torch.float32)
+    fin.fin_ppo_prepare(z_old, eps, a, logp_old)
+    L64 = omlp.layers_f64(layers)
+    w = [dev(W.astype(np.float32)) for W, _ in L64]
+    b = [dev(bb.astype(np.float32)) for _, bb in L64]
+    grads = [(zeros(W.shape, torch.float32), zeros(W.shape[0], torch.float32)) for W in w]
+    stats = zeros(4, torch.float64)
+    fin.fin_ppo_grad(x, hid, z_old, a, logp_old, adv, w[1], w[2], grads, stats)
+    s0 = host(stats)
+    # rho = 1 at the old weights, up to the f32 rounding of the stored log pi_old (~5e-6 of |log pi|)
+    assert abs(s0[1] - 1.0) < 1e-5 and s0[2] == 0.0
+    assert s0[0] == pytest.approx(float(host(adv).astype(np.float64).mean()), abs=1e-7)
+    _, _, _, g3, _ = olearn.ppo_head(zg.tolist(), host(a).astype(np.float64).tolist(),
+                                     host(logp_old).astype(np.float64).tolist(), host(adv).astype(np.float64).tolist())
+    ref = olearn.mlp_backward_np(L64, omlp.bf16_bits_to_f64(xb.reshape(B, 301)),
+                                 omlp.bf16_bits_to_f64(host(hid).view(np.uint16)), g3)
+    for (dw, db), (rw, rb) in zip(grads, ref):
+        for g, o in ((host(dw).astype(np.float64), rw), (host(db).astype(np.float64), rb)):
+            assert np.all(np.abs(g - o) <= 5e-5 * np.abs(o).max() + 2e-4 * np.abs(o))
+    # (e) Adam on the f32 master weights, install, check the new forward and the improvement
+    params = w + b
+    gl = [g for g, _ in grads] + [g for _, g in grads]
+    for p, g in zip(params, gl):
+        mm, vv = torch.zeros_like(p), torch.zeros_like(p)
+        fin.fin_adam_step(p, mm, vv, g, 1, lr=1e-4)
+    fin.fin_policy_load(pol, w, b)
+    z_new = zeros((B, K), torch.float32)
+    hid_new = zeros((B, 2, 256), torch.int16)
+    fin.fin_mlp_forward(pol, x, z_new, hid_new)
+    new_layers = [(spol.f64_to_bf16_bits(host(W).astype(np.float64)), host(bb)) for W, bb in zip(w, b)]
+    N64 = omlp.layers_f64(new_layers)
+    sub = slice(0, 2000)
+    omlp.teacher_forced_layers(N64, omlp.bf16_bits_to_f64(xb.reshape(B, 301))[sub],
+                               host(hid_new).view(np.uint16)[sub], host(z_new)[sub])
+    fin.fin_ppo_grad(x, hid_new, z_new, a, logp_old, adv, dev(N64[1][0].astype(np.float32)),
+                     dev(N64[2][0].astype(np.float32)), grads, stats)
+    s1 = host(stats)
+    assert math.isfinite(s1[0]) and math.isfinite(s1[1]) and s1[1] != s0[1]   # the policy moved
+    assert not np.array_equal(host(z_new), host(z_old))
+    # (f) the next rollout runs on the new policy (its z1s term recomputed for the new weights)
+    fin.fin_rollout(env, [pol], 5, fin.make_noise(fin.FIN_NOISE_PHILOX, seed),
+                    fin.make_traj(reward=zeros((5, N), torch.float32)))
+    assert fin.fin_env_check(env) == 0
