@@ -229,3 +229,67 @@ def adam(theta, m, v, g, step: int, lr: float = 3e-4, beta1: float = 0.9, beta2:
         vv[i] = beta2 * vv[i] + (1.0 - beta2) * g[i] * g[i]
         th[i] = th[i] - lr * (mm[i] / c1) / (math.sqrt(vv[i] / c2) + eps)
     return th, mm, vv
+
+
+# ---------------------------------------------------------------- the DQN family's update (R-DQN)
+# PAPER.md P:317-321, P:346 (DQN, Double DQN, Dueling DQN members of the crypto ensemble); SPEC
+# S:362-391.  For a batch of transitions (s, a, r, done, s'):
+#   DQN:        y = r + gamma (1 - done) max_a' Q_target(s', a')
+#   Double DQN: y = r + gamma (1 - done) Q_target(s', argmax_a' Q_online(s', a'))   (lowest index on ties)
+#   Dueling:    the network's outputs are (A_0, A_1, A_2, V) and Q(s, a) = V + A_a - mean_j A_j
+#   loss:       L = (1/B) sum_s (Q(s, a_s) - y_s)^2  (y is a constant: no gradient through the target)
+#   dL/d out:   plain nets: 2 (Q - y) / B on output a_s;  dueling: 2 (Q - y) / B (delta_{a j} - 1/3) on
+#               A_j and 2 (Q - y) / B on V
+# then the same backward pass through the MLP (mlp_backward) and Adam.
+
+def dueling_q(out):
+    """out [A_0 .. A_{n-1}, V] -> Q [n] = V + A - mean A."""
+    n = len(out) - 1
+    m = 0.0
+    for j in range(n):
+        m += out[j]
+    m /= n
+    return [out[n] + out[j] - m for j in range(n)]
+
+
+def q_values(out, dueling: bool):
+    return dueling_q(out) if dueling else list(out)
+
+
+def dqn_targets(q_next_target, r, done, gamma: float, q_next_online=None, dueling: bool = False):
+    """y [B] from the target net's outputs at s' (and the online net's for Double DQN)."""
+    y = []
+    for s in range(len(r)):
+        qt = q_values([float(v) for v in q_next_target[s]], dueling)
+        if q_next_online is None:
+            boot = max(qt)
+        else:
+            qo = q_values([float(v) for v in q_next_online[s]], dueling)
+            best = 0
+            for j in range(1, len(qo)):
+                if qo[j] > qo[best]:
+                    best = j
+            boot = qt[best]
+        keep = 0.0 if done[s] else 1.0
+        y.append(float(r[s]) + gamma * keep * boot)
+    return y
+
+
+def dqn_head(out, a, y, dueling: bool = False):
+    """(L, g_out [B][O]) for the online net's outputs ``out`` at s and actions a [B]."""
+    B, O = len(out), len(out[0])
+    g = [[0.0] * O for _ in range(B)]
+    L = 0.0
+    for s in range(B):
+        q = q_values([float(v) for v in out[s]], dueling)
+        d = q[int(a[s])] - float(y[s])
+        L += d * d
+        c = 2.0 * d / B
+        if dueling:
+            n = O - 1
+            for j in range(n):
+                g[s][j] = c * ((1.0 if j == int(a[s]) else 0.0) - 1.0 / n)
+            g[s][n] = c
+        else:
+            g[s][int(a[s])] = c
+    return L / B, g

@@ -174,3 +174,66 @@ def test_adam_first_steps_closed_form():
     th2, _, _ = learn.adam(th, m, v, g, 2, lr=0.1)
     for t2, t, gi in zip(th2, th, g):
         assert (t2 - t) == pytest.approx(-0.1 * gi / (abs(gi) + 1e-8), rel=1e-9, abs=1e-12)
+
+
+# ---------------------------------------------------------------- DQN family (R-DQN)
+def test_dqn_targets_spec_examples():
+    """done = 1 -> y = r; gamma = 0 -> y = r; a constant target Q = c with r = 0,
+    gamma = 0.99, done = 0 -> y = 0.99 c; Double DQN with online = target equals DQN; online argmax
+    a1 while the target's max is at a2 -> the target's value at a1."""
+    qt = [[1.0, 5.0, 2.0], [3.0, 3.0, 3.0]]
+    assert learn.dqn_targets(qt, [0.5, -1.0], [1, 1], 0.99) == [0.5, -1.0]
+    assert learn.dqn_targets(qt, [0.5, -1.0], [0, 0], 0.0) == [0.5, -1.0]
+    assert learn.dqn_targets([[2.0, 2.0, 2.0]], [0.0], [0], 0.99) == [0.99 * 2.0]
+    assert learn.dqn_targets(qt, [0.1, 0.2], [0, 0], 0.9, q_next_online=qt) == learn.dqn_targets(qt, [0.1, 0.2],
+                                                                                                [0, 0], 0.9)
+    y = learn.dqn_targets([[1.0, 5.0, 2.0]], [0.0], [0], 1.0, q_next_online=[[0.0, 1.0, 7.0]])
+    assert y == [2.0]                                   # argmax online = 2 -> Q_target(s', 2)
+
+
+def test_dueling_identities_and_head():
+    """equal advantages -> Q = V for every action; V = 0, A = [1, 2, 3] ->
+    Q = [-1, 0, 1]; argmax Q = argmax A.  The dueling head's output gradient sums to 2 (Q - y) / B
+    on V and to 0 over the advantages (the mean-centering)."""
+    assert learn.dueling_q([0.5, 0.5, 0.5, 2.0]) == [2.0, 2.0, 2.0]
+    assert learn.dueling_q([1.0, 2.0, 3.0, 0.0]) == [-1.0, 0.0, 1.0]
+    L, g = learn.dqn_head([[1.0, 2.0, 3.0, 0.5]], [2], [0.0], dueling=True)
+    q = learn.dueling_q([1.0, 2.0, 3.0, 0.5])[2]
+    assert L == q * q and g[0][3] == 2 * q and abs(sum(g[0][:3])) < 1e-15
+
+
+def test_dqn_gradient_against_finite_differences():
+    """d L / d theta (dqn_head + mlp_backward) against central finite differences, plain and dueling
+    heads, with some terminal transitions; the target is held fixed (computed once)."""
+    rng = np.random.default_rng(13)
+    for dueling in (False, True):
+        layers = _tiny_net(rng, (5, 6, 4, 4 if dueling else 3))
+        B = 6
+        x = rng.normal(size=(B, 5))
+        xn = rng.normal(size=(B, 5))
+        a = rng.integers(0, 3, B)
+        r = rng.normal(size=B)
+        done = rng.random(B) < 0.3
+        qt, _ = _forward64(layers, xn)
+        y = learn.dqn_targets(qt.tolist(), r, done, 0.9, dueling=dueling)
+
+        def loss():
+            out, _ = _forward64(layers, x)
+            return learn.dqn_head(out.tolist(), a, y, dueling)[0]
+
+        out, hid = _forward64(layers, x)
+        _, g = learn.dqn_head(out.tolist(), a, y, dueling)
+        grads = learn.mlp_backward(layers, x.tolist(), hid.tolist(), g)
+        h = 1e-6
+        for li in range(3):
+            for which in (0, 1):
+                p = layers[li][which]
+                for idx in np.ndindex(p.shape):
+                    old = p[idx]
+                    p[idx] = old + h
+                    lp = loss()
+                    p[idx] = old - h
+                    lm = loss()
+                    p[idx] = old
+                    fd = (lp - lm) / (2 * h)
+                    assert abs(fd - grads[li][which][idx]) <= 1e-6 * max(1.0, abs(fd)), (dueling, li, which, idx)
