@@ -350,6 +350,22 @@ int fin_ppo_grad(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t k_ou
                  double sigma, double clip_eps, const float* w2, const float* w3, float* dw1, float* db1, float* dw2,
                  float* db2, float* dw3, float* db3, double* stats, void* stream);
 
+/* The DQN family's gradient step (the crypto members of P:317-321 / P:346;
+ * SPEC S:362-391; reading R-DQN, formulas in oracle/learn.py): for B transitions (s, a, r, done,
+ * s') of a 3-layer ReLU Q-net (device): x bf16 bits [B][in_dim], hidden bf16 bits
+ * [B][2][max(h1, h2)] and out f32 [B][k_out] of the online net at s (fin_mlp_forward), action u8
+ * [B] (0 .. number of actions - 1), reward f32 [B], done u8 [B], q_next_target f32 [B][k_out] the
+ * target net's outputs at s', q_next_online f32 [B][k_out] the online net's at s' for Double DQN
+ * (NULL: DQN).  dueling != 0: outputs are (A_0 .. A_{n-1}, V) and Q = V + A - mean A.  Target y =
+ * r + gamma (1 - done) max_a Q_target(s', a) (Double: Q_target(s', argmax_a Q_online(s', a))),
+ * loss L = mean (Q(s, a) - y)^2 with y held fixed; writes dL/dtheta (device f32, as fin_ppo_grad)
+ * and stats (device f64 [4]: L, mean Q(s, a), mean y, B).  Weights w2 / w3 as in fin_ppo_grad. */
+int fin_dqn_grad(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t k_out, const uint16_t* x,
+                 const uint16_t* hidden, const float* out, const uint8_t* action, const float* reward,
+                 const uint8_t* done, const float* q_next_target, const float* q_next_online, double gamma,
+                 int32_t dueling, const float* w2, const float* w3, float* dw1, float* db1, float* dw2, float* db2,
+                 float* dw3, float* db3, double* stats, void* stream);
+
 /* The learner's view of a rollout's samples (NEXT-4).  A sample is idx = t N + env (step t of
  * the call, local env).  fin_env_clock: the handle's global step counter (host out) -- record it
  * before a rollout: its Philox noise of step t is drawn at t_global + t.

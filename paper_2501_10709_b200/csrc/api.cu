@@ -31,6 +31,11 @@ cudaError_t launch_ppo_grad(int B, int in, int H1, int H2, int K, const uint16_t
                             float* db2, float* dw3, float* db3, double* stats, cudaStream_t s);
 cudaError_t launch_adam(int64_t n, float* th, float* m, float* v, const float* g, int step, double lr, double b1,
                         double b2, double eps, cudaStream_t s);
+cudaError_t launch_dqn_grad(int B, int in, int H1, int H2, int O, const uint16_t* x, const uint16_t* hid,
+                            const float* out, const uint8_t* act, const float* rew, const uint8_t* done,
+                            const float* qt, const float* qo, double gamma, int dueling, const float* w2,
+                            const float* w3, float* dw1, float* db1, float* dw2, float* db2, float* dw3, float* db3,
+                            double* stats, cudaStream_t s);
 cudaError_t launch_gather_obs(const EnvDev& e, const uint16_t* priv, int P, const int32_t* day, const int64_t* idx,
                               int B, uint16_t* x, cudaStream_t s);
 cudaError_t launch_noise_at(uint64_t seed, int64_t off, int N, int64_t t_base, const int64_t* idx, int B, int K,
@@ -1052,6 +1057,25 @@ int fin_ppo_grad(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t k_ou
   cudaError_t e = fin::launch_ppo_grad(B, in_dim, h1, h2, k_out, x, hidden, z, a, logp_old, adv, sigma, clip_eps, w2, w3,
                                        dw1, db1, dw2, db2, dw3, db3, stats, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fin_ppo_grad launch");
+  return FIN_OK;
+}
+
+int fin_dqn_grad(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t k_out, const uint16_t* x,
+                 const uint16_t* hidden, const float* out, const uint8_t* action, const float* reward,
+                 const uint8_t* done, const float* q_next_target, const float* q_next_online, double gamma,
+                 int32_t dueling, const float* w2, const float* w3, float* dw1, float* db1, float* dw2, float* db2,
+                 float* dw3, float* db3, double* stats, void* stream) {
+  if (!x || !hidden || !out || !action || !reward || !done || !q_next_target || !w2 || !w3 || !dw1 || !db1 || !dw2 ||
+      !db2 || !dw3 || !db3 || !stats)
+    return fail(FIN_E_CONFIG, "fin_dqn_grad: null argument");
+  if (B < 1 || in_dim < 1 || in_dim > 4096 || h1 < 1 || h1 > 1024 || h2 < 1 || h2 > 1024 || k_out < 2 || k_out > 8)
+    return fail(FIN_E_CONFIG, "fin_dqn_grad: bad sizes");
+  if (dueling && k_out < 3) return fail(FIN_E_CONFIG, "fin_dqn_grad: a dueling head needs >= 2 actions + V");
+  if (!(gamma >= 0.0 && gamma <= 1.0)) return fail(FIN_E_CONFIG, "fin_dqn_grad: gamma must be in [0, 1]");
+  cudaError_t e = fin::launch_dqn_grad(B, in_dim, h1, h2, k_out, x, hidden, out, action, reward, done, q_next_target,
+                                       q_next_online, gamma, dueling, w2, w3, dw1, db1, dw2, db2, dw3, db3, stats,
+                                       S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_dqn_grad launch");
   return FIN_OK;
 }
 

@@ -67,6 +67,71 @@ __global__ void k_ppo_head(int B, int K, const float* __restrict__ z, const floa
   }
 }
 
+// ---- DQN family head (reading R-DQN): one thread per transition, float64; g_out = dL/d out
+__device__ __forceinline__ void qvals(const float* o, int O, bool dueling, double* q) {
+  if (!dueling) {
+    for (int j = 0; j < O; ++j) q[j] = (double)o[j];
+    return;
+  }
+  const int n = O - 1;
+  double m = 0.0;
+  for (int j = 0; j < n; ++j) m += (double)o[j];
+  m /= n;
+  for (int j = 0; j < n; ++j) q[j] = (double)o[n] + (double)o[j] - m;
+}
+__global__ void k_dqn_head(int B, int O, const float* __restrict__ out, const uint8_t* __restrict__ act,
+                           const float* __restrict__ rew, const uint8_t* __restrict__ done,
+                           const float* __restrict__ qt, const float* __restrict__ qo, double gamma, int dueling,
+                           float* __restrict__ g, double* __restrict__ part) {
+  __shared__ double red[4][kThr / 32];
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  double st[4] = {0.0, 0.0, 0.0, 0.0};
+  if (s < B) {
+    const bool du = dueling != 0;
+    const int n = du ? O - 1 : O;
+    double q[8], t[8];
+    qvals(qt + (size_t)s * O, O, du, t);
+    double boot;
+    if (qo) {   // Double DQN: the online net picks, the target net evaluates (lowest index on ties)
+      double w[8];
+      qvals(qo + (size_t)s * O, O, du, w);
+      int best = 0;
+      for (int j = 1; j < n; ++j)
+        if (w[j] > w[best]) best = j;
+      boot = t[best];
+    } else {
+      boot = t[0];
+      for (int j = 1; j < n; ++j) boot = fmax(boot, t[j]);
+    }
+    const double y = (double)rew[s] + gamma * (done[s] ? 0.0 : 1.0) * boot;
+    qvals(out + (size_t)s * O, O, du, q);
+    const int a = act[s];
+    const double d = q[a] - y;
+    const double c = 2.0 * d / (double)B;
+    for (int j = 0; j < O; ++j) {
+      double v;
+      if (du) v = j < n ? c * ((j == a ? 1.0 : 0.0) - 1.0 / n) : c;
+      else v = j == a ? c : 0.0;
+      g[(size_t)s * O + j] = (float)v;
+    }
+    st[0] = d * d;
+    st[1] = q[a];
+    st[2] = y;
+    st[3] = 1.0;
+  }
+  for (int j = 0; j < 4; ++j) {
+    double v = st[j];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[j][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double v = 0.0;
+    for (int w = 0; w < kThr / 32; ++w) v += red[threadIdx.x][w];
+    part[(size_t)blockIdx.x * 4 + threadIdx.x] = v;
+  }
+}
+
 __global__ void k_stats_final(const double* __restrict__ part, int nb, double* __restrict__ stats) {
   if (threadIdx.x < 4) {
     double v = 0.0;
@@ -321,32 +386,26 @@ cudaError_t launch_to_bf16(int64_t n, const float* x, uint16_t* y, cudaStream_t 
   return cudaGetLastError();
 }
 
-cudaError_t launch_ppo_grad(int B, int in, int H1, int H2, int K, const uint16_t* x, const uint16_t* hid,
-                            const float* z, const float* a, const float* logp_old, const float* adv, double sigma,
-                            double eps, const float* w2, const float* w3, float* dw1, float* db1, float* dw2,
-                            float* db2, float* dw3, float* db3, double* stats, cudaStream_t s) {
+// the backward pass from g3 = dL/d z_out [B][K] (device, f32): g2, g1, weight and bias gradients
+cudaError_t backward(int B, int in, int H1, int H2, int K, const uint16_t* x, const uint16_t* hid, const float* g3,
+                     const float* w2, const float* w3, float* dw1, float* db1, float* dw2, float* db2, float* dw3,
+                     float* db3, cudaStream_t s) {
   const int Hs = H1 > H2 ? H1 : H2;   // hidden log row width ([B][2][Hs], fin_mlp_forward)
-  const int nb = (B + kThr - 1) / kThr;
-  float *g3 = nullptr, *g2 = nullptr, *g1 = nullptr, *scr = nullptr;
-  double* part = nullptr;
   auto part_n = [](int M, int N, int Kk) {   // split partials of one weight-gradient GEMM
     const int sp = splits_for(M, N, Kk);
     const int kc = ((Kk + sp - 1) / sp + kBK - 1) / kBK * kBK;
     const int used = (Kk + kc - 1) / kc;
     return used > 1 ? (size_t)used * M * N : (size_t)1;
   };
-  size_t scr_n = (size_t)((B + 2047) / 2048) * (H1 > H2 ? (H1 > K ? H1 : K) : (H2 > K ? H2 : K));   // bias partials
+  size_t scr_n = (size_t)((B + kColRows - 1) / kColRows) * (H1 > H2 ? (H1 > K ? H1 : K) : (H2 > K ? H2 : K));
   if (part_n(K, H2, B) > scr_n) scr_n = part_n(K, H2, B);
   if (part_n(H2, H1, B) > scr_n) scr_n = part_n(H2, H1, B);
   if (part_n(H1, in, B) > scr_n) scr_n = part_n(H1, in, B);
-  cudaError_t e = cudaMallocAsync(&g3, sizeof(float) * (size_t)B * K, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&g2, sizeof(float) * (size_t)B * H2, s);
+  float *g2 = nullptr, *g1 = nullptr, *scr = nullptr;
+  cudaError_t e = cudaMallocAsync(&g2, sizeof(float) * (size_t)B * H2, s);
   if (e == cudaSuccess) e = cudaMallocAsync(&g1, sizeof(float) * (size_t)B * H1, s);
   if (e == cudaSuccess) e = cudaMallocAsync(&scr, sizeof(float) * scr_n, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&part, sizeof(double) * 4 * (size_t)nb, s);
   if (e != cudaSuccess) return e;
-  k_ppo_head<<<nb, kThr, 0, s>>>(B, K, z, a, logp_old, adv, sigma, eps, g3, part);
-  k_stats_final<<<1, 32, 0, s>>>(part, nb, stats);
   const size_t n2 = (size_t)B * H2;
   k_back_out<<<(unsigned)((n2 + 255) / 256), 256, 0, s>>>(B, K, H2, Hs, g3, w3, hid, g2);
   // g1 = (g2 W2) * [h1 > 0]: A = g2 [B][H2] row-major, B = W2 [H2][H1], mask = h1 (row stride 2 Hs)
@@ -364,10 +423,45 @@ cudaError_t launch_ppo_grad(int B, int in, int H1, int H2, int K, const uint16_t
     k_colsum_final<<<(hs[l] + 127) / 128, 128, 0, s>>>(chunks, hs[l], scr, bs[l]);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
-  cudaFreeAsync(g3, s);
   cudaFreeAsync(g2, s);
   cudaFreeAsync(g1, s);
   cudaFreeAsync(scr, s);
+  return e;
+}
+
+cudaError_t launch_ppo_grad(int B, int in, int H1, int H2, int K, const uint16_t* x, const uint16_t* hid,
+                            const float* z, const float* a, const float* logp_old, const float* adv, double sigma,
+                            double eps, const float* w2, const float* w3, float* dw1, float* db1, float* dw2,
+                            float* db2, float* dw3, float* db3, double* stats, cudaStream_t s) {
+  const int nb = (B + kThr - 1) / kThr;
+  float* g3 = nullptr;
+  double* part = nullptr;
+  cudaError_t e = cudaMallocAsync(&g3, sizeof(float) * (size_t)B * K, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&part, sizeof(double) * 4 * (size_t)nb, s);
+  if (e != cudaSuccess) return e;
+  k_ppo_head<<<nb, kThr, 0, s>>>(B, K, z, a, logp_old, adv, sigma, eps, g3, part);
+  k_stats_final<<<1, 32, 0, s>>>(part, nb, stats);
+  e = backward(B, in, H1, H2, K, x, hid, g3, w2, w3, dw1, db1, dw2, db2, dw3, db3, s);
+  cudaFreeAsync(g3, s);
+  cudaFreeAsync(part, s);
+  return e;
+}
+
+cudaError_t launch_dqn_grad(int B, int in, int H1, int H2, int O, const uint16_t* x, const uint16_t* hid,
+                            const float* out, const uint8_t* act, const float* rew, const uint8_t* done,
+                            const float* qt, const float* qo, double gamma, int dueling, const float* w2,
+                            const float* w3, float* dw1, float* db1, float* dw2, float* db2, float* dw3, float* db3,
+                            double* stats, cudaStream_t s) {
+  const int nb = (B + kThr - 1) / kThr;
+  float* g3 = nullptr;
+  double* part = nullptr;
+  cudaError_t e = cudaMallocAsync(&g3, sizeof(float) * (size_t)B * O, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&part, sizeof(double) * 4 * (size_t)nb, s);
+  if (e != cudaSuccess) return e;
+  k_dqn_head<<<nb, kThr, 0, s>>>(B, O, out, act, rew, done, qt, qo, gamma, dueling, g3, part);
+  k_stats_final<<<1, 32, 0, s>>>(part, nb, stats);
+  e = backward(B, in, H1, H2, O, x, hid, g3, w2, w3, dw1, db1, dw2, db2, dw3, db3, s);
+  cudaFreeAsync(g3, s);
   cudaFreeAsync(part, s);
   return e;
 }

@@ -52,7 +52,8 @@ EXPORTS = ("fin_env_create", "fin_env_reset", "fin_env_step", "fin_env_get_state
            "fin_rollout_actions", "fin_ensemble_act", "fin_episode_metrics", "fin_mlp_forward",
            "fin_philox_normals", "fin_member_weights", "fin_market_prepare", "fin_crypto_market", "fin_gae", "fin_kl_diversity", "fin_last_error", "fin_abi_version", "fin_device_check",
            "fin_debug_trace", "fin_env_counters", "fin_stock_market", "fin_ppo_grad", "fin_adam_step",
-           "fin_env_clock", "fin_gather_observations", "fin_rollout_noise", "fin_ppo_prepare", "fin_policy_load")
+           "fin_env_clock", "fin_gather_observations", "fin_rollout_noise", "fin_ppo_prepare", "fin_policy_load",
+           "fin_dqn_grad")
 
 
 class FinError(RuntimeError):
@@ -114,6 +115,7 @@ _sig = {
     "fin_adam_step": ([C.c_int64, _P, _P, _P, _P, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double, _P],
                       C.c_int),
     "fin_env_clock": ([_P, _P], C.c_int),
+    "fin_dqn_grad": ([C.c_int32] * 5 + [_P] * 8 + [C.c_double, C.c_int32] + [_P] * 10, C.c_int),
     "fin_gather_observations": ([_P, _P, _P, _P, C.c_int32, _P, _P], C.c_int),
     "fin_rollout_noise": ([_P, C.c_uint64, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P], C.c_int),
     "fin_ppo_prepare": ([C.c_int32, C.c_int32, _P, _P, C.c_double, _P, _P, _P], C.c_int),
@@ -504,6 +506,32 @@ def fin_stock_market(days: int, K: int, seed: int, ohlcv, mu: float = 2e-4, sigm
         raise ValueError("ohlcv must be [days][5][K]")
     _check(_lib.fin_stock_market(int(days), int(K), int(seed), float(mu), float(sigma), float(s0_lo), float(s0_hi),
                                  _ptr(ohlcv, torch.float32, "ohlcv"), _stream(stream)), "fin_stock_market")
+
+
+def fin_dqn_grad(x_bf16_bits, hidden, out, action, reward, done, q_next_target, w2, w3, grads, stats,
+                 q_next_online=None, gamma: float = 0.99, dueling: bool = False, stream=None) -> None:
+    """DQN / Double DQN (q_next_online given) / Dueling gradient step (include/fin.h); grads as in
+    fin_ppo_grad; stats f64 [4] (L, mean Q(s, a), mean y, B)."""
+    import torch
+    B, in_dim = int(x_bf16_bits.shape[0]), int(x_bf16_bits.shape[1])
+    k_out = int(out.shape[1])
+    h2, h1 = int(w2.shape[0]), int(w2.shape[1])
+    if tuple(w3.shape) != (k_out, h2) or tuple(q_next_target.shape) != (B, k_out) or int(hidden.shape[0]) != B:
+        raise ValueError("fin_dqn_grad: inconsistent shapes")
+    if q_next_online is not None and tuple(q_next_online.shape) != (B, k_out):
+        raise ValueError("fin_dqn_grad: q_next_online must be [B][k_out]")
+    _need(hidden, B * 2 * max(h1, h2), "hidden [B][2][H]")
+    for t, w in ((action, "action"), (reward, "reward"), (done, "done")):
+        _need(t, B, w)
+    f32 = torch.float32
+    p = [_ptr(t, f32, "grad") for pair in grads for t in pair]
+    _check(_lib.fin_dqn_grad(B, in_dim, h1, h2, k_out, _ptr(x_bf16_bits, torch.int16, "x"),
+                             _ptr(hidden, torch.int16, "hidden"), _ptr(out, f32, "out"),
+                             _ptr(action, torch.uint8, "action"), _ptr(reward, f32, "reward"),
+                             _ptr(done, torch.uint8, "done"), _ptr(q_next_target, f32, "q_next_target"),
+                             _ptr(q_next_online, f32, "q_next_online"), float(gamma), int(bool(dueling)),
+                             _ptr(w2, f32, "w2"), _ptr(w3, f32, "w3"), *p, _ptr(stats, torch.float64, "stats"),
+                             _stream(stream)), "fin_dqn_grad")
 
 
 def fin_env_clock(env: Env) -> int:

@@ -269,3 +269,55 @@ def test_ppo_iteration_end_to_end():
     fin.fin_rollout(env, [pol], 5, fin.make_noise(fin.FIN_NOISE_PHILOX, seed),
                     fin.make_traj(reward=zeros((5, N), torch.float32)))
     assert fin.fin_env_check(env) == 0
+
+
+@pytest.mark.parametrize("variant", ["dqn", "double", "dueling"])
+def test_dqn_grad_matches_oracle(variant):
+    """fin_dqn_grad against oracle.learn (dqn_targets + dqn_head + mlp_backward) on the device
+    forwards' own outputs (online net at s and s', a target net at s'): the C3 Q-net (103-128-128-3,
+    dueling: -4), 1,000 transitions with 20% terminal ones; gradients within 2e-5 max|o| + 1e-4|o|,
+    the loss and the mean target to 1e-6 (f32 network outputs, float64 head)."""
+    import torch
+    from oracle import learn as olearn
+    from oracle import mlp as omlp
+    from paper_2501_10709_b200 import fin
+    from synth import policy as spol
+    rng = np.random.default_rng(31)
+    dueling = variant == "dueling"
+    dims = tuple(spol.CRYPTO_DIMS[:-1]) + ((4,) if dueling else (3,))
+    kind = fin.FIN_Q_DUELING if dueling else fin.FIN_Q_ARGMAX
+    online = spol.random_bias(spol.kaiming_bf16(dims, 4), 5)
+    target = spol.random_bias(spol.kaiming_bf16(dims, 6), 7)
+    pol, tgt = fin.fin_policy_create(kind, online), fin.fin_policy_create(kind, target)
+    B, O = 1000, dims[-1]
+    xs = spol.f64_to_bf16_bits(rng.standard_normal((B, 103)))
+    xn = spol.f64_to_bf16_bits(rng.standard_normal((B, 103)))
+
+    def fwd(p, xb):
+        z = zeros((B, O), torch.float32)
+        h = zeros((B, 2, 128), torch.int16)
+        fin.fin_mlp_forward(p, dev(xb.view(np.int16)), z, h)
+        return z, h
+
+    out, hid = fwd(pol, xs)
+    qt, _ = fwd(tgt, xn)
+    qo, _ = fwd(pol, xn) if variant == "double" else (None, None)
+    act = rng.integers(0, 3, B).astype(np.uint8)
+    rew = rng.standard_normal(B).astype(np.float32)
+    done = (rng.random(B) < 0.2).astype(np.uint8)
+    L64 = omlp.layers_f64(online)
+    grads = [(zeros(W.shape, torch.float32), zeros(W.shape[0], torch.float32)) for W, _ in L64]
+    stats = zeros(4, torch.float64)
+    fin.fin_dqn_grad(dev(xs.view(np.int16)), hid, out, dev(act), dev(rew), dev(done), qt,
+                     dev(L64[1][0].astype(np.float32)), dev(L64[2][0].astype(np.float32)), grads, stats,
+                     q_next_online=qo, gamma=0.99, dueling=dueling)
+    y = olearn.dqn_targets(host(qt).astype(np.float64).tolist(), rew.astype(np.float64), done, 0.99,
+                           q_next_online=None if qo is None else host(qo).astype(np.float64).tolist(), dueling=dueling)
+    Lo, g = olearn.dqn_head(host(out).astype(np.float64).tolist(), act, y, dueling)
+    ref = olearn.mlp_backward_np(L64, omlp.bf16_bits_to_f64(xs), omlp.bf16_bits_to_f64(host(hid).view(np.uint16)), g)
+    for (dw, db), (rw, rb) in zip(grads, ref):
+        for gg, o in ((host(dw).astype(np.float64), rw), (host(db).astype(np.float64), rb)):
+            assert np.all(np.abs(gg - o) <= 2e-5 * np.abs(o).max() + 1e-4 * np.abs(o)), float(np.abs(gg - o).max())
+    st = host(stats)
+    assert st[0] == pytest.approx(Lo, rel=1e-6) and st[2] == pytest.approx(np.mean(y), rel=1e-6, abs=1e-9)
+    assert st[3] == B
