@@ -293,3 +293,158 @@ def dqn_head(out, a, y, dueling: bool = False):
         else:
             g[s][int(a[s])] = c
     return L / B, g
+
+
+# ---------------------------------------------------------------- the actor-critic updates (R-AC)
+# The stock ensemble's DDPG and SAC members (reading
+# R-AC).  A critic Q(s, a) is a 3-layer ReLU MLP on the concatenated input [x(s); a] with a linear
+# scalar output (a learner-only network: float32 weights, no bf16 quantisation; ``dense_forward``).
+# The actor is the rollout's policy MLP z(s) (oracle.mlp), its action head that of R17:
+#   DDPG: a = mu(s) = tanh(z(s))
+#         y    = r + gamma (1 - done) Q_targ(s', tanh(z_targ(s')))
+#         L_Q  = (1/B) sum_s (Q(s, a_s) - y_s)^2                         (y held fixed)
+#         L_mu = -(1/B) sum_s Q(s, tanh(z(s)));   dL_mu/dz_k = -(1/B) dQ/da_k (1 - a_k^2)
+#   SAC (fixed std sigma around the pre-tanh mean, R17; fixed temperature alpha):
+#         u = z(s) + sigma eps,  a = tanh(u)
+#         log pi(a|s) = sum_k [-eps_k^2 / 2 - ln(sigma sqrt(2 pi)) - ln(1 - tanh(u_k)^2)]
+#                       with ln(1 - tanh(u)^2) = 2 (ln 2 - u - softplus(-2 u))  (the stable form)
+#         y    = r + gamma (1 - done) (min(Q1_targ, Q2_targ)(s', a') - alpha log pi(a'|s')),
+#                a' = tanh(z(s') + sigma eps') a fresh sample
+#         L_Qi = (1/B) sum_s (Qi(s, a_s) - y_s)^2,  i = 1, 2
+#         L_pi = (1/B) sum_s [alpha log pi(a~|s) - min(Q1, Q2)(s, a~)],  a~ = tanh(z(s) + sigma eps)
+#         dL_pi/dz_k = (1/B) [2 alpha a~_k - dQm/da_k (1 - a~_k^2)],  Qm the smaller critic at
+#                      (s, a~) (Q1 on ties); at fixed eps the Gaussian term of log pi does not move
+#                      with z, and d/du [-ln(1 - tanh(u)^2)] = 2 tanh(u)
+#   Soft target update: theta_targ <- tau theta + (1 - tau) theta_targ (tau = 0.005), float64,
+#   one rounding to float32.
+
+def softplus(x: float) -> float:
+    """ln(1 + e^x) without overflow."""
+    return max(x, 0.0) + math.log1p(math.exp(-abs(x)))
+
+
+def log1m_tanh2(u: float) -> float:
+    """ln(1 - tanh(u)^2) = 2 (ln 2 - u - softplus(-2 u)) (finite for every finite u)."""
+    return 2.0 * (math.log(2.0) - u - softplus(-2.0 * u))
+
+
+def squash(z, eps=None, sigma: float = 0.1):
+    """Rows z [B][K]: a = tanh(z + sigma eps) and log pi(a|s) [B] (SAC), or a = tanh(z) and no
+    log-density (DDPG, eps None).  float64 loops."""
+    B, K = len(z), len(z[0])
+    a = [[0.0] * K for _ in range(B)]
+    logp = None if eps is None else [0.0] * B
+    c = math.log(sigma * math.sqrt(2.0 * math.pi))
+    for s in range(B):
+        acc = 0.0
+        for k in range(K):
+            e = 0.0 if eps is None else float(eps[s][k])
+            u = float(z[s][k]) + sigma * e
+            a[s][k] = math.tanh(u)
+            if eps is not None:
+                acc += -0.5 * e * e - c - log1m_tanh2(u)
+        if eps is not None:
+            logp[s] = acc
+    return a, logp
+
+
+def dense_forward(layers64, x):
+    """Critic forward, float64 with no quantisation: [(W [out][in], b [out])] x 3, x [B][in] ->
+    (h1 [B][H1], h2 [B][H2], out [B][O]); h = ReLU(W x + b) for the hidden layers, the last
+    linear.  The matrix product is the library primitive ``@`` (pinned against the loops)."""
+    (w1, b1), (w2, b2), (w3, b3) = layers64
+    x = np.asarray(x, dtype=np.float64)
+    h1 = np.maximum(x @ w1.T + b1, 0.0)
+    h2 = np.maximum(h1 @ w2.T + b2, 0.0)
+    return h1, h2, h2 @ w3.T + b3
+
+
+def dense_forward_loops(layers64, x):
+    """``dense_forward`` with explicit loops (small cases)."""
+    out = []
+    for row in x:
+        h = [float(v) for v in row]
+        for li, (w, b) in enumerate(layers64):
+            nxt = []
+            for j in range(w.shape[0]):
+                acc = float(b[j])
+                for i in range(w.shape[1]):
+                    acc += float(w[j, i]) * h[i]
+                nxt.append(max(acc, 0.0) if li < 2 else acc)
+            h = nxt
+        out.append(h)
+    return np.array(out)
+
+
+def dense_backward_np(layers64, x, h1, h2, g_out):
+    """Gradients of sum_s g_out[s] . out(s) of ``dense_forward``: ([(dW_l, db_l)] for l = 1..3,
+    g_x [B][in]); ReLU derivative 1 where the activation is > 0."""
+    (w1, _), (w2, _), (w3, _) = layers64
+    x = np.asarray(x, dtype=np.float64)
+    g3 = np.asarray(g_out, dtype=np.float64)
+    g2 = (g3 @ w3) * (h2 > 0)
+    g1 = (g2 @ w2) * (h1 > 0)
+    return [(g1.T @ x, g1.sum(0)), (g2.T @ h1, g2.sum(0)), (g3.T @ h2, g3.sum(0))], g1 @ w1
+
+
+def critic_targets(r, done, q1_next, gamma: float, q2_next=None, logp_next=None, alpha: float = 0.0):
+    """y [B] = r + gamma (1 - done) (min(q1', q2') - alpha log pi'), q2' / log pi' optional (DDPG:
+    y = r + gamma (1 - done) q')."""
+    y = []
+    for s in range(len(r)):
+        boot = float(q1_next[s])
+        if q2_next is not None and float(q2_next[s]) < boot:
+            boot = float(q2_next[s])
+        if logp_next is not None:
+            boot = boot - alpha * float(logp_next[s])
+        keep = 0.0 if done[s] else 1.0
+        y.append(float(r[s]) + gamma * keep * boot)
+    return y
+
+
+def critic_head(q, y):
+    """(L = (1/B) sum (q - y)^2, g [B] = dL/dq = 2 (q - y) / B)."""
+    B = len(q)
+    L = 0.0
+    g = [0.0] * B
+    for s in range(B):
+        d = float(q[s]) - float(y[s])
+        L += d * d
+        g[s] = 2.0 * d / B
+    return L / B, g
+
+
+def ddpg_actor_head(a, q, dq):
+    """(L_mu = -(1/B) sum q, g_z [B][K] = -(1/B) dq (1 - a^2)) for a = tanh(z), the critic's value q
+    [B] and its gradient dq [B][K] = dQ/da at (s, a)."""
+    B, K = len(a), len(a[0])
+    L = 0.0
+    g = [[0.0] * K for _ in range(B)]
+    for s in range(B):
+        L -= float(q[s])
+        for k in range(K):
+            g[s][k] = -float(dq[s][k]) * (1.0 - a[s][k] * a[s][k]) / B
+    return L / B, g
+
+
+def sac_actor_head(a, logp, q1, dq1, q2, dq2, alpha: float):
+    """(L_pi, g_z [B][K]) of R-AC for the reparameterised sample a = tanh(z + sigma eps), its log pi,
+    and both critics' values / action gradients at (s, a)."""
+    B, K = len(a), len(a[0])
+    L = 0.0
+    g = [[0.0] * K for _ in range(B)]
+    for s in range(B):
+        two = q2 is not None and float(q2[s]) < float(q1[s])
+        qm = float(q2[s]) if two else float(q1[s])
+        dqm = dq2[s] if two else dq1[s]
+        L += alpha * float(logp[s]) - qm
+        for k in range(K):
+            g[s][k] = (2.0 * alpha * a[s][k] - float(dqm[k]) * (1.0 - a[s][k] * a[s][k])) / B
+    return L / B, g
+
+
+def soft_update(target, online, tau: float):
+    """float32 target <- f32(tau theta + (1 - tau) theta_target), the sum in float64."""
+    t = np.asarray(target, dtype=np.float64)
+    o = np.asarray(online, dtype=np.float64)
+    return (tau * o + (1.0 - tau) * t).astype(np.float32)

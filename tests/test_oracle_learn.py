@@ -237,3 +237,188 @@ def test_dqn_gradient_against_finite_differences():
                     p[idx] = old
                     fd = (lp - lm) / (2 * h)
                     assert abs(fd - grads[li][which][idx]) <= 1e-6 * max(1.0, abs(fd)), (dueling, li, which, idx)
+
+
+# ---------------------------------------------------------------- actor-critic (R-AC)
+def test_log1m_tanh2_stable_form():
+    """ln(1 - tanh(u)^2) against the naive formula where it is accurate, and its asymptote
+    2 (ln 2 - |u|) where tanh rounds to 1 (the naive form gives -inf there); even in u."""
+    for u in np.linspace(-5, 5, 41):
+        assert learn.log1m_tanh2(u) == pytest.approx(math.log(1.0 - math.tanh(u) ** 2), rel=1e-9, abs=1e-12)
+        assert learn.log1m_tanh2(u) == pytest.approx(learn.log1m_tanh2(-u), rel=1e-13, abs=1e-15)
+    for u in (30.0, -40.0, 300.0):
+        assert learn.log1m_tanh2(u) == pytest.approx(2.0 * (math.log(2.0) - abs(u)), rel=1e-13)
+    assert learn.log1m_tanh2(0.0) == 0.0
+
+
+def test_squash_density_integrates_to_one():
+    """The tanh-squashed Gaussian's log pi (K = 1) is a density on (-1, 1): the integral of
+    exp(log pi(a)) da is 1 (scipy quadrature; a = tanh(z + sigma eps) -> eps = (atanh a - z) / sigma),
+    which fixes the Gaussian constant and the sign of the log-det term; its mean is E[tanh(z + sigma
+    N)] (Gauss-Hermite quadrature); K = 2 log pi is the sum over the two entries."""
+    from scipy import integrate
+    for z, sigma in ((0.3, 0.5), (-1.2, 0.1), (2.0, 1.0)):
+        def dens(a):
+            e = (math.atanh(a) - z) / sigma
+            return math.exp(learn.squash([[z]], [[e]], sigma)[1][0])
+        tot, _ = integrate.quad(dens, -1.0, 1.0, limit=400, points=[math.tanh(z)])
+        assert tot == pytest.approx(1.0, abs=1e-7), (z, sigma)
+        mean, _ = integrate.quad(lambda a: a * dens(a), -1.0, 1.0, limit=400, points=[math.tanh(z)])
+        x, w = np.polynomial.hermite_e.hermegauss(60)
+        assert mean == pytest.approx(float(np.sum(w * np.tanh(z + sigma * x)) / math.sqrt(2 * math.pi)), abs=1e-7)
+    a2, lp2 = learn.squash([[0.1, -0.4]], [[0.5, 1.5]], 0.2)
+    a0, lp0 = learn.squash([[0.1]], [[0.5]], 0.2)
+    a1, lp1 = learn.squash([[-0.4]], [[1.5]], 0.2)
+    assert lp2[0] == pytest.approx(lp0[0] + lp1[0], rel=1e-14) and a2[0] == [a0[0][0], a1[0][0]]
+    a, lp = learn.squash([[0.25, -3.0]])                    # DDPG: a = tanh(z), no density
+    assert a[0] == [math.tanh(0.25), math.tanh(-3.0)] and lp is None
+
+
+def test_dense_forward_and_backward():
+    """dense_forward equals its loops; dense_backward_np's parameter and input gradients of
+    sum g_out . out against central finite differences of dense_forward (a critic with a scalar
+    output and one with 3 outputs)."""
+    rng = np.random.default_rng(17)
+    for dims in ((6, 7, 5, 1), (4, 5, 6, 3)):
+        layers = _tiny_net(rng, dims)
+        B = 5
+        x = rng.normal(size=(B, dims[0]))
+        h1, h2, out = learn.dense_forward(layers, x)
+        np.testing.assert_allclose(out, learn.dense_forward_loops(layers, x.tolist()), rtol=1e-13, atol=1e-14)
+        g = rng.normal(size=out.shape)
+        grads, gx = learn.dense_backward_np(layers, x, h1, h2, g)
+
+        def f():
+            return float(np.sum(g * learn.dense_forward(layers, x)[2]))
+        h = 1e-6
+        for li in range(3):
+            for which in (0, 1):
+                p = layers[li][which]
+                for idx in np.ndindex(p.shape):
+                    old = p[idx]
+                    p[idx] = old + h
+                    fp = f()
+                    p[idx] = old - h
+                    fm = f()
+                    p[idx] = old
+                    assert abs((fp - fm) / (2 * h) - grads[li][which][idx]) <= 1e-6 * max(1.0, abs(fp)), (li, which, idx)
+        for idx in np.ndindex(x.shape):
+            old = x[idx]
+            x[idx] = old + h
+            fp = f()
+            x[idx] = old - h
+            fm = f()
+            x[idx] = old
+            assert abs((fp - fm) / (2 * h) - gx[idx]) <= 1e-6 * max(1.0, abs(fp)), idx
+
+
+def test_critic_targets_spec_cases():
+    """done = 1 -> y = r; alpha = 0 and identical twin critics -> the DDPG-style
+    target; Q1' < Q2' everywhere -> the target uses Q1'; a worked SAC value."""
+    r, q1, q2, lp = [0.5, -1.0], [2.0, 4.0], [3.0, 1.0], [-0.7, 0.2]
+    assert learn.critic_targets(r, [1, 1], q1, 0.99, q2, lp, 0.2) == r
+    assert learn.critic_targets(r, [0, 0], q1, 0.9, q1, lp, 0.0) == learn.critic_targets(r, [0, 0], q1, 0.9)
+    assert learn.critic_targets([0.0], [0], [1.0], 1.0, [5.0]) == [1.0]
+    y = learn.critic_targets(r, [0, 0], q1, 0.9, q2, lp, 0.2)
+    assert y == [0.5 + 0.9 * (2.0 + 0.2 * 0.7), -1.0 + 0.9 * (1.0 - 0.2 * 0.2)]
+    L, g = learn.critic_head([1.0, 3.0], [0.0, 1.0])
+    assert L == 2.5 and g == [1.0, 2.0]
+
+
+def _critic_q(critic, x, a):
+    return learn.dense_forward(critic, np.concatenate([x, a], axis=1))[2][:, 0]
+
+
+def test_actor_heads_against_finite_differences():
+    """The DDPG and SAC actor gradients dL/dz (heads fed with the critics' action gradients from
+    dense_backward_np) against central finite differences of the composed float64 losses
+    L_mu(z) = -(1/B) sum Q(s, tanh z) and L_pi(z) = (1/B) sum [alpha log pi - min(Q1, Q2)](s,
+    tanh(z + sigma eps)); the SAC batch has samples on both sides of the min."""
+    rng = np.random.default_rng(23)
+    B, S, K = 6, 5, 3
+    x = rng.normal(size=(B, S))
+    z = rng.normal(0, 0.8, (B, K))
+    eps = rng.normal(size=(B, K))
+    c1 = _tiny_net(rng, (S + K, 7, 6, 1))
+    c2 = _tiny_net(rng, (S + K, 7, 6, 1))
+    sigma, alpha = 0.3, 0.2
+
+    def qgrad(critic, a):
+        xa = np.concatenate([x, np.asarray(a)], axis=1)
+        h1, h2, out = learn.dense_forward(critic, xa)
+        _, gx = learn.dense_backward_np(critic, xa, h1, h2, np.ones((B, 1)))
+        return out[:, 0], gx[:, S:]
+
+    def l_ddpg(zz):
+        a, _ = learn.squash(zz.tolist())
+        return -float(np.mean(_critic_q(c1, x, np.array(a))))
+
+    def l_sac(zz):
+        a, lp = learn.squash(zz.tolist(), eps.tolist(), sigma)
+        q = np.minimum(_critic_q(c1, x, np.array(a)), _critic_q(c2, x, np.array(a)))
+        return float(np.mean(alpha * np.array(lp) - q))
+
+    a, _ = learn.squash(z.tolist())
+    q, dq = qgrad(c1, a)
+    L, g = learn.ddpg_actor_head(a, q, dq)
+    assert L == pytest.approx(l_ddpg(z), rel=1e-13)
+    a, lp = learn.squash(z.tolist(), eps.tolist(), sigma)
+    q1, _ = qgrad(c1, a)
+    q2, _ = qgrad(c2, a)
+    c2[2][1][0] += float(np.median(q1 - q2))            # shift Q2 so the min switches inside the batch
+    q1, d1 = qgrad(c1, a)
+    q2, d2 = qgrad(c2, a)
+    assert np.any(q1 < q2) and np.any(q2 < q1)
+    Ls, gs = learn.sac_actor_head(a, lp, q1, d1, q2, d2, alpha)
+    assert Ls == pytest.approx(l_sac(z), rel=1e-13)
+    h = 1e-6
+    for fn, gg in ((l_ddpg, g), (l_sac, gs)):
+        for idx in np.ndindex(z.shape):
+            old = z[idx]
+            z[idx] = old + h
+            fp = fn(z)
+            z[idx] = old - h
+            fm = fn(z)
+            z[idx] = old
+            assert abs((fp - fm) / (2 * h) - gg[idx[0]][idx[1]]) <= 1e-7 * max(1.0, abs(fp)), (fn.__name__, idx)
+
+
+def test_critic_loss_gradient_against_finite_differences():
+    """d L_Q / d theta (critic_head's dL/dq through dense_backward_np) against central finite
+    differences of the float64 critic loss with the target held fixed."""
+    rng = np.random.default_rng(29)
+    B, D = 7, 6
+    critic = _tiny_net(rng, (D, 5, 4, 1))
+    x = rng.normal(size=(B, D))
+    y = rng.normal(size=B).tolist()
+
+    def loss():
+        return learn.critic_head(learn.dense_forward(critic, x)[2][:, 0].tolist(), y)[0]
+
+    h1, h2, out = learn.dense_forward(critic, x)
+    _, g = learn.critic_head(out[:, 0].tolist(), y)
+    grads, _ = learn.dense_backward_np(critic, x, h1, h2, np.array(g)[:, None])
+    h = 1e-6
+    for li in range(3):
+        for which in (0, 1):
+            p = critic[li][which]
+            for idx in np.ndindex(p.shape):
+                old = p[idx]
+                p[idx] = old + h
+                lp = loss()
+                p[idx] = old - h
+                lm = loss()
+                p[idx] = old
+                assert abs((lp - lm) / (2 * h) - grads[li][which][idx]) <= 1e-6 * max(1.0, abs(lp)), (li, which, idx)
+
+
+def test_soft_update_cases():
+    """tau = 1 copies the online weights, tau = 0 keeps the target; tau = 0.005 is the float64
+    convex combination rounded once."""
+    t = np.array([1.0, -2.0, 3.5], dtype=np.float32)
+    o = np.array([0.25, 4.0, -1.0], dtype=np.float32)
+    assert np.array_equal(learn.soft_update(t, o, 1.0), o)
+    assert np.array_equal(learn.soft_update(t, o, 0.0), t)
+    assert np.array_equal(learn.soft_update(t, o, 0.005),
+                          np.array([0.005 * 0.25 + 0.995 * 1.0, 0.005 * 4.0 + 0.995 * -2.0,
+                                    0.005 * -1.0 + 0.995 * 3.5], dtype=np.float32))
