@@ -366,6 +366,59 @@ int fin_dqn_grad(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t k_ou
                  int32_t dueling, const float* w2, const float* w3, float* dw1, float* db1, float* dw2, float* db2,
                  float* dw3, float* db3, double* stats, void* stream);
 
+/* The DDPG / SAC updates (the stock ensemble's other members, P:78, P:300,
+ * P:343; reading R-AC, formulas in oracle/learn.py).  A critic Q(s, a) is a
+ * 3-layer ReLU MLP in float32 on the concatenated input [x(s); a] with a linear output (learner-
+ * only; the actor is the rollout's policy).  All arrays are device memory; every call is
+ * stream-ordered, allocates stream-ordered scratch and frees it on the stream; bad arguments
+ * return FIN_E_CONFIG before any launch.
+ *
+ * fin_dense_forward: x f32 [B][in_dim] -> hidden f32 [B][h1 + h2] (h1 = ReLU(W1 x + b1) then h2 =
+ *   ReLU(W2 h1 + b2) per row; NULL: not stored) and out f32 [B][out_dim] = W3 h2 + b3; weights f32
+ *   [out][in] row-major, biases f32 [out].  fp32 CUDA-core contractions (deterministic).
+ * fin_dense_backward: from g_out = dL/d out f32 [B][out_dim] and the forward's x / hidden: the
+ *   parameter gradients dw1 [h1][in_dim], db1, dw2 [h2][h1], db2, dw3 [out_dim][h2], db3 (all six
+ *   or none) and / or g_x = dL/dx f32 [B][in_dim] (NULL: skipped); ReLU derivative 1 where the
+ *   activation is > 0.  Split-K over the batch with partials summed in a fixed order.
+ * fin_concat_obs_action: out f32 [B][in_s + K] = [x (bf16 bits [B][in_s], widened); a f32 [B][K]].
+ * fin_squash: a f32 [B][K] = tanh(z + sigma eps) (eps NULL: tanh z, DDPG's mu(s)); logp f32 [B]
+ *   (needs eps; NULL: skipped) = sum_k [-eps^2 / 2 - ln(sigma sqrt(2 pi)) - ln(1 - tanh(u)^2)], the
+ *   last term in the stable form 2 (ln 2 - u - softplus(-2 u)); float64 arithmetic.
+ * fin_critic_head: y = r + gamma (1 - done) (min(q1_next, q2_next) - alpha logp_next) (q2_next /
+ *   logp_next NULL: omitted -- DDPG), the loss L = mean (q - y)^2 with y held fixed, g_q f32 [B] =
+ *   dL/dq = 2 (q - y) / B, stats f64 [4] = (L, mean q, mean y, B); float64 head.  SAC calls it
+ *   once per critic with the same next-state inputs.
+ * fin_actor_head: DDPG (logp NULL, q2 / dq2 NULL): L = -mean q1, g_z = -(1/B) dq1 (1 - a^2).  SAC
+ *   (logp = log pi(a|s) of the reparameterised sample a = tanh(z + sigma eps)): per sample the
+ *   smaller critic m (Q1 on ties), L = mean (alpha logp - q_m), g_z = (1/B) (2 alpha a - dq_m (1 -
+ *   a^2)).  dq rows (dQ/da, e.g. the last K columns of fin_dense_backward's g_x) have stride ld_dq
+ *   >= K.  stats f64 [4] = (L, mean q_m, mean logp, B).  The actor's parameter gradients follow
+ *   from fin_policy_backward with g_z.
+ * fin_policy_backward: the backward pass of fin_ppo_grad from a given g_z = dL/dz f32 [B][k_out]
+ *   through the policy MLP (inputs and hidden activations of fin_mlp_forward; weights as there).
+ * fin_soft_update: target[i] = f32(tau online[i] + (1 - tau) target[i]) with the products and the
+ *   sum in float64 (0 <= tau <= 1). */
+int fin_dense_forward(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t out_dim, const float* x,
+                      const float* w1, const float* b1, const float* w2, const float* b2, const float* w3,
+                      const float* b3, float* hidden, float* out, void* stream);
+int fin_dense_backward(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t out_dim, const float* x,
+                       const float* hidden, const float* g_out, const float* w1, const float* w2, const float* w3,
+                       float* dw1, float* db1, float* dw2, float* db2, float* dw3, float* db3, float* g_x, void* stream);
+int fin_concat_obs_action(int32_t B, int32_t in_s, const uint16_t* x, int32_t K, const float* a, float* out,
+                          void* stream);
+int fin_squash(int32_t B, int32_t K, const float* z, const float* eps, double sigma, float* a, float* logp,
+               void* stream);
+int fin_critic_head(int32_t B, const float* q, const float* reward, const uint8_t* done, const float* q1_next,
+                    const float* q2_next, const float* logp_next, double gamma, double alpha, float* g_q,
+                    double* stats, void* stream);
+int fin_actor_head(int32_t B, int32_t K, const float* a, const float* logp, const float* q1, const float* dq1,
+                   const float* q2, const float* dq2, int32_t ld_dq, double alpha, float* g_z, double* stats,
+                   void* stream);
+int fin_policy_backward(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t k_out, const uint16_t* x,
+                        const uint16_t* hidden, const float* g_z, const float* w2, const float* w3, float* dw1,
+                        float* db1, float* dw2, float* db2, float* dw3, float* db3, void* stream);
+int fin_soft_update(int64_t n, float* target, const float* online, double tau, void* stream);
+
 /* The learner's view of a rollout's samples (NEXT-4).  A sample is idx = t N + env (step t of
  * the call, local env).  fin_env_clock: the handle's global step counter (host out) -- record it
  * before a rollout: its Philox noise of step t is drawn at t_global + t.

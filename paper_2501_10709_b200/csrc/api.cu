@@ -36,6 +36,25 @@ cudaError_t launch_dqn_grad(int B, int in, int H1, int H2, int O, const uint16_t
                             const float* qt, const float* qo, double gamma, int dueling, const float* w2,
                             const float* w3, float* dw1, float* db1, float* dw2, float* db2, float* dw3, float* db3,
                             double* stats, cudaStream_t s);
+cudaError_t backward(int B, int in, int H1, int H2, int K, const uint16_t* x, const uint16_t* hid, const float* g3,
+                     const float* w2, const float* w3, float* dw1, float* db1, float* dw2, float* db2, float* dw3,
+                     float* db3, cudaStream_t s);
+cudaError_t launch_concat_sa(int B, int S, const uint16_t* x, int K, const float* a, float* out, cudaStream_t s);
+cudaError_t launch_squash(int B, int K, const float* z, const float* eps, double sigma, float* a, float* logp,
+                          cudaStream_t s);
+cudaError_t launch_critic_head(int B, const float* q, const float* r, const uint8_t* done, const float* q1n,
+                               const float* q2n, const float* lpn, double gamma, double alpha, float* g, double* stats,
+                               cudaStream_t s);
+cudaError_t launch_actor_head(int B, int K, const float* a, const float* lp, const float* q1, const float* dq1,
+                              const float* q2, const float* dq2, int ldq, double alpha, float* gz, double* stats,
+                              cudaStream_t s);
+cudaError_t launch_soft_update(int64_t n, float* t, const float* o, double tau, cudaStream_t s);
+cudaError_t dense_forward(int B, int in, int H1, int H2, int O, const float* x, const float* w1, const float* b1,
+                          const float* w2, const float* b2, const float* w3, const float* b3, float* hid, float* out,
+                          cudaStream_t s);
+cudaError_t dense_backward(int B, int in, int H1, int H2, int O, const float* x, const float* hid, const float* g3,
+                           const float* w1, const float* w2, const float* w3, float* dw1, float* db1, float* dw2,
+                           float* db2, float* dw3, float* db3, float* gx, cudaStream_t s);
 cudaError_t launch_gather_obs(const EnvDev& e, const uint16_t* priv, int P, const int32_t* day, const int64_t* idx,
                               int B, uint16_t* x, cudaStream_t s);
 cudaError_t launch_noise_at(uint64_t seed, int64_t off, int N, int64_t t_base, const int64_t* idx, int B, int K,
@@ -1076,6 +1095,102 @@ int fin_dqn_grad(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t k_ou
                                        q_next_online, gamma, dueling, w2, w3, dw1, db1, dw2, db2, dw3, db3, stats,
                                        S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fin_dqn_grad launch");
+  return FIN_OK;
+}
+
+static bool dense_sizes_ok(int32_t B, int32_t in, int32_t h1, int32_t h2, int32_t out) {
+  return B >= 1 && in >= 1 && in <= 8192 && h1 >= 1 && h1 <= 4096 && h2 >= 1 && h2 <= 4096 && out >= 1 && out <= 4096;
+}
+
+int fin_dense_forward(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t out_dim, const float* x,
+                      const float* w1, const float* b1, const float* w2, const float* b2, const float* w3,
+                      const float* b3, float* hidden, float* out, void* stream) {
+  if (!x || !w1 || !b1 || !w2 || !b2 || !w3 || !b3 || !out) return fail(FIN_E_CONFIG, "fin_dense_forward: null argument");
+  if (!dense_sizes_ok(B, in_dim, h1, h2, out_dim)) return fail(FIN_E_CONFIG, "fin_dense_forward: bad sizes");
+  cudaError_t e = fin::dense_forward(B, in_dim, h1, h2, out_dim, x, w1, b1, w2, b2, w3, b3, hidden, out, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_dense_forward launch");
+  return FIN_OK;
+}
+
+int fin_dense_backward(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t out_dim, const float* x,
+                       const float* hidden, const float* g_out, const float* w1, const float* w2, const float* w3,
+                       float* dw1, float* db1, float* dw2, float* db2, float* dw3, float* db3, float* g_x, void* stream) {
+  if (!x || !hidden || !g_out || !w1 || !w2 || !w3) return fail(FIN_E_CONFIG, "fin_dense_backward: null argument");
+  const int np = (dw1 != nullptr) + (db1 != nullptr) + (dw2 != nullptr) + (db2 != nullptr) + (dw3 != nullptr) +
+                 (db3 != nullptr);
+  if (np != 0 && np != 6) return fail(FIN_E_CONFIG, "fin_dense_backward: pass all six gradient tensors or none");
+  if (np == 0 && !g_x) return fail(FIN_E_CONFIG, "fin_dense_backward: nothing to compute");
+  if (!dense_sizes_ok(B, in_dim, h1, h2, out_dim)) return fail(FIN_E_CONFIG, "fin_dense_backward: bad sizes");
+  cudaError_t e = fin::dense_backward(B, in_dim, h1, h2, out_dim, x, hidden, g_out, w1, w2, w3, dw1, db1, dw2, db2, dw3,
+                                      db3, g_x, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_dense_backward launch");
+  return FIN_OK;
+}
+
+int fin_concat_obs_action(int32_t B, int32_t in_s, const uint16_t* x, int32_t K, const float* a, float* out,
+                          void* stream) {
+  if (!x || !a || !out) return fail(FIN_E_CONFIG, "fin_concat_obs_action: null argument");
+  if (B < 1 || in_s < 1 || K < 1) return fail(FIN_E_CONFIG, "fin_concat_obs_action: bad sizes");
+  cudaError_t e = fin::launch_concat_sa(B, in_s, x, K, a, out, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_concat_obs_action launch");
+  return FIN_OK;
+}
+
+int fin_squash(int32_t B, int32_t K, const float* z, const float* eps, double sigma, float* a, float* logp,
+               void* stream) {
+  if (!z || !a) return fail(FIN_E_CONFIG, "fin_squash: null argument");
+  if (B < 1 || K < 1) return fail(FIN_E_CONFIG, "fin_squash: bad sizes");
+  if (eps && !(sigma > 0.0 && std::isfinite(sigma))) return fail(FIN_E_CONFIG, "fin_squash: need sigma > 0");
+  if (logp && !eps) return fail(FIN_E_CONFIG, "fin_squash: the log-density needs eps");
+  cudaError_t e = fin::launch_squash(B, K, z, eps, sigma, a, logp, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_squash launch");
+  return FIN_OK;
+}
+
+int fin_critic_head(int32_t B, const float* q, const float* reward, const uint8_t* done, const float* q1_next,
+                    const float* q2_next, const float* logp_next, double gamma, double alpha, float* g_q,
+                    double* stats, void* stream) {
+  if (!q || !reward || !done || !q1_next || !g_q || !stats) return fail(FIN_E_CONFIG, "fin_critic_head: null argument");
+  if (B < 1) return fail(FIN_E_CONFIG, "fin_critic_head: B must be >= 1");
+  if (!(gamma >= 0.0 && gamma <= 1.0) || !(alpha >= 0.0 && std::isfinite(alpha)))
+    return fail(FIN_E_CONFIG, "fin_critic_head: need 0 <= gamma <= 1 and alpha >= 0");
+  cudaError_t e = fin::launch_critic_head(B, q, reward, done, q1_next, q2_next, logp_next, gamma, alpha, g_q, stats,
+                                          S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_critic_head launch");
+  return FIN_OK;
+}
+
+int fin_actor_head(int32_t B, int32_t K, const float* a, const float* logp, const float* q1, const float* dq1,
+                   const float* q2, const float* dq2, int32_t ld_dq, double alpha, float* g_z, double* stats,
+                   void* stream) {
+  if (!a || !q1 || !dq1 || !g_z || !stats) return fail(FIN_E_CONFIG, "fin_actor_head: null argument");
+  if (B < 1 || K < 1 || ld_dq < K) return fail(FIN_E_CONFIG, "fin_actor_head: bad sizes");
+  if ((q2 == nullptr) != (dq2 == nullptr)) return fail(FIN_E_CONFIG, "fin_actor_head: q2 and dq2 go together");
+  if (q2 && !logp) return fail(FIN_E_CONFIG, "fin_actor_head: twin critics are SAC's (pass logp)");
+  if (!(alpha >= 0.0 && std::isfinite(alpha))) return fail(FIN_E_CONFIG, "fin_actor_head: need alpha >= 0");
+  cudaError_t e = fin::launch_actor_head(B, K, a, logp, q1, dq1, q2, dq2, ld_dq, alpha, g_z, stats, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_actor_head launch");
+  return FIN_OK;
+}
+
+int fin_policy_backward(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t k_out, const uint16_t* x,
+                        const uint16_t* hidden, const float* g_z, const float* w2, const float* w3, float* dw1,
+                        float* db1, float* dw2, float* db2, float* dw3, float* db3, void* stream) {
+  if (!x || !hidden || !g_z || !w2 || !w3 || !dw1 || !db1 || !dw2 || !db2 || !dw3 || !db3)
+    return fail(FIN_E_CONFIG, "fin_policy_backward: null argument");
+  if (B < 1 || in_dim < 1 || in_dim > 4096 || h1 < 1 || h1 > 1024 || h2 < 1 || h2 > 1024 || k_out < 1 || k_out > 64)
+    return fail(FIN_E_CONFIG, "fin_policy_backward: bad sizes");
+  cudaError_t e = fin::backward(B, in_dim, h1, h2, k_out, x, hidden, g_z, w2, w3, dw1, db1, dw2, db2, dw3, db3,
+                                S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_policy_backward launch");
+  return FIN_OK;
+}
+
+int fin_soft_update(int64_t n, float* target, const float* online, double tau, void* stream) {
+  if (!target || !online) return fail(FIN_E_CONFIG, "fin_soft_update: null argument");
+  if (n < 1 || !(tau >= 0.0 && tau <= 1.0)) return fail(FIN_E_CONFIG, "fin_soft_update: need n >= 1, 0 <= tau <= 1");
+  cudaError_t e = fin::launch_soft_update(n, target, online, tau, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fin_soft_update launch");
   return FIN_OK;
 }
 

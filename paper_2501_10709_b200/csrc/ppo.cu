@@ -12,15 +12,13 @@
 #include <cuda_bf16.h>
 
 #include "fin_internal.cuh"
+#include "gemm_f32.cuh"
 #include "philox.cuh"
 
 namespace {
 
-constexpr int kTile = 64, kBK = 16, kThr = 256;
-
-__device__ __forceinline__ float bf16_at(const uint16_t* p, size_t i) {
-  return __uint_as_float((uint32_t)p[i] << 16);
-}
+using gemmf::bf16_at;
+constexpr int kThr = gemmf::kThr;
 
 // ---- head: one thread per sample; stats partials per block [4]: sum L, sum rho, clipped, n
 __global__ void k_ppo_head(int B, int K, const float* __restrict__ z, const float* __restrict__ a,
@@ -159,108 +157,6 @@ __global__ void k_back_out(int B, int K, int H2, int Hs, const float* __restrict
   g2[i] = acc;
 }
 
-// ---- generic fp32 GEMM: C[m][n] = sum_k A(m, k) B(k, n) over k in this split's range
-//   A(m, k) = AKM ? A[k * lda + m] : A[m * lda + k]           (f32)
-//   B(k, n) = BBF ? bf16 Bh[k * ldb + n] : Bf[k * ldb + n]
-//   out: part[split][M][N] (or C when splits == 1), optional mask (bf16 > 0) of C(m, n) at
-//   mask[m * ldm + n] applied when splits == 1
-template <bool AKM, bool BBF>
-__global__ void __launch_bounds__(kThr) k_gemm(int M, int N, int Ktot, int kchunk, const float* __restrict__ A,
-                                               int lda, const float* __restrict__ Bf, const uint16_t* __restrict__ Bh,
-                                               int ldb, float* __restrict__ out, const uint16_t* __restrict__ mask,
-                                               int ldm) {
-  __shared__ float As[kBK][kTile + 4];
-  __shared__ float Bs[kBK][kTile + 4];
-  const int m0 = blockIdx.y * kTile, n0 = blockIdx.x * kTile;
-  const int k0 = blockIdx.z * kchunk, k1 = min(Ktot, k0 + kchunk);
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  float acc[4][4] = {};
-  for (int kb = k0; kb < k1; kb += kBK) {
-    for (int e = threadIdx.x; e < kBK * kTile; e += kThr) {
-      const int kk = e / kTile, mm = e % kTile;   // consecutive threads: consecutive m (AKM) / n
-      const int k = kb + kk;
-      float av = 0.f, bv = 0.f;
-      if (AKM) {
-        if (k < k1 && m0 + mm < M) av = A[(size_t)k * lda + m0 + mm];
-        As[kk][mm] = av;
-      }
-      if (k < k1 && n0 + mm < N) bv = BBF ? bf16_at(Bh, (size_t)k * ldb + n0 + mm) : Bf[(size_t)k * ldb + n0 + mm];
-      Bs[kk][mm] = bv;
-    }
-    if (!AKM) {   // A row-major [M][lda]: consecutive threads read consecutive k of one row
-      for (int e = threadIdx.x; e < kBK * kTile; e += kThr) {
-        const int mm = e / kBK, kk = e % kBK;
-        const int k = kb + kk;
-        As[kk][mm] = (k < k1 && m0 + mm < M) ? A[(size_t)(m0 + mm) * lda + k] : 0.f;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < kBK; ++kk) {
-      float av[4], bv[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) av[r] = As[kk][ty * 4 + r];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) bv[c] = Bs[kk][tx * 4 + c];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(av[r], bv[c], acc[r][c]);
-    }
-    __syncthreads();
-  }
-  float* dst = out + (size_t)blockIdx.z * M * N;
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int m = m0 + ty * 4 + r;
-    if (m >= M) continue;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int n = n0 + tx * 4 + c;
-      if (n >= N) continue;
-      float v = acc[r][c];
-      if (mask && !(bf16_at(mask, (size_t)m * ldm + n) > 0.f)) v = 0.f;
-      dst[(size_t)m * N + n] = v;
-    }
-  }
-}
-
-// fixed-order sum of the split partials: C[i] = sum_z part[z][i]
-__global__ void k_sum_splits(const float* __restrict__ part, int splits, size_t n, float* __restrict__ C) {
-  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  float v = 0.f;
-  for (int z = 0; z < splits; ++z) v += part[(size_t)z * n + i];
-  C[i] = v;
-}
-
-// column sums of g [B][H] (bias gradients), deterministic: block (column group of 32, row chunk)
-// -> 8 row-strided partials per column reduced in a fixed order -> part[chunk][H]; then the chunks
-// summed in order
-constexpr int kColRows = 2048;
-__global__ void k_colsum_part(int B, int H, const float* __restrict__ g, float* __restrict__ part) {
-  __shared__ float red[8][33];
-  const int j = blockIdx.x * 32 + (threadIdx.x & 31), r = threadIdx.x >> 5;
-  const int s0 = blockIdx.y * kColRows, s1 = min(B, s0 + kColRows);
-  float v = 0.f;
-  if (j < H)
-    for (int s = s0 + r; s < s1; s += 8) v += g[(size_t)s * H + j];
-  red[r][threadIdx.x & 31] = v;
-  __syncthreads();
-  if (r == 0 && j < H) {
-    float t = 0.f;
-    for (int q = 0; q < 8; ++q) t += red[q][threadIdx.x & 31];
-    part[(size_t)blockIdx.y * H + j] = t;
-  }
-}
-__global__ void k_colsum_final(int chunks, int H, const float* __restrict__ part, float* __restrict__ out) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= H) return;
-  float v = 0.f;
-  for (int c = 0; c < chunks; ++c) v += part[(size_t)c * H + j];
-  out[j] = v;
-}
-
 __global__ void k_adam(int64_t n, float* __restrict__ th, float* __restrict__ m, float* __restrict__ v,
                        const float* __restrict__ g, float b1, float b2, float lr_c, float inv_c2, float eps) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -271,31 +167,6 @@ __global__ void k_adam(int64_t n, float* __restrict__ th, float* __restrict__ m,
   m[i] = mi;
   v[i] = vi;
   th[i] -= lr_c * mi / (sqrtf(vi * inv_c2) + eps);
-}
-
-int splits_for(int M, int N, int K) {
-  const int tiles = ((M + kTile - 1) / kTile) * ((N + kTile - 1) / kTile);
-  int s = (2 * 148 + tiles - 1) / tiles;                  // ~2 waves of blocks
-  const int maxs = (K + 4 * kBK - 1) / (4 * kBK);          // >= 64 rows of K per split
-  if (s > maxs) s = maxs;
-  return s < 1 ? 1 : s;
-}
-
-// C[M][N] (= sum over K of A^T-ish products) with split-K and deterministic reduction
-template <bool AKM, bool BBF>
-cudaError_t gemm(int M, int N, int K, const float* A, int lda, const float* Bf, const uint16_t* Bh, int ldb, float* C,
-                 const uint16_t* mask, int ldm, float* scratch, cudaStream_t s) {
-  const int splits = mask ? 1 : splits_for(M, N, K);
-  const int kchunk = ((K + splits - 1) / splits + kBK - 1) / kBK * kBK;
-  const int used = (K + kchunk - 1) / kchunk;
-  dim3 grid((N + kTile - 1) / kTile, (M + kTile - 1) / kTile, used);
-  float* out = used == 1 ? C : scratch;
-  k_gemm<AKM, BBF><<<grid, kThr, 0, s>>>(M, N, K, kchunk, A, lda, Bf, Bh, ldb, out, mask, ldm);
-  if (used > 1) {
-    const size_t n = (size_t)M * N;
-    k_sum_splits<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(scratch, used, n, C);
-  }
-  return cudaGetLastError();
 }
 
 // ---- the learner's view of the rollout's samples (sample s = idx[s] = t N + env)
@@ -390,17 +261,10 @@ cudaError_t launch_to_bf16(int64_t n, const float* x, uint16_t* y, cudaStream_t 
 cudaError_t backward(int B, int in, int H1, int H2, int K, const uint16_t* x, const uint16_t* hid, const float* g3,
                      const float* w2, const float* w3, float* dw1, float* db1, float* dw2, float* db2, float* dw3,
                      float* db3, cudaStream_t s) {
+  using namespace gemmf;
   const int Hs = H1 > H2 ? H1 : H2;   // hidden log row width ([B][2][Hs], fin_mlp_forward)
-  auto part_n = [](int M, int N, int Kk) {   // split partials of one weight-gradient GEMM
-    const int sp = splits_for(M, N, Kk);
-    const int kc = ((Kk + sp - 1) / sp + kBK - 1) / kBK * kBK;
-    const int used = (Kk + kc - 1) / kc;
-    return used > 1 ? (size_t)used * M * N : (size_t)1;
-  };
-  size_t scr_n = (size_t)((B + kColRows - 1) / kColRows) * (H1 > H2 ? (H1 > K ? H1 : K) : (H2 > K ? H2 : K));
-  if (part_n(K, H2, B) > scr_n) scr_n = part_n(K, H2, B);
-  if (part_n(H2, H1, B) > scr_n) scr_n = part_n(H2, H1, B);
-  if (part_n(H1, in, B) > scr_n) scr_n = part_n(H1, in, B);
+  size_t scr_n = colsum_floats(B, H1 > H2 ? (H1 > K ? H1 : K) : (H2 > K ? H2 : K));
+  for (size_t q : {split_floats(K, H2, B), split_floats(H2, H1, B), split_floats(H1, in, B)}) scr_n = q > scr_n ? q : scr_n;
   float *g2 = nullptr, *g1 = nullptr, *scr = nullptr;
   cudaError_t e = cudaMallocAsync(&g2, sizeof(float) * (size_t)B * H2, s);
   if (e == cudaSuccess) e = cudaMallocAsync(&g1, sizeof(float) * (size_t)B * H1, s);
@@ -409,19 +273,18 @@ cudaError_t backward(int B, int in, int H1, int H2, int K, const uint16_t* x, co
   const size_t n2 = (size_t)B * H2;
   k_back_out<<<(unsigned)((n2 + 255) / 256), 256, 0, s>>>(B, K, H2, Hs, g3, w3, hid, g2);
   // g1 = (g2 W2) * [h1 > 0]: A = g2 [B][H2] row-major, B = W2 [H2][H1], mask = h1 (row stride 2 Hs)
-  e = gemm<false, false>(B, H1, H2, g2, H2, w2, nullptr, H1, g1, hid, 2 * Hs, scr, s);
+  e = gemm<false, kBF32, kMaskBF16>(B, H1, H2, g2, H2, w2, nullptr, H1, g1, hid, 2 * Hs, nullptr, 0, scr, s);
   // weight gradients: A = g_l [B][M] (k = sample: AKM), B = activations [B][N]
-  if (e == cudaSuccess) e = gemm<true, true>(K, H2, B, g3, K, nullptr, hid + Hs, 2 * Hs, dw3, nullptr, 0, scr, s);
-  if (e == cudaSuccess) e = gemm<true, true>(H2, H1, B, g2, H2, nullptr, hid, 2 * Hs, dw2, nullptr, 0, scr, s);
-  if (e == cudaSuccess) e = gemm<true, true>(H1, in, B, g1, H1, nullptr, x, in, dw1, nullptr, 0, scr, s);
-  const int chunks = (B + kColRows - 1) / kColRows;
-  const float* gs[3] = {g3, g2, g1};
-  float* bs[3] = {db3, db2, db1};
-  const int hs[3] = {K, H2, H1};
-  for (int l = 0; l < 3; ++l) {   // (scr is free again: the split partials were reduced above)
-    k_colsum_part<<<dim3((hs[l] + 31) / 32, chunks), 256, 0, s>>>(B, hs[l], gs[l], scr);
-    k_colsum_final<<<(hs[l] + 127) / 128, 128, 0, s>>>(chunks, hs[l], scr, bs[l]);
-  }
+  if (e == cudaSuccess)
+    e = gemm<true, kBBF16, kMaskNone>(K, H2, B, g3, K, nullptr, hid + Hs, 2 * Hs, dw3, nullptr, 0, nullptr, 0, scr, s);
+  if (e == cudaSuccess)
+    e = gemm<true, kBBF16, kMaskNone>(H2, H1, B, g2, H2, nullptr, hid, 2 * Hs, dw2, nullptr, 0, nullptr, 0, scr, s);
+  if (e == cudaSuccess)
+    e = gemm<true, kBBF16, kMaskNone>(H1, in, B, g1, H1, nullptr, x, in, dw1, nullptr, 0, nullptr, 0, scr, s);
+  // (scr is free again: the split partials were reduced above)
+  colsum(B, K, g3, K, db3, scr, s);
+  colsum(B, H2, g2, H2, db2, scr, s);
+  colsum(B, H1, g1, H1, db1, scr, s);
   if (e == cudaSuccess) e = cudaGetLastError();
   cudaFreeAsync(g2, s);
   cudaFreeAsync(g1, s);

@@ -53,7 +53,8 @@ EXPORTS = ("fin_env_create", "fin_env_reset", "fin_env_step", "fin_env_get_state
            "fin_philox_normals", "fin_member_weights", "fin_market_prepare", "fin_crypto_market", "fin_gae", "fin_kl_diversity", "fin_last_error", "fin_abi_version", "fin_device_check",
            "fin_debug_trace", "fin_env_counters", "fin_stock_market", "fin_ppo_grad", "fin_adam_step",
            "fin_env_clock", "fin_gather_observations", "fin_rollout_noise", "fin_ppo_prepare", "fin_policy_load",
-           "fin_dqn_grad")
+           "fin_dqn_grad", "fin_dense_forward", "fin_dense_backward", "fin_concat_obs_action", "fin_squash",
+           "fin_critic_head", "fin_actor_head", "fin_policy_backward", "fin_soft_update")
 
 
 class FinError(RuntimeError):
@@ -124,6 +125,14 @@ _sig = {
                          C.c_int),
     "fin_market_prepare": ([_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_double,
                             C.c_uint64, _P, _P, _P], C.c_int),
+    "fin_dense_forward": ([C.c_int32] * 5 + [_P] * 10, C.c_int),
+    "fin_dense_backward": ([C.c_int32] * 5 + [_P] * 14, C.c_int),
+    "fin_concat_obs_action": ([C.c_int32, C.c_int32, _P, C.c_int32, _P, _P, _P], C.c_int),
+    "fin_squash": ([C.c_int32, C.c_int32, _P, _P, C.c_double, _P, _P, _P], C.c_int),
+    "fin_critic_head": ([C.c_int32] + [_P] * 6 + [C.c_double, C.c_double, _P, _P, _P], C.c_int),
+    "fin_actor_head": ([C.c_int32, C.c_int32] + [_P] * 6 + [C.c_int32, C.c_double, _P, _P, _P], C.c_int),
+    "fin_policy_backward": ([C.c_int32] * 5 + [_P] * 12, C.c_int),
+    "fin_soft_update": ([C.c_int64, _P, _P, C.c_double, _P], C.c_int),
     "fin_last_error": ([], C.c_char_p),
     "fin_abi_version": ([], C.c_int),
     "fin_device_check": ([C.c_int32], C.c_int),
@@ -154,6 +163,16 @@ def _ptr(t, dtype=None, what=""):
         raise TypeError(f"{what}: dtype {t.dtype}, expected {dtype}")
     if not t.is_contiguous():
         raise ValueError(f"{what}: tensor must be contiguous")
+    return t.data_ptr()
+
+
+def _ptr_rows(t, dtype, what=""):
+    """Device pointer of a 2-D CUDA tensor view whose rows are contiguous (any row stride)."""
+    if t is None:
+        return None
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != dtype or t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError(f"{what}: expected a 2-D {dtype} CUDA tensor with contiguous rows")
     return t.data_ptr()
 
 
@@ -532,6 +551,141 @@ def fin_dqn_grad(x_bf16_bits, hidden, out, action, reward, done, q_next_target, 
                              _ptr(q_next_online, f32, "q_next_online"), float(gamma), int(bool(dueling)),
                              _ptr(w2, f32, "w2"), _ptr(w3, f32, "w3"), *p, _ptr(stats, torch.float64, "stats"),
                              _stream(stream)), "fin_dqn_grad")
+
+
+# ---------------------------------------------------------------- actor-critic updates (R-AC)
+def _grad_shapes(dims):
+    return [((dims[1], dims[0]), (dims[1],)), ((dims[2], dims[1]), (dims[2],)), ((dims[3], dims[2]), (dims[3],))]
+
+
+def _check_grads(grads, dims, where):
+    for (dw, db), (sw, sb) in zip(grads, _grad_shapes(dims)):
+        if tuple(dw.shape) != sw or tuple(db.shape) != sb:
+            raise ValueError(f"{where}: gradient shapes must be {_grad_shapes(dims)}")
+
+
+def fin_dense_forward(x, layers, out, hidden=None, stream=None) -> None:
+    """Critic forward (include/fin.h): x f32 [B][in], layers = [(W f32 [out][in], b f32 [out])] x 3
+    (device), out f32 [B][O], hidden f32 [B][h1 + h2] or None."""
+    import torch
+    B, in_dim = int(x.shape[0]), int(x.shape[1])
+    dims = [in_dim] + [int(w.shape[0]) for w, _ in layers]
+    if len(layers) != 3 or any(tuple(w.shape) != (dims[i + 1], dims[i]) or tuple(b.shape) != (dims[i + 1],)
+                               for i, (w, b) in enumerate(layers)):
+        raise ValueError("fin_dense_forward: three layers [out][in] / [out] chained from x's width")
+    if tuple(out.shape) != (B, dims[3]):
+        raise ValueError("fin_dense_forward: out must be [B][O]")
+    _need(hidden, B * (dims[1] + dims[2]), "hidden [B][h1 + h2]")
+    f32 = torch.float32
+    wb = [_ptr(t, f32, "layer") for pair in layers for t in pair]
+    _check(_lib.fin_dense_forward(B, *dims, _ptr(x, f32, "x"), *wb, _ptr(hidden, f32, "hidden"), _ptr(out, f32, "out"),
+                                  _stream(stream)), "fin_dense_forward")
+
+
+def fin_dense_backward(x, hidden, g_out, weights, grads=None, g_x=None, stream=None) -> None:
+    """Critic backward: weights = [W1, W2, W3] f32 (device), grads = [(dw, db)] x 3 or None, g_x f32
+    [B][in] or None."""
+    import torch
+    B, in_dim = int(x.shape[0]), int(x.shape[1])
+    dims = [in_dim] + [int(w.shape[0]) for w in weights]
+    if len(weights) != 3 or any(tuple(w.shape) != (dims[i + 1], dims[i]) for i, w in enumerate(weights)):
+        raise ValueError("fin_dense_backward: three weights [out][in] chained from x's width")
+    if tuple(g_out.shape) != (B, dims[3]):
+        raise ValueError("fin_dense_backward: g_out must be [B][O]")
+    _need(hidden, B * (dims[1] + dims[2]), "hidden [B][h1 + h2]")
+    if grads is not None:
+        _check_grads(grads, dims, "fin_dense_backward")
+    if g_x is not None and tuple(g_x.shape) != (B, in_dim):
+        raise ValueError("fin_dense_backward: g_x must be [B][in]")
+    f32 = torch.float32
+    p = [None] * 6 if grads is None else [_ptr(t, f32, "grad") for pair in grads for t in pair]
+    _check(_lib.fin_dense_backward(B, *dims, _ptr(x, f32, "x"), _ptr(hidden, f32, "hidden"), _ptr(g_out, f32, "g_out"),
+                                   *[_ptr(w, f32, "w") for w in weights], *p, _ptr(g_x, f32, "g_x"),
+                                   _stream(stream)), "fin_dense_backward")
+
+
+def fin_concat_obs_action(x_bf16_bits, a, out, stream=None) -> None:
+    """out f32 [B][S + K] = [x (bf16 bits [B][S]); a f32 [B][K]]."""
+    import torch
+    B, S = int(x_bf16_bits.shape[0]), int(x_bf16_bits.shape[1])
+    K = int(a.shape[1])
+    if int(a.shape[0]) != B or tuple(out.shape) != (B, S + K):
+        raise ValueError("fin_concat_obs_action: a [B][K], out [B][S + K]")
+    _check(_lib.fin_concat_obs_action(B, S, _ptr(x_bf16_bits, torch.int16, "x"), K, _ptr(a, torch.float32, "a"),
+                                      _ptr(out, torch.float32, "out"), _stream(stream)), "fin_concat_obs_action")
+
+
+def fin_squash(z, a, eps=None, logp=None, sigma: float = 0.1, stream=None) -> None:
+    """a = tanh(z + sigma eps) (eps None: tanh z) and log pi(a|s) into logp [B] (needs eps)."""
+    import torch
+    B, K = int(z.shape[0]), int(z.shape[1])
+    _need(a, B * K, "a [B][K]")
+    _need(eps, B * K, "eps [B][K]")
+    _need(logp, B, "logp [B]")
+    f32 = torch.float32
+    _check(_lib.fin_squash(B, K, _ptr(z, f32, "z"), _ptr(eps, f32, "eps"), float(sigma), _ptr(a, f32, "a"),
+                           _ptr(logp, f32, "logp"), _stream(stream)), "fin_squash")
+
+
+def fin_critic_head(q, reward, done, q1_next, g_q, stats, q2_next=None, logp_next=None, gamma: float = 0.99,
+                    alpha: float = 0.2, stream=None) -> None:
+    """Critic target and squared TD loss: g_q f32 [B] = dL/dq; stats f64 [4] (L, mean q, mean y, B)."""
+    import torch
+    B = int(q.numel())
+    for t, w in ((reward, "reward"), (done, "done"), (q1_next, "q1_next"), (g_q, "g_q"), (q2_next, "q2_next"),
+                 (logp_next, "logp_next")):
+        _need(t, B, w)
+    _need(stats, 4, "stats")
+    f32 = torch.float32
+    _check(_lib.fin_critic_head(B, _ptr(q, f32, "q"), _ptr(reward, f32, "reward"), _ptr(done, torch.uint8, "done"),
+                                _ptr(q1_next, f32, "q1_next"), _ptr(q2_next, f32, "q2_next"),
+                                _ptr(logp_next, f32, "logp_next"), float(gamma), float(alpha), _ptr(g_q, f32, "g_q"),
+                                _ptr(stats, torch.float64, "stats"), _stream(stream)), "fin_critic_head")
+
+
+def fin_actor_head(a, q1, dq1, g_z, stats, logp=None, q2=None, dq2=None, alpha: float = 0.2, stream=None) -> None:
+    """DDPG (logp None) or SAC actor head: g_z f32 [B][K] = dL/dz; dq1 / dq2 [B][ld] views whose first
+    K columns are dQ/da (e.g. g_x[:, S:]); stats f64 [4] (L, mean q_min, mean logp, B)."""
+    import torch
+    B, K = int(a.shape[0]), int(a.shape[1])
+    ld = int(dq1.stride(0))
+    for d in (dq1, dq2):
+        if d is not None and (int(d.shape[0]) != B or int(d.shape[1]) != K or int(d.stride(1)) != 1 or int(d.stride(0)) != ld):
+            raise ValueError("fin_actor_head: dq1 / dq2 must be [B][K] row views with one row stride")
+    for t, w in ((q1, "q1"), (q2, "q2"), (logp, "logp")):
+        _need(t, B, w)
+    _need(g_z, B * K, "g_z [B][K]")
+    f32 = torch.float32
+    _check(_lib.fin_actor_head(B, K, _ptr(a, f32, "a"), _ptr(logp, f32, "logp"), _ptr(q1, f32, "q1"),
+                               _ptr_rows(dq1, f32, "dq1"), _ptr(q2, f32, "q2"), _ptr_rows(dq2, f32, "dq2"), ld, float(alpha),
+                               _ptr(g_z, f32, "g_z"), _ptr(stats, torch.float64, "stats"), _stream(stream)),
+           "fin_actor_head")
+
+
+def fin_policy_backward(x_bf16_bits, hidden, g_z, w2, w3, grads, stream=None) -> None:
+    """The policy MLP's backward from g_z f32 [B][k_out] (fin_ppo_grad's pass)."""
+    import torch
+    B, in_dim = int(x_bf16_bits.shape[0]), int(x_bf16_bits.shape[1])
+    k_out = int(g_z.shape[1])
+    h2, h1 = int(w2.shape[0]), int(w2.shape[1])
+    if tuple(w3.shape) != (k_out, h2) or int(g_z.shape[0]) != B or int(hidden.shape[0]) != B:
+        raise ValueError("fin_policy_backward: inconsistent shapes")
+    _need(hidden, B * 2 * max(h1, h2), "hidden [B][2][H]")
+    _check_grads(grads, (in_dim, h1, h2, k_out), "fin_policy_backward")
+    f32 = torch.float32
+    p = [_ptr(t, f32, "grad") for pair in grads for t in pair]
+    _check(_lib.fin_policy_backward(B, in_dim, h1, h2, k_out, _ptr(x_bf16_bits, torch.int16, "x"),
+                                    _ptr(hidden, torch.int16, "hidden"), _ptr(g_z, f32, "g_z"), _ptr(w2, f32, "w2"),
+                                    _ptr(w3, f32, "w3"), *p, _stream(stream)), "fin_policy_backward")
+
+
+def fin_soft_update(target, online, tau: float = 0.005, stream=None) -> None:
+    """target <- f32(tau online + (1 - tau) target) (float64 arithmetic), flat f32 device tensors."""
+    import torch
+    n = int(target.numel())
+    _need(online, n, "online")
+    _check(_lib.fin_soft_update(n, _ptr(target, torch.float32, "target"), _ptr(online, torch.float32, "online"),
+                                float(tau), _stream(stream)), "fin_soft_update")
 
 
 def fin_env_clock(env: Env) -> int:
