@@ -591,6 +591,7 @@ def consumer(fin, torch):
     res["kl_diversity_3x65536x30"] = {"ms": a.elapsed_time(b)}
     res["ppo_step"] = ppo_step(fin, torch)
     res["ppo_iteration"] = ppo_iteration(fin, torch)
+    res["actor_critic"] = {f"{kind}_B{B}": ac_update(fin, torch, kind, B) for kind in ("ddpg", "sac") for B in (64, 65536)}
     return res
 
 
@@ -651,6 +652,48 @@ def ppo_iteration(fin, torch, B=65536):
             "policy_load_ms_host_wall": load_ms, "obs_log_bytes_per_env_step": 64 + 4,
             "note": "learner = gather + forward + noise + prepare + PPO gradient + Adam; policy_load repacks "
                     "the bf16 image on the host (synchronous)"}
+
+
+def ac_update(fin, torch, kind: str, B: int):
+    """One DDPG or SAC update (reading R-AC; learner.ddpg_update / sac_update) on B samples of the C1
+    actor (301-256-256-30, tcgen05 forward) with 331-256-256-1 fp32 critics (two for SAC) and their
+    targets: forwards, float64 heads, backwards, Adam, soft updates and the actor's fin_policy_load
+    (a host repack that synchronises the stream).  B = 64 is the paper's batch size."""
+    import numpy as np
+    from paper_2501_10709_b200 import learner
+    from synth import policy as spol
+    sac = kind == "sac"
+    layers = spol.kaiming_bf16(spol.STOCK_DIMS, 0)
+    k = fin.FIN_SAC_SQUASH if sac else fin.FIN_DDPG_OU
+    actor = learner.Actor(k, layers)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    batch = dict(x=torch.randn((B, 301), device="cuda", generator=g).to(torch.bfloat16).view(torch.int16),
+                 x_next=torch.randn((B, 301), device="cuda", generator=g).to(torch.bfloat16).view(torch.int16),
+                 a=torch.tanh(torch.randn((B, 30), device="cuda", generator=g)),
+                 reward=torch.randn(B, device="cuda", generator=g), done=torch.zeros(B, dtype=torch.uint8, device="cuda"))
+    if sac:
+        batch["eps"] = torch.randn((B, 30), device="cuda", generator=g)
+        batch["eps_next"] = torch.randn((B, 30), device="cuda", generator=g)
+        critics = [learner.DenseNet((331, 256, 256, 1), s) for s in (1, 2)]
+        targs = [c.copy() for c in critics]
+        step = lambda: learner.sac_update(actor, critics, targs, batch)
+    else:
+        actor_t = learner.Actor(k, layers)
+        critic = learner.DenseNet((331, 256, 256, 1), 1)
+        targ = critic.copy()
+        step = lambda: learner.ddpg_update(actor, actor_t, critic, targ, batch)
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    return {"samples": B, "ms_per_update": ms, "samples_per_s": B / (ms / 1e3),
+            "note": "fp32 CUDA-core critics; includes fin_policy_load (host repack, synchronous)"}
 
 
 def ppo_step(fin, torch, B=65536):
