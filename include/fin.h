@@ -380,7 +380,8 @@ int fin_dqn_grad(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_t k_ou
  *   parameter gradients dw1 [h1][in_dim], db1, dw2 [h2][h1], db2, dw3 [out_dim][h2], db3 (all six
  *   or none) and / or g_x = dL/dx f32 [B][in_dim] (NULL: skipped); ReLU derivative 1 where the
  *   activation is > 0.  Split-K over the batch with partials summed in a fixed order.
- * fin_concat_obs_action: out f32 [B][in_s + K] = [x (bf16 bits [B][in_s], widened); a f32 [B][K]].
+ * fin_concat_obs_action: out f32 [B][in_s + K] = [x (bf16 bits [B][in_s], widened); a f32 [B][K]]
+ *   (K = 0, a NULL: the widened observation alone -- the input of a value net V(s)).
  * fin_squash: a f32 [B][K] = tanh(z + sigma eps) (eps NULL: tanh z, DDPG's mu(s)); logp f32 [B]
  *   (needs eps; NULL: skipped) = sum_k [-eps^2 / 2 - ln(sigma sqrt(2 pi)) - ln(1 - tanh(u)^2)], the
  *   last term in the stable form 2 (ln 2 - u - softplus(-2 u)); float64 arithmetic.

@@ -1129,8 +1129,8 @@ int fin_dense_backward(int32_t B, int32_t in_dim, int32_t h1, int32_t h2, int32_
 
 int fin_concat_obs_action(int32_t B, int32_t in_s, const uint16_t* x, int32_t K, const float* a, float* out,
                           void* stream) {
-  if (!x || !a || !out) return fail(FIN_E_CONFIG, "fin_concat_obs_action: null argument");
-  if (B < 1 || in_s < 1 || K < 1) return fail(FIN_E_CONFIG, "fin_concat_obs_action: bad sizes");
+  if (!x || (!a && K > 0) || !out) return fail(FIN_E_CONFIG, "fin_concat_obs_action: null argument");
+  if (B < 1 || in_s < 1 || K < 0) return fail(FIN_E_CONFIG, "fin_concat_obs_action: bad sizes");
   cudaError_t e = fin::launch_concat_sa(B, in_s, x, K, a, out, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fin_concat_obs_action launch");
   return FIN_OK;

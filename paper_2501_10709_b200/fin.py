@@ -605,11 +605,11 @@ def fin_dense_backward(x, hidden, g_out, weights, grads=None, g_x=None, stream=N
 
 
 def fin_concat_obs_action(x_bf16_bits, a, out, stream=None) -> None:
-    """out f32 [B][S + K] = [x (bf16 bits [B][S]); a f32 [B][K]]."""
+    """out f32 [B][S + K] = [x (bf16 bits [B][S]); a f32 [B][K]] (a None: the widened x alone)."""
     import torch
     B, S = int(x_bf16_bits.shape[0]), int(x_bf16_bits.shape[1])
-    K = int(a.shape[1])
-    if int(a.shape[0]) != B or tuple(out.shape) != (B, S + K):
+    K = 0 if a is None else int(a.shape[1])
+    if (a is not None and int(a.shape[0]) != B) or tuple(out.shape) != (B, S + K):
         raise ValueError("fin_concat_obs_action: a [B][K], out [B][S + K]")
     _check(_lib.fin_concat_obs_action(B, S, _ptr(x_bf16_bits, torch.int16, "x"), K, _ptr(a, torch.float32, "a"),
                                       _ptr(out, torch.float32, "out"), _stream(stream)), "fin_concat_obs_action")

@@ -229,3 +229,24 @@ def sac_update(actor: Actor, critics, critics_targ, batch, sigma: float = 0.1, a
     for t, c in zip(critics_targ, critics):
         t.soft_update_from(c, tau, stream=stream)
     return st_c[0], st_c[1], st_a
+
+
+def value_update(vnet: DenseNet, x, returns, lr: float = 3e-4, stream=None):
+    """The PPO member's value regression (the value MSE of its loss; reading R-AC's
+    critic head with gamma = 0, so y = the GAE return R): V(s) a float32 DenseNet on the widened
+    observation, L_V = mean (V(s) - R)^2, one Adam step.  Returns the device stats [4] (L, mean V,
+    mean R, B)."""
+    import torch
+    B, S = int(x.shape[0]), int(x.shape[1])
+    xf = _zeros((B, S), torch.float32)
+    fin.fin_concat_obs_action(x, None, xf, stream=stream)
+    hid = _zeros((B, vnet.dims[1] + vnet.dims[2]), torch.float32)
+    v = _zeros((B, 1), torch.float32)
+    vnet.forward(xf, v, hid, stream=stream)
+    g = _zeros(B, torch.float32)
+    st = _zeros(4, torch.float64)
+    zero = _zeros(B, torch.uint8)
+    fin.fin_critic_head(v.view(-1), returns, zero, returns, g, st, gamma=0.0, alpha=0.0, stream=stream)
+    fin.fin_dense_backward(xf, hid, g.view(B, 1), vnet.weights(), grads=vnet.grads, stream=stream)
+    vnet.adam(lr, stream=stream)
+    return st

@@ -286,3 +286,36 @@ def test_update_end_to_end(variant):
     else:
         learner.ddpg_update(actor, actor_targ, critics[0], targs[0], batch)
     torch.cuda.synchronize()
+
+
+def test_value_update_matches_oracle():
+    """PPO's value regression (learner.value_update): V(s) on the widened observation, the squared
+    error to the returns (critic head with gamma = 0), its gradient against the oracle's critic_head +
+    dense_backward_np on the device's activations (checked before the Adam step), the loss then lower."""
+    import torch
+    from oracle import mlp as omlp
+    from paper_2501_10709_b200 import fin, learner
+    rng = np.random.default_rng(50)
+    B = 900
+    xb = _obs(rng, B)
+    x = dev(xb.view(np.int16))
+    R = dev(rng.normal(0, 2, B).astype(np.float32))
+    v = learner.DenseNet((S, 256, 256, 1), 9)
+    xf = zeros((B, S), torch.float32)
+    fin.fin_concat_obs_action(x, None, xf)
+    assert np.array_equal(host(xf).astype(np.float64), omlp.bf16_bits_to_f64(xb))
+    hid = zeros((B, 512), torch.float32)
+    out = zeros((B, 1), torch.float32)
+    v.forward(xf, out, hid)
+    L64 = _layers64(v)
+    L0, g = olearn.critic_head(host(out)[:, 0].astype(np.float64), host(R).astype(np.float64))
+    hd = host(hid).astype(np.float64)
+    ref, _ = olearn.dense_backward_np(L64, omlp.bf16_bits_to_f64(xb), hd[:, :256], hd[:, 256:], np.array(g)[:, None])
+    st = learner.value_update(v, x, R, lr=1e-5)
+    assert host(st)[0] == pytest.approx(L0, rel=1e-9)
+    for (dw, db), (rw, rb) in zip(v.grads, ref):
+        _close(host(dw), rw)
+        _close(host(db), rb)
+    v.forward(xf, out)
+    L1, _ = olearn.critic_head(host(out)[:, 0].astype(np.float64), host(R).astype(np.float64))
+    assert L1 < L0
