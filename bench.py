@@ -645,13 +645,17 @@ def ppo_iteration(fin, torch, B=65536):
     learner()
     b1.record()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    learner_ms = b0.elapsed_time(b1)
+    fin.fin_policy_load(pol, w, bias)   # first call: builds the handle's gather table
+    torch.cuda.synchronize()
+    b0.record()
     fin.fin_policy_load(pol, w, bias)
-    load_ms = 1e3 * (time.perf_counter() - t0)
-    return {"rollout_ms_with_obs_logs": a0.elapsed_time(a1), "minibatch": B, "learner_ms": b0.elapsed_time(b1),
-            "policy_load_ms_host_wall": load_ms, "obs_log_bytes_per_env_step": 64 + 4,
-            "note": "learner = gather + forward + noise + prepare + PPO gradient + Adam; policy_load repacks "
-                    "the bf16 image on the host (synchronous)"}
+    b1.record()
+    torch.cuda.synchronize()
+    return {"rollout_ms_with_obs_logs": a0.elapsed_time(a1), "minibatch": B, "learner_ms": learner_ms,
+            "policy_load_ms": b0.elapsed_time(b1), "obs_log_bytes_per_env_step": 64 + 4,
+            "note": "learner = gather + forward + noise + prepare + PPO gradient + Adam; policy_load gathers the "
+                    "bf16 tcgen05 image on the device (stream-ordered)"}
 
 
 def ac_update(fin, torch, kind: str, B: int):
@@ -693,7 +697,7 @@ def ac_update(fin, torch, kind: str, B: int):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 5
     return {"samples": B, "ms_per_update": ms, "samples_per_s": B / (ms / 1e3),
-            "note": "fp32 CUDA-core critics; includes fin_policy_load (host repack, synchronous)"}
+            "note": "fp32 CUDA-core critics; includes the actor's fin_policy_load (device gather)"}
 
 
 def ppo_step(fin, torch, B=65536):

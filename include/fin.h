@@ -441,10 +441,14 @@ int fin_ppo_prepare(int32_t B, int32_t K, const float* z_old, const float* eps, 
                     void* stream);
 
 /* Replace a policy's weights (same network) with device f32 values w[l] [dims[l+1]][dims[l]]
- * and optional biases b[l] [dims[l+1]] (host arrays of DEVICE pointers; NULL bias = 0): rounded
- * to bf16 (nearest even) on the device and repacked into the tcgen05 image; the policy gets a
- * new id, so envs recompute their cached layer-1 term.  Waits for the policy's last use first;
- * synchronises the stream (the learner's update -> the next rollout). */
+ * and optional biases b[l] [dims[l+1]] (host arrays of DEVICE pointers; NULL bias = 0): gathered
+ * into the tcgen05 image on the device (bf16 round to nearest even) through a per-handle index
+ * table of the layout (built and uploaded by the first call, synchronously); stream-ordered after
+ * the policy's last use (its event), no host synchronisation.  A given bias is added even if it is
+ * all zero (fin_policy_create skips all-zero biases: the results differ at most in the sign of a
+ * zero output).  Non-finite values are not checked here (rollouts flag FIN_FLAG_NONFINITE).  The
+ * policy gets a new id, so envs recompute their cached layer-1 term.  The caller orders the next
+ * use on another stream after this one. */
 int fin_policy_load(fin_policy* policy, const float* const* w, const float* const* b, void* stream);
 
 /* One Adam step (Kingma & Ba) on n parameters (device f32 theta, m, v updated in place; grad the

@@ -62,6 +62,8 @@ cudaError_t launch_noise_at(uint64_t seed, int64_t off, int N, int64_t t_base, c
 cudaError_t launch_ppo_prepare(int B, int K, const float* z, const float* eps, double sigma, float* a, float* logp,
                                cudaStream_t s);
 cudaError_t launch_to_bf16(int64_t n, const float* x, uint16_t* y, cudaStream_t s);
+cudaError_t launch_policy_gather(int64_t n_pack, const int32_t* pack_src, const float* const (&w)[4], uint16_t* wpack,
+                                 int64_t n_w1s, const int32_t* w1s_src, float* w1s, cudaStream_t s);
 cudaError_t launch_gae(const float* rew, const float* val, const uint8_t* done, int T, int N, double gamma,
                        double lam, int normalise, float* adv, float* ret, cudaStream_t s);
 cudaError_t launch_kl_diversity(const float* out, int M, int B, int K, int kind, double sigma, double* D,
@@ -106,6 +108,9 @@ struct fin_policy {
   float* w1s_t;                // stock: device [S][HID] shared columns of W1 (exact bf16 values), else null
   bool b1_in_z1s;              // factored stock net with a non-zero layer-1 bias: folded into z1s (f64)
   uint64_t uid;                // process-unique id (keys the env's z1s cache; addresses can be reused)
+  int32_t* pack_src = nullptr; // device gather table of fin_policy_load: per bf16 of wpack (l << 24 | index) or -1
+  int32_t* w1s_src = nullptr;  // ... per float of w1s_t: the index into W1, or -1
+  int64_t n_pack = 0, n_w1s = 0;
   cudaEvent_t used;            // recorded on the stream of every call that reads the policy (destroy waits on it)
 };
 
@@ -236,6 +241,48 @@ void pack_member(const int32_t* dims, const uint16_t* const* w, const float* con
     if (bias && bias[l])
       for (int n = 0; n < dims[l + 1]; ++n) bp[off + n] = bias[l][n];
   }
+}
+
+// the same layout as a gather table (fin_policy_load on the device): src[i] = (l << 24) | (n in_l + k)
+// for bf16 i of the image, -1 for padding; w1s_src[sidx H + n] = n in_0 + shared_col(sidx); bias_off[l]
+template <class Plan, class Obs>
+void index_member(const int32_t* dims, std::vector<int32_t>& src, std::vector<int32_t>& w1s_src,
+                  std::vector<int>& bias_off, int& bias_floats) {
+  constexpr bool kFactored = !std::is_void<Obs>::value;
+  src.assign(Plan::kMemberBytes / 2, -1);
+  for (int s = 0; s < Plan::kStages; ++s) {
+    const int l = Plan::layer_of(s), j0 = Plan::j0_of(s), nks = Plan::nks_of(s);
+    const int kt = nks * 16, rows = Plan::nrows(l);
+    const int in_l = dims[l], out_l = dims[l + 1];
+    const size_t base = Plan::offset_of(s);
+    for (int n = 0; n < rows; ++n)
+      for (int kk = 0; kk < kt; ++kk) {
+        int k = j0 * 16 + kk;
+        if constexpr (kFactored) {
+          if (l == 0) k = k < Obs::kEnv ? Obs::env_col(k) : in_l;
+        }
+        if (n < out_l && k < in_l) src[(base + tc_cm_offset(n, kk, kt)) / 2] = (l << 24) | (n * in_l + k);
+      }
+  }
+  w1s_src.clear();
+  if constexpr (kFactored) {
+    const int H = dims[1];
+    w1s_src.assign((size_t)Obs::kShared * H, -1);
+    for (int sidx = 0; sidx < Obs::kShared; ++sidx)
+      for (int n = 0; n < H; ++n) w1s_src[(size_t)sidx * H + n] = n * dims[0] + Obs::shared_col(sidx);
+  }
+  bias_off.assign(Plan::kNL, 0);
+  for (int l = 0; l < Plan::kNL; ++l) bias_off[l] = Plan::bias_off(l);
+  bias_floats = Plan::kBiasFloats;
+}
+
+void index_any(int net, const int32_t* dims, std::vector<int32_t>& src, std::vector<int32_t>& w1s_src,
+               std::vector<int>& bias_off, int& bias_floats) {
+  if (net == 0) index_member<PlanStockC1, ObsC1>(dims, src, w1s_src, bias_off, bias_floats);
+  else if (net == 1) index_member<PlanStockSmall, ObsSmall>(dims, src, w1s_src, bias_off, bias_floats);
+  else if (net == 3) index_member<PlanStockPaper, ObsC1>(dims, src, w1s_src, bias_off, bias_floats);
+  else if (net == 4) index_member<PlanCryptoPaper, void>(dims, src, w1s_src, bias_off, bias_floats);
+  else index_member<PlanCrypto, void>(dims, src, w1s_src, bias_off, bias_floats);
 }
 
 void pack_any(int net, const int32_t* dims, const uint16_t* const* w, const float* const* b, std::vector<uint8_t>& wp,
@@ -623,52 +670,40 @@ int fin_policy_load(fin_policy* pol, const float* const* w, const float* const* 
   for (int l = 0; l < L; ++l)
     if (!w[l]) return fail(FIN_E_CONFIG, "fin_policy_load: weight %d is null", l);
   cudaStream_t s = S(stream);
-  if (pol->used) FIN_CUDA(cudaEventSynchronize(pol->used));   // no call may still read the old image
-  // f32 -> bf16 (round to nearest even) on the device, then the host packs the image
-  std::vector<std::vector<uint16_t>> hw(L);
-  std::vector<std::vector<float>> hb(L);
-  uint16_t* tmp = nullptr;
-  size_t maxn = 0;
-  for (int l = 0; l < L; ++l) maxn = std::max(maxn, (size_t)pol->dims[l + 1] * pol->dims[l]);
-  FIN_CUDA(cudaMallocAsync(&tmp, maxn * sizeof(uint16_t), s));
-  cudaError_t e = cudaSuccess;
-  for (int l = 0; l < L && e == cudaSuccess; ++l) {
-    const size_t n = (size_t)pol->dims[l + 1] * pol->dims[l];
-    hw[l].resize(n);
-    e = fin::launch_to_bf16((int64_t)n, w[l], tmp, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hw[l].data(), tmp, n * 2, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e == cudaSuccess && bias && bias[l]) {
-      hb[l].resize(pol->dims[l + 1]);
-      e = cudaMemcpyAsync(hb[l].data(), bias[l], hb[l].size() * 4, cudaMemcpyDeviceToHost, s);
+  // the gather tables of this network's image (built once per handle, host layout code only)
+  std::vector<int> boff;
+  int bfloats = 0;
+  {
+    std::vector<int32_t> src, w1s_src;
+    index_any(pol->net, pol->dims, src, w1s_src, boff, bfloats);
+    if (!pol->pack_src) {
+      FIN_CUDA(cudaMalloc(&pol->pack_src, src.size() * sizeof(int32_t)));
+      FIN_CUDA(cudaMemcpy(pol->pack_src, src.data(), src.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+      pol->n_pack = (int64_t)src.size();
+      if (!w1s_src.empty()) {
+        FIN_CUDA(cudaMalloc(&pol->w1s_src, w1s_src.size() * sizeof(int32_t)));
+        FIN_CUDA(cudaMemcpy(pol->w1s_src, w1s_src.data(), w1s_src.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        pol->n_w1s = (int64_t)w1s_src.size();
+      }
     }
   }
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  cudaFreeAsync(tmp, s);
-  if (e != cudaSuccess) return cuda_fail(e, "fin_policy_load download");
-  std::vector<const uint16_t*> wpt(L);
-  std::vector<const float*> bpt(L);
-  for (int l = 0; l < L; ++l) {
-    wpt[l] = hw[l].data();
-    bpt[l] = hb[l].empty() ? nullptr : hb[l].data();
-    if (bpt[l] && !finite_all(bpt[l], pol->dims[l + 1])) return fail(FIN_E_DATA, "bias %d non-finite", l);
-  }
-  std::vector<uint8_t> wp;
-  std::vector<float> bp, w1s;
-  pack_any(pol->net, pol->dims, wpt.data(), bpt.data(), wp, bp, w1s);
-  pol->bias_nz = 0;
-  for (int l = 0; l < L; ++l)
-    if (bpt[l])
-      for (int n = 0; n < pol->dims[l + 1]; ++n)
-        if (bpt[l][n] != 0.f) pol->bias_nz |= 1u << l;
-  pol->b1_in_z1s = !w1s.empty() && (pol->bias_nz & 1u);
-  if (pol->b1_in_z1s) pol->bias_nz &= ~1u;
-  e = cudaMemcpyAsync(pol->wpack, wp.data(), wp.size(), cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(pol->bias, bp.data(), bp.size() * 4, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess && !w1s.empty())
-    e = cudaMemcpyAsync(pol->w1s_t, w1s.data(), w1s.size() * 4, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return cuda_fail(e, "fin_policy_load upload");
+  // stream-ordered after the last call that read the old image (any stream)
+  if (pol->used) FIN_CUDA(cudaStreamWaitEvent(s, pol->used, 0));
+  const float* wl[4] = {w[0], w[1], w[2], L > 3 ? w[3] : nullptr};
+  cudaError_t e = fin::launch_policy_gather(pol->n_pack, pol->pack_src, wl, reinterpret_cast<uint16_t*>(pol->wpack),
+                                            pol->n_w1s, pol->w1s_src, pol->w1s_t, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(pol->bias, 0, (size_t)bfloats * sizeof(float), s);
+  uint8_t nz = 0;
+  for (int l = 0; l < L && e == cudaSuccess; ++l)
+    if (bias && bias[l]) {
+      e = cudaMemcpyAsync(pol->bias + boff[l], bias[l], (size_t)pol->dims[l + 1] * sizeof(float),
+                          cudaMemcpyDeviceToDevice, s);
+      nz |= (uint8_t)(1u << l);   // added whether or not it is all zero (+0 is the identity up to a zero's sign)
+    }
+  if (e != cudaSuccess) return cuda_fail(e, "fin_policy_load");
+  pol->b1_in_z1s = pol->w1s_t != nullptr && (nz & 1u);
+  pol->bias_nz = pol->b1_in_z1s ? (uint8_t)(nz & ~1u) : nz;
+  if (pol->used) cudaEventRecord(pol->used, s);   // the new image is being written on s
   pol->uid = new_uid();   // envs recompute their z1s term for the new weights
   return FIN_OK;
 }
@@ -682,6 +717,8 @@ void fin_policy_destroy(fin_policy* pol) {
   cudaFree(pol->wpack);
   cudaFree(pol->bias);
   if (pol->w1s_t) cudaFree(pol->w1s_t);
+  if (pol->pack_src) cudaFree(pol->pack_src);
+  if (pol->w1s_src) cudaFree(pol->w1s_src);
   delete pol;
 }
 
@@ -693,6 +730,8 @@ namespace {
 // fin_policy_load): layout only, no arithmetic
 void pack_any(int net, const int32_t* dims, const uint16_t* const* w, const float* const* b, std::vector<uint8_t>& wp,
               std::vector<float>& bp, std::vector<float>& w1s);
+void index_any(int net, const int32_t* dims, std::vector<int32_t>& src, std::vector<int32_t>& w1s_src,
+               std::vector<int>& bias_off, int& bias_floats);
 
 // every policy of a call records its `used` event on the call's stream after the launch
 void mark_used(const fin_policy* const* members, int n, cudaStream_t s) {

@@ -227,6 +227,28 @@ __global__ void k_ppo_prepare(int B, int K, const float* __restrict__ z, const f
   logp[s] = (float)(-q / (2.0 * sigma * sigma) - (double)K * log(sigma * sqrt(2.0 * 3.141592653589793)));
 }
 
+// fin_policy_load: the tcgen05 image and the factored net's shared W1 columns gathered from the f32
+// master weights through the handle's tables, bf16 round to nearest even on the way
+__global__ void k_policy_gather(int64_t n, const int32_t* __restrict__ src, const float* w0, const float* w1,
+                                const float* w2, const float* w3, uint16_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t t = src[i];
+  uint16_t v = 0;
+  if (t >= 0) {
+    const int l = t >> 24, idx = t & 0xffffff;
+    const float* w = l == 0 ? w0 : l == 1 ? w1 : l == 2 ? w2 : w3;
+    v = __bfloat16_as_ushort(__float2bfloat16_rn(w[idx]));
+  }
+  out[i] = v;
+}
+__global__ void k_w1s_gather(int64_t n, const int32_t* __restrict__ src, const float* __restrict__ w0,
+                             float* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = __bfloat162float(__float2bfloat16_rn(w0[src[i]]));
+}
+
 __global__ void k_to_bf16(int64_t n, const float* __restrict__ x, uint16_t* __restrict__ y) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = __bfloat16_as_ushort(__float2bfloat16_rn(x[i]));
@@ -250,6 +272,12 @@ cudaError_t launch_noise_at(uint64_t seed, int64_t off, int N, int64_t t_base, c
 cudaError_t launch_ppo_prepare(int B, int K, const float* z, const float* eps, double sigma, float* a, float* logp,
                                cudaStream_t s) {
   k_ppo_prepare<<<(B + 127) / 128, 128, 0, s>>>(B, K, z, eps, sigma, a, logp);
+  return cudaGetLastError();
+}
+cudaError_t launch_policy_gather(int64_t n_pack, const int32_t* pack_src, const float* const (&w)[4], uint16_t* wpack,
+                                 int64_t n_w1s, const int32_t* w1s_src, float* w1s, cudaStream_t s) {
+  k_policy_gather<<<(unsigned)((n_pack + 255) / 256), 256, 0, s>>>(n_pack, pack_src, w[0], w[1], w[2], w[3], wpack);
+  if (n_w1s > 0) k_w1s_gather<<<(unsigned)((n_w1s + 255) / 256), 256, 0, s>>>(n_w1s, w1s_src, w[0], w1s);
   return cudaGetLastError();
 }
 cudaError_t launch_to_bf16(int64_t n, const float* x, uint16_t* y, cudaStream_t s) {

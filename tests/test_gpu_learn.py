@@ -321,3 +321,40 @@ def test_dqn_grad_matches_oracle(variant):
     st = host(stats)
     assert st[0] == pytest.approx(Lo, rel=1e-6) and st[2] == pytest.approx(np.mean(y), rel=1e-6, abs=1e-9)
     assert st[3] == B
+
+
+@pytest.mark.parametrize("dims,kind", [((301, 256, 256, 30), 0), ((301, 64, 32, 30), 1), ((25, 128, 128, 4), 2),
+                                       ((103, 128, 128, 3), 3), ((103, 128, 128, 4), 4),
+                                       ((103, 128, 128, 128, 3), 3)])
+def test_policy_load_equals_create(dims, kind):
+    """fin_policy_load (the device gather into the tcgen05 image, bf16 round to nearest even, the
+    factored nets' shared W1 columns, biases) installs exactly what fin_policy_create packs on the host
+    from the same bf16 weights: the forward outputs and hidden activations are bit-identical, for every
+    compiled network."""
+    import torch
+    from paper_2501_10709_b200 import fin
+    from synth import policy as spol
+    kinds = [fin.FIN_PPO_GAUSS, fin.FIN_SAC_SQUASH, fin.FIN_PPO_GAUSS, fin.FIN_Q_ARGMAX, fin.FIN_Q_DUELING]
+    k = kinds[kind]
+    target = spol.random_bias(spol.kaiming_bf16(dims, 31), 32)
+    ref = fin.fin_policy_create(k, target)
+    pol = fin.fin_policy_create(k, spol.random_bias(spol.kaiming_bf16(dims, 33), 34))
+    # f32 master values that round to the target's bf16 (the bf16 value plus a sub-half-ulp offset)
+    ws = []
+    for w, _ in target:
+        wf = (np.asarray(w, dtype=np.uint32) << 16).view(np.float32)
+        ws.append(dev((wf * np.float32(1 + 2 ** -10)).astype(np.float32)))
+    bs = [dev(np.asarray(b, dtype=np.float32)) for _, b in target]
+    fin.fin_policy_load(pol, ws, bs)
+    rng = np.random.default_rng(3)
+    B = 300
+    x = dev(spol.f64_to_bf16_bits(rng.standard_normal((B, dims[0]))).view(np.int16))
+    H = max(dims[1:-1])
+    outs = []
+    for p in (ref, pol):
+        z = zeros((B, dims[-1]), torch.float32)
+        h = zeros((B, 2, H), torch.int16)
+        fin.fin_mlp_forward(p, x, z, h)
+        outs.append((host(z), host(h)))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
