@@ -337,6 +337,7 @@ int fin_env_create(const fin_env_config* cfg, const float* market, int64_t marke
   d.L = c.episode_len;
   d.autoreset = c.autoreset ? 1 : 0;
   d.cash0 = c.initial_cash;
+  d.rcash0 = 1.0 / c.initial_cash;
   d.cost = c.cost_rate;
   d.scale = c.reward_scale;
   d.up = 1.0 + c.cost_rate;
@@ -386,6 +387,7 @@ int fin_env_create(const fin_env_config* cfg, const float* market, int64_t marke
     d.max_hold = c.max_hold;
     expect = (int64_t)c.num_rows * 144;
   }
+  d.rmax_trade = 1.f / (float)d.max_trade;
   if (market_elems != expect)
     return fail(FIN_E_CONFIG, "market_elems %lld != expected %lld", (long long)market_elems, (long long)expect);
   // ---- validate the market: finite, prices > 0
@@ -788,6 +790,7 @@ int fill_members(fin_env* env, const fin_policy* const* members, int32_t n, cons
     if (member_w) return fail(FIN_E_CONFIG, "crypto ensembles vote: member_w must be NULL");
   }
   p.M = n;
+  p.inv_m = 1.f / (float)n;
   p.weighted = member_w ? 1 : 0;
   *net_out = net;
   return FIN_OK;
@@ -1037,6 +1040,7 @@ int fin_mlp_forward(const fin_policy* pol, const uint16_t* x, int32_t B, float* 
   p.kinds[0] = pol->kind;
   p.bias_nz[0] = pol->bias_nz;
   p.M = 1;
+  p.inv_m = 1.f;
   p.T = 1;
   p.x_in = x;
   p.z_out = z;

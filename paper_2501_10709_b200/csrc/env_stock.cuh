@@ -61,21 +61,37 @@ __device__ __forceinline__ double stock_mark(double b, const int (&h)[KA], const
   return acc;
 }
 
-// Buys of one step in the definition's order (R5): each asset the largest n <= want
-// with fl(n u) <= b.  Out of line: only the rare steps where some request is not
-// affordable come here.
-static __device__ __noinline__ double stock_buys_exact(double b, int* h, const int* a, int K, const double* U,
-                                                       const double* MU) {
-  for (int k = 0; k < K; ++k) {
-    const int want = max(min(a[k], FIN_HOLD_MAX - h[k]), 0);
+// The exact buys of one step in the definition's order (R5), from the post-sell holdings packed
+// in ``save`` ([octet] x stride uint4) and the cash before the buys: each asset the largest n <=
+// want with fl(n u) <= b (fp32 estimate, then exact fp64 checks).  Only the rare steps whose
+// branch-free estimate failed its check come here.  Inline and register-only: a call in the env
+// code makes ptxas keep the env state out of its caller-saved registers on every step.
+__device__ __forceinline__ int affordable_exact(double b, double u, int want) {
+  if (!(b >= u)) return 0;                                 // not even one share (also b < 0, NaN)
+  const float qf = fminf(__fdividef((float)b, (float)u), (float)want);
+  int n = qf > 0.f ? (int)qf : 0;
+  while (n > 0 && fmul64((double)n, u) > b) --n;
+  while (n < want && fmul64((double)(n + 1), u) <= b) ++n;
+  return n;
+}
+template <int KA, class Acts>
+__device__ __forceinline__ double stock_buys_redo(double b, int (&h)[KA], const Acts& a, const uint4* save,
+                                                  int save_stride, const double* U, const double* MU) {
+#pragma unroll
+  for (int k = 0; k < KA; ++k) {
+    const uint4 v = save[(k >> 3) * save_stride];
+    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+    const uint32_t x = wv[(k >> 1) & 3];
+    const int hk = (int)((k & 1) ? (x >> 16) : (x & 0xffffu));
+    const int want = max(min(a[k], FIN_HOLD_MAX - hk), 0);
     double c = nprod(want, U[k], MU[k]);
     int n = want;
     if (!(c <= b)) {
-      n = affordable_slow(b, U[k], want);
+      n = affordable_exact(b, U[k], want);
       c = nprod(n, U[k], MU[k]);
     }
     b = fsub64(b, c);
-    h[k] += n;
+    h[k] = hk + n;
   }
   return b;
 }
@@ -199,20 +215,9 @@ __device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)
     buy_one(b, h[k], a[k], U[k + o_], RU[k + o_], miss);
   })
 buys_done:
-  if (miss) {   // rare: arrays in local memory only on this path
+  if (miss) {   // rare
     atomicAdd(e.flags + FIN_CTR_EXACT_REDO, 1u);
-    int hh[KA], aa[KA];
-#pragma unroll
-    for (int k = 0; k < KA; ++k) {
-      const uint4 v = save[(k >> 3) * save_stride];
-      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-      const uint32_t x = wv[(k >> 1) & 3];
-      hh[k] = (int)((k & 1) ? (x >> 16) : (x & 0xffffu));
-      aa[k] = a[k];
-    }
-    b = stock_buys_exact(bpre, hh, aa, KA, U, MU);
-#pragma unroll
-    for (int k = 0; k < KA; ++k) h[k] = hh[k];
+    b = stock_buys_redo<KA>(bpre, h, a, save, save_stride, U, MU);
   }
 }
 
@@ -277,20 +282,9 @@ __device__ __forceinline__ void stock_trade_e(const EnvDev& e, double (&b)[E], i
 buys_done_e:
 #pragma unroll
   for (int q = 0; q < E; ++q) {
-    if (miss[q]) {   // rare: arrays in local memory only on this path
+    if (miss[q]) {   // rare
       atomicAdd(e.flags + FIN_CTR_EXACT_REDO, 1u);
-      int hh[KA], aa[KA];
-#pragma unroll
-      for (int k = 0; k < KA; ++k) {
-        const uint4 v = save[q][(k >> 3) * save_stride];
-        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-        const uint32_t x = wv[(k >> 1) & 3];
-        hh[k] = (int)((k & 1) ? (x >> 16) : (x & 0xffffu));
-        aa[k] = a[q][k];
-      }
-      b[q] = stock_buys_exact(bpre[q], hh, aa, KA, R[q] + kRowU * RS, R[q] + kRowMU * RS);
-#pragma unroll
-      for (int k = 0; k < KA; ++k) h[q][k] = hh[k];
+      b[q] = stock_buys_redo<KA>(bpre[q], h[q], a[q], save[q], save_stride, R[q] + kRowU * RS, R[q] + kRowMU * RS);
     }
   }
 }

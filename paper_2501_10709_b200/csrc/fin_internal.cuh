@@ -45,6 +45,8 @@ struct EnvDev {
   int32_t kp;            // K padded to a multiple of 4 (market channel stride)
   int32_t row_floats;    // floats per market row: (2+I)*kp (stock) or 144 (crypto)
   double cash0, cost, scale;
+  double rcash0;
+  float rmax_trade;      // fl(1 / max_trade) (host division): the observation's h / max_trade         // fl(1 / cash0) (host division): the observation's b / b0 by Markstein's correction
   double up, dn;         // fl(1 + cost), fl(1 - cost)
   float noise_std, ou_theta, ou_sigma, eps;
   uint64_t seed;
@@ -105,6 +107,15 @@ __device__ __forceinline__ double fadd64(double a, double b) { return __dadd_rn(
 __device__ __forceinline__ double fsub64(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double fmul64(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double fdiv64(double a, double b) { return __ddiv_rn(a, b); }
+// a / b correctly rounded from y = fl(1 / b) without a call (the slow-path CALL of __ddiv_rn makes
+// ptxas keep the env state out of its caller-saved registers): q = fl(a y), r = a - b q exactly (fma),
+// q' = fl(q + r y) -- Markstein's correction, the correctly rounded quotient whenever y is the
+// correctly rounded reciprocal and nothing over- or underflows (b = b0 > 0 here, |a| < 2^1000)
+__device__ __forceinline__ double fdiv64_rcp(double a, double b, double y) {
+  const double q = __dmul_rn(a, y);
+  const double r = __fma_rn(-q, b, a);
+  return __fma_rn(r, y, q);
+}
 
 // Price rows of day d, precomputed on the host at create (px), staged per step:
 //   P  = p_d   close of the execution day (exact widening of the fp32 market)
@@ -168,21 +179,6 @@ __device__ __forceinline__ int32_t day_of(const EnvDev& e, int32_t w, int32_t t)
   return e.woff + w * e.wstride + t;
 }
 
-// ----------------------------------------------------------------- affordability (R5)
-// Largest n in [0, want] with fl(n*u) <= b.  fl(n*u) is monotone in n.  The fast
-// path (enough cash) is one multiply; otherwise an fp32 estimate of b/u (relative
-// error ~1e-7, so within +-1 of the answer for n < 2^15) is corrected by exact
-// fp64 checks until the definition holds.
-// slow path, out of line: one copy in the binary however often it is inlined around
-static __device__ __noinline__ int affordable_slow(double b, double u, int want) {
-  if (!(b >= u)) return 0;                                 // not even one share (also b < 0, NaN)
-  const float qf = fminf(__fdividef((float)b, (float)u), (float)want);   // estimate, corrected below
-  int n = qf > 0.f ? (int)qf : 0;
-  while (n > 0 && fmul64((double)n, u) > b) --n;
-  while (n < want && fmul64((double)(n + 1), u) <= b) ++n;
-  return n;
-}
-
 // h / d correctly rounded in fp32 for integer |h| < 2^24 and d >= 1, without the IEEE
 // division subroutine: q = h * (1/d) then one FMA residual correction (exhaustively
 // checked for |h| < 2^15 and the divisors used here); the bf16 of the
@@ -193,12 +189,6 @@ __device__ __forceinline__ float div_int_f32(int h, float d, float inv_d) {
   const float r = __fmaf_rn(-q, d, hf);
   return __fmaf_rn(r, inv_d, q);
 }
-__device__ __forceinline__ int affordable(double b, double u, int want) {
-  if (want <= 0) return 0;
-  if (fmul64((double)want, u) <= b) return want;
-  return affordable_slow(b, u, want);
-}
-
 // ----------------------------------------------------------------- online metrics
 // Per-episode accumulators: equity v_0 .. v_L, returns
 // r_t = v_t / v_{t-1} - 1 (Welford mean / M2), running peak and min drawdown.
@@ -219,6 +209,19 @@ __device__ __forceinline__ double rcp_nr(double x) {
   double e = __fma_rn(-x, y, 1.0);
   y = __fma_rn(y, e, y);
   e = __fma_rn(-x, y, 1.0);
+  return __fma_rn(y, e, y);
+}
+
+// 1 / sqrt(x) for normal x > 0 from the MUFU seed and two Newton steps (~1 ulp), inline: the
+// library rsqrt carries a slow-path CALL, which makes ptxas keep the rollout's env state out of
+// caller-saved registers (spills around every step)
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double h = __dmul_rn(0.5, x);
+  double e = __fma_rn(-h, __dmul_rn(y, y), 0.5);
+  y = __fma_rn(y, e, y);
+  e = __fma_rn(-h, __dmul_rn(y, y), 0.5);
   return __fma_rn(y, e, y);
 }
 
@@ -246,7 +249,7 @@ __device__ __forceinline__ void metric_finish(const MetricAcc& m, double ppy, do
   double sh = __longlong_as_double(0x7ff8000000000000ULL);
   if (m.n >= 2) {
     const double var = fmul64(m.m2, rcp_nr(nn2d(m.n - 1)));
-    if (var > 0.0) sh = fmul64(fmul64(sqrt(ppy), fsub64(m.mean, rf)), rsqrt(var));
+    if (var > 0.0) sh = fmul64(fmul64(sqrt(ppy), fsub64(m.mean, rf)), rsqrt_nr(var));
   }
   out[1] = sh;
   out[2] = m.mdd;

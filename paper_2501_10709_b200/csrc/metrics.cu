@@ -225,7 +225,7 @@ __device__ __forceinline__ void fast_finish(const FastAcc& a, double ppy, double
     const double rn = rcp_nr(nn2d(a.n));
     const double mean = fadd64(a.k, fmul64(a.s1, rn));
     const double var = fmul64(fsub64(a.s2, fmul64(fmul64(a.s1, a.s1), rn)), rcp_nr(nn2d(a.n - 1)));
-    if (var > 0.0) sh = fmul64(fmul64(sqrt(ppy), fsub64(mean, rf)), rsqrt(var));
+    if (var > 0.0) sh = fmul64(fmul64(sqrt(ppy), fsub64(mean, rf)), rsqrt_nr(var));
   }
   out[1] = sh;
   out[2] = a.mdd;

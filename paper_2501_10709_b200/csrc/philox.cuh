@@ -28,7 +28,8 @@ __device__ __forceinline__ float philox_u01(uint32_t x) {
 // 1 - 2^-25), angle 2 pi u_a evaluated as 2 pi (u_a - [u_a >= 1/2]) in [-pi, pi) with
 // the fast sincos (absolute error ~4e-7 there).
 __device__ __forceinline__ void box_muller(float ur, float ua, float& z0, float& z1) {
-  const float r = sqrtf(-2.0f * logf(ur));
+  float r;   // sqrt.approx (rel. error ~2^-23; no slow-path call in the env warps' code)
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(-2.0f * logf(ur)));
   const float a = 6.283185307179586f * (ua >= 0.5f ? ua - 1.0f : ua);
   float s, c;
   __sincosf(a, &s, &c);

@@ -308,7 +308,8 @@ struct CryptoOps {
     st.act = best - 1;
   }
 
-  __device__ __forceinline__ static void finish_step(State& st, const TcParams& p, int env, int t, uint8_t* stg) {
+  __device__ __forceinline__ static void finish_step(State& st, const TcParams& p, int env, int t, uint8_t* stg,
+                                                     uint8_t*) {
     if (!st.live) return;
     const EnvDev& e = p.e;
     const size_t ti = (size_t)t * e.N + env;

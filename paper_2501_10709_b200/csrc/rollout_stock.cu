@@ -96,6 +96,8 @@ struct StockOps {
   static constexpr int kOffB = kOffS + 16;      // int[4]: d0, predicted day, -, -
   static constexpr int kOffImgT = 0;
   static constexpr int kStageBytes = kOffB + 16;
+  static constexpr int kSaveOff = tc::kTileM * Plan::kIn * 2;   // exact-redo scratch in the A operand
+  static_assert(kSaveOff + (KA + 7) / 8 * tc::kTileM * 16 <= tc::kTileM * Plan::kHidMax * 2, "save fits the A operand");
 
   struct State {
     bool live;
@@ -164,7 +166,7 @@ struct StockOps {
   }
 
   // stage day k into buffer region reg: f64 price rows of day k and the members' z1s rows
-  __device__ __noinline__ static void stage_row(const TcParams& p, int k, int gtid, uint8_t* reg) {
+  __device__ __forceinline__ static void stage_row(const TcParams& p, int k, int gtid, uint8_t* reg) {
     const EnvDev& e = p.e;
     FIN_CHECK(k >= 0 && k < e.rows && k < p.z1s_rows);
     stage_price_rows(e, reinterpret_cast<double*>(reg + kOffP), k, gtid, 128);
@@ -225,7 +227,7 @@ struct StockOps {
     if (st.live) {
       st.d = day_of(e, st.w, st.t_ep);
       if (st.d < 0 || st.d + 1 >= e.rows) { st.bad = true; st.d = 0; }
-      st.b0bits = (uint32_t)__bfloat16_as_ushort(__double2bfloat16(fdiv64(st.b, e.cash0)));
+      st.b0bits = (uint32_t)__bfloat16_as_ushort(__double2bfloat16(fdiv64_rcp(st.b, e.cash0, e.rcash0)));
     }
     if (gtid == 0) {
       bc[0] = st.live ? st.d : -1;
@@ -285,7 +287,7 @@ struct StockOps {
       for (int k = 0; k < KA; ++k) st.asum[k] = 0.f;
     }
     const float den = (float)e.max_trade;
-    const float inv_den = __frcp_rn(den);
+    const float inv_den = e.rmax_trade;   // = __frcp_rn(den), computed on the host
 #pragma unroll
     for (int c = 0; c < KT8; ++c) {
       uint32_t w4[4];
@@ -407,14 +409,15 @@ struct StockOps {
     }
   }
 
-  __device__ __forceinline__ static void finish_step(State& st, const TcParams& p, int env, int t, uint8_t* stg) {
+  __device__ __forceinline__ static void finish_step(State& st, const TcParams& p, int env, int t, uint8_t* stg,
+                                                     uint8_t* a_tile) {
     const EnvDev& e = p.e;
     const size_t ti = (size_t)t * e.N + env;
     FIN_CHECK(!st.live || (t >= 0 && t < p.T && env >= 0 && env < e.N));
     FIN_CHECK(!st.live || st.bad || (st.d >= 0 && st.d + 1 < e.rows));
     int a[KA];
     FIN_TR(threadIdx.x == 128, t, 17);
-    const float inv_m = 1.f / (float)p.M;   // uniform mean (R20); the weighted sum is already scaled
+    const float inv_m = p.inv_m;   // fl(1 / M) (host): uniform mean (R20); the weighted sum is already scaled
 #pragma unroll
     for (int k = 0; k < KA; ++k) {
       const float abar = (!ENS || p.M == 1 || p.weighted) ? st.asum[k] : __fmul_rn(st.asum[k], inv_m);
@@ -445,9 +448,12 @@ struct StockOps {
           const double* pd = reinterpret_cast<const double*>(region(stg, st.sb) + kOffP);
           FIN_TR(threadIdx.x == 128, t, 19);
           const double v = st.vc;
-          uint4 save[(KA + 7) / 8];   // local: read only by the rare exact buy redo
+          // post-sell holdings for the rare exact buy redo: [octet][row] in the tile's A operand
+          // past the observation columns (free while the env steps: the layer-3 MMAs have completed
+          // and the next observation only fills the first kTileM x kIn bf16)
+          uint4* save = reinterpret_cast<uint4*>(a_tile + kSaveOff) + st.gtid;
           clamp_actions<KA>(e, a, st.oor, (LOG && p.o.actions) ? p.o.actions + ti * KA : nullptr);
-          stock_trade<KA>(e, st.b, st.h, pd, KP4, pack_acts<KA>(a), save, 1);
+          stock_trade<KA>(e, st.b, st.h, pd, KP4, pack_acts<KA>(a), save, tc::kTileM);
           const double vn = stock_mark<KA>(st.b, st.h, pd + kRowPN * KP4);
           st.vc = vn;
           FIN_TR(threadIdx.x == 128, t, 20);
@@ -607,7 +613,7 @@ struct ProbeOps {
     if (st.b >= p.B) return;
     for (int k = 0; k < p.out_dim; ++k) p.z_out[(size_t)st.b * p.out_dim + k] = z[k];
   }
-  __device__ __forceinline__ static void finish_step(State&, const TcParams&, int, int, uint8_t*) {}
+  __device__ __forceinline__ static void finish_step(State&, const TcParams&, int, int, uint8_t*, uint8_t*) {}
   __device__ __forceinline__ static void finalize(State&, const TcParams&, int, int, int, int) {}
 };
 

@@ -53,6 +53,7 @@ struct TcParams {
   int32_t kinds[FIN_MAX_MEMBERS];
   float mw[FIN_MAX_MEMBERS];              // member weights (weighted mode)
   int32_t M;
+  float inv_m;                            // fl(1 / M), host division
   int32_t weighted;
   int32_t T;
   int32_t noise_mode;
@@ -156,7 +157,8 @@ struct Smem {
 //     build_obs(State&, p, env, row, t, m, x_addr, stage_ptr)
 //     hidden_ptr(State&, p, env, t, m, l, hid) -> uint16_t* or nullptr
 //     consume(State&, p, env, t, m, const float* z)
-//     finish_step(State&, p, env, t, stage_ptr)
+//     finish_step(State&, p, env, t, stage_ptr, a_tile)   (a_tile: the tile's A operand, free during the
+//                                                        env step -- scratch for the env side)
 //     finalize(State&, p, env, group_tid, bar_id)
 //   };
 // RING: weight-ring slots; MINB: CTAs per SM (MINB = 2 runs two independent tiles per
@@ -652,7 +654,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
         Ops::consume(st, p, env, t, m, z);
         FIN_TR(row == 0 && tile == 0 && m == 0, t, 7);
       }
-      Ops::finish_step(st, p, env, t, stg);
+      Ops::finish_step(st, p, env, t, stg, sA + tile * S::kA);
       FIN_TR(row == 0 && tile == 0, t, 8);
     }
     if constexpr (kSeg) {
