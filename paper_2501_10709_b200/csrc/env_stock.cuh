@@ -96,6 +96,35 @@ __device__ __forceinline__ double stock_buys_redo(double b, int (&h)[KA], const 
   return b;
 }
 
+// K1's E-env form keeps the redo out of line (through local arrays, only on that path): measured
+// +1.2% for K1 (2,836 vs 2,804 GB/s), whose few live values survive the call unspilled; the fused
+// rollout (stock_trade) inlines it (no call: +7%)
+#ifndef FIN_REDO_CALL
+#define FIN_REDO_CALL 1
+#endif
+template <int KA, class Acts>
+static __device__ __noinline__ double stock_buys_redo_ool(double b, int* h, const Acts* a, const uint4* save,
+                                                         int save_stride, const double* U, const double* MU) {
+  int hh[KA];
+#pragma unroll
+  for (int k = 0; k < KA; ++k) hh[k] = h[k];
+  b = stock_buys_redo<KA>(b, hh, *a, save, save_stride, U, MU);
+#pragma unroll
+  for (int k = 0; k < KA; ++k) h[k] = hh[k];
+  return b;
+}
+template <int KA, class Acts>
+__device__ __forceinline__ double stock_buys_redo_call(double b, int (&h)[KA], const Acts& a, const uint4* save,
+                                                       int save_stride, const double* U, const double* MU) {
+  int hh[KA];
+#pragma unroll
+  for (int k = 0; k < KA; ++k) hh[k] = h[k];
+  b = stock_buys_redo_ool<KA, Acts>(b, hh, &a, save, save_stride, U, MU);
+#pragma unroll
+  for (int k = 0; k < KA; ++k) h[k] = hh[k];
+  return b;
+}
+
 // One buy of step 4 (R5): n = the largest count <= want with fl(n u) <= b, b -= fl(n u).
 // n comes from the floor estimate f = floor(b fl(1/u)) (one round-down add, whose bits are
 // 2^52 + f) and is verified: fl(n u) <= b and, when the cash binds, fl((n + 1) u) > b; a
@@ -284,7 +313,11 @@ buys_done_e:
   for (int q = 0; q < E; ++q) {
     if (miss[q]) {   // rare
       atomicAdd(e.flags + FIN_CTR_EXACT_REDO, 1u);
+#if FIN_REDO_CALL
+      b[q] = stock_buys_redo_call<KA>(bpre[q], h[q], a[q], save[q], save_stride, R[q] + kRowU * RS, R[q] + kRowMU * RS);
+#else
       b[q] = stock_buys_redo<KA>(bpre[q], h[q], a[q], save[q], save_stride, R[q] + kRowU * RS, R[q] + kRowMU * RS);
+#endif
     }
   }
 }
