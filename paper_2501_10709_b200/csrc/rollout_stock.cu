@@ -95,7 +95,15 @@ struct StockOps {
   static constexpr int kOffS = 2 * kRegion;
   static constexpr int kOffB = kOffS + 16;      // int[4]: d0, predicted day, -, -
   static constexpr int kOffImgT = 0;
-  static constexpr int kStageBytes = kOffB + 16;
+  // single policy: the episode-metric accumulators live in shared memory between steps ([6][row]
+  // doubles, episode count n in a register) -- 12 shared accesses per step instead of ~12 registers
+  // held across it, whose pressure made ptxas spill ~47 values per warp-step (FIN_METRIC_SM=0: A/B)
+#ifndef FIN_METRIC_SM
+#define FIN_METRIC_SM 1
+#endif
+  static constexpr bool kMetricSm = FIN_METRIC_SM && !ENS;
+  static constexpr int kOffM = kOffB + 16;
+  static constexpr int kStageBytes = kOffM + (kMetricSm ? 6 * tc::kTileM * 8 : 0);
   static constexpr int kSaveOff = tc::kTileM * Plan::kIn * 2;   // exact-redo scratch in the A operand
   static_assert(kSaveOff + (KA + 7) / 8 * tc::kTileM * 16 <= tc::kTileM * Plan::kHidMax * 2, "save fits the A operand");
 
@@ -115,7 +123,9 @@ struct StockOps {
     float asum[KA];
     float eps[KA];     // this member's noise of the step (prepare(), while layer 2 runs)
     float ou[KOU];
-    MetricAcc m;       // (the aggregate partials live in e.agg_env: touched once per episode)
+    MetricAcc m;       // (the aggregate partials live in e.agg_env: touched once per episode); kMetricSm:
+                       // only m.n (and m until the first stage(), which moves it to shared memory)
+    uint32_t msa;      // kMetricSm: shared address of this row's accumulators (field f at + f * 128 * 8)
     int cnt;
     double rsum;
     int t_begin, t_end;   // steps of this segment (whole call: 0, T)
@@ -193,6 +203,32 @@ struct StockOps {
   }
   __device__ __forceinline__ static uint8_t* region(uint8_t* stg, int b) { return stg + b * kRegion; }
 
+  __device__ __forceinline__ static void m_put(State& st, const MetricAcc& m) {
+    if constexpr (kMetricSm) {
+      const double f[6] = {m.v0, m.vprev, m.peak, m.mdd, m.mean, m.m2};
+#pragma unroll
+      for (int i = 0; i < 6; ++i)
+        asm volatile("st.shared.f64 [%0], %1;" ::"r"(st.msa + (uint32_t)(i * tc::kTileM * 8)), "d"(f[i]) : "memory");
+      st.m.n = m.n;
+    } else {
+      st.m = m;
+    }
+  }
+  __device__ __forceinline__ static MetricAcc m_get(const State& st) {
+    if constexpr (kMetricSm) {
+      double f[6];
+#pragma unroll
+      for (int i = 0; i < 6; ++i)
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(f[i]) : "r"(st.msa + (uint32_t)(i * tc::kTileM * 8)) : "memory");
+      MetricAcc m;
+      m.v0 = f[0]; m.vprev = f[1]; m.peak = f[2]; m.mdd = f[3]; m.mean = f[4]; m.m2 = f[5];
+      m.n = st.m.n;
+      return m;
+    } else {
+      return st.m;
+    }
+  }
+
   // kL1Init: this env's row of the layer-1 accumulator <- z1s[d] (+ b1) of its day
   __device__ __forceinline__ static void l1_init_rows(State& st, const TcParams& p, uint32_t t_lane, uint8_t* stg) {
     if constexpr (kL1Init) {
@@ -223,7 +259,14 @@ struct StockOps {
     st.bar_id = bar_id;
     GroupSlots* gs = reinterpret_cast<GroupSlots*>(stg + kOffS);
     int* bc = reinterpret_cast<int*>(stg + kOffB);
-    if (t == st.t_begin) gs_init(gs, gtid, bar_id);
+    if (t == st.t_begin) {
+      gs_init(gs, gtid, bar_id);
+      if constexpr (kMetricSm) {
+        st.msa = sm100::smem_u32(stg + kOffM) + (uint32_t)gtid * 8u;
+        const MetricAcc m0 = st.m;
+        m_put(st, m0);
+      }
+    }
     if (st.live) {
       st.d = day_of(e, st.w, st.t_ep);
       if (st.d < 0 || st.d + 1 >= e.rows) { st.bad = true; st.d = 0; }
@@ -469,11 +512,12 @@ struct StockOps {
 #pragma unroll
             for (int k = 0; k < KA; ++k) p.o.hold[ti * KA + k] = (int16_t)st.h[k];
           }
-          metric_push(st.m, vn);
+          MetricAcc m = m_get(st);
+          metric_push(m, vn);
           FIN_TR(threadIdx.x == 128, t, 21);
           if (done) {
             double em[3];
-            metric_finish(st.m, 252.0, 0.0, em);
+            metric_finish(m, 252.0, 0.0, em);
             if (p.o.ep_metrics && st.cnt < p.o.ep_capacity) {
               double* dst = p.o.ep_metrics + ((size_t)st.cnt * e.N + env) * 3;
               dst[0] = em[0]; dst[1] = em[1]; dst[2] = em[2];
@@ -492,9 +536,10 @@ struct StockOps {
               st.t_ep = 0;
               st.vc = e.cash0;
               if (e.wadv) st.w = (st.w + 1) % e.W;
-              metric_start(st.m, e.cash0);
+              metric_start(m, e.cash0);
             }
           }
+          m_put(st, m);
         },
         st.zsm ? st.d0 : -1);   // uniform tile: its day's rows were staged by stage()
   }
@@ -530,8 +575,9 @@ struct StockOps {
       store_hold<KA>(e, env, st.h);
       e.t_ep[env] = st.t_ep;
       e.window[env] = st.w;
-      e.m_v0[env] = st.m.v0; e.m_vprev[env] = st.m.vprev; e.m_peak[env] = st.m.peak; e.m_mdd[env] = st.m.mdd;
-      e.m_mean[env] = st.m.mean; e.m_m2[env] = st.m.m2; e.m_n[env] = st.m.n;
+      const MetricAcc m = m_get(st);
+      e.m_v0[env] = m.v0; e.m_vprev[env] = m.vprev; e.m_peak[env] = m.peak; e.m_mdd[env] = m.mdd;
+      e.m_mean[env] = m.mean; e.m_m2[env] = m.m2; e.m_n[env] = m.n;
       if (ENS && p.n_ddpg == 1) {
 #pragma unroll
         for (int k = 0; k < KOU; ++k) e.ou[(size_t)k * e.N + env] = st.ou[k];
