@@ -388,6 +388,7 @@ int fin_env_create(const fin_env_config* cfg, const float* market, int64_t marke
     expect = (int64_t)c.num_rows * 144;
   }
   d.rmax_trade = 1.f / (float)d.max_trade;
+  d.rmax_hold = d.max_hold > 0 ? 1.f / (float)d.max_hold : 0.f;
   if (market_elems != expect)
     return fail(FIN_E_CONFIG, "market_elems %lld != expected %lld", (long long)market_elems, (long long)expect);
   // ---- validate the market: finite, prices > 0

@@ -46,7 +46,8 @@ struct EnvDev {
   int32_t row_floats;    // floats per market row: (2+I)*kp (stock) or 144 (crypto)
   double cash0, cost, scale;
   double rcash0;
-  float rmax_trade;      // fl(1 / max_trade) (host division): the observation's h / max_trade         // fl(1 / cash0) (host division): the observation's b / b0 by Markstein's correction
+  float rmax_trade;      // fl(1 / max_trade) (host division): the observation's h / max_trade
+  float rmax_hold;       // crypto: fl(1 / max_hold) (host division): the observation's tau / max_hold         // fl(1 / cash0) (host division): the observation's b / b0 by Markstein's correction
   double up, dn;         // fl(1 + cost), fl(1 - cost)
   float noise_std, ou_theta, ou_sigma, eps;
   uint64_t seed;

@@ -201,7 +201,7 @@ struct CryptoOps {
       return;
     }
     const float den = (float)e.max_hold;
-    const uint32_t priv = bf16_bits((float)st.h) | (bf16_bits(div_int_f32(st.tau, den, __frcp_rn(den))) << 16);
+    const uint32_t priv = bf16_bits((float)st.h) | (bf16_bits(div_int_f32(st.tau, den, e.rmax_hold)) << 16);
     if (st.uniform) {
       const uint4* xs = reinterpret_cast<const uint4*>(stg + kOffX);
 #pragma unroll
@@ -241,7 +241,7 @@ struct CryptoOps {
     uint32_t priv = 0u;
     if (st.live) {
       const float den = (float)e.max_hold;
-      priv = bf16_bits((float)st.h) | (bf16_bits(div_int_f32(st.tau, den, __frcp_rn(den))) << 16);
+      priv = bf16_bits((float)st.h) | (bf16_bits(div_int_f32(st.tau, den, e.rmax_hold)) << 16);
     }
     tc::sts128(xa + tc::cm_off(row, 0, KT8), priv, v0.y, v0.z, v0.w);
     tc::sts128(xa + tc::cm_off(row, 1, KT8), v1.x, v1.y, v1.z, v1.w);
