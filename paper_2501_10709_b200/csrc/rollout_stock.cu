@@ -59,7 +59,10 @@ struct StockOps {
   static constexpr bool kSplitOK = false;
   static constexpr bool kSegments = true;   // balanced persistent schedule (init_seg / finalize_seg)
   static constexpr bool kL1Bcast = false;   // (crypto only: broadcast layer-1 A operand)
-  static constexpr bool kEpiPipe = false;
+#ifndef FIN_STOCK_EPIPIPE
+#define FIN_STOCK_EPIPIPE 0
+#endif
+  static constexpr bool kEpiPipe = FIN_STOCK_EPIPIPE;
   // ensembles read biases from L2 (no staged copy): the C2 ensemble then fits the dual layout
   // (two CTAs per SM), 6.1e8 -> 6.8e8 env-steps/s; the single policy keeps its staged copy
   static constexpr bool kStageBias = !ENS;
