@@ -63,7 +63,24 @@ struct StepSmem {
   uint64_t rows[2];
   int pred[2];
   alignas(16) int16_t act[2][4][32 * KA];   // [buffer][warp] action rows
+  // K4: each env's episode-metric and aggregate accumulators between steps ([field][thread]):
+  // touched once per step / episode, and out of the registers the trade needs (FIN_K4_ACC_SM)
+  double met[6][kStep];
+  double agg[FIN_AGG_LEN][kStep];
 };
+#ifndef FIN_K4_ACC_SM
+#define FIN_K4_ACC_SM 1
+#endif
+template <int KA>
+__device__ __forceinline__ void met_put(StepSmem<KA>& sm, int tid, const MetricAcc& m) {
+  sm.met[0][tid] = m.v0; sm.met[1][tid] = m.vprev; sm.met[2][tid] = m.peak;
+  sm.met[3][tid] = m.mdd; sm.met[4][tid] = m.mean; sm.met[5][tid] = m.m2;
+}
+template <int KA>
+__device__ __forceinline__ void met_get(const StepSmem<KA>& sm, int tid, MetricAcc& m) {
+  m.v0 = sm.met[0][tid]; m.vprev = sm.met[1][tid]; m.peak = sm.met[2][tid];
+  m.mdd = sm.met[3][tid]; m.mean = sm.met[4][tid]; m.m2 = sm.met[5][tid];
+}
 
 // copy this warp's action rows [n_valid][K] (contiguous in the caller's [N][K]) to shared
 __device__ __forceinline__ void slab_load(int16_t* dst, const int16_t* src, int n_valid, int K, int lane, bool vec) {
@@ -410,6 +427,11 @@ __global__ void __launch_bounds__(kStep, FIN_K4_MINB) k_stock_replay(EnvDev e, c
     load_hold<KA>(e, i, h);
     m = load_metric(e, i);
   }
+  if (FIN_K4_ACC_SM) {
+    met_put(sm, tid, m);
+#pragma unroll
+    for (int j = 0; j < FIN_AGG_LEN; ++j) sm.agg[j][tid] = agg.s[j];
+  }
   const int i0 = blockIdx.x * kStep + wid * 32;
   const int nv = max(0, min(32, N - i0));
   const bool vec = vec_ok && nv == 32;
@@ -475,6 +497,7 @@ __global__ void __launch_bounds__(kStep, FIN_K4_MINB) k_stock_replay(EnvDev e, c
           if (o.cash) o.cash[ti] = b;
           if (o.asset) o.asset[ti] = vn;
           write_hold_row<KA>(e, o, ti, h);
+          if (FIN_K4_ACC_SM) met_get(sm, tid, m);
           metric_push(m, vn);
           if (done) {
             double em[3];
@@ -484,7 +507,16 @@ __global__ void __launch_bounds__(kStep, FIN_K4_MINB) k_stock_replay(EnvDev e, c
               dst[0] = em[0]; dst[1] = em[1]; dst[2] = em[2];
             }
             ++cnt;
-            agg_episode(agg, em);
+            if (FIN_K4_ACC_SM) {
+              AggAcc ag;
+#pragma unroll
+              for (int j = 0; j < FIN_AGG_LEN; ++j) ag.s[j] = sm.agg[j][tid];
+              agg_episode(ag, em);
+#pragma unroll
+              for (int j = 0; j < FIN_AGG_LEN; ++j) sm.agg[j][tid] = ag.s[j];
+            } else {
+              agg_episode(agg, em);
+            }
             if (e.autoreset) {
               b = e.cash0;
 #pragma unroll
@@ -495,7 +527,13 @@ __global__ void __launch_bounds__(kStep, FIN_K4_MINB) k_stock_replay(EnvDev e, c
               metric_start(m, e.cash0);
             }
           }
+          if (FIN_K4_ACC_SM) met_put(sm, tid, m);
         });
+  }
+  if (FIN_K4_ACC_SM) {
+    met_get(sm, tid, m);
+#pragma unroll
+    for (int j = 0; j < FIN_AGG_LEN; ++j) agg.s[j] = sm.agg[j][tid];
   }
   if (live) {
     if (oor) set_flag(e, FIN_FLAG_ACTION_RANGE);
