@@ -136,6 +136,40 @@ def test_exact_affordability_redo_path(cost):
     assert fin.fin_env_counters(env)["exact_redo"] == 0
 
 
+def test_exact_affordability_redo_path_fused_rollout():
+    """The same boundary cases through the fused policy rollout (K3: the exact redo inline, the
+    post-sell holdings kept in the tile's A operand): a zero-weight PPO policy (tanh 0 = 0) and
+    supplied noise eps = (q + 3) / 10 on each env's asset give 100 clip(0.1 eps) = q + 3 shares; the
+    redo counter proves the exact path ran, and cash / holdings equal the oracle's bit for bit."""
+    import torch
+    fin = _fin()
+    K, N, I = 30, 3000, 8
+    mk3, cash, acts = _redo_case(K, N, 1e-3)
+    mk = np.zeros((3, 2 + I, K), dtype=np.float32)
+    mk[:, :2, :] = mk3[:, :2, :]
+    ocfg, fcfg = stock_pair(num_envs=N, num_assets=K, num_indicators=I, num_rows=3, episode_len=2, cost_rate=1e-3,
+                            window_block=N)
+    p, pn = [float(x) for x in mk[0, 0]], [float(x) for x in mk[1, 0]]
+    want_b, want_h = np.empty(N), np.zeros((N, K), dtype=np.int64)
+    for i in range(N):
+        b, h, _, _, _, _, _ = ostock.step_one(ocfg, float(cash[i]), [0] * K, p, pn, [int(x) for x in acts[i]])
+        want_b[i], want_h[i] = b, h
+    dims = (1 + 2 * K + I * K, 256, 256, K)
+    zero = [(np.zeros((o, i), dtype=np.uint16), np.zeros(o, dtype=np.float32)) for i, o in zip(dims[:-1], dims[1:])]
+    pol = fin.fin_policy_create(fin.FIN_PPO_GAUSS, zero)
+    env = fin.fin_env_create(fcfg, mk)
+    fin.fin_env_set_state(env, cash=dev(cash), hold=zeros((N, K), torch.int16), t_ep=zeros(N, torch.int32))
+    fin.fin_env_counters(env, clear=True)
+    noise = (acts.astype(np.float32) / np.float32(10.0))[None, None]          # [T=1][M=1][N][K]
+    c, h, a = zeros((1, N), torch.float64), zeros((1, N, K), torch.int16), zeros((1, N, K), torch.int16)
+    fin.fin_rollout(env, [pol], 1, fin.make_noise(fin.FIN_NOISE_SUPPLIED, 0, dev(noise)),
+                    fin.make_traj(cash=c, hold=h, actions=a))
+    assert np.array_equal(host(a)[0], acts)
+    assert fin.fin_env_counters(env)["exact_redo"] > 0
+    assert np.array_equal(host(c)[0].view(np.uint64), want_b.view(np.uint64))
+    assert np.array_equal(host(h)[0], want_h)
+
+
 def test_replay_rollout_parity_and_episode_metrics():
     """K4: T steps in one launch; trajectory + online episode metrics vs oracle."""
     import torch
