@@ -749,7 +749,7 @@ def ppo_step(fin, torch, B=65536):
     return {"samples": B, "ms_forward_grad_adam": ms_step, "ms_grad": ms_grad,
             "samples_per_s": B / (ms_step / 1e3), "grad_tflops": flop_grad / (ms_grad / 1e3) / 1e12,
             "grad_frac_of_fp32_simt_peak": flop_grad / (ms_grad / 1e3) / 1e12 / 74.4,
-            "note": "fp32 CUDA-core contractions (first slice); the tensor-core backward is not built"}
+            "note": "fp32 CUDA-core contractions (128 x 128 register-tiled GEMMs for the large shapes); no tensor-core backward"}
 
 
 def market_prep(fin, torch):

@@ -145,18 +145,6 @@ __global__ void k_stats_final(const double* __restrict__ part, int nb, double* _
   }
 }
 
-// ---- g2 = (g3 W3) * [h2 > 0]: one thread per (sample, unit); K3 <= 32 terms
-__global__ void k_back_out(int B, int K, int H2, int Hs, const float* __restrict__ g3, const float* __restrict__ w3,
-                           const uint16_t* __restrict__ hid, float* __restrict__ g2) {
-  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (size_t)B * H2) return;
-  const int s = (int)(i / H2), j = (int)(i % H2);
-  float acc = 0.f;
-  if (bf16_at(hid, ((size_t)s * 2 + 1) * Hs + j) > 0.f)
-    for (int o = 0; o < K; ++o) acc = fmaf(g3[(size_t)s * K + o], w3[(size_t)o * H2 + j], acc);
-  g2[i] = acc;
-}
-
 __global__ void k_adam(int64_t n, float* __restrict__ th, float* __restrict__ m, float* __restrict__ v,
                        const float* __restrict__ g, float b1, float b2, float lr_c, float inv_c2, float eps) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -298,10 +286,11 @@ cudaError_t backward(int B, int in, int H1, int H2, int K, const uint16_t* x, co
   if (e == cudaSuccess) e = cudaMallocAsync(&g1, sizeof(float) * (size_t)B * H1, s);
   if (e == cudaSuccess) e = cudaMallocAsync(&scr, sizeof(float) * scr_n, s);
   if (e != cudaSuccess) return e;
-  const size_t n2 = (size_t)B * H2;
-  k_back_out<<<(unsigned)((n2 + 255) / 256), 256, 0, s>>>(B, K, H2, Hs, g3, w3, hid, g2);
+  // g2 = (g3 W3) * [h2 > 0]: A = g3 [B][K] row-major, B = W3 [K][H2], mask = h2 (row stride 2 Hs)
+  e = gemm<false, kBF32, kMaskBF16>(B, H2, K, g3, K, w3, nullptr, H2, g2, hid + Hs, 2 * Hs, nullptr, 0, scr, s);
   // g1 = (g2 W2) * [h1 > 0]: A = g2 [B][H2] row-major, B = W2 [H2][H1], mask = h1 (row stride 2 Hs)
-  e = gemm<false, kBF32, kMaskBF16>(B, H1, H2, g2, H2, w2, nullptr, H1, g1, hid, 2 * Hs, nullptr, 0, scr, s);
+  if (e == cudaSuccess)
+    e = gemm<false, kBF32, kMaskBF16>(B, H1, H2, g2, H2, w2, nullptr, H1, g1, hid, 2 * Hs, nullptr, 0, scr, s);
   // weight gradients: A = g_l [B][M] (k = sample: AKM), B = activations [B][N]
   if (e == cudaSuccess)
     e = gemm<true, kBBF16, kMaskNone>(K, H2, B, g3, K, nullptr, hid + Hs, 2 * Hs, dw3, nullptr, 0, nullptr, 0, scr, s);
