@@ -90,6 +90,9 @@ struct TcParams {
   unsigned long long* seg_prof;           // debug (FIN_SEG_PROF): [grid][16] globaltimer stamps, or null
 };
 
+#ifndef FIN_PIPE_KICK
+#define FIN_PIPE_KICK 0   // 1: column-split resident plans issue each layer's MMAs in two halves (kPipeKick; A/B: C3 3.56 vs 3.28 us, off)
+#endif
 #ifndef FIN_PREPARE_LAYER
 #define FIN_PREPARE_LAYER 0   // Ops::prepare runs after the kick of layer FIN_PREPARE_LAYER + 1
 #endif
@@ -176,7 +179,14 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
   const int T = p.T;
   constexpr int NS = Plan::kStages;
   constexpr int kTc = Plan::kHidMax > Plan::kOut ? Plan::kHidMax : Plan::kOut;   // TMEM columns per tile
-  constexpr uint32_t kTmemCols = (TILES * kTc <= 128) ? 128 : (TILES * kTc <= 256 ? 256 : 512);
+  // Column-split resident plans (kPipeKick, see run_epi): the next layer's MMAs start while the
+  // epilogue still reads this layer's accumulator, so consecutive layers alternate between two
+  // accumulator banks of kTc columns
+  constexpr bool kPipeKick = SPLIT > 1 && RESIDENT && FIN_PIPE_KICK;
+  constexpr int kBanks = kPipeKick ? 2 : 1;
+  static_assert(TILES * kTc * kBanks <= 512, "TMEM holds 512 fp32 columns");
+  constexpr uint32_t kTmemCols =
+      (TILES * kTc * kBanks <= 128) ? 128 : (TILES * kTc * kBanks <= 256 ? 256 : 512);
   static_assert(TILES * kTc <= 512, "TMEM holds 512 fp32 columns");
 
   uint8_t* sA = smem;                                           // TILES x kA
@@ -382,7 +392,9 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
     const int row = q * 32 + lane;          // env row of the tile == TMEM lane
     const int gtid = (warp - 4 - (tile + part) * 4) * 32 + lane;   // thread index within its warpgroup
     const int env = (blockIdx.x * TILES + tile) * kTileM + row;
-    const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tile * kTc);
+    const uint32_t t_lane0 = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tile * kTc * kBanks);
+    uint32_t t_lane = t_lane0;   // this layer's accumulator bank (kPipeKick: layer l in bank l % 2)
+    auto bank_of = [&](int l) -> uint32_t { return kBanks > 1 ? (uint32_t)((l & 1) * kTc) : 0u; };
     const uint32_t xa = sm100::smem_u32(sA + tile * S::kA);
     uint8_t* stg = sStage + tile * Ops::kStageBytes;
     const int bar_id = 1 + tile;
@@ -392,7 +404,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
     // chunks (the env state lives in registers across the whole rollout).  One loop per
     // addend combination (uniform branch), so an absent addend costs no issue slots.
     auto epi = [&](auto has_b, auto has_add, const float* bl, const float* add, uint4* hlog, int ncol, int c0,
-                   int c1) {
+                   int c1, int cs) {
       constexpr bool HB = decltype(has_b)::value, HA = decltype(has_add)::value;
       // addend b (+ z1s for the factored layer 1) of chunk c, 128-bit broadcast loads
       auto addend = [&](int c, float (&ad)[16]) {
@@ -441,19 +453,19 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
       sm100::tmem_ld16(t_lane + (uint32_t)(c0 * 16), va);
       sm100::tmem_wait_ld();
 #pragma unroll 1
-      for (int c = c0; c < c1; c += 2) {
-        sm100::tmem_ld16(t_lane + (uint32_t)((c + 1) * 16), vb);
+      for (int c = c0; c < c1; c += 2 * cs) {
+        sm100::tmem_ld16(t_lane + (uint32_t)((c + cs) * 16), vb);
         addend(c, ad);
         proc(c, va, ad);
         sm100::tmem_wait_ld();
-        if (c + 2 < c1) sm100::tmem_ld16(t_lane + (uint32_t)((c + 2) * 16), va);
-        addend(c + 1, ad);
-        proc(c + 1, vb, ad);
+        if (c + 2 * cs < c1) sm100::tmem_ld16(t_lane + (uint32_t)((c + 2 * cs) * 16), va);
+        addend(c + cs, ad);
+        proc(c + cs, vb, ad);
         sm100::tmem_wait_ld();
       }
       } else {
 #pragma unroll 1
-      for (int c = c0; c < c1; ++c) {
+      for (int c = c0; c < c1; c += cs) {
         uint32_t v[16];
         sm100::tmem_ld16(t_lane + (uint32_t)(c * 16), v);
         // the addend loads are issued while the TMEM load is in flight
@@ -464,15 +476,21 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
       }
       }
     };
-    auto run_epi = [&](const float* bl, const float* add, uint4* hlog, int ncol, int c0, int c1) {
+    auto run_epi = [&](const float* bl, const float* add, uint4* hlog, int ncol, int c0, int c1, int cs = 1) {
       using T1 = std::true_type;
       using F0 = std::false_type;
       // (bl is uniform; add is null for every thread or for none -- Ops contract)
-      if (bl && add) epi(T1{}, T1{}, bl, add, hlog, ncol, c0, c1);
-      else if (bl) epi(T1{}, F0{}, bl, add, hlog, ncol, c0, c1);
-      else if (add) epi(F0{}, T1{}, bl, add, hlog, ncol, c0, c1);
-      else epi(F0{}, F0{}, bl, add, hlog, ncol, c0, c1);
+      if (bl && add) epi(T1{}, T1{}, bl, add, hlog, ncol, c0, c1, cs);
+      else if (bl) epi(T1{}, F0{}, bl, add, hlog, ncol, c0, c1, cs);
+      else if (add) epi(F0{}, T1{}, bl, add, hlog, ncol, c0, c1, cs);
+      else epi(F0{}, F0{}, bl, add, hlog, ncol, c0, c1, cs);
     };
+    // Column-split resident plans (kPipeKick): each warpgroup takes the chunks c = part (mod SPLIT)
+    // and the next layer's MMAs are issued in two halves -- k-steps [0, K/2) as soon as the first
+    // half of every warpgroup's chunks is in the A operand, the rest after the second half -- so
+    // the issue of the first half (and its tensor work) overlaps the second half of the epilogue.
+    // Same k-step order, so the same accumulation as one issue after the whole epilogue.
+    static_assert(!kPipeKick || ((Plan::kH1 / 16) / 2) % SPLIT == 0, "halves must divide among the warpgroups");
     // this layer's width = the next layer's K (a compile-time constant when all hidden
     // layers have one width, as in the BASELINE nets: the runtime bound cost ~10%)
     constexpr bool kUniformHid = Plan::hid(0) == Plan::hid(1) && (Plan::kNH < 3 || Plan::hid(2) == Plan::hid(0));
@@ -494,10 +512,21 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
             const int ncol = kUniformHid ? Plan::kH1 : Plan::nrows(l);
             const int cpp = (ncol / 16) / SPLIT;
             uint4* hlog = reinterpret_cast<uint4*>(Ops::helper_hidden_ptr(p, env, t, m, l, Plan::kHidMax));
-            run_epi(bl, nullptr, hlog, ncol, part * cpp, (part + 1) * cpp);
-            sm100::fence_proxy_async_smem();
-            sm100::tc_fence_before();
-            sm100::named_bar_sync(kSplitBar, 128 * SPLIT);
+            t_lane = t_lane0 + bank_of(l);
+            if constexpr (kPipeKick) {
+              const int nch = ncol / 16;
+              for (int h = 0; h < 2; ++h) {
+                run_epi(bl, nullptr, hlog, ncol, h * (nch / 2) + part, (h + 1) * (nch / 2), SPLIT);
+                sm100::fence_proxy_async_smem();
+                sm100::tc_fence_before();
+                sm100::named_bar_sync(kSplitBar, 128 * SPLIT);
+              }
+            } else {
+              run_epi(bl, nullptr, hlog, ncol, part * cpp, (part + 1) * cpp);
+              sm100::fence_proxy_async_smem();
+              sm100::tc_fence_before();
+              sm100::named_bar_sync(kSplitBar, 128 * SPLIT);
+            }
           }
           // the output layer's phase (read by the first warpgroup only) must still be waited
           // for: parity waits only tell the current phase from the previous one
@@ -513,7 +542,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
     bool w_ready = false;   // resident weights landed (env-issued MMAs)
     int t_cur = 0;          // (the timeline's step index inside kick)
     // A operand of layer l of member m written by this thread: hand it to the tensor core
-    auto kick = [&](int m, int l) {
+    auto kick = [&](int m, int l, int half = -1) {   // half 0 / 1: kPipeKick's k-step halves (commit after 1)
       sm100::fence_proxy_async_smem();
       sm100::tc_fence_before();
       if constexpr (kEnvIssue) {
@@ -529,7 +558,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
           const uint32_t a_sbo = (uint32_t)(Plan::kdim(l) / 8) * 128u;
           const uint32_t idesc = sm100::make_idesc_bf16(kTileM, Plan::nrows(l));
           const uint32_t a_base = sm100::smem_u32(sA) + (uint32_t)(tile * S::kA);
-          const uint32_t d_tmem = tmem + (uint32_t)(tile * kTc);
+          const uint32_t d_tmem = tmem + (uint32_t)(tile * kTc * kBanks) + bank_of(l);
           // layer 1 of a tile whose envs share the step's row (Ops::kL1Bcast): k-steps >= 1 read
           // one 8-row core-matrix column per k-group with SBO = 0, so every 8-row group of the
           // tile sees the same shared inputs (same operand values, same MMA sequence)
@@ -542,14 +571,17 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
             const uint32_t b_sbo = (uint32_t)(nks * 2) * 128u;
             const uint64_t ad0 = sm100::make_sdesc(a_base + (uint32_t)j0 * 256u, 128u, a_sbo);
             const uint64_t bd0 = sm100::make_sdesc(b_base, 128u, b_sbo);
+            const int ks = Plan::ksteps(l);
+            const int jlo = half == 1 ? ks / 2 : 0, jhi = half == 0 ? ks / 2 : ks;
             for (int j = 0; j < nks; ++j) {
+              if (half >= 0 && (j0 + j < jlo || j0 + j >= jhi)) continue;
               uint64_t ad = ad0 + (uint64_t)(16 * j);
               if (bc && j0 + j > 0) ad = sm100::make_sdesc(bc + (uint32_t)(j0 + j - 1) * 256u, 128u, 0u);
               sm100::mma_bf16(d_tmem, ad, bd0 + (uint64_t)(16 * j), idesc, (l1init || (j0 + j) > 0) ? 1u : 0u);
             }
           }
           FIN_TR(tile == 0 && m == 0 && l == 0, t_cur, 26);
-          sm100::mma_commit(&d_full[tile]);
+          if (half != 0) sm100::mma_commit(&d_full[tile]);
         }
       } else {
         sm100::mbar_arrive(a_full);
@@ -605,7 +637,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
       for (int m = 0; m < M; ++m) {
         if constexpr (Ops::kL1Bcast && kEnvIssue) Ops::build_obs_bcast(st, p, env, row, t, m, xa, stg);
         else Ops::build_obs(st, p, env, row, t, m, xa, stg);
-        if constexpr (Ops::kL1Init) Ops::l1_init_rows(st, p, t_lane, stg);
+        if constexpr (Ops::kL1Init) Ops::l1_init_rows(st, p, t_lane0, stg);
         kick(m, 0);
         FIN_TR(row == 0 && tile == 0 && m == 0, t, 1);
         // biases of the first FIN_STAGE_MEMBERS members in shared memory, the rest from L2
@@ -623,8 +655,17 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
           const float* add = l == 0 ? Ops::l1_addend(st, p, m, stg) : nullptr;
           // debug / parity log of the bf16 hidden activations (teacher-forced layer checks)
           uint4* hlog = reinterpret_cast<uint4*>(Ops::hidden_ptr(st, p, env, t, m, l, Plan::kHidMax));
-          run_epi(bl, add, hlog, ncol, 0, (ncol / 16) / SPLIT);
-          kick(m, l + 1);
+          t_lane = t_lane0 + bank_of(l);
+          if constexpr (kPipeKick) {
+            const int nch = ncol / 16;
+            run_epi(bl, add, hlog, ncol, 0, nch / 2, SPLIT);
+            kick(m, l + 1, 0);
+            run_epi(bl, add, hlog, ncol, nch / 2, nch, SPLIT);
+            kick(m, l + 1, 1);
+          } else {
+            run_epi(bl, add, hlog, ncol, 0, (ncol / 16) / SPLIT);
+            kick(m, l + 1);
+          }
           // work that does not depend on the network output (e.g. the step's noise)
           // overlaps the largest MMA (layer 2) instead of following the last one
           if (l == (Plan::kNH > FIN_PREPARE_LAYER ? FIN_PREPARE_LAYER : Plan::kNH - 1)) Ops::prepare(st, p, env, t, m);
@@ -636,6 +677,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
         FIN_TR(row == 0 && tile == 0 && m == 0, t, 6);
         sm100::tc_fence_after();
         float z[Plan::kOut];
+        t_lane = t_lane0 + bank_of(Plan::kNH);
 #pragma unroll
         for (int c = 0; c < Plan::kOut / 16; ++c) {
           uint32_t v[16];
