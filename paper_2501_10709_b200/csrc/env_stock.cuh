@@ -96,9 +96,9 @@ __device__ __forceinline__ double stock_buys_redo(double b, int (&h)[KA], const 
   return b;
 }
 
-// K1's E-env form keeps the redo out of line (through local arrays, only on that path): measured
-// +1.2% for K1 (2,836 vs 2,804 GB/s), whose few live values survive the call unspilled; the fused
-// rollout (stock_trade) inlines it (no call: +7%)
+// K1's E-env form keeps the redo out of line (through local arrays, only on that path, the actions
+// copied there so the caller's stay in registers): measured +3.1% for K1 (2,890 vs 2,803 GB/s), whose
+// few live values survive the call unspilled; the fused rollout (stock_trade) inlines it (no call: +7%)
 #ifndef FIN_REDO_CALL
 #define FIN_REDO_CALL 1
 #endif
@@ -119,7 +119,8 @@ __device__ __forceinline__ double stock_buys_redo_call(double b, int (&h)[KA], c
   int hh[KA];
 #pragma unroll
   for (int k = 0; k < KA; ++k) hh[k] = h[k];
-  b = stock_buys_redo_ool<KA, Acts>(b, hh, &a, save, save_stride, U, MU);
+  Acts ac = a;   // a copy on this (rare) path: the caller's actions stay in registers
+  b = stock_buys_redo_ool<KA, Acts>(b, hh, &ac, save, save_stride, U, MU);
 #pragma unroll
   for (int k = 0; k < KA; ++k) h[k] = hh[k];
   return b;
