@@ -319,3 +319,50 @@ def test_value_update_matches_oracle():
     v.forward(xf, out)
     L1, _ = olearn.critic_head(host(out)[:, 0].astype(np.float64), host(R).astype(np.float64))
     assert L1 < L0
+
+
+def test_learner_contractions_are_deterministic():
+    """The split-K contractions sum their partials in a fixed order: two identical calls of the
+    critic backward (B = 65,536, split over the batch) and of the PPO gradient give the same bits."""
+    import torch
+    from paper_2501_10709_b200 import fin
+    from paper_2501_10709_b200.learner import DenseNet
+    g = torch.Generator(device="cuda").manual_seed(3)
+    B = 65536
+    net = DenseNet(CRITIC, 7)
+    x = torch.randn((B, S + K), device="cuda", generator=g)
+    hid = zeros((B, 512), torch.float32)
+    out = zeros((B, 1), torch.float32)
+    net.forward(x, out, hid)
+    go = torch.randn((B, 1), device="cuda", generator=g)
+    res = []
+    for _ in range(2):
+        gx = zeros((B, S + K), torch.float32)
+        fin.fin_dense_backward(x, hid, go, net.weights(), grads=net.grads, g_x=gx)
+        res.append([host(t).copy() for pair in net.grads for t in pair] + [host(gx)])
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
+
+
+def test_ac_entry_points_reject_bad_arguments():
+    """Shape and argument errors are refused before any launch (FIN_E_CONFIG / ValueError)."""
+    import torch
+    from paper_2501_10709_b200 import fin
+    z = zeros((4, K), torch.float32)
+    a = zeros((4, K), torch.float32)
+    st = zeros(4, torch.float64)
+    with pytest.raises(ValueError):
+        fin.fin_concat_obs_action(zeros((4, S), torch.int16), zeros((5, K), torch.float32), zeros((4, S + K), torch.float32))
+    with pytest.raises(fin.FinError):
+        fin.fin_squash(z, a, eps=z, sigma=0.0)
+    with pytest.raises(fin.FinError):   # twin critics without log pi (SAC's head needs it)
+        fin.fin_actor_head(a, zeros(4, torch.float32), z, zeros((4, K), torch.float32), st, q2=zeros(4, torch.float32),
+                           dq2=z)
+    with pytest.raises(fin.FinError):
+        fin.fin_critic_head(zeros(4, torch.float32), zeros(4, torch.float32), zeros(4, torch.uint8),
+                            zeros(4, torch.float32), zeros(4, torch.float32), st, gamma=1.5)
+    with pytest.raises(fin.FinError):
+        fin.fin_soft_update(zeros(8, torch.float32), zeros(8, torch.float32), tau=2.0)
+    with pytest.raises(ValueError):
+        fin.fin_dense_forward(zeros((4, 10), torch.float32),
+                              [(zeros((8, 9), torch.float32), zeros(8, torch.float32))] * 3, zeros((4, 1), torch.float32))
