@@ -141,7 +141,16 @@ __global__ void k_soft_update(int64_t n, float* __restrict__ t, const float* __r
 
 }  // namespace
 
+#ifndef FIN_TC_WGRAD
+#define FIN_TC_WGRAD 1
+#endif
+
 namespace fin {
+
+cudaError_t launch_wgrad_tc(int M, int N, int K, const float* g, int ldg, const uint16_t* xh, const float* xf,
+                            int ldx, float* dw, cudaStream_t s);
+cudaError_t launch_gemm_tc(int M, int N, int K, const float* g, int ldg, int arow, const uint16_t* xh, const float* xf,
+                           int ldx, float* C, const void* mask, int ldm, int maskf, cudaStream_t s);
 
 cudaError_t launch_concat_sa(int B, int S, const uint16_t* x, int K, const float* a, float* out, cudaStream_t s) {
   const int64_t n = (int64_t)B * (S + K);
@@ -236,6 +245,12 @@ cudaError_t dense_backward(int B, int in, int H1, int H2, int O, const float* x,
   if (e == cudaSuccess) e = cudaMallocAsync(&g1, sizeof(float) * (size_t)B * H1, s);
   if (e == cudaSuccess) e = cudaMallocAsync(&scr, sizeof(float) * scr_n, s);
   if (e != cudaSuccess) return e;
+#if FIN_TC_WGRAD
+  // g2 = (g3 W3) * [h2 > 0], g1 = (g2 W2) * [h1 > 0], g_x = g1 W1 (rows = samples) on the tensor cores
+  e = gemm<false, kBF32, kMaskF32>(B, H2, O, g3, O, w3, nullptr, H2, g2, hid + H1, Hs, nullptr, 0, nullptr, s);
+  if (e == cudaSuccess) e = launch_gemm_tc(B, H1, H2, g2, H2, 1, nullptr, w2, H1, g1, hid, Hs, 1, s);
+  if (e == cudaSuccess && gx) e = launch_gemm_tc(B, in, H1, g1, H1, 1, nullptr, w1, in, gx, nullptr, 0, 0, s);
+#else
   // g2 = (g3 W3) * [h2 > 0]: A = g3 [B][O], B = W3 [O][H2]; g1 = (g2 W2) * [h1 > 0]
   e = gemm<false, kBF32, kMaskF32>(B, H2, O, g3, O, w3, nullptr, H2, g2, hid + H1, Hs, nullptr, 0, nullptr, s);
   if (e == cudaSuccess)
@@ -243,12 +258,19 @@ cudaError_t dense_backward(int B, int in, int H1, int H2, int O, const float* x,
   // g_x = g1 W1: A = g1 [B][H1], B = W1 [H1][in]
   if (e == cudaSuccess && gx)
     e = gemm<false, kBF32, kMaskNone>(B, in, H1, g1, H1, w1, nullptr, in, gx, nullptr, 0, nullptr, 0, scr, s);
+#endif
   if (e == cudaSuccess && params) {
+#if FIN_TC_WGRAD
+    e = launch_wgrad_tc(O, H2, B, g3, O, nullptr, hid + H1, Hs, dw3, s);
+    if (e == cudaSuccess) e = launch_wgrad_tc(H2, H1, B, g2, H2, nullptr, hid, Hs, dw2, s);
+    if (e == cudaSuccess) e = launch_wgrad_tc(H1, in, B, g1, H1, nullptr, x, in, dw1, s);
+#else
     e = gemm<true, kBF32, kMaskNone>(O, H2, B, g3, O, hid + H1, nullptr, Hs, dw3, nullptr, 0, nullptr, 0, scr, s);
     if (e == cudaSuccess)
       e = gemm<true, kBF32, kMaskNone>(H2, H1, B, g2, H2, hid, nullptr, Hs, dw2, nullptr, 0, nullptr, 0, scr, s);
     if (e == cudaSuccess)
       e = gemm<true, kBF32, kMaskNone>(H1, in, B, g1, H1, x, nullptr, in, dw1, nullptr, 0, nullptr, 0, scr, s);
+#endif
     colsum(B, O, g3, O, db3, scr, s);
     colsum(B, H2, g2, H2, db2, scr, s);
     colsum(B, H1, g1, H1, db1, scr, s);

@@ -244,7 +244,16 @@ __global__ void k_to_bf16(int64_t n, const float* __restrict__ x, uint16_t* __re
 
 }  // namespace
 
+#ifndef FIN_TC_WGRAD
+#define FIN_TC_WGRAD 1   // weight gradients on the tensor cores (tc_wgrad.cu); 0: fp32 CUDA-core GEMMs
+#endif
+
 namespace fin {
+
+cudaError_t launch_wgrad_tc(int M, int N, int K, const float* g, int ldg, const uint16_t* xh, const float* xf,
+                            int ldx, float* dw, cudaStream_t s);
+cudaError_t launch_gemm_tc(int M, int N, int K, const float* g, int ldg, int arow, const uint16_t* xh, const float* xf,
+                           int ldx, float* C, const void* mask, int ldm, int maskf, cudaStream_t s);
 
 cudaError_t launch_gather_obs(const EnvDev& e, const uint16_t* priv, int P, const int32_t* day, const int64_t* idx,
                               int B, uint16_t* x, cudaStream_t s) {
@@ -286,18 +295,33 @@ cudaError_t backward(int B, int in, int H1, int H2, int K, const uint16_t* x, co
   if (e == cudaSuccess) e = cudaMallocAsync(&g1, sizeof(float) * (size_t)B * H1, s);
   if (e == cudaSuccess) e = cudaMallocAsync(&scr, sizeof(float) * scr_n, s);
   if (e != cudaSuccess) return e;
+#if FIN_TC_WGRAD
+  // g2 = (g3 W3) * [h2 > 0], g1 = (g2 W2) * [h1 > 0] (rows = samples; masks = the hidden log, row
+  // stride 2 Hs) on the tensor cores
+  // (the short K = k_out contraction stays on the CUDA cores: 77 vs 170 us at B = 65,536)
+  e = gemm<false, kBF32, kMaskBF16>(B, H2, K, g3, K, w3, nullptr, H2, g2, hid + Hs, 2 * Hs, nullptr, 0, scr, s);
+  if (e == cudaSuccess) e = launch_gemm_tc(B, H1, H2, g2, H2, 1, nullptr, w2, H1, g1, hid, 2 * Hs, 0, s);
+#else
   // g2 = (g3 W3) * [h2 > 0]: A = g3 [B][K] row-major, B = W3 [K][H2], mask = h2 (row stride 2 Hs)
   e = gemm<false, kBF32, kMaskBF16>(B, H2, K, g3, K, w3, nullptr, H2, g2, hid + Hs, 2 * Hs, nullptr, 0, scr, s);
   // g1 = (g2 W2) * [h1 > 0]: A = g2 [B][H2] row-major, B = W2 [H2][H1], mask = h1 (row stride 2 Hs)
   if (e == cudaSuccess)
     e = gemm<false, kBF32, kMaskBF16>(B, H1, H2, g2, H2, w2, nullptr, H1, g1, hid, 2 * Hs, nullptr, 0, scr, s);
-  // weight gradients: A = g_l [B][M] (k = sample: AKM), B = activations [B][N]
+#endif
+  // weight gradients dW_l = g_l^T a_l over the batch (a_l the bf16 activations): tensor cores
+#if FIN_TC_WGRAD
+  if (e == cudaSuccess) e = launch_wgrad_tc(K, H2, B, g3, K, hid + Hs, nullptr, 2 * Hs, dw3, s);
+  if (e == cudaSuccess) e = launch_wgrad_tc(H2, H1, B, g2, H2, hid, nullptr, 2 * Hs, dw2, s);
+  if (e == cudaSuccess) e = launch_wgrad_tc(H1, in, B, g1, H1, x, nullptr, in, dw1, s);
+#else
+  // (CUDA-core form: A = g_l [B][M] (k = sample: AKM), B = activations [B][N])
   if (e == cudaSuccess)
     e = gemm<true, kBBF16, kMaskNone>(K, H2, B, g3, K, nullptr, hid + Hs, 2 * Hs, dw3, nullptr, 0, nullptr, 0, scr, s);
   if (e == cudaSuccess)
     e = gemm<true, kBBF16, kMaskNone>(H2, H1, B, g2, H2, nullptr, hid, 2 * Hs, dw2, nullptr, 0, nullptr, 0, scr, s);
   if (e == cudaSuccess)
     e = gemm<true, kBBF16, kMaskNone>(H1, in, B, g1, H1, nullptr, x, in, dw1, nullptr, 0, nullptr, 0, scr, s);
+#endif
   // (scr is free again: the split partials were reduced above)
   colsum(B, K, g3, K, db3, scr, s);
   colsum(B, H2, g2, H2, db2, scr, s);
