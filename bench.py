@@ -697,7 +697,7 @@ def ac_update(fin, torch, kind: str, B: int):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 5
     return {"samples": B, "ms_per_update": ms, "samples_per_s": B / (ms / 1e3),
-            "note": "fp32 CUDA-core critics; includes the actor's fin_policy_load (device gather)"}
+            "note": "critic layers and weight gradients on the tensor cores (bf16 hi/lo split), heads in float64; includes the actor's fin_policy_load (device gather)"}
 
 
 def ppo_step(fin, torch, B=65536):

@@ -150,7 +150,8 @@ namespace fin {
 cudaError_t launch_wgrad_tc(int M, int N, int K, const float* g, int ldg, const uint16_t* xh, const float* xf,
                             int ldx, float* dw, cudaStream_t s);
 cudaError_t launch_gemm_tc(int M, int N, int K, const float* g, int ldg, int arow, const uint16_t* xh, const float* xf,
-                           int ldx, float* C, const void* mask, int ldm, int maskf, cudaStream_t s);
+                           int ldx, float* C, const void* mask, int ldm, int maskf, cudaStream_t s, int wt = 0,
+                           const float* bias = nullptr, int relu = 0);
 
 cudaError_t launch_concat_sa(int B, int S, const uint16_t* x, int K, const float* a, float* out, cudaStream_t s) {
   const int64_t n = (int64_t)B * (S + K);
@@ -209,9 +210,16 @@ cudaError_t dense_forward(int B, int in, int H1, int H2, int O, const float* x, 
   cudaError_t e = cudaMallocAsync(&h1, sizeof(float) * (size_t)B * H1, s);
   if (e == cudaSuccess) e = cudaMallocAsync(&h2, sizeof(float) * (size_t)B * H2, s);
   if (e != cudaSuccess) return e;
+#if FIN_TC_WGRAD
+  // the two wide layers on the tensor cores (weights pre-split once per call), the output layer (N = O,
+  // a few columns) on the CUDA cores
+  e = launch_gemm_tc(B, H1, in, x, in, 1, nullptr, w1, in, h1, nullptr, 0, 0, s, 1, b1, 1);
+  if (e == cudaSuccess) e = launch_gemm_tc(B, H2, H1, h1, H1, 1, nullptr, w2, H1, h2, nullptr, 0, 0, s, 1, b2, 1);
+#else
   e = gemm<false, kBF32T, kMaskNone>(B, H1, in, x, in, w1, nullptr, in, h1, nullptr, 0, b1, 1, nullptr, s);
   if (e == cudaSuccess)
     e = gemm<false, kBF32T, kMaskNone>(B, H2, H1, h1, H1, w2, nullptr, H1, h2, nullptr, 0, b2, 1, nullptr, s);
+#endif
   if (e == cudaSuccess)
     e = gemm<false, kBF32T, kMaskNone>(B, O, H2, h2, H2, w3, nullptr, H2, out, nullptr, 0, b3, 0, nullptr, s);
   if (e == cudaSuccess && hid) {

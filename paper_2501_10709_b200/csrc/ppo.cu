@@ -253,7 +253,8 @@ namespace fin {
 cudaError_t launch_wgrad_tc(int M, int N, int K, const float* g, int ldg, const uint16_t* xh, const float* xf,
                             int ldx, float* dw, cudaStream_t s);
 cudaError_t launch_gemm_tc(int M, int N, int K, const float* g, int ldg, int arow, const uint16_t* xh, const float* xf,
-                           int ldx, float* C, const void* mask, int ldm, int maskf, cudaStream_t s);
+                           int ldx, float* C, const void* mask, int ldm, int maskf, cudaStream_t s, int wt = 0,
+                           const float* bias = nullptr, int relu = 0);
 
 cudaError_t launch_gather_obs(const EnvDev& e, const uint16_t* priv, int P, const int32_t* day, const int64_t* idx,
                               int B, uint16_t* x, cudaStream_t s) {

@@ -55,7 +55,8 @@ __global__ void __launch_bounds__(kThreads) k_wgrad_tc(int M, int N, int K, int 
                                                       int ldg, const uint16_t* __restrict__ xh,
                                                       const float* __restrict__ xf, int ldx,
                                                       float* __restrict__ out, const void* __restrict__ mask,
-                                                      int ldm, const uint4* __restrict__ bpk = nullptr) {
+                                                      int ldm, const uint4* __restrict__ bpk = nullptr,
+                                                      const float* __restrict__ bias = nullptr, int relu = 0) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int kStage = 2 * kTileA + (XF32 ? 2 : 1) * kTileB;
   __shared__ uint64_t done[2];
@@ -113,10 +114,9 @@ __global__ void __launch_bounds__(kThreads) k_wgrad_tc(int M, int N, int K, int 
       const uint4* src = bpk + ((size_t)blockIdx.x * nbt + (size_t)(k0 / kKB + b)) * (2 * 256 * 4);
 #pragma unroll
       for (int j = 0; j < 8; ++j) xp[j] = __ldg(src + tid + 256 * j);
-      return;
     }
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < (BPACK ? 0 : 2); ++h) {
       const int n = r + 128 * h;
       const bool nv = n < nt && n0 + n < N;
 #pragma unroll
@@ -211,6 +211,8 @@ __global__ void __launch_bounds__(kThreads) k_wgrad_tc(int M, int N, int K, int 
         const int n = n0 + c * 16 + j;
         if (n < N) {
           float y = __uint_as_float(v[j]);
+          if (bias) y += bias[n];   // (not split: the forward's epilogue, z = x W^T + b, then ReLU)
+          if (relu) y = fmaxf(y, 0.f);
           if constexpr (MASK) {
             const bool on = MASKF ? static_cast<const float*>(mask)[(size_t)m * ldm + n] > 0.f
                                   : gemmf::bf16_at(static_cast<const uint16_t*>(mask), (size_t)m * ldm + n) > 0.f;
@@ -231,6 +233,8 @@ __global__ void __launch_bounds__(kThreads) k_wgrad_tc(int M, int N, int K, int 
 
 // W [K][ldw] fp32 (K x N) -> per 256-column tile t and 32-row block b: the hi image then the lo image of
 // the B operand tile (256 rows n x 32 k, K-major canonical), rows n >= N zero; one thread per 8 k of a row
+// WT: W is stored [N][ldw] (the out-major weight of a forward layer: B(k, n) = W[n][k]), else [K][ldw]
+template <bool WT>
 __global__ void k_pack_b(int K, int N, const float* __restrict__ w, int ldw, uint4* __restrict__ out) {
   const int nbt = (K + kKB - 1) / kKB;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -244,7 +248,7 @@ __global__ void k_pack_b(int K, int N, const float* __restrict__ w, int ldw, uin
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const int k = b * kKB + kc * 8 + j;
-    v[j] = (col < N && k < K) ? w[(size_t)k * ldw + col] : 0.f;
+    v[j] = (col < N && k < K) ? (WT ? w[(size_t)col * ldw + k] : w[(size_t)k * ldw + col]) : 0.f;
   }
   uint32_t hi[4], lo[4];
 #pragma unroll
@@ -261,10 +265,12 @@ namespace fin {
 
 template <bool XF32, bool AROW, bool MASK, bool MASKF, bool BPACK>
 static cudaError_t run_tc_p(dim3 grid, int bytes, cudaStream_t s, int M, int N, int K, int kchunk, const float* g,
-                            int ldg, const float* xf, int ldx, float* out, const void* mask, int ldm, const uint4* bp) {
+                            int ldg, const float* xf, int ldx, float* out, const void* mask, int ldm, const uint4* bp,
+                            const float* bias, int relu) {
   auto kern = k_wgrad_tc<XF32, AROW, MASK, MASKF, BPACK>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) kern<<<grid, kThreads, bytes, s>>>(M, N, K, kchunk, g, ldg, nullptr, xf, ldx, out, mask, ldm, bp);
+  if (e == cudaSuccess)
+    kern<<<grid, kThreads, bytes, s>>>(M, N, K, kchunk, g, ldg, nullptr, xf, ldx, out, mask, ldm, bp, bias, relu);
   return e;
 }
 
@@ -284,13 +290,14 @@ static cudaError_t run_tc(dim3 grid, int bytes, cudaStream_t s, int M, int N, in
 // batch-long contractions over CTAs (partials summed in a fixed order); allocates stream-ordered scratch
 // for them and frees it on the stream.
 cudaError_t launch_gemm_tc(int M, int N, int K, const float* g, int ldg, int arow, const uint16_t* xh, const float* xf,
-                           int ldx, float* C, const void* mask, int ldm, int maskf, cudaStream_t s) {
+                           int ldx, float* C, const void* mask, int ldm, int maskf, cudaStream_t s, int wt,
+                           const float* bias, int relu) {
   const int gx = (N + 255) / 256, gy = (M + 127) / 128;
   const int tiles = gx * gy;
   int splits = (2 * 148 + tiles - 1) / tiles;
   const int maxs = (K + 8 * kKB - 1) / (8 * kKB);   // >= 256 batch rows per split
   if (splits > maxs) splits = maxs;
-  if (splits < 1 || mask) splits = 1;
+  if (splits < 1 || mask || bias || relu) splits = 1;
   const int kchunk = ((K + splits - 1) / splits + kKB - 1) / kKB * kKB;
   const int used = K > 0 ? (K + kchunk - 1) / kchunk : 1;
   float* part = C;
@@ -309,10 +316,17 @@ cudaError_t launch_gemm_tc(int M, int N, int K, const float* g, int ldg, int aro
     e = cudaMallocAsync(&bp, n16 * 16, s);
     if (e != cudaSuccess) return e;
     const int64_t threads = (int64_t)gx * nbt * 256 * 4;
-    k_pack_b<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(K, N, xf, ldx, bp);
-    if (!mask) e = run_tc_p<true, true, false, false, true>(grid, bytes, s, M, N, K, kchunk, g, ldg, xf, ldx, C, nullptr, 0, bp);
-    else if (maskf) e = run_tc_p<true, true, true, true, true>(grid, bytes, s, M, N, K, kchunk, g, ldg, xf, ldx, C, mask, ldm, bp);
-    else e = run_tc_p<true, true, true, false, true>(grid, bytes, s, M, N, K, kchunk, g, ldg, xf, ldx, C, mask, ldm, bp);
+    if (wt) k_pack_b<true><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(K, N, xf, ldx, bp);
+    else k_pack_b<false><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(K, N, xf, ldx, bp);
+    if (!mask)
+      e = run_tc_p<true, true, false, false, true>(grid, bytes, s, M, N, K, kchunk, g, ldg, xf, ldx, C, nullptr, 0, bp,
+                                                   bias, relu);
+    else if (maskf)
+      e = run_tc_p<true, true, true, true, true>(grid, bytes, s, M, N, K, kchunk, g, ldg, xf, ldx, C, mask, ldm, bp,
+                                                 bias, relu);
+    else
+      e = run_tc_p<true, true, true, false, true>(grid, bytes, s, M, N, K, kchunk, g, ldg, xf, ldx, C, mask, ldm, bp,
+                                                  bias, relu);
     if (e == cudaSuccess) e = cudaGetLastError();
     cudaFreeAsync(bp, s);
     return e;
@@ -342,7 +356,7 @@ cudaError_t launch_gemm_tc(int M, int N, int K, const float* g, int ldg, int aro
 // dW [M][N] = sum_k G[k * ldg + m] X[k * ldx + n] over k < K (X bf16 bits xh or fp32 xf)
 cudaError_t launch_wgrad_tc(int M, int N, int K, const float* g, int ldg, const uint16_t* xh, const float* xf,
                             int ldx, float* dw, cudaStream_t s) {
-  return launch_gemm_tc(M, N, K, g, ldg, 0, xh, xf, ldx, dw, nullptr, 0, 0, s);
+  return launch_gemm_tc(M, N, K, g, ldg, 0, xh, xf, ldx, dw, nullptr, 0, 0, s, 0, nullptr, 0);
 }
 
 }  // namespace fin
