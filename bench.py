@@ -749,7 +749,7 @@ def ppo_step(fin, torch, B=65536):
     return {"samples": B, "ms_forward_grad_adam": ms_step, "ms_grad": ms_grad,
             "samples_per_s": B / (ms_step / 1e3), "grad_tflops": flop_grad / (ms_grad / 1e3) / 1e12,
             "grad_frac_of_fp32_simt_peak": flop_grad / (ms_grad / 1e3) / 1e12 / 74.4,  # (context: mixed TC / CUDA-core path)
-            "note": "weight gradients and the K = 256 backpropagated product on the tensor cores (tc_wgrad.cu: bf16 hi/lo split operands, fp32 accumulation); the K = 30 product and the forward on fp32 CUDA cores; grad_tflops counts the useful FLOPs"}
+            "note": "weight gradients and the K = 256 backpropagated product on the tensor cores (tc_gemm.cu: bf16 hi/lo split operands, fp32 accumulation); the K = 30 product and the forward on fp32 CUDA cores; grad_tflops counts the useful FLOPs"}
 
 
 def market_prep(fin, torch):

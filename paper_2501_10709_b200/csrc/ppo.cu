@@ -245,7 +245,7 @@ __global__ void k_to_bf16(int64_t n, const float* __restrict__ x, uint16_t* __re
 }  // namespace
 
 #ifndef FIN_TC_WGRAD
-#define FIN_TC_WGRAD 1   // weight gradients on the tensor cores (tc_wgrad.cu); 0: fp32 CUDA-core GEMMs
+#define FIN_TC_WGRAD 1   // weight gradients on the tensor cores (tc_gemm.cu); 0: fp32 CUDA-core GEMMs
 #endif
 
 namespace fin {

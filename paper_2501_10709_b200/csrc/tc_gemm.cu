@@ -1,4 +1,5 @@
-// tc_wgrad.cu -- the learner's weight-gradient contractions dW = G^T X on the tensor cores
+// tc_gemm.cu -- the learner's contractions on the tensor cores: weight gradients dW = G^T X, the
+// backpropagated products g W and the critics' forward layers x W^T + b
 // (the backward passes of fin_ppo_grad / fin_dqn_grad / fin_policy_backward and
 // fin_dense_backward, readings R-PPO / R-DQN / R-AC).
 //
@@ -51,7 +52,7 @@ __device__ __forceinline__ void split_pair(float a, float b, uint32_t& hi, uint3
 // BPACK (with XF32): X is a weight matrix already split and laid out by k_pack_b -- per 256-column
 // tile and 32-row block, the hi then the lo tile image -- so its staging is 16-byte copies.
 template <bool XF32, bool AROW, bool MASK, bool MASKF, bool BPACK = false>
-__global__ void __launch_bounds__(kThreads) k_wgrad_tc(int M, int N, int K, int kchunk, const float* __restrict__ g,
+__global__ void __launch_bounds__(kThreads) k_gemm_tc(int M, int N, int K, int kchunk, const float* __restrict__ g,
                                                       int ldg, const uint16_t* __restrict__ xh,
                                                       const float* __restrict__ xf, int ldx,
                                                       float* __restrict__ out, const void* __restrict__ mask,
@@ -267,7 +268,7 @@ template <bool XF32, bool AROW, bool MASK, bool MASKF, bool BPACK>
 static cudaError_t run_tc_p(dim3 grid, int bytes, cudaStream_t s, int M, int N, int K, int kchunk, const float* g,
                             int ldg, const float* xf, int ldx, float* out, const void* mask, int ldm, const uint4* bp,
                             const float* bias, int relu) {
-  auto kern = k_wgrad_tc<XF32, AROW, MASK, MASKF, BPACK>;
+  auto kern = k_gemm_tc<XF32, AROW, MASK, MASKF, BPACK>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess)
     kern<<<grid, kThreads, bytes, s>>>(M, N, K, kchunk, g, ldg, nullptr, xf, ldx, out, mask, ldm, bp, bias, relu);
@@ -278,7 +279,7 @@ template <bool XF32, bool AROW, bool MASK, bool MASKF>
 static cudaError_t run_tc(dim3 grid, int bytes, cudaStream_t s, int M, int N, int K, int kchunk, const float* g,
                           int ldg, const uint16_t* xh, const float* xf, int ldx, float* out, const void* mask,
                           int ldm) {
-  auto kern = k_wgrad_tc<XF32, AROW, MASK, MASKF>;
+  auto kern = k_gemm_tc<XF32, AROW, MASK, MASKF>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) kern<<<grid, kThreads, bytes, s>>>(M, N, K, kchunk, g, ldg, xh, xf, ldx, out, mask, ldm, nullptr);
   return e;
