@@ -281,7 +281,8 @@ static cudaError_t run_tc(dim3 grid, int bytes, cudaStream_t s, int M, int N, in
                           int ldm) {
   auto kern = k_gemm_tc<XF32, AROW, MASK, MASKF>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) kern<<<grid, kThreads, bytes, s>>>(M, N, K, kchunk, g, ldg, xh, xf, ldx, out, mask, ldm, nullptr);
+  if (e == cudaSuccess)
+    kern<<<grid, kThreads, bytes, s>>>(M, N, K, kchunk, g, ldg, xh, xf, ldx, out, mask, ldm, nullptr, nullptr, 0);
   return e;
 }
 
