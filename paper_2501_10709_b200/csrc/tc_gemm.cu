@@ -206,7 +206,47 @@ __global__ void __launch_bounds__(kThreads) k_gemm_tc(int M, int N, int K, int k
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = 0u;
     }
-    if (m < M) {
+    const int nb = n0 + c * 16;
+    // full 16-column chunk of an aligned row: 16-byte mask loads and stores
+    const bool vec = m < M && nb + 16 <= N && (N & 3) == 0 && (!MASK || MASKF || (ldm & 7) == 0) &&
+                     (!MASK || !MASKF || (ldm & 3) == 0);
+    if (vec) {
+      float y[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        y[j] = __uint_as_float(v[j]);
+        if (bias) y[j] += bias[nb + j];
+        if (relu) y[j] = fmaxf(y[j], 0.f);
+      }
+      if constexpr (MASK) {
+        if constexpr (MASKF) {
+          const float4* mk = reinterpret_cast<const float4*>(static_cast<const float*>(mask) + (size_t)m * ldm + nb);
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const float4 mm = __ldg(mk + q4);
+            if (!(mm.x > 0.f)) y[4 * q4] = 0.f;
+            if (!(mm.y > 0.f)) y[4 * q4 + 1] = 0.f;
+            if (!(mm.z > 0.f)) y[4 * q4 + 2] = 0.f;
+            if (!(mm.w > 0.f)) y[4 * q4 + 3] = 0.f;
+          }
+        } else {
+          const uint4* mk = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(mask) + (size_t)m * ldm + nb);
+#pragma unroll
+          for (int q8 = 0; q8 < 2; ++q8) {
+            const uint4 mm = __ldg(mk + q8);
+            const uint32_t w[4] = {mm.x, mm.y, mm.z, mm.w};
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              const uint32_t bits = (t & 1) ? (w[t >> 1] & 0xffff0000u) : (w[t >> 1] << 16);
+              if (!(__uint_as_float(bits) > 0.f)) y[8 * q8 + t] = 0.f;
+            }
+          }
+        }
+      }
+      float4* o4 = reinterpret_cast<float4*>(dst + (size_t)m * N + nb);
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) o4[q4] = make_float4(y[4 * q4], y[4 * q4 + 1], y[4 * q4 + 2], y[4 * q4 + 3]);
+    } else if (m < M) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int n = n0 + c * 16 + j;
