@@ -18,8 +18,8 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(ROOT, "build", "finenv")
-LIB = os.path.join(PKG, "libfinenv.so")
+BUILD = os.environ.get("FIN_BUILD_DIR") or os.path.join(ROOT, "build", "finenv")
+LIB = os.environ.get("FIN_LIB_OUT") or os.path.join(PKG, "libfinenv.so")   # overrides: A/B variant builds
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

@@ -30,7 +30,10 @@
 // the start of chunk c: (x >> 31) with x the high word of a non-negative double or a
 // non-negative int, which is 0 at run time but not provably so at compile time.  At
 // most two chunks of row values are live.
-constexpr int kChunk = 6;
+#ifndef FIN_KCHUNK
+#define FIN_KCHUNK 6
+#endif
+constexpr int kChunk = FIN_KCHUNK;
 __device__ __forceinline__ int zdep(double x) { return __double2hiint(x) >> 31; }
 __device__ __forceinline__ int zdep(int x) { return x >> 31; }
 #define FIN_CHUNKED(KA, dep_expr, BODY)                                            \
@@ -127,39 +130,51 @@ __device__ __forceinline__ double stock_buys_redo_call(double b, int (&h)[KA], c
 }
 
 // One buy of step 4 (R5): n = the largest count <= want with fl(n u) <= b, b -= fl(n u).
-// n comes from the floor estimate f = floor(b fl(1/u)) (one round-down add, whose bits are
-// 2^52 + f) and is verified: fl(n u) <= b and, when the cash binds, fl((n + 1) u) > b; a
-// failed check (NaN cash, x within ~1e-11 of an integer) sets ``miss`` (the caller redoes
-// the step's buys exactly).  FIN_BUY_FAST=1 (A/B, off): first try n = want with one product
-// and one compare (exact by the definition when fl(want u) <= b) -- measured 26% slower on
-// the K1 bench workload, where the cash binds in most steps and warps run both paths.
-#ifndef FIN_BUY_FAST
-#define FIN_BUY_FAST 0
+// n comes from the floor estimate f = floor(b fl(1/u)): one round-down add D = 2^52 + x
+// whose bits are the biased operand 0x43300000:f that nprod needs -- n = min(want, f) is
+// written over its low word, so the product takes D's own register pair.  Verified, with
+// b' = fl(b - fl(n u)) the cash after the buy:
+//  * hi(D) == 0x43300000, i.e. 0 <= x < 2^32 (else NaN / huge / negative cash);
+//  * fl(n u) <= b  <=>  b' >= 0 (the sign of a rounded difference is exact).  Buys only
+//    subtract (n >= 0), so a negative b' stays negative (or trips the hi(D) check of a
+//    later asset): the caller checks the final cash once (``stock_buys_ok``);
+//  * when the cash binds (n < want): fl((n + 1) u) > b.  It holds whenever b' < ut =
+//    fl(u (1 - 2^-34)): with c = fl(n u) = n u + e1 and b - c = b' + e2 (|e1|, |e2| <=
+//    2^-53 (n + 1) u <= 2^-38 u for n < want <= 32767), (n + 1) u - b > u (2^-34 - 2^-37),
+//    more than the rounding of (n + 1) u itself.  b' in [ut, u) (frac(b / u) within 2^-34
+//    of 1) is a false alarm, not an error.
+// A failed check sets ``miss`` (the caller redoes the step's buys exactly).
+// FIN_BUY_V1=1 (A/B, the round-2 form): n + 1 product and both checks per asset.
+#ifndef FIN_BUY_V1
+#define FIN_BUY_V1 0
 #endif
 __device__ __forceinline__ void buy_one(double& b, int& hk, int ak, double u, double ru, bool& miss) {
   const int want = max(min(ak, FIN_HOLD_MAX - hk), 0);
   const double mu = __dmul_rn(u, -4503599627370496.0);
-#if FIN_BUY_FAST
-  double c = nprod(want, u, mu);
-  int n = want;
-  if (!(c <= b)) {
-    // floor(b / u) estimate; its low word is used even when x >= 2^32 or b is NaN:
-    // the checks accept n only if it satisfies the definition itself
-    const double D = __dadd_rd(fmul64(b, ru), 4503599627370496.0);
-    n = min(want, __double2loint(D));
-    c = nprod(n, u, mu);
-    const double c1 = nprod(n + 1, u, mu);
-    miss |= (!(c <= b)) | ((n < want) & !(c1 > b)) | (n < 0);
-  }
-#else
   const double D = __dadd_rd(fmul64(b, ru), 4503599627370496.0);
+#if FIN_BUY_V1
   const int n = min(want, __double2loint(D));
   const double c = nprod(n, u, mu);
   const double c1 = nprod(n + 1, u, mu);
   miss |= (!(c <= b)) | ((n < want) & !(c1 > b)) | (n < 0);
-#endif
   b = fsub64(b, c);
+#else
+  const int hi = __double2hiint(D);
+  const int n = (int)umin((unsigned)want, (unsigned)__double2loint(D));
+  const double c = __fma_rn(__hiloint2double(hi, n), u, mu);
+  b = fsub64(b, c);
+  const double ut = __dmul_rn(u, 0.99999999994179233908653259277344);   // 1 - 2^-34
+  miss |= (hi != 0x43300000) | ((n < want) & !(b < ut));
+#endif
   hk += n;
+}
+// the final check of the branch-free buys (see buy_one): fl(n u) <= b held at every asset
+__device__ __forceinline__ bool stock_buys_ok(double b) {
+#if FIN_BUY_V1
+  return true;
+#else
+  return b >= 0.0;
+#endif
 }
 
 // Step 2 of the transition, clamp (R6): any clamped entry sets the sticky range flag;
@@ -245,6 +260,7 @@ __device__ __forceinline__ void stock_trade(const EnvDev& e, double& b, int (&h)
     buy_one(b, h[k], a[k], U[k + o_], RU[k + o_], miss);
   })
 buys_done:
+  miss |= !stock_buys_ok(b);
   if (miss) {   // rare
     atomicAdd(e.flags + FIN_CTR_EXACT_REDO, 1u);
     b = stock_buys_redo<KA>(bpre, h, a, save, save_stride, U, MU);
@@ -312,6 +328,7 @@ __device__ __forceinline__ void stock_trade_e(const EnvDev& e, double (&b)[E], i
 buys_done_e:
 #pragma unroll
   for (int q = 0; q < E; ++q) {
+    miss[q] |= !stock_buys_ok(b[q]);
     if (miss[q]) {   // rare
       atomicAdd(e.flags + FIN_CTR_EXACT_REDO, 1u);
 #if FIN_REDO_CALL
