@@ -130,52 +130,256 @@ __device__ __forceinline__ void write_hold_row(const EnvDev& e, const TrajDev& o
 // K1: one step of every env with supplied actions [N][K].
 //
 // Persistent and software-pipelined: each block walks tiles of 128 envs (stride
-// gridDim.x).  While the block computes tile j, one thread has already issued the
-// 1-D bulk-TMA copies of tile j + gridDim.x's state (cash, clock, window, holdings
-// octets) and action rows into the other shared-memory buffer, completing on an
-// mbarrier -- so the HBM latency of the loads overlaps the arithmetic instead of
-// stalling every new block (round-1 ncu: long_scoreboard was the top stall).
+// gridDim.x), and each of its 4 warps runs its own pipeline over its 32-env slice of
+// those tiles: while the warp steps slice j, its lanes have already issued the 16-byte
+// cp.async copies of slice j + gridDim.x's state (cash, asset, clock, window, holdings
+// octets) and action rows into the other shared-memory buffer, plus the price-row block
+// of the day PREDICTED for that slice (envs step in lockstep and their windows advance
+// together, so the next slice's window is this slice's shifted by the difference of
+// their initial assignments, R10).  A wrong prediction only sends the warp to the
+// L2-resident row table.  No barrier but __syncwarp: no warp ever waits for another.
+// Round 2 had one producer thread per block issuing 1-D bulk copies: its warp carried
+// ~340 extra instructions per tile (uniform-operand set-up of ten bulk copies, the 64-bit
+// divisions of the prediction), and the warps of the other SM sub-partitions waited on
+// its refills (ncu: 22% of the warp samples on the full-barrier wait).
 // Results go straight from registers to global memory (coalesced stores).
-// The f64 price rows of a tile's day (kPriceRows x kp doubles, one contiguous block
-// of px) are prefetched the same way, one tile ahead, for the day PREDICTED from
-// the current tile (envs step in lockstep and their windows advance together, so
-// the next tile's window is its initial window shifted like this tile's).  A wrong
-// prediction only costs a restage (group_apply).
 template <int KA>
-struct K1Buf {
-  double cash[kStep];
-  double v[kStep];
-  int32_t t[kStep];
-  int32_t w[kStep];
-  uint4 hold[(KA + 7) / 8][kStep];
-  alignas(16) int16_t act[kStep * KA];
+struct K1Slice {   // one warp's 32 envs of a tile
+  double cash[32];
+  double v[32];
+  int32_t t[32];
+  int32_t w[32];
+  uint4 hold[(KA + 7) / 8][32];
+  alignas(16) int16_t act[32 * KA];
 };
 #ifndef FIN_K1_LDS
 #define FIN_K1_LDS 1   // shared-typed trade path when every env of the warp is on the predicted day
 #endif
 #ifndef FIN_K1_NBUF
-#define FIN_K1_NBUF 2   // tile buffers: NBUF - 1 tiles in flight ahead of the one being stepped
+#define FIN_K1_NBUF 2   // slice buffers: NBUF - 1 slices in flight ahead of the one being stepped
 #endif
 constexpr int kK1Buf = FIN_K1_NBUF;
+constexpr int kK1W = kStep / 32;   // warps per K1 block
 template <int KA>
 struct K1Smem {
-  K1Buf<KA> buf[kK1Buf];
+  K1Slice<KA> sl[kK1Buf][kK1W];
   uint4 save[(KA + 7) / 8][kStep];   // [octet][thread]: conflict-free 16-B stores
-  alignas(16) double pr[kK1Buf][kPriceRows * ((KA + 3) / 4 * 4)];
-  uint64_t full[kK1Buf];    // state + actions of the buffer's tile landed (TMA)
-  uint64_t rows[kK1Buf];    // price rows of the buffer's predicted day landed (TMA), or no prediction
-  uint64_t empty[kK1Buf];   // the 4 warps are done with the buffer (state and rows)
-  int pred[kK1Buf];
+  alignas(16) double pr[kK1Buf][kK1W][kPriceRows * ((KA + 3) / 4 * 4)];
 };
 
-// day of the next tile predicted from (t0, w0) of global env g0 of this tile
-__device__ __forceinline__ int predict_day(const EnvDev& e, int t0, int w0, int64_t g0, int64_t gn) {
-  const int shift = ((w0 - window_of(e, g0)) % e.W + e.W) % e.W;
-  return day_of(e, (window_of(e, gn) + shift) % e.W, t0);
+// all lanes of a warp: cp.async the slice of 32 envs starting at env i (state + action rows)
+template <int KA>
+__device__ __forceinline__ void k1_fetch(const EnvDev& e, const int16_t* actions, int K, K1Slice<KA>& S, int i,
+                                         int lane) {
+  {  // cash | asset: 16 + 16 chunks (the two arrays are adjacent in the slice)
+    const double* src = lane < 16 ? e.cash + i + 2 * lane : e.vcur + i + 2 * (lane - 16);
+    sm100::cp_async16(S.cash + 2 * lane, src);
+  }
+  if (lane < 16) {  // clock | window: 8 + 8 chunks
+    const int32_t* src = lane < 8 ? e.t_ep + i + 4 * lane : e.window + i + 4 * (lane - 8);
+    sm100::cp_async16(S.t + 4 * lane, src);
+  }
+  const uint4* hq = reinterpret_cast<const uint4*>(e.hold);
+#pragma unroll
+  for (int o = 0; o < (KA + 7) / 8; ++o)
+    if (8 * o < K) sm100::cp_async16(&S.hold[o][lane], hq + (size_t)o * e.N + i + lane);
+  const uint4* aq = reinterpret_cast<const uint4*>(actions + (size_t)i * K);   // 32 K int16 = 4 K chunks
+  uint4* ad = reinterpret_cast<uint4*>(S.act);
+#pragma unroll
+  for (int c = 0; c < (4 * KA + 31) / 32; ++c)
+    if (32 * c + lane < 4 * K) sm100::cp_async16(ad + 32 * c + lane, aq + 32 * c + lane);
+}
+// all lanes: cp.async the price-row block of day d (kPriceRows x kp doubles) into pr
+__device__ __forceinline__ void k1_fetch_rows(const EnvDev& e, double* pr, int d, int lane) {
+  const int chunks = kPriceRows * e.kp / 2;
+  const double* src = e.px + (size_t)d * kPriceRows * e.kp;
+  for (int c = lane; c < chunks; c += 32) sm100::cp_async16(pr + 2 * c, src + 2 * c);
+}
+__device__ __forceinline__ bool day_ok(const EnvDev& e, int d) { return d >= 0 && d + 1 < e.rows; }
+
+#ifndef FIN_K1_E
+#define FIN_K1_E 1      // envs per thread (2 and 4 measured slower, round 1; the per-warp pipelines need 1)
+#endif
+#ifndef FIN_K1_MINB
+#define FIN_K1_MINB 3   // resident K1 blocks per SM (4: 128 registers, measured slower)
+#endif
+constexpr int kK1Threads = kStep;
+template <int KA, bool EXACT>
+__global__ void __launch_bounds__(kK1Threads, FIN_K1_MINB)
+    k_stock_step(EnvDev e, const int16_t* __restrict__ actions, TrajDev o, int tma_ok) {
+  static_assert(FIN_K1_E == 1, "K1's per-warp pipelines step one env per thread");
+  extern __shared__ __align__(16) uint8_t k1_smem[];   // dynamic: > 48 KB static limit
+  K1Smem<KA>& sm = *reinterpret_cast<K1Smem<KA>*>(k1_smem);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, r0 = wid * 32;
+  const int K = EXACT ? KA : e.K;
+  const int n_tiles = (e.N + kStep - 1) / kStep;
+  const int n_full = tma_ok ? e.N / kStep : 0;   // tiles served by the cp.async pipeline
+  const int RS = EXACT ? (KA + 3) / 4 * 4 : e.kp;   // staged row stride (= kp)
+  const int G = gridDim.x;
+  // window shift between a slice and the one (NBUF - 1) G tiles later (exact when the window
+  // block divides that env distance, R10; otherwise a prediction that may miss)
+  const int dW = (int)(((int64_t)kStep * G * (kK1Buf - 1) / e.wblock) % e.W);
+  // predicted day of the rows of the slices in flight, oldest first (-1: none; the same in every
+  // lane); a shift register, so it stays in registers
+  int pred[kK1Buf];
+#pragma unroll
+  for (int q = 0; q < kK1Buf; ++q) pred[q] = -1;
+  // prologue: the warp's slices of the block's first NBUF - 1 tiles, rows of each slice's actual day
+#pragma unroll
+  for (int q = 0; q + 1 < kK1Buf; ++q) {
+    const int jq = blockIdx.x + q * G;
+    if (jq < n_tiles) {
+      const int i0 = jq * kStep + r0;
+      if (jq < n_full) k1_fetch<KA>(e, actions, K, sm.sl[q][wid], i0, lane);
+      const int ir = min(i0, e.N - 1);
+      const int dq = day_of(e, __ldg(e.window + ir), __ldg(e.t_ep + ir));
+      if (day_ok(e, dq)) {
+        k1_fetch_rows(e, sm.pr[q][wid], dq, lane);
+        pred[q] = dq;
+      }
+    }
+    sm100::cp_async_commit();
+  }
+  bool oor = false;
+  int it = 0;
+  for (int j = blockIdx.x; j < n_tiles; j += G, ++it) {
+    const int sb = it % kK1Buf;
+    const int ps = pred[0];
+    const int jn = j + (kK1Buf - 1) * G;           // tile whose slice is fetched this iteration
+    const int sn = (it + kK1Buf - 1) % kK1Buf;      // ... into the slot of tile j - G
+    const bool tma = j < n_full;
+    K1Slice<KA>& S = sm.sl[sb][wid];
+    sm100::cp_async_wait<kK1Buf - 2>();            // this lane's copies of slot sb landed
+    __syncwarp();                                  // ... and every lane's
+    const int r = r0 + lane;   // env row in the tile
+    const int i = j * kStep + r;
+    const bool live = i < e.N;
+    int t = 0, w = 0;
+    double b = 0.0, v = 0.0;
+    int h[1][KA];
+    PackedActs<KA> a[1];
+#pragma unroll
+    for (int k = 0; k < KA; ++k) h[0][k] = 0;
+    if (tma) {
+      t = S.t[lane];
+      w = S.w[lane];
+      b = S.cash[lane];
+      v = S.v[lane];
+#pragma unroll
+      for (int oc = 0; oc < (KA + 7) / 8; ++oc) {
+        const uint4 x = S.hold[oc][lane];
+        const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (8 * oc + c < KA) h[0][8 * oc + c] = (int)((c & 1) ? (wv[c >> 1] >> 16) : (wv[c >> 1] & 0xffffu));
+      }
+      slab_read<KA, EXACT>(e, S.act, lane, K, true, a[0], oor, o.actions ? o.actions + (size_t)i * K : nullptr);
+    } else if (live) {   // ragged last tile / unaligned actions: direct loads
+      t = e.t_ep[i];
+      w = e.window[i];
+      b = e.cash[i];
+      v = e.vcur[i];
+      load_hold<KA>(e, i, h[0]);
+      int x[KA];
+#pragma unroll
+      for (int k = 0; k < KA; ++k) x[k] = (k < K) ? (int)actions[(size_t)i * K + k] : 0;
+      clamp_actions<KA>(e, x, oor, nullptr);
+      if (o.actions)
+        for (int k = 0; k < K; ++k) o.actions[(size_t)i * K + k] = (int16_t)x[k];
+      a[0] = pack_acts<KA>(x);
+    } else {
+#pragma unroll
+      for (int c = 0; c < (KA + 1) / 2; ++c) a[0].w[c] = 0u;
+    }
+    const bool stepping = live && t < e.L;
+    if (live && !stepping) {  // done env, autoreset = 0: ignored
+      set_flag(e, FIN_FLAG_EPISODE_DONE);
+      if (o.reward) o.reward[i] = 0.f;
+      if (o.done) o.done[i] = 1;
+    }
+    const int d = day_of(e, w, t);
+    FIN_CHECK(!live || (i >= 0 && i < e.N && w >= 0 && w < e.W));
+    const bool bad = stepping && (d < 0 || d + 1 >= e.rows);
+    if (bad) set_flag(e, FIN_FLAG_BAD_INDEX);
+    const bool go = stepping && !bad;
+    if (!go) {   // steps with no trade: leaves b and h untouched
+#pragma unroll
+      for (int c = 0; c < (KA + 1) / 2; ++c) a[0].w[c] = 0u;
+    }
+    // fetch (all lanes): slice jn's state into the slot of tile j - G (read in the previous
+    // iteration, before the __syncwarp above) and the rows of its predicted day -- lane 0's
+    // window shifted by dW at lane 0's clock
+    {
+      const int t0 = __shfl_sync(0xffffffffu, t, 0), w0 = __shfl_sync(0xffffffffu, w, 0);
+      int pn = -1;
+      if (jn < n_tiles) {
+        if (jn < n_full) k1_fetch<KA>(e, actions, K, sm.sl[sn][wid], jn * kStep + r0, lane);
+        int wn = w0 + dW;
+        if (wn >= e.W) wn -= e.W;
+        const int dn = day_of(e, wn, t0);
+        if (day_ok(e, dn)) {
+          k1_fetch_rows(e, sm.pr[sn][wid], dn, lane);
+          pn = dn;
+        }
+      }
+      sm100::cp_async_commit();
+#pragma unroll
+      for (int q = 0; q + 2 < kK1Buf; ++q) pred[q] = pred[q + 1];
+      pred[kK1Buf - 2] = pn;
+    }
+    const bool staged = !go || d == ps;
+    const double* R[1] = {static_cast<const double*>(__builtin_assume_aligned(
+        staged ? sm.pr[sb][wid] : e.px + (size_t)d * kPriceRows * e.kp, 16))};
+    uint4* sv[1] = {&sm.save[0][tid]};
+    double bb[1] = {b}, vn[1];
+#if FIN_K1_LDS
+    // the normal case (every env of the warp on the predicted day): the rows are addressed
+    // from the shared array itself, so they are read with shared loads, not generic ones
+    if (__all_sync(0xffffffffu, staged)) {
+      const double* Rs[1] = {sm.pr[sb][wid]};
+      stock_trade_e<KA, 1>(e, bb, h, Rs, RS, a, sv, kStep);
+      vn[0] = bb[0];
+      const double* PNs[1] = {sm.pr[sb][wid] + kRowPN * RS};
+      stock_mark_e<KA, 1>(vn, h, PNs);
+    } else
+#endif
+    {
+      stock_trade_e<KA, 1>(e, bb, h, R, RS, a, sv, kStep);
+      vn[0] = bb[0];
+      const double* PN[1] = {R[0] + kRowPN * RS};
+      stock_mark_e<KA, 1>(vn, h, PN);
+    }
+    b = bb[0];
+    if (go) {
+      double vnext = vn[0];
+      t += 1;
+      const bool done = (t == e.L);
+      if (o.reward) o.reward[i] = stock_reward(e, v, vn[0]);
+      if (o.done) o.done[i] = done ? 1 : 0;
+      if (o.cash) o.cash[i] = b;
+      if (o.asset) o.asset[i] = vn[0];
+      write_hold_row<KA>(e, o, (size_t)i, h[0]);
+      if (done && e.autoreset) {
+        b = e.cash0;
+        vnext = e.cash0;
+#pragma unroll
+        for (int k = 0; k < KA; ++k) h[0][k] = 0;
+        t = 0;
+        if (e.wadv) w = (w + 1) % e.W;
+      }
+      e.cash[i] = b;
+      e.vcur[i] = vnext;
+      store_hold<KA>(e, i, h[0]);
+      e.t_ep[i] = t;
+      if (e.wadv) e.window[i] = w;
+    }
+  }
+  sm100::cp_async_wait<0>();
+  if (oor) set_flag(e, FIN_FLAG_ACTION_RANGE);
 }
 
 // thread 0: publish the prediction, then bulk-copy the price rows of day d into pr
-// (completing on bar); with no usable prediction the barrier phase completes at once
+// (completing on bar); with no usable prediction the barrier phase completes at once (K4)
 __device__ __forceinline__ void rows_issue(const EnvDev& e, double* pr, uint64_t* bar, int* pred, int d) {
   if (d >= 0 && d + 1 < e.rows) {
     *pred = d;
@@ -186,212 +390,6 @@ __device__ __forceinline__ void rows_issue(const EnvDev& e, double* pr, uint64_t
     *pred = -1;
     sm100::mbar_arrive(bar);
   }
-}
-
-template <int KA>
-__device__ __forceinline__ void k1_issue(const EnvDev& e, const int16_t* actions, int K, K1Buf<KA>& B,
-                                         uint64_t* bar, int i0) {
-  const int ko = (K + 7) / 8;
-  const uint32_t bytes = kStep * (8 + 8 + 4 + 4) + (uint32_t)ko * kStep * 16 + kStep * K * 2;
-  sm100::mbar_arrive_expect_tx(bar, bytes);
-  sm100::bulk_g2s(B.cash, e.cash + i0, kStep * 8, bar);
-  sm100::bulk_g2s(B.v, e.vcur + i0, kStep * 8, bar);
-  sm100::bulk_g2s(B.t, e.t_ep + i0, kStep * 4, bar);
-  sm100::bulk_g2s(B.w, e.window + i0, kStep * 4, bar);
-  const uint4* hq = reinterpret_cast<const uint4*>(e.hold);
-  for (int o = 0; o < ko; ++o) sm100::bulk_g2s(B.hold[o], hq + (size_t)o * e.N + i0, kStep * 16, bar);
-  sm100::bulk_g2s(B.act, actions + (size_t)i0 * K, kStep * K * 2, bar);
-}
-
-#ifndef FIN_K1_E
-#define FIN_K1_E 1      // envs per thread (2 and 4 measured slower: scripts/k1_sweep.sh)
-#endif
-#ifndef FIN_K1_MINB
-#define FIN_K1_MINB (FIN_K1_E == 1 ? 3 : 4)   // resident K1 blocks per SM
-#endif
-constexpr int kK1E = FIN_K1_E;
-constexpr int kK1Threads = kStep / kK1E;      // a block owns a 128-env tile per iteration
-// No block-wide barrier inside the tile loop: warps are decoupled by the full / rows
-// / empty mbarriers, and an env whose day is not the predicted one reads its rows
-// from the (L2-resident) global table instead of a restaged copy.  Thread r of the
-// block steps envs r, r + kK1Threads, ... of the tile.
-template <int KA, bool EXACT>
-__global__ void __launch_bounds__(kK1Threads, FIN_K1_MINB)
-    k_stock_step(EnvDev e, const int16_t* __restrict__ actions, TrajDev o, int tma_ok) {
-  constexpr int E = kK1E;
-  extern __shared__ __align__(16) uint8_t k1_smem[];   // dynamic: > 48 KB static limit
-  K1Smem<KA>& sm = *reinterpret_cast<K1Smem<KA>*>(k1_smem);
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int K = EXACT ? KA : e.K;
-  const int n_tiles = (e.N + kStep - 1) / kStep;
-  const int n_full = tma_ok ? e.N / kStep : 0;   // tiles served by the bulk-copy pipeline
-  const int RS = EXACT ? (KA + 3) / 4 * 4 : e.kp;   // staged row stride (= kp)
-  if (tid == 0) {
-    for (int q = 0; q < kK1Buf; ++q) {
-      sm100::mbar_init(&sm.full[q], 1);
-      sm100::mbar_init(&sm.rows[q], 1);
-      sm100::mbar_init(&sm.empty[q], kK1Threads / 32);
-    }
-    sm100::fence_mbar_init();
-  }
-  __syncthreads();
-  // prologue: the block's first NBUF - 1 tiles, rows of each tile's actual day
-  if (tid == 0) {
-    for (int q = 0; q + 1 < kK1Buf; ++q) {
-      const int jq = blockIdx.x + q * gridDim.x;
-      if (jq >= n_tiles) break;
-      const int i0 = jq * kStep;
-      if (jq < n_full) k1_issue<KA>(e, actions, K, sm.buf[q], &sm.full[q], i0);
-      rows_issue(e, sm.pr[q], &sm.rows[q], &sm.pred[q], day_of(e, __ldg(e.window + i0), __ldg(e.t_ep + i0)));
-    }
-  }
-  bool oor = false;
-  int it = 0;
-  for (int j = blockIdx.x; j < n_tiles; j += gridDim.x, ++it) {
-    const int sb = it % kK1Buf;
-    const uint32_t par = (uint32_t)(it / kK1Buf) & 1u;   // phase of slot sb's current use
-    const int jn = j + (kK1Buf - 1) * gridDim.x;          // tile refilled this iteration
-    const int sn = (it + kK1Buf - 1) % kK1Buf;            // ... into the slot of tile j - G
-    const bool tma = j < n_full;
-    K1Buf<KA>& B = sm.buf[sb];
-    if (tma) sm100::mbar_wait(&sm.full[sb], par);
-    int t[E], w[E], d[E];
-    double b[E], v[E];
-    int h[E][KA];
-    PackedActs<KA> a[E];
-    bool live[E], go[E];
-#pragma unroll
-    for (int q = 0; q < E; ++q) {
-      const int r = tid + q * kK1Threads;   // env row in the tile
-      const int i = j * kStep + r;
-      live[q] = i < e.N;
-      t[q] = 0; w[q] = 0; b[q] = 0.0; v[q] = 0.0;
-#pragma unroll
-      for (int k = 0; k < KA; ++k) h[q][k] = 0;
-      if (tma) {
-        t[q] = B.t[r];
-        w[q] = B.w[r];
-        b[q] = B.cash[r];
-        v[q] = B.v[r];
-#pragma unroll
-        for (int oc = 0; oc < (KA + 7) / 8; ++oc) {
-          const uint4 x = B.hold[oc][r];
-          const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            if (8 * oc + c < KA) h[q][8 * oc + c] = (int)((c & 1) ? (wv[c >> 1] >> 16) : (wv[c >> 1] & 0xffffu));
-        }
-        slab_read<KA, EXACT>(e, B.act, r, K, true, a[q], oor, o.actions ? o.actions + (size_t)i * K : nullptr);
-      } else if (live[q]) {   // ragged last tile / unaligned actions: direct loads
-        t[q] = e.t_ep[i];
-        w[q] = e.window[i];
-        b[q] = e.cash[i];
-        v[q] = e.vcur[i];
-        load_hold<KA>(e, i, h[q]);
-        int x[KA];
-#pragma unroll
-        for (int k = 0; k < KA; ++k) x[k] = (k < K) ? (int)actions[(size_t)i * K + k] : 0;
-        clamp_actions<KA>(e, x, oor, nullptr);
-        if (o.actions)
-          for (int k = 0; k < K; ++k) o.actions[(size_t)i * K + k] = (int16_t)x[k];
-        a[q] = pack_acts<KA>(x);
-      } else {
-#pragma unroll
-        for (int c = 0; c < (KA + 1) / 2; ++c) a[q].w[c] = 0u;
-      }
-      const bool stepping = live[q] && t[q] < e.L;
-      if (live[q] && !stepping) {  // done env, autoreset = 0: ignored
-        set_flag(e, FIN_FLAG_EPISODE_DONE);
-        if (o.reward) o.reward[i] = 0.f;
-        if (o.done) o.done[i] = 1;
-      }
-      d[q] = day_of(e, w[q], t[q]);
-      FIN_CHECK(!live[q] || (i >= 0 && i < e.N && w[q] >= 0 && w[q] < e.W));
-      const bool bad = stepping && (d[q] < 0 || d[q] + 1 >= e.rows);
-      if (bad) set_flag(e, FIN_FLAG_BAD_INDEX);
-      go[q] = stepping && !bad;
-      if (!go[q]) {   // steps with no trade: leaves b and h untouched
-#pragma unroll
-        for (int c = 0; c < (KA + 1) / 2; ++c) a[q].w[c] = 0u;
-      }
-    }
-    // producer (thread 0): once the warps are done with tile j - G's buffer, refill it
-    // with tile jn's state and the rows of its predicted day
-    if (tid == 0 && jn < n_tiles) {
-      if (it >= 1) sm100::mbar_wait(&sm.empty[sn], (uint32_t)((it - 1) / kK1Buf) & 1u);
-      if (jn < n_full) k1_issue<KA>(e, actions, K, sm.buf[sn], &sm.full[sn], jn * kStep);
-      rows_issue(e, sm.pr[sn], &sm.rows[sn], &sm.pred[sn],
-                 predict_day(e, t[0], w[0], e.env_offset + (int64_t)j * kStep, e.env_offset + (int64_t)jn * kStep));
-    }
-    sm100::mbar_wait(&sm.rows[sb], par);
-    const double* R[E];
-    uint4* sv[E];
-    bool staged = true;
-#pragma unroll
-    for (int q = 0; q < E; ++q) {
-      staged &= !go[q] || d[q] == sm.pred[sb];
-      R[q] = static_cast<const double*>(__builtin_assume_aligned(
-          (!go[q] || d[q] == sm.pred[sb]) ? sm.pr[sb] : e.px + (size_t)d[q] * kPriceRows * e.kp, 16));
-      sv[q] = &sm.save[0][tid + q * kK1Threads];
-    }
-    double vn[E];
-#if FIN_K1_LDS
-    // the normal case (every env of the warp on the predicted day): the rows are addressed
-    // from the shared array itself, so they are read with shared loads, not generic ones
-    if (__all_sync(0xffffffffu, staged)) {
-      const double* Rs[E];
-      const double* PNs[E];
-#pragma unroll
-      for (int q = 0; q < E; ++q) Rs[q] = sm.pr[sb];
-      stock_trade_e<KA, E>(e, b, h, Rs, RS, a, sv, kStep);
-#pragma unroll
-      for (int q = 0; q < E; ++q) {
-        vn[q] = b[q];
-        PNs[q] = sm.pr[sb] + kRowPN * RS;
-      }
-      stock_mark_e<KA, E>(vn, h, PNs);
-    } else
-#endif
-    {
-      stock_trade_e<KA, E>(e, b, h, R, RS, a, sv, kStep);
-      const double* PN[E];
-#pragma unroll
-      for (int q = 0; q < E; ++q) {
-        vn[q] = b[q];
-        PN[q] = R[q] + kRowPN * RS;
-      }
-      stock_mark_e<KA, E>(vn, h, PN);
-    }
-#pragma unroll
-    for (int q = 0; q < E; ++q) {
-      if (!go[q]) continue;
-      const int i = j * kStep + tid + q * kK1Threads;
-      double vnext = vn[q];
-      t[q] += 1;
-      const bool done = (t[q] == e.L);
-      if (o.reward) o.reward[i] = stock_reward(e, v[q], vn[q]);
-      if (o.done) o.done[i] = done ? 1 : 0;
-      if (o.cash) o.cash[i] = b[q];
-      if (o.asset) o.asset[i] = vn[q];
-      write_hold_row<KA>(e, o, (size_t)i, h[q]);
-      if (done && e.autoreset) {
-        b[q] = e.cash0;
-        vnext = e.cash0;
-#pragma unroll
-        for (int k = 0; k < KA; ++k) h[q][k] = 0;
-        t[q] = 0;
-        if (e.wadv) w[q] = (w[q] + 1) % e.W;
-      }
-      e.cash[i] = b[q];
-      e.vcur[i] = vnext;
-      store_hold<KA>(e, i, h[q]);
-      e.t_ep[i] = t[q];
-      if (e.wadv) e.window[i] = w[q];
-    }
-    __syncwarp();
-    if (lane == 0) sm100::mbar_arrive(&sm.empty[sb]);
-  }
-  if (oor) set_flag(e, FIN_FLAG_ACTION_RANGE);
 }
 
 // K4: T steps with supplied actions [T][N][K]; the env state (cash, holdings,
