@@ -483,7 +483,7 @@ int fin_env_create(const fin_env_config* cfg, const float* market, int64_t marke
         row[kRowU * d.kp + k] = uk;
         row[kRowMP * d.kp + k] = pk * m52;
         row[kRowMU * d.kp + k] = uk * m52;
-        row[kRowRU * d.kp + k] = 1.0 / uk;
+        row[kRowRU * d.kp + k] = (1.0 / uk) * (1.0 + 0x1p-40);   // biased up (env_stock.cuh buy_want)
         row[kRowPN * d.kp + k] = pn;
         row[kRowMPN * d.kp + k] = pn * m52;
         double& umin = row[kRowMeta * d.kp];

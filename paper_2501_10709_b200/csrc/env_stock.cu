@@ -378,6 +378,397 @@ __global__ void __launch_bounds__(kK1Threads, FIN_K1_MINB)
   if (oor) set_flag(e, FIN_FLAG_ACTION_RANGE);
 }
 
+// ---------------------------------------------------------------- K1, packed form (default)
+// The same step with holdings / actions kept packed two assets per 32-bit word (asset 2j in
+// the low half), for even compile-time K (K = 30, the C1 shape; K = 4):
+//  * 16-bit SIMD for the integer side: sells n = relu(min(-a, h)) and h -= n for two assets
+//    in three instructions; the buy limit want = relu(min(a, 32767 - h)) of a pair before
+//    its buys (an asset's limit depends on its own holding only);
+//  * no holdings unpack / repack at load and store, and no post-sell save for the redo (the
+//    rare exact redo recomputes the env's whole trade from its pre-step state, still in the
+//    slice buffer), so 3 blocks of 4 warps keep 162 registers and 54 KB of shared memory;
+//  * E envs per thread (FIN_K2_E; both read the same staged row values).
+// Every float64 operation is the one of stock_trade, in the same order, so cash / asset are
+// bit-identical.
+#ifndef FIN_K1_PACKED
+#define FIN_K1_PACKED 1
+#endif
+#ifndef FIN_K2_E
+#define FIN_K2_E 1      // envs per thread of the packed K1 (2: 226 registers, 2 warps per
+#endif                  // scheduler, 5% slower despite 19% fewer instructions per env-step)
+#ifndef FIN_K2_MINB
+#define FIN_K2_MINB 3   // resident blocks per SM (E = 1: 4 forces 128 registers, 7% slower)
+#endif
+constexpr int kK2E = FIN_K2_E;
+constexpr int kK2Threads = kStep / kK2E;
+constexpr int kK2W = kK2Threads / 32;
+constexpr int kK2Slice = kStep / kK2W;   // 32 E envs per warp slice
+template <int KA>
+struct K2Slice {
+  double cash[kK2Slice];
+  double v[kK2Slice];
+  int32_t t[kK2Slice];
+  int32_t w[kK2Slice];
+  uint4 hold[(KA + 7) / 8][kK2Slice];
+  alignas(16) int16_t act[kK2Slice * KA];
+};
+template <int KA>
+struct K2Smem {
+  K2Slice<KA> sl[kK1Buf][kK2W];
+  alignas(16) double pr[kK1Buf][kK2W][kPriceRows * ((KA + 3) / 4 * 4)];
+};
+template <int KA>
+__device__ __forceinline__ void k2_fetch(const EnvDev& e, const int16_t* actions, K2Slice<KA>& S, int i, int lane) {
+  constexpr int NS = kK2Slice, H = NS / 2;   // cash | asset: NS / 2 + NS / 2 chunks
+#pragma unroll
+  for (int c = 0; c < kK2E; ++c) {
+    const int x = 32 * c + lane;
+    const double* src = x < H ? e.cash + i + 2 * x : e.vcur + i + 2 * (x - H);
+    sm100::cp_async16(S.cash + 2 * x, src);
+  }
+  if (lane < NS / 2) {  // clock | window: NS / 4 + NS / 4 chunks
+    const int32_t* src = lane < NS / 4 ? e.t_ep + i + 4 * lane : e.window + i + 4 * (lane - NS / 4);
+    sm100::cp_async16(S.t + 4 * lane, src);
+  }
+  const uint4* hq = reinterpret_cast<const uint4*>(e.hold);
+#pragma unroll
+  for (int o = 0; o < (KA + 7) / 8; ++o) {
+#pragma unroll
+    for (int c = 0; c < kK2E; ++c)
+      sm100::cp_async16(&S.hold[o][lane + 32 * c], hq + (size_t)o * e.N + i + lane + 32 * c);
+  }
+  const uint4* aq = reinterpret_cast<const uint4*>(actions + (size_t)i * KA);   // NS KA int16 = NS KA / 8 chunks
+  uint4* ad = reinterpret_cast<uint4*>(S.act);
+#pragma unroll
+  for (int c = 0; c < (NS * KA / 8 + 31) / 32; ++c)
+    if (32 * c + lane < NS * KA / 8) sm100::cp_async16(ad + 32 * c + lane, aq + 32 * c + lane);
+}
+
+__device__ __forceinline__ int half_of(uint32_t w, int s) { return s ? (int)(w >> 16) : (int)(w & 0xffffu); }
+
+// the exact redo of one env's trade (rare: a branch-free buy failed its check): sells and exact
+// buys from the pre-step cash and holdings (hold_pre[o * stride]) and the clamped actions a2
+template <int KA>
+static __device__ __noinline__ double k2_redo(const EnvDev& e, double b, const uint4* hold_pre, int stride,
+                                             const uint32_t* a2, const double* R, int RS, uint32_t* h2) {
+  int h[KA], a[KA];
+#pragma unroll
+  for (int o = 0; o < (KA + 7) / 8; ++o) {
+    const uint4 x = hold_pre[(size_t)o * stride];
+    const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (8 * o + c < KA) h[8 * o + c] = half_of(wv[c >> 1], c & 1);
+  }
+#pragma unroll
+  for (int k = 0; k < KA; ++k) a[k] = (k & 1) ? ((int)a2[k >> 1] >> 16) : (int)(int16_t)(a2[k >> 1] & 0xffffu);
+  const double* P = R + kRowP * RS;
+  const double* U = R + kRowU * RS;
+  const double* MU = R + kRowMU * RS;
+#pragma unroll
+  for (int k = 0; k < KA; ++k) {   // 3. sells (the fast path's operations)
+    const int n = max(min(-a[k], h[k]), 0);
+    b = fadd64(b, fmul64(nprodx(n, P[k]), e.dn));
+    h[k] -= n;
+  }
+#pragma unroll
+  for (int k = 0; k < KA; ++k) {   // 4. exact buys (R5)
+    const int want = max(min(a[k], FIN_HOLD_MAX - h[k]), 0);
+    double c = nprod(want, U[k], MU[k]);
+    int n = want;
+    if (!(c <= b)) {
+      n = affordable_exact(b, U[k], want);
+      c = nprod(n, U[k], MU[k]);
+    }
+    b = fsub64(b, c);
+    h[k] += n;
+  }
+#pragma unroll
+  for (int j = 0; j < KA / 2; ++j) h2[j] = __byte_perm((uint32_t)h[2 * j], (uint32_t)h[2 * j + 1], 0x5410);
+  return b;
+}
+
+// steps 3-4 for E envs with packed holdings / actions; sets miss[q] when env q needs the redo
+template <int KA, int E>
+__device__ __forceinline__ void k2_trade(const EnvDev& e, double (&b)[E], uint32_t (&h2)[E][KA / 2],
+                                         const uint32_t (&a2)[E][KA / 2], const double* const (&R)[E], int RS,
+                                         bool (&miss)[E]) {
+  // 3. sells, clipped to holdings: n = relu(min(-a, h)) (-a = ~a + 1 per half), b += fl(fl(n p)(1 - c))
+  uint32_t n2[E];
+  FIN_CHUNKED(KA, b[0], {
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      if ((k & 1) == 0) {
+        n2[q] = __vmaxs2(__vmins2(__vneg2(a2[q][k >> 1]), h2[q][k >> 1]), 0u);
+        h2[q][k >> 1] -= n2[q];   // no borrow across halves: n <= h per half
+      }
+      b[q] = fadd64(b[q], fmul64(nprodx(half_of(n2[q], k & 1), R[q][kRowP * RS + k + o_]), e.dn));
+    }
+  })
+  // 4. buys, ascending k (buy_one); a pair's limits before its buys
+  uint32_t want2[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) miss[q] = false;
+  double umin[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) umin[q] = R[q][kRowMeta * RS];
+  FIN_CHUNKED(KA, b[0], {
+    if (k == c_ && c_ > 0) {
+      bool poor = true;
+#pragma unroll
+      for (int q = 0; q < E; ++q) poor &= !(b[q] >= umin[q]);
+      if (__all_sync(__activemask(), poor)) goto k2_buys_done;
+    }
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      if ((k & 1) == 0)
+        want2[q] = __vmaxs2(__vmins2(a2[q][k >> 1], __vsub2(0x7fff7fffu, h2[q][k >> 1])), 0u);
+      const int n = buy_want(b[q], half_of(want2[q], k & 1), R[q][kRowU * RS + k + o_], R[q][kRowRU * RS + k + o_],
+                             miss[q]);
+      h2[q][k >> 1] += (k & 1) ? ((uint32_t)n << 16) : (uint32_t)n;
+    }
+  })
+k2_buys_done:
+#pragma unroll
+  for (int q = 0; q < E; ++q) miss[q] |= !stock_buys_ok(b[q]);
+}
+
+template <int KA, int E>
+__device__ __forceinline__ void k2_mark(double (&acc)[E], const uint32_t (&h2)[E][KA / 2], const double* const (&PN)[E]) {
+  FIN_CHUNKED(KA, acc[0], {
+#pragma unroll
+    for (int q = 0; q < E; ++q) acc[q] = fadd64(acc[q], nprodx(half_of(h2[q][k >> 1], k & 1), PN[q][k + o_]));
+  })
+}
+
+template <int KA>
+__global__ void __launch_bounds__(kK2Threads, FIN_K2_MINB)
+    k_stock_step2(EnvDev e, const int16_t* __restrict__ actions, TrajDev o, int tma_ok) {
+  constexpr int E = kK2E, KP = KA / 2;
+  static_assert(KA % 2 == 0, "packed K1: even K");
+  extern __shared__ __align__(16) uint8_t k2_smem[];
+  K2Smem<KA>& sm = *reinterpret_cast<K2Smem<KA>*>(k2_smem);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, r0 = wid * kK2Slice;
+  const int n_tiles = (e.N + kStep - 1) / kStep;
+  const int n_full = tma_ok ? e.N / kStep : 0;
+  constexpr int RS = (KA + 3) / 4 * 4;
+  const int G = gridDim.x;
+  const int dW = (int)(((int64_t)kStep * G * (kK1Buf - 1) / e.wblock) % e.W);
+  const uint32_t mt2 = (uint32_t)e.max_trade * 0x10001u;
+  int pred[kK1Buf];
+#pragma unroll
+  for (int q = 0; q < kK1Buf; ++q) pred[q] = -1;
+#pragma unroll
+  for (int q = 0; q + 1 < kK1Buf; ++q) {
+    const int jq = blockIdx.x + q * G;
+    if (jq < n_tiles) {
+      const int i0 = jq * kStep + r0;
+      if (jq < n_full) k2_fetch<KA>(e, actions, sm.sl[q][wid], i0, lane);
+      const int ir = min(i0, e.N - 1);
+      const int dq = day_of(e, __ldg(e.window + ir), __ldg(e.t_ep + ir));
+      if (day_ok(e, dq)) {
+        k1_fetch_rows(e, sm.pr[q][wid], dq, lane);
+        pred[q] = dq;
+      }
+    }
+    sm100::cp_async_commit();
+  }
+  bool oor = false;
+  int it = 0;
+  for (int j = blockIdx.x; j < n_tiles; j += G, ++it) {
+    const int sb = it % kK1Buf;
+    const int ps = pred[0];
+    const int jn = j + (kK1Buf - 1) * G;
+    const int sn = (it + kK1Buf - 1) % kK1Buf;
+    const bool tma = j < n_full;
+    K2Slice<KA>& S = sm.sl[sb][wid];
+    sm100::cp_async_wait<kK1Buf - 2>();
+    __syncwarp();
+    int t[E], w[E], d[E], idx[E], gi[E];
+    bool live[E], go[E];
+    double b[E], v[E];
+    uint32_t h2[E][KP], a2[E][KP];
+    uint32_t diff = 0;
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      idx[q] = lane + 32 * q;              // env row in the warp's slice
+      gi[q] = j * kStep + r0 + idx[q];
+      live[q] = gi[q] < e.N;
+      t[q] = 0; w[q] = 0; b[q] = 0.0; v[q] = 0.0;
+#pragma unroll
+      for (int c = 0; c < KP; ++c) { h2[q][c] = 0u; a2[q][c] = 0u; }
+      if (tma) {
+        t[q] = S.t[idx[q]];
+        w[q] = S.w[idx[q]];
+        b[q] = S.cash[idx[q]];
+        v[q] = S.v[idx[q]];
+#pragma unroll
+        for (int oc = 0; oc < (KA + 7) / 8; ++oc) {
+          const uint4 x = S.hold[oc][idx[q]];
+          const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (4 * oc + c < KP) h2[q][4 * oc + c] = wv[c];
+        }
+        const uint32_t* aw = reinterpret_cast<const uint32_t*>(S.act) + idx[q] * KP;
+#pragma unroll
+        for (int c = 0; c < KP; ++c) a2[q][c] = aw[c];
+      } else if (live[q]) {   // ragged last tile / unaligned actions: direct loads
+        const int i = gi[q];
+        t[q] = e.t_ep[i];
+        w[q] = e.window[i];
+        b[q] = e.cash[i];
+        v[q] = e.vcur[i];
+        const uint4* hq = reinterpret_cast<const uint4*>(e.hold);
+#pragma unroll
+        for (int oc = 0; oc < (KA + 7) / 8; ++oc) {
+          const uint4 x = hq[(size_t)oc * e.N + i];
+          const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (4 * oc + c < KP) h2[q][4 * oc + c] = wv[c];
+        }
+#pragma unroll
+        for (int c = 0; c < KP; ++c)
+          a2[q][c] = __byte_perm((uint32_t)(uint16_t)actions[(size_t)i * KA + 2 * c],
+                                 (uint32_t)(uint16_t)actions[(size_t)i * KA + 2 * c + 1], 0x5410);
+      }
+      // 2. clamp (R6), two assets per instruction
+#pragma unroll
+      for (int c = 0; c < KP; ++c) a2[q][c] = clamp_pair(a2[q][c], mt2, diff);
+      if (o.actions && live[q]) {
+#pragma unroll
+        for (int c = 0; c < KP; ++c) reinterpret_cast<uint32_t*>(o.actions + (size_t)gi[q] * KA)[c] = a2[q][c];
+      }
+      const bool stepping = live[q] && t[q] < e.L;
+      if (live[q] && !stepping) {  // done env, autoreset = 0: ignored
+        set_flag(e, FIN_FLAG_EPISODE_DONE);
+        if (o.reward) o.reward[gi[q]] = 0.f;
+        if (o.done) o.done[gi[q]] = 1;
+      }
+      d[q] = day_of(e, w[q], t[q]);
+      FIN_CHECK(!live[q] || (w[q] >= 0 && w[q] < e.W));
+      const bool bad = stepping && (d[q] < 0 || d[q] + 1 >= e.rows);
+      if (bad) set_flag(e, FIN_FLAG_BAD_INDEX);
+      go[q] = stepping && !bad;
+      if (!go[q]) {
+#pragma unroll
+        for (int c = 0; c < KP; ++c) a2[q][c] = 0u;
+      }
+    }
+    oor |= diff != 0;
+    {  // fetch slice jn and the rows of its predicted day (see k_stock_step)
+      const int t0 = __shfl_sync(0xffffffffu, t[0], 0), w0 = __shfl_sync(0xffffffffu, w[0], 0);
+      int pn = -1;
+      if (jn < n_tiles) {
+        if (jn < n_full) k2_fetch<KA>(e, actions, sm.sl[sn][wid], jn * kStep + r0, lane);
+        int wn = w0 + dW;
+        if (wn >= e.W) wn -= e.W;
+        const int dn = day_of(e, wn, t0);
+        if (day_ok(e, dn)) {
+          k1_fetch_rows(e, sm.pr[sn][wid], dn, lane);
+          pn = dn;
+        }
+      }
+      sm100::cp_async_commit();
+#pragma unroll
+      for (int q = 0; q + 2 < kK1Buf; ++q) pred[q] = pred[q + 1];
+      pred[kK1Buf - 2] = pn;
+    }
+    bool staged = true;
+    const double* R[E];
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      const bool st = !go[q] || d[q] == ps;
+      staged &= st;
+      R[q] = static_cast<const double*>(__builtin_assume_aligned(
+          st ? sm.pr[sb][wid] : e.px + (size_t)d[q] * kPriceRows * e.kp, 16));
+    }
+    double bb[E], vn[E];
+    bool miss[E];
+#pragma unroll
+    for (int q = 0; q < E; ++q) bb[q] = b[q];
+    if (__all_sync(0xffffffffu, staged)) {   // shared-typed row reads
+      const double* Rs[E];
+      const double* PNs[E];
+#pragma unroll
+      for (int q = 0; q < E; ++q) Rs[q] = sm.pr[sb][wid];
+      k2_trade<KA, E>(e, bb, h2, a2, Rs, RS, miss);
+#pragma unroll
+      for (int q = 0; q < E; ++q) { vn[q] = bb[q]; PNs[q] = sm.pr[sb][wid] + kRowPN * RS; }
+      k2_mark<KA, E>(vn, h2, PNs);
+    } else {
+      k2_trade<KA, E>(e, bb, h2, a2, R, RS, miss);
+      const double* PN[E];
+#pragma unroll
+      for (int q = 0; q < E; ++q) { vn[q] = bb[q]; PN[q] = R[q] + kRowPN * RS; }
+      k2_mark<KA, E>(vn, h2, PN);
+    }
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      if (miss[q]) {   // rare: redo env q's trade exactly from its pre-step state
+        atomicAdd(e.flags + FIN_CTR_EXACT_REDO, 1u);
+        const uint4* hp = tma ? &S.hold[0][idx[q]] : reinterpret_cast<const uint4*>(e.hold) + gi[q];
+        uint32_t ac[KP];
+#pragma unroll
+        for (int c = 0; c < KP; ++c) ac[c] = a2[q][c];
+        uint32_t hn[KP];
+        bb[q] = k2_redo<KA>(e, b[q], hp, tma ? kK2Slice : e.N, ac, R[q], RS, hn);
+#pragma unroll
+        for (int c = 0; c < KP; ++c) h2[q][c] = hn[c];
+        vn[q] = bb[q];
+        const double* PNq[1] = {R[q] + kRowPN * RS};
+        double acc[1] = {bb[q]};
+        uint32_t hq1[1][KP];
+#pragma unroll
+        for (int c = 0; c < KP; ++c) hq1[0][c] = hn[c];
+        k2_mark<KA, 1>(acc, hq1, PNq);
+        vn[q] = acc[0];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      if (!go[q]) continue;
+      const int i = gi[q];
+      double bq = bb[q], vnext = vn[q];
+      int tq = t[q] + 1, wq = w[q];
+      const bool done = (tq == e.L);
+      if (o.reward) o.reward[i] = stock_reward(e, v[q], vn[q]);
+      if (o.done) o.done[i] = done ? 1 : 0;
+      if (o.cash) o.cash[i] = bq;
+      if (o.asset) o.asset[i] = vn[q];
+      if (o.hold) {
+#pragma unroll
+        for (int c = 0; c < KP; ++c) reinterpret_cast<uint32_t*>(o.hold + (size_t)i * KA)[c] = h2[q][c];
+      }
+      uint32_t hs[KP];
+#pragma unroll
+      for (int c = 0; c < KP; ++c) hs[c] = h2[q][c];
+      if (done && e.autoreset) {
+        bq = e.cash0;
+        vnext = e.cash0;
+#pragma unroll
+        for (int c = 0; c < KP; ++c) hs[c] = 0u;
+        tq = 0;
+        if (e.wadv) wq = (wq + 1) % e.W;
+      }
+      e.cash[i] = bq;
+      e.vcur[i] = vnext;
+      uint4* hq = reinterpret_cast<uint4*>(e.hold);
+#pragma unroll
+      for (int oc = 0; oc < (KA + 7) / 8; ++oc) {
+        const uint32_t w0_ = 4 * oc < KP ? hs[4 * oc] : 0u, w1_ = 4 * oc + 1 < KP ? hs[4 * oc + 1] : 0u;
+        const uint32_t w2_ = 4 * oc + 2 < KP ? hs[4 * oc + 2] : 0u, w3_ = 4 * oc + 3 < KP ? hs[4 * oc + 3] : 0u;
+        hq[(size_t)oc * e.N + i] = make_uint4(w0_, w1_, w2_, w3_);
+      }
+      e.t_ep[i] = tq;
+      if (e.wadv) e.window[i] = wq;
+    }
+  }
+  sm100::cp_async_wait<0>();
+  if (oor) set_flag(e, FIN_FLAG_ACTION_RANGE);
+}
+
 // thread 0: publish the prediction, then bulk-copy the price rows of day d into pr
 // (completing on bar); with no usable prediction the barrier phase completes at once (K4)
 __device__ __forceinline__ void rows_issue(const EnvDev& e, double* pr, uint64_t* bar, int* pred, int d) {
@@ -655,12 +1046,34 @@ int k1_grid(int N) {
   return std::min(tiles, per_sm * num_sms());
 }
 
+// persistent grid for the packed K1: resident blocks per SM x SMs, capped by the tiles
+template <int KA>
+int k2_grid(int N) {
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaFuncSetAttribute(k_stock_step2<KA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K2Smem<KA>));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stock_step2<KA>, kK2Threads, sizeof(K2Smem<KA>)) !=
+        cudaSuccess)
+      per_sm = 1;
+  }
+  if (per_sm < 1) per_sm = 1;
+  const int tiles = (N + kStep - 1) / kStep;
+  return std::min(tiles, per_sm * num_sms());
+}
+#define K2_LAUNCH(KA) \
+  k_stock_step2<KA><<<k2_grid<KA>(e.N), kK2Threads, sizeof(K2Smem<KA>), s>>>(e, actions, o, v)
+
 cudaError_t launch_stock_step(const EnvDev& e, const int16_t* actions, const TrajDev& o, cudaStream_t s) {
   const int v = vec_ok(actions, 8);   // bulk copies of whole 128-env tiles: 256 K bytes each
 #define FIN_K1(KA, EX) \
   k_stock_step<KA, EX><<<k1_grid<KA, EX>(e.N), kK1Threads, sizeof(K1Smem<KA>), s>>>(e, actions, o, v)
+#if FIN_K1_PACKED
+  if (e.K == 30) K2_LAUNCH(30);
+  else if (e.K == 4) K2_LAUNCH(4);
+#else
   if (e.K == 30) FIN_K1(30, true);
   else if (e.K == 4) FIN_K1(4, true);
+#endif
   else if (e.K <= 8) FIN_K1(8, false);
   else if (e.K <= 16) FIN_K1(16, false);
   else FIN_K1(32, false);

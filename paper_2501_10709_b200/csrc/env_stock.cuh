@@ -130,26 +130,23 @@ __device__ __forceinline__ double stock_buys_redo_call(double b, int (&h)[KA], c
 }
 
 // One buy of step 4 (R5): n = the largest count <= want with fl(n u) <= b, b -= fl(n u).
-// n comes from the floor estimate f = floor(b fl(1/u)): one round-down add D = 2^52 + x
-// whose bits are the biased operand 0x43300000:f that nprod needs -- n = min(want, f) is
-// written over its low word, so the product takes D's own register pair.  Verified, with
-// b' = fl(b - fl(n u)) the cash after the buy:
+// The estimate f = floor(x), x = fl(b RU) with RU = fl(fl(1/u)(1 + 2^-40)) (host, biased up),
+// comes from one round-down add D = 2^52 + x whose bits are the biased operand 0x43300000:f
+// that nprod needs -- n = min(want, f) is written over its low word, so the product takes D's
+// own register pair.  Because x > (b/u)(1 + 2^-41), the estimate is never below the answer:
+// fl((f + 1) u) <= b gives b/u >= (f + 1)(1 - 2^-53), hence x > f + 1.  It can exceed the
+// answer by one (b/u within 2^-40 below an integer), and then fl(n u) > b, i.e. the cash after
+// the buy b' = fl(b - fl(n u)) < 0 (the sign of a rounded difference is exact).  So the checks:
 //  * hi(D) == 0x43300000, i.e. 0 <= x < 2^32 (else NaN / huge / negative cash);
-//  * fl(n u) <= b  <=>  b' >= 0 (the sign of a rounded difference is exact).  Buys only
-//    subtract (n >= 0), so a negative b' stays negative (or trips the hi(D) check of a
-//    later asset): the caller checks the final cash once (``stock_buys_ok``);
-//  * when the cash binds (n < want): fl((n + 1) u) > b.  It holds whenever b' < ut =
-//    fl(u (1 - 2^-34)): with c = fl(n u) = n u + e1 and b - c = b' + e2 (|e1|, |e2| <=
-//    2^-53 (n + 1) u <= 2^-38 u for n < want <= 32767), (n + 1) u - b > u (2^-34 - 2^-37),
-//    more than the rounding of (n + 1) u itself.  b' in [ut, u) (frac(b / u) within 2^-34
-//    of 1) is a false alarm, not an error.
+//  * b' >= 0 once, on the final cash (``stock_buys_ok``): buys only subtract (n >= 0), so a
+//    negative b' stays negative, or trips the hi(D) check of the next asset (x < 0).
+// With both passing, n satisfies the predicate and is >= the largest n that does: n is it.
 // A failed check sets ``miss`` (the caller redoes the step's buys exactly).
 // FIN_BUY_V1=1 (A/B, the round-2 form): n + 1 product and both checks per asset.
 #ifndef FIN_BUY_V1
 #define FIN_BUY_V1 0
 #endif
-__device__ __forceinline__ void buy_one(double& b, int& hk, int ak, double u, double ru, bool& miss) {
-  const int want = max(min(ak, FIN_HOLD_MAX - hk), 0);
+__device__ __forceinline__ int buy_want(double& b, int want, double u, double ru, bool& miss) {
   const double mu = __dmul_rn(u, -4503599627370496.0);
   const double D = __dadd_rd(fmul64(b, ru), 4503599627370496.0);
 #if FIN_BUY_V1
@@ -163,10 +160,12 @@ __device__ __forceinline__ void buy_one(double& b, int& hk, int ak, double u, do
   const int n = (int)umin((unsigned)want, (unsigned)__double2loint(D));
   const double c = __fma_rn(__hiloint2double(hi, n), u, mu);
   b = fsub64(b, c);
-  const double ut = __dmul_rn(u, 0.99999999994179233908653259277344);   // 1 - 2^-34
-  miss |= (hi != 0x43300000) | ((n < want) & !(b < ut));
+  miss |= hi != 0x43300000;
 #endif
-  hk += n;
+  return n;
+}
+__device__ __forceinline__ void buy_one(double& b, int& hk, int ak, double u, double ru, bool& miss) {
+  hk += buy_want(b, max(min(ak, FIN_HOLD_MAX - hk), 0), u, ru, miss);
 }
 // the final check of the branch-free buys (see buy_one): fl(n u) <= b held at every asset
 __device__ __forceinline__ bool stock_buys_ok(double b) {

@@ -122,7 +122,7 @@ __device__ __forceinline__ double fdiv64_rcp(double a, double b, double y) {
 //   P  = p_d   close of the execution day (exact widening of the fp32 market)
 //   U  = u_d   = fl(p_d * (1 + c)), the buy price per share
 //   MP = -2^52 p_d,  MU = -2^52 u_d   (exact scalings)
-//   RU = fl(1 / u_d)                  (estimate of the affordable count only)
+//   RU = fl(fl(1 / u_d) (1 + 2^-40))  (estimate of the affordable count only, biased up)
 //   PN = p_d+1, MPN = -2^52 p_d+1     (marking day; 0 on the last row)
 //   META[0] = min_k u_k               (cash below it buys nothing more this step)
 enum { kRowP = 0, kRowU, kRowMP, kRowMU, kRowRU, kRowPN, kRowMPN, kRowMeta, kPriceRows };
