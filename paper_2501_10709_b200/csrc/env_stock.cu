@@ -340,14 +340,14 @@ __global__ void __launch_bounds__(kK1Threads, FIN_K1_MINB)
       stock_trade_e<KA, 1>(e, bb, h, Rs, RS, a, sv, kStep);
       vn[0] = bb[0];
       const double* PNs[1] = {sm.pr[sb][wid] + kRowPN * RS};
-      stock_mark_e<KA, 1>(vn, h, PNs);
+      stock_mark_e<KA, 1>(vn, h, PNs, RS);
     } else
 #endif
     {
       stock_trade_e<KA, 1>(e, bb, h, R, RS, a, sv, kStep);
       vn[0] = bb[0];
       const double* PN[1] = {R[0] + kRowPN * RS};
-      stock_mark_e<KA, 1>(vn, h, PN);
+      stock_mark_e<KA, 1>(vn, h, PN, RS);
     }
     b = bb[0];
     if (go) {
@@ -396,6 +396,7 @@ __global__ void __launch_bounds__(kK1Threads, FIN_K1_MINB)
 #ifndef FIN_K2_E
 #define FIN_K2_E 1      // envs per thread of the packed K1 (2: 226 registers, 2 warps per
 #endif                  // scheduler, 5% slower despite 19% fewer instructions per env-step)
+#define FIN_K2_MROWS FIN_MROWS
 #ifndef FIN_K2_MINB
 #define FIN_K2_MINB 3   // resident blocks per SM (E = 1: 4 forces 128 registers, 7% slower)
 #endif
@@ -502,7 +503,12 @@ __device__ __forceinline__ void k2_trade(const EnvDev& e, double (&b)[E], uint32
         n2[q] = __vmaxs2(__vmins2(__vneg2(a2[q][k >> 1]), h2[q][k >> 1]), 0u);
         h2[q][k >> 1] -= n2[q];   // no borrow across halves: n <= h per half
       }
+#if FIN_K2_MROWS
+      b[q] = fadd64(b[q], fmul64(nprod(half_of(n2[q], k & 1), R[q][kRowP * RS + k + o_], R[q][kRowMP * RS + k + o_]),
+                                 e.dn));
+#else
       b[q] = fadd64(b[q], fmul64(nprodx(half_of(n2[q], k & 1), R[q][kRowP * RS + k + o_]), e.dn));
+#endif
     }
   })
   // 4. buys, ascending k (buy_one); a pair's limits before its buys
@@ -523,8 +529,13 @@ __device__ __forceinline__ void k2_trade(const EnvDev& e, double (&b)[E], uint32
     for (int q = 0; q < E; ++q) {
       if ((k & 1) == 0)
         want2[q] = __vmaxs2(__vmins2(a2[q][k >> 1], __vsub2(0x7fff7fffu, h2[q][k >> 1])), 0u);
+#if FIN_K2_MROWS
+      const int n = buy_want_m(b[q], half_of(want2[q], k & 1), R[q][kRowU * RS + k + o_], R[q][kRowMU * RS + k + o_],
+                               R[q][kRowRU * RS + k + o_], miss[q]);
+#else
       const int n = buy_want(b[q], half_of(want2[q], k & 1), R[q][kRowU * RS + k + o_], R[q][kRowRU * RS + k + o_],
                              miss[q]);
+#endif
       h2[q][k >> 1] += (k & 1) ? ((uint32_t)n << 16) : (uint32_t)n;
     }
   })
@@ -534,10 +545,17 @@ k2_buys_done:
 }
 
 template <int KA, int E>
-__device__ __forceinline__ void k2_mark(double (&acc)[E], const uint32_t (&h2)[E][KA / 2], const double* const (&PN)[E]) {
+__device__ __forceinline__ void k2_mark(double (&acc)[E], const uint32_t (&h2)[E][KA / 2], const double* const (&PN)[E],
+                                        int RS) {
   FIN_CHUNKED(KA, acc[0], {
 #pragma unroll
-    for (int q = 0; q < E; ++q) acc[q] = fadd64(acc[q], nprodx(half_of(h2[q][k >> 1], k & 1), PN[q][k + o_]));
+    for (int q = 0; q < E; ++q) {
+#if FIN_K2_MROWS   // PN[q] points at row PN; row MPN follows it
+      acc[q] = fadd64(acc[q], nprod(half_of(h2[q][k >> 1], k & 1), PN[q][k + o_], PN[q][(kRowMPN - kRowPN) * RS + k + o_]));
+#else
+      acc[q] = fadd64(acc[q], nprodx(half_of(h2[q][k >> 1], k & 1), PN[q][k + o_]));
+#endif
+    }
   })
 }
 
@@ -696,13 +714,13 @@ __global__ void __launch_bounds__(kK2Threads, FIN_K2_MINB)
       k2_trade<KA, E>(e, bb, h2, a2, Rs, RS, miss);
 #pragma unroll
       for (int q = 0; q < E; ++q) { vn[q] = bb[q]; PNs[q] = sm.pr[sb][wid] + kRowPN * RS; }
-      k2_mark<KA, E>(vn, h2, PNs);
+      k2_mark<KA, E>(vn, h2, PNs, RS);
     } else {
       k2_trade<KA, E>(e, bb, h2, a2, R, RS, miss);
       const double* PN[E];
 #pragma unroll
       for (int q = 0; q < E; ++q) { vn[q] = bb[q]; PN[q] = R[q] + kRowPN * RS; }
-      k2_mark<KA, E>(vn, h2, PN);
+      k2_mark<KA, E>(vn, h2, PN, RS);
     }
 #pragma unroll
     for (int q = 0; q < E; ++q) {
@@ -722,7 +740,7 @@ __global__ void __launch_bounds__(kK2Threads, FIN_K2_MINB)
         uint32_t hq1[1][KP];
 #pragma unroll
         for (int c = 0; c < KP; ++c) hq1[0][c] = hn[c];
-        k2_mark<KA, 1>(acc, hq1, PNq);
+        k2_mark<KA, 1>(acc, hq1, PNq, RS);
         vn[q] = acc[0];
       }
     }
@@ -875,7 +893,7 @@ __global__ void __launch_bounds__(kStep, FIN_K4_MINB) k_stock_replay(EnvDev e, c
         [&]() {
           const double v = vc;
           stock_trade<KA>(e, b, h, pr, RS, a, &sm.save[0][tid], kStep);
-          const double vn = stock_mark<KA>(b, h, pr + kRowPN * RS);
+          const double vn = stock_mark<KA>(b, h, pr + kRowPN * RS, RS);
           vc = vn;
           t += 1;
           const bool done = (t == e.L);

@@ -21,6 +21,11 @@
 
 #include <type_traits>
 
+// the fused rollout forms the -2^52 x product operands with a DMUL (FIN_MROWS=1, staged rows,
+// raises the spills of every K3 variant: its env warps run under the MMA warps' register budget)
+#ifndef FIN_MROWS
+#define FIN_MROWS 0
+#endif
 #include "env_stock.cuh"
 #include "group_stage.cuh"
 #include "philox.cuh"
@@ -500,7 +505,7 @@ struct StockOps {
           uint4* save = reinterpret_cast<uint4*>(a_tile + kSaveOff) + st.gtid;
           clamp_actions<KA>(e, a, st.oor, (LOG && p.o.actions) ? p.o.actions + ti * KA : nullptr);
           stock_trade<KA>(e, st.b, st.h, pd, KP4, pack_acts<KA>(a), save, tc::kTileM);
-          const double vn = stock_mark<KA>(st.b, st.h, pd + kRowPN * KP4);
+          const double vn = stock_mark<KA>(st.b, st.h, pd + kRowPN * KP4, KP4);
           st.vc = vn;
           FIN_TR(threadIdx.x == 128, t, 20);
           st.t_ep += 1;
