@@ -374,6 +374,153 @@ buys_done_e:
   }
 }
 
+// ---------------------------------------------------------------- packed form
+// Holdings and clamped actions two assets per 32-bit word (asset 2j in the low half; even K):
+// 16-bit SIMD for the integer side of the trade, the float64 operations of stock_trade in the
+// same order (bit-identical cash / asset).  Used by K1 (k_stock_step2) and the fused rollout.
+__device__ __forceinline__ int half_of(uint32_t w, int s) { return s ? (int)(w >> 16) : (int)(w & 0xffffu); }
+
+// the exact redo of one env's trade (rare: a branch-free buy failed its check): sells and exact
+// buys from the pre-step cash and holdings (hold_pre[o * stride]) and the clamped actions a2
+template <int KA>
+__device__ __forceinline__ double k2_redo_body(const EnvDev& e, double b, const uint4* hold_pre, int stride,
+                                               const uint32_t* a2, const double* R, int RS, uint32_t* h2) {
+  int h[KA], a[KA];
+#pragma unroll
+  for (int o = 0; o < (KA + 7) / 8; ++o) {
+    const uint4 x = hold_pre[(size_t)o * stride];
+    const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (8 * o + c < KA) h[8 * o + c] = half_of(wv[c >> 1], c & 1);
+  }
+#pragma unroll
+  for (int k = 0; k < KA; ++k) a[k] = (k & 1) ? ((int)a2[k >> 1] >> 16) : (int)(int16_t)(a2[k >> 1] & 0xffffu);
+  const double* P = R + kRowP * RS;
+  const double* U = R + kRowU * RS;
+  const double* MU = R + kRowMU * RS;
+#pragma unroll
+  for (int k = 0; k < KA; ++k) {   // 3. sells (the fast path's operations)
+    const int n = max(min(-a[k], h[k]), 0);
+    b = fadd64(b, fmul64(nprodx(n, P[k]), e.dn));
+    h[k] -= n;
+  }
+#pragma unroll
+  for (int k = 0; k < KA; ++k) {   // 4. exact buys (R5)
+    const int want = max(min(a[k], FIN_HOLD_MAX - h[k]), 0);
+    double c = nprod(want, U[k], MU[k]);
+    int n = want;
+    if (!(c <= b)) {
+      n = affordable_exact(b, U[k], want);
+      c = nprod(n, U[k], MU[k]);
+    }
+    b = fsub64(b, c);
+    h[k] += n;
+  }
+#pragma unroll
+  for (int j = 0; j < KA / 2; ++j) h2[j] = __byte_perm((uint32_t)h[2 * j], (uint32_t)h[2 * j + 1], 0x5410);
+  return b;
+}
+template <int KA>
+static __device__ __noinline__ double k2_redo(const EnvDev& e, double b, const uint4* hold_pre, int stride,
+                                             const uint32_t* a2, const double* R, int RS, uint32_t* h2) {
+  return k2_redo_body<KA>(e, b, hold_pre, stride, a2, R, RS, h2);
+}
+// packed holdings of env i from / to the asset octets [ceil(K/8)][N] x uint4
+template <int KA>
+__device__ __forceinline__ void load_hold2(const EnvDev& e, int i, uint32_t (&h2)[KA / 2]) {
+  const uint4* q = reinterpret_cast<const uint4*>(e.hold);
+#pragma unroll
+  for (int o = 0; o < (KA + 7) / 8; ++o) {
+    const uint4 x = q[(size_t)o * e.N + i];
+    const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (4 * o + c < KA / 2) h2[4 * o + c] = wv[c];
+  }
+}
+template <int KA>
+__device__ __forceinline__ uint4 hold_octet(const uint32_t (&h2)[KA / 2], int o) {
+  return make_uint4(4 * o < KA / 2 ? h2[4 * o] : 0u, 4 * o + 1 < KA / 2 ? h2[4 * o + 1] : 0u,
+                    4 * o + 2 < KA / 2 ? h2[4 * o + 2] : 0u, 4 * o + 3 < KA / 2 ? h2[4 * o + 3] : 0u);
+}
+template <int KA>
+__device__ __forceinline__ void store_hold2(const EnvDev& e, int i, const uint32_t (&h2)[KA / 2]) {
+  uint4* q = reinterpret_cast<uint4*>(e.hold);
+#pragma unroll
+  for (int o = 0; o < (KA + 7) / 8; ++o) q[(size_t)o * e.N + i] = hold_octet<KA>(h2, o);
+}
+
+// steps 3-4 for E envs with packed holdings / actions; sets miss[q] when env q needs the redo
+template <int KA, int E>
+__device__ __forceinline__ void k2_trade(const EnvDev& e, double (&b)[E], uint32_t (&h2)[E][KA / 2],
+                                         const uint32_t (&a2)[E][KA / 2], const double* const (&R)[E], int RS,
+                                         bool (&miss)[E]) {
+  // 3. sells, clipped to holdings: n = relu(min(-a, h)) (-a = ~a + 1 per half), b += fl(fl(n p)(1 - c))
+  uint32_t n2[E];
+  FIN_CHUNKED(KA, b[0], {
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      if ((k & 1) == 0) {
+        n2[q] = __vmaxs2(__vmins2(__vneg2(a2[q][k >> 1]), h2[q][k >> 1]), 0u);
+        h2[q][k >> 1] -= n2[q];   // no borrow across halves: n <= h per half
+      }
+#if FIN_MROWS
+      b[q] = fadd64(b[q], fmul64(nprod(half_of(n2[q], k & 1), R[q][kRowP * RS + k + o_], R[q][kRowMP * RS + k + o_]),
+                                 e.dn));
+#else
+      b[q] = fadd64(b[q], fmul64(nprodx(half_of(n2[q], k & 1), R[q][kRowP * RS + k + o_]), e.dn));
+#endif
+    }
+  })
+  // 4. buys, ascending k (buy_one); a pair's limits before its buys
+  uint32_t want2[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) miss[q] = false;
+  double umin[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) umin[q] = R[q][kRowMeta * RS];
+  FIN_CHUNKED(KA, b[0], {
+    if (k == c_ && c_ > 0) {
+      bool poor = true;
+#pragma unroll
+      for (int q = 0; q < E; ++q) poor &= !(b[q] >= umin[q]);
+      if (__all_sync(__activemask(), poor)) goto k2_buys_done;
+    }
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      if ((k & 1) == 0)
+        want2[q] = __vmaxs2(__vmins2(a2[q][k >> 1], __vsub2(0x7fff7fffu, h2[q][k >> 1])), 0u);
+#if FIN_MROWS
+      const int n = buy_want_m(b[q], half_of(want2[q], k & 1), R[q][kRowU * RS + k + o_], R[q][kRowMU * RS + k + o_],
+                               R[q][kRowRU * RS + k + o_], miss[q]);
+#else
+      const int n = buy_want(b[q], half_of(want2[q], k & 1), R[q][kRowU * RS + k + o_], R[q][kRowRU * RS + k + o_],
+                             miss[q]);
+#endif
+      h2[q][k >> 1] += (k & 1) ? ((uint32_t)n << 16) : (uint32_t)n;
+    }
+  })
+k2_buys_done:
+#pragma unroll
+  for (int q = 0; q < E; ++q) miss[q] |= !stock_buys_ok(b[q]);
+}
+
+template <int KA, int E>
+__device__ __forceinline__ void k2_mark(double (&acc)[E], const uint32_t (&h2)[E][KA / 2], const double* const (&PN)[E],
+                                        int RS) {
+  FIN_CHUNKED(KA, acc[0], {
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+#if FIN_MROWS   // PN[q] points at row PN; row MPN follows it
+      acc[q] = fadd64(acc[q], nprod(half_of(h2[q][k >> 1], k & 1), PN[q][k + o_], PN[q][(kRowMPN - kRowPN) * RS + k + o_]));
+#else
+      acc[q] = fadd64(acc[q], nprodx(half_of(h2[q][k >> 1], k & 1), PN[q][k + o_]));
+#endif
+    }
+  })
+}
+
 // copy the price rows of day d (px[d], kPriceRows x kp doubles) into pr[kPriceRows][kp]
 // (threads tid = 0 .. nthr-1 of the staging group)
 __device__ __forceinline__ void stage_price_rows(const EnvDev& e, double* pr, int d, int tid, int nthr) {
