@@ -140,10 +140,11 @@ __device__ __forceinline__ double stock_buys_redo_call(double b, int (&h)[KA], c
 }
 
 // One buy of step 4 (R5): n = the largest count <= want with fl(n u) <= b, b -= fl(n u).
-// The estimate f = floor(x), x = fl(b RU) with RU = fl(fl(1/u)(1 + 2^-40)) (host, biased up),
-// comes from one round-down add D = 2^52 + x whose bits are the biased operand 0x43300000:f
-// that nprod needs -- n = min(want, f) is written over its low word, so the product takes D's
-// own register pair.  Because x > (b/u)(1 + 2^-41), the estimate is never below the answer:
+// The estimate f = floor(x), x = b RU exactly with RU = fl(fl(1/u)(1 + 2^-40)) (host, biased
+// up), comes from one round-down fma D = RD(b RU + 2^52) whose bits are the biased operand
+// 0x43300000:f that nprod needs -- n = min(want, f) is written over its low word, so the product takes D's
+// own register pair.  Because x > (b/u)(1 + 2^-41) (RU's two roundings cost < 2^-52), the
+// estimate is never below the answer:
 // fl((f + 1) u) <= b gives b/u >= (f + 1)(1 - 2^-53), hence x > f + 1.  It can exceed the
 // answer by one (b/u within 2^-40 below an integer), and then fl(n u) > b, i.e. the cash after
 // the buy b' = fl(b - fl(n u)) < 0 (the sign of a rounded difference is exact).  So the checks:
@@ -157,14 +158,17 @@ __device__ __forceinline__ double stock_buys_redo_call(double b, int (&h)[KA], c
 #define FIN_BUY_V1 0
 #endif
 __device__ __forceinline__ int buy_want_m(double& b, int want, double u, double mu, double ru, bool& miss) {
-  const double D = __dadd_rd(fmul64(b, ru), 4503599627370496.0);
 #if FIN_BUY_V1
+  const double D = __dadd_rd(fmul64(b, ru), 4503599627370496.0);
   const int n = min(want, __double2loint(D));
   const double c = nprod(n, u, mu);
   const double c1 = nprod(n + 1, u, mu);
   miss |= (!(c <= b)) | ((n < want) & !(c1 > b)) | (n < 0);
   b = fsub64(b, c);
 #else
+  // D = RD(b RU + 2^52) in one fused op: the floor of the exact product (x above), one f64
+  // latency less on the serial cash chain than rounding b RU first
+  const double D = __fma_rd(b, ru, 4503599627370496.0);
   const int hi = __double2hiint(D);
   const int n = (int)umin((unsigned)want, (unsigned)__double2loint(D));
   const double c = __fma_rn(__hiloint2double(hi, n), u, mu);
