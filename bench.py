@@ -44,10 +44,11 @@ MLP_FLOP_PER_ENV_STEP = 2 * (301 * 256 + 256 * 256 + 256 * 30)    # 300,544: the
 FLOP_PER_ENV_STEP = 2 * (31 * 256 + 256 * 256 + 256 * 30)          # 162,304
 Z1S_FLOP_PER_ROLLOUT = 2 * 270 * 256 * ROWS   # fp64 CUDA-core precompute of the per-day layer-1 term
 # K1 algorithmic bytes per env-step: read cash 8 + holdings 60 + clock 4 + action 60,
-# write cash 8 + holdings 60 + clock 4 + reward 4 + done 1 = 209 B.  The kernel moves 229 B: it also
-# reads and writes the cached asset v (8 + 8) and reads the window (4) -- DESIGN.md 4.2.
+# write cash 8 + holdings 60 + clock 4 + reward 4 + done 1 = 209 B.  The kernel moves 237 B: it also
+# reads and writes the cached asset v (8 + 8), reads the window (4), and the holdings travel as
+# 16-B asset octets (2 pad assets: 4 + 4) -- DESIGN.md 4.2.
 STEP_BYTES_ALGO = 8 + 60 + 4 + 60 + 8 + 60 + 4 + 4 + 1                  # 209
-STEP_BYTES_MOVED = STEP_BYTES_ALGO + 8 + 8 + 4                            # 229
+STEP_BYTES_MOVED = STEP_BYTES_ALGO + 8 + 8 + 4 + 4 + 4                    # 237
 # K3 HBM bytes per env-step the fused rollout must write (reward f32 + done u8; state is on chip)
 ROLLOUT_HBM_BYTES = 5
 METRIC = "env-steps/sec (whole box) at 2048-65536 envs, 1/2/4/8 B200; % HBM roofline"
@@ -964,7 +965,8 @@ def hbm_kernels(fin, torch):
     tr = fin.make_traj(reward=z(N, torch.float32), done=z(N, torch.uint8))
     ms = b2b(lambda: fin.fin_env_step(env, acts, tr))
     entry("step_kernel_hbm", "k_stock_step (K1)", N, STEP_BYTES_ALGO * N, ms,
-          "SURVEY d.3's 209 B/env-step (the kernel moves 229 B: cached asset and window too); steady state: "
+          "SURVEY d.3's 209 B/env-step (the kernel moves 237 B: cached asset, window, holdings octet padding); "
+          "steady state: "
           "the same seeded U{-100..100} actions every step, so the cash binds in most steps")
     res["step_kernel_hbm"]["moved_gbs"] = STEP_BYTES_MOVED * N / (ms / 1e3) / 1e9
     del env, acts, tr
