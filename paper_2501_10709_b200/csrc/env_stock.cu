@@ -76,6 +76,14 @@ __device__ __forceinline__ void met_put(StepSmem<KA>& sm, int tid, const MetricA
   sm.met[0][tid] = m.v0; sm.met[1][tid] = m.vprev; sm.met[2][tid] = m.peak;
   sm.met[3][tid] = m.mdd; sm.met[4][tid] = m.mean; sm.met[5][tid] = m.m2;
 }
+__device__ __forceinline__ void met_put_k4(double (*met)[kStep], int tid, const MetricAcc& m) {
+  met[0][tid] = m.v0; met[1][tid] = m.vprev; met[2][tid] = m.peak;
+  met[3][tid] = m.mdd; met[4][tid] = m.mean; met[5][tid] = m.m2;
+}
+__device__ __forceinline__ void met_get_k4(const double (*met)[kStep], int tid, MetricAcc& m) {
+  m.v0 = met[0][tid]; m.vprev = met[1][tid]; m.peak = met[2][tid];
+  m.mdd = met[3][tid]; m.mean = met[4][tid]; m.m2 = met[5][tid];
+}
 template <int KA>
 __device__ __forceinline__ void met_get(const StepSmem<KA>& sm, int tid, MetricAcc& m) {
   m.v0 = sm.met[0][tid]; m.vprev = sm.met[1][tid]; m.peak = sm.met[2][tid];
@@ -919,6 +927,228 @@ int num_sms();
 
 // K = 30 (C1) and K = 4 (C0) are compiled exactly; any other K runs in the next
 // power-of-two bound with zero padding.
+// K4, packed form (default for even K): the replay with K1's round-2 structure -- holdings and
+// actions two assets per word (k2_trade), each warp prefetching its own next step (action slab
+// + the rows of the day predicted from lane 0's env) with cp.async, no block barrier (round 2's
+// K4 staged the rows once per block and day behind a named barrier, thread 0 issuing them).
+#ifndef FIN_K4_PACKED
+#define FIN_K4_PACKED 1
+#endif
+template <int KA>
+struct K4Smem {
+  alignas(16) int16_t act[2][4][32 * KA];
+  alignas(16) double pr[2][4][kPriceRows * ((KA + 3) / 4 * 4)];
+  uint4 save[(KA + 7) / 8][kStep];   // pre-step holdings of the rare exact redo
+  double met[6][kStep];
+  double agg[FIN_AGG_LEN][kStep];
+};
+template <int KA>
+__global__ void __launch_bounds__(kStep, FIN_K4_MINB) k_stock_replay2(EnvDev e, const int16_t* __restrict__ actions,
+                                                                     int T, TrajDev o, int vec_ok) {
+  constexpr int KP = KA / 2;
+  constexpr int RS = (KA + 3) / 4 * 4;
+  static_assert(KA % 2 == 0, "packed K4: even K");
+  extern __shared__ __align__(16) uint8_t k4_smem[];   // dynamic: > 48 KB static limit
+  K4Smem<KA>& sm = *reinterpret_cast<K4Smem<KA>*>(k4_smem);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int i = blockIdx.x * kStep + tid;
+  const bool live = i < e.N;
+  const int N = e.N;
+  int t = 0, w = 0, mn = 0;
+  double b = 0.0, vc = 0.0;
+  uint32_t h2[KP];
+#pragma unroll
+  for (int c = 0; c < KP; ++c) h2[c] = 0u;
+  {
+    MetricAcc m;
+    metric_start(m, 0.0);
+    if (live) {
+      t = e.t_ep[i];
+      w = e.window[i];
+      b = e.cash[i];
+      vc = e.vcur[i];
+      load_hold2<KA>(e, i, h2);
+      m = load_metric(e, i);
+    }
+    met_put_k4(sm.met, tid, m);
+    mn = m.n;
+#pragma unroll
+    for (int j = 0; j < FIN_AGG_LEN; ++j) sm.agg[j][tid] = 0.0;
+    AggAcc a0;
+    agg_init(a0);
+#pragma unroll
+    for (int j = 0; j < FIN_AGG_LEN; ++j) sm.agg[j][tid] = a0.s[j];
+  }
+  const int i0 = blockIdx.x * kStep + wid * 32;
+  const int nv = max(0, min(32, N - i0));
+  const bool vec = vec_ok && nv == 32;
+  const uint32_t mt2 = (uint32_t)e.max_trade * 0x10001u;
+  // fetch (all lanes, one cp.async group): step s's action slab of this warp + the rows of day ds
+  auto fetch = [&](int s, int ds) {
+    if (nv > 0) {
+      const int16_t* src = actions + ((size_t)s * N + i0) * KA;
+      int16_t* dst = sm.act[s & 1][wid];
+      if (vec) {
+        for (int j = lane; j < 4 * KA; j += 32) sm100::cp_async16(dst + 8 * j, src + 8 * j);
+      } else {
+        for (int j = lane; j < nv * KA; j += 32) dst[j] = src[j];
+      }
+    }
+    if (day_ok(e, ds)) k1_fetch_rows(e, sm.pr[s & 1][wid], ds, lane);
+    sm100::cp_async_commit();
+  };
+  int pred_cur;
+  {
+    const int t0 = __shfl_sync(0xffffffffu, t, 0), w0 = __shfl_sync(0xffffffffu, w, 0);
+    const int d0 = day_of(e, w0, t0);
+    pred_cur = day_ok(e, d0) ? d0 : -1;
+    fetch(0, pred_cur);
+  }
+  int cnt = 0;
+  double rsum = 0.0;
+  bool oor = false, bad = false;
+  for (int s = 0; s < T; ++s) {
+    const size_t ti = (size_t)s * N + i;
+    const int d = day_of(e, w, t);
+    const bool stepping = live && !bad && t < e.L;
+    // prefetch step s+1: its slab and the rows of lane 0's next day (d + 1, or the first day of
+    // its (possibly advanced) window after a reset)
+    int pred_next = -1;
+    if (s + 1 < T) {
+      const int t0 = __shfl_sync(0xffffffffu, t, 0), w0 = __shfl_sync(0xffffffffu, w, 0);
+      const int d0 = __shfl_sync(0xffffffffu, d, 0);
+      const int w1 = (e.wadv && t0 + 1 >= e.L) ? (w0 + 1) % e.W : w0;
+      const int dn = t0 + 1 < e.L ? d0 + 1 : (e.autoreset ? day_of(e, w1, 0) : -1);
+      pred_next = day_ok(e, dn) ? dn : -1;
+      fetch(s + 1, pred_next);
+      sm100::cp_async_wait<1>();
+    } else {
+      sm100::cp_async_wait<0>();
+    }
+    __syncwarp();
+    uint32_t a2[1][KP];
+    uint32_t diff = 0;
+    {
+      const uint32_t* aw = reinterpret_cast<const uint32_t*>(sm.act[s & 1][wid]) + lane * KP;
+#pragma unroll
+      for (int c = 0; c < KP; ++c) a2[0][c] = clamp_pair(live ? aw[c] : 0u, mt2, diff);
+    }
+    oor |= diff != 0;
+    if (o.actions && live) {
+#pragma unroll
+      for (int c = 0; c < KP; ++c) reinterpret_cast<uint32_t*>(o.actions + ti * KA)[c] = a2[0][c];
+    }
+    if (live && !bad && !stepping) {
+      set_flag(e, FIN_FLAG_EPISODE_DONE);
+      if (o.reward) o.reward[ti] = 0.f;
+      if (o.done) o.done[ti] = 1;
+    }
+    if (stepping && !day_ok(e, d)) bad = true;
+    const bool go = stepping && !bad;
+    if (!go) {
+#pragma unroll
+      for (int c = 0; c < KP; ++c) a2[0][c] = 0u;
+    }
+    const bool st_ok = !go || d == pred_cur;
+    const double* R1[1] = {static_cast<const double*>(__builtin_assume_aligned(
+        st_ok ? sm.pr[s & 1][wid] : e.px + (size_t)(go ? d : 0) * kPriceRows * e.kp, 16))};
+    const MetricRcp mr = metric_rcps(sm.met[1][tid], sm.met[2][tid], mn);
+#pragma unroll
+    for (int oc = 0; oc < (KA + 7) / 8; ++oc) sm.save[oc][tid] = hold_octet<KA>(h2, oc);
+    double bb[1] = {b};
+    uint32_t hh[1][KP];
+#pragma unroll
+    for (int c = 0; c < KP; ++c) hh[0][c] = h2[c];
+    bool miss[1];
+    if (__all_sync(0xffffffffu, st_ok)) {
+      const double* Rs[1] = {sm.pr[s & 1][wid]};
+      k2_trade<KA, 1>(e, bb, hh, a2, Rs, RS, miss);
+    } else {
+      k2_trade<KA, 1>(e, bb, hh, a2, R1, RS, miss);
+    }
+    if (miss[0]) {   // rare: the exact trade from the pre-step state
+      atomicAdd(e.flags + FIN_CTR_EXACT_REDO, 1u);
+      uint32_t ac[KP];
+#pragma unroll
+      for (int c = 0; c < KP; ++c) ac[c] = a2[0][c];
+      bb[0] = k2_redo<KA>(e, b, &sm.save[0][tid], kStep, ac, R1[0], RS, hh[0]);
+    }
+    pred_cur = pred_next;
+    if (go) {
+      const double v = vc;
+      b = bb[0];
+#pragma unroll
+      for (int c = 0; c < KP; ++c) h2[c] = hh[0][c];
+      double acc[1] = {b};
+      const double* PN1[1] = {R1[0] + kRowPN * RS};
+      k2_mark<KA, 1>(acc, hh, PN1, RS);
+      const double vn = acc[0];
+      vc = vn;
+      t += 1;
+      const bool done = (t == e.L);
+      const float r = stock_reward(e, v, vn);
+      rsum += (double)r;
+      if (o.reward) o.reward[ti] = r;
+      if (o.done) o.done[ti] = done ? 1 : 0;
+      if (o.cash) o.cash[ti] = b;
+      if (o.asset) o.asset[ti] = vn;
+      if (o.hold) {
+#pragma unroll
+        for (int c = 0; c < KP; ++c) reinterpret_cast<uint32_t*>(o.hold + ti * KA)[c] = h2[c];
+      }
+      MetricAcc m;
+      met_get_k4(sm.met, tid, m);
+      m.n = mn;
+      metric_push_pre(m, vn, mr);
+      if (done) {
+        double em[3];
+        metric_finish(m, 252.0, 0.0, em);
+        if (o.ep_metrics && cnt < o.ep_capacity) {
+          double* dst = o.ep_metrics + ((size_t)cnt * N + i) * 3;
+          dst[0] = em[0]; dst[1] = em[1]; dst[2] = em[2];
+        }
+        ++cnt;
+        AggAcc ag;
+#pragma unroll
+        for (int j = 0; j < FIN_AGG_LEN; ++j) ag.s[j] = sm.agg[j][tid];
+        agg_episode(ag, em);
+#pragma unroll
+        for (int j = 0; j < FIN_AGG_LEN; ++j) sm.agg[j][tid] = ag.s[j];
+        if (e.autoreset) {
+          b = e.cash0;
+#pragma unroll
+          for (int c = 0; c < KP; ++c) h2[c] = 0u;
+          t = 0;
+          vc = e.cash0;
+          if (e.wadv) w = (w + 1) % e.W;
+          metric_start(m, e.cash0);
+        }
+      }
+      met_put_k4(sm.met, tid, m);
+      mn = m.n;
+    }
+  }
+  MetricAcc m;
+  met_get_k4(sm.met, tid, m);
+  m.n = mn;
+  AggAcc agg;
+#pragma unroll
+  for (int j = 0; j < FIN_AGG_LEN; ++j) agg.s[j] = sm.agg[j][tid];
+  if (live) {
+    if (oor) set_flag(e, FIN_FLAG_ACTION_RANGE);
+    if (bad) set_flag(e, FIN_FLAG_BAD_INDEX);
+    e.cash[i] = b;
+    e.vcur[i] = vc;
+    store_hold2<KA>(e, i, h2);
+    e.t_ep[i] = t;
+    e.window[i] = w;
+    store_metric(e, i, m);
+    if (o.ep_count) o.ep_count[i] = cnt;
+  }
+  agg.s[FIN_AGG_SUM_REWARD] = rsum;
+  if (o.agg_partial) agg_block_write(agg, o.agg_partial + (size_t)blockIdx.x * FIN_AGG_LEN);
+}
+
 #define FIN_DISPATCH_K(K, KERNEL, GRID, STREAM, ...)                                         \
   do {                                                                                       \
     if ((K) == 30) KERNEL<30, true><<<GRID, kStep, 0, STREAM>>>(__VA_ARGS__);                \
@@ -988,6 +1218,19 @@ cudaError_t launch_stock_replay(const EnvDev& e, const int16_t* actions, int T, 
                                 cudaStream_t s) {
   *n_blocks = blocks_for(e.N, kStep);
   const int v = vec_ok(actions, (long long)e.N * e.K);
+#if FIN_K4_PACKED
+  if (e.K == 30 || e.K == 4) {
+    if (e.K == 30) {
+      static const bool attr30 = cudaFuncSetAttribute(k_stock_replay2<30>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      (int)sizeof(K4Smem<30>)) == cudaSuccess;
+      (void)attr30;
+      k_stock_replay2<30><<<blocks_for(e.N, kStep), kStep, sizeof(K4Smem<30>), s>>>(e, actions, T, o, v);
+    } else {
+      k_stock_replay2<4><<<blocks_for(e.N, kStep), kStep, sizeof(K4Smem<4>), s>>>(e, actions, T, o, v);
+    }
+    return cudaGetLastError();
+  }
+#endif
   FIN_DISPATCH_K(e.K, k_stock_replay, blocks_for(e.N, kStep), s, e, actions, T, o, v);
   return cudaGetLastError();
 }

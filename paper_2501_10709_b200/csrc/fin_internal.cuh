@@ -241,6 +241,27 @@ __device__ __forceinline__ void metric_push(MetricAcc& m, double v) {
   m.vprev = v;
 }
 
+// The same push with its three reciprocals formed from the pre-step state (metric_rcps: before
+// the trade, off the serial cash chain): rv = rcp(v_prev), rn = rcp(n + 1), rp = rcp(peak).  The
+// drawdown uses the old peak: when v exceeds it the new peak is v and the term is 0 either way.
+struct MetricRcp {
+  double rv, rn, rp;
+};
+__device__ __forceinline__ MetricRcp metric_rcps(double vprev, double peak, int n) {
+  return MetricRcp{rcp_nr(vprev), rcp_nr(nn2d(n + 1)), rcp_nr(peak)};
+}
+__device__ __forceinline__ void metric_push_pre(MetricAcc& m, double v, const MetricRcp& q) {
+  const double r = fmul64(fsub64(v, m.vprev), q.rv);
+  m.n += 1;
+  const double delta = fsub64(r, m.mean);
+  m.mean = fadd64(m.mean, fmul64(delta, q.rn));
+  m.m2 = fadd64(m.m2, fmul64(delta, fsub64(r, m.mean)));
+  const double dd = v > m.peak ? 0.0 : fmul64(fsub64(v, m.peak), q.rp);
+  m.peak = fmax(m.peak, v);
+  m.mdd = fmin(m.mdd, dd);
+  m.vprev = v;
+}
+
 // (cum, sharpe, mdd) of a finished episode; Sharpe = sqrt(ppy) mean / std(ddof 1),
 // NaN when n < 2 or std == 0 (reading R21).  Reciprocals instead of divisions (each
 // within an ulp): when episodes end at different steps across a warp this runs
