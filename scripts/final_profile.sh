@@ -13,6 +13,8 @@ ncu --set full --clock-control none --import-source on -k "regex:k_tc_rollout" -
     -o gpurun_out/prof_k3 -f python scripts/prof_rollout.py 65536 32 2 > gpurun_out/ncu_k3.log 2>&1
 FIN_TIMING=b2b ncu --set full --clock-control none --import-source on -k "regex:k_stock_step" -s 10 -c 1 \
     -o gpurun_out/prof_k1 -f python scripts/prof_hbm.py k1 > gpurun_out/ncu_k1.log 2>&1
+FIN_TIMING=b2b ncu --set full --clock-control none --import-source on -k "regex:k_stock_replay" -s 10 -c 1 \
+    -o gpurun_out/prof_k4 -f python scripts/prof_hbm.py k4 > gpurun_out/ncu_k4.log 2>&1
 ncu --set full --clock-control none --import-source on -k "regex:k_metrics" -s 3 -c 1 \
     -o gpurun_out/prof_k6 -f python scripts/prof_hbm.py k6 3 > gpurun_out/ncu_k6.log 2>&1
 ncu --set full --clock-control none --import-source on -k "regex:k_gae_tma" -s 2 -c 1 \
