@@ -13,6 +13,11 @@
 //  * prices: the three f64 rows a step needs (p_d, u_d, p_{d+1}) are staged in
 //    shared memory once per block and day (group_apply, group_stage.cuh).
 //  * arithmetic: exact f64 in the oracle's order, int -> f64 on the fp64 pipe.
+// K1 / K4: row values of a whole step's assets in one chunk (ptxas schedules the loads freely;
+// A/B at 6 / 8 / 10 / 12 / 15 / 30 assets per chunk: 30 best, K1 +3%, K4 +4% over 6)
+#ifndef FIN_KCHUNK
+#define FIN_KCHUNK 30
+#endif
 #include "env_stock.cuh"
 #include "group_stage.cuh"
 #include "sm100.cuh"

@@ -26,6 +26,9 @@
 #ifndef FIN_MROWS
 #define FIN_MROWS 0
 #endif
+#ifndef FIN_KCHUNK
+#define FIN_KCHUNK 10  // assets per row chunk (A/B on the headline: 3 / 6 / 8 / 10 / 15 / 30 -> 10 best, +0.7% over 6)
+#endif
 #include "env_stock.cuh"
 #include "group_stage.cuh"
 #include "philox.cuh"

@@ -385,3 +385,54 @@ def test_k4_bench_size_sampled():
         err = np.abs(r[:, j].astype(np.float64) - o["reward"][:, 0])
         assert np.all(err <= 1e-5 * np.abs(o["reward"][:, 0]) + 1e-5 * 2.0 ** -12 * 1e4)
         assert np.asarray(st.cash)[0] == cash[j]
+
+
+@pytest.mark.parametrize("wblock", [1, 100])
+def test_k1_k4_mixed_days_mispredicted_rows(wblock):
+    """K1 and K4 (round-2 packed per-warp forms) where a warp's envs sit on different market days
+    (window block 1: every env its own window) or the next slice's predicted day is wrong (window
+    block 100 does not divide the slice distance): the warps take the L2 row-table path.  Several
+    tiles per persistent block (N = 113,741: 889 tiles, a ragged last one), 33 steps with a reset
+    and a test-mode window advance; sampled envs (slice and tile edges, the tail) against the oracle
+    env by env -- holdings, done, cash bit-exact, reward within tolerance."""
+    import torch
+    fin = _fin()
+    N, T, K = 444 * 128 * 2 + 77, 33, 30
+    m = market.stock_c1(rows=1008)
+    kw = dict(num_envs=N, num_assets=30, num_indicators=8, num_rows=1008, episode_len=30, window_stride=5,
+              num_windows=195, window_block=wblock, advance_window_on_reset=True)
+    ocfg, fcfg = stock_pair(**kw)
+    cols = sorted(set(_sample(N, 30, 5 + wblock) + [31, 32, 63, 64, 95, 96, N - 77, N - 78]))
+    idx = torch.tensor(cols, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(21 + wblock)
+    acts = torch.randint(-100, 101, (T, N, K), device="cuda", generator=g, dtype=torch.int16)
+    a = host(acts[:, idx])
+    # K1: one fin_env_step per step
+    env = fin.fin_env_create(fcfg, m.market)
+    rew, done, cash = [], [], []
+    for t in range(T):
+        r, d, c = zeros(N, torch.float32), zeros(N, torch.uint8), zeros(N, torch.float64)
+        fin.fin_env_step(env, acts[t], fin.make_traj(reward=r, done=d, cash=c))
+        rew.append(host(r[idx])); done.append(host(d[idx])); cash.append(host(c[idx]))
+    hold = zeros((N, K), torch.int16)
+    fin.fin_env_get_state(env, hold=hold)
+    hold = host(hold[idx])
+    assert fin.fin_env_check(env) == 0
+    rew, done, cash = (np.stack(x) for x in (rew, done, cash))
+    # K4: the same actions replayed in one call on a fresh env
+    env4 = fin.fin_env_create(fcfg, m.market)
+    rew4, done4, cash4 = zeros((T, N), torch.float32), zeros((T, N), torch.uint8), zeros((T, N), torch.float64)
+    fin.fin_rollout_actions(env4, acts, T, fin.make_traj(reward=rew4, done=done4, cash=cash4))
+    assert fin.fin_env_check(env4) == 0
+    rew4, done4, cash4 = host(rew4[:, idx]), host(done4[:, idx]), host(cash4[:, idx])
+    for j, i in enumerate(cols):
+        oc = ostock.StockEnvConfig(num_envs=1, env_offset=int(i), num_assets=30, num_indicators=8, num_rows=1008,
+                                   episode_len=30, window_stride=5, num_windows=195, window_block=wblock,
+                                   advance_window_on_reset=True)
+        o, st = ostock.run_actions(oc, m.market, a[:, j:j + 1])
+        tol = 1e-5 * np.abs(o["reward"][:, 0]) + 1e-5 * 2.0 ** -12 * 1e4
+        for rr, dd, cc in ((rew, done, cash), (rew4, done4, cash4)):
+            assert np.array_equal(o["done"][:, 0], dd[:, j] > 0), i
+            assert np.array_equal(o["cash"][:, 0], cc[:, j]), i
+            assert np.all(np.abs(rr[:, j].astype(np.float64) - o["reward"][:, 0]) <= tol), i
+        assert np.array_equal(np.asarray(st.hold)[0], hold[j]), i
