@@ -204,6 +204,7 @@ __device__ __forceinline__ void k1_fetch(const EnvDev& e, const int16_t* actions
 }
 // all lanes: cp.async the price-row block of day d (kPriceRows x kp doubles) into pr
 __device__ __forceinline__ void k1_fetch_rows(const EnvDev& e, double* pr, int d, int lane) {
+  FIN_CHECK(d >= 0 && d + 1 < e.rows);
   const int chunks = kPriceRows * e.kp / 2;
   const double* src = e.px + (size_t)d * kPriceRows * e.kp;
   for (int c = lane; c < chunks; c += 32) sm100::cp_async16(pr + 2 * c, src + 2 * c);
@@ -432,6 +433,7 @@ struct K2Smem {
 };
 template <int KA>
 __device__ __forceinline__ void k2_fetch(const EnvDev& e, const int16_t* actions, K2Slice<KA>& S, int i, int lane) {
+  FIN_CHECK(i >= 0 && i + kK2Slice <= e.N && (i & 1) == 0);   // whole slices of full tiles, 16-B aligned
   constexpr int NS = kK2Slice, H = NS / 2;   // cash | asset: NS / 2 + NS / 2 chunks
 #pragma unroll
   for (int c = 0; c < kK2E; ++c) {
@@ -563,7 +565,8 @@ __global__ void __launch_bounds__(kK2Threads, FIN_K2_MINB)
         if (o.done) o.done[gi[q]] = 1;
       }
       d[q] = day_of(e, w[q], t[q]);
-      FIN_CHECK(!live[q] || (w[q] >= 0 && w[q] < e.W));
+      FIN_CHECK(!live[q] || (gi[q] >= 0 && gi[q] < e.N && w[q] >= 0 && w[q] < e.W && t[q] >= 0));
+      FIN_CHECK(!tma || (idx[q] >= 0 && idx[q] < kK2Slice && gi[q] < e.N));
       const bool bad = stepping && (d[q] < 0 || d[q] + 1 >= e.rows);
       if (bad) set_flag(e, FIN_FLAG_BAD_INDEX);
       go[q] = stepping && !bad;
@@ -990,6 +993,7 @@ __global__ void __launch_bounds__(kStep, FIN_K4_MINB) k_stock_replay2(EnvDev e, 
   const uint32_t mt2 = (uint32_t)e.max_trade * 0x10001u;
   // fetch (all lanes, one cp.async group): step s's action slab of this warp + the rows of day ds
   auto fetch = [&](int s, int ds) {
+    FIN_CHECK(s >= 0 && s < T && (nv == 0 || i0 + nv <= N));
     if (nv > 0) {
       const int16_t* src = actions + ((size_t)s * N + i0) * KA;
       int16_t* dst = sm.act[s & 1][wid];
@@ -1016,6 +1020,7 @@ __global__ void __launch_bounds__(kStep, FIN_K4_MINB) k_stock_replay2(EnvDev e, 
     const size_t ti = (size_t)s * N + i;
     const int d = day_of(e, w, t);
     const bool stepping = live && !bad && t < e.L;
+    FIN_CHECK(!live || (i < N && w >= 0 && w < e.W && t >= 0 && t <= e.L));
     // prefetch step s+1: its slab and the rows of lane 0's next day (d + 1, or the first day of
     // its (possibly advanced) window after a reset)
     int pred_next = -1;
