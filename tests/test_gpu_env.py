@@ -97,15 +97,15 @@ def _redo_case(K=30, N=3000, cost=1e-3):
     return mk, cash, acts
 
 
-@pytest.mark.parametrize("cost", [1e-3, 0.0])
-def test_exact_affordability_redo_path(cost):
+@pytest.mark.parametrize("cost,K", [(1e-3, 30), (0.0, 30), (1e-3, 4)])
+def test_exact_affordability_redo_path(cost, K):
     """The exact out-of-line buy path (env_stock.cuh stock_buys_exact, reached only when
     the fast floor estimate fails its check) runs -- the handle's event counter proves
     it -- and gives cash and holdings bitwise equal to the oracle's definition (R5), in
     K1 (fin_env_step) and K4 (fin_rollout_actions).  Control: unbinding buys never take it."""
     import torch
     fin = _fin()
-    K, N = 30, 3000
+    N = 3000
     mk, cash, acts = _redo_case(K, N, cost)
     ocfg, fcfg = stock_pair(num_envs=N, num_assets=K, num_indicators=1, num_rows=3, episode_len=2,
                             cost_rate=cost, window_block=N)
