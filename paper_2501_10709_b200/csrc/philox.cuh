@@ -67,6 +67,36 @@ __device__ __forceinline__ Normals8 philox_normals8_v(uint64_t g, uint32_t t, ui
   return o;
 }
 
+// Four counters (word2 = w2[0..3]) interleaved: 16 normals (Box-Muller pairs of each counter's
+// words 0-1 and 2-3, as philox_normals8_v per counter)
+struct Normals16 {
+  float v[16];
+};
+__device__ __forceinline__ Normals16 philox_normals16_v(uint64_t g, uint32_t t, const uint32_t (&w2)[4], uint64_t seed) {
+  uint32_t c[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) { c[q][0] = (uint32_t)g; c[q][1] = t; c[q][2] = w2[q]; c[q][3] = 0u; }
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t h0 = __umulhi(0xD2511F53u, c[q][0]), l0 = 0xD2511F53u * c[q][0];
+      const uint32_t h1 = __umulhi(0xCD9E8D57u, c[q][2]), l1 = 0xCD9E8D57u * c[q][2];
+      const uint32_t n0 = h1 ^ c[q][1] ^ k0, n2 = h0 ^ c[q][3] ^ k1;
+      c[q][0] = n0; c[q][1] = l1; c[q][2] = n2; c[q][3] = l0;
+    }
+  }
+  Normals16 o;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    box_muller(philox_u01(c[q][0]), philox_u01(c[q][1]), o.v[4 * q], o.v[4 * q + 1]);
+    box_muller(philox_u01(c[q][2]), philox_u01(c[q][3]), o.v[4 * q + 2], o.v[4 * q + 3]);
+  }
+  return o;
+}
+
 __device__ __forceinline__ void philox_normals4(uint64_t g, uint32_t t, uint32_t word2, uint64_t seed, float z[4]) {
   const Normals8 v = philox_normals8_v(g, t, word2, word2, seed);
   z[0] = v.a.x; z[1] = v.a.y; z[2] = v.a.z; z[3] = v.a.w;

@@ -42,6 +42,9 @@ __device__ __forceinline__ uint32_t bf16_bits(float v) {
   return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v));
 }
 
+#ifndef FIN_PHILOX16
+#define FIN_PHILOX16 0   // 1: consume draws 16 normals per Philox call (4 counters interleaved)
+#endif
 #ifndef FIN_NOISE_LATE
 #define FIN_NOISE_LATE 1   // 1: noise in consume for the single policy, under layer 2 for ensembles
 #endif
@@ -413,9 +416,36 @@ struct StockOps {
       for (int k = 0; k < KA; ++k) dst[k] = z[k];
     }
     const float wm = p.weighted ? p.mw[m] : 1.f;
+#if FIN_PHILOX16
+    // in-kernel Philox noise: four counters per call (16 normals), twice the interleave
+    Normals16 n16;
+#endif
 #pragma unroll
     for (int pb = 0; pb < (KA + 7) / 8; ++pb) {
       float eps[8];
+#if FIN_PHILOX16
+      if constexpr (kNoiseLate) {
+        if (p.noise_mode == FIN_NOISE_PHILOX) {
+          if ((pb & 1) == 0) {
+            const uint32_t mb = (uint32_t)m << 16;
+            const uint32_t w2[4] = {mb | (uint32_t)(2 * pb), mb | (uint32_t)(2 * pb + 1), mb | (uint32_t)(2 * pb + 2),
+                                    mb | (uint32_t)(2 * pb + 3)};
+            n16 = philox_normals16_v((uint64_t)(e.env_offset + env), (uint32_t)(e.t_global + t), w2, p.noise_seed);
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) eps[j] = n16.v[8 * (pb & 1) + j];
+        } else {
+          const float* nz = p.noise + (((size_t)t * p.M + m) * e.N + env) * KA;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) eps[j] = 0.f;
+          if (p.noise_mode == FIN_NOISE_SUPPLIED) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (pb * 8 + j < KA) eps[j] = __ldg(nz + pb * 8 + j);
+          }
+        }
+      } else
+#endif
       if constexpr (kNoiseLate) {
         const float* nz = p.noise + (((size_t)t * p.M + m) * e.N + env) * KA;
 #pragma unroll
