@@ -964,7 +964,7 @@ def hbm_kernels(fin, torch):
     acts = torch.randint(-100, 101, (N, K_ASSETS), device="cuda", generator=g, dtype=torch.int16)
     tr = fin.make_traj(reward=z(N, torch.float32), done=z(N, torch.uint8))
     ms = b2b(lambda: fin.fin_env_step(env, acts, tr))
-    entry("step_kernel_hbm", "k_stock_step (K1)", N, STEP_BYTES_ALGO * N, ms,
+    entry("step_kernel_hbm", "k_stock_step2 (K1, packed per-warp form)", N, STEP_BYTES_ALGO * N, ms,
           "SURVEY d.3's 209 B/env-step (the kernel moves 237 B: cached asset, window, holdings octet padding); "
           "steady state: "
           "the same seeded U{-100..100} actions every step, so the cash binds in most steps")
@@ -976,7 +976,7 @@ def hbm_kernels(fin, torch):
     tr = fin.make_traj(reward=z((T, N), torch.float32), done=z((T, N), torch.uint8))
     ms = b2b(lambda: fin.fin_rollout_actions(env, acts, T, tr))
     state = 2 * (8 + 8 + 60 + 4 + 4 + 52)   # per env per call: cash, asset, holdings, clock, window, metrics
-    entry("replay_kernel_hbm", "k_stock_replay (K4)", N * T, N * T * 65 + N * state, ms,
+    entry("replay_kernel_hbm", "k_stock_replay2 (K4, packed per-warp form)", N * T, N * T * 65 + N * state, ms,
           "actions 60 + reward 4 + done 1 per env-step, state in/out once per call")
     del env, acts, tr
     T, N = 2048, 1 << 18

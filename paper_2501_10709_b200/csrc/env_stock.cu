@@ -5,13 +5,16 @@
 //
 // K1 / K4 layout of work: one env per thread, 128-thread blocks
 // (one window block of envs, so the block normally sits on one market day).
-//  * state: coalesced SoA loads; holdings as 16-byte asset octets (hold_at).
+//  * state: coalesced SoA; holdings as 16-byte asset octets (hold_at), kept packed two
+//    assets per 32-bit word in registers by the default (even K) kernels k_stock_step2 /
+//    k_stock_replay2, which run the 16-bit SIMD / exact-f64 trade of env_stock.cuh k2_trade.
 //  * actions [N][K] int16 (caller layout, 60 B per env at K = 30): each warp copies
-//    its 32 contiguous rows into shared memory with 16-byte cp.async, then every
-//    thread reads its row as 32-bit words (stride K/2 words: conflict-free for odd
-//    K/2).  K4 double-buffers the copy of step s+1 under the arithmetic of step s.
-//  * prices: the three f64 rows a step needs (p_d, u_d, p_{d+1}) are staged in
-//    shared memory once per block and day (group_apply, group_stage.cuh).
+//    its contiguous rows into shared memory with 16-byte cp.async, one slice / step
+//    ahead, then every thread reads its row as 32-bit words (stride K/2 words:
+//    conflict-free for odd K/2).
+//  * prices: the f64 price-row block of a day (px, fin_internal.cuh) is prefetched per
+//    warp for the day predicted from lane 0's env; a warp whose envs sit elsewhere reads
+//    the L2-resident table (the padded-K replay k_stock_replay stages per block and day).
 //  * arithmetic: exact f64 in the oracle's order, int -> f64 on the fp64 pipe.
 // K1 / K4: row values of a whole step's assets in one chunk (ptxas schedules the loads freely;
 // A/B at 6 / 8 / 10 / 12 / 15 / 30 assets per chunk: 30 best, K1 +3%, K4 +4% over 6)
