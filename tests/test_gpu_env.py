@@ -436,3 +436,34 @@ def test_k1_k4_mixed_days_mispredicted_rows(wblock):
             assert np.array_equal(o["cash"][:, 0], cc[:, j]), i
             assert np.all(np.abs(rr[:, j].astype(np.float64) - o["reward"][:, 0]) <= tol), i
         assert np.array_equal(np.asarray(st.hold)[0], hold[j]), i
+
+
+def test_k1_k4_extreme_cash_takes_the_exact_path():
+    """Cash far beyond 2^32 shares of any asset (1e15, 2^40, +inf): the floor estimate's hi-word
+    check fails, the exact redo runs (counter) and cash / holdings equal the oracle's definition
+    bit for bit (R5: every buy is its full want), in K1 and K4, full tiles and a ragged one."""
+    import torch
+    fin = _fin()
+    K = 30
+    for N in (256, 300):
+        mk = market.stock_c1(rows=80)
+        ocfg, fcfg = stock_pair(num_envs=N, num_assets=K, num_indicators=8, num_rows=80, episode_len=5,
+                                num_windows=10, window_block=N)
+        acts = inputs.stock_actions(1, N, K, seed=3)[0]
+        cash = np.array([[1e15, 2.0 ** 40, np.inf, 7.5e12][i % 4] for i in range(N)])
+        st0 = ostock.reset(ocfg)
+        st0.cash = [float(x) for x in cash]
+        o = ostock.step(ocfg, st0, mk.market, acts)
+        want_b, want_h = np.array(o["cash"]), np.array(o["hold"], dtype=np.int64)
+        for path in ("k1", "k4"):
+            env = fin.fin_env_create(fcfg, mk.market)
+            fin.fin_env_set_state(env, cash=dev(cash), hold=zeros((N, K), torch.int16), t_ep=zeros(N, torch.int32))
+            fin.fin_env_counters(env, clear=True)
+            c, h = zeros((1, N), torch.float64), zeros((1, N, K), torch.int16)
+            if path == "k1":
+                fin.fin_env_step(env, dev(acts, torch.int16), fin.make_traj(cash=c, hold=h))
+            else:
+                fin.fin_rollout_actions(env, dev(acts[None], torch.int16), 1, fin.make_traj(cash=c, hold=h))
+            assert fin.fin_env_counters(env)["exact_redo"] > 0, (path, N)
+            assert np.array_equal(host(c)[0].view(np.uint64), want_b.view(np.uint64)), (path, N)
+            assert np.array_equal(host(h)[0], want_h), (path, N)
