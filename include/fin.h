@@ -65,7 +65,9 @@ enum {
   FIN_FLAG_ACTION_RANGE = 1,   /* |action| > max_trade: clamped (R6) */
   FIN_FLAG_EPISODE_DONE = 2,   /* step of a done env with autoreset = 0: ignored */
   FIN_FLAG_NONFINITE = 4,      /* non-finite MLP output / noise: action forced to 0 */
-  FIN_FLAG_BAD_INDEX = 8       /* market row index out of range: env left unchanged */
+  FIN_FLAG_BAD_INDEX = 8,      /* market row index out of range: env left unchanged */
+  FIN_FLAG_NOISE_WAIT = 16     /* small-N rollout: the streamed pre-drawn noise of a step did not
+                                  arrive within ~8 s (the step used whatever the buffer held) */
 };
 
 enum { FIN_STOCK = 0, FIN_CRYPTO = 1 };
@@ -208,8 +210,11 @@ int fin_env_check(fin_env* env, uint32_t* flags /*host*/);
  *       of the unit cost); for tests, which prove the slow path ran;
  *   [1] fused stock rollouts launched with the balanced persistent schedule;
  *   [2] rollouts where that cooperative launch was refused and one tile per CTA ran instead;
- *   [3] the cudaError_t of the last refusal (0: none). */
-enum { FIN_CTR_LEN = 4 };
+ *   [3] the cudaError_t of the last refusal (0: none);
+ *   [4] fused stock rollouts whose Philox noise was drawn by a separate kernel (small N: tiles
+ *       at most twice the idle SMs; streamed on those SMs while the rollout runs; the same
+ *       normals, bitwise, as the in-kernel draws). */
+enum { FIN_CTR_LEN = 5 };
 int fin_env_counters(fin_env* env, uint32_t* counters /*host*/, int32_t clear);
 
 void fin_env_destroy(fin_env* env);

@@ -9,6 +9,7 @@
 #include <new>
 #include <string>
 #include <type_traits>
+#include <algorithm>
 #include <atomic>
 #include <vector>
 
@@ -21,6 +22,12 @@ namespace fin {
 // = ceil(n_envs / (128 * tiles)) * tiles)
 cudaError_t launch_stock_rollout(int net, const tc::TcParams& p, int n_envs, int* tiles, cudaStream_t s);
 int stock_seg_grid(int net, const tc::TcParams& p, int n_envs);
+int num_sms();
+cudaError_t launch_pregen_noise(uint64_t seed, int64_t off, int N, int K, int M, int64_t t0, int T, float* out,
+                                cudaStream_t s);
+cudaError_t load_stream_noise();
+cudaError_t launch_stream_noise(uint64_t seed, int64_t off, int N, int K, int M, int64_t t0, int T, float* out,
+                                uint32_t* ready, int blocks, cudaStream_t s);
 cudaError_t launch_crypto_market(int64_t steps, uint64_t seed, double sigma, double m0, double phi, float* rows,
                                  cudaStream_t s);
 cudaError_t launch_stock_market(int D, int K, uint64_t seed, double mu, double sigma, double s0_lo, double s0_hi,
@@ -95,6 +102,14 @@ struct fin_env {
   uint32_t seg_epoch;   // per-call value of the tiles' progress flags
   uint32_t ctr_seg, ctr_seg_fallback;   // rollouts launched with the chunk schedule / refused
   int seg_fallback_err;                 // cudaError_t of the last refusal
+  // small-N rollouts: the step noise pre-drawn by k_pregen_noise
+  float* noise_mem;     // [T][M][N][K] normals of the last pre-drawn rollout
+  size_t noise_cap;     // floats
+  uint32_t ctr_pregen;  // rollouts that ran on pre-drawn noise
+  uint32_t* noise_ready;   // [ceil(T / FIN_NOISE_GROUP)] streamed mode: producer blocks finished per step group
+  size_t ready_cap;
+  cudaStream_t noise_side;              // streamed mode: the producer's stream (forked / joined per call)
+  cudaEvent_t noise_fork, noise_join;
 };
 
 struct fin_policy {
@@ -573,7 +588,7 @@ int fin_env_check(fin_env* env, uint32_t* flags) {
   FIN_CUDA(cudaMemcpy(&f, env->d.flags, sizeof(f), cudaMemcpyDeviceToHost));
   FIN_CUDA(cudaMemset(env->d.flags, 0, sizeof(uint32_t)));
   if (flags) *flags = f;
-  if (f) return fail(FIN_E_DEVICE_ASYNC, "device flags 0x%x (1 action range, 2 episode done, 4 non-finite, 8 index)", f);
+  if (f) return fail(FIN_E_DEVICE_ASYNC, "device flags 0x%x (1 action range, 2 episode done, 4 non-finite, 8 index, 16 noise wait)", f);
   return FIN_OK;
 }
 
@@ -585,9 +600,10 @@ int fin_env_counters(fin_env* env, uint32_t* counters, int32_t clear) {
   counters[1] = env->ctr_seg;
   counters[2] = env->ctr_seg_fallback;
   counters[3] = (uint32_t)env->seg_fallback_err;
+  counters[4] = env->ctr_pregen;
   if (clear) {
     FIN_CUDA(cudaMemset(env->d.flags + FIN_CTR_EXACT_REDO, 0, FIN_CTR_LEN * sizeof(uint32_t)));
-    env->ctr_seg = env->ctr_seg_fallback = 0;
+    env->ctr_seg = env->ctr_seg_fallback = env->ctr_pregen = 0;
   }
   return FIN_OK;
 }
@@ -596,6 +612,11 @@ void fin_env_destroy(fin_env* env) {
   if (!env) return;
   cudaStreamSynchronize(env->last_stream);
   if (env->q_ctr) cudaFree(env->q_ctr);
+  if (env->noise_mem) cudaFree(env->noise_mem);
+  if (env->noise_ready) cudaFree(env->noise_ready);
+  if (env->noise_side) cudaStreamDestroy(env->noise_side);
+  if (env->noise_fork) cudaEventDestroy(env->noise_fork);
+  if (env->noise_join) cudaEventDestroy(env->noise_join);
   if (env->agg_scratch) cudaFree(env->agg_scratch);
   if (env->z1s) cudaFree(env->z1s);
   if (env->ou_mem) cudaFree(env->ou_mem);
@@ -880,6 +901,100 @@ int fill_noise(const fin_noise* noise, tc::TcParams& p) {
   return FIN_OK;
 }
 
+// Small N (fewer tiles than SMs: the fused rollout is latency-bound on each tile's serial step
+// chain): the rollout's Philox normals are drawn by a separate kernel and read
+// as supplied noise, taking the Philox / Box-Muller work off the chain -- bitwise the in-kernel
+// draws (same counters, same philox_normals8_v).  "Streamed" (FIN_PREGEN=2): the
+// producer k_stream_noise runs on the idle SMs concurrently with the rollout (a side stream
+// forked after the flag reset and joined after the rollout) and publishes each finished group of
+// 8 steps in noise_ready[t / 8]; used when the idle SMs number at least half the tiles (A/B,
+// scripts/pregen_ab.py, N x 256 steps: +8.0% at N = 64, +7.3% at 2,048, +5.4% at 8,192, +5.0% at
+// 12,288 = 96 tiles; -10.7% at 16,384, whose 20 idle SMs cannot keep up).  FIN_PREGEN=1: the whole
+// buffer drawn before the rollout (k_pregen_noise; A/B: +10.9% at N = 64, +6.5% at 2,048 x 30
+// (streamed +3.1%), -0.8% at 8,192 x 256); FIN_PREGEN=0: in-kernel draws.  Large N keeps the in-kernel draws,
+// which ride on issue slots the env phases leave idle.
+constexpr size_t kPregenCapBytes = size_t(1) << 30;
+struct NoisePlan {
+  int mode = 0;   // 0 none, 1 drawn before the rollout, 2 streamed (producer launched after it)
+  int blocks = 0;
+  size_t elems = 0;
+};
+int plan_noise(fin_env* env, tc::TcParams& p, int n_tiles, int T, cudaStream_t s, NoisePlan& np) {
+  np = NoisePlan();
+  if (env->d.task != FIN_STOCK || p.noise_mode != FIN_NOISE_PHILOX || p.act_only) return FIN_OK;
+  const size_t elems = (size_t)T * p.M * env->d.N * env->d.K;
+  if (elems * sizeof(float) > kPregenCapBytes) return FIN_OK;
+  const int free_sms = fin::num_sms() - n_tiles;
+  const char* force = getenv("FIN_PREGEN");
+  // default: drawn before the rollout up to 2,048 env-members (its cost ~N T / 7,700 us against a
+  // gain of ~T us: it pays below ~7,700 envs, and beats streaming where the producer's start-up
+  // shows, e.g. T = 30), streamed while the idle SMs number at least half the tiles
+  int mode = force ? atoi(force) : (2 * free_sms < n_tiles ? 0 : (size_t)p.M * env->d.N <= 2048 ? 1 : 2);
+  if (mode == 2 && free_sms < 1) mode = 0;   // the producer needs SMs the rollout's tiles leave free
+  if (mode == 2 && getenv("FIN_SEG_PROF")) mode = 1;   // that debug path synchronises right after the launch
+  if (mode < 1 || mode > 3) return FIN_OK;   // 3 (A/B only): the streamed path with the producer run first
+  if (env->noise_cap < elems) {
+    if (env->noise_mem) cudaFree(env->noise_mem);   // synchronises: no rollout still reads it
+    env->noise_mem = nullptr;
+    env->noise_cap = 0;
+    FIN_CUDA(cudaMalloc(&env->noise_mem, elems * sizeof(float)));
+    env->noise_cap = elems;
+  }
+  if (mode == 1) {
+    cudaError_t e = fin::launch_pregen_noise(p.noise_seed, env->d.env_offset, env->d.N, env->d.K, p.M,
+                                             env->d.t_global, T, env->noise_mem, s);
+    if (e != cudaSuccess) return cuda_fail(e, "fin_rollout pre-drawn noise");
+  } else {
+    const size_t groups = ((size_t)T + FIN_NOISE_GROUP - 1) / FIN_NOISE_GROUP;
+    if (env->ready_cap < groups) {
+      if (env->noise_ready) cudaFree(env->noise_ready);
+      env->noise_ready = nullptr;
+      env->ready_cap = 0;
+      FIN_CUDA(cudaMalloc(&env->noise_ready, groups * sizeof(uint32_t)));
+      env->ready_cap = groups;
+    }
+    cudaError_t le = fin::load_stream_noise();   // before the rollout that will wait on it
+    if (le != cudaSuccess) return cuda_fail(le, "fin_rollout streamed noise (load)");
+    if (!env->noise_side) {
+      FIN_CUDA(cudaStreamCreateWithFlags(&env->noise_side, cudaStreamNonBlocking));
+      FIN_CUDA(cudaEventCreateWithFlags(&env->noise_fork, cudaEventDisableTiming));
+      FIN_CUDA(cudaEventCreateWithFlags(&env->noise_join, cudaEventDisableTiming));
+    }
+    FIN_CUDA(cudaMemsetAsync(env->noise_ready, 0, groups * sizeof(uint32_t), s));
+    FIN_CUDA(cudaEventRecord(env->noise_fork, s));   // the producer waits for the reset only
+    const size_t per_t = (size_t)p.M * env->d.N * ((env->d.K + 7) / 8);
+    const size_t need = (per_t + 511) / 512;   // 512-thread blocks, one per idle SM
+    np.blocks = (int)std::min<size_t>(need, (size_t)std::max(free_sms, 1));
+    p.noise_ready = env->noise_ready;
+    p.noise_ready_target = (uint32_t)np.blocks;
+    if (mode == 3) {
+      cudaError_t e3 = fin::launch_stream_noise(p.noise_seed, env->d.env_offset, env->d.N, env->d.K, p.M,
+                                                env->d.t_global, T, env->noise_mem, env->noise_ready, np.blocks, s);
+      if (e3 != cudaSuccess) return cuda_fail(e3, "fin_rollout streamed noise");
+    }
+  }
+  p.noise_mode = FIN_NOISE_SUPPLIED;
+  p.noise = env->noise_mem;
+  np.mode = mode;
+  np.elems = elems;
+  ++env->ctr_pregen;
+  return FIN_OK;
+}
+
+// streamed mode, after the rollout's launch (so its tiles take their SMs first): the producer
+// on the side stream, then the caller's stream joins it
+int launch_noise_producer(fin_env* env, const tc::TcParams& p, const NoisePlan& np, int T, cudaStream_t s) {
+  if (np.mode != 2) return FIN_OK;
+  FIN_CUDA(cudaStreamWaitEvent(env->noise_side, env->noise_fork, 0));
+  cudaError_t e = fin::launch_stream_noise(p.noise_seed, env->d.env_offset, env->d.N, env->d.K, p.M,
+                                           env->d.t_global, T, env->noise_mem, env->noise_ready, np.blocks,
+                                           env->noise_side);
+  if (e != cudaSuccess) return cuda_fail(e, "fin_rollout streamed noise");
+  FIN_CUDA(cudaEventRecord(env->noise_join, env->noise_side));
+  FIN_CUDA(cudaStreamWaitEvent(s, env->noise_join, 0));
+  return FIN_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -899,6 +1014,9 @@ int fin_rollout(fin_env* env, const fin_policy* const* members, int32_t n_member
   rc = prepare_z1s(env, members, n_members, net, p, S(stream));
   if (rc != FIN_OK) return rc;
   const int n_tiles = (env->d.N + tc::kTileM - 1) / tc::kTileM;
+  NoisePlan np;
+  rc = plan_noise(env, p, n_tiles, T, S(stream), np);
+  if (rc != FIN_OK) return rc;
   p.e = env->d;
   p.o = to_dev(out);
   p.T = T;
@@ -944,6 +1062,10 @@ int fin_rollout(fin_env* env, const fin_policy* const* members, int32_t n_member
       p.q_ctr = nullptr;
       e = fin::launch_stock_rollout(net, p, env->d.N, &tiles, S(stream));
     }
+  }
+  if (e == cudaSuccess) {
+    rc = launch_noise_producer(env, p, np, T, S(stream));
+    if (rc != FIN_OK) return rc;
   }
   mark_used(members, n_members, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fin_rollout launch");

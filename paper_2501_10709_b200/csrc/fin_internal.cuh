@@ -81,7 +81,9 @@ struct EnvDev {
   uint32_t* flags;       // sticky device error word; flags[FIN_CTR_*] are event counters (fin_env_counters)
 };
 // counters after the flags word (same 64-B block)
-#define FIN_CTR_EXACT_REDO 4   // stock: steps whose buys took the exact out-of-line affordability path
+#define FIN_CTR_EXACT_REDO 4
+// streamed small-N noise: steps per published group (k_stream_noise / noise_wait)
+#define FIN_NOISE_GROUP 8   // stock: steps whose buys took the exact out-of-line affordability path
 
 struct TrajDev {
   float* reward;

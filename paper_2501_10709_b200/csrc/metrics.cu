@@ -441,6 +441,62 @@ __global__ void k_philox_normals(uint64_t seed, int64_t off, int N, int K, int m
   }
 }
 
+// Pre-drawn exploration noise of a latency-bound (small-N) fused stock rollout
+// (DESIGN.md §4.3 "small N"): the normals consume() / prepare() would draw in-kernel --
+// the same Philox4x32-10 counters {global env id, t_global + t, m << 16 | counter, 0}
+// and Box-Muller (reading R-NOISE, PAPER.md P:130 eps) through the same
+// philox_normals8_v -- written in the supplied-noise layout [T][M][N][K]. One thread per
+// (t, m, env, 8-asset block); grid-stride; total < 2^31 (the caller caps the buffer).
+__global__ void k_pregen_noise(uint64_t seed, int64_t off, int N, int K, int M, int64_t t0, int T, float* out) {
+  const uint32_t nb = (uint32_t)(K + 7) / 8;
+  const uint32_t total = (uint32_t)T * (uint32_t)M * (uint32_t)N * nb;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t pb = i % nb;
+    const uint32_t r = i / nb;
+    const uint32_t env = r % (uint32_t)N, tm = r / (uint32_t)N;
+    const uint32_t m = tm % (uint32_t)M, t = tm / (uint32_t)M;
+    const Normals8 v = philox_normals8_v((uint64_t)(off + env), (uint32_t)(t0 + t), (m << 16) | (2 * pb),
+                                         (m << 16) | (2 * pb + 1), seed);
+    const float z[8] = {v.a.x, v.a.y, v.a.z, v.a.w, v.b.x, v.b.y, v.b.z, v.b.w};
+    float* dst = out + (size_t)r * K + 8 * pb;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (8 * (int)pb + j < K) dst[j] = z[j];
+  }
+}
+
+// The same normals streamed step by step while the rollout runs (small N: the rollout's
+// tiles occupy few SMs; this kernel runs on the idle ones).  Every block takes its share of
+// step t's (m, env, 8-asset block) items; after every FIN_NOISE_GROUP steps it counts the group
+// finished in ready[t / FIN_NOISE_GROUP] (each thread's stores fenced, block barrier, one release
+// add -- per group, so the consumers' acquire round trips are 1/8 of the steps); blocks never wait on the
+// rollout, so the pair cannot deadlock whatever the order the blocks become resident in.
+__global__ void k_stream_noise(uint64_t seed, int64_t off, int N, int K, int M, int64_t t0, int T, float* out,
+                               uint32_t* ready) {
+  const uint32_t nb = (uint32_t)(K + 7) / 8;
+  const uint32_t per_t = (uint32_t)M * (uint32_t)N * nb;
+  for (int t = 0; t < T; ++t) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < per_t; i += gridDim.x * blockDim.x) {
+      const uint32_t pb = i % nb;
+      const uint32_t r = i / nb;
+      const uint32_t env = r % (uint32_t)N, m = r / (uint32_t)N;
+      const Normals8 v = philox_normals8_v((uint64_t)(off + env), (uint32_t)(t0 + t), (m << 16) | (2 * pb),
+                                           (m << 16) | (2 * pb + 1), seed);
+      const float z[8] = {v.a.x, v.a.y, v.a.z, v.a.w, v.b.x, v.b.y, v.b.z, v.b.w};
+      float* dst = out + ((size_t)t * M * N + r) * K + 8 * pb;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (8 * (int)pb + j < K) dst[j] = z[j];
+    }
+    if ((t + 1) % FIN_NOISE_GROUP == 0 || t == T - 1) {   // publish a group of steps
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0)
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ready + t / FIN_NOISE_GROUP) : "memory");
+    }
+  }
+}
+
 // Ensemble member weights from validation statistics (reading
 // R-GATE): Sharpe_m = sum_m / count_m; discard Sharpe < threshold or NaN; softmax at
 // temperature tau over the rest (shifted by the largest kept Sharpe); none kept -> the
@@ -535,6 +591,44 @@ cudaError_t launch_episode_metrics(const double* equity, const uint8_t* done, in
 cudaError_t launch_philox_normals(uint64_t seed, int64_t off, int N, int K, int member, int64_t t, float* out,
                                   cudaStream_t s) {
   k_philox_normals<<<(N + 127) / 128, 128, 0, s>>>(seed, off, N, K, member, t, out);
+  return cudaGetLastError();
+}
+
+int num_sms();
+
+// Load the producer's module and set its attributes before the rollout that waits on it is
+// launched: with lazy module loading a first launch of k_stream_noise behind a running
+// (spinning) rollout waits for the device to idle -- the pair would deadlock.
+constexpr int kStreamSmem = 117 * 1024;   // > half an SM: a producer block never shares an SM with another
+                                          // one or with a rollout CTA (> 100 KB), so it cannot steal issue
+                                          // slots from a tile's step chain
+cudaError_t load_stream_noise() {
+  static cudaError_t st = cudaErrorNotReady;
+  if (st == cudaErrorNotReady) {
+    cudaFuncAttributes fa;
+    st = cudaFuncGetAttributes(&fa, k_stream_noise);
+    if (st == cudaSuccess)
+      st = cudaFuncSetAttribute(k_stream_noise, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmem);
+  }
+  return st;
+}
+
+cudaError_t launch_stream_noise(uint64_t seed, int64_t off, int N, int K, int M, int64_t t0, int T, float* out,
+                                uint32_t* ready, int blocks, cudaStream_t s) {
+  if ((size_t)M * N * ((K + 7) / 8) >= (1ull << 31) || blocks <= 0) return cudaErrorInvalidValue;
+  cudaError_t e = load_stream_noise();
+  if (e != cudaSuccess) return e;
+  k_stream_noise<<<blocks, 512, kStreamSmem, s>>>(seed, off, N, K, M, t0, T, out, ready);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pregen_noise(uint64_t seed, int64_t off, int N, int K, int M, int64_t t0, int T, float* out,
+                                cudaStream_t s) {
+  const size_t total = (size_t)T * M * N * ((K + 7) / 8);
+  if (total == 0) return cudaSuccess;
+  if (total >= (1ull << 31)) return cudaErrorInvalidValue;
+  const size_t blocks = (total + 255) / 256, cap = (size_t)num_sms() * 8;
+  k_pregen_noise<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, s>>>(seed, off, N, K, M, t0, T, out);
   return cudaGetLastError();
 }
 

@@ -49,6 +49,55 @@ __device__ __forceinline__ uint32_t bf16_bits(float v) {
 #define FIN_NOISE_LATE 1   // 1: noise in consume for the single policy, under layer 2 for ensembles
 #endif
 
+// Supplied normals [T][M][N][K].  Streamed (p.noise_ready != null, small N):
+// k_stream_noise writes them on the idle SMs while this kernel runs; each of its blocks finishes
+// the steps in order and counts each group of FIN_NOISE_GROUP steps in noise_ready[t / G]
+// (release), so a full count at group g publishes every step before its end.  A consumer that
+// has not yet seen step t complete (avail < t) first checks the last group (once the producer is
+// done: no further waits in the call), else waits for t's group (acquire).  The data are then
+// read by weak loads, ordered after the acquire by the memory model (never the non-coherent
+// path, whose lines may predate the producer's stores), from a pointer laundered after the
+// wait so the compiler cannot hoist them above it.  The wait is bounded (~8 s): past it the
+// sticky FIN_FLAG_NOISE_WAIT is raised and later waits return at once.
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* f) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  return v;
+}
+// the step's noise pointer, laundered through a volatile asm after the wait: the loads depend
+// on it, so the compiler cannot hoist them above the wait (they stay free to batch)
+__device__ __forceinline__ const float* noise_after_wait(const float* a) {
+  const float* q;
+  asm volatile("mov.b64 %0, %1;" : "=l"(q) : "l"(a));
+  return q;
+}
+template <bool STREAM>
+__device__ __forceinline__ float noise_ld(const float* a) {
+  if constexpr (STREAM) return *noise_after_wait(a);   // a weak load ordered after the acquire
+  else return __ldg(a);
+}
+__device__ __forceinline__ void noise_wait(const TcParams& p, const EnvDev& e, int t, int& avail) {
+  if (t <= avail) return;   // (the laundered loads follow the wait)
+  const uint32_t tgt = p.noise_ready_target;
+  const int last = (p.T - 1) / FIN_NOISE_GROUP, g = t / FIN_NOISE_GROUP;
+  if (g < last && ld_acquire_u32(p.noise_ready + last) >= tgt) {
+    avail = p.T - 1;
+    return;
+  }
+  for (uint32_t spin = 0;; ++spin) {
+    if (ld_acquire_u32(p.noise_ready + g) >= tgt) {
+      avail = g * FIN_NOISE_GROUP + FIN_NOISE_GROUP - 1;
+      return;
+    }
+    if (spin == 0 && (*(const volatile uint32_t*)e.flags & FIN_FLAG_NOISE_WAIT)) return;   // sticky: wait once
+    if (spin > (1u << 26)) {
+      set_flag(e, FIN_FLAG_NOISE_WAIT);
+      return;
+    }
+    __nanosleep(128);
+  }
+}
+
 // tanh(x) = sign(x) (1 - 2 / (exp(2|x|) + 1)) with the fast exp / reciprocal: absolute
 // error ~1e-7 (the sampled share count 100 a moves by ~1e-5, well inside the 1e-4
 // rounding-boundary allowance of the parity check); ~8 instructions instead of the
@@ -64,8 +113,12 @@ __device__ __forceinline__ float tanh_f32(float x) {
 // asset, holdings, network outputs / hidden activations) and no fin_ensemble_act mode
 // -- the production rollout (reward, done, episode metrics, aggregate) carries none of
 // their per-step branches.
-template <int KA, int IA, class Plan, bool ENS = true, bool LOG = true>
+// STREAM = true: the small-N instantiation that reads streamed pre-drawn noise (p.noise_ready,
+// DESIGN.md §4.3); the others carry none of its code (A/B: the wait code alone in the large-N
+// kernel cost 3% of the headline).
+template <int KA, int IA, class Plan, bool ENS = true, bool LOG = true, bool STREAM = false>
 struct StockOps {
+  static constexpr bool kStream = STREAM;
   static constexpr int KOU = ENS ? KA : 1;
   static constexpr bool kSplitOK = false;
   static constexpr bool kSegments = true;   // balanced persistent schedule (init_seg / finalize_seg)
@@ -143,6 +196,7 @@ struct StockOps {
     int cnt;
     double rsum;
     int t_begin, t_end;   // steps of this segment (whole call: 0, T)
+    int navail;           // streamed noise: last step known complete (noise_wait)
     bool oor, bad, nonfinite;
   };
 
@@ -154,6 +208,7 @@ struct StockOps {
   __device__ __forceinline__ static void init_seg(State& st, const TcParams& p, int env, int row, int t0, int t1) {
     const EnvDev& e = p.e;
     st.live = env < e.N;
+    if constexpr (STREAM) st.navail = -1;
     st.t_begin = t0;
     st.t_end = t1;
     st.round = 0;
@@ -395,9 +450,10 @@ struct StockOps {
         eps[4] = nv.b.x; eps[5] = nv.b.y; eps[6] = nv.b.z; eps[7] = nv.b.w;
         if (pb == 0) FIN_TR(threadIdx.x == 128 && m == 0, t, 16);
       } else if (p.noise_mode == FIN_NOISE_SUPPLIED) {
+        if constexpr (STREAM) if (pb == 0) noise_wait(p, e, t, st.navail);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if (pb * 8 + j < KA) eps[j] = __ldg(nz + pb * 8 + j);
+          if (pb * 8 + j < KA) eps[j] = noise_ld<STREAM>(nz + pb * 8 + j);
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j)
@@ -439,9 +495,10 @@ struct StockOps {
 #pragma unroll
           for (int j = 0; j < 8; ++j) eps[j] = 0.f;
           if (p.noise_mode == FIN_NOISE_SUPPLIED) {
+            if constexpr (STREAM) if (pb == 0) noise_wait(p, e, t, st.navail);
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-              if (pb * 8 + j < KA) eps[j] = __ldg(nz + pb * 8 + j);
+              if (pb * 8 + j < KA) eps[j] = noise_ld<STREAM>(nz + pb * 8 + j);
           }
         }
       } else
@@ -458,9 +515,10 @@ struct StockOps {
           eps[0] = nv.a.x; eps[1] = nv.a.y; eps[2] = nv.a.z; eps[3] = nv.a.w;
           eps[4] = nv.b.x; eps[5] = nv.b.y; eps[6] = nv.b.z; eps[7] = nv.b.w;
         } else if (p.noise_mode == FIN_NOISE_SUPPLIED) {
+          if constexpr (STREAM) if (pb == 0) noise_wait(p, e, t, st.navail);
 #pragma unroll
           for (int j = 0; j < 8; ++j)
-            if (pb * 8 + j < KA) eps[j] = __ldg(nz + pb * 8 + j);
+            if (pb * 8 + j < KA) eps[j] = noise_ld<STREAM>(nz + pb * 8 + j);
         }
       } else {
 #pragma unroll
@@ -646,6 +704,7 @@ struct StockOps {
 // shared columns enter through z1s), void for the crypto Q-net (X = x).
 template <class Plan, class Obs>
 struct ProbeOps {
+  static constexpr bool kStream = false;
   static constexpr int kStageBytes = 16;
   static constexpr bool kStageBias = true;
   static constexpr bool kSplitOK = false;
@@ -732,6 +791,10 @@ constexpr int kDualRing = FIN_DUAL_RING;
 template <class Plan, bool RES, class Ops>
 cudaError_t launch_auto(const TcParams& p, int n_envs, int* tiles, cudaStream_t s) {
   const int n_tiles = (n_envs + tc::kTileM - 1) / tc::kTileM;
+  if constexpr (Ops::kStream) {   // streamed noise: small N, one tile per CTA only
+    *tiles = 1;
+    return tc::launch<Plan, RES, 1, Ops>(p, n_envs, s);
+  }
   const char* mode = getenv("FIN_TC_MODE");   // read per launch (tests switch it)
   const bool pair = mode && mode[0] == 'p';
   if constexpr (!RES) {
@@ -785,6 +848,18 @@ auto dispatch_stock(int net, const tc::TcParams& p, F&& f) -> decltype(f(StockKe
   const bool single = p.M == 1 && p.kinds[0] != FIN_DDPG_OU;
   const bool logs = p.act_only || p.o.mlp_out || p.o.mlp_hidden || p.o.cash || p.o.asset || p.o.hold || p.o.actions ||
                     p.o.obs_private || p.o.day;
+  if (p.noise_ready) {   // streamed small-N noise (api.cu plan_noise): the STREAM instantiations
+    if (net == 0 && single && !logs)
+      return f(StockKernel<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false, false, true>>{});
+    if (net == 0 && single) return f(StockKernel<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false, true, true>>{});
+    if (net == 0) return f(StockKernel<PlanStockC1, false, StockOps<30, 8, PlanStockC1, true, true, true>>{});
+    if (net == 3 && single && !logs)
+      return f(StockKernel<PlanStockPaper, true, StockOps<30, 8, PlanStockPaper, false, false, true>>{});
+    if (net == 3 && single)
+      return f(StockKernel<PlanStockPaper, true, StockOps<30, 8, PlanStockPaper, false, true, true>>{});
+    if (net == 3) return f(StockKernel<PlanStockPaper, true, StockOps<30, 8, PlanStockPaper, true, true, true>>{});
+    return f(StockKernel<PlanStockSmall, true, StockOps<4, 4, PlanStockSmall, true, true, true>>{});
+  }
   if (net == 0 && single && !logs) return f(StockKernel<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false, false>>{});
   if (net == 0 && single) return f(StockKernel<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false>>{});
   if (net == 0) return f(StockKernel<PlanStockC1, false, StockOps<30, 8, PlanStockC1, true>>{});

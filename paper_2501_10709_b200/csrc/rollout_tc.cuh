@@ -59,6 +59,8 @@ struct TcParams {
   int32_t noise_mode;
   uint64_t noise_seed;
   const float* noise;                     // supplied noise
+  const uint32_t* noise_ready;            // streamed supplied noise: finished producer blocks per step, or null
+  uint32_t noise_ready_target;            // producer blocks (step t is complete at this count)
   // fin_ensemble_act: compute the (ensemble) action only, no env transition
   int32_t act_only;
   int32_t commit_ou;                      // fin_ensemble_act: advance the DDPG OU states (else left untouched)

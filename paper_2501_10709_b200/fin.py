@@ -373,11 +373,12 @@ def fin_env_check(env: Env) -> int:
 def fin_env_counters(env: Env, clear: bool = False) -> dict:
     """Event counters of the handle (synchronises): exact_redo = stock steps whose buys
     took the exact out-of-line affordability path; balanced_rollouts / balanced_refused =
-    fused stock rollouts launched with the balanced persistent schedule / refused it."""
-    c = (C.c_uint32 * 4)()
+    fused stock rollouts launched with the balanced persistent schedule / refused it;
+    pregen_rollouts = fused stock rollouts that ran on noise pre-drawn by a separate kernel."""
+    c = (C.c_uint32 * 5)()
     _check(_lib.fin_env_counters(env.handle, C.cast(c, _P), int(bool(clear))), "fin_env_counters")
     return {"exact_redo": int(c[0]), "balanced_rollouts": int(c[1]), "balanced_refused": int(c[2]),
-            "balanced_refused_err": int(c[3])}
+            "balanced_refused_err": int(c[3]), "pregen_rollouts": int(c[4])}
 
 
 def fin_env_destroy(env: Env) -> None:

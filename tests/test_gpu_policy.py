@@ -811,3 +811,54 @@ def test_crypto_tile_composition_invariance():
     for k in out[0]:
         assert np.array_equal(out[0][k][:, 1:], out[1][k][:, 1:]), k
     assert not np.array_equal(out[0]["mlp_out"][:, 0], out[1]["mlp_out"][:, 0])
+
+
+@pytest.mark.parametrize("ens,logged", [(False, False), (False, True), (True, True)])
+def test_pregen_noise_matches_in_kernel_draws(ens, logged, monkeypatch):
+    """Small N (fewer tiles than SMs): the rollout's Philox normals drawn by a separate kernel and
+    read as supplied noise (DESIGN.md 4.3 "small N") -- streamed by k_stream_noise on the idle
+    SMs while the rollout runs (FIN_PREGEN=2, the default here) or drawn before it by
+    k_pregen_noise (FIN_PREGEN=1) -- are bitwise the in-kernel draws (FIN_PREGEN=0): N = 2,050 (17 tiles, the last ragged), env_offset 1,000, two rollouts
+    back to back (T = 37 then 9: the second starts at t_global = 37, inside an episode) --
+    rewards, done flags, episode metrics, the aggregate, the final state and (logged) the
+    executed actions, MLP outputs and OU state; single policy (log-free production kernel
+    and the logged one) and the PPO / SAC / DDPG ensemble (noise drawn under layer 2)."""
+    import torch
+    fin = _fin()
+    m = market.stock_c1(rows=1008)
+    spec = [(1, fin.FIN_PPO_GAUSS), (2, fin.FIN_SAC_SQUASH), (3, fin.FIN_DDPG_OU)] if ens else \
+        [(0, fin.FIN_PPO_GAUSS)]
+    pols = [fin.fin_policy_create(k, spol.kaiming_bf16(spol.STOCK_DIMS, s)) for s, k in spec]
+    N, M = 2050, len(spec)
+    _, fcfg = stock_pair(num_envs=N, num_assets=30, num_indicators=8, num_rows=1008, episode_len=30,
+                         window_stride=5, num_windows=195, window_block=128, env_offset=1000)
+    res = []
+    for pre in ("2", "1", "0", None):
+        if pre is None:
+            monkeypatch.delenv("FIN_PREGEN", raising=False)   # the default rule: streamed (17 tiles)
+        else:
+            monkeypatch.setenv("FIN_PREGEN", pre)
+        env = fin.fin_env_create(fcfg, m.market)
+        fin.fin_env_counters(env, clear=True)
+        r = {}
+        for call, T in enumerate((37, 9)):
+            logs = dict(reward=zeros((T, N), torch.float32), done=zeros((T, N), torch.uint8),
+                        ep_metrics=zeros((3, N, 3), torch.float64), ep_count=zeros(N, torch.int32),
+                        agg=zeros(8, torch.float64))
+            if logged:
+                logs.update(actions=zeros((T, N, 30), torch.int16), cash=zeros((T, N), torch.float64),
+                            mlp_out=zeros((T, M, N, 30), torch.float32))
+            fin.fin_rollout(env, pols, T, fin.make_noise(fin.FIN_NOISE_PHILOX, 4242), fin.make_traj(**logs))
+            r.update({f"{k}{call}": host(v) for k, v in logs.items()})
+        c = fin.fin_env_counters(env)
+        assert c["pregen_rollouts"] == (0 if pre == "0" else 2), c
+        assert fin.fin_env_check(env) == 0
+        cash, hold = zeros(N, torch.float64), zeros((N, 30), torch.int16)
+        fin.fin_env_get_state(env, cash=cash, hold=hold)
+        r["cash_end"], r["hold_end"] = host(cash), host(hold)
+        res.append(r)
+        fin.fin_env_destroy(env)
+    for other in res[1:]:
+        for k in res[0]:
+            assert np.array_equal(res[0][k].view(np.uint8), other[k].view(np.uint8)), k
+    assert res[0]["done0"].sum() == N and np.abs(res[0]["hold_end"]).sum() > 0
