@@ -940,19 +940,23 @@ int plan_noise(fin_env* env, tc::TcParams& p, int n_tiles, int T, cudaStream_t s
     FIN_CUDA(cudaMalloc(&env->noise_mem, elems * sizeof(float)));
     env->noise_cap = elems;
   }
+  const size_t groups = ((size_t)T + FIN_NOISE_GROUP - 1) / FIN_NOISE_GROUP;
+  if (env->ready_cap < groups) {
+    if (env->noise_ready) cudaFree(env->noise_ready);
+    env->noise_ready = nullptr;
+    env->ready_cap = 0;
+    FIN_CUDA(cudaMalloc(&env->noise_ready, groups * sizeof(uint32_t)));
+    env->ready_cap = groups;
+  }
   if (mode == 1) {
     cudaError_t e = fin::launch_pregen_noise(p.noise_seed, env->d.env_offset, env->d.N, env->d.K, p.M,
                                              env->d.t_global, T, env->noise_mem, s);
     if (e != cudaSuccess) return cuda_fail(e, "fin_rollout pre-drawn noise");
+    // the small-N (STREAM) kernel with every step complete from the start (target 0): its
+    // column-split epilogues, no waits
+    p.noise_ready = env->noise_ready;
+    p.noise_ready_target = 0;
   } else {
-    const size_t groups = ((size_t)T + FIN_NOISE_GROUP - 1) / FIN_NOISE_GROUP;
-    if (env->ready_cap < groups) {
-      if (env->noise_ready) cudaFree(env->noise_ready);
-      env->noise_ready = nullptr;
-      env->ready_cap = 0;
-      FIN_CUDA(cudaMalloc(&env->noise_ready, groups * sizeof(uint32_t)));
-      env->ready_cap = groups;
-    }
     cudaError_t le = fin::load_stream_noise();   // before the rollout that will wait on it
     if (le != cudaSuccess) return cuda_fail(le, "fin_rollout streamed noise (load)");
     if (!env->noise_side) {

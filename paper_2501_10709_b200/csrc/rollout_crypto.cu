@@ -50,6 +50,7 @@ struct CryptoOps {
   static constexpr int IN = 2 + FIN_C_FACTORS;  // 103
   static constexpr int KT8 = Plan::kIn / 8;
   static constexpr bool kSplitOK = true;        // column-split epilogues (no layer-1 addend)
+  static constexpr bool kSplitAddend = false;
   static constexpr bool kSegments = false;
   static constexpr bool kL1Init = false;
   static constexpr int kOffImgT = 0;

@@ -120,7 +120,11 @@ template <int KA, int IA, class Plan, bool ENS = true, bool LOG = true, bool STR
 struct StockOps {
   static constexpr bool kStream = STREAM;
   static constexpr int KOU = ENS ? KA : 1;
-  static constexpr bool kSplitOK = false;
+  // the streamed-noise (small-N) instantiation of the streamed-weight plan also splits the
+  // hidden epilogues over two warpgroups; layer 1's z1s addend pointer is
+  // handed to the helper through shared memory
+  static constexpr bool kSplitOK = STREAM;
+  static constexpr bool kSplitAddend = true;
   static constexpr bool kSegments = true;   // balanced persistent schedule (init_seg / finalize_seg)
   static constexpr bool kL1Bcast = false;   // (crypto only: broadcast layer-1 A operand)
 #ifndef FIN_STOCK_EPIPIPE
@@ -424,6 +428,12 @@ struct StockOps {
     if (LOG && m == 0 && st.live && p.o.day) p.o.day[(size_t)t * e.N + env] = st.d;
   }
 
+  // the column-split helper's rows of the same log (no env state)
+  __device__ __forceinline__ static uint16_t* helper_hidden_ptr(const TcParams& p, int env, int t, int m, int l,
+                                                                int hid) {
+    if (!LOG || env >= p.e.N || !p.o.mlp_hidden) return nullptr;
+    return p.o.mlp_hidden + ((((size_t)t * p.M + m) * p.e.N + env) * Plan::kNH + l) * hid;
+  }
   __device__ __forceinline__ static uint16_t* hidden_ptr(State& st, const TcParams& p, int env, int t, int m, int l,
                                                          int hid) {
     if (!LOG || !st.live || !p.o.mlp_hidden) return nullptr;
@@ -708,6 +718,7 @@ struct ProbeOps {
   static constexpr int kStageBytes = 16;
   static constexpr bool kStageBias = true;
   static constexpr bool kSplitOK = false;
+  static constexpr bool kSplitAddend = false;
   static constexpr bool kSegments = false;
   static constexpr bool kL1Init = false;
   static constexpr int kOffB = 0;
@@ -793,6 +804,11 @@ cudaError_t launch_auto(const TcParams& p, int n_envs, int* tiles, cudaStream_t 
   const int n_tiles = (n_envs + tc::kTileM - 1) / tc::kTileM;
   if constexpr (Ops::kStream) {   // streamed noise: small N, one tile per CTA only
     *tiles = 1;
+    // streamed-weight plan: the hidden epilogues split over two warpgroups (FIN_SPLIT=0: not)
+    const char* sp = getenv("FIN_SPLIT");
+    if constexpr (!RES)
+      if (!(sp && sp[0] == '0') && tc::Smem<Plan, RES, 1, Ops>::total(p.M) + 1024 <= tc::kSmemLimit)
+        return tc::launch<Plan, RES, 1, Ops, tc::kRing, 1, 2>(p, n_envs, s);
     return tc::launch<Plan, RES, 1, Ops>(p, n_envs, s);
   }
   const char* mode = getenv("FIN_TC_MODE");   // read per launch (tests switch it)

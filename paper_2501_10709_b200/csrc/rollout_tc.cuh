@@ -168,12 +168,15 @@ struct Smem {
 //   };
 // RING: weight-ring slots; MINB: CTAs per SM (MINB = 2 runs two independent tiles per
 // SM whose env phases overlap each other's MMA / weight-streaming phases).
-// SPLIT > 1 (resident plans, one tile per CTA: the latency-bound crypto rollout): SPLIT
-// warpgroups share each hidden layer's epilogue by columns (warpgroup w takes chunk
-// range w of the layer's 16-column chunks); the first runs everything else.
+// SPLIT > 1 (one tile per CTA: the latency-bound crypto rollout and, round 2, the small-N
+// stock rollout): SPLIT warpgroups share each hidden layer's epilogue by columns (warpgroup w
+// takes chunk range w of the layer's 16-column chunks); the first runs everything else.  A
+// factored layer 1 (stock): the first warpgroup publishes each row's addend pointer in shared
+// memory past the plan's layout (named barrier kSplitBar0, arrive / sync) before the layer's
+// MMAs; the launch adds 1 KB.
 template <class Plan, bool RESIDENT, int TILES, class Ops, int RING = kRing, int MINB = 1, int SPLIT = 1>
 __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(const __grid_constant__ TcParams p) {
-  static_assert(SPLIT == 1 || (TILES == 1 && RESIDENT && Ops::kSplitOK), "column-split epilogues: resident, 1 tile");
+  static_assert(SPLIT == 1 || (TILES == 1 && Ops::kSplitOK), "column-split epilogues: 1 tile");
   static_assert((Plan::kHidMax / 16) % SPLIT == 0, "chunks must divide among the warpgroups");
   using S = Smem<Plan, RESIDENT, TILES, Ops, RING>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -250,13 +253,15 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
   // it against the new budget.
   // (two tiles, one CTA per SM: 4 x 40 + 8 x 232 warps' worth = 64 K registers; one tile, two
   // CTAs per SM: each CTA 4 x 40 + 4 x 216 of its 128-per-thread launch allocation)
-  constexpr bool kSplitRegs = (TILES == 2 && MINB == 1) || (TILES == 1 && MINB == 2);
+  // (the column-split streamed-weight stock tile, 1 CTA per SM: 4 x 40 + 8 x 232 as two tiles)
+  constexpr bool kSplit2 = TILES == 1 && SPLIT == 2 && MINB == 1 && !RESIDENT;
+  constexpr bool kSplitRegs = (TILES == 2 && MINB == 1) || (TILES == 1 && MINB == 2) || kSplit2;
 #ifndef FIN_DUAL_LOW_REGS
 #define FIN_DUAL_LOW_REGS 32   // producer / MMA warpgroup registers in the dual layout (A/B: 32 +0.4% vs 40, 48 -0.4%)
 #endif
   // dual layout (one tile, two CTAs per SM): 128 x (low + env) = 32 K registers per CTA
-  constexpr uint32_t kLowRegs = TILES == 2 ? 40 : FIN_DUAL_LOW_REGS;
-  constexpr uint32_t kEnvRegs = TILES == 2 ? 232 : 256 - kLowRegs;
+  constexpr uint32_t kLowRegs = (TILES == 2 || kSplit2) ? 40 : FIN_DUAL_LOW_REGS;
+  constexpr uint32_t kEnvRegs = (TILES == 2 || kSplit2) ? 232 : 256 - kLowRegs;
   if (warp < 4) {
   if constexpr (kSplitRegs) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kLowRegs) : "memory");
   if (warp == 0) {
@@ -401,6 +406,9 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
     uint8_t* stg = sStage + tile * Ops::kStageBytes;
     const int bar_id = 1 + tile;
     constexpr int kSplitBar = 1 + TILES;     // the warpgroups of a column-split tile meet here
+    constexpr int kSplitBar0 = 2 + TILES;    // ... and here for the layer-1 addend pointers
+    // (SPLIT > 1) per-row layer-1 addend pointers, past the plan's shared-memory layout
+    const float** sAdd = reinterpret_cast<const float**>(smem + S::total(M));
     // Hidden-layer epilogue of chunks [c0, c1): D -> +bias (+ addend) -> ReLU -> bf16 -> A
     // (K-major core matrices).  16 columns per TMEM load: half the registers of 32-column
     // chunks (the env state lives in registers across the whole rollout).  One loop per
@@ -514,6 +522,13 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
             const int ncol = kUniformHid ? Plan::kH1 : Plan::nrows(l);
             const int cpp = (ncol / 16) / SPLIT;
             uint4* hlog = reinterpret_cast<uint4*>(Ops::helper_hidden_ptr(p, env, t, m, l, Plan::kHidMax));
+            const float* add = nullptr;
+            if constexpr (Ops::kSplitAddend) {
+              if (l == 0) {
+                sm100::named_bar_sync(kSplitBar0, 128 * SPLIT);
+                add = sAdd[row];
+              }
+            }
             t_lane = t_lane0 + bank_of(l);
             if constexpr (kPipeKick) {
               const int nch = ncol / 16;
@@ -524,7 +539,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
                 sm100::named_bar_sync(kSplitBar, 128 * SPLIT);
               }
             } else {
-              run_epi(bl, nullptr, hlog, ncol, part * cpp, (part + 1) * cpp);
+              run_epi(bl, add, hlog, ncol, part * cpp, (part + 1) * cpp);
               sm100::fence_proxy_async_smem();
               sm100::tc_fence_before();
               sm100::named_bar_sync(kSplitBar, 128 * SPLIT);
@@ -586,6 +601,7 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
           if (half != 0) sm100::mma_commit(&d_full[tile]);
         }
       } else {
+        if (SPLIT > 1 && l > 0) sm100::named_bar_sync(kSplitBar, 128 * SPLIT);   // the helpers' columns too
         sm100::mbar_arrive(a_full);
       }
     };
@@ -640,6 +656,10 @@ __global__ void __launch_bounds__(128 + 128 * TILES * SPLIT, MINB) k_tc_rollout(
         if constexpr (Ops::kL1Bcast && kEnvIssue) Ops::build_obs_bcast(st, p, env, row, t, m, xa, stg);
         else Ops::build_obs(st, p, env, row, t, m, xa, stg);
         if constexpr (Ops::kL1Init) Ops::l1_init_rows(st, p, t_lane0, stg);
+        if constexpr (SPLIT > 1 && Ops::kSplitAddend) {
+          sAdd[row] = Ops::l1_addend(st, p, m, stg);
+          sm100::named_bar_arrive(kSplitBar0, 128 * SPLIT);
+        }
         kick(m, 0);
         FIN_TR(row == 0 && tile == 0 && m == 0, t, 1);
         // biases of the first FIN_STAGE_MEMBERS members in shared memory, the rest from L2
@@ -733,8 +753,9 @@ template <class Plan, bool RESIDENT, int TILES, class Ops, int RING = kRing, int
 cudaError_t launch(const TcParams& p, int n_envs, cudaStream_t s, int seg_grid = 0) {
   using Sm = Smem<Plan, RESIDENT, TILES, Ops, RING>;
   auto kern = k_tc_rollout<Plan, RESIDENT, TILES, Ops, RING, MINB, SPLIT>;
-  const int bytes = Sm::total(p.M);
+  const int bytes = Sm::total(p.M) + (SPLIT > 1 ? 1024 : 0);   // (SPLIT: the addend pointers)
   if (MINB > 1 && bytes * MINB > kSmemLimit) return cudaErrorInvalidConfiguration;
+  if (bytes > kSmemLimit) return cudaErrorInvalidConfiguration;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (err != cudaSuccess) return err;
   // all of the SM's shared memory as shared memory (the occupancy that cooperative launches
