@@ -921,32 +921,43 @@ struct NoisePlan {
 };
 int plan_noise(fin_env* env, tc::TcParams& p, int n_tiles, int T, cudaStream_t s, NoisePlan& np) {
   np = NoisePlan();
-  if (env->d.task != FIN_STOCK || p.noise_mode != FIN_NOISE_PHILOX || p.act_only) return FIN_OK;
-  const size_t elems = (size_t)T * p.M * env->d.N * env->d.K;
-  if (elems * sizeof(float) > kPregenCapBytes) return FIN_OK;
+  if (env->d.task != FIN_STOCK || p.act_only) return FIN_OK;
   const int free_sms = fin::num_sms() - n_tiles;
+  if (free_sms < 0) return FIN_OK;   // more tiles than SMs: the large-N layouts
+  const size_t groups = ((size_t)T + FIN_NOISE_GROUP - 1) / FIN_NOISE_GROUP;
+  if (env->ready_cap < groups) {
+    if (env->noise_ready) cudaFree(env->noise_ready);   // synchronises: no rollout still reads it
+    env->noise_ready = nullptr;
+    env->ready_cap = 0;
+    FIN_CUDA(cudaMalloc(&env->noise_ready, groups * sizeof(uint32_t)));
+    env->ready_cap = groups;
+  }
+  const size_t elems = (size_t)T * p.M * env->d.N * env->d.K;
   const char* force = getenv("FIN_PREGEN");
-  // default: drawn before the rollout up to 2,048 env-members (its cost ~N T / 7,700 us against a
-  // gain of ~T us: it pays below ~7,700 envs, and beats streaming where the producer's start-up
-  // shows, e.g. T = 30), streamed while the idle SMs number at least half the tiles
-  int mode = force ? atoi(force) : (2 * free_sms < n_tiles ? 0 : (size_t)p.M * env->d.N <= 2048 ? 1 : 2);
-  if (mode == 2 && free_sms < 1) mode = 0;   // the producer needs SMs the rollout's tiles leave free
+  // Philox noise, default: drawn before the rollout up to 2,048 env-members (its cost ~N T / 7,700 us
+  // against a gain of ~T us: it pays below ~7,700 envs, and beats streaming where the producer's
+  // start-up shows, e.g. T = 30), streamed while the idle SMs number at least half the tiles,
+  // else in-kernel.  Mode 4 (and any supplied / no noise): the small-N kernel with every step
+  // complete from the start (target 0) -- its column-split epilogues without a noise pass.
+  int mode = 4;
+  if (p.noise_mode == FIN_NOISE_PHILOX)
+    mode = force ? atoi(force) : (2 * free_sms < n_tiles ? 4 : (size_t)p.M * env->d.N <= 2048 ? 1 : 2);
+  if (mode == 2 && free_sms < 1) mode = 4;   // the producer needs SMs the rollout's tiles leave free
   if (mode == 2 && getenv("FIN_SEG_PROF")) mode = 1;   // that debug path synchronises right after the launch
-  if (mode < 1 || mode > 3) return FIN_OK;   // 3 (A/B only): the streamed path with the producer run first
+  if (mode != 4 && elems * sizeof(float) > kPregenCapBytes) mode = 4;
+  if (mode < 1 || mode > 4) return FIN_OK;   // 0: in-kernel draws, one env warpgroup (A/B);
+                                             // 3 (A/B only): the streamed path with the producer run first
+  if (mode == 4) {
+    p.noise_ready = env->noise_ready;
+    p.noise_ready_target = 0;
+    return FIN_OK;
+  }
   if (env->noise_cap < elems) {
     if (env->noise_mem) cudaFree(env->noise_mem);   // synchronises: no rollout still reads it
     env->noise_mem = nullptr;
     env->noise_cap = 0;
     FIN_CUDA(cudaMalloc(&env->noise_mem, elems * sizeof(float)));
     env->noise_cap = elems;
-  }
-  const size_t groups = ((size_t)T + FIN_NOISE_GROUP - 1) / FIN_NOISE_GROUP;
-  if (env->ready_cap < groups) {
-    if (env->noise_ready) cudaFree(env->noise_ready);
-    env->noise_ready = nullptr;
-    env->ready_cap = 0;
-    FIN_CUDA(cudaMalloc(&env->noise_ready, groups * sizeof(uint32_t)));
-    env->ready_cap = groups;
   }
   if (mode == 1) {
     cudaError_t e = fin::launch_pregen_noise(p.noise_seed, env->d.env_offset, env->d.N, env->d.K, p.M,

@@ -44,7 +44,7 @@ def run(N, T, env_vars):
     return statistics.median(ts)
 
 
-for N, T in ((64, 256), (2048, 30), (2048, 256), (8192, 256), (12288, 256), (16384, 256)):
+for N, T in ((64, 256), (2048, 30), (2048, 256), (8192, 256), (12288, 256), (16384, 256), (18944, 256)):
     out = {}
     for rep in range(2):
         for name, ev in VARIANTS.items():
