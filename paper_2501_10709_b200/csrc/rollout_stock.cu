@@ -45,6 +45,9 @@ __device__ __forceinline__ uint32_t bf16_bits(float v) {
 #ifndef FIN_PHILOX16
 #define FIN_PHILOX16 0   // 1: consume draws 16 normals per Philox call (4 counters interleaved)
 #endif
+#ifndef FIN_STREAM_EARLY
+#define FIN_STREAM_EARLY 1   // 1: the small-N kernel's own Philox draws (mode 4) under layer 2 (StockOps EARLY)
+#endif
 #ifndef FIN_NOISE_LATE
 #define FIN_NOISE_LATE 1   // 1: noise in consume for the single policy, under layer 2 for ensembles
 #endif
@@ -116,7 +119,7 @@ __device__ __forceinline__ float tanh_f32(float x) {
 // STREAM = true: the small-N instantiation that reads streamed pre-drawn noise (p.noise_ready,
 // DESIGN.md §4.3); the others carry none of its code (A/B: the wait code alone in the large-N
 // kernel cost 3% of the headline).
-template <int KA, int IA, class Plan, bool ENS = true, bool LOG = true, bool STREAM = false>
+template <int KA, int IA, class Plan, bool ENS = true, bool LOG = true, bool STREAM = false, bool EARLY = false>
 struct StockOps {
   static constexpr bool kStream = STREAM;
   static constexpr int KOU = ENS ? KA : 1;
@@ -137,7 +140,12 @@ struct StockOps {
   // where the step's noise is drawn: inside consume for the single policy (+3.6%: no noise
   // registers live across the layer-2 epilogue), under layer 2 for ensembles (FIN_NOISE_LATE
   // overrides: 0 never late, 2 always late)
-  static constexpr bool kNoiseLate = FIN_NOISE_LATE == 2 || (FIN_NOISE_LATE == 1 && !ENS);
+  // EARLY (the small-N production kernel drawing Philox itself, api.cu's mode 4: 99-148 tiles): its
+  // env threads idle through the layer-2 MMA (one tile per SM), so the draws are made in prepare()
+  // under layer 2 instead of on the chain in consume (A/B, scripts/early_ab.py: +3.4% at 16,384 x
+  // 256).  A separate instantiation: supplied / pre-drawn normals taken early were 9% slower, and
+  // one kernel holding both paths lost the whole small-N gain (register pressure).
+  static constexpr bool kNoiseLate = !EARLY && (FIN_NOISE_LATE == 2 || (FIN_NOISE_LATE == 1 && !ENS));
   static constexpr int KP4 = (KA + 3) / 4 * 4;
   static constexpr int IN = 1 + 2 * KA + IA * KA;
   static constexpr int KT8 = Plan::kIn / 8;
@@ -865,6 +873,8 @@ auto dispatch_stock(int net, const tc::TcParams& p, F&& f) -> decltype(f(StockKe
   const bool logs = p.act_only || p.o.mlp_out || p.o.mlp_hidden || p.o.cash || p.o.asset || p.o.hold || p.o.actions ||
                     p.o.obs_private || p.o.day;
   if (p.noise_ready) {   // streamed small-N noise (api.cu plan_noise): the STREAM instantiations
+    if (FIN_STREAM_EARLY && net == 0 && single && !logs && p.noise_mode == FIN_NOISE_PHILOX)
+      return f(StockKernel<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false, false, true, true>>{});
     if (net == 0 && single && !logs)
       return f(StockKernel<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false, false, true>>{});
     if (net == 0 && single) return f(StockKernel<PlanStockC1, false, StockOps<30, 8, PlanStockC1, false, true, true>>{});

@@ -818,7 +818,8 @@ def test_pregen_noise_matches_in_kernel_draws(ens, logged, monkeypatch):
     """Small N (fewer tiles than SMs): the rollout's Philox normals drawn by a separate kernel and
     read as supplied noise (DESIGN.md 4.3 "small N") -- streamed by k_stream_noise on the idle
     SMs while the rollout runs (FIN_PREGEN=2, the default here) or drawn before it by
-    k_pregen_noise (FIN_PREGEN=1) -- are bitwise the in-kernel draws (FIN_PREGEN=0): N = 2,050 (17 tiles, the last ragged), env_offset 1,000, two rollouts
+    k_pregen_noise (FIN_PREGEN=1) -- and the small-N kernel's own Philox draws made under layer 2
+    (FIN_PREGEN=4, prepare()) are bitwise the in-kernel draws of consume (FIN_PREGEN=0): N = 2,050 (17 tiles, the last ragged), env_offset 1,000, two rollouts
     back to back (T = 37 then 9: the second starts at t_global = 37, inside an episode) --
     rewards, done flags, episode metrics, the aggregate, the final state and (logged) the
     executed actions, MLP outputs and OU state; single policy (log-free production kernel
@@ -833,7 +834,7 @@ def test_pregen_noise_matches_in_kernel_draws(ens, logged, monkeypatch):
     _, fcfg = stock_pair(num_envs=N, num_assets=30, num_indicators=8, num_rows=1008, episode_len=30,
                          window_stride=5, num_windows=195, window_block=128, env_offset=1000)
     res = []
-    for pre in ("2", "1", "0", None):
+    for pre in ("2", "1", "0", "4", None):   # "4": the small-N kernel drawing Philox itself, under layer 2
         if pre is None:
             monkeypatch.delenv("FIN_PREGEN", raising=False)   # the default rule: streamed (17 tiles)
         else:
@@ -851,7 +852,7 @@ def test_pregen_noise_matches_in_kernel_draws(ens, logged, monkeypatch):
             fin.fin_rollout(env, pols, T, fin.make_noise(fin.FIN_NOISE_PHILOX, 4242), fin.make_traj(**logs))
             r.update({f"{k}{call}": host(v) for k, v in logs.items()})
         c = fin.fin_env_counters(env)
-        assert c["pregen_rollouts"] == (0 if pre == "0" else 2), c
+        assert c["pregen_rollouts"] == (0 if pre in ("0", "4") else 2), c
         assert fin.fin_env_check(env) == 0
         cash, hold = zeros(N, torch.float64), zeros((N, 30), torch.int16)
         fin.fin_env_get_state(env, cash=cash, hold=hold)
